@@ -1,0 +1,448 @@
+#!/usr/bin/env python
+"""Benchmark of the IRL-SR hot path on B200 (contract: see DESIGN.md §Measurement).
+
+Metric (BASELINE.json): S*v + H_eff*v MVPs/sec (+ % of HBM roofline, + IRL
+solve wall time) on one B200.  Workload: config 2 (RBM f64, N_s = 65536,
+P = 6600, O = 3.46 GB resident in HBM, larger than the 126 MB L2 so no flush
+is needed).  One step = one H_eff*v product + one S*v product on fresh
+random vectors (2 MVPs).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+
+--impl reference times the reference's algorithm on the host CPU: the
+reference package cannot travel to the GPU box, so the oracle port
+(oracle/estimators.py, a line-by-line numpy restatement of est:146-186
+including its per-call centring copy) is timed on a row sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BASELINE_METRIC = "S*v + H_eff*v MVPs/sec (1 B200)"
+UNIT = "MVP/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--mode", type=int, default=0, help="0 auto, 1 fused single pass, 2 two-pass")
+    ap.add_argument("--no-irl", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+# ------------------------------------------------------------ clocks ------
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int, period: float = 0.02):
+        self.index = index
+        self.period = period
+        self.samples = []
+        self.reasons = 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        self.ok = False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:  # pragma: no cover - NVML missing
+            self.ok = False
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml_unavailable"]}
+        reasons = [name for bit, name in self.REASONS.items() if self.reasons & bit and name != "gpu_idle"]
+        return {
+            "sm_mhz": float(statistics.median(self.samples)) if self.samples else None,
+            "sm_max_mhz": self.max_mhz,
+            "reasons": reasons,
+            "samples": len(self.samples),
+        }
+
+
+def measured_peak_gbs():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(cfg_index: int):
+    """Per-launch dram bytes of the dominant kernel from the committed ncu summary, if any."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as fh:
+            data = json.load(fh)
+        return data.get(f"cfg{cfg_index}")
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------- CPU reference ----
+class CpuReference:
+    """The oracle port of est.heff_matvec (H and S products) on the first n_sub rows."""
+
+    def __init__(self, cfg, n_sub: int):
+        from oracle import estimators as oest
+        from oracle import nqs
+        from paper_2601_01437_b200 import synthetic as S
+
+        inp = S.make_inputs(cfg.with_rows(n_sub))
+        fn = nqs.rbm_rows if cfg.model == "rbm" else nqs.mlp_rows
+        o = fn(inp.theta, inp.x, cfg.n_inputs, cfg.hidden)
+        w = np.full(n_sub, 1.0 / n_sub)
+        mean, _, _ = oest.energy(w, inp.e_loc, n_sub)
+        rng = np.random.default_rng(0)
+        e = inp.e_loc
+        if cfg.complex_params:  # reference real embedding [O, iO] with Re(e)
+            o = np.concatenate([o, 1j * o], axis=1)
+            e = inp.e_loc.real
+        self.v = rng.standard_normal(o.shape[1])
+        self.o, self.w, self.e, self.mean = o, w, e, mean
+        self.oest = oest
+
+    def step(self) -> float:
+        """One H_eff*v + one S*v; returns seconds."""
+        t0 = time.perf_counter()
+        self.oest.heff(self.w, self.e, self.o, self.mean, self.v)
+        self.oest.qgt(self.w, self.o, self.v)
+        return time.perf_counter() - t0
+
+
+def cpu_reference_sample(cfg, n_sub: int, reps: int = 3):
+    """Median seconds per MVP of the oracle port at n_sub rows."""
+    ref = CpuReference(cfg, n_sub)
+    ref.step()
+    return statistics.median(ref.step() / 2.0 for _ in range(reps))
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    from paper_2601_01437_b200 import synthetic as S
+
+    cfg = S.CONFIGS[args.config]
+    n_sub = min(cfg.n_rows, 2048)
+    scale = cfg.n_rows / n_sub
+    ref = CpuReference(cfg, n_sub)
+    for _ in range(args.warmup):
+        ref.step()
+    per_step = [ref.step() for _ in range(args.steps)]
+    t_step_full = statistics.fmean(per_step) * scale
+    value = 2.0 / t_step_full
+    cores = cpu_cores()
+    line = {
+        "impl": "reference",
+        "metric": BASELINE_METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": t_step_full * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "c128" if cfg.complex_params else "f64",
+        "data": "synthetic (seeded, BASELINE.json shapes)",
+        "config": {"workload": cfg.name, "n_rows": cfg.n_rows, "param_count": cfg.param_count},
+        "cpu_baseline": {
+            "value": value,
+            "unit": UNIT,
+            "cores": cores,
+            "kind": "port",
+            "sample": (f"oracle port of est.heff_matvec (S*v via e_loc=1) on the first {n_sub} of {cfg.n_rows} "
+                       f"rows, full P={cfg.param_count}; per-step time x{scale:g} (linear in N_s); numpy/BLAS "
+                       f"threads = all {cores} cores"),
+        },
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ------------------------------------------------------------- ours -------
+def run_ours(args):
+    import torch
+
+    world, rank, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+
+    from paper_2601_01437_b200 import _lib, ansatz as A, estimators as E, optimizer as OPT, synthetic as S
+
+    cfg = S.CONFIGS[args.config]
+    inp = S.make_inputs(cfg)
+    if cfg.model == "rbm":
+        arch = A.RBMArchitecture(cfg.n_inputs, cfg.hidden, cfg.complex_params)
+    else:
+        arch = A.MLPArchitecture(cfg.n_inputs, cfg.hidden)
+    params = A.AnsatzParameters(arch, inp.theta)
+    # O-build (K1/K2) timed once for the record
+    torch.cuda.synchronize()
+    ob0 = torch.cuda.Event(enable_timing=True)
+    ob1 = torch.cuda.Event(enable_timing=True)
+    ob0.record()
+    batch = A.build_batch(params, inp.x, inp.e_loc, device=dev)
+    ob1.record()
+    torch.cuda.synchronize()
+    obuild_ms = ob0.elapsed_time(ob1)
+    energy = E.estimate_energy(batch)
+    P, ld, N = batch.param_count, batch.ld, batch.n_rows
+    herm = batch.kind == E.KIND_HERMITIAN
+    plan = _lib.mvp_plan(N, ld, batch.is_complex, args.mode)
+    launches_per_mvp = 2 if plan["path"] == "fused" else 3
+    coef_h = batch.coefficients(energy.mean)
+    coef_s = batch.weights if not batch.is_complex else batch.weights.to(torch.complex128)
+    batch.obar()
+
+    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+    nvec = 8
+    if herm:
+        vin = torch.randn((nvec, 2, ld), dtype=torch.float64, device=dev, generator=gen)
+        vin[:, :, P:] = 0
+        vout = torch.empty((2, 2, ld), dtype=torch.float64, device=dev)
+    else:
+        vin = torch.randn((nvec, ld), dtype=torch.float64, device=dev, generator=gen)
+        vin[:, P:] = 0
+        vout = torch.empty((2, ld), dtype=torch.float64, device=dev)
+
+    def one(i, coeff, slot):
+        if herm:
+            E._apply(batch, coeff, (vin[i, 0], vin[i, 1]), (vout[slot, 0], vout[slot, 1]), mode=args.mode)
+        else:
+            E._apply(batch, coeff, vin[i], vout[slot], mode=args.mode)
+
+    def step(k):
+        one(k % nvec, coef_h, 0)
+        one((k + 1) % nvec, coef_s, 1)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+
+    for k in range(args.warmup):
+        step(k)
+    torch.cuda.synchronize()
+
+    # ---- device-timed steps (max over ranks)
+    stream = torch.cuda.current_stream()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    per = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(2 * args.steps)]
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(torch.cuda.current_device()) as clocks:
+        t0.record(stream)
+        for k in range(args.steps):
+            a, b = per[2 * k]
+            a.record(stream)
+            one(k % nvec, coef_h, 0)
+            b.record(stream)
+            a, b = per[2 * k + 1]
+            a.record(stream)
+            one((k + 1) % nvec, coef_s, 1)
+            b.record(stream)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    elapsed = t0.elapsed_time(t1) / 1e3
+    mvp_ms = [a.elapsed_time(b) for a, b in per]
+    if world > 1:
+        import torch.distributed as dist
+
+        tt = torch.tensor([elapsed], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        elapsed = float(tt)
+    mvps = 2 * args.steps
+    value = world * mvps / elapsed
+
+    # ---- end to end through the public API with pinned host vectors
+    vh = torch.randn(P, dtype=torch.complex128 if herm else torch.float64, generator=torch.Generator().manual_seed(7))
+    vh = vh.pin_memory()
+    e2e_steps = max(args.steps // 2, 5)
+    for _ in range(2):
+        E.heff_matvec(batch, energy, vh)
+    barrier()
+    torch.cuda.synchronize()
+    h0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        E.heff_matvec(batch, energy, vh)
+        E.qgt_matvec(batch, vh)
+    torch.cuda.synchronize()
+    e2e_time = time.perf_counter() - h0
+    barrier()
+    if world > 1:
+        import torch.distributed as dist
+
+        tt = torch.tensor([e2e_time], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_time = float(tt)
+    vbytes = P * (16 if herm else 8)
+    e2e = {"value": world * 2 * e2e_steps / e2e_time, "unit": UNIT, "h2d_bytes_per_step": 2 * vbytes,
+           "d2h_bytes_per_step": 2 * vbytes,
+           "api": "estimators.heff_matvec + qgt_matvec on pinned host tensors (H2D, product, D2H, sync)"}
+
+    # ---- IRL solve wall time (one outer step's eigen-solve + direction)
+    irl = None
+    if not args.no_irl:
+        conf = OPT.OptimizerConfig(m=cfg.m, max_restarts=cfg.max_restarts)
+        OPT.solve_step(batch, conf, seed=cfg.lanczos_seed, energy=energy)  # warm
+        torch.cuda.synchronize()
+        i0 = time.perf_counter()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        res = OPT.solve_step(batch, conf, seed=cfg.lanczos_seed, energy=energy)
+        ev1.record()
+        torch.cuda.synchronize()
+        irl = {"wall_ms": (time.perf_counter() - i0) * 1e3, "device_ms": ev0.elapsed_time(ev1),
+               "n_matvec": res.n_matvec, "lambda_min": res.lambda_min, "converged": res.converged,
+               "m": cfg.m, "max_restarts": cfg.max_restarts}
+
+    if rank != 0:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+        return 0
+
+    # ---- roofline of the dominant kernel (the streaming MVP launch)
+    b_el = 16 if batch.is_complex else 8
+    alg_bytes = (1 if plan["path"] == "fused" else 2) * N * P * b_el
+    mvp_avg_s = statistics.mean(mvp_ms) / 1e3
+    achieved = alg_bytes / mvp_avg_s / 1e9
+    peak, peak_src = measured_peak_gbs()
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": ncu_traffic(args.config), "peak_source": peak_src,
+                "bytes_per_launch": alg_bytes,
+                "accounting": ("one read of O (N*P*b) per MVP: the fused kernel streams O once; "
+                               "SURVEY 8(d)'s 2-pass figure would be 2*N*P*b"),
+                "kernel_ms_mean": mvp_avg_s * 1e3, "kernel_ms_median": statistics.median(mvp_ms)}
+
+    cpu = None
+    if not args.no_cpu and world == 1:
+        n_sub = min(cfg.n_rows, 8192)
+        sec = cpu_reference_sample(cfg, n_sub)
+        full = sec * cfg.n_rows / n_sub
+        cpu = {"value": 1.0 / full, "unit": UNIT, "cores": cpu_cores(), "kind": "port",
+               "sample": (f"oracle port of est.heff_matvec / S-trick, median of 3 on the first {n_sub} of "
+                          f"{cfg.n_rows} rows (full P), x{cfg.n_rows / n_sub:g} to full N_s")}
+
+    line = {
+        "metric": BASELINE_METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": elapsed / args.steps * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "c128" if batch.is_complex else "f64",
+        "data": "synthetic (seeded, BASELINE.json shapes)",
+        "config": {"workload": cfg.name, "n_rows": N, "param_count": P, "ld": ld,
+                   "o_bytes": N * ld * b_el, "step": "1 H_eff*v + 1 S*v (2 MVPs)",
+                   "l2": "O (%.2f GB) > 126 MB L2: no flush needed" % (N * ld * b_el / 1e9),
+                   "parallelism": f"replicas x{world}", "mvp_path": plan["path"], "plan": plan},
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": mvps * launches_per_mvp,
+        "clocks": clocks.summary(),
+        "irl_solve": irl,
+        "obuild_ms": obuild_ms,
+        "mvp_ms_per_product": elapsed / mvps * 1e3,
+    }
+    print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,133 @@
+/*
+ * irl_sr.h — C-ABI of the B200 (sm_100a) IRL stochastic-reconfiguration hot path.
+ *
+ * Drop-in boundary for the reference package `irlnqs` (arXiv 2601.01437,
+ * /root/reference/pkg/src/irlnqs).  Every entry point replaces one reference
+ * function on the hot path; the reference-side binding (ctypes) is shown in
+ * INTEGRATION.md and implemented in paper_2601_01437_b200/_lib.py.
+ *
+ * Conventions:
+ *   - all array pointers are DEVICE pointers owned by the caller; kernels never
+ *     allocate, free or retain them past the call; inputs are const;
+ *   - `stream` is a cudaStream_t passed as void* (the caller's current stream);
+ *     every call is asynchronous on that stream and re-entrant;
+ *   - O is row-major N x ld (ld >= P, from irl_padded_ld), padding columns zero;
+ *     f64: ld doubles per row; c128: ld interleaved complex (re, im) per row;
+ *   - P-length vectors are allocated with the padded length ld, padding zero;
+ *   - complex vectors passed as *_re / *_im are PLANAR arrays of length ld;
+ *     a NULL *_im means "imaginary part zero" (input) or "not wanted" (output);
+ *   - workspace is caller-allocated, >= the matching *_workspace_bytes(), 256-B aligned;
+ *   - return value: IRL_OK or an IRL_ERR_* code; irl_last_error() gives text
+ *     (thread-local).  No exception or exit() crosses the ABI.
+ */
+#ifndef IRL_SR_H_
+#define IRL_SR_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+#define IRL_OK 0
+#define IRL_ERR_ARG 1       /* bad shape / null pointer / bad mode */
+#define IRL_ERR_ALIGN 2     /* pointer or ld not 16-byte aligned / padded */
+#define IRL_ERR_WORKSPACE 3 /* workspace too small */
+#define IRL_ERR_CUDA 4      /* CUDA runtime error (text in irl_last_error) */
+#define IRL_ERR_DEVICE 5    /* no sm_100 device / unsupported plan */
+
+#define IRL_MVP_AUTO 0      /* fused single pass when it fits, else two-pass */
+#define IRL_MVP_FUSED 1     /* one HBM pass, column slices over a CTA cluster (DSMEM exchange) */
+#define IRL_MVP_TWO_PASS 2  /* t = O v pass, then O^H y pass */
+
+#define IRL_MODEL_RBM 0
+#define IRL_MODEL_MLP 1
+
+/* Library identity / diagnostics. */
+int irl_version(void);
+const char* irl_last_error(void);
+
+/* Padded leading dimension (in elements: doubles for f64, complex for c128) for
+ * P parameters.  Rows are padded to whole 16-B units and to a multiple of 16
+ * (64 for very wide rows) units so every column split is TMA-aligned. */
+int64_t irl_padded_ld(int64_t p, int is_complex);
+
+/* ---------------------------------------------------------------- A3 ----
+ * estimate_energy (estimators.py:146-153) + centred coefficients (:166-168).
+ * stats3 (device, 3 doubles) = {E = Re sum w e, Im sum w e, sum w |e - E|^2};
+ * coeff[n] = w_n (e_n - E)  (c128 hermitian=1: w_n Re(e_n - E), imag 0).   */
+int irl_energy_f64(const double* w, const double* e, int64_t n, double* stats3, double* coeff, void* stream);
+int irl_energy_c128(const double* w, const double* e, int64_t n, int hermitian, double* stats3, double* coeff,
+                    void* stream);
+
+/* ------------------------------------------------------------- A4/A5 ----
+ * Column statistics of a stored O: obar = w @ O (estimators.py:167) and
+ * g = coeff @ conj(O)  (so F = 2 Re g reproduces energy_gradient, :156-163). */
+size_t irl_colstats_workspace_bytes(int64_t n, int64_t ld, int is_complex);
+int irl_colstats_f64(const double* O, int64_t n, int64_t ld, const double* w, const double* coeff, double* obar,
+                     double* g, void* ws, size_t ws_bytes, void* stream);
+int irl_colstats_c128(const double* O, int64_t n, int64_t ld, const double* w, const double* coeff, double* obar,
+                      double* g, void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------- A2 ----
+ * Batched log-derivative rows (role of ansatz.log_derivative, ansatz.py:249-290,
+ * called per sample by build_batch, estimators.py:112-126) for the shallow NQS,
+ * with the column statistics of A4/A5 fused into the same pass.
+ *   x     : N x n_vis uint8 (0/1)
+ *   theta : RBM [a (n), b (h), W (h x n)]  (c128: interleaved complex)
+ *           MLP [W (h x n_in), b (h), u (h), c]
+ *   hidden-unit activations are also returned: t (N x h, S-typed) and, MLP only,
+ *   g = u (1 - t^2) (N x h f64), inside the workspace (see irl_hidden_*). */
+size_t irl_obuild_workspace_bytes(int model, int64_t n, int n_vis, int hidden, int64_t ld, int is_complex);
+int irl_obuild_rbm_f64(const uint8_t* x, int64_t n, int n_vis, int hidden, const double* theta, double* O,
+                       int64_t ld, const double* w, const double* coeff, double* obar, double* g, void* ws,
+                       size_t ws_bytes, void* stream);
+int irl_obuild_rbm_c128(const uint8_t* x, int64_t n, int n_vis, int hidden, const double* theta, double* O,
+                        int64_t ld, const double* w, const double* coeff, double* obar, double* g, void* ws,
+                        size_t ws_bytes, void* stream);
+int irl_obuild_mlp_f64(const uint8_t* x, int64_t n, int n_in, int hidden, const double* theta, double* O,
+                       int64_t ld, const double* w, const double* coeff, double* obar, double* g, void* ws,
+                       size_t ws_bytes, void* stream);
+/* Hidden layer only: t = tanh(b + W x) (N x h), and MLP g = u (1 - t^2). */
+int irl_hidden_rbm_f64(const uint8_t* x, int64_t n, int n_vis, int hidden, const double* theta, double* t,
+                       void* stream);
+int irl_hidden_rbm_c128(const uint8_t* x, int64_t n, int n_vis, int hidden, const double* theta, double* t,
+                        void* stream);
+int irl_hidden_mlp_f64(const uint8_t* x, int64_t n, int n_in, int hidden, const double* theta, double* t,
+                       double* g, void* stream);
+
+/* ------------------------------------------------------- A6/A7/A10 ----
+ * Matrix-free centred product (heff_matvec, estimators.py:171-186; dense_qgt's
+ * matrix-free form, :335-344) with the optional bordered row/column of the
+ * optimizer's closure (optimizer.py:140-148):
+ *   out = O_c^H (coeff * (O_c v))  (+ u0 * half_f)          O_c = O - obar
+ *   out0 = half_f . v   (real part of half_f^H v for c128)
+ * coeff = w (e - E) gives H_eff v ; coeff = w gives S v.
+ * half_f / u0 / out0 may be NULL (plain product).  u0, out0 are device scalars. */
+size_t irl_mvp_workspace_bytes(int64_t n, int64_t ld, int is_complex);
+int irl_mvp_f64(const double* O, int64_t n, int64_t p, int64_t ld, const double* obar, const double* coeff,
+                const double* v, double* out, const double* half_f, const double* u0, double* out0, int mode,
+                void* ws, size_t ws_bytes, void* stream);
+int irl_mvp_c128(const double* O, int64_t n, int64_t p, int64_t ld, const double* obar, const double* coeff,
+                 const double* v_re, const double* v_im, double* out_re, double* out_im, const double* hf_re,
+                 const double* hf_im, const double* u0, double* out0, int mode, void* ws, size_t ws_bytes,
+                 void* stream);
+/* Which path (IRL_MVP_FUSED / IRL_MVP_TWO_PASS) AUTO takes, and its launch
+ * geometry (cluster size, units per slice, threads, rows per stage, stages,
+ * row blocks); for benches and tests.  Returns IRL_OK or an error. */
+int irl_mvp_plan(int64_t n, int64_t ld, int is_complex, int mode, int* out_path, int* out_geom7);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* IRL_SR_H_ */

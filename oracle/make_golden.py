@@ -1,0 +1,226 @@
+"""Generate tests/golden/*.npz from the REAL reference package (this container only).
+
+Run:  python oracle/make_golden.py
+Imports irlnqs read-only from /root/reference/pkg/src (bytecode writing off)
+and records its outputs on small seeded inputs.  The fixtures pin the
+oracle restatement (tests/test_oracle_golden.py) and the device path
+(tests/test_gpu_parity.py).  /root/reference is NOT needed at test time.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+sys.dont_write_bytecode = True
+REF = "/root/reference/pkg"
+sys.path.insert(0, os.path.join(REF, "src"))
+sys.path.insert(0, os.path.join(REF, "tests"))
+
+import numpy as np  # noqa: E402
+
+from irlnqs import ansatz as ans  # noqa: E402
+from irlnqs import estimators as est  # noqa: E402
+from irlnqs import krylov as kry  # noqa: E402
+from irlnqs.hamiltonian import parse_fcidump  # noqa: E402
+from irlnqs.hilbert import OccupationVector  # noqa: E402
+
+OUT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden")
+
+
+def placeholder_batch(w, e, o, n_samples):
+    """SampleBatch with placeholder configs."""
+    configs = (OccupationVector(0, 2),) * len(w)
+    return est.SampleBatch(configs=configs, weights=w, e_loc=e, o_matrix=o, n_samples=n_samples)
+
+
+def bordered(batch, energy, grad):
+    """opt:140-148 minus the offdiag term (synthetic E_loc)."""
+    p = batch.param_count
+    half = 0.5 * grad
+
+    def matvec(u):
+        out = np.empty(p + 1)
+        out[0] = half @ u[1:]
+        out[1:] = u[0] * half + est.heff_matvec(batch, energy, u[1:])
+        return out
+
+    return matvec
+
+
+def direction(vec, grad):
+    c0 = vec[0]
+    d = vec[1:]
+    if abs(c0) > 1e-12:
+        return d / c0
+    return -d if float(grad @ d) > 0 else d
+
+
+def rbm_rows_np(theta, x, n, h):
+    xf = x.astype(float)
+    a, b, w = theta[:n], theta[n : n + h], theta[n + h :].reshape(h, n)
+    t = np.tanh(b + xf @ w.T)
+    return np.concatenate([xf.astype(t.dtype), t, (t[:, :, None] * xf[:, None, :]).reshape(len(x), -1)], axis=1)
+
+
+def case_real(seed=7, n=6, h=5, N=96, m=20):
+    """Real RBM-shaped batch (P = n + h + h n = 41)."""
+    rng = np.random.default_rng(seed)
+    x = np.zeros((N, n), dtype=np.uint8)
+    occ = np.argsort(rng.random((N, n)), axis=1)[:, : n // 2]
+    x[np.arange(N)[:, None], occ] = 1
+    theta = rng.normal(0, 0.3, n + h + h * n)
+    e = rng.normal(-7.5, 0.4, N)
+    w = np.full(N, 1.0 / N)
+    o = rbm_rows_np(theta, x, n, h)
+    batch = placeholder_batch(w, e, o, N)
+    energy = est.estimate_energy(batch)
+    grad = est.energy_gradient(batch, energy)
+    vs = rng.standard_normal((4, o.shape[1]))
+    hv = np.array([est.heff_matvec(batch, energy, v) for v in vs])
+    sb = placeholder_batch(w, np.ones(N), o, N)
+    sv = np.array([est.heff_matvec(sb, est.EnergyEstimate(0.0, 0.0, 0.0), v) for v in vs])
+    pair = kry.irl_smallest(bordered(batch, energy, grad), o.shape[1] + 1, m=m, tol=1e-12, max_restarts=3, seed=seed)
+    return dict(
+        x=x, theta=theta, n=n, h=h, e=e, w=w, o=o, mean=energy.mean, variance=energy.variance,
+        std_error=energy.std_error, grad=grad, vs=vs, hv=hv, sv=sv,
+        dense_heff=est.dense_heff(batch, energy), dense_qgt=est.dense_qgt(batch),
+        lam=pair.value, vec=pair.vector, residual=pair.residual, n_matvec=pair.n_matvec,
+        n_restarts=pair.n_restarts, converged=pair.converged, direction=direction(pair.vector, grad),
+        m=m, seed=seed,
+    )
+
+
+def case_complex_raw(seed=11, N=80, P=19, m=20):
+    """Complex O and E_loc with real parameters: the reference's own convention."""
+    rng = np.random.default_rng(seed)
+    o = rng.normal(0.2, 0.5, (N, P)) + 1j * rng.normal(-0.1, 0.5, (N, P))
+    e = rng.normal(-3.0, 0.2, N) + 1j * rng.normal(0.0, 0.05, N)
+    w = rng.random(N) + 0.1
+    w = w / w.sum()
+    batch = placeholder_batch(w, e, o, N)
+    energy = est.estimate_energy(batch)
+    grad = est.energy_gradient(batch, energy)
+    vs = rng.standard_normal((4, P))
+    hv = np.array([est.heff_matvec(batch, energy, v) for v in vs])
+    pair = kry.irl_smallest(bordered(batch, energy, grad), P + 1, m=m, tol=1e-12, max_restarts=3, seed=seed)
+    return dict(o=o, e=e, w=w, mean=energy.mean, variance=energy.variance, std_error=energy.std_error, grad=grad,
+                vs=vs, hv=hv, lam=pair.value, vec=pair.vector, n_matvec=pair.n_matvec, residual=pair.residual,
+                direction=direction(pair.vector, grad), m=m, seed=seed, n_samples=N)
+
+
+def case_hermitian(seed=13, n=4, h=3, N=72, m=20):
+    """Complex-parameter RBM through the real embedding [O, iO]."""
+    rng = np.random.default_rng(seed)
+    x = np.zeros((N, n), dtype=np.uint8)
+    occ = np.argsort(rng.random((N, n)), axis=1)[:, : n // 2]
+    x[np.arange(N)[:, None], occ] = 1
+    P = n + h + h * n
+    theta = rng.normal(0, 0.2, P) + 1j * rng.normal(0, 0.2, P)
+    e = rng.normal(-5.0, 0.3, N) + 1j * rng.normal(0.0, 0.1, N)
+    w = np.full(N, 1.0 / N)
+    o = rbm_rows_np(theta, x, n, h)
+    emb = np.concatenate([o, 1j * o], axis=1)
+    gbatch = placeholder_batch(w, e, emb, N)
+    energy = est.estimate_energy(gbatch)
+    grad = est.energy_gradient(gbatch, energy)
+    hbatch = placeholder_batch(w, e.real.copy(), emb, N)
+    vs = rng.standard_normal((3, 2 * P))
+    hv = np.array([est.heff_matvec(hbatch, energy, v) for v in vs])
+    pair = kry.irl_smallest(bordered(hbatch, energy, grad), 2 * P + 1, m=m, tol=1e-12, max_restarts=3, seed=seed)
+    return dict(x=x, theta=theta, n=n, h=h, e=e, w=w, o=o, mean=energy.mean, grad=grad, vs=vs, hv=hv,
+                lam=pair.value, vec=pair.vector, n_matvec=pair.n_matvec, residual=pair.residual,
+                direction=direction(pair.vector, grad), m=m, seed=seed)
+
+
+def case_h2():
+    """The reference's own data path: H2 exact mode, autoregressive ansatz
+    (T/test_estimators.py:20-28 setup, hidden 3, seed 9)."""
+    with open(os.path.join(REF, "tests", "data", "h2_sto3g.fcidump")) as fh:
+        integrals = parse_fcidump(fh.read())
+    sector = integrals.sector()
+    arch = ans.Architecture(sector.n_orbitals, 3)
+    params = ans.init_parameters(arch, seed=9)
+    rng = np.random.default_rng(41)
+    theta = params.theta + 0.1 * rng.standard_normal(arch.param_count)  # generic complex state (:31-41)
+    params = ans.AnsatzParameters(arch, theta)
+    batch = est.build_batch(params, integrals, sector)
+    energy = est.estimate_energy(batch)
+    grad = est.energy_gradient(batch, energy)
+    vs = np.random.default_rng(55).standard_normal((5, batch.param_count))
+    hv = np.array([est.heff_matvec(batch, energy, v) for v in vs])
+    return dict(o=np.array(batch.o_matrix), e=np.array(batch.e_loc), w=np.array(batch.weights),
+                mean=energy.mean, variance=energy.variance, grad=grad, vs=vs, hv=hv,
+                dense_heff=est.dense_heff(batch, energy), dense_qgt=est.dense_qgt(batch))
+
+
+def case_mlp_phase_head(seed=17):
+    """MLP rows == reference phase-head gradient (ans:278-288) minus w_lin."""
+    arch = ans.Architecture(6, 5)
+    rng = np.random.default_rng(seed)
+    theta = ans.init_parameters(arch, seed=seed).theta + 0.3 * rng.standard_normal(arch.param_count)
+    params = ans.AnsatzParameters(arch, theta)
+    from irlnqs.hilbert import Sector, enumerate_sector
+
+    sector = Sector(6, 2, 1)
+    xs = enumerate_sector(sector)[:12]
+    m, h = arch.n_orbitals, arch.hidden
+    sizes = [h * 2 * m, h, 2 * h, 2, h * m, h, h, m, 1]
+    off = np.cumsum([0] + sizes)
+    rows = []
+    s_list = []
+    for x in xs:
+        od = ans.log_derivative(params, x, sector).imag
+        rows.append(np.concatenate([od[off[4] : off[5]], od[off[5] : off[6]], od[off[6] : off[7]], od[off[8] : off[9]]]))
+        s_list.append([1.0 if x.occupied(j) else -1.0 for j in range(m)])
+    mlp_theta = np.concatenate([theta[off[4] : off[5]], theta[off[5] : off[6]], theta[off[6] : off[7]], theta[off[8] : off[9]]])
+    return dict(s=np.array(s_list), theta=mlp_theta, n=m, h=h, rows=np.array(rows))
+
+
+def case_krylov(seed=100, count=4):
+    """Reference irl_smallest / lanczos / implicit_restart on random symmetric matrices
+    (the T/oracles.py:158-163 construction)."""
+    from oracles import random_symmetric
+
+    rng = np.random.default_rng(seed)
+    out = {}
+    for i in range(count):
+        dim = int(rng.integers(60, 160))
+        mat = random_symmetric(rng, dim, condition=10.0 ** rng.uniform(1, 3))
+        pair = kry.irl_smallest(lambda v: mat @ v, dim, m=20, tol=1e-12, seed=i)
+        v1 = rng.standard_normal(dim)
+        v1 /= np.linalg.norm(v1)
+        lz = kry.lanczos(lambda v: mat @ v, v1, 20)
+        vals, _ = kry.tridiag_eigen(lz.tri)
+        nb, nt = kry.implicit_restart(lz.basis, lz.tri, vals[1:], 1)
+        nb5, nt5 = kry.implicit_restart(lz.basis, lz.tri, vals[5:], 5)
+        out.update({
+            f"mat{i}": mat, f"value{i}": pair.value, f"vector{i}": pair.vector, f"residual{i}": pair.residual,
+            f"n_matvec{i}": pair.n_matvec, f"n_restarts{i}": pair.n_restarts, f"v1_{i}": v1,
+            f"alpha{i}": lz.tri.alpha, f"beta{i}": lz.tri.beta, f"beta_last{i}": lz.tri.beta_last,
+            f"restart_v{i}": nb.vectors, f"restart_next{i}": nb.next_vector, f"restart_alpha{i}": nt.alpha,
+            f"restart_beta_last{i}": nt.beta_last, f"restart5_v{i}": nb5.vectors, f"restart5_alpha{i}": nt5.alpha,
+            f"restart5_beta{i}": nt5.beta, f"restart5_beta_last{i}": nt5.beta_last,
+        })
+    out["count"] = count
+    return out
+
+
+def main():
+    os.makedirs(OUT, exist_ok=True)
+    cases = {
+        "real_rbm": case_real(),
+        "complex_raw": case_complex_raw(),
+        "hermitian_rbm": case_hermitian(),
+        "h2_exact": case_h2(),
+        "mlp_phase_head": case_mlp_phase_head(),
+        "krylov": case_krylov(),
+    }
+    for name, data in cases.items():
+        path = os.path.join(OUT, f"{name}.npz")
+        np.savez_compressed(path, **data)
+        print(f"wrote {path} ({os.path.getsize(path)} bytes)")
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,216 @@
+"""Shallow NQS ansaetze (RBM, one-hidden-layer MLP) with batched device O-rows.
+
+The reference's only ansatz is autoregressive (``ansatz.py:1-14``); BASELINE
+names RBM and shallow-MLP NQS, so this module keeps the reference's *NQS
+seam* — ``Architecture.param_count`` (``ans:26-38``), ``AnsatzParameters``
+(``ans:41-53``), ``log_derivative(params, x, sector)`` (``ans:249-290``) — and
+adds the batched form the hot path needs, ``log_derivative_batch`` and
+``build_batch`` (the role of ``estimators.build_batch``, ``est:79-133``, with
+synthetic E_loc instead of a Hamiltonian).
+
+Encodings: inputs are 0/1 occupations (``sigma_i = x_i``), not
+the reference's +-1 encodings (``ans:156-162``, ``ans:243-246``).
+
+Rows (layouts SURVEY Appendix A):
+
+* RBM  theta = [a (n), b (h), W (h x n)],  theta_j = b_j + sum_i W_ji x_i,
+  O = [x (n), tanh theta (h), (tanh theta_j x_i)_{j,i} (h n)]   (holomorphic
+  in complex theta: cfg4);
+* MLP  theta = [W (h x n_in), b (h), u (h), c],  t = tanh(W x + b),
+  g = u (1 - t^2),  O = [(g_j x_k)_{j,k} (h n_in), g (h), t (h), 1]
+  — the reference phase-head gradient (``ans:278-288``) without ``w_lin``.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .estimators import KIND_HERMITIAN, KIND_REAL, SampleBatch, _as_tensor, _device
+
+
+@dataclass(frozen=True)
+class RBMArchitecture:
+    n_visible: int
+    hidden: int
+    complex_params: bool = False
+
+    @property
+    def param_count(self) -> int:
+        n, h = self.n_visible, self.hidden
+        return n + h + h * n
+
+    @property
+    def model(self) -> int:
+        return _lib.MODEL_RBM
+
+    @property
+    def n_inputs(self) -> int:
+        return self.n_visible
+
+
+@dataclass(frozen=True)
+class MLPArchitecture:
+    n_in: int
+    hidden: int
+    complex_params: bool = False
+
+    def __post_init__(self):
+        if self.complex_params:
+            raise ValueError("the shallow MLP NQS has real parameters")
+
+    @property
+    def param_count(self) -> int:
+        return self.hidden * self.n_in + 2 * self.hidden + 1
+
+    @property
+    def model(self) -> int:
+        return _lib.MODEL_MLP
+
+    @property
+    def n_inputs(self) -> int:
+        return self.n_in
+
+
+Architecture = RBMArchitecture | MLPArchitecture
+
+
+@dataclass(frozen=True)
+class AnsatzParameters:
+    """Flat parameter vector for an architecture (ans:41-53)."""
+
+    architecture: RBMArchitecture | MLPArchitecture
+    theta: np.ndarray
+
+    def __post_init__(self):
+        want = (self.architecture.param_count,)
+        if tuple(np.shape(self.theta)) != want:
+            raise ValueError(
+                f"theta has length {np.shape(self.theta)}, architecture needs {self.architecture.param_count}"
+            )
+        if self.architecture.complex_params != np.iscomplexobj(self.theta):
+            raise ValueError("theta dtype does not match architecture.complex_params")
+        if isinstance(self.theta, np.ndarray):
+            self.theta.setflags(write=False)
+
+
+def _theta_device(params: AnsatzParameters, dev) -> torch.Tensor:
+    arch = params.architecture
+    if arch.complex_params:
+        t = torch.as_tensor(np.ascontiguousarray(params.theta, dtype=np.complex128), device=dev)
+        return torch.view_as_real(t).reshape(-1).contiguous()  # interleaved (re, im)
+    return torch.as_tensor(np.ascontiguousarray(params.theta, dtype=np.float64), device=dev)
+
+
+def _x_device(x, n_inputs: int, dev) -> torch.Tensor:
+    xt = _as_tensor(x, torch.uint8, dev).contiguous()
+    if xt.dim() != 2 or xt.shape[1] != n_inputs:
+        raise ValueError(f"x must be (N, {n_inputs}) 0/1 occupations")
+    return xt
+
+
+def build_batch(params: AnsatzParameters, x, e_loc, weights=None, n_samples: int | None = None,
+                device=None) -> SampleBatch:
+    """Device SampleBatch with O built by the fused row kernel (K1/K2).
+
+    One launch sequence: k_energy (E, c = w (e - E)) -> k_hidden (tanh layer)
+    -> k_orows (O rows + fused sum w conj(O), sum c conj(O)) -> finisher.
+    ``weights`` defaults to 1/N (stochastic mode, est:99-100).
+    """
+    dev = _device(device)
+    arch = params.architecture
+    xt = _x_device(x, arch.n_inputs, dev)
+    n = int(xt.shape[0])
+    if n < 1:
+        raise ValueError("empty batch")
+    if weights is None:
+        weights = torch.full((n,), 1.0 / n, dtype=torch.float64, device=dev)
+        if n_samples is None:
+            n_samples = n
+    kind = KIND_HERMITIAN if arch.complex_params else KIND_REAL
+    p = arch.param_count
+    ld = _lib.padded_ld(p, arch.complex_params)
+    odt = torch.complex128 if arch.complex_params else torch.float64
+    o = torch.empty((n, ld), dtype=odt, device=dev)
+    batch = SampleBatch(None, weights, e_loc, o, n_samples or 0, kind=kind, param_count=p, device=dev)
+    _, coeff = batch._energy_pass(None)
+    obar = torch.empty(ld, dtype=odt, device=dev)
+    g = torch.empty(ld, dtype=odt, device=dev)
+    fill_o_rows(params, xt, o, batch.weights, coeff, obar, g)
+    batch._set_colstats(batch._stats_e, obar, g, coeff)
+    return batch
+
+
+def fill_o_rows(params: AnsatzParameters, xt: torch.Tensor, o: torch.Tensor, w: torch.Tensor,
+                coeff: torch.Tensor, obar: torch.Tensor, g: torch.Tensor) -> None:
+    """Launch the O-row kernel into preallocated device buffers."""
+    arch = params.architecture
+    dev = o.device
+    n = int(xt.shape[0])
+    ld = int(o.shape[1])
+    theta = _theta_device(params, dev)
+    lib = _lib.lib()
+    nbytes = int(lib.irl_obuild_workspace_bytes(arch.model, n, arch.n_inputs, arch.hidden, ld,
+                                                int(arch.complex_params)))
+    if nbytes == 0:
+        raise _lib.NativeError("irl_obuild_workspace_bytes", -1, lib.irl_last_error().decode())
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    if arch.model == _lib.MODEL_RBM:
+        fn = "irl_obuild_rbm_c128" if arch.complex_params else "irl_obuild_rbm_f64"
+    else:
+        fn = "irl_obuild_mlp_f64"
+    _lib.call(fn, _lib.ptr(xt), n, arch.n_inputs, arch.hidden, _lib.ptr(theta), _lib.ptr(o), ld, _lib.ptr(w),
+              _lib.ptr(coeff), _lib.ptr(obar), _lib.ptr(g), _lib.ptr(ws), nbytes, _lib.stream_handle(dev))
+
+
+def log_derivative_batch(params: AnsatzParameters, x, device=None) -> torch.Tensor:
+    """O = d log psi / d theta for every row of x: device tensor (N, P) view of
+    the padded (N, ld) row-major buffer (weights 1/N for the fused stats)."""
+    dev = _device(device)
+    arch = params.architecture
+    xt = _x_device(x, arch.n_inputs, dev)
+    n = int(xt.shape[0])
+    ld = _lib.padded_ld(arch.param_count, arch.complex_params)
+    odt = torch.complex128 if arch.complex_params else torch.float64
+    o = torch.empty((n, ld), dtype=odt, device=dev)
+    w = torch.full((n,), 1.0 / n, dtype=torch.float64, device=dev)
+    coeff = torch.zeros(n, dtype=odt, device=dev)
+    obar = torch.empty(ld, dtype=odt, device=dev)
+    g = torch.empty(ld, dtype=odt, device=dev)
+    fill_o_rows(params, xt, o, w, coeff, obar, g)
+    return o[:, : arch.param_count]
+
+
+def log_derivative(params: AnsatzParameters, x, sector=None) -> np.ndarray:
+    """Single-sample O(x) (ans:249-290 signature); ``sector`` is accepted for
+    API parity and unused (RBM/MLP have no particle-number mask)."""
+    xa = np.asarray(x, dtype=np.uint8).reshape(1, -1)
+    return log_derivative_batch(params, xa)[0].cpu().numpy()
+
+
+def hidden_activations(params: AnsatzParameters, x, device=None):
+    """(t, g) hidden-layer activations on device (g is None for the RBM)."""
+    dev = _device(device)
+    arch = params.architecture
+    xt = _x_device(x, arch.n_inputs, dev)
+    n = int(xt.shape[0])
+    theta = _theta_device(params, dev)
+    st = _lib.stream_handle(dev)
+    if arch.model == _lib.MODEL_RBM:
+        if arch.complex_params:
+            t = torch.empty((n, arch.hidden), dtype=torch.complex128, device=dev)
+            _lib.call("irl_hidden_rbm_c128", _lib.ptr(xt), n, arch.n_visible, arch.hidden, _lib.ptr(theta),
+                      _lib.ptr(t), st)
+        else:
+            t = torch.empty((n, arch.hidden), dtype=torch.float64, device=dev)
+            _lib.call("irl_hidden_rbm_f64", _lib.ptr(xt), n, arch.n_visible, arch.hidden, _lib.ptr(theta),
+                      _lib.ptr(t), st)
+        return t, None
+    t = torch.empty((n, arch.hidden), dtype=torch.float64, device=dev)
+    g = torch.empty((n, arch.hidden), dtype=torch.float64, device=dev)
+    _lib.call("irl_hidden_mlp_f64", _lib.ptr(xt), n, arch.n_in, arch.hidden, _lib.ptr(theta), _lib.ptr(t),
+              _lib.ptr(g), st)
+    return t, g

@@ -1,0 +1,663 @@
+// Host side of the C-ABI (include/irl_sr.h): argument checks, launch plans,
+// workspace carving, kernel dispatch.  No allocation, no synchronisation.
+#include <climits>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_set>
+
+#include "../../include/irl_sr.h"
+#include "obuild.cuh"
+#include "stream.cuh"
+
+using namespace irl;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return IRL_OK;
+  cudaGetLastError();
+  return fail(IRL_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define IRL_TRY(expr)            \
+  do {                           \
+    int _rc = (expr);            \
+    if (_rc != IRL_OK) return _rc; \
+  } while (0)
+
+struct DevInfo {
+  int sms = 0;
+  int smem_optin = 0;
+  int major = 0;
+};
+
+int dev_info(DevInfo& d) {
+  static DevInfo cache[64];
+  static std::mutex mu;
+  int dev = 0;
+  IRL_TRY(cuda_check(cudaGetDevice(&dev), "cudaGetDevice"));
+  if (dev < 0 || dev >= 64) return fail(IRL_ERR_DEVICE, "device index %d", dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (cache[dev].sms == 0) {
+    DevInfo t;
+    IRL_TRY(cuda_check(cudaDeviceGetAttribute(&t.sms, cudaDevAttrMultiProcessorCount, dev), "attr"));
+    IRL_TRY(cuda_check(cudaDeviceGetAttribute(&t.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev), "attr"));
+    IRL_TRY(cuda_check(cudaDeviceGetAttribute(&t.major, cudaDevAttrComputeCapabilityMajor, dev), "attr"));
+    cache[dev] = t;
+  }
+  d = cache[dev];
+  if (d.major != 10) return fail(IRL_ERR_DEVICE, "compute capability %d.x: this library is built for sm_100a", d.major);
+  return IRL_OK;
+}
+
+int ensure_fn_attrs(const void* fn, int smem_optin) {
+  static std::mutex mu;
+  static std::unordered_set<const void*> done;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count(fn)) return IRL_OK;
+  IRL_TRY(cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin),
+                     "cudaFuncSetAttribute(smem)"));
+  // cluster size 16 is non-portable; harmless for non-cluster launches
+  cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaGetLastError();
+  done.insert(fn);
+  return IRL_OK;
+}
+
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int64_t rup(int64_t a, int64_t b) { return cdiv(a, b) * b; }
+inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+bool aligned16(const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// ----------------------------------------------------------- kernels ----
+using StreamFn = void (*)(StreamArgs);
+
+template <bool CPLX, int MODE>
+StreamFn pick_stream(int ppt, int R) {
+#define IRL_CASE(P, RR) \
+  if (ppt == P && R == RR) return k_stream<CPLX, P, RR, MODE>;
+  IRL_CASE(2, 1) IRL_CASE(2, 4) IRL_CASE(4, 1) IRL_CASE(4, 4)
+  IRL_CASE(8, 1) IRL_CASE(8, 4) IRL_CASE(16, 1) IRL_CASE(16, 4)
+#undef IRL_CASE
+  return nullptr;
+}
+
+StreamFn pick_stream_any(bool cplx, int mode, int ppt, int R) {
+  switch (mode) {
+    case MODE_FUSED: return cplx ? pick_stream<true, MODE_FUSED>(ppt, R) : pick_stream<false, MODE_FUSED>(ppt, R);
+    case MODE_DOT: return cplx ? pick_stream<true, MODE_DOT>(ppt, R) : pick_stream<false, MODE_DOT>(ppt, R);
+    case MODE_ACC: return cplx ? pick_stream<true, MODE_ACC>(ppt, R) : pick_stream<false, MODE_ACC>(ppt, R);
+    default: return cplx ? pick_stream<true, MODE_STATS>(ppt, R) : pick_stream<false, MODE_STATS>(ppt, R);
+  }
+}
+
+struct Plan {
+  int mode = 0;
+  int C = 0, W = 0, PPT = 0, R = 0, NT = 0, NS = 0, nb = 0;
+  size_t smem = 0;
+  StreamFn fn = nullptr;
+};
+
+size_t stream_extra_smem(bool cplx, int R, int NW, int C, int NS) {
+  const size_t sS = cplx ? 16 : 8;
+  return (size_t)(2 * NS + 2) * 8 + (size_t)2 * R * (NW + 1) * sS + (size_t)2 * C * R * sS + 33 * sS + 33 * 8;
+}
+
+bool choose_geom(int64_t ld_u, int C, bool cplx, int mode, int budget, Plan& p) {
+  if (ld_u % C) return false;
+  const int64_t W = ld_u / C;
+  if (W > INT_MAX / 16) return false;
+  int best_ppt = 0, best_nt = 0;
+  int64_t best_waste = INT64_MAX;
+  for (int ppt : {16, 8, 4, 2}) {
+    int64_t nt = rup(cdiv(W, ppt), 32);
+    if (nt < 64) nt = 64;
+    if (nt > stream_max_nt(ppt)) continue;
+    const int64_t waste = nt * ppt - W;
+    if (waste < best_waste) {
+      best_waste = waste;
+      best_ppt = ppt;
+      best_nt = (int)nt;
+    }
+  }
+  if (!best_ppt) return false;
+  const size_t slice = (size_t)W * 16;
+  const int R = (4 * slice <= 64 * 1024) ? 4 : 1;
+  const int NW = best_nt / 32;
+  const size_t extra = stream_extra_smem(cplx, R, NW, C, 8);
+  if ((size_t)budget <= extra) return false;
+  int NS = (int)std::min<size_t>(8, ((size_t)budget - extra) / (R * slice));
+  if (NS < 2) return false;
+  p.mode = mode;
+  p.C = C;
+  p.W = (int)W;
+  p.PPT = best_ppt;
+  p.R = R;
+  p.NT = best_nt;
+  p.NS = NS;
+  p.smem = (size_t)NS * R * slice + stream_extra_smem(cplx, R, NW, C, NS);
+  p.fn = pick_stream_any(cplx, mode, best_ppt, R);
+  return p.fn != nullptr;
+}
+
+int occupancy_blocks(const Plan& p, int& occ) {
+  IRL_TRY(cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)p.fn, p.NT + 32, p.smem),
+                     "occupancy"));
+  if (occ < 1) return fail(IRL_ERR_DEVICE, "kernel does not fit on an SM (smem %zu)", p.smem);
+  return IRL_OK;
+}
+
+int make_plan(int64_t n, int64_t ld_u, bool cplx, int mode, Plan& p) {
+  (void)n;
+  DevInfo d;
+  IRL_TRY(dev_info(d));
+  const int budget = d.smem_optin;
+  if (mode == MODE_FUSED) {
+    for (int C : {1, 2, 4, 8, 16}) {
+      if (!choose_geom(ld_u, C, cplx, mode, budget, p)) continue;
+      IRL_TRY(ensure_fn_attrs((const void*)p.fn, budget));
+      if (C == 1) {
+        int occ = 0;
+        IRL_TRY(occupancy_blocks(p, occ));
+        p.nb = d.sms * occ;
+        return IRL_OK;
+      }
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = C;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.gridDim = dim3(C * (d.sms / C));
+      cfg.blockDim = dim3(p.NT + 32);
+      cfg.dynamicSmemBytes = p.smem;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      int ncl = 0;
+      cudaError_t e = cudaOccupancyMaxActiveClusters(&ncl, (const void*)p.fn, &cfg);
+      if (e != cudaSuccess || ncl < 1) {
+        cudaGetLastError();
+        continue;
+      }
+      p.nb = ncl;
+      return IRL_OK;
+    }
+    return fail(IRL_ERR_DEVICE, "no fused single-pass geometry for ld=%lld units", (long long)ld_u);
+  }
+  for (int C = 1; C <= 1024; C *= 2) {
+    if (!choose_geom(ld_u, C, cplx, mode, budget, p)) continue;
+    IRL_TRY(ensure_fn_attrs((const void*)p.fn, budget));
+    int occ = 0;
+    IRL_TRY(occupancy_blocks(p, occ));
+    p.nb = std::max(1, (d.sms * occ) / C);
+    return IRL_OK;
+  }
+  return fail(IRL_ERR_DEVICE, "no streaming geometry for ld=%lld units", (long long)ld_u);
+}
+
+int launch_stream(const Plan& p, const StreamArgs& a, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  cfg.gridDim = dim3((unsigned)(p.nb * p.C));
+  cfg.blockDim = dim3(p.NT + 32);
+  cfg.dynamicSmemBytes = p.smem;
+  cfg.stream = st;
+  cfg.numAttrs = 0;
+  if (p.mode == MODE_FUSED && p.C > 1) {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = p.C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  StreamArgs args = a;
+  args.W = p.W;
+  args.C = p.C;
+  args.nb = p.nb;
+  args.stages = p.NS;
+  void* kargs[] = {&args};
+  return cuda_check(cudaLaunchKernelExC(&cfg, (const void*)p.fn, kargs), "stream kernel launch");
+}
+
+// MVP workspace layout for one plan
+struct MvpWs {
+  double2* part;
+  void* ysum;
+  void* tpart;
+  void* spart;
+  double* gpart;
+  size_t bytes;
+};
+
+MvpWs mvp_ws_layout(const Plan& p, int64_t n, int64_t ld_u, bool cplx, void* base) {
+  const size_t sS = cplx ? 16 : 8;
+  size_t off = 0;
+  MvpWs w{};
+  auto carve = [&](size_t b) {
+    void* r = base ? static_cast<char*>(base) + off : nullptr;
+    off += align256(b);
+    return r;
+  };
+  w.part = (double2*)carve((size_t)p.nb * ld_u * 16);
+  w.ysum = carve((size_t)p.nb * sS);
+  w.tpart = carve(p.mode == MODE_FUSED ? 0 : (size_t)p.C * n * sS);
+  w.spart = carve((size_t)std::max(p.C, 1) * sS);
+  w.gpart = (double*)carve((size_t)std::max(p.C, 1) * 8);
+  w.bytes = off;
+  return w;
+}
+
+int mvp_impl(bool cplx, const double* O, int64_t n, int64_t p, int64_t ld, const double* obar, const double* coeff,
+             const double* v_re, const double* v_im, double* out_re, double* out_im, const double* hf_re,
+             const double* hf_im, const double* u0, double* out0, int mode, void* ws, size_t ws_bytes,
+             cudaStream_t st) {
+  if (!O || !coeff || !v_re || !out_re) return fail(IRL_ERR_ARG, "null required pointer");
+  if (n < 1 || p < 1 || ld < p) return fail(IRL_ERR_ARG, "bad shape n=%lld p=%lld ld=%lld", (long long)n,
+                                            (long long)p, (long long)ld);
+  if (ld != irl_padded_ld(p, cplx)) return fail(IRL_ERR_ALIGN, "ld must equal irl_padded_ld(p)");
+  if (!aligned16(O) || !aligned16(obar) || !aligned16(ws) || (!cplx && (!aligned16(v_re) || !aligned16(out_re) ||
+                                                                       !aligned16(hf_re))))
+    return fail(IRL_ERR_ALIGN, "pointers must be 16-byte aligned");
+  const int64_t ld_u = cplx ? ld : ld / 2;
+  int path = mode;
+  Plan pl;
+  if (mode == IRL_MVP_AUTO || mode == IRL_MVP_FUSED) {
+    int rc = make_plan(n, ld_u, cplx, MODE_FUSED, pl);
+    if (rc == IRL_OK) {
+      path = IRL_MVP_FUSED;
+    } else if (mode == IRL_MVP_FUSED) {
+      return rc;
+    } else {
+      path = IRL_MVP_TWO_PASS;
+    }
+  } else if (mode != IRL_MVP_TWO_PASS) {
+    return fail(IRL_ERR_ARG, "bad mvp mode %d", mode);
+  }
+  StreamArgs a{};
+  a.O = reinterpret_cast<const double2*>(O);
+  a.n_rows = n;
+  a.ld_u = ld_u;
+  a.v_re = v_re;
+  a.v_im = v_im;
+  a.hf_re = hf_re;
+  a.hf_im = hf_im;
+  a.obar = reinterpret_cast<const double2*>(obar);
+  a.coeff0 = coeff;
+  if (path == IRL_MVP_FUSED) {
+    MvpWs w = mvp_ws_layout(pl, n, ld_u, cplx, ws);
+    if (ws_bytes < w.bytes) return fail(IRL_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, w.bytes);
+    a.part0 = w.part;
+    a.ysum = w.ysum;
+    a.spart = w.spart;
+    a.gpart = w.gpart;
+    IRL_TRY(launch_stream(pl, a, st));
+    const int64_t blocks = std::min<int64_t>(cdiv(ld_u, 256), 4096);
+    if (cplx)
+      k_finish_mvp<true><<<(unsigned)blocks, 256, 0, st>>>(w.part, pl.nb, ld_u, w.ysum, a.obar, hf_re, hf_im, u0,
+                                                           out_re, out_im, w.gpart, 1, out0);
+    else
+      k_finish_mvp<false><<<(unsigned)blocks, 256, 0, st>>>(w.part, pl.nb, ld_u, w.ysum, a.obar, hf_re, hf_im, u0,
+                                                            out_re, out_im, w.gpart, 1, out0);
+    return cuda_check(cudaGetLastError(), "finish kernel launch");
+  }
+  Plan p1, p2;
+  IRL_TRY(make_plan(n, ld_u, cplx, MODE_DOT, p1));
+  IRL_TRY(make_plan(n, ld_u, cplx, MODE_ACC, p2));
+  // both passes must agree on the column split (ACC sums the DOT tile partials)
+  if (p1.C != p2.C) return fail(IRL_ERR_DEVICE, "two-pass plans disagree on column split");
+  Plan pw = p1;
+  pw.nb = std::max(p1.nb, p2.nb);
+  MvpWs w = mvp_ws_layout(pw, n, ld_u, cplx, ws);
+  if (ws_bytes < w.bytes) return fail(IRL_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, w.bytes);
+  a.part0 = w.part;
+  a.ysum = w.ysum;
+  a.tpart = w.tpart;
+  a.spart = w.spart;
+  a.gpart = w.gpart;
+  IRL_TRY(launch_stream(p1, a, st));
+  IRL_TRY(launch_stream(p2, a, st));
+  const int64_t blocks = std::min<int64_t>(cdiv(ld_u, 256), 4096);
+  if (cplx)
+    k_finish_mvp<true><<<(unsigned)blocks, 256, 0, st>>>(w.part, p2.nb, ld_u, w.ysum, a.obar, hf_re, hf_im, u0,
+                                                         out_re, out_im, w.gpart, p1.C, out0);
+  else
+    k_finish_mvp<false><<<(unsigned)blocks, 256, 0, st>>>(w.part, p2.nb, ld_u, w.ysum, a.obar, hf_re, hf_im, u0,
+                                                          out_re, out_im, w.gpart, p1.C, out0);
+  return cuda_check(cudaGetLastError(), "finish kernel launch");
+}
+
+size_t mvp_ws_bytes(int64_t n, int64_t ld, bool cplx) {
+  const int64_t ld_u = cplx ? ld : ld / 2;
+  size_t best = 0;
+  Plan p;
+  if (make_plan(n, ld_u, cplx, MODE_FUSED, p) == IRL_OK) best = std::max(best, mvp_ws_layout(p, n, ld_u, cplx, nullptr).bytes);
+  Plan p1, p2;
+  if (make_plan(n, ld_u, cplx, MODE_DOT, p1) == IRL_OK && make_plan(n, ld_u, cplx, MODE_ACC, p2) == IRL_OK) {
+    p1.nb = std::max(p1.nb, p2.nb);
+    best = std::max(best, mvp_ws_layout(p1, n, ld_u, cplx, nullptr).bytes);
+  }
+  g_err.clear();
+  return best;
+}
+
+// --------------------------------------------------------- colstats ----
+size_t colstats_bytes(const Plan& p, int64_t ld_u) { return 2 * align256((size_t)p.nb * ld_u * 16); }
+
+int colstats_impl(bool cplx, const double* O, int64_t n, int64_t ld, const double* w, const double* coeff,
+                  double* obar, double* g, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (!O || !w || !coeff || !obar || !g) return fail(IRL_ERR_ARG, "null pointer");
+  if (n < 1 || ld < 1 || (!cplx && (ld & 1))) return fail(IRL_ERR_ARG, "bad shape");
+  if (!aligned16(O) || !aligned16(obar) || !aligned16(g) || !aligned16(ws)) return fail(IRL_ERR_ALIGN, "alignment");
+  const int64_t ld_u = cplx ? ld : ld / 2;
+  Plan p;
+  IRL_TRY(make_plan(n, ld_u, cplx, MODE_STATS, p));
+  const size_t need = colstats_bytes(p, ld_u);
+  if (ws_bytes < need) return fail(IRL_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, need);
+  StreamArgs a{};
+  a.O = reinterpret_cast<const double2*>(O);
+  a.n_rows = n;
+  a.ld_u = ld_u;
+  a.coeff0 = w;
+  a.coeff1 = coeff;
+  a.part0 = static_cast<double2*>(ws);
+  a.part1 = reinterpret_cast<double2*>(static_cast<char*>(ws) + align256((size_t)p.nb * ld_u * 16));
+  IRL_TRY(launch_stream(p, a, st));
+  const int64_t blocks = std::min<int64_t>(cdiv(ld_u, 256), 4096);
+  if (cplx)
+    k_finish_stats<true><<<(unsigned)blocks, 256, 0, st>>>(a.part0, a.part1, p.nb, ld_u, (double2*)obar, (double2*)g);
+  else
+    k_finish_stats<false><<<(unsigned)blocks, 256, 0, st>>>(a.part0, a.part1, p.nb, ld_u, (double2*)obar, (double2*)g);
+  return cuda_check(cudaGetLastError(), "colstats finish launch");
+}
+
+// ------------------------------------------------------------ obuild ----
+struct OPlan {
+  int C, W, PPT, NT, nb;
+  void (*fn)(ORowArgs);
+};
+
+template <bool CPLX, int MODEL>
+void (*pick_orows(int ppt))(ORowArgs) {
+  switch (ppt) {
+    case 1: return k_orows<CPLX, MODEL, 1>;
+    case 2: return k_orows<CPLX, MODEL, 2>;
+    case 4: return k_orows<CPLX, MODEL, 4>;
+    default: return k_orows<CPLX, MODEL, 8>;
+  }
+}
+
+int make_oplan(int64_t ld_u, bool cplx, int model, OPlan& p) {
+  DevInfo d;
+  IRL_TRY(dev_info(d));
+  for (int C = 1; C <= 4096; C *= 2) {
+    if (ld_u % C) continue;
+    const int64_t W = ld_u / C;
+    for (int ppt : {1, 2, 4, 8}) {
+      int64_t nt = rup(cdiv(W, ppt), 32);
+      if (nt > 512) continue;
+      if (nt < 32) nt = 32;
+      p.C = C;
+      p.W = (int)W;
+      p.PPT = ppt;
+      p.NT = (int)nt;
+      if (cplx)
+        p.fn = pick_orows<true, MODEL_RBM>(ppt);
+      else
+        p.fn = model == MODEL_RBM ? pick_orows<false, MODEL_RBM>(ppt) : pick_orows<false, MODEL_MLP>(ppt);
+      int occ = 0;
+      IRL_TRY(cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)p.fn, p.NT, 0), "occ"));
+      occ = std::max(occ, 1);
+      p.nb = std::max(1, (d.sms * occ) / C);
+      return IRL_OK;
+    }
+  }
+  return fail(IRL_ERR_DEVICE, "no O-build geometry");
+}
+
+size_t obuild_bytes(const OPlan& p, int model, int64_t n, int hidden, int64_t ld_u, bool cplx) {
+  const size_t sS = cplx ? 16 : 8;
+  size_t b = align256((size_t)n * hidden * sS);                    // t
+  if (model == MODEL_MLP) b += align256((size_t)n * hidden * 8);    // g
+  b += 2 * align256((size_t)p.nb * ld_u * 16);                     // partials
+  return b;
+}
+
+template <bool CPLX, int MODEL>
+int launch_hidden(const uint8_t* x, int64_t n, int n_vis, int hidden, const void* Wm, const void* bvec,
+                  const double* uvec, void* T, double* G, cudaStream_t st) {
+  using S = typename Traits<CPLX>::S;
+  DevInfo d;
+  IRL_TRY(dev_info(d));
+  const size_t smem = (size_t)n_vis * 32 * sizeof(S);
+  if (smem > (size_t)d.smem_optin) return fail(IRL_ERR_ARG, "n_vis too large");
+  auto fn = k_hidden<CPLX, MODEL>;
+  IRL_TRY(ensure_fn_attrs((const void*)fn, d.smem_optin));
+  const int jt = (int)cdiv(hidden, 32);
+  int64_t rb = std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 8), cdiv((int64_t)d.sms * 8, jt)));
+  dim3 grid((unsigned)rb, (unsigned)jt);
+  fn<<<grid, 256, smem, st>>>(x, n, n_vis, hidden, (const S*)Wm, (const S*)bvec, uvec, (S*)T, G);
+  return cuda_check(cudaGetLastError(), "hidden kernel launch");
+}
+
+int obuild_impl(bool cplx, int model, const uint8_t* x, int64_t n, int n_vis, int hidden, const double* theta,
+                double* O, int64_t ld, const double* w, const double* coeff, double* obar, double* g, void* ws,
+                size_t ws_bytes, cudaStream_t st) {
+  if (!x || !theta || !O || !w || !coeff || !obar || !g) return fail(IRL_ERR_ARG, "null pointer");
+  if (n < 1 || n_vis < 1 || hidden < 1 || n_vis > 4095 || hidden > 65535) return fail(IRL_ERR_ARG, "bad shape");
+  const int64_t P = model == MODEL_RBM ? (int64_t)n_vis + hidden + (int64_t)hidden * n_vis
+                                       : (int64_t)hidden * n_vis + 2 * (int64_t)hidden + 1;
+  if (ld != irl_padded_ld(P, cplx)) return fail(IRL_ERR_ALIGN, "ld must equal irl_padded_ld(P=%lld)", (long long)P);
+  if (!aligned16(O) || !aligned16(obar) || !aligned16(g) || !aligned16(ws)) return fail(IRL_ERR_ALIGN, "alignment");
+  const int64_t ld_u = cplx ? ld : ld / 2;
+  OPlan p;
+  IRL_TRY(make_oplan(ld_u, cplx, model, p));
+  const size_t need = obuild_bytes(p, model, n, hidden, ld_u, cplx);
+  if (ws_bytes < need) return fail(IRL_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, need);
+  const size_t sS = cplx ? 16 : 8;
+  char* base = static_cast<char*>(ws);
+  void* T = base;
+  size_t off = align256((size_t)n * hidden * sS);
+  double* G = nullptr;
+  if (model == MODEL_MLP) {
+    G = reinterpret_cast<double*>(base + off);
+    off += align256((size_t)n * hidden * 8);
+  }
+  double2* part0 = reinterpret_cast<double2*>(base + off);
+  off += align256((size_t)p.nb * ld_u * 16);
+  double2* part1 = reinterpret_cast<double2*>(base + off);
+  if (model == MODEL_RBM) {
+    const double* bvec = theta + (size_t)n_vis * (cplx ? 2 : 1);
+    const double* Wm = theta + (size_t)(n_vis + hidden) * (cplx ? 2 : 1);
+    if (cplx)
+      IRL_TRY((launch_hidden<true, MODEL_RBM>(x, n, n_vis, hidden, Wm, bvec, nullptr, T, nullptr, st)));
+    else
+      IRL_TRY((launch_hidden<false, MODEL_RBM>(x, n, n_vis, hidden, Wm, bvec, nullptr, T, nullptr, st)));
+  } else {
+    const double* Wm = theta;
+    const double* bvec = theta + (size_t)hidden * n_vis;
+    const double* uvec = bvec + hidden;
+    IRL_TRY((launch_hidden<false, MODEL_MLP>(x, n, n_vis, hidden, Wm, bvec, uvec, T, G, st)));
+  }
+  ORowArgs a{};
+  a.x = x;
+  a.n_rows = n;
+  a.n_vis = n_vis;
+  a.hidden = hidden;
+  a.p = P;
+  a.T = T;
+  a.G = G;
+  a.O = reinterpret_cast<double2*>(O);
+  a.ld_u = ld_u;
+  a.w = w;
+  a.coeff = coeff;
+  a.part0 = part0;
+  a.part1 = part1;
+  a.W = p.W;
+  a.C = p.C;
+  a.nb = p.nb;
+  p.fn<<<(unsigned)(p.nb * p.C), p.NT, 0, st>>>(a);
+  IRL_TRY(cuda_check(cudaGetLastError(), "orows launch"));
+  const int64_t blocks = std::min<int64_t>(cdiv(ld_u, 256), 4096);
+  if (cplx)
+    k_finish_stats<true><<<(unsigned)blocks, 256, 0, st>>>(part0, part1, p.nb, ld_u, (double2*)obar, (double2*)g);
+  else
+    k_finish_stats<false><<<(unsigned)blocks, 256, 0, st>>>(part0, part1, p.nb, ld_u, (double2*)obar, (double2*)g);
+  return cuda_check(cudaGetLastError(), "obuild finish launch");
+}
+
+}  // namespace
+
+// =================================================================== ABI ==
+extern "C" {
+
+int irl_version(void) { return 100; }
+
+const char* irl_last_error(void) { return g_err.c_str(); }
+
+int64_t irl_padded_ld(int64_t p, int is_complex) {
+  if (p < 1) return 0;
+  const int64_t E = is_complex ? 1 : 2;
+  const int64_t units = cdiv(p, E);
+  const int64_t A = units < 32768 ? 16 : 64;
+  return rup(units, A) * E;
+}
+
+int irl_energy_f64(const double* w, const double* e, int64_t n, double* stats3, double* coeff, void* stream) {
+  if (!w || !e || !stats3 || !coeff || n < 1) return fail(IRL_ERR_ARG, "bad energy arguments");
+  DevInfo d;
+  IRL_TRY(dev_info(d));
+  k_energy<false><<<1, 1024, 0, (cudaStream_t)stream>>>(w, e, n, 0, stats3, coeff);
+  return cuda_check(cudaGetLastError(), "energy launch");
+}
+
+int irl_energy_c128(const double* w, const double* e, int64_t n, int hermitian, double* stats3, double* coeff,
+                    void* stream) {
+  if (!w || !e || !stats3 || !coeff || n < 1) return fail(IRL_ERR_ARG, "bad energy arguments");
+  DevInfo d;
+  IRL_TRY(dev_info(d));
+  k_energy<true><<<1, 1024, 0, (cudaStream_t)stream>>>(w, e, n, hermitian, stats3, coeff);
+  return cuda_check(cudaGetLastError(), "energy launch");
+}
+
+size_t irl_colstats_workspace_bytes(int64_t n, int64_t ld, int is_complex) {
+  const int64_t ld_u = is_complex ? ld : ld / 2;
+  Plan p;
+  if (make_plan(n, ld_u, is_complex != 0, MODE_STATS, p) != IRL_OK) return 0;
+  return colstats_bytes(p, ld_u);
+}
+
+int irl_colstats_f64(const double* O, int64_t n, int64_t ld, const double* w, const double* coeff, double* obar,
+                     double* g, void* ws, size_t ws_bytes, void* stream) {
+  return colstats_impl(false, O, n, ld, w, coeff, obar, g, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int irl_colstats_c128(const double* O, int64_t n, int64_t ld, const double* w, const double* coeff, double* obar,
+                      double* g, void* ws, size_t ws_bytes, void* stream) {
+  return colstats_impl(true, O, n, ld, w, coeff, obar, g, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+size_t irl_obuild_workspace_bytes(int model, int64_t n, int n_vis, int hidden, int64_t ld, int is_complex) {
+  const int64_t ld_u = is_complex ? ld : ld / 2;
+  OPlan p;
+  if (make_oplan(ld_u, is_complex != 0, model, p) != IRL_OK) return 0;
+  (void)n_vis;
+  return obuild_bytes(p, model, n, hidden, ld_u, is_complex != 0);
+}
+
+int irl_obuild_rbm_f64(const uint8_t* x, int64_t n, int n_vis, int hidden, const double* theta, double* O,
+                       int64_t ld, const double* w, const double* coeff, double* obar, double* g, void* ws,
+                       size_t ws_bytes, void* stream) {
+  return obuild_impl(false, MODEL_RBM, x, n, n_vis, hidden, theta, O, ld, w, coeff, obar, g, ws, ws_bytes,
+                     (cudaStream_t)stream);
+}
+
+int irl_obuild_rbm_c128(const uint8_t* x, int64_t n, int n_vis, int hidden, const double* theta, double* O,
+                        int64_t ld, const double* w, const double* coeff, double* obar, double* g, void* ws,
+                        size_t ws_bytes, void* stream) {
+  return obuild_impl(true, MODEL_RBM, x, n, n_vis, hidden, theta, O, ld, w, coeff, obar, g, ws, ws_bytes,
+                     (cudaStream_t)stream);
+}
+
+int irl_obuild_mlp_f64(const uint8_t* x, int64_t n, int n_in, int hidden, const double* theta, double* O,
+                       int64_t ld, const double* w, const double* coeff, double* obar, double* g, void* ws,
+                       size_t ws_bytes, void* stream) {
+  return obuild_impl(false, MODEL_MLP, x, n, n_in, hidden, theta, O, ld, w, coeff, obar, g, ws, ws_bytes,
+                     (cudaStream_t)stream);
+}
+
+int irl_hidden_rbm_f64(const uint8_t* x, int64_t n, int n_vis, int hidden, const double* theta, double* t,
+                       void* stream) {
+  if (!x || !theta || !t || n < 1 || n_vis < 1 || hidden < 1) return fail(IRL_ERR_ARG, "bad hidden arguments");
+  return launch_hidden<false, MODEL_RBM>(x, n, n_vis, hidden, theta + n_vis + hidden, theta + n_vis, nullptr, t,
+                                         nullptr, (cudaStream_t)stream);
+}
+
+int irl_hidden_rbm_c128(const uint8_t* x, int64_t n, int n_vis, int hidden, const double* theta, double* t,
+                        void* stream) {
+  if (!x || !theta || !t || n < 1 || n_vis < 1 || hidden < 1) return fail(IRL_ERR_ARG, "bad hidden arguments");
+  return launch_hidden<true, MODEL_RBM>(x, n, n_vis, hidden, theta + 2 * (n_vis + hidden), theta + 2 * n_vis,
+                                        nullptr, t, nullptr, (cudaStream_t)stream);
+}
+
+int irl_hidden_mlp_f64(const uint8_t* x, int64_t n, int n_in, int hidden, const double* theta, double* t,
+                       double* g, void* stream) {
+  if (!x || !theta || !t || !g || n < 1 || n_in < 1 || hidden < 1) return fail(IRL_ERR_ARG, "bad hidden arguments");
+  const double* bvec = theta + (size_t)hidden * n_in;
+  return launch_hidden<false, MODEL_MLP>(x, n, n_in, hidden, theta, bvec, bvec + hidden, t, g,
+                                         (cudaStream_t)stream);
+}
+
+size_t irl_mvp_workspace_bytes(int64_t n, int64_t ld, int is_complex) { return mvp_ws_bytes(n, ld, is_complex != 0); }
+
+int irl_mvp_f64(const double* O, int64_t n, int64_t p, int64_t ld, const double* obar, const double* coeff,
+                const double* v, double* out, const double* half_f, const double* u0, double* out0, int mode,
+                void* ws, size_t ws_bytes, void* stream) {
+  return mvp_impl(false, O, n, p, ld, obar, coeff, v, nullptr, out, nullptr, half_f, nullptr, u0, out0, mode, ws,
+                  ws_bytes, (cudaStream_t)stream);
+}
+
+int irl_mvp_c128(const double* O, int64_t n, int64_t p, int64_t ld, const double* obar, const double* coeff,
+                 const double* v_re, const double* v_im, double* out_re, double* out_im, const double* hf_re,
+                 const double* hf_im, const double* u0, double* out0, int mode, void* ws, size_t ws_bytes,
+                 void* stream) {
+  return mvp_impl(true, O, n, p, ld, obar, coeff, v_re, v_im, out_re, out_im, hf_re, hf_im, u0, out0, mode, ws,
+                  ws_bytes, (cudaStream_t)stream);
+}
+
+int irl_mvp_plan(int64_t n, int64_t ld, int is_complex, int mode, int* out_path, int* out_geom7) {
+  if (!out_path || !out_geom7) return fail(IRL_ERR_ARG, "null output");
+  const int64_t ld_u = is_complex ? ld : ld / 2;
+  Plan p;
+  int path = IRL_MVP_TWO_PASS;
+  if (mode == IRL_MVP_AUTO || mode == IRL_MVP_FUSED) {
+    if (make_plan(n, ld_u, is_complex != 0, MODE_FUSED, p) == IRL_OK) {
+      path = IRL_MVP_FUSED;
+    } else if (mode == IRL_MVP_FUSED) {
+      return IRL_ERR_DEVICE;
+    }
+  }
+  if (path == IRL_MVP_TWO_PASS) IRL_TRY(make_plan(n, ld_u, is_complex != 0, MODE_DOT, p));
+  *out_path = path;
+  int g[7] = {p.C, p.W, p.NT, p.R, p.NS, p.nb, p.PPT};
+  memcpy(out_geom7, g, sizeof(g));
+  return IRL_OK;
+}
+
+}  // extern "C"

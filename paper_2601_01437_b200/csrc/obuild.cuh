@@ -1,0 +1,303 @@
+// O-row producers (K1 RBM f64/c128, K2 MLP f64) and the energy statistics.
+//
+// Replaces the per-sample `ans.log_derivative` loop inside `build_batch`
+// (est:112-126 -> ans:249-290) with two launches over all N_s rows:
+//   k_hidden : pre-activation  b + W x_n  for every row (x is 0/1, so this is
+//              a gather-sum over the occupied inputs, summed in ascending
+//              input order), then tanh (and g = u (1 - t^2) for the MLP).
+//   k_orows  : writes the rows  O_n  (row-major, padded ld) with streaming
+//              16-B stores and, in the same pass, accumulates the column
+//              statistics  sum w conj(O)  and  sum c conj(O)  that give
+//              Obar (est:167) and the gradient F (est:156-163).
+//
+// Parameter layout:
+//   RBM : [a (n), b (h), W (h x n) row-major, index j*n + i]
+//   MLP : [W (h x n_in) row-major, b (h), u (h), c (1)]   (mirrors _Weights, ans:67-83)
+#pragma once
+#include "common.cuh"
+
+namespace irl {
+
+enum { MODEL_RBM = 0, MODEL_MLP = 1 };
+
+// complex tanh: (sinh 2a + i sin 2b) / (cosh 2a + cos 2b)
+__device__ __forceinline__ double2 ctanh(double2 z) {
+  const double d = cosh(2.0 * z.x) + cos(2.0 * z.y);
+  return make_double2(sinh(2.0 * z.x) / d, sin(2.0 * z.y) / d);
+}
+
+// pre[n][j] = b_j + sum_{i : x[n][i] = 1} W[j][i]  ->  T = tanh(pre), G = u (1 - T^2)
+template <bool CPLX, int MODEL>
+__global__ void __launch_bounds__(256) k_hidden(const uint8_t* __restrict__ x, int64_t n_rows, int n_vis, int hidden,
+                                                const typename Traits<CPLX>::S* __restrict__ Wm,
+                                                const typename Traits<CPLX>::S* __restrict__ bvec,
+                                                const double* __restrict__ uvec, typename Traits<CPLX>::S* Tout,
+                                                double* Gout) {
+  using S = typename Traits<CPLX>::S;
+  extern __shared__ __align__(16) unsigned char smem_h[];
+  S* Wt = reinterpret_cast<S*>(smem_h);  // [n_vis][32]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int j0 = blockIdx.y * 32;
+  const int j = j0 + lane;
+  const bool jok = j < hidden;
+  for (int e = threadIdx.x; e < n_vis * 32; e += blockDim.x) {
+    const int i = e / 32, jj = e % 32;
+    S val;
+    if constexpr (CPLX) val = make_double2(0.0, 0.0); else val = 0.0;
+    if (j0 + jj < hidden) val = Wm[(int64_t)(j0 + jj) * n_vis + i];
+    Wt[i * 32 + jj] = val;
+  }
+  __syncthreads();
+  S bj;
+  if constexpr (CPLX) bj = make_double2(0.0, 0.0); else bj = 0.0;
+  double uj = 0.0;
+  if (jok) {
+    bj = bvec[j];
+    if (MODEL == MODEL_MLP) uj = uvec[j];
+  }
+  const int64_t rows_per_blk = (n_rows + gridDim.x - 1) / gridDim.x;
+  const int64_t r_lo = blockIdx.x * rows_per_blk;
+  const int64_t r_hi = min(n_rows, r_lo + rows_per_blk);
+  for (int64_t n = r_lo + warp; n < r_hi; n += 8) {
+    S acc = bj;
+    const uint8_t* xr = x + n * n_vis;
+    for (int i0 = 0; i0 < n_vis; i0 += 32) {
+      const bool on = (i0 + lane < n_vis) && xr[i0 + lane] != 0;
+      uint32_t bits = __ballot_sync(0xffffffffu, on);
+      while (bits) {
+        const int b = __ffs(bits) - 1;
+        bits &= bits - 1;
+        const S wv = Wt[(i0 + b) * 32 + lane];
+        if constexpr (CPLX) {
+          acc.x += wv.x;
+          acc.y += wv.y;
+        } else {
+          acc += wv;
+        }
+      }
+    }
+    if (jok) {
+      if constexpr (CPLX) {
+        Tout[n * hidden + j] = ctanh(acc);
+      } else {
+        const double t = tanh(acc);
+        Tout[n * hidden + j] = t;
+        if (MODEL == MODEL_MLP) Gout[n * hidden + j] = uj * (1.0 - t * t);
+      }
+    }
+  }
+}
+
+struct ORowArgs {
+  const uint8_t* x;
+  int64_t n_rows;
+  int n_vis;
+  int hidden;
+  int64_t p;  // true parameter count
+  const void* T;   // S[N][hidden]
+  const double* G; // MLP only
+  double2* O;
+  int64_t ld_u;
+  const double* w;
+  const void* coeff;  // S[N] : w (e - E)
+  double2* part0;     // [nb][ld_u]  sum w conj(O)
+  double2* part1;     // [nb][ld_u]  sum c conj(O)
+  int W, C, nb;
+};
+
+// element descriptor: kind<<28 | j<<12 | i
+enum { EK_PAD = 0, EK_X = 1, EK_T = 2, EK_TX = 3, EK_GX = 4, EK_G = 5, EK_ONE = 6 };
+
+template <int MODEL>
+__device__ __forceinline__ uint32_t elem_desc(int64_t p, int n, int h, int64_t P) {
+  if (p >= P) return 0u;
+  uint32_t kind, j = 0, i = 0;
+  if constexpr (MODEL == MODEL_RBM) {
+    if (p < n) {
+      kind = EK_X;
+      i = (uint32_t)p;
+    } else if (p < n + h) {
+      kind = EK_T;
+      j = (uint32_t)(p - n);
+    } else {
+      const int64_t q = p - n - h;
+      kind = EK_TX;
+      j = (uint32_t)(q / n);
+      i = (uint32_t)(q % n);
+    }
+  } else {
+    const int64_t hn = (int64_t)h * n;
+    if (p < hn) {
+      kind = EK_GX;
+      j = (uint32_t)(p / n);
+      i = (uint32_t)(p % n);
+    } else if (p < hn + h) {
+      kind = EK_G;
+      j = (uint32_t)(p - hn);
+    } else if (p < hn + 2 * h) {
+      kind = EK_T;
+      j = (uint32_t)(p - hn - h);
+    } else {
+      kind = EK_ONE;
+    }
+  }
+  return (kind << 28) | (j << 12) | i;
+}
+
+template <bool CPLX>
+__device__ __forceinline__ typename Traits<CPLX>::S elem_value(uint32_t d, const uint8_t* xr,
+                                                               const typename Traits<CPLX>::S* Tr,
+                                                               const double* Gr) {
+  using S = typename Traits<CPLX>::S;
+  const uint32_t kind = d >> 28, j = (d >> 12) & 0xffffu, i = d & 0xfffu;
+  double xv = 0.0;
+  if (kind == EK_X || kind == EK_TX || kind == EK_GX) xv = xr[i] ? 1.0 : 0.0;
+  if constexpr (CPLX) {
+    S t = (kind == EK_T || kind == EK_TX) ? Tr[j] : make_double2(0.0, 0.0);
+    switch (kind) {
+      case EK_X: return make_double2(xv, 0.0);
+      case EK_T: return t;
+      case EK_TX: return make_double2(t.x * xv, t.y * xv);
+      default: return make_double2(0.0, 0.0);
+    }
+  } else {
+    switch (kind) {
+      case EK_X: return xv;
+      case EK_T: return Tr[j];
+      case EK_TX: return Tr[j] * xv;
+      case EK_GX: return Gr[j] * xv;
+      case EK_G: return Gr[j];
+      case EK_ONE: return 1.0;
+      default: return 0.0;
+    }
+  }
+}
+
+template <bool CPLX, int MODEL, int PPT>
+__global__ void __launch_bounds__(512) k_orows(const ORowArgs a) {
+  using T = Traits<CPLX>;
+  using S = typename T::S;
+  const int NT = blockDim.x;
+  const int tid = threadIdx.x;
+  const int rank = blockIdx.x % a.C, blk = blockIdx.x / a.C;
+  const int64_t lo = (a.n_rows * blk) / a.nb, hi = (a.n_rows * (blk + 1)) / a.nb;
+  const int64_t col0 = (int64_t)rank * a.W;
+  constexpr int E = Traits<CPLX>::kElemsPerUnit;
+
+  uint32_t desc[PPT][E];
+  double2 acc0[PPT], acc1[PPT];
+#pragma unroll
+  for (int k = 0; k < PPT; ++k) {
+    const int idx = tid + k * NT;
+    const int64_t u = col0 + idx;
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+      desc[k][e] = (idx < a.W) ? elem_desc<MODEL>(u * E + e, a.n_vis, a.hidden, a.p) : 0u;
+    acc0[k] = make_double2(0.0, 0.0);
+    acc1[k] = make_double2(0.0, 0.0);
+  }
+  const S* Tm = reinterpret_cast<const S*>(a.T);
+  const S* cf = reinterpret_cast<const S*>(a.coeff);
+  for (int64_t n = lo; n < hi; ++n) {
+    const uint8_t* xr = a.x + n * a.n_vis;
+    const S* Tr = Tm + n * a.hidden;
+    const double* Gr = (MODEL == MODEL_MLP) ? a.G + n * a.hidden : nullptr;
+    const double wn = __ldg(a.w + n);
+    const S cn = cf[n];
+    double2* orow = a.O + n * a.ld_u + col0;
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) {
+      const int idx = tid + k * NT;
+      if (idx < a.W) {
+        double2 u;
+        if constexpr (CPLX) {
+          u = elem_value<true>(desc[k][0], xr, Tr, Gr);
+          // acc0 += w conj(O) ; acc1 += conj(O) c
+          acc0[k].x = fma(wn, u.x, acc0[k].x);
+          acc0[k].y = fma(-wn, u.y, acc0[k].y);
+          T::axpy(acc1[k], u, cn);
+        } else {
+          u.x = elem_value<false>(desc[k][0], xr, Tr, Gr);
+          u.y = elem_value<false>(desc[k][1], xr, Tr, Gr);
+          acc0[k].x = fma(wn, u.x, acc0[k].x);
+          acc0[k].y = fma(wn, u.y, acc0[k].y);
+          acc1[k].x = fma(cn, u.x, acc1[k].x);
+          acc1[k].y = fma(cn, u.y, acc1[k].y);
+        }
+        st_stream(orow + idx, u);
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < PPT; ++k) {
+    const int idx = tid + k * NT;
+    if (idx < a.W) {
+      a.part0[(int64_t)blk * a.ld_u + col0 + idx] = acc0[k];
+      a.part1[(int64_t)blk * a.ld_u + col0 + idx] = acc1[k];
+    }
+  }
+}
+
+// Energy statistics (est:146-153) and the H_eff coefficient c_n = w_n (e_n - E)
+// (est:166-168, est:186).  One CTA, fixed-order tree: deterministic.
+//   stats[0] = E = Re sum w e ; stats[1] = Im sum w e ; stats[2] = sum w |e - E|^2
+// hermitian (complex only): c_n = w_n Re(e_n - E)
+template <bool CPLX>
+__global__ void __launch_bounds__(1024) k_energy(const double* __restrict__ w, const void* e_, int64_t n,
+                                                 int hermitian, double* stats, void* coeff_) {
+  using T = Traits<CPLX>;
+  using S = typename T::S;
+  const S* e = reinterpret_cast<const S*>(e_);
+  S* coeff = reinterpret_cast<S*>(coeff_);
+  __shared__ S sh[32];
+  __shared__ double shd[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  S acc = T::zero();
+  for (int64_t i = tid; i < n; i += blockDim.x) {
+    const S ei = e[i];
+    if constexpr (CPLX) {
+      acc.x = fma(w[i], ei.x, acc.x);
+      acc.y = fma(w[i], ei.y, acc.y);
+    } else {
+      acc = fma(w[i], ei, acc);
+    }
+  }
+  acc = warp_sum<CPLX>(acc);
+  if (lane == 0) sh[warp] = acc;
+  __syncthreads();
+  S tot = T::zero();
+  for (int k = 0; k < nw; ++k) tot = T::add(tot, sh[k]);
+  double E, Ei;
+  if constexpr (CPLX) {
+    E = tot.x;
+    Ei = tot.y;
+  } else {
+    E = tot;
+    Ei = 0.0;
+  }
+  double v = 0.0;
+  for (int64_t i = tid; i < n; i += blockDim.x) {
+    const S ei = e[i];
+    if constexpr (CPLX) {
+      const double dr = ei.x - E, di = ei.y;
+      v = fma(w[i], dr * dr + di * di, v);
+      coeff[i] = hermitian ? make_double2(w[i] * dr, 0.0) : make_double2(w[i] * dr, w[i] * di);
+    } else {
+      const double d = ei - E;
+      v = fma(w[i], d * d, v);
+      coeff[i] = w[i] * d;
+    }
+  }
+  v = warp_sum<false>(v);
+  if (lane == 0) shd[warp] = v;
+  __syncthreads();
+  if (tid == 0) {
+    double var = 0.0;
+    for (int k = 0; k < nw; ++k) var += shd[k];
+    stats[0] = E;
+    stats[1] = Ei;
+    stats[2] = var;
+  }
+}
+
+}  // namespace irl

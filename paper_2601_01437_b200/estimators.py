@@ -1,0 +1,375 @@
+"""Device-resident VMC estimators: the drop-in for ``irlnqs.estimators``.
+
+Mirrors the reference entry points on the hot path:
+
+* :class:`SampleBatch` — ``estimators.py:30-61`` (same constructor and
+  validation: shapes, ``w >= 0``, ``sum w = 1 +- 1e-12``), but the caches
+  live in HBM: ``o_matrix`` is an N x ld row-major device tensor with a
+  padded leading dimension (``irl_padded_ld``), padding columns zero.
+* :func:`estimate_energy`   — ``estimators.py:146-153``  (k_energy)
+* :func:`energy_gradient`   — ``estimators.py:156-163``  (fused column stats)
+* :func:`heff_matvec`       — ``estimators.py:171-186``  (single-pass fused MVP)
+* :func:`qgt_matvec`        — matrix-free form of ``dense_qgt`` (``:335-344``)
+* :func:`dense_heff`, :func:`dense_qgt`, :class:`DensePCapError` — ``:319-344``
+
+Three parameter/O conventions are supported:
+
+* ``real``         real theta, real O (RBM/MLP f64 configs);
+* ``complex_raw``  real theta, complex O and E_loc — the reference's own
+  autoregressive ansatz; products are ``Re(O_c^H (w e_c (O_c v)))`` with real v,
+  exactly ``est.heff_matvec``;
+* ``hermitian``    complex theta, holomorphic complex O (cfg4): products are
+  the Hermitian ``O_c^H (w Re(e_c) (O_c v))`` on complex v.
+
+The arithmetic runs only in the sm_100a kernels of ``libirlsr.so``; torch is
+used for device memory and streams.  Without the library or a GPU every call
+raises :class:`~paper_2601_01437_b200._lib.NativeUnavailable`.
+"""
+
+from __future__ import annotations
+
+import warnings
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+
+DEFAULT_DENSE_P_CAP = 200  # est:22
+IMAG_RESIDUAL_WARN = 1e-8  # est:23
+
+KIND_REAL = "real"
+KIND_COMPLEX_RAW = "complex_raw"
+KIND_HERMITIAN = "hermitian"
+
+
+class DensePCapError(Exception):
+    """Parameter count too large for the dense p x p oracles (est:26-27)."""
+
+
+@dataclass(frozen=True)
+class EnergyEstimate:
+    """est:64-68."""
+
+    mean: float
+    variance: float
+    std_error: float
+
+
+def _device(dev=None) -> torch.device:
+    if dev is not None:
+        return torch.device(dev)
+    if not torch.cuda.is_available():
+        raise _lib.NativeUnavailable("no CUDA device: the IRL-SR hot path runs only on sm_100a")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _as_tensor(x, dtype, device) -> torch.Tensor:
+    if isinstance(x, torch.Tensor):
+        return x.to(device=device, dtype=dtype)
+    return torch.as_tensor(np.asarray(x), dtype=dtype, device=device)
+
+
+class SampleBatch:
+    """Configurations with weights and device-resident E_loc / O caches (est:30-61).
+
+    ``o_matrix`` may be a host array (N, P) — it is uploaded once into the
+    padded device layout — or an already padded device tensor (N, ld).
+    ``kind`` selects the parameter convention (see module docstring); by
+    default real O -> ``real`` and complex O -> ``complex_raw``.
+    """
+
+    def __init__(self, configs, weights, e_loc, o_matrix, n_samples: int = 0, *, kind: str | None = None,
+                 param_count: int | None = None, device=None):
+        dev = _device(device if device is not None else (o_matrix.device if isinstance(o_matrix, torch.Tensor) and o_matrix.is_cuda else None))
+        is_complex = torch.is_complex(o_matrix) if isinstance(o_matrix, torch.Tensor) else np.iscomplexobj(o_matrix)
+        if kind is None:
+            kind = KIND_COMPLEX_RAW if is_complex else KIND_REAL
+        if kind not in (KIND_REAL, KIND_COMPLEX_RAW, KIND_HERMITIAN):
+            raise ValueError(f"unknown batch kind {kind!r}")
+        if kind == KIND_REAL and is_complex:
+            raise ValueError("complex o_matrix needs kind 'complex_raw' or 'hermitian'")
+        cdt = torch.complex128 if kind != KIND_REAL else torch.float64
+        n = len(configs) if configs is not None else int(np.shape(weights)[0])
+        w = _as_tensor(weights, torch.float64, dev).contiguous()
+        e_is_c = torch.is_complex(e_loc) if isinstance(e_loc, torch.Tensor) else np.iscomplexobj(e_loc)
+        if kind == KIND_REAL and e_is_c:
+            raise ValueError("complex e_loc needs a complex batch kind")
+        e = _as_tensor(e_loc, cdt, dev).contiguous()
+        if tuple(w.shape) != (n,) or tuple(e.shape) != (n,):
+            raise ValueError("cache shapes do not match the config list")
+        if o_matrix.shape[0] != n:
+            raise ValueError("o_matrix rows do not match the config list")
+        p = int(param_count) if param_count is not None else int(o_matrix.shape[1])
+        ld = _lib.padded_ld(p, kind != KIND_REAL)
+        if isinstance(o_matrix, torch.Tensor) and o_matrix.is_cuda and o_matrix.shape[1] == ld:
+            o = o_matrix if o_matrix.dtype == cdt else o_matrix.to(cdt)
+            if not o.is_contiguous():
+                raise ValueError("device o_matrix must be contiguous")
+        else:
+            if o_matrix.shape[1] != p:
+                raise ValueError("o_matrix width does not match param_count")
+            o = torch.zeros((n, ld), dtype=cdt, device=dev)
+            o[:, :p] = _as_tensor(o_matrix, cdt, dev)
+        # est:50-51 validation (one host sync, once per batch)
+        wmin = float(w.min()) if n else 0.0
+        wsum = float(w.sum()) if n else 0.0
+        if n and (wmin < 0 or abs(wsum - 1.0) > 1e-12):
+            raise ValueError("weights must be nonnegative and sum to 1")
+        self.configs = tuple(configs) if configs is not None else None
+        self.weights = w
+        self.e_loc = e
+        self.o_matrix = o
+        self.n_samples = int(n_samples)
+        self.kind = kind
+        self._p = p
+        self.ld = ld
+        self.device = dev
+        self._coeff: dict = {}
+        self._colstats: dict = {}
+        self._ws: torch.Tensor | None = None
+        self._stats_e: float | None = None
+
+    # -- reference properties (est:55-61)
+    @property
+    def param_count(self) -> int:
+        return self._p
+
+    @property
+    def exact(self) -> bool:
+        return self.n_samples == 0
+
+    @property
+    def n_rows(self) -> int:
+        return int(self.weights.shape[0])
+
+    @property
+    def is_complex(self) -> bool:
+        return self.kind != KIND_REAL
+
+    # -- internals
+    def _stream(self) -> int:
+        return _lib.stream_handle(self.device)
+
+    def mvp_workspace(self) -> torch.Tensor:
+        if self._ws is None:
+            nbytes = int(_lib.lib().irl_mvp_workspace_bytes(self.n_rows, self.ld, int(self.is_complex)))
+            self._ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
+        return self._ws
+
+    def coefficients(self, mean: float) -> torch.Tensor:
+        """c_n = w_n (e_n - E): est:166-168 (Hermitian mode: w Re(e - E))."""
+        key = float(mean)
+        c = self._coeff.get(key)
+        if c is None:
+            c = self._energy_pass(key)[1]
+        return c
+
+    def _energy_pass(self, mean: float | None):
+        """Run k_energy; returns (stats3 host array, coeff for the batch's own E)."""
+        n = self.n_rows
+        stats = torch.empty(3, dtype=torch.float64, device=self.device)
+        coeff = torch.empty(n, dtype=self.e_loc.dtype, device=self.device)
+        if self.is_complex:
+            _lib.call("irl_energy_c128", _lib.ptr(self.weights), _lib.ptr(self.e_loc), n,
+                      int(self.kind == KIND_HERMITIAN), _lib.ptr(stats), _lib.ptr(coeff), self._stream())
+        else:
+            _lib.call("irl_energy_f64", _lib.ptr(self.weights), _lib.ptr(self.e_loc), n,
+                      _lib.ptr(stats), _lib.ptr(coeff), self._stream())
+        host = stats.cpu().numpy()
+        own = float(host[0])
+        self._coeff[own] = coeff
+        self._stats_e = own
+        if mean is not None and float(mean) != own:
+            # another energy reference (e.g. E = 0 for the S trick of SURVEY §8(c)):
+            # c = w (e - mean), formed on device
+            d = self.e_loc - float(mean)
+            if self.kind == KIND_HERMITIAN:
+                d = torch.complex(d.real, torch.zeros_like(d.real))
+            c = (self.weights * d).contiguous()
+            self._coeff[float(mean)] = c
+            return host, c
+        return host, coeff
+
+    def colstats(self, mean: float):
+        """(obar, g) with obar = w @ O and g = c @ conj(O), c = w (e - mean)."""
+        key = float(mean)
+        hit = self._colstats.get(key)
+        if hit is not None:
+            return hit
+        c = self.coefficients(key)
+        n = self.n_rows
+        obar = torch.empty(self.ld, dtype=self.o_matrix.dtype, device=self.device)
+        g = torch.empty(self.ld, dtype=self.o_matrix.dtype, device=self.device)
+        nbytes = int(_lib.lib().irl_colstats_workspace_bytes(n, self.ld, int(self.is_complex)))
+        ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
+        fn = "irl_colstats_c128" if self.is_complex else "irl_colstats_f64"
+        _lib.call(fn, _lib.ptr(self.o_matrix), n, self.ld, _lib.ptr(self.weights), _lib.ptr(c),
+                  _lib.ptr(obar), _lib.ptr(g), _lib.ptr(ws), ws.numel(), self._stream())
+        self._colstats[key] = (obar, g)
+        return obar, g
+
+    def _set_colstats(self, mean: float, obar: torch.Tensor, g: torch.Tensor, coeff: torch.Tensor) -> None:
+        self._coeff[float(mean)] = coeff
+        self._colstats[float(mean)] = (obar, g)
+
+    def obar(self) -> torch.Tensor:
+        if self._colstats:
+            return next(iter(self._colstats.values()))[0]
+        if self._stats_e is None:
+            self._energy_pass(None)
+        return self.colstats(self._stats_e)[0]
+
+
+def _check_imag(value: complex, what: str) -> float:
+    """est:136-143."""
+    if abs(value.imag) > IMAG_RESIDUAL_WARN * max(1.0, abs(value.real)):
+        warnings.warn(
+            f"{what} has imaginary residual {value.imag:.3e}; expected a real-symmetric problem",
+            stacklevel=3,
+        )
+    return value.real
+
+
+def estimate_energy(batch: SampleBatch) -> EnergyEstimate:
+    """est:146-153: E = Re sum w e, variance = sum w |e - E|^2, std error."""
+    if batch.n_rows == 0:
+        raise ValueError("empty batch")
+    host, _ = batch._energy_pass(None)
+    mean = _check_imag(complex(host[0], host[1]), "energy mean")
+    variance = float(host[2])
+    std_error = 0.0 if batch.exact else float(np.sqrt(variance / batch.n_samples))
+    return EnergyEstimate(mean=mean, variance=variance, std_error=std_error)
+
+
+def energy_gradient(batch: SampleBatch, energy: EnergyEstimate) -> torch.Tensor:
+    """est:156-163: F = 2 Re( (w e) @ conj(O) - E (w @ conj(O)) ), device tensor (P,).
+
+    Computed as 2 Re sum w (e - E) conj(O) (same value, no
+    cancellation).  Hermitian batches return the complex 2 g, whose real and
+    imaginary parts are the reference's real-embedding gradient halves.
+    """
+    if batch.n_rows == 0:
+        raise ValueError("empty batch")
+    _, g = batch.colstats(energy.mean)
+    g = g[: batch.param_count]
+    if batch.kind == KIND_HERMITIAN:
+        return 2.0 * g
+    return 2.0 * (g.real if batch.is_complex else g)
+
+
+def _apply(batch: SampleBatch, coeff: torch.Tensor, v: torch.Tensor, out: torch.Tensor, *,
+           mode: int = _lib.MVP_AUTO, half_f=None, u0=None, out0=None) -> None:
+    """Raw device product on padded vectors; no validation (driver fast path).
+
+    real/complex_raw: v, out, half_f are real padded vectors (ld,) (views OK).
+    hermitian: v, out, half_f are (re, im) tuples of real padded vectors.
+    """
+    obar = batch.obar()
+    stream = batch._stream()
+    ws = batch.mvp_workspace()
+    n = batch.n_rows
+    if not batch.is_complex:
+        _lib.call("irl_mvp_f64", _lib.ptr(batch.o_matrix), n, batch.param_count, batch.ld, _lib.ptr(obar),
+                  _lib.ptr(coeff), _lib.ptr(v), _lib.ptr(out), _lib.ptr(half_f), _lib.ptr(u0), _lib.ptr(out0),
+                  int(mode), _lib.ptr(ws), ws.numel(), stream)
+        return
+    if batch.kind == KIND_HERMITIAN:
+        v_re, v_im = v
+        o_re, o_im = out
+        h_re, h_im = half_f if half_f is not None else (None, None)
+    else:
+        v_re, v_im, o_re, o_im = v, None, out, None
+        h_re, h_im = half_f, None
+    _lib.call("irl_mvp_c128", _lib.ptr(batch.o_matrix), n, batch.param_count, batch.ld, _lib.ptr(obar),
+              _lib.ptr(coeff), _lib.ptr(v_re), _lib.ptr(v_im), _lib.ptr(o_re), _lib.ptr(o_im), _lib.ptr(h_re),
+              _lib.ptr(h_im), _lib.ptr(u0), _lib.ptr(out0), int(mode), _lib.ptr(ws), ws.numel(), stream)
+
+
+def _product(batch: SampleBatch, coeff: torch.Tensor, v, mode: int):
+    p = batch.param_count
+    as_numpy = not isinstance(v, torch.Tensor)
+    if as_numpy:
+        v_arr = np.asarray(v)
+        shape = v_arr.shape
+        finite = bool(np.all(np.isfinite(v_arr))) if shape == (p,) else True
+    else:
+        shape = tuple(v.shape)
+        finite = bool(torch.isfinite(v).all()) if shape == (p,) else True
+    if shape != (p,):  # est:178-181
+        raise ValueError(f"vector length {shape} does not match p={p}")
+    if not finite:  # est:182-183
+        raise ValueError("non-finite input vector")
+    dev = batch.device
+    ld = batch.ld
+    # host tensors (pinned for async copies) in -> host tensor out: the e2e path
+    on_host = (not as_numpy) and not v.is_cuda
+    if batch.kind == KIND_HERMITIAN:
+        vt = _as_tensor(v, torch.complex128, dev) if not on_host else v.to(torch.complex128).to(dev, non_blocking=True)
+        vin = torch.zeros((2, ld), dtype=torch.float64, device=dev)
+        vin[0, :p] = vt.real
+        vin[1, :p] = vt.imag
+        vout = torch.empty((2, ld), dtype=torch.float64, device=dev)
+        _apply(batch, coeff, (vin[0], vin[1]), (vout[0], vout[1]), mode=mode)
+        res = torch.complex(vout[0, :p], vout[1, :p])
+    else:
+        if (not as_numpy) and torch.is_complex(v):
+            raise ValueError("complex vector needs a hermitian batch")
+        vin = torch.zeros(ld, dtype=torch.float64, device=dev)
+        if on_host:
+            vin[:p].copy_(v, non_blocking=True)
+        else:
+            vin[:p] = _as_tensor(v, torch.float64, dev)
+        vout = torch.empty(ld, dtype=torch.float64, device=dev)
+        _apply(batch, coeff, vin, vout, mode=mode)
+        res = vout[:p]
+    if on_host:
+        dst = torch.empty(res.shape, dtype=res.dtype, pin_memory=v.is_pinned())
+        dst.copy_(res, non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+        return dst
+    return res.cpu().numpy() if as_numpy else res
+
+
+def heff_matvec(batch: SampleBatch, energy: EnergyEstimate, v, *, mode: int = _lib.MVP_AUTO):
+    """est:171-186: H_eff v = O_c^H (w e_c (O_c v)) without forming O_c or H_eff.
+
+    numpy in -> numpy out (reference behaviour); torch in -> torch out.
+    """
+    return _product(batch, batch.coefficients(energy.mean), v, mode)
+
+
+def qgt_matvec(batch: SampleBatch, v, *, mode: int = _lib.MVP_AUTO):
+    """S v = O_c^H (w (O_c v)) — matrix-free ``dense_qgt`` (est:335-344)."""
+    return _product(batch, batch.weights if not batch.is_complex else batch.weights.to(torch.complex128), v, mode)
+
+
+def _dense_from_products(batch: SampleBatch, coeff: torch.Tensor, cap: int) -> np.ndarray:
+    p = batch.param_count
+    if p > cap:
+        raise DensePCapError(f"p={p} above the dense cap of {cap}")
+    cols = []
+    for k in range(p):
+        e_k = np.zeros(p, dtype=complex if batch.kind == KIND_HERMITIAN else float)
+        e_k[k] = 1.0
+        cols.append(_product(batch, coeff, e_k, _lib.MVP_AUTO))
+    mat = np.stack(cols, axis=1)
+    if batch.kind != KIND_HERMITIAN:
+        mat = mat.real
+        asym = float(np.max(np.abs(mat - mat.T))) if p else 0.0
+        if asym > IMAG_RESIDUAL_WARN:
+            warnings.warn(f"dense H_eff asymmetric by {asym:.3e}", stacklevel=3)
+        return (mat + mat.T) / 2
+    return (mat + mat.conj().T) / 2
+
+
+def dense_heff(batch: SampleBatch, energy: EnergyEstimate, cap: int = DEFAULT_DENSE_P_CAP) -> np.ndarray:
+    """est:319-332, assembled column by column from the device product."""
+    return _dense_from_products(batch, batch.coefficients(energy.mean), cap)
+
+
+def dense_qgt(batch: SampleBatch, cap: int = DEFAULT_DENSE_P_CAP) -> np.ndarray:
+    """est:335-344, assembled column by column from the device product."""
+    coeff = batch.weights if not batch.is_complex else batch.weights.to(torch.complex128)
+    return _dense_from_products(batch, coeff, cap)

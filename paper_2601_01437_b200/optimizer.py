@@ -1,0 +1,176 @@
+"""IRL-SR outer-step core: bordered operator, IRL solve, update direction.
+
+The data-parallel part of ``irlnqs.optimizer.outer_step`` (``opt:130-165``):
+
+* the bordered (p+1) closure of ``opt:140-148``
+      A([u0; u]) = [ (F/2).u ; u0 F/2 + H_eff u ]
+  — here ONE fused device launch (+ finisher) per product: the F/2 row and
+  column are folded into the streaming kernel's prologue and epilogue;
+  ``heff_offdiag_matvec`` is absent for synthetic E_loc;
+* ``krylov.irl_smallest`` on it with the reference's seed rule
+  ``_batch_seed`` (``opt:100-101``);
+* the direction ``d = c[1:]/c0`` (``opt:160-165``).
+
+Line search, Adam and the run loop (``opt:167-269``) need the energy
+re-evaluated from a Hamiltonian and are out of scope.
+
+Complex-parameter (Hermitian, cfg4) batches use the reference's real
+embedding ``[u0, Re c, Im c]`` (dimension 2P+1), so the driver,
+start vector and matvec count are those of ``kry.irl_smallest`` on the
+embedded operator.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib, krylov
+from .estimators import (
+    KIND_HERMITIAN,
+    EnergyEstimate,
+    SampleBatch,
+    _apply,
+    energy_gradient,
+    estimate_energy,
+)
+
+
+@dataclass(frozen=True)
+class OptimizerConfig:
+    """Solver subset of ``opt:41-57`` (defaults identical)."""
+
+    method: str = "irl"  # irl | sl
+    m: int = 20
+    tol: float = 1e-12
+    max_restarts: int = 300
+    sl_budget: int = 100
+    seed: int = 111
+
+    def __post_init__(self):
+        if self.method not in ("irl", "sl"):
+            raise ValueError(f"unknown method {self.method!r}")
+
+
+def _batch_seed(config: OptimizerConfig, step: int) -> int:
+    """opt:100-101."""
+    return (config.seed * 1_000_003 + step) % 2**31
+
+
+class BorderedLayout:
+    """Physical device layout of the bordered vector.
+
+    real / complex_raw : logical [u0, u (P)]            -> [u0, 0, u, 0-pad]  length 2 + ld
+    hermitian          : logical [u0, Re c (P), Im c (P)] -> [u0, 0, Re c, pad, Im c, pad]  length 2 + 2 ld
+    The zero slot after u0 keeps the P-part 16-byte aligned for the kernels.
+    """
+
+    def __init__(self, batch: SampleBatch):
+        self.p = batch.param_count
+        self.ld = batch.ld
+        self.hermitian = batch.kind == KIND_HERMITIAN
+        self.device = batch.device
+        self.dim = 1 + (2 * self.p if self.hermitian else self.p)
+        self.length = 2 + (2 * self.ld if self.hermitian else self.ld)
+        idx = [0] + list(range(2, 2 + self.p))
+        if self.hermitian:
+            idx += list(range(2 + self.ld, 2 + self.ld + self.p))
+        self.index = torch.as_tensor(np.array(idx, dtype=np.int64), device=self.device)
+
+    def scatter(self, x: np.ndarray) -> torch.Tensor:
+        out = torch.zeros(self.length, dtype=torch.float64, device=self.device)
+        out[self.index] = torch.as_tensor(np.asarray(x, dtype=np.float64), device=self.device)
+        return out
+
+    def gather(self, v: torch.Tensor) -> torch.Tensor:
+        return v[self.index]
+
+    def parts(self, v: torch.Tensor):
+        """(u0 view (1,), u-part views) for the kernel ABI."""
+        u0 = v[0:1]
+        if self.hermitian:
+            return u0, (v[2 : 2 + self.ld], v[2 + self.ld : 2 + 2 * self.ld])
+        return u0, v[2 : 2 + self.ld]
+
+
+class BorderedOperator:
+    """opt:140-148 on the device: one fused streaming launch per product."""
+
+    def __init__(self, batch: SampleBatch, energy: EnergyEstimate, gradient: torch.Tensor | None = None,
+                 mode: int = _lib.MVP_AUTO):
+        self.batch = batch
+        self.energy = energy
+        self.layout = BorderedLayout(batch)
+        self.mode = mode
+        self.coeff = batch.coefficients(energy.mean)
+        if gradient is None:
+            gradient = energy_gradient(batch, energy)
+        self.gradient = gradient
+        ld, p = batch.ld, batch.param_count
+        if self.layout.hermitian:
+            half = torch.zeros((2, ld), dtype=torch.float64, device=batch.device)
+            half[0, :p] = 0.5 * gradient.real
+            half[1, :p] = 0.5 * gradient.imag
+            self.half_f = (half[0], half[1])
+            self._half = half
+        else:
+            half = torch.zeros(ld, dtype=torch.float64, device=batch.device)
+            half[:p] = 0.5 * gradient
+            self.half_f = half
+        self.count = 0
+
+    def __call__(self, u: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        if out is None:
+            out = torch.zeros(self.layout.length, dtype=torch.float64, device=u.device)
+        u0, uin = self.layout.parts(u)
+        out0, uout = self.layout.parts(out)
+        _apply(self.batch, self.coeff, uin, uout, mode=self.mode, half_f=self.half_f, u0=u0, out0=out0)
+        self.count += 1
+        return out
+
+
+@dataclass(frozen=True)
+class StepResult:
+    direction: torch.Tensor  # (P,) device; complex for hermitian batches
+    lambda_min: float
+    n_matvec: int
+    converged: bool
+    pair: krylov.RitzPair
+    energy: EnergyEstimate
+
+
+def direction_from_vector(vec: torch.Tensor, gradient: torch.Tensor, p: int, hermitian: bool) -> torch.Tensor:
+    """opt:160-165: d = c[1:] / c0, or the descent-oriented c[1:] when c0 ~ 0."""
+    c0 = float(vec[0])
+    if hermitian:
+        d = torch.complex(vec[1 : 1 + p], vec[1 + p : 1 + 2 * p])
+        slope = float((gradient.real * d.real + gradient.imag * d.imag).sum())
+    else:
+        d = vec[1:]
+        slope = None
+    if abs(c0) > 1e-12:
+        return d / c0
+    if slope is None:
+        slope = float(gradient @ d)
+    return -d if slope > 0 else d
+
+
+def solve_step(batch: SampleBatch, config: OptimizerConfig = OptimizerConfig(), step: int = 0, *,
+               energy: EnergyEstimate | None = None, mode: int = _lib.MVP_AUTO, seed: int | None = None) -> StepResult:
+    """The IRL-SR hot path of one outer step (opt:134-165) on a device batch."""
+    if energy is None:
+        energy = estimate_energy(batch)
+    gradient = energy_gradient(batch, energy)
+    op = BorderedOperator(batch, energy, gradient, mode=mode)
+    s = _batch_seed(config, step) if seed is None else seed
+    lay = op.layout
+    if config.method == "irl":
+        pair = krylov.irl_smallest(op, lay.dim, m=config.m, tol=config.tol, max_restarts=config.max_restarts,
+                                   seed=s, device=batch.device, layout=lay)
+    else:
+        pair = krylov.sl_smallest(op, lay.dim, budget=config.sl_budget, seed=s, device=batch.device, layout=lay)
+    d = direction_from_vector(pair.vector, gradient, batch.param_count, lay.hermitian)
+    return StepResult(direction=d, lambda_min=float(pair.value), n_matvec=pair.n_matvec,
+                      converged=pair.converged, pair=pair, energy=energy)

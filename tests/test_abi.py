@@ -1,0 +1,58 @@
+"""The C-ABI library loads and exports every symbol include/irl_sr.h declares (no GPU needed)."""
+
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+from paper_2601_01437_b200 import _lib
+
+
+def declared_symbols():
+    text = open(os.path.join(ROOT, "include", "irl_sr.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(irl_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_and_binding_agree():
+    assert declared_symbols() == sorted(_lib.SIGNATURES)
+
+
+def test_library_loads_and_exports_everything():
+    lib = _lib.load()
+    for name in declared_symbols():
+        assert hasattr(lib, name), name
+    assert lib.irl_version() >= 100
+
+
+@pytest.mark.parametrize(
+    "p,cplx,ld",
+    [(860, False, 864), (6600, False, 6624), (11265, False, 11296), (29340, True, 29344), (208897, False, 209024),
+     (1, False, 32), (1, True, 16)],
+)
+def test_padded_ld(p, cplx, ld):
+    assert _lib.padded_ld(p, cplx) == ld
+    assert ld >= p and (ld * (16 if cplx else 8)) % 256 == 0
+
+
+def test_no_cpu_fallback():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2601_01437_b200 import estimators
+
+    with pytest.raises(_lib.NativeUnavailable):
+        estimators.SampleBatch(None, np.full(4, 0.25), np.zeros(4), np.zeros((4, 3)), 4)
+    with pytest.raises(_lib.NativeUnavailable):
+        _lib.lib()
+
+
+def test_errors_without_device_are_codes_not_crashes():
+    # argument validation happens before any CUDA call
+    lib = _lib.load()
+    rc = lib.irl_energy_f64(None, None, 0, None, None, None)
+    assert rc == _lib.IRL_ERR_ARG
+    assert b"bad energy" in lib.irl_last_error()
