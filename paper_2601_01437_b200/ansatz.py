@@ -100,9 +100,9 @@ class AnsatzParameters:
 def _theta_device(params: AnsatzParameters, dev) -> torch.Tensor:
     arch = params.architecture
     if arch.complex_params:
-        t = torch.as_tensor(np.ascontiguousarray(params.theta, dtype=np.complex128), device=dev)
+        t = torch.as_tensor(np.array(params.theta, dtype=np.complex128), device=dev)
         return torch.view_as_real(t).reshape(-1).contiguous()  # interleaved (re, im)
-    return torch.as_tensor(np.ascontiguousarray(params.theta, dtype=np.float64), device=dev)
+    return torch.as_tensor(np.array(params.theta, dtype=np.float64), device=dev)
 
 
 def _x_device(x, n_inputs: int, dev) -> torch.Tensor:
@@ -136,11 +136,11 @@ def build_batch(params: AnsatzParameters, x, e_loc, weights=None, n_samples: int
     odt = torch.complex128 if arch.complex_params else torch.float64
     o = torch.empty((n, ld), dtype=odt, device=dev)
     batch = SampleBatch(None, weights, e_loc, o, n_samples or 0, kind=kind, param_count=p, device=dev)
-    _, coeff = batch._energy_pass(None)
+    _, mean = batch._energy_pass(None)
     obar = torch.empty(ld, dtype=odt, device=dev)
     g = torch.empty(ld, dtype=odt, device=dev)
-    fill_o_rows(params, xt, o, batch.weights, coeff, obar, g)
-    batch._set_colstats(batch._stats_e, obar, g, coeff)
+    fill_o_rows(params, xt, o, batch.weights, batch.gradient_coefficients(mean), obar, g)
+    batch._set_colstats(mean, obar, g)
     return batch
 
 

@@ -127,6 +127,7 @@ class SampleBatch:
         self.ld = ld
         self.device = dev
         self._coeff: dict = {}
+        self._gcoeff: dict = {}
         self._colstats: dict = {}
         self._ws: torch.Tensor | None = None
         self._stats_e: float | None = None
@@ -159,38 +160,53 @@ class SampleBatch:
         return self._ws
 
     def coefficients(self, mean: float) -> torch.Tensor:
-        """c_n = w_n (e_n - E): est:166-168 (Hermitian mode: w Re(e - E))."""
+        """Product coefficient c_n = w_n (e_n - E): est:166-168, est:186
+        (Hermitian batches: w_n Re(e_n - E))."""
         key = float(mean)
-        c = self._coeff.get(key)
-        if c is None:
-            c = self._energy_pass(key)[1]
-        return c
+        if key not in self._coeff:
+            self._energy_pass(key)
+        return self._coeff[key]
+
+    def gradient_coefficients(self, mean: float) -> torch.Tensor:
+        """Gradient coefficient w_n (e_n - E) with the full complex e (est:162)."""
+        key = float(mean)
+        if key not in self._gcoeff:
+            self._energy_pass(key)
+        return self._gcoeff[key]
 
     def _energy_pass(self, mean: float | None):
-        """Run k_energy; returns (stats3 host array, coeff for the batch's own E)."""
+        """Run k_energy; caches both coefficient vectors; returns (stats3 host array, E)."""
         n = self.n_rows
         stats = torch.empty(3, dtype=torch.float64, device=self.device)
-        coeff = torch.empty(n, dtype=self.e_loc.dtype, device=self.device)
+        gcoeff = torch.empty(n, dtype=self.e_loc.dtype, device=self.device)
         if self.is_complex:
-            _lib.call("irl_energy_c128", _lib.ptr(self.weights), _lib.ptr(self.e_loc), n,
-                      int(self.kind == KIND_HERMITIAN), _lib.ptr(stats), _lib.ptr(coeff), self._stream())
+            _lib.call("irl_energy_c128", _lib.ptr(self.weights), _lib.ptr(self.e_loc), n, 0,
+                      _lib.ptr(stats), _lib.ptr(gcoeff), self._stream())
         else:
             _lib.call("irl_energy_f64", _lib.ptr(self.weights), _lib.ptr(self.e_loc), n,
+                      _lib.ptr(stats), _lib.ptr(gcoeff), self._stream())
+        coeff = gcoeff
+        if self.kind == KIND_HERMITIAN:
+            coeff = torch.empty_like(gcoeff)
+            _lib.call("irl_energy_c128", _lib.ptr(self.weights), _lib.ptr(self.e_loc), n, 1,
                       _lib.ptr(stats), _lib.ptr(coeff), self._stream())
         host = stats.cpu().numpy()
         own = float(host[0])
         self._coeff[own] = coeff
+        self._gcoeff[own] = gcoeff
         self._stats_e = own
         if mean is not None and float(mean) != own:
             # another energy reference (e.g. E = 0 for the S trick of SURVEY §8(c)):
             # c = w (e - mean), formed on device
             d = self.e_loc - float(mean)
+            g = (self.weights * d).contiguous()
+            self._gcoeff[float(mean)] = g
             if self.kind == KIND_HERMITIAN:
                 d = torch.complex(d.real, torch.zeros_like(d.real))
-            c = (self.weights * d).contiguous()
-            self._coeff[float(mean)] = c
-            return host, c
-        return host, coeff
+                self._coeff[float(mean)] = (self.weights * d).contiguous()
+            else:
+                self._coeff[float(mean)] = g
+        return host, own
 
     def colstats(self, mean: float):
         """(obar, g) with obar = w @ O and g = c @ conj(O), c = w (e - mean)."""
@@ -198,7 +214,7 @@ class SampleBatch:
         hit = self._colstats.get(key)
         if hit is not None:
             return hit
-        c = self.coefficients(key)
+        c = self.gradient_coefficients(key)
         n = self.n_rows
         obar = torch.empty(self.ld, dtype=self.o_matrix.dtype, device=self.device)
         g = torch.empty(self.ld, dtype=self.o_matrix.dtype, device=self.device)
@@ -210,8 +226,7 @@ class SampleBatch:
         self._colstats[key] = (obar, g)
         return obar, g
 
-    def _set_colstats(self, mean: float, obar: torch.Tensor, g: torch.Tensor, coeff: torch.Tensor) -> None:
-        self._coeff[float(mean)] = coeff
+    def _set_colstats(self, mean: float, obar: torch.Tensor, g: torch.Tensor) -> None:
         self._colstats[float(mean)] = (obar, g)
 
     def obar(self) -> torch.Tensor:

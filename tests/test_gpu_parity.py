@@ -117,9 +117,9 @@ def test_h2_reference_data_path(pkg):
 
     g = golden("h2_exact")
     b = E.SampleBatch(None, g["w"], g["e"], g["o"], 0)
-    with pytest.warns(UserWarning):
-        en = E.estimate_energy(b)
+    en = E.estimate_energy(b)
     assert en.mean == pytest.approx(float(g["mean"]), abs=1e-13)
+    assert en.variance == pytest.approx(float(g["variance"]), rel=1e-10)
     assert rel(host(E.energy_gradient(b, en)), g["grad"]) < 1e-10
     for v, hv in zip(g["vs"], g["hv"]):
         assert rel(E.heff_matvec(b, en, v), hv) < PROD_TOL

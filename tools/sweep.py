@@ -1,0 +1,112 @@
+#!/usr/bin/env python
+"""Per-config performance sweep (one JSON line per config) — development tool.
+
+For each BASELINE config: O-build time (warm), fused / two-pass MVP time and
+GB/s (one O read per fused product, two per two-pass), IRL solve wall time.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from paper_2601_01437_b200 import _lib, ansatz as A, estimators as E, optimizer as OPT, synthetic as S  # noqa: E402
+
+
+def timed(fn, reps):
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    for a, b in evs:
+        a.record()
+        fn()
+        b.record()
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in evs]
+
+
+def flush_l2(buf):
+    buf.add_(1.0)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="1,2,3,4,5")
+    ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--rows", type=int, default=0)
+    ap.add_argument("--irl", type=int, default=1)
+    args = ap.parse_args()
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    l2buf = torch.zeros(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > L2
+    for idx in [int(c) for c in args.configs.split(",")]:
+        cfg = S.CONFIGS[idx]
+        if args.rows:
+            cfg = cfg.with_rows(args.rows)
+        t0 = time.perf_counter()
+        inp = S.make_inputs(cfg)
+        gen_s = time.perf_counter() - t0
+        arch = (A.RBMArchitecture(cfg.n_inputs, cfg.hidden, cfg.complex_params) if cfg.model == "rbm"
+                else A.MLPArchitecture(cfg.n_inputs, cfg.hidden))
+        params = A.AnsatzParameters(arch, inp.theta)
+        batch = A.build_batch(params, inp.x, inp.e_loc)
+        torch.cuda.synchronize()
+        # warm O-build time: refill the same buffers
+        xt = A._x_device(inp.x, arch.n_inputs, dev)
+        mean = batch._stats_e
+        obar, g = batch.colstats(mean)
+        gc = batch.gradient_coefficients(mean)
+        ob = timed(lambda: A.fill_o_rows(params, xt, batch.o_matrix, batch.weights, gc, obar, g), 3)
+        en = E.estimate_energy(batch)
+        N, P, ld = batch.n_rows, batch.param_count, batch.ld
+        b_el = 16 if batch.is_complex else 8
+        herm = batch.kind == E.KIND_HERMITIAN
+        coeff = batch.coefficients(en.mean)
+        if herm:
+            vin = torch.randn((2, ld), dtype=torch.float64, device=dev)
+            vin[:, P:] = 0
+            vout = torch.empty((2, ld), dtype=torch.float64, device=dev)
+            vi, vo = (vin[0], vin[1]), (vout[0], vout[1])
+        else:
+            vin = torch.randn(ld, dtype=torch.float64, device=dev)
+            vin[P:] = 0
+            vout = torch.empty(ld, dtype=torch.float64, device=dev)
+            vi, vo = vin, vout
+        out = {"config": cfg.name, "gen_s": gen_s, "obuild_ms": min(ob),
+               "obuild_gbs": N * P * b_el / (min(ob) / 1e3) / 1e9}
+        for mode, name, passes in ((1, "fused", 1), (2, "two_pass", 2)):
+            try:
+                plan = _lib.mvp_plan(N, ld, batch.is_complex, mode)
+                E._apply(batch, coeff, vi, vo, mode=mode)
+                torch.cuda.synchronize()
+            except Exception as exc:  # noqa: BLE001
+                out[name] = {"error": str(exc)[:200]}
+                continue
+            ms = []
+            for _ in range(args.reps):
+                flush_l2(l2buf)
+                ms += timed(lambda: E._apply(batch, coeff, vi, vo, mode=mode), 1)
+            med = statistics.median(ms)
+            out[name] = {"ms": med, "mvp_s": 1e3 / med, "gbs_one_read": N * P * b_el / (med / 1e3) / 1e9,
+                         "gbs_traffic": passes * N * ld * b_el / (med / 1e3) / 1e9, "plan": plan}
+        if args.irl:
+            conf = OPT.OptimizerConfig(m=cfg.m, max_restarts=cfg.max_restarts)
+            OPT.solve_step(batch, conf, seed=cfg.lanczos_seed, energy=en)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            res = OPT.solve_step(batch, conf, seed=cfg.lanczos_seed, energy=en)
+            torch.cuda.synchronize()
+            out["irl"] = {"wall_ms": (time.perf_counter() - t0) * 1e3, "n_matvec": res.n_matvec,
+                          "lambda": res.lambda_min, "converged": res.converged}
+        print(json.dumps(out), flush=True)
+        del batch, inp, xt, obar, g, gc, coeff
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
