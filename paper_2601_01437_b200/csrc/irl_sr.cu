@@ -6,6 +6,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <unordered_map>
 #include <unordered_set>
 
 #include "../../include/irl_sr.h"
@@ -114,14 +115,15 @@ struct Plan {
   StreamFn fn = nullptr;
 };
 
-size_t stream_extra_smem(bool cplx, int R, int NW, int C, int NS) {
+size_t stream_extra_smem(bool cplx, int R, int C, int NS) {
   const size_t sS = cplx ? 16 : 8;
-  return (size_t)(2 * NS + 2) * 8 + (size_t)2 * R * (NW + 1) * sS + (size_t)2 * C * R * sS + 33 * sS + 33 * 8;
+  return (size_t)(2 * NS + kXchSlots) * 8 + (size_t)2 * R * 32 * sS + (size_t)kXchSlots * C * R * sS + sS + 8;
 }
 
+// Geometry for C column slices (uneven split, slot width Wmax = ceil(ld_u / C)).
 bool choose_geom(int64_t ld_u, int C, bool cplx, int mode, int budget, Plan& p) {
-  if (ld_u % C) return false;
-  const int64_t W = ld_u / C;
+  if (C < 1 || C > ld_u) return false;
+  const int64_t W = cdiv(ld_u, C);
   if (W > INT_MAX / 16) return false;
   int best_ppt = 0, best_nt = 0;
   int64_t best_waste = INT64_MAX;
@@ -139,8 +141,7 @@ bool choose_geom(int64_t ld_u, int C, bool cplx, int mode, int budget, Plan& p) 
   if (!best_ppt) return false;
   const size_t slice = (size_t)W * 16;
   const int R = (4 * slice <= 64 * 1024) ? 4 : 1;
-  const int NW = best_nt / 32;
-  const size_t extra = stream_extra_smem(cplx, R, NW, C, 8);
+  const size_t extra = stream_extra_smem(cplx, R, C, 8);
   if ((size_t)budget <= extra) return false;
   int NS = (int)std::min<size_t>(8, ((size_t)budget - extra) / (R * slice));
   if (NS < 2) return false;
@@ -151,7 +152,7 @@ bool choose_geom(int64_t ld_u, int C, bool cplx, int mode, int budget, Plan& p) 
   p.R = R;
   p.NT = best_nt;
   p.NS = NS;
-  p.smem = (size_t)NS * R * slice + stream_extra_smem(cplx, R, NW, C, NS);
+  p.smem = (size_t)NS * R * slice + stream_extra_smem(cplx, R, C, NS);
   p.fn = pick_stream_any(cplx, mode, best_ppt, R);
   return p.fn != nullptr;
 }
@@ -163,52 +164,108 @@ int occupancy_blocks(const Plan& p, int& occ) {
   return IRL_OK;
 }
 
-int make_plan(int64_t n, int64_t ld_u, bool cplx, int mode, Plan& p) {
-  (void)n;
+int active_clusters(const Plan& p, int sms) {
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = p.C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(p.C * std::max(1, sms / p.C));
+  cfg.blockDim = dim3(p.NT + 32);
+  cfg.dynamicSmemBytes = p.smem;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int ncl = 0;
+  if (cudaOccupancyMaxActiveClusters(&ncl, (const void*)p.fn, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return ncl;
+}
+
+struct PlanKey {
+  int64_t ld_u;
+  int cplx, mode, dev;
+  bool operator==(const PlanKey& o) const {
+    return ld_u == o.ld_u && cplx == o.cplx && mode == o.mode && dev == o.dev;
+  }
+};
+struct PlanKeyHash {
+  size_t operator()(const PlanKey& k) const {
+    return std::hash<int64_t>()(k.ld_u * 131 + k.cplx * 17 + k.mode * 3 + k.dev * 7919);
+  }
+};
+
+int make_plan_uncached(int64_t ld_u, bool cplx, int mode, Plan& out) {
   DevInfo d;
   IRL_TRY(dev_info(d));
   const int budget = d.smem_optin;
   if (mode == MODE_FUSED) {
-    for (int C : {1, 2, 4, 8, 16}) {
+    // pick the cluster size that keeps the most SMs streaming (GPC packing
+    // limits how many clusters of a given size are co-resident)
+    Plan best;
+    int best_active = 0;
+    for (int C = 1; C <= 16; ++C) {
+      Plan p;
       if (!choose_geom(ld_u, C, cplx, mode, budget, p)) continue;
       IRL_TRY(ensure_fn_attrs((const void*)p.fn, budget));
+      int active = 0;
       if (C == 1) {
         int occ = 0;
         IRL_TRY(occupancy_blocks(p, occ));
         p.nb = d.sms * occ;
-        return IRL_OK;
+        active = p.nb;
+      } else {
+        p.nb = active_clusters(p, d.sms);
+        active = p.nb * C;
       }
-      cudaLaunchConfig_t cfg = {};
-      cudaLaunchAttribute attr[1];
-      attr[0].id = cudaLaunchAttributeClusterDimension;
-      attr[0].val.clusterDim.x = C;
-      attr[0].val.clusterDim.y = 1;
-      attr[0].val.clusterDim.z = 1;
-      cfg.gridDim = dim3(C * (d.sms / C));
-      cfg.blockDim = dim3(p.NT + 32);
-      cfg.dynamicSmemBytes = p.smem;
-      cfg.attrs = attr;
-      cfg.numAttrs = 1;
-      int ncl = 0;
-      cudaError_t e = cudaOccupancyMaxActiveClusters(&ncl, (const void*)p.fn, &cfg);
-      if (e != cudaSuccess || ncl < 1) {
-        cudaGetLastError();
-        continue;
+      if (active > best_active * 1.04) {  // a bigger cluster must buy > 4% more SMs
+        best = p;
+        best_active = active;
       }
-      p.nb = ncl;
-      return IRL_OK;
     }
-    return fail(IRL_ERR_DEVICE, "no fused single-pass geometry for ld=%lld units", (long long)ld_u);
+    if (best_active == 0) return fail(IRL_ERR_DEVICE, "no fused single-pass geometry for ld=%lld units", (long long)ld_u);
+    out = best;
+    return IRL_OK;
   }
-  for (int C = 1; C <= 1024; C *= 2) {
+  for (int C = 1; C <= 256; ++C) {
+    Plan p;
     if (!choose_geom(ld_u, C, cplx, mode, budget, p)) continue;
     IRL_TRY(ensure_fn_attrs((const void*)p.fn, budget));
     int occ = 0;
     IRL_TRY(occupancy_blocks(p, occ));
-    p.nb = std::max(1, (d.sms * occ) / C);
+    // ~2 waves of CTAs over the SMs
+    p.nb = std::max(1, (int)((2LL * d.sms * occ + C / 2) / C));
+    out = p;
     return IRL_OK;
   }
   return fail(IRL_ERR_DEVICE, "no streaming geometry for ld=%lld units", (long long)ld_u);
+}
+
+int make_plan(int64_t n, int64_t ld_u, bool cplx, int mode, Plan& p) {
+  (void)n;
+  static std::mutex mu;
+  static std::unordered_map<PlanKey, std::pair<int, Plan>, PlanKeyHash> cache;
+  int dev = 0;
+  IRL_TRY(cuda_check(cudaGetDevice(&dev), "cudaGetDevice"));
+  PlanKey key{ld_u, cplx ? 1 : 0, mode, dev};
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      p = it->second.second;
+      return it->second.first;
+    }
+  }
+  Plan q;
+  const int rc = make_plan_uncached(ld_u, cplx, mode, q);
+  const std::string err = g_err;
+  std::lock_guard<std::mutex> lk(mu);
+  cache[key] = {rc, q};
+  p = q;
+  if (rc != IRL_OK) g_err = err;
+  return rc;
 }
 
 int launch_stream(const Plan& p, const StreamArgs& a, cudaStream_t st) {
@@ -228,12 +285,32 @@ int launch_stream(const Plan& p, const StreamArgs& a, cudaStream_t st) {
     cfg.numAttrs = 1;
   }
   StreamArgs args = a;
-  args.W = p.W;
+  args.Wmax = p.W;
   args.C = p.C;
   args.nb = p.nb;
   args.stages = p.NS;
   void* kargs[] = {&args};
   return cuda_check(cudaLaunchKernelExC(&cfg, (const void*)p.fn, kargs), "stream kernel launch");
+}
+
+// finisher launched with programmatic dependent launch (overlaps its launch
+// with the streaming kernel's tail; it waits in griddepcontrol.wait)
+template <bool CPLX>
+int launch_finish_mvp(const double2* part, int nb, int64_t ld_u, const void* ysum, const double2* obar,
+                      const double* hf_re, const double* hf_im, const double* u0, double* out_re, double* out_im,
+                      const double* gpart, int n_gpart, double* out0, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.gridDim = dim3((unsigned)cdiv(ld_u, 32));
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cuda_check(cudaLaunchKernelEx(&cfg, k_finish_mvp<CPLX>, part, nb, ld_u, ysum, obar, hf_re, hf_im, u0,
+                                       out_re, out_im, gpart, n_gpart, out0),
+                    "finish kernel launch");
 }
 
 // MVP workspace layout for one plan
@@ -308,14 +385,11 @@ int mvp_impl(bool cplx, const double* O, int64_t n, int64_t p, int64_t ld, const
     a.spart = w.spart;
     a.gpart = w.gpart;
     IRL_TRY(launch_stream(pl, a, st));
-    const int64_t blocks = std::min<int64_t>(cdiv(ld_u, 256), 4096);
     if (cplx)
-      k_finish_mvp<true><<<(unsigned)blocks, 256, 0, st>>>(w.part, pl.nb, ld_u, w.ysum, a.obar, hf_re, hf_im, u0,
-                                                           out_re, out_im, w.gpart, 1, out0);
-    else
-      k_finish_mvp<false><<<(unsigned)blocks, 256, 0, st>>>(w.part, pl.nb, ld_u, w.ysum, a.obar, hf_re, hf_im, u0,
-                                                            out_re, out_im, w.gpart, 1, out0);
-    return cuda_check(cudaGetLastError(), "finish kernel launch");
+      return launch_finish_mvp<true>(w.part, pl.nb, ld_u, w.ysum, a.obar, hf_re, hf_im, u0, out_re, out_im, w.gpart, 1,
+                                     out0, st);
+    return launch_finish_mvp<false>(w.part, pl.nb, ld_u, w.ysum, a.obar, hf_re, hf_im, u0, out_re, out_im, w.gpart, 1,
+                                    out0, st);
   }
   Plan p1, p2;
   IRL_TRY(make_plan(n, ld_u, cplx, MODE_DOT, p1));
@@ -333,14 +407,11 @@ int mvp_impl(bool cplx, const double* O, int64_t n, int64_t p, int64_t ld, const
   a.gpart = w.gpart;
   IRL_TRY(launch_stream(p1, a, st));
   IRL_TRY(launch_stream(p2, a, st));
-  const int64_t blocks = std::min<int64_t>(cdiv(ld_u, 256), 4096);
   if (cplx)
-    k_finish_mvp<true><<<(unsigned)blocks, 256, 0, st>>>(w.part, p2.nb, ld_u, w.ysum, a.obar, hf_re, hf_im, u0,
-                                                         out_re, out_im, w.gpart, p1.C, out0);
-  else
-    k_finish_mvp<false><<<(unsigned)blocks, 256, 0, st>>>(w.part, p2.nb, ld_u, w.ysum, a.obar, hf_re, hf_im, u0,
-                                                          out_re, out_im, w.gpart, p1.C, out0);
-  return cuda_check(cudaGetLastError(), "finish kernel launch");
+    return launch_finish_mvp<true>(w.part, p2.nb, ld_u, w.ysum, a.obar, hf_re, hf_im, u0, out_re, out_im, w.gpart,
+                                   p1.C, out0, st);
+  return launch_finish_mvp<false>(w.part, p2.nb, ld_u, w.ysum, a.obar, hf_re, hf_im, u0, out_re, out_im, w.gpart,
+                                  p1.C, out0, st);
 }
 
 size_t mvp_ws_bytes(int64_t n, int64_t ld, bool cplx) {
@@ -379,11 +450,11 @@ int colstats_impl(bool cplx, const double* O, int64_t n, int64_t ld, const doubl
   a.part0 = static_cast<double2*>(ws);
   a.part1 = reinterpret_cast<double2*>(static_cast<char*>(ws) + align256((size_t)p.nb * ld_u * 16));
   IRL_TRY(launch_stream(p, a, st));
-  const int64_t blocks = std::min<int64_t>(cdiv(ld_u, 256), 4096);
+  const unsigned blocks = (unsigned)cdiv(ld_u, 32);
   if (cplx)
-    k_finish_stats<true><<<(unsigned)blocks, 256, 0, st>>>(a.part0, a.part1, p.nb, ld_u, (double2*)obar, (double2*)g);
+    k_finish_stats<true><<<blocks, 256, 0, st>>>(a.part0, a.part1, p.nb, ld_u, (double2*)obar, (double2*)g);
   else
-    k_finish_stats<false><<<(unsigned)blocks, 256, 0, st>>>(a.part0, a.part1, p.nb, ld_u, (double2*)obar, (double2*)g);
+    k_finish_stats<false><<<blocks, 256, 0, st>>>(a.part0, a.part1, p.nb, ld_u, (double2*)obar, (double2*)g);
   return cuda_check(cudaGetLastError(), "colstats finish launch");
 }
 
@@ -514,11 +585,11 @@ int obuild_impl(bool cplx, int model, const uint8_t* x, int64_t n, int n_vis, in
   a.nb = p.nb;
   p.fn<<<(unsigned)(p.nb * p.C), p.NT, 0, st>>>(a);
   IRL_TRY(cuda_check(cudaGetLastError(), "orows launch"));
-  const int64_t blocks = std::min<int64_t>(cdiv(ld_u, 256), 4096);
+  const unsigned blocks = (unsigned)cdiv(ld_u, 32);
   if (cplx)
-    k_finish_stats<true><<<(unsigned)blocks, 256, 0, st>>>(part0, part1, p.nb, ld_u, (double2*)obar, (double2*)g);
+    k_finish_stats<true><<<blocks, 256, 0, st>>>(part0, part1, p.nb, ld_u, (double2*)obar, (double2*)g);
   else
-    k_finish_stats<false><<<(unsigned)blocks, 256, 0, st>>>(part0, part1, p.nb, ld_u, (double2*)obar, (double2*)g);
+    k_finish_stats<false><<<blocks, 256, 0, st>>>(part0, part1, p.nb, ld_u, (double2*)obar, (double2*)g);
   return cuda_check(cudaGetLastError(), "obuild finish launch");
 }
 

@@ -16,6 +16,11 @@
 //   MODE_STATS  column statistics (A4/A5): acc0 = sum w conj(O),
 //               acc1 = sum c conj(O)   -> Obar (est:167), F/2 (est:162).
 //
+// The consumer loop is software-pipelined one row group deep: the dot
+// product, block reduction and DSMEM send of group g+1 are issued before
+// group g's exchange is awaited and accumulated, so the exchange latency
+// hides behind the next tile instead of stalling the HBM stream.
+//
 // Every reduction has a fixed order (warp butterfly, warps in index order,
 // cluster ranks in order, row blocks in order): results are bit-identical
 // run to run, no float atomics anywhere.
@@ -26,11 +31,13 @@ namespace irl {
 
 enum StreamMode { MODE_FUSED = 0, MODE_DOT = 1, MODE_ACC = 2, MODE_STATS = 3 };
 
+constexpr int kXchSlots = 4;  // DSMEM exchange ring depth (lookahead 1 needs 4, see below)
+
 struct StreamArgs {
   const double2* O;  // units; row stride ld_u
   int64_t n_rows;
   int64_t ld_u;
-  int W;       // units per column slice
+  int Wmax;    // max units per column slice (ring slot width)
   int C;       // column slices (cluster size in MODE_FUSED)
   int nb;      // row blocks (clusters in MODE_FUSED)
   int stages;  // ring depth
@@ -51,6 +58,10 @@ struct StreamArgs {
   void* spart;     // S[C]          (DOT -> ACC; FUSED writes [0])
   double* gpart;   // double[C]     (DOT; FUSED writes [0])
 };
+
+// Column split: slice r covers units [slice_lo(r), slice_lo(r+1)).  Uneven
+// splits let any cluster size tile the row (every unit is 16-B aligned).
+__host__ __device__ __forceinline__ int64_t slice_lo(int64_t ld_u, int C, int r) { return (ld_u * r) / C; }
 
 template <bool CPLX>
 __device__ __forceinline__ double2 load_vec_unit(const double* re, const double* im, int64_t u) {
@@ -74,20 +85,17 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
   const int NT = blockDim.x - 32;  // consumer threads; last warp = producer
   const int NW = NT >> 5;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int W = a.W, C = a.C, NS = a.stages;
-  const int RP = NW + 1;
+  const int C = a.C, NS = a.stages, WM = a.Wmax;
   const int64_t N = a.n_rows;
 
   double2* ring = reinterpret_cast<double2*>(smem);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)NS * R * W * 16);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)NS * R * WM * 16);
   uint64_t* empty = full + NS;
-  uint64_t* xbar = empty + NS;                  // [2]
-  S* red = reinterpret_cast<S*>(xbar + 2);      // [2][R][RP]
-  S* xch = red + 2 * R * RP;                    // [2][C][R]
-  S* scr_s = xch + 2 * C * R;                   // [32] block-reduce scratch
-  S* pro_s = scr_s + 32;                        // [1] cluster-visible prologue slot
-  double* scr_g = reinterpret_cast<double*>(pro_s + 1);  // [32]
-  double* pro_g = scr_g + 32;                            // [1]
+  uint64_t* xbar = empty + NS;                       // [kXchSlots]
+  S* red = reinterpret_cast<S*>(xbar + kXchSlots);   // [2][R][32]
+  S* xch = red + 2 * R * 32;                         // [kXchSlots][C][R]
+  S* pro_s = xch + kXchSlots * C * R;                // [1] cluster-visible prologue slot
+  double* pro_g = reinterpret_cast<double*>(pro_s + 1);  // [1]
 
   const bool clustered = (MODE == MODE_FUSED) && (C > 1);
   int rank, blk;
@@ -100,19 +108,21 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
   }
   const int64_t lo = (N * blk) / a.nb, hi = (N * (blk + 1)) / a.nb;
   const int G = (int)((hi - lo + R - 1) / R);
-  const int64_t col0 = (int64_t)rank * W;
+  const int64_t col0 = slice_lo(a.ld_u, C, rank);
+  const int W = (int)(slice_lo(a.ld_u, C, rank + 1) - col0);
 
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], NW);
     }
-    mbar_init(&xbar[0], 1);
-    mbar_init(&xbar[1], 1);
+    for (int s = 0; s < kXchSlots; ++s) mbar_init(&xbar[s], 1);
     fence_mbar_init();
   }
   __syncthreads();
   if (clustered) cluster_sync();  // peers' barriers initialised before any st.async
+  // let the (PDL-launched) finisher get scheduled; it waits for our completion
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   // ------------------------------------------------------------ producer --
   if (warp == NW) {
@@ -125,9 +135,9 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
         const int64_t r0 = lo + (int64_t)g * R;
         const int rows = (int)min((int64_t)R, hi - r0);
         mbar_arrive_expect_tx(&full[s], slice_bytes * rows);
-        double2* dst = ring + (size_t)s * R * W;
+        double2* dst = ring + (size_t)s * R * WM;
         const double2* src = a.O + r0 * a.ld_u + col0;
-        for (int r = 0; r < rows; ++r) bulk_g2s(dst + (size_t)r * W, src + r * a.ld_u, slice_bytes, &full[s]);
+        for (int r = 0; r < rows; ++r) bulk_g2s(dst + (size_t)r * WM, src + r * a.ld_u, slice_bytes, &full[s]);
       }
     }
     __syncwarp();
@@ -139,6 +149,8 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
   }
 
   // ----------------------------------------------------------- consumers --
+  // number of this thread's units inside the slice (units tid + k*NT)
+  const int kval = (W > tid) ? min(PPT, (W - tid + NT - 1) / NT) : 0;
   double2 vreg[PPT];
   double2 acc0[PPT];
   double2 acc1[PPT];
@@ -149,15 +161,21 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
     acc1[k] = make_double2(0.0, 0.0);
   }
 
+  // warp-parallel block reduction of per-warp values v[w] stored at buf[w]:
+  // every lane of every warp returns the same fixed-order butterfly sum.
+  auto block_sum = [&](const S* buf) -> S {
+    S x = (lane < NW) ? buf[lane] : T::zero();
+    return warp_sum<CPLX>(x);
+  };
+
   S s_val = T::zero();
   if constexpr (MODE == MODE_FUSED || MODE == MODE_DOT) {
     S sp = T::zero();
     double gp = 0.0;
 #pragma unroll
     for (int k = 0; k < PPT; ++k) {
-      const int idx = tid + k * NT;
-      if (idx < W) {
-        const int64_t u = col0 + idx;
+      if (k < kval) {
+        const int64_t u = col0 + tid + k * NT;
         vreg[k] = load_vec_unit<CPLX>(a.v_re, a.v_im, u);
         if (a.obar) T::dot_acc(sp, a.obar[u], vreg[k]);
         if (a.hf_re) {
@@ -169,17 +187,16 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
     }
     sp = warp_sum<CPLX>(sp);
     gp = warp_sum<false>(gp);
+    S* scr = red;  // red[0][0][*] is free before the main loop
+    double* scrg = reinterpret_cast<double*>(red + 32);
     if (lane == 0) {
-      scr_s[warp] = sp;
-      scr_g[warp] = gp;
+      scr[warp] = sp;
+      scrg[warp] = gp;
     }
     named_bar_sync(1, NT);
-    S sc = T::zero();
-    double gc = 0.0;
-    for (int w = 0; w < NW; ++w) {
-      sc = T::add(sc, scr_s[w]);
-      gc += scr_g[w];
-    }
+    S sc = block_sum(scr);
+    double gc = warp_sum<false>((lane < NW) ? scrg[lane] : 0.0);
+    named_bar_sync(1, NT);  // scratch reused by the main loop
     if (MODE == MODE_DOT) {
       if (blk == 0 && tid == 0) {
         reinterpret_cast<S*>(a.spart)[rank] = sc;
@@ -209,16 +226,101 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
     for (int c = 0; c < C; ++c) s_val = T::add(s_val, reinterpret_cast<const S*>(a.spart)[c]);
   }
 
-  S ys = T::zero();
-  for (int g = 0; g < G; ++g) {
-    const int s = g % NS;
-    const int64_t r0 = lo + (int64_t)g * R;
-    const int rows = (int)min((int64_t)R, hi - r0);
+  auto rows_of = [&](int g) -> int { return (int)min((int64_t)R, hi - (lo + (int64_t)g * R)); };
+  auto stage_ptr = [&](int g) -> const double2* { return ring + (size_t)(g % NS) * R * WM; };
 
-    // per-row scalars, lane r owns row r of the group (prefetched before the wait)
-    S cf0 = T::zero();
-    S cf1 = T::zero();
-    S tin = T::zero();
+  // dot + block reduction (+ DSMEM send) of group g; returns the CTA-level
+  // partial t for row `lane` (valid for lane < rows) in every warp.
+  auto dot_group = [&](int g) -> S {
+    const int rows = rows_of(g);
+    mbar_wait(&full[g % NS], (g / NS) & 1);
+    const double2* st = stage_ptr(g);
+    S dp[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) dp[r] = T::zero();
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) {
+      if (k < kval) {
+        const int idx = tid + k * NT;
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          if (r < rows) T::dot_acc(dp[r], st[(size_t)r * WM + idx], vreg[k]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) dp[r] = warp_sum<CPLX>(dp[r]);
+    S* rb = red + (g & 1) * R * 32;
+    if (lane == 0) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) rb[r * 32 + warp] = dp[r];
+    }
+    named_bar_sync(1, NT);
+    S t = T::zero();
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const S tr = block_sum(rb + r * 32);
+      if (lane == r) t = tr;
+    }
+    if (clustered && warp == 0) {
+      const int b = g % kXchSlots;
+      if (lane == 0) mbar_arrive_expect_tx(&xbar[b], (uint32_t)(C * rows * sizeof(S)));
+      if (lane < rows) {
+        const uint32_t la = smem_addr(&xch[(b * C + rank) * R + lane]);
+        const uint32_t lb = smem_addr(&xbar[b]);
+        for (int q = 0; q < C; ++q) st_async(map_to_rank(la, q), t, map_to_rank(lb, q));
+      }
+    }
+    return t;
+  };
+
+  // finish group g: cluster-summed t -> y -> accumulate -> release the stage
+  S ys = T::zero();
+  auto acc_group = [&](int g, S tcta, S cf0, S cf1) {
+    const int rows = rows_of(g);
+    const double2* st = stage_ptr(g);
+    S yv = T::zero();
+    if constexpr (MODE == MODE_FUSED || MODE == MODE_ACC) {
+      S t = tcta;
+      if (clustered) {
+        const int b = g % kXchSlots;
+        mbar_wait(&xbar[b], (g / kXchSlots) & 1);
+        t = T::zero();
+        if (lane < rows)
+          for (int q = 0; q < C; ++q) t = T::add(t, xch[(b * C + q) * R + lane]);
+      }
+      if (lane < rows) yv = T::mul(cf0, T::sub(t, s_val));
+    } else {
+      yv = cf0;
+    }
+    if constexpr (MODE == MODE_ACC || MODE == MODE_STATS) mbar_wait(&full[g % NS], (g / NS) & 1);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (r < rows) {
+        const S y = T::shfl(yv, r);
+        S y1 = T::zero();
+        if constexpr (MODE == MODE_STATS) y1 = T::shfl(cf1, r);
+        if (MODE != MODE_STATS && tid == 0) ys = T::add(ys, y);
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+          if (k < kval) {
+            const double2 u = st[(size_t)r * WM + tid + k * NT];
+            T::axpy(acc0[k], u, y);
+            if constexpr (MODE == MODE_STATS) T::axpy(acc1[k], u, y1);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[g % NS]);
+  };
+
+  // per-row coefficients for group g (lane r owns row r)
+  auto load_coeffs = [&](int g, S& cf0, S& cf1, S& tin) {
+    const int64_t r0 = lo + (int64_t)g * R;
+    const int rows = rows_of(g);
+    cf0 = T::zero();
+    cf1 = T::zero();
+    tin = T::zero();
     if (lane < rows) {
       if constexpr (MODE == MODE_STATS) {
         const double w = reinterpret_cast<const double*>(a.coeff0)[r0 + lane];
@@ -228,86 +330,42 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
         cf0 = reinterpret_cast<const S*>(a.coeff0)[r0 + lane];
       }
       if constexpr (MODE == MODE_ACC) {
-        for (int c = 0; c < C; ++c) tin = T::add(tin, reinterpret_cast<const S*>(a.tpart)[(int64_t)c * N + r0 + lane]);
+        for (int c = 0; c < C; ++c)
+          tin = T::add(tin, reinterpret_cast<const S*>(a.tpart)[(int64_t)c * N + r0 + lane]);
       }
     }
+  };
 
-    mbar_wait(&full[s], (g / NS) & 1);
-    const double2* st = ring + (size_t)s * R * W;
-
-    S yv = T::zero();
-    if constexpr (MODE == MODE_FUSED || MODE == MODE_DOT) {
-      S dp[R];
-#pragma unroll
-      for (int r = 0; r < R; ++r) dp[r] = T::zero();
-#pragma unroll
-      for (int k = 0; k < PPT; ++k) {
-        const int idx = tid + k * NT;
-        if (idx < W) {
-#pragma unroll
-          for (int r = 0; r < R; ++r)
-            if (r < rows) T::dot_acc(dp[r], st[(size_t)r * W + idx], vreg[k]);
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < R; ++r) dp[r] = warp_sum<CPLX>(dp[r]);
-      S* rb = red + (g & 1) * R * RP;
-      if (lane == 0) {
-#pragma unroll
-        for (int r = 0; r < R; ++r) rb[r * RP + warp] = dp[r];
-      }
-      named_bar_sync(1, NT);
-      S t = T::zero();
-      if (lane < rows)
-        for (int w = 0; w < NW; ++w) t = T::add(t, rb[lane * RP + w]);
-      if constexpr (MODE == MODE_DOT) {
-        if (warp == 0 && lane < rows) reinterpret_cast<S*>(a.tpart)[(int64_t)rank * N + r0 + lane] = t;
-      } else {
-        if (clustered) {
-          const int b = g & 1;
-          if (warp == 0) {
-            if (lane == 0) mbar_arrive_expect_tx(&xbar[b], (uint32_t)(C * rows * sizeof(S)));
-            if (lane < rows) {
-              const uint32_t la = smem_addr(&xch[(b * C + rank) * R + lane]);
-              const uint32_t lb = smem_addr(&xbar[b]);
-              for (int q = 0; q < C; ++q) st_async(map_to_rank(la, q), t, map_to_rank(lb, q));
-            }
-          }
-          mbar_wait(&xbar[b], (g >> 1) & 1);
-          t = T::zero();
-          if (lane < rows)
-            for (int q = 0; q < C; ++q) t = T::add(t, xch[(b * C + q) * R + lane]);
-        }
-        if (lane < rows) yv = T::mul(cf0, T::sub(t, s_val));
-      }
-    } else if constexpr (MODE == MODE_ACC) {
-      if (lane < rows) yv = T::mul(cf0, T::sub(tin, s_val));
-    } else {
-      yv = cf0;
+  if constexpr (MODE == MODE_DOT) {
+    for (int g = 0; g < G; ++g) {
+      const S t = dot_group(g);
+      const int rows = rows_of(g);
+      if (warp == 0 && lane < rows) reinterpret_cast<S*>(a.tpart)[(int64_t)rank * N + lo + (int64_t)g * R + lane] = t;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[g % NS]);
     }
-
-    if constexpr (MODE != MODE_DOT) {
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        if (r < rows) {
-          const S y = T::shfl(yv, r);
-          S y1 = T::zero();
-          if constexpr (MODE == MODE_STATS) y1 = T::shfl(cf1, r);
-          if (MODE != MODE_STATS && tid == 0) ys = T::add(ys, y);
-#pragma unroll
-          for (int k = 0; k < PPT; ++k) {
-            const int idx = tid + k * NT;
-            if (idx < W) {
-              const double2 u = st[(size_t)r * W + idx];
-              T::axpy(acc0[k], u, y);
-              if constexpr (MODE == MODE_STATS) T::axpy(acc1[k], u, y1);
-            }
-          }
+  } else if constexpr (MODE == MODE_FUSED) {
+    if (G > 0) {
+      S cf0, cf1, tin;
+      load_coeffs(0, cf0, cf1, tin);
+      S t_cur = dot_group(0);
+      for (int g = 0; g < G; ++g) {
+        S t_next = T::zero(), cn0 = T::zero(), cn1 = T::zero(), tn = T::zero();
+        if (g + 1 < G) {
+          load_coeffs(g + 1, cn0, cn1, tn);
+          t_next = dot_group(g + 1);  // lookahead: overlaps group g's exchange latency
         }
+        acc_group(g, t_cur, cf0, cf1);
+        t_cur = t_next;
+        cf0 = cn0;
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
+  } else {
+    for (int g = 0; g < G; ++g) {
+      S cf0, cf1, tin;
+      load_coeffs(g, cf0, cf1, tin);
+      acc_group(g, tin, cf0, cf1);
+    }
   }
 
   if constexpr (MODE != MODE_DOT) {
@@ -315,10 +373,9 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
     double2* p1 = (MODE == MODE_STATS) ? a.part1 + (int64_t)blk * a.ld_u + col0 : nullptr;
 #pragma unroll
     for (int k = 0; k < PPT; ++k) {
-      const int idx = tid + k * NT;
-      if (idx < W) {
-        p0[idx] = acc0[k];
-        if constexpr (MODE == MODE_STATS) p1[idx] = acc1[k];
+      if (k < kval) {
+        p0[tid + k * NT] = acc0[k];
+        if constexpr (MODE == MODE_STATS) p1[tid + k * NT] = acc1[k];
       }
     }
     if (MODE != MODE_STATS && rank == 0 && tid == 0) reinterpret_cast<S*>(a.ysum)[blk] = ys;
@@ -326,63 +383,105 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
   if (clustered) cluster_sync();
 }
 
+// Deterministic fixed-order sum of nb per-block partials, 32 units x 8 row
+// groups per CTA.  Launched with programmatic dependent launch: the CTA is
+// resident before the producer kernel ends and waits in griddepcontrol.wait.
+//
 // out = sum_b part[b] - conj(obar) * sum_b ysum[b]  (+ u0 * hf)    ; out0 = sum gpart
 template <bool CPLX>
-__global__ void k_finish_mvp(const double2* __restrict__ part, int nb, int64_t ld_u, const void* ysum,
-                             const double2* __restrict__ obar, const double* hf_re, const double* hf_im,
-                             const double* u0, double* out_re, double* out_im, const double* gpart, int n_gpart,
-                             double* out0) {
+__global__ void __launch_bounds__(256) k_finish_mvp(const double2* __restrict__ part, int nb, int64_t ld_u,
+                                                    const void* ysum, const double2* __restrict__ obar,
+                                                    const double* hf_re, const double* hf_im, const double* u0,
+                                                    double* out_re, double* out_im, const double* gpart,
+                                                    int n_gpart, double* out0) {
   using T = Traits<CPLX>;
   using S = typename T::S;
-  S Y = T::zero();
-  const S* ys = reinterpret_cast<const S*>(ysum);
-  for (int b = 0; b < nb; ++b) Y = T::add(Y, ys[b]);
-  const double uu = (hf_re && u0) ? *u0 : 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ld_u; i += (int64_t)gridDim.x * blockDim.x) {
-    double2 acc = make_double2(0.0, 0.0);
-    for (int b = 0; b < nb; ++b) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  __shared__ double2 sh[8][33];
+  __shared__ S shy[8];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  // Y = sum_b ysum[b]: each warp a strided fixed-order partial, then 8 in order
+  const S* ysv = reinterpret_cast<const S*>(ysum);
+  S yp = T::zero();
+  for (int b = tx; b < nb; b += 32) yp = T::add(yp, ysv[b]);
+  yp = warp_sum<CPLX>(yp);
+  if (ty == 0 && tx == 0) shy[0] = yp;
+  const int64_t i = blockIdx.x * 32 + tx;
+  double2 acc = make_double2(0.0, 0.0);
+  if (i < ld_u) {
+    for (int b = ty; b < nb; b += 8) {
       const double2 p = part[(int64_t)b * ld_u + i];
       acc.x += p.x;
       acc.y += p.y;
     }
-    if (obar) {
-      S negY;
-      if constexpr (CPLX) negY = make_double2(-Y.x, -Y.y); else negY = -Y;
-      T::axpy(acc, obar[i], negY);
-    }
-    if (hf_re && u0) {
-      const double2 h = load_vec_unit<CPLX>(hf_re, hf_im, i);
-      acc.x = fma(uu, h.x, acc.x);
-      acc.y = fma(uu, h.y, acc.y);
-    }
-    if constexpr (!CPLX) {
-      reinterpret_cast<double2*>(out_re)[i] = acc;
-    } else {
-      out_re[i] = acc.x;
-      if (out_im) out_im[i] = acc.y;
-    }
   }
-  if (out0 && blockIdx.x == 0 && threadIdx.x == 0) {
-    double g = 0.0;
-    if (hf_re)
-      for (int c = 0; c < n_gpart; ++c) g += gpart[c];
-    *out0 = g;
+  sh[ty][tx] = acc;
+  __syncthreads();
+  if (ty == 0) {
+    const S Y = shy[0];
+    acc = sh[0][tx];
+    for (int k = 1; k < 8; ++k) {
+      acc.x += sh[k][tx].x;
+      acc.y += sh[k][tx].y;
+    }
+    if (i < ld_u) {
+      if (obar) {
+        S negY;
+        if constexpr (CPLX) negY = make_double2(-Y.x, -Y.y); else negY = -Y;
+        T::axpy(acc, obar[i], negY);
+      }
+      if (hf_re && u0) {
+        const double uu = *u0;
+        const double2 h = load_vec_unit<CPLX>(hf_re, hf_im, i);
+        acc.x = fma(uu, h.x, acc.x);
+        acc.y = fma(uu, h.y, acc.y);
+      }
+      if constexpr (!CPLX) {
+        reinterpret_cast<double2*>(out_re)[i] = acc;
+      } else {
+        out_re[i] = acc.x;
+        if (out_im) out_im[i] = acc.y;
+      }
+    }
+    if (out0 && blockIdx.x == 0 && tx == 0) {
+      double g = 0.0;
+      if (hf_re)
+        for (int c = 0; c < n_gpart; ++c) g += gpart[c];
+      *out0 = g;
+    }
   }
 }
 
 // obar = sum_b part0[b] (conjugated back for complex) ; g = sum_b part1[b]
 template <bool CPLX>
-__global__ void k_finish_stats(const double2* __restrict__ part0, const double2* __restrict__ part1, int nb,
-                               int64_t ld_u, double2* obar, double2* g) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ld_u; i += (int64_t)gridDim.x * blockDim.x) {
-    double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
-    for (int b = 0; b < nb; ++b) {
+__global__ void __launch_bounds__(256) k_finish_stats(const double2* __restrict__ part0,
+                                                      const double2* __restrict__ part1, int nb, int64_t ld_u,
+                                                      double2* obar, double2* g) {
+  __shared__ double2 sh0[8][33], sh1[8][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t i = blockIdx.x * 32 + tx;
+  double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
+  if (i < ld_u) {
+    for (int b = ty; b < nb; b += 8) {
       const double2 p = part0[(int64_t)b * ld_u + i];
       const double2 q = part1[(int64_t)b * ld_u + i];
       a0.x += p.x;
       a0.y += p.y;
       a1.x += q.x;
       a1.y += q.y;
+    }
+  }
+  sh0[ty][tx] = a0;
+  sh1[ty][tx] = a1;
+  __syncthreads();
+  if (ty == 0 && i < ld_u) {
+    a0 = sh0[0][tx];
+    a1 = sh1[0][tx];
+    for (int k = 1; k < 8; ++k) {
+      a0.x += sh0[k][tx].x;
+      a0.y += sh0[k][tx].y;
+      a1.x += sh1[k][tx].x;
+      a1.y += sh1[k][tx].y;
     }
     if (CPLX) a0.y = -a0.y;
     obar[i] = a0;
