@@ -3,6 +3,7 @@
 #include <climits>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -206,7 +207,10 @@ int make_plan_uncached(int64_t ld_u, bool cplx, int mode, Plan& out) {
     // limits how many clusters of a given size are co-resident)
     Plan best;
     int best_active = 0;
+    const char* force = getenv("IRL_FUSED_CLUSTER");  // tuning override
+    const int c_force = force ? atoi(force) : 0;
     for (int C = 1; C <= 16; ++C) {
+      if (c_force > 0 && C != c_force) continue;
       Plan p;
       if (!choose_geom(ld_u, C, cplx, mode, budget, p)) continue;
       IRL_TRY(ensure_fn_attrs((const void*)p.fn, budget));
@@ -220,6 +224,7 @@ int make_plan_uncached(int64_t ld_u, bool cplx, int mode, Plan& out) {
         p.nb = active_clusters(p, d.sms);
         active = p.nb * C;
       }
+      active = std::min(active, d.sms);  // SMs kept streaming; extra co-resident CTAs buy nothing
       if (active > best_active * 1.04) {  // a bigger cluster must buy > 4% more SMs
         best = p;
         best_active = active;
