@@ -99,7 +99,7 @@ class BorderedOperator:
     """opt:140-148 on the device: one fused streaming launch per product."""
 
     def __init__(self, batch: SampleBatch, energy: EnergyEstimate, gradient: torch.Tensor | None = None,
-                 mode: int = _lib.MVP_AUTO):
+                 mode: int = _lib.MVP_AUTO, use_graph: bool = True):
         self.batch = batch
         self.energy = energy
         self.layout = BorderedLayout(batch)
@@ -120,6 +120,20 @@ class BorderedOperator:
             half[:p] = 0.5 * gradient
             self.half_f = half
         self.count = 0
+        self.use_graph = use_graph
+        self._sweepers: dict = {}
+
+    supports_out = True
+
+    def sweeper(self, length: int, m: int):
+        """Persistent graph-captured Lanczos sweeper bound to this operator."""
+        key = (length, m)
+        sw = self._sweepers.get(key)
+        if sw is None:
+            sw = krylov._GraphSweeper(lambda v, w: self(v, out=w), length, m, self.batch.device,
+                                      use_graph=self.use_graph)
+            self._sweepers[key] = sw
+        return sw
 
     def __call__(self, u: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         if out is None:
@@ -158,12 +172,19 @@ def direction_from_vector(vec: torch.Tensor, gradient: torch.Tensor, p: int, her
 
 
 def solve_step(batch: SampleBatch, config: OptimizerConfig = OptimizerConfig(), step: int = 0, *,
-               energy: EnergyEstimate | None = None, mode: int = _lib.MVP_AUTO, seed: int | None = None) -> StepResult:
+               energy: EnergyEstimate | None = None, mode: int = _lib.MVP_AUTO, seed: int | None = None,
+               use_graph: bool = True) -> StepResult:
     """The IRL-SR hot path of one outer step (opt:134-165) on a device batch."""
     if energy is None:
         energy = estimate_energy(batch)
-    gradient = energy_gradient(batch, energy)
-    op = BorderedOperator(batch, energy, gradient, mode=mode)
+    # the operator (and its captured Lanczos graphs) is cached on the batch
+    cache = batch.__dict__.setdefault("_bordered_ops", {})
+    key = (float(energy.mean), int(mode), use_graph)
+    op = cache.get(key)
+    if op is None:
+        op = BorderedOperator(batch, energy, energy_gradient(batch, energy), mode=mode, use_graph=use_graph)
+        cache[key] = op
+    gradient = op.gradient
     s = _batch_seed(config, step) if seed is None else seed
     lay = op.layout
     if config.method == "irl":

@@ -242,3 +242,61 @@ def test_cfg2_full_properties(pkg):
     # a chunked CPU restatement on a row subset agrees with the device batch of that subset
     sub = S.make_inputs(S.CONFIGS[2].with_rows(4096))
     assert np.array_equal(sub.x, inp.x[:4096])
+
+
+def test_graph_sweeper_matches_eager_driver(pkg):
+    """The CUDA-graph Lanczos sweep returns the same solve as the eager driver."""
+    from paper_2601_01437_b200 import optimizer as OPT, synthetic as S
+
+    cfg = S.CONFIGS[1].with_rows(2048)
+    b = device_batch(S.make_inputs(cfg))
+    conf = OPT.OptimizerConfig(m=cfg.m, max_restarts=3)
+    eager = OPT.solve_step(b, conf, seed=5, use_graph=False)
+    graph = OPT.solve_step(b, conf, seed=5)
+    again = OPT.solve_step(b, conf, seed=5)  # graph replay path
+    for r in (graph, again):
+        assert r.n_matvec == eager.n_matvec
+        assert abs(r.lambda_min - eager.lambda_min) <= 1e-12 * abs(eager.lambda_min)
+        assert rel(host(r.direction), host(eager.direction)) < 1e-9
+
+
+def test_graph_sweeper_restarts_and_breakdown(pkg):
+    """Restart (j0 = 1 graph) and lucky breakdown paths of the device sweeper."""
+    import torch
+    from paper_2601_01437_b200 import krylov
+
+    dev = torch.device("cuda")
+    rng = np.random.default_rng(7)
+    dim = 300
+    q, _ = np.linalg.qr(rng.standard_normal((dim, dim)))
+    vals = np.geomspace(1.0, 1e3, dim) * rng.choice([-1.0, 1.0], dim)
+    a = torch.as_tensor((q * vals) @ q.T, device=dev)
+
+    class Op:
+        supports_out = True
+
+        def __init__(self, mat):
+            self.mat = mat
+            self._sw = {}
+
+        def __call__(self, v, out=None):
+            r = self.mat @ v
+            if out is None:
+                return r
+            out.copy_(r)
+            return out
+
+        def sweeper(self, length, m):
+            if (length, m) not in self._sw:
+                self._sw[(length, m)] = krylov._GraphSweeper(lambda v, w: self(v, out=w), length, m, dev)
+            return self._sw[(length, m)]
+
+    op = Op(a)
+    pair = krylov.irl_smallest(op, dim, m=20, tol=1e-10, seed=3, device=dev)
+    ref = krylov.irl_smallest(lambda v: a.cpu().numpy() @ v, dim, m=20, tol=1e-10, seed=3)
+    assert pair.n_restarts > 0
+    assert abs(pair.value - np.linalg.eigvalsh((q * vals) @ q.T)[0]) < 1e-9 * 1e3
+    assert abs(pair.value - ref.value) < 1e-9 * 1e3
+    ident = Op(torch.eye(40, dtype=torch.float64, device=dev))
+    p2 = krylov.irl_smallest(ident, 40, seed=2, device=dev)
+    assert abs(p2.value - 1.0) < 1e-12 and p2.n_matvec <= 5
