@@ -251,7 +251,12 @@ int make_plan_uncached(int64_t ld_u, bool cplx, int mode, Plan& out) {
 int make_plan(int64_t n, int64_t ld_u, bool cplx, int mode, Plan& p) {
   (void)n;
   static std::mutex mu;
-  static std::unordered_map<PlanKey, std::pair<int, Plan>, PlanKeyHash> cache;
+  struct Entry {
+    int rc;
+    Plan plan;
+    std::string err;
+  };
+  static std::unordered_map<PlanKey, Entry, PlanKeyHash> cache;
   int dev = 0;
   IRL_TRY(cuda_check(cudaGetDevice(&dev), "cudaGetDevice"));
   PlanKey key{ld_u, cplx ? 1 : 0, mode, dev};
@@ -259,17 +264,17 @@ int make_plan(int64_t n, int64_t ld_u, bool cplx, int mode, Plan& p) {
     std::lock_guard<std::mutex> lk(mu);
     auto it = cache.find(key);
     if (it != cache.end()) {
-      p = it->second.second;
-      return it->second.first;
+      p = it->second.plan;
+      if (it->second.rc != IRL_OK) g_err = it->second.err;
+      return it->second.rc;
     }
   }
   Plan q;
   const int rc = make_plan_uncached(ld_u, cplx, mode, q);
-  const std::string err = g_err;
+  const std::string err = rc != IRL_OK ? g_err : std::string();
   std::lock_guard<std::mutex> lk(mu);
-  cache[key] = {rc, q};
+  cache[key] = Entry{rc, q, err};
   p = q;
-  if (rc != IRL_OK) g_err = err;
   return rc;
 }
 
