@@ -122,6 +122,24 @@ int irl_mvp_c128(const double* O, int64_t n, int64_t p, int64_t ld, const double
  * row blocks); for benches and tests.  Returns IRL_OK or an error. */
 int irl_mvp_plan(int64_t n, int64_t ld, int is_complex, int mode, int* out_path, int* out_geom7);
 
+/* --------------------------------------------------------- K6 (cfg5) ----
+ * On-the-fly O regeneration for the shallow MLP: O is never stored.  The same
+ * products (heff_matvec / S v, estimators.py:171-186, bordered opt:140-148)
+ * and column statistics (estimators.py:156-168) are regenerated from the
+ * bit-packed inputs and the hidden activations t, g (N x h f64) with FP64
+ * tensor-core GEMMs.  x bits: N x 2 uint64 (n_in <= 100).  Vectors use the
+ * padded MLP layout [W (h x n_in), b, u, c] of length ld = irl_padded_ld(P). */
+size_t irl_otf_workspace_bytes(int64_t n, int n_in, int hidden);
+int irl_otf_prepare_mlp_f64(const uint8_t* x, int64_t n, int n_in, int hidden, const double* theta, uint64_t* xbits,
+                            double* t, double* g, void* stream);
+int irl_otf_colstats_mlp_f64(const uint64_t* xbits, const double* t, const double* g, int64_t n, int n_in, int hidden,
+                             int64_t ld, const double* w, const double* coeff, double* obar, double* grad, void* ws,
+                             size_t ws_bytes, void* stream);
+int irl_otf_mvp_mlp_f64(const uint64_t* xbits, const double* t, const double* g, int64_t n, int n_in, int hidden,
+                        int64_t ld, const double* obar, const double* coeff, const double* v, double* out,
+                        const double* half_f, const double* u0, double* out0, void* ws, size_t ws_bytes,
+                        void* stream);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

@@ -214,3 +214,41 @@ def hidden_activations(params: AnsatzParameters, x, device=None):
     _lib.call("irl_hidden_mlp_f64", _lib.ptr(xt), n, arch.n_in, arch.hidden, _lib.ptr(theta), _lib.ptr(t),
               _lib.ptr(g), st)
     return t, g
+
+
+def build_batch_otf(params: AnsatzParameters, x, e_loc, weights=None, n_samples: int | None = None,
+                    device=None) -> SampleBatch:
+    """MLP batch in on-the-fly mode (K6): O is never stored.
+
+    Keeps the bit-packed inputs and the hidden activations t, g (N x h) in HBM;
+    every product regenerates O's contribution with FP64 tensor-core GEMMs.
+    Same SampleBatch interface (estimate_energy, energy_gradient, heff_matvec,
+    qgt_matvec, solve_step) as a stored-O batch.
+    """
+    arch = params.architecture
+    if arch.model != _lib.MODEL_MLP:
+        raise ValueError("on-the-fly mode is implemented for the shallow MLP")
+    dev = _device(device)
+    xt = _x_device(x, arch.n_inputs, dev)
+    n = int(xt.shape[0])
+    if n < 1:
+        raise ValueError("empty batch")
+    if weights is None:
+        weights = torch.full((n,), 1.0 / n, dtype=torch.float64, device=dev)
+        if n_samples is None:
+            n_samples = n
+    p = arch.param_count
+    ld = _lib.padded_ld(p, False)
+    # a zero-width placeholder keeps SampleBatch's validation; O is not stored
+    placeholder = torch.empty((n, ld), dtype=torch.float64, device="meta")
+    batch = SampleBatch.__new__(SampleBatch)
+    SampleBatch._init_common(batch, weights, e_loc, n, n_samples or 0, KIND_REAL, p, ld, dev)
+    batch.o_matrix = placeholder
+    xbits = torch.empty((n, 2), dtype=torch.int64, device=dev)
+    t = torch.empty((n, arch.hidden), dtype=torch.float64, device=dev)
+    g = torch.empty((n, arch.hidden), dtype=torch.float64, device=dev)
+    theta = _theta_device(params, dev)
+    _lib.call("irl_otf_prepare_mlp_f64", _lib.ptr(xt), n, arch.n_in, arch.hidden, _lib.ptr(theta), _lib.ptr(xbits),
+              _lib.ptr(t), _lib.ptr(g), _lib.stream_handle(dev))
+    batch.otf = {"xbits": xbits, "t": t, "g": g, "n_in": arch.n_in, "hidden": arch.hidden}
+    return batch

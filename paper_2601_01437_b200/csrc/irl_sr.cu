@@ -12,6 +12,7 @@
 
 #include "../../include/irl_sr.h"
 #include "obuild.cuh"
+#include "otf.cuh"
 #include "stream.cuh"
 
 using namespace irl;
@@ -603,6 +604,69 @@ int obuild_impl(bool cplx, int model, const uint8_t* x, int64_t n, int n_vis, in
   return cuda_check(cudaGetLastError(), "obuild finish launch");
 }
 
+// --------------------------------------------------------------- otf ----
+struct OtfPlan {
+  int jc, nb, ny;
+  size_t smem_dot, smem_acc;
+};
+
+int make_otf_plan(int64_t n, int n_in, int hidden, OtfPlan& p) {
+  DevInfo d;
+  IRL_TRY(dev_info(d));
+  if (n_in < 1 || n_in > OTF_MAX_NIN) return fail(IRL_ERR_ARG, "on-the-fly mode supports n_in <= %d", OTF_MAX_NIN);
+  p.jc = (int)cdiv(hidden, OTF_BJ);
+  p.nb = std::max(1, (int)((2LL * d.sms + p.jc / 2) / p.jc));
+  p.nb = (int)std::min<int64_t>(p.nb, std::max<int64_t>(1, cdiv(n, OTF_BM)));
+  p.ny = d.sms;
+  p.smem_dot = (size_t)(OTF_BJ * OTF_MAX_NIN + 2 * OTF_BJ + 4 * OTF_BM * OTF_BJ) * 8 + 2 * OTF_BM * OTF_XW * 8 +
+               4 * OTF_BM * 8;
+  p.smem_acc = (size_t)4 * OTF_BM * OTF_BJ * 8 + 2 * OTF_BM * OTF_XW * 8 + 2 * OTF_BM * 8;
+  IRL_TRY(ensure_fn_attrs((const void*)k_otf_dot, d.smem_optin));
+  IRL_TRY(ensure_fn_attrs((const void*)k_otf_acc, d.smem_optin));
+  return IRL_OK;
+}
+
+struct OtfWs {
+  double *tpart, *y, *ypart, *dpart, *gpart, *part, *partu;
+  size_t bytes;
+};
+
+OtfWs otf_ws_layout(const OtfPlan& p, int64_t n, int hidden, void* base) {
+  OtfWs w{};
+  size_t off = 0;
+  auto carve = [&](size_t b) {
+    double* r = base ? reinterpret_cast<double*>(static_cast<char*>(base) + off) : nullptr;
+    off += align256(b);
+    return r;
+  };
+  w.tpart = carve((size_t)p.jc * n * 8);
+  w.y = carve((size_t)n * 8);
+  w.ypart = carve((size_t)p.ny * 8);
+  w.dpart = carve((size_t)p.ny * 8);
+  w.gpart = carve((size_t)p.ny * 8);
+  w.part = carve((size_t)p.nb * hidden * OTF_KC * 8);
+  w.partu = carve((size_t)p.nb * hidden * 8);
+  w.bytes = off;
+  return w;
+}
+
+int otf_check(const uint64_t* xbits, const double* t, const double* g, int64_t n, int n_in, int hidden, int64_t ld) {
+  if (!xbits || !t || !g) return fail(IRL_ERR_ARG, "null pointer");
+  if (n < 1 || hidden < 1 || n_in < 1) return fail(IRL_ERR_ARG, "bad shape");
+  const int64_t P = (int64_t)hidden * n_in + 2 * (int64_t)hidden + 1;
+  if (ld != irl_padded_ld(P, 0)) return fail(IRL_ERR_ALIGN, "ld must equal irl_padded_ld(P=%lld)", (long long)P);
+  if (!aligned16(xbits) || !aligned16(t) || !aligned16(g) || (hidden & 1))
+    return fail(IRL_ERR_ALIGN, "on-the-fly operands must be 16-byte aligned with an even hidden width");
+  return IRL_OK;
+}
+
+int otf_acc_launch(const OtfPlan& pl, OtfArgs& a, cudaStream_t st) {
+  dim3 grid((unsigned)pl.jc, (unsigned)pl.nb);
+  a.nb = pl.nb;
+  k_otf_acc<<<grid, 256, pl.smem_acc, st>>>(a);
+  return cuda_check(cudaGetLastError(), "otf acc launch");
+}
+
 }  // namespace
 
 // =================================================================== ABI ==
@@ -739,6 +803,94 @@ int irl_mvp_plan(int64_t n, int64_t ld, int is_complex, int mode, int* out_path,
   int g[7] = {p.C, p.W, p.NT, p.R, p.NS, p.nb, p.PPT};
   memcpy(out_geom7, g, sizeof(g));
   return IRL_OK;
+}
+
+size_t irl_otf_workspace_bytes(int64_t n, int n_in, int hidden) {
+  OtfPlan p;
+  if (make_otf_plan(n, n_in, hidden, p) != IRL_OK) return 0;
+  return otf_ws_layout(p, n, hidden, nullptr).bytes;
+}
+
+int irl_otf_prepare_mlp_f64(const uint8_t* x, int64_t n, int n_in, int hidden, const double* theta, uint64_t* xbits,
+                            double* t, double* g, void* stream) {
+  if (!x || !theta || !xbits || !t || !g || n < 1 || n_in < 1 || hidden < 1)
+    return fail(IRL_ERR_ARG, "bad prepare arguments");
+  if (n_in > OTF_MAX_NIN) return fail(IRL_ERR_ARG, "on-the-fly mode supports n_in <= %d", OTF_MAX_NIN);
+  cudaStream_t st = (cudaStream_t)stream;
+  DevInfo d;
+  IRL_TRY(dev_info(d));
+  k_pack_bits<<<(unsigned)std::min<int64_t>(cdiv(n, 256), 4 * d.sms), 256, 0, st>>>(x, n, n_in, xbits);
+  IRL_TRY(cuda_check(cudaGetLastError(), "pack bits launch"));
+  const double* bvec = theta + (size_t)hidden * n_in;
+  return launch_hidden<false, MODEL_MLP>(x, n, n_in, hidden, theta, bvec, bvec + hidden, t, g, st);
+}
+
+int irl_otf_colstats_mlp_f64(const uint64_t* xbits, const double* t, const double* g, int64_t n, int n_in, int hidden,
+                             int64_t ld, const double* w, const double* coeff, double* obar, double* grad,
+                             void* ws, size_t ws_bytes, void* stream) {
+  IRL_TRY(otf_check(xbits, t, g, n, n_in, hidden, ld));
+  if (!w || !coeff || !obar || !grad) return fail(IRL_ERR_ARG, "null pointer");
+  OtfPlan pl;
+  IRL_TRY(make_otf_plan(n, n_in, hidden, pl));
+  OtfWs wl = otf_ws_layout(pl, n, hidden, ws);
+  if (ws_bytes < wl.bytes) return fail(IRL_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, wl.bytes);
+  cudaStream_t st = (cudaStream_t)stream;
+  OtfArgs a{};
+  a.xbits = xbits;
+  a.T = t;
+  a.G = g;
+  a.n_rows = n;
+  a.n_in = n_in;
+  a.hidden = hidden;
+  a.part = wl.part;
+  a.partu = wl.partu;
+  const double* ys[2] = {w, coeff};
+  double* outs[2] = {obar, grad};
+  for (int q = 0; q < 2; ++q) {
+    a.y = ys[q];
+    IRL_TRY(otf_acc_launch(pl, a, st));
+    k_vsum<<<pl.ny, 256, 0, st>>>(ys[q], n, wl.ypart);
+    k_otf_finish<<<(unsigned)cdiv(ld, 256), 256, 0, st>>>(wl.part, wl.partu, pl.nb, hidden, n_in, ld, wl.ypart,
+                                                         pl.ny, nullptr, nullptr, nullptr, nullptr, 0, outs[q],
+                                                         nullptr);
+    IRL_TRY(cuda_check(cudaGetLastError(), "otf colstats launch"));
+  }
+  return IRL_OK;
+}
+
+int irl_otf_mvp_mlp_f64(const uint64_t* xbits, const double* t, const double* g, int64_t n, int n_in, int hidden,
+                        int64_t ld, const double* obar, const double* coeff, const double* v, double* out,
+                        const double* half_f, const double* u0, double* out0, void* ws, size_t ws_bytes,
+                        void* stream) {
+  IRL_TRY(otf_check(xbits, t, g, n, n_in, hidden, ld));
+  if (!coeff || !v || !out) return fail(IRL_ERR_ARG, "null pointer");
+  OtfPlan pl;
+  IRL_TRY(make_otf_plan(n, n_in, hidden, pl));
+  OtfWs wl = otf_ws_layout(pl, n, hidden, ws);
+  if (ws_bytes < wl.bytes) return fail(IRL_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, wl.bytes);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t P = (int64_t)hidden * n_in + 2 * (int64_t)hidden + 1;
+  k_vdot2<<<pl.ny, 256, 0, st>>>(obar, half_f, v, ld, wl.dpart, wl.gpart);
+  OtfArgs a{};
+  a.xbits = xbits;
+  a.T = t;
+  a.G = g;
+  a.n_rows = n;
+  a.n_in = n_in;
+  a.hidden = hidden;
+  a.nb = pl.nb;
+  a.v = v;
+  a.tpart = wl.tpart;
+  a.y = wl.y;
+  a.part = wl.part;
+  a.partu = wl.partu;
+  k_otf_dot<<<dim3((unsigned)pl.jc, (unsigned)pl.nb), 256, pl.smem_dot, st>>>(a);
+  IRL_TRY(cuda_check(cudaGetLastError(), "otf dot launch"));
+  k_otf_y<<<pl.ny, 256, 0, st>>>(wl.tpart, pl.jc, n, coeff, v, P - 1, wl.dpart, obar ? pl.ny : 0, wl.y, wl.ypart);
+  IRL_TRY(otf_acc_launch(pl, a, st));
+  k_otf_finish<<<(unsigned)cdiv(ld, 256), 256, 0, st>>>(wl.part, wl.partu, pl.nb, hidden, n_in, ld, wl.ypart, pl.ny,
+                                                       obar, half_f, u0, wl.gpart, pl.ny, out, out0);
+  return cuda_check(cudaGetLastError(), "otf finish launch");
 }
 
 }  // extern "C"

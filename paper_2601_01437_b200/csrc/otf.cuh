@@ -1,0 +1,413 @@
+// On-the-fly O regeneration for the shallow MLP (K6).
+//
+// O_n = [g_n (x) x_n (h x n_in, j-major), g_n (h), t_n (h), 1] is never stored.
+// The centred product out = O_c^T (c (O_c v)) is regenerated from the 0/1
+// inputs X (bit-packed), T = tanh(W x + b) and G = u (1 - T^2) as two FP64
+// tensor-core GEMMs (mma.sync m8n8k4 f64, SASS DMMA) with fused epilogues:
+//
+//   k_otf_dot : A = X V_W^T (+ v_b)  ->  t_n = sum_j G_nj A_nj + T_nj v_u,j
+//               (the N x h product is reduced with G/T in registers, never stored;
+//                per-j-chunk row partials go to tpart)
+//   k_otf_y   : y_n = c_n (sum_chunks tpart + v_c - Obar.v), fixed order
+//   k_otf_acc : out_W = (G (.) y)^T X, out_b = (G (.) y)^T 1, out_u = (T (.) y)^T 1
+//               (split over row blocks; partials reduced in k_otf_finish)
+//
+// With y = w or y = w (e - E) the same k_otf_acc yields Obar and the gradient
+// (est:167, est:156-163) without ever materialising O.
+#pragma once
+#include "common.cuh"
+
+namespace irl {
+
+constexpr int OTF_BJ = 64;   // hidden units per CTA chunk
+constexpr int OTF_BM = 64;   // rows per tile
+constexpr int OTF_KC = 104;  // k columns of the acc GEMM: n_in (<=100) + ones column, padded to 13 n-tiles
+constexpr int OTF_MAX_NIN = 100;
+constexpr int OTF_XW = 2;    // 64-bit words per packed input row (n_in <= 128)
+
+struct OtfArgs {
+  const uint64_t* xbits;  // [N][OTF_XW]
+  const double* T;        // [N][h]
+  const double* G;        // [N][h]
+  int64_t n_rows;
+  int n_in, hidden;
+  int nb;                 // row blocks
+  // dot
+  const double* v;        // padded parameter vector (MLP layout)
+  double* tpart;          // [JC][N]
+  // acc
+  const double* y;        // [N]
+  double* part;           // [nb][h][OTF_KC]
+  double* partu;          // [nb][h]
+};
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// 0/1 -> 0.0/1.0 without a conversion instruction (1.0 = 0x3FF00000:00000000)
+__device__ __forceinline__ double bit_to_double(uint32_t bit) {
+  return __hiloint2double((int)((0u - bit) & 0x3FF00000u), 0);
+}
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc, bool pred) {
+  const uint32_t d = smem_addr(smem_dst);
+  const int sz = pred ? 16 : 0;  // zero-fill when out of range
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(gsrc), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// x (N x n_in uint8) -> bit-packed rows
+__global__ void k_pack_bits(const uint8_t* __restrict__ x, int64_t n, int n_in, uint64_t* __restrict__ xbits) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t w[OTF_XW] = {0, 0};
+    for (int k = 0; k < n_in; ++k)
+      if (x[r * n_in + k]) w[k >> 6] |= 1ull << (k & 63);
+    for (int q = 0; q < OTF_XW; ++q) xbits[r * OTF_XW + q] = w[q];
+  }
+}
+
+// Tile loader: G/T rows [r0, r0+BM) x columns [j0, j0+BJ) and the packed bits.
+__device__ __forceinline__ void otf_load_tile(const OtfArgs& a, int64_t r0, int64_t hi, int j0, double* gs, double* ts,
+                                              uint64_t* xs, int tid, int nthreads) {
+  // 64 rows x 64 doubles = 512 B per row = 32 x 16 B per row, for G and T
+  for (int e = tid; e < OTF_BM * (OTF_BJ / 2); e += nthreads) {
+    const int r = e / (OTF_BJ / 2), c = (e % (OTF_BJ / 2)) * 2;
+    const int64_t row = r0 + r;
+    const bool ok = row < hi && (j0 + c) < a.hidden;
+    const int64_t off = ok ? row * a.hidden + j0 + c : 0;
+    cp_async16(gs + r * OTF_BJ + c, a.G + off, ok);
+    cp_async16(ts + r * OTF_BJ + c, a.T + off, ok);
+  }
+  for (int e = tid; e < OTF_BM; e += nthreads) {
+    const int64_t row = r0 + e;
+    const bool ok = row < hi;
+    cp_async16(xs + e * OTF_XW, a.xbits + (ok ? row * OTF_XW : 0), ok);
+  }
+}
+
+// grid (JC, nb), 256 threads: t partials for hidden chunk jc over row block
+__global__ void __launch_bounds__(256) k_otf_dot(const OtfArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_o[];
+  double* vw = reinterpret_cast<double*>(smem_o);            // [BJ][OTF_MAX_NIN]
+  double* vb = vw + OTF_BJ * OTF_MAX_NIN;                    // [BJ]
+  double* vu = vb + OTF_BJ;                                  // [BJ]
+  double* gs = vu + OTF_BJ;                                  // [2][BM][BJ]
+  double* ts = gs + 2 * OTF_BM * OTF_BJ;                     // [2][BM][BJ]
+  uint64_t* xs = reinterpret_cast<uint64_t*>(ts + 2 * OTF_BM * OTF_BJ);  // [2][BM][XW]
+  double* red = reinterpret_cast<double*>(xs + 2 * OTF_BM * OTF_XW);     // [4][BM]
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wr = warp >> 2, wj = warp & 3;  // rows [wr*32, +32), j [wj*16, +16)
+  const int jc = blockIdx.x, j0 = jc * OTF_BJ;
+  const int64_t N = a.n_rows;
+  const int64_t lo = (N * blockIdx.y) / a.nb, hi = (N * (blockIdx.y + 1)) / a.nb;
+  const int h = a.hidden, nin = a.n_in;
+  const int64_t offb = (int64_t)h * nin, offu = offb + h;
+
+  // v_W chunk, v_b, v_u (zero beyond h / n_in)
+  for (int e = tid; e < OTF_BJ * OTF_MAX_NIN; e += blockDim.x) {
+    const int jj = e / OTF_MAX_NIN, k = e % OTF_MAX_NIN;
+    vw[e] = (j0 + jj < h && k < nin) ? a.v[(int64_t)(j0 + jj) * nin + k] : 0.0;
+  }
+  for (int e = tid; e < OTF_BJ; e += blockDim.x) {
+    vb[e] = (j0 + e < h) ? a.v[offb + j0 + e] : 0.0;
+    vu[e] = (j0 + e < h) ? a.v[offu + j0 + e] : 0.0;
+  }
+  const int ntiles = (int)((hi - lo + OTF_BM - 1) / OTF_BM);
+  if (ntiles > 0) otf_load_tile(a, lo, hi, j0, gs, ts, xs, tid, blockDim.x);
+  cp_async_commit();
+  const int ksteps = (nin + 3) / 4;
+
+  for (int it = 0; it < ntiles; ++it) {
+    const int buf = it & 1;
+    const int64_t r0 = lo + (int64_t)it * OTF_BM;
+    if (it + 1 < ntiles)
+      otf_load_tile(a, r0 + OTF_BM, hi, j0, gs + (buf ^ 1) * OTF_BM * OTF_BJ, ts + (buf ^ 1) * OTF_BM * OTF_BJ,
+                    xs + (buf ^ 1) * OTF_BM * OTF_XW, tid, blockDim.x);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const double* G = gs + buf * OTF_BM * OTF_BJ;
+    const double* Tt = ts + buf * OTF_BM * OTF_BJ;
+    const uint64_t* X = xs + buf * OTF_BM * OTF_XW;
+
+    // C = v_b (broadcast per column) + X V_W^T
+    double c[4][2][2];
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      const int jl = wj * 16 + nt * 8 + (lane & 3) * 2;
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        c[mt][nt][0] = vb[jl];
+        c[mt][nt][1] = vb[jl + 1];
+      }
+    }
+    uint64_t xr[4][OTF_XW];
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int q = 0; q < OTF_XW; ++q) xr[mt][q] = X[(wr * 32 + mt * 8 + (lane >> 2)) * OTF_XW + q];
+    const double* vrow0 = vw + (wj * 16 + (lane >> 2)) * OTF_MAX_NIN + (lane & 3);
+    for (int kk = 0; kk < ksteps; ++kk) {
+      const int k = kk * 4 + (lane & 3);
+      const double b0 = vrow0[kk * 4];
+      const double b1 = vrow0[kk * 4 + 8 * OTF_MAX_NIN];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        const uint64_t word = (k < 64) ? xr[mt][0] : xr[mt][1];
+        const double av = bit_to_double((uint32_t)(word >> (k & 63)) & 1u);
+        dmma(c[mt][0][0], c[mt][0][1], av, b0);
+        dmma(c[mt][1][0], c[mt][1][1], av, b1);
+      }
+    }
+    // epilogue: row sums of G (.) C + T (.) v_u
+    double rs[4];
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {
+      const int rl = wr * 32 + mt * 8 + (lane >> 2);
+      double s = 0.0;
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const int jl = wj * 16 + nt * 8 + (lane & 3) * 2;
+        const double2 g2 = *reinterpret_cast<const double2*>(G + rl * OTF_BJ + jl);
+        const double2 t2 = *reinterpret_cast<const double2*>(Tt + rl * OTF_BJ + jl);
+        s = fma(g2.x, c[mt][nt][0], s);
+        s = fma(g2.y, c[mt][nt][1], s);
+        s = fma(t2.x, vu[jl], s);
+        s = fma(t2.y, vu[jl + 1], s);
+      }
+      s += __shfl_xor_sync(0xffffffffu, s, 1);
+      s += __shfl_xor_sync(0xffffffffu, s, 2);
+      rs[mt] = s;
+    }
+    if ((lane & 3) == 0) {
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) red[wj * OTF_BM + wr * 32 + mt * 8 + (lane >> 2)] = rs[mt];
+    }
+    __syncthreads();
+    if (tid < OTF_BM) {
+      const int64_t row = r0 + tid;
+      if (row < hi) {
+        const double t = ((red[tid] + red[OTF_BM + tid]) + red[2 * OTF_BM + tid]) + red[3 * OTF_BM + tid];
+        a.tpart[(int64_t)jc * N + row] = t;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// y_n = c_n (sum_jc tpart + v_c - s) ; s, g0 from per-CTA partial dots (fixed order)
+// Y partials per CTA.
+__global__ void __launch_bounds__(256) k_otf_y(const double* __restrict__ tpart, int jc_count, int64_t n,
+                                               const double* __restrict__ coeff, const double* v, int64_t p_last,
+                                               const double* __restrict__ dpart, int n_dpart, double* y,
+                                               double* ypart) {
+  __shared__ double sh[8];
+  double s = 0.0;
+  for (int q = 0; q < n_dpart; ++q) s += dpart[q];
+  const double vc = v[p_last];
+  double acc = 0.0;
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = blockIdx.x * per, hi = min(n, lo + per);
+  for (int64_t r = lo + threadIdx.x; r < hi; r += blockDim.x) {
+    double t = 0.0;
+    for (int q = 0; q < jc_count; ++q) t += tpart[(int64_t)q * n + r];
+    const double yy = coeff[r] * ((t + vc) - s);
+    y[r] = yy;
+    acc += yy;
+  }
+  acc = warp_sum<false>(acc);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += sh[w];
+    ypart[blockIdx.x] = tot;
+  }
+}
+
+// grid (JC, nb), 256 threads (warp w owns hidden units j0 + 8w .. +7):
+// part[blk][j][kc] = sum_rows y g_j x_kc (kc = n_in is the ones column), partu = sum y t_j
+__global__ void __launch_bounds__(256) k_otf_acc(const OtfArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_o[];
+  double* gs = reinterpret_cast<double*>(smem_o);           // [2][BM][BJ]
+  double* ts = gs + 2 * OTF_BM * OTF_BJ;                     // [2][BM][BJ]
+  uint64_t* xs = reinterpret_cast<uint64_t*>(ts + 2 * OTF_BM * OTF_BJ);  // [2][BM][XW]
+  double* ys = reinterpret_cast<double*>(xs + 2 * OTF_BM * OTF_XW);      // [2][BM]
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int jc = blockIdx.x, j0 = jc * OTF_BJ;
+  const int64_t N = a.n_rows;
+  const int64_t lo = (N * blockIdx.y) / a.nb, hi = (N * (blockIdx.y + 1)) / a.nb;
+  const int nin = a.n_in;
+  const int ntiles = (int)((hi - lo + OTF_BM - 1) / OTF_BM);
+
+  auto load_y = [&](int64_t r0, double* dst) {
+    for (int e = tid; e < OTF_BM; e += blockDim.x) dst[e] = (r0 + e < hi) ? a.y[r0 + e] : 0.0;
+  };
+  if (ntiles > 0) {
+    otf_load_tile(a, lo, hi, j0, gs, ts, xs, tid, blockDim.x);
+    load_y(lo, ys);
+  }
+  cp_async_commit();
+
+  double c[13][2];
+  double cu[2] = {0.0, 0.0};
+#pragma unroll
+  for (int nt = 0; nt < 13; ++nt) c[nt][0] = c[nt][1] = 0.0;
+  const int jl = warp * 8 + (lane >> 2);  // A row (hidden unit) of this lane
+  const int sh_base = lane >> 2;          // B column offset within an n-tile
+  const double one_b = (lane >> 2) == 0 ? 1.0 : 0.0;
+
+  for (int it = 0; it < ntiles; ++it) {
+    const int buf = it & 1;
+    const int64_t r0 = lo + (int64_t)it * OTF_BM;
+    if (it + 1 < ntiles) {
+      otf_load_tile(a, r0 + OTF_BM, hi, j0, gs + (buf ^ 1) * OTF_BM * OTF_BJ, ts + (buf ^ 1) * OTF_BM * OTF_BJ,
+                    xs + (buf ^ 1) * OTF_BM * OTF_XW, tid, blockDim.x);
+      load_y(r0 + OTF_BM, ys + (buf ^ 1) * OTF_BM);
+    }
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const double* G = gs + buf * OTF_BM * OTF_BJ;
+    const double* Tt = ts + buf * OTF_BM * OTF_BJ;
+    const uint64_t* X = xs + buf * OTF_BM * OTF_XW;
+    const double* Y = ys + buf * OTF_BM;
+#pragma unroll 2
+    for (int kk = 0; kk < OTF_BM / 4; ++kk) {
+      const int rl = kk * 4 + (lane & 3);
+      const double yv = Y[rl];
+      const double av = G[rl * OTF_BJ + jl] * yv;
+      const double au = Tt[rl * OTF_BJ + jl] * yv;
+      const uint64_t w0 = X[rl * OTF_XW] >> sh_base, w1 = X[rl * OTF_XW + 1] >> sh_base;
+#pragma unroll
+      for (int nt = 0; nt < 13; ++nt) {
+        const int kcol = nt * 8 + sh_base;
+        uint32_t bit;
+        if (nt < 8) {
+          bit = (uint32_t)(w0 >> (nt * 8)) & 1u;
+        } else {
+          bit = (uint32_t)(w1 >> ((nt - 8) * 8)) & 1u;
+        }
+        double bv = bit_to_double(bit);
+        if (nt * 8 + 7 >= nin) bv = (kcol < nin) ? bv : (kcol == nin ? 1.0 : 0.0);
+        dmma(c[nt][0], c[nt][1], av, bv);
+      }
+      dmma(cu[0], cu[1], au, one_b);
+    }
+    __syncthreads();
+  }
+  // partials: C[j][kc] fragment -> part[blk][j][kc]
+  double* pb = a.part + ((int64_t)blockIdx.y * a.hidden + j0 + warp * 8 + (lane >> 2)) * OTF_KC;
+  const bool jok = (j0 + warp * 8 + (lane >> 2)) < a.hidden;
+  if (jok) {
+#pragma unroll
+    for (int nt = 0; nt < 13; ++nt) {
+      const int kc = nt * 8 + (lane & 3) * 2;
+      pb[kc] = c[nt][0];
+      pb[kc + 1] = c[nt][1];
+    }
+    if ((lane & 3) == 0) a.partu[(int64_t)blockIdx.y * a.hidden + j0 + warp * 8 + (lane >> 2)] = cu[0];
+  }
+}
+
+// Assemble the MLP-layout parameter vector from the acc partials:
+//   mode 0 (product): out = sum part - obar * Y (+ u0 hf), out0 = g0
+//   mode 1 (stats)  : out = sum part          (Y, obar unused)
+__global__ void __launch_bounds__(256) k_otf_finish(const double* __restrict__ part, const double* __restrict__ partu,
+                                                    int nb, int hidden, int n_in, int64_t ld,
+                                                    const double* __restrict__ ypart, int n_ypart,
+                                                    const double* __restrict__ obar, const double* hf,
+                                                    const double* u0, const double* dgpart, int n_dgpart,
+                                                    double* out, double* out0) {
+  double Y = 0.0;
+  for (int q = 0; q < n_ypart; ++q) Y += ypart[q];
+  const int64_t hn = (int64_t)hidden * n_in;
+  const int64_t P = hn + 2 * hidden + 1;
+  const double uu = (hf && u0) ? *u0 : 0.0;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < ld; p += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    if (p < hn) {
+      const int64_t j = p / n_in, k = p % n_in;
+      for (int b = 0; b < nb; ++b) acc += part[((int64_t)b * hidden + j) * OTF_KC + k];
+    } else if (p < hn + hidden) {
+      const int64_t j = p - hn;
+      for (int b = 0; b < nb; ++b) acc += part[((int64_t)b * hidden + j) * OTF_KC + n_in];
+    } else if (p < hn + 2 * hidden) {
+      const int64_t j = p - hn - hidden;
+      for (int b = 0; b < nb; ++b) acc += partu[(int64_t)b * hidden + j];
+    } else if (p == P - 1) {
+      acc = Y;
+    }
+    if (p < P) {
+      if (obar) acc = fma(-obar[p], Y, acc);
+      if (hf && u0) acc = fma(uu, hf[p], acc);
+    } else {
+      acc = 0.0;
+    }
+    out[p] = acc;
+  }
+  if (out0 && blockIdx.x == 0 && threadIdx.x == 0) {
+    double g = 0.0;
+    if (hf)
+      for (int q = 0; q < n_dgpart; ++q) g += dgpart[q];
+    *out0 = g;
+  }
+}
+
+// per-CTA partial dots s = obar . v and g0 = hf . v over the padded vector
+__global__ void __launch_bounds__(256) k_vdot2(const double* __restrict__ a1, const double* __restrict__ a2,
+                                               const double* __restrict__ v, int64_t len, double* p1, double* p2) {
+  __shared__ double s1[8], s2[8];
+  double x1 = 0.0, x2 = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x) {
+    const double vi = v[i];
+    if (a1) x1 = fma(a1[i], vi, x1);
+    if (a2) x2 = fma(a2[i], vi, x2);
+  }
+  x1 = warp_sum<false>(x1);
+  x2 = warp_sum<false>(x2);
+  if ((threadIdx.x & 31) == 0) {
+    s1[threadIdx.x >> 5] = x1;
+    s2[threadIdx.x >> 5] = x2;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t1 = 0.0, t2 = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      t1 += s1[w];
+      t2 += s2[w];
+    }
+    p1[blockIdx.x] = t1;
+    p2[blockIdx.x] = t2;
+  }
+}
+
+}  // namespace irl
+
+namespace irl {
+// per-CTA partial sums of y (fixed order)
+__global__ void __launch_bounds__(256) k_vsum(const double* __restrict__ y, int64_t n, double* part) {
+  __shared__ double s[8];
+  double x = 0.0;
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = blockIdx.x * per, hi = min(n, lo + per);
+  for (int64_t r = lo + threadIdx.x; r < hi; r += blockDim.x) x += y[r];
+  x = warp_sum<false>(x);
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s[w];
+    part[blockIdx.x] = t;
+  }
+}
+}  // namespace irl

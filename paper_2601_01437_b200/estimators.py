@@ -82,7 +82,9 @@ class SampleBatch:
 
     def __init__(self, configs, weights, e_loc, o_matrix, n_samples: int = 0, *, kind: str | None = None,
                  param_count: int | None = None, device=None):
-        dev = _device(device if device is not None else (o_matrix.device if isinstance(o_matrix, torch.Tensor) and o_matrix.is_cuda else None))
+        if device is None and isinstance(o_matrix, torch.Tensor) and o_matrix.is_cuda:
+            device = o_matrix.device
+        dev = _device(device)
         is_complex = torch.is_complex(o_matrix) if isinstance(o_matrix, torch.Tensor) else np.iscomplexobj(o_matrix)
         if kind is None:
             kind = KIND_COMPLEX_RAW if is_complex else KIND_REAL
@@ -90,19 +92,13 @@ class SampleBatch:
             raise ValueError(f"unknown batch kind {kind!r}")
         if kind == KIND_REAL and is_complex:
             raise ValueError("complex o_matrix needs kind 'complex_raw' or 'hermitian'")
-        cdt = torch.complex128 if kind != KIND_REAL else torch.float64
         n = len(configs) if configs is not None else int(np.shape(weights)[0])
-        w = _as_tensor(weights, torch.float64, dev).contiguous()
-        e_is_c = torch.is_complex(e_loc) if isinstance(e_loc, torch.Tensor) else np.iscomplexobj(e_loc)
-        if kind == KIND_REAL and e_is_c:
-            raise ValueError("complex e_loc needs a complex batch kind")
-        e = _as_tensor(e_loc, cdt, dev).contiguous()
-        if tuple(w.shape) != (n,) or tuple(e.shape) != (n,):
-            raise ValueError("cache shapes do not match the config list")
         if o_matrix.shape[0] != n:
             raise ValueError("o_matrix rows do not match the config list")
         p = int(param_count) if param_count is not None else int(o_matrix.shape[1])
         ld = _lib.padded_ld(p, kind != KIND_REAL)
+        self._init_common(weights, e_loc, n, n_samples, kind, p, ld, dev)
+        cdt = torch.complex128 if kind != KIND_REAL else torch.float64
         if isinstance(o_matrix, torch.Tensor) and o_matrix.is_cuda and o_matrix.shape[1] == ld:
             o = o_matrix if o_matrix.dtype == cdt else o_matrix.to(cdt)
             if not o.is_contiguous():
@@ -112,15 +108,27 @@ class SampleBatch:
                 raise ValueError("o_matrix width does not match param_count")
             o = torch.zeros((n, ld), dtype=cdt, device=dev)
             o[:, :p] = _as_tensor(o_matrix, cdt, dev)
+        self.configs = tuple(configs) if configs is not None else None
+        self.o_matrix = o
+
+    def _init_common(self, weights, e_loc, n, n_samples, kind, p, ld, dev) -> None:
+        """Weights / E_loc validation of est:44-53 and the device caches."""
+        cdt = torch.complex128 if kind != KIND_REAL else torch.float64
+        w = _as_tensor(weights, torch.float64, dev).contiguous()
+        e_is_c = torch.is_complex(e_loc) if isinstance(e_loc, torch.Tensor) else np.iscomplexobj(e_loc)
+        if kind == KIND_REAL and e_is_c:
+            raise ValueError("complex e_loc needs a complex batch kind")
+        e = _as_tensor(e_loc, cdt, dev).contiguous()
+        if tuple(w.shape) != (n,) or tuple(e.shape) != (n,):
+            raise ValueError("cache shapes do not match the config list")
         # est:50-51 validation (one host sync, once per batch)
         wmin = float(w.min()) if n else 0.0
         wsum = float(w.sum()) if n else 0.0
         if n and (wmin < 0 or abs(wsum - 1.0) > 1e-12):
             raise ValueError("weights must be nonnegative and sum to 1")
-        self.configs = tuple(configs) if configs is not None else None
+        self.configs = None
         self.weights = w
         self.e_loc = e
-        self.o_matrix = o
         self.n_samples = int(n_samples)
         self.kind = kind
         self._p = p
@@ -155,7 +163,10 @@ class SampleBatch:
 
     def mvp_workspace(self) -> torch.Tensor:
         if self._ws is None:
-            nbytes = int(_lib.lib().irl_mvp_workspace_bytes(self.n_rows, self.ld, int(self.is_complex)))
+            if self.otf is not None:
+                nbytes = int(_lib.lib().irl_otf_workspace_bytes(self.n_rows, self.otf["n_in"], self.otf["hidden"]))
+            else:
+                nbytes = int(_lib.lib().irl_mvp_workspace_bytes(self.n_rows, self.ld, int(self.is_complex)))
             self._ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
         return self._ws
 
@@ -216,6 +227,8 @@ class SampleBatch:
             return hit
         c = self.gradient_coefficients(key)
         n = self.n_rows
+        if self.otf is not None:
+            return self._otf_colstats(key, c)
         obar = torch.empty(self.ld, dtype=self.o_matrix.dtype, device=self.device)
         g = torch.empty(self.ld, dtype=self.o_matrix.dtype, device=self.device)
         nbytes = int(_lib.lib().irl_colstats_workspace_bytes(n, self.ld, int(self.is_complex)))
@@ -223,6 +236,21 @@ class SampleBatch:
         fn = "irl_colstats_c128" if self.is_complex else "irl_colstats_f64"
         _lib.call(fn, _lib.ptr(self.o_matrix), n, self.ld, _lib.ptr(self.weights), _lib.ptr(c),
                   _lib.ptr(obar), _lib.ptr(g), _lib.ptr(ws), ws.numel(), self._stream())
+        self._colstats[key] = (obar, g)
+        return obar, g
+
+    # ---- on-the-fly (K6) MLP batches: O is never stored
+    otf = None  # dict(xbits, t, g, n_in, hidden) for on-the-fly batches
+
+    def _otf_colstats(self, key: float, c: torch.Tensor):
+        o = self.otf
+        n = self.n_rows
+        obar = torch.empty(self.ld, dtype=torch.float64, device=self.device)
+        g = torch.empty(self.ld, dtype=torch.float64, device=self.device)
+        ws = self.mvp_workspace()
+        _lib.call("irl_otf_colstats_mlp_f64", _lib.ptr(o["xbits"]), _lib.ptr(o["t"]), _lib.ptr(o["g"]), n,
+                  o["n_in"], o["hidden"], self.ld, _lib.ptr(self.weights), _lib.ptr(c), _lib.ptr(obar), _lib.ptr(g),
+                  _lib.ptr(ws), ws.numel(), self._stream())
         self._colstats[key] = (obar, g)
         return obar, g
 
@@ -285,6 +313,12 @@ def _apply(batch: SampleBatch, coeff: torch.Tensor, v: torch.Tensor, out: torch.
     stream = batch._stream()
     ws = batch.mvp_workspace()
     n = batch.n_rows
+    if batch.otf is not None:
+        o = batch.otf
+        _lib.call("irl_otf_mvp_mlp_f64", _lib.ptr(o["xbits"]), _lib.ptr(o["t"]), _lib.ptr(o["g"]), n, o["n_in"],
+                  o["hidden"], batch.ld, _lib.ptr(obar), _lib.ptr(coeff), _lib.ptr(v), _lib.ptr(out),
+                  _lib.ptr(half_f), _lib.ptr(u0), _lib.ptr(out0), _lib.ptr(ws), ws.numel(), stream)
+        return
     if not batch.is_complex:
         _lib.call("irl_mvp_f64", _lib.ptr(batch.o_matrix), n, batch.param_count, batch.ld, _lib.ptr(obar),
                   _lib.ptr(coeff), _lib.ptr(v), _lib.ptr(out), _lib.ptr(half_f), _lib.ptr(u0), _lib.ptr(out0),

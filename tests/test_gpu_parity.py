@@ -300,3 +300,39 @@ def test_graph_sweeper_restarts_and_breakdown(pkg):
     ident = Op(torch.eye(40, dtype=torch.float64, device=dev))
     p2 = krylov.irl_smallest(ident, 40, seed=2, device=dev)
     assert abs(p2.value - 1.0) < 1e-12 and p2.n_matvec <= 5
+
+
+@pytest.mark.parametrize("rows,n_in,hidden", [(300, 20, 64), (257, 100, 130), (1024, 100, 2048)])
+def test_otf_mlp_matches_stored(pkg, rows, n_in, hidden):
+    """On-the-fly (K6, DMMA) products, stats and IRL == stored-O batch and oracle."""
+    from paper_2601_01437_b200 import ansatz as A, estimators as E, optimizer as OPT
+
+    rng = np.random.default_rng(rows + n_in)
+    x = np.zeros((rows, n_in), dtype=np.uint8)
+    occ = np.argsort(rng.random((rows, n_in)), axis=1)[:, : n_in // 2]
+    x[np.arange(rows)[:, None], occ] = 1
+    arch = A.MLPArchitecture(n_in, hidden)
+    P = arch.param_count
+    theta = np.concatenate([rng.normal(0, np.sqrt(1 / n_in), hidden * n_in + hidden),
+                            rng.normal(0, np.sqrt(1 / hidden), hidden + 1)])
+    e = rng.normal(-10.0, 0.1, rows)
+    params = A.AnsatzParameters(arch, theta)
+    stored = A.build_batch(params, x, e)
+    otf = A.build_batch_otf(params, x, e)
+    es, eo = E.estimate_energy(stored), E.estimate_energy(otf)
+    assert eo.mean == es.mean
+    assert rel(host(E.energy_gradient(otf, eo)), host(E.energy_gradient(stored, es))) < 1e-12
+    assert rel(host(otf.obar()[:P]), host(stored.obar()[:P])) < 1e-13
+    o = nqs.mlp_rows(theta, x, n_in, hidden)
+    w = np.full(rows, 1.0 / rows)
+    for k in range(2):
+        v = rng.standard_normal(P)
+        ref = oest.heff(w, e, o, es.mean, v)
+        assert rel(E.heff_matvec(otf, eo, v), ref) < PROD_TOL
+        assert rel(E.qgt_matvec(otf, v), oest.qgt(w, o, v)) < PROD_TOL
+    conf = OPT.OptimizerConfig(m=20, max_restarts=3)
+    r1 = OPT.solve_step(stored, conf, seed=9)
+    r2 = OPT.solve_step(otf, conf, seed=9)
+    assert r1.n_matvec == r2.n_matvec
+    assert abs(r1.lambda_min - r2.lambda_min) <= RITZ_TOL * abs(r1.lambda_min)
+    assert rel(host(r2.direction), host(r1.direction)) < DIR_TOL

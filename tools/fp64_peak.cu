@@ -1,0 +1,60 @@
+// FP64 throughput microbenchmark on the GPU box: DFMA (CUDA cores) vs DMMA
+// (mma.sync m8n8k4 f64 tensor path).  Development tool.
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__global__ void k_dfma(double* out, int iters) {
+  double a0 = threadIdx.x, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5, a6 = a0 + 6, a7 = a0 + 7;
+  const double b = 1.0000001, c = 0.999999;
+  for (int i = 0; i < iters; ++i) {
+    a0 = fma(a0, b, c); a1 = fma(a1, b, c); a2 = fma(a2, b, c); a3 = fma(a3, b, c);
+    a4 = fma(a4, b, c); a5 = fma(a5, b, c); a6 = fma(a6, b, c); a7 = fma(a7, b, c);
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+}
+
+__global__ void k_dmma(double* out, int iters) {
+  double a = threadIdx.x * 1e-3, b = 1.0 + threadIdx.x * 1e-4;
+  double c[8][2];
+  for (int t = 0; t < 8; ++t) c[t][0] = c[t][1] = 0.0;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int t = 0; t < 8; ++t)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                   : "+d"(c[t][0]), "+d"(c[t][1]) : "d"(a), "d"(b));
+  }
+  double s = 0;
+  for (int t = 0; t < 8; ++t) s += c[t][0] + c[t][1];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+int main() {
+  int sms;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  double* out;
+  cudaMalloc(&out, sizeof(double) * sms * 8 * 1024);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  for (int threads : {256, 512, 1024}) {
+    const int iters = 20000;
+    k_dfma<<<sms * 2, threads>>>(out, 100);
+    cudaEventRecord(e0);
+    k_dfma<<<sms * 2, threads>>>(out, iters);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    double flops = 2.0 * 8 * iters * (double)threads * sms * 2;
+    printf("DFMA threads=%d: %.2f TFLOP/s\n", threads, flops / ms / 1e9);
+    k_dmma<<<sms * 2, threads>>>(out, 100);
+    cudaEventRecord(e0);
+    k_dmma<<<sms * 2, threads>>>(out, iters / 4);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+    flops = 2.0 * 256 * 8 * (iters / 4) * (double)(threads / 32) * sms * 2;
+    printf("DMMA threads=%d: %.2f TFLOP/s  (%s)\n", threads, flops / ms / 1e9, cudaGetErrorString(cudaGetLastError()));
+  }
+  return 0;
+}
