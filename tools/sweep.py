@@ -40,6 +40,7 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--rows", type=int, default=0)
     ap.add_argument("--irl", type=int, default=1)
+    ap.add_argument("--otf", type=int, default=0, help="MLP configs in on-the-fly mode (O not stored)")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     dev = torch.device("cuda", 0)
@@ -54,6 +55,38 @@ def main():
         arch = (A.RBMArchitecture(cfg.n_inputs, cfg.hidden, cfg.complex_params) if cfg.model == "rbm"
                 else A.MLPArchitecture(cfg.n_inputs, cfg.hidden))
         params = A.AnsatzParameters(arch, inp.theta)
+        if args.otf and cfg.model == "mlp":
+            t0 = time.perf_counter()
+            batch = A.build_batch_otf(params, inp.x, inp.e_loc)
+            en = E.estimate_energy(batch)
+            batch.obar()
+            torch.cuda.synchronize()
+            prep = (time.perf_counter() - t0) * 1e3
+            P, ld = batch.param_count, batch.ld
+            coeff = batch.coefficients(en.mean)
+            vin = torch.randn(ld, dtype=torch.float64, device=dev)
+            vin[P:] = 0
+            vout = torch.empty(ld, dtype=torch.float64, device=dev)
+            E._apply(batch, coeff, vin, vout)
+            torch.cuda.synchronize()
+            ms = timed(lambda: E._apply(batch, coeff, vin, vout), args.reps)
+            med = statistics.median(ms)
+            flops = 2.0 * batch.n_rows * cfg.hidden * (cfg.n_inputs + 104)
+            out = {"config": cfg.name + "-otf", "prepare_ms": prep, "otf": {"ms": med, "mvp_s": 1e3 / med,
+                   "tflops": flops / (med / 1e3) / 1e12}}
+            if args.irl:
+                conf = OPT.OptimizerConfig(m=cfg.m, max_restarts=cfg.max_restarts)
+                OPT.solve_step(batch, conf, seed=cfg.lanczos_seed, energy=en)
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                res = OPT.solve_step(batch, conf, seed=cfg.lanczos_seed, energy=en)
+                torch.cuda.synchronize()
+                out["irl"] = {"wall_ms": (time.perf_counter() - t0) * 1e3, "n_matvec": res.n_matvec,
+                              "lambda": res.lambda_min, "converged": res.converged}
+            print(json.dumps(out), flush=True)
+            del batch
+            torch.cuda.empty_cache()
+            continue
         batch = A.build_batch(params, inp.x, inp.e_loc)
         torch.cuda.synchronize()
         # warm O-build time: refill the same buffers
