@@ -472,6 +472,7 @@ int colstats_impl(bool cplx, const double* O, int64_t n, int64_t ld, const doubl
 // ------------------------------------------------------------ obuild ----
 struct OPlan {
   int C, W, PPT, NT, nb;
+  size_t smem;
   void (*fn)(ORowArgs);
 };
 
@@ -503,6 +504,7 @@ int make_oplan(int64_t ld_u, bool cplx, int model, OPlan& p) {
         p.fn = pick_orows<true, MODEL_RBM>(ppt);
       else
         p.fn = model == MODEL_RBM ? pick_orows<false, MODEL_RBM>(ppt) : pick_orows<false, MODEL_MLP>(ppt);
+      p.smem = 0;  // set by the caller (depends on n_vis, hidden)
       int occ = 0;
       IRL_TRY(cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)p.fn, p.NT, 0), "occ"));
       occ = std::max(occ, 1);
@@ -547,6 +549,7 @@ int obuild_impl(bool cplx, int model, const uint8_t* x, int64_t n, int n_vis, in
                                        : (int64_t)hidden * n_vis + 2 * (int64_t)hidden + 1;
   if (ld != irl_padded_ld(P, cplx)) return fail(IRL_ERR_ALIGN, "ld must equal irl_padded_ld(P=%lld)", (long long)P);
   if (!aligned16(O) || !aligned16(obar) || !aligned16(g) || !aligned16(ws)) return fail(IRL_ERR_ALIGN, "alignment");
+  if (!cplx && (hidden & 1)) return fail(IRL_ERR_ALIGN, "real models need an even hidden width (16-B row staging)");
   const int64_t ld_u = cplx ? ld : ld / 2;
   OPlan p;
   IRL_TRY(make_oplan(ld_u, cplx, model, p));
@@ -594,7 +597,15 @@ int obuild_impl(bool cplx, int model, const uint8_t* x, int64_t n, int n_vis, in
   a.W = p.W;
   a.C = p.C;
   a.nb = p.nb;
-  p.fn<<<(unsigned)(p.nb * p.C), p.NT, 0, st>>>(a);
+  const int tab_len = model == MODEL_MLP ? orow_tab_len<MODEL_MLP>(n_vis, hidden) : orow_tab_len<MODEL_RBM>(n_vis, hidden);
+  const size_t smem = (size_t)2 * ((tab_len + 1) & ~1) * sS;
+  {
+    DevInfo d;
+    IRL_TRY(dev_info(d));
+    if (smem > (size_t)d.smem_optin) return fail(IRL_ERR_ARG, "hidden layer too wide for the row table");
+    IRL_TRY(ensure_fn_attrs((const void*)p.fn, d.smem_optin));
+  }
+  p.fn<<<(unsigned)(p.nb * p.C), p.NT, smem, st>>>(a);
   IRL_TRY(cuda_check(cudaGetLastError(), "orows launch"));
   const unsigned blocks = (unsigned)cdiv(ld_u, 32);
   if (cplx)

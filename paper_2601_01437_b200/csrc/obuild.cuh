@@ -105,103 +105,125 @@ struct ORowArgs {
   int W, C, nb;
 };
 
-// element descriptor: kind<<28 | j<<12 | i
-enum { EK_PAD = 0, EK_X = 1, EK_T = 2, EK_TX = 3, EK_GX = 4, EK_G = 5, EK_ONE = 6 };
-
+// Per-row factor table (S-typed, in shared memory):
+//   [0] = 0, [1] = 1, [2, 2+h) = t_n, [2+h, 2+2h) = g_n (MLP), then x_n (0/1).
+// Every element of O_n is tab[ia] * tab[ib] with (ia, ib) fixed per column:
+//   RBM  x_i -> (x_i, 1)   t_j -> (t_j, 1)   t_j x_i -> (t_j, x_i)
+//   MLP  g_j x_k -> (g_j, x_k)   g_j -> (g_j, 1)   t_j -> (t_j, 1)   1 -> (1, 1)
+//   padding -> (0, 1)
+// so the row writer is one multiply per element, no per-element branching.
 template <int MODEL>
-__device__ __forceinline__ uint32_t elem_desc(int64_t p, int n, int h, int64_t P) {
-  if (p >= P) return 0u;
-  uint32_t kind, j = 0, i = 0;
-  if constexpr (MODEL == MODEL_RBM) {
-    if (p < n) {
-      kind = EK_X;
-      i = (uint32_t)p;
-    } else if (p < n + h) {
-      kind = EK_T;
-      j = (uint32_t)(p - n);
-    } else {
-      const int64_t q = p - n - h;
-      kind = EK_TX;
-      j = (uint32_t)(q / n);
-      i = (uint32_t)(q % n);
-    }
-  } else {
-    const int64_t hn = (int64_t)h * n;
-    if (p < hn) {
-      kind = EK_GX;
-      j = (uint32_t)(p / n);
-      i = (uint32_t)(p % n);
-    } else if (p < hn + h) {
-      kind = EK_G;
-      j = (uint32_t)(p - hn);
-    } else if (p < hn + 2 * h) {
-      kind = EK_T;
-      j = (uint32_t)(p - hn - h);
-    } else {
-      kind = EK_ONE;
-    }
-  }
-  return (kind << 28) | (j << 12) | i;
+__host__ __device__ __forceinline__ int orow_tab_len(int n, int h) {
+  return 2 + h * (MODEL == MODEL_MLP ? 2 : 1) + n;
 }
 
-template <bool CPLX>
-__device__ __forceinline__ typename Traits<CPLX>::S elem_value(uint32_t d, const uint8_t* xr,
-                                                               const typename Traits<CPLX>::S* Tr,
-                                                               const double* Gr) {
-  using S = typename Traits<CPLX>::S;
-  const uint32_t kind = d >> 28, j = (d >> 12) & 0xffffu, i = d & 0xfffu;
-  double xv = 0.0;
-  if (kind == EK_X || kind == EK_TX || kind == EK_GX) xv = xr[i] ? 1.0 : 0.0;
-  if constexpr (CPLX) {
-    S t = (kind == EK_T || kind == EK_TX) ? Tr[j] : make_double2(0.0, 0.0);
-    switch (kind) {
-      case EK_X: return make_double2(xv, 0.0);
-      case EK_T: return t;
-      case EK_TX: return make_double2(t.x * xv, t.y * xv);
-      default: return make_double2(0.0, 0.0);
-    }
-  } else {
-    switch (kind) {
-      case EK_X: return xv;
-      case EK_T: return Tr[j];
-      case EK_TX: return Tr[j] * xv;
-      case EK_GX: return Gr[j] * xv;
-      case EK_G: return Gr[j];
-      case EK_ONE: return 1.0;
-      default: return 0.0;
+template <int MODEL>
+__device__ __forceinline__ uint32_t elem_pair(int64_t p, int n, int h, int64_t P) {
+  const int OT = 2, OG = 2 + h, OX = 2 + h * (MODEL == MODEL_MLP ? 2 : 1);
+  uint32_t ia = 0, ib = 1;
+  if (p < P) {
+    if constexpr (MODEL == MODEL_RBM) {
+      if (p < n) {
+        ia = OX + (uint32_t)p;
+      } else if (p < n + h) {
+        ia = OT + (uint32_t)(p - n);
+      } else {
+        const int64_t q = p - n - h;
+        ia = OT + (uint32_t)(q / n);
+        ib = OX + (uint32_t)(q % n);
+      }
+    } else {
+      const int64_t hn = (int64_t)h * n;
+      if (p < hn) {
+        ia = OG + (uint32_t)(p / n);
+        ib = OX + (uint32_t)(p % n);
+      } else if (p < hn + h) {
+        ia = OG + (uint32_t)(p - hn);
+      } else if (p < hn + 2 * h) {
+        ia = OT + (uint32_t)(p - hn - h);
+      } else {
+        ia = 1;
+      }
     }
   }
+  return (ia << 16) | ib;
+}
+
+// stage the factor table of row n into tab (cp.async for t/g, direct for x)
+template <bool CPLX, int MODEL>
+__device__ __forceinline__ void orow_stage(const ORowArgs& a, int64_t n, typename Traits<CPLX>::S* tab, int tid,
+                                           int nthreads) {
+  using S = typename Traits<CPLX>::S;
+  const int h = a.hidden, nv = a.n_vis;
+  const int OX = 2 + h * (MODEL == MODEL_MLP ? 2 : 1);
+  const char* trow = reinterpret_cast<const char*>(a.T) + (size_t)n * h * sizeof(S);
+  const int tchunks = (int)((size_t)h * sizeof(S) / 16);
+  for (int c = tid; c < tchunks; c += nthreads) {
+    const uint32_t d = smem_addr(reinterpret_cast<char*>(tab + 2) + 16 * c);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(trow + 16 * c) : "memory");
+  }
+  if constexpr (MODEL == MODEL_MLP) {
+    const char* grow = reinterpret_cast<const char*>(a.G + (size_t)n * h);
+    for (int c = tid; c < h / 2; c += nthreads) {
+      const uint32_t d = smem_addr(reinterpret_cast<char*>(tab + 2 + h) + 16 * c);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(grow + 16 * c) : "memory");
+    }
+  }
+  for (int i = tid; i < nv; i += nthreads) {
+    const double xv = a.x[n * nv + i] ? 1.0 : 0.0;
+    if constexpr (CPLX) tab[OX + i] = make_double2(xv, 0.0); else tab[OX + i] = xv;
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
 template <bool CPLX, int MODEL, int PPT>
 __global__ void __launch_bounds__(512) k_orows(const ORowArgs a) {
   using T = Traits<CPLX>;
   using S = typename T::S;
+  extern __shared__ __align__(16) unsigned char smem_r[];
   const int NT = blockDim.x;
   const int tid = threadIdx.x;
   const int rank = blockIdx.x % a.C, blk = blockIdx.x / a.C;
   const int64_t lo = (a.n_rows * blk) / a.nb, hi = (a.n_rows * (blk + 1)) / a.nb;
   const int64_t col0 = (int64_t)rank * a.W;
   constexpr int E = Traits<CPLX>::kElemsPerUnit;
+  const int TL = (orow_tab_len<MODEL>(a.n_vis, a.hidden) + 1) & ~1;
+  S* tabs = reinterpret_cast<S*>(smem_r);  // [2][TL]
 
-  uint32_t desc[PPT][E];
+  uint32_t pr[PPT][E];
   double2 acc0[PPT], acc1[PPT];
 #pragma unroll
   for (int k = 0; k < PPT; ++k) {
     const int idx = tid + k * NT;
     const int64_t u = col0 + idx;
 #pragma unroll
-    for (int e = 0; e < E; ++e)
-      desc[k][e] = (idx < a.W) ? elem_desc<MODEL>(u * E + e, a.n_vis, a.hidden, a.p) : 0u;
+    for (int e = 0; e < E; ++e) pr[k][e] = (idx < a.W) ? elem_pair<MODEL>(u * E + e, a.n_vis, a.hidden, a.p) : 1u;
     acc0[k] = make_double2(0.0, 0.0);
     acc1[k] = make_double2(0.0, 0.0);
   }
-  const S* Tm = reinterpret_cast<const S*>(a.T);
+  for (int b = 0; b < 2; ++b) {
+    if (tid == 0) {
+      if constexpr (CPLX) {
+        tabs[b * TL] = make_double2(0.0, 0.0);
+        tabs[b * TL + 1] = make_double2(1.0, 0.0);
+      } else {
+        tabs[b * TL] = 0.0;
+        tabs[b * TL + 1] = 1.0;
+      }
+    }
+  }
   const S* cf = reinterpret_cast<const S*>(a.coeff);
+  if (lo < hi) orow_stage<CPLX, MODEL>(a, lo, tabs, tid, NT);
   for (int64_t n = lo; n < hi; ++n) {
-    const uint8_t* xr = a.x + n * a.n_vis;
-    const S* Tr = Tm + n * a.hidden;
-    const double* Gr = (MODEL == MODEL_MLP) ? a.G + n * a.hidden : nullptr;
+    const int buf = (int)((n - lo) & 1);
+    if (n + 1 < hi) {
+      orow_stage<CPLX, MODEL>(a, n + 1, tabs + (buf ^ 1) * TL, tid, NT);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const S* tab = tabs + buf * TL;
     const double wn = __ldg(a.w + n);
     const S cn = cf[n];
     double2* orow = a.O + n * a.ld_u + col0;
@@ -211,14 +233,13 @@ __global__ void __launch_bounds__(512) k_orows(const ORowArgs a) {
       if (idx < a.W) {
         double2 u;
         if constexpr (CPLX) {
-          u = elem_value<true>(desc[k][0], xr, Tr, Gr);
-          // acc0 += w conj(O) ; acc1 += conj(O) c
+          u = T::mul(tab[pr[k][0] >> 16], tab[pr[k][0] & 0xffffu]);
           acc0[k].x = fma(wn, u.x, acc0[k].x);
           acc0[k].y = fma(-wn, u.y, acc0[k].y);
           T::axpy(acc1[k], u, cn);
         } else {
-          u.x = elem_value<false>(desc[k][0], xr, Tr, Gr);
-          u.y = elem_value<false>(desc[k][1], xr, Tr, Gr);
+          u.x = tab[pr[k][0] >> 16] * tab[pr[k][0] & 0xffffu];
+          u.y = tab[pr[k][1] >> 16] * tab[pr[k][1] & 0xffffu];
           acc0[k].x = fma(wn, u.x, acc0[k].x);
           acc0[k].y = fma(wn, u.y, acc0[k].y);
           acc1[k].x = fma(cn, u.x, acc1[k].x);
@@ -227,6 +248,7 @@ __global__ void __launch_bounds__(512) k_orows(const ORowArgs a) {
         st_stream(orow + idx, u);
       }
     }
+    __syncthreads();  // buffer `buf` is restaged two rows later
   }
 #pragma unroll
   for (int k = 0; k < PPT; ++k) {
