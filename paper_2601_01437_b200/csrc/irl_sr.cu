@@ -489,14 +489,15 @@ void (*pick_orows(int ppt))(ORowArgs) {
 int make_oplan(int64_t ld_u, bool cplx, int model, OPlan& p) {
   DevInfo d;
   IRL_TRY(dev_info(d));
-  for (int C = 1; C <= 4096; C *= 2) {
-    if (ld_u % C) continue;
-    const int64_t W = ld_u / C;
-    for (int ppt : {1, 2, 4, 8}) {
+  // write-bound: prefer few units per thread (low registers, several CTAs per
+  // SM with independent row barriers); column tiles may be uneven
+  for (int ppt : {2, 4, 8}) {
+    for (int64_t C = std::max<int64_t>(1, cdiv(ld_u, (int64_t)512 * ppt)); C <= 4096; ++C) {
+      const int64_t W = cdiv(ld_u, C);
       int64_t nt = rup(cdiv(W, ppt), 32);
       if (nt > 512) continue;
-      if (nt < 32) nt = 32;
-      p.C = C;
+      if (nt < 64) nt = 64;
+      p.C = (int)C;
       p.W = (int)W;
       p.PPT = ppt;
       p.NT = (int)nt;
@@ -504,11 +505,11 @@ int make_oplan(int64_t ld_u, bool cplx, int model, OPlan& p) {
         p.fn = pick_orows<true, MODEL_RBM>(ppt);
       else
         p.fn = model == MODEL_RBM ? pick_orows<false, MODEL_RBM>(ppt) : pick_orows<false, MODEL_MLP>(ppt);
-      p.smem = 0;  // set by the caller (depends on n_vis, hidden)
+      p.smem = 0;
       int occ = 0;
       IRL_TRY(cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)p.fn, p.NT, 0), "occ"));
       occ = std::max(occ, 1);
-      p.nb = std::max(1, (d.sms * occ) / C);
+      p.nb = std::max(1, (int)((d.sms * occ + C - 1) / C));
       return IRL_OK;
     }
   }
@@ -549,7 +550,6 @@ int obuild_impl(bool cplx, int model, const uint8_t* x, int64_t n, int n_vis, in
                                        : (int64_t)hidden * n_vis + 2 * (int64_t)hidden + 1;
   if (ld != irl_padded_ld(P, cplx)) return fail(IRL_ERR_ALIGN, "ld must equal irl_padded_ld(P=%lld)", (long long)P);
   if (!aligned16(O) || !aligned16(obar) || !aligned16(g) || !aligned16(ws)) return fail(IRL_ERR_ALIGN, "alignment");
-  if (!cplx && (hidden & 1)) return fail(IRL_ERR_ALIGN, "real models need an even hidden width (16-B row staging)");
   const int64_t ld_u = cplx ? ld : ld / 2;
   OPlan p;
   IRL_TRY(make_oplan(ld_u, cplx, model, p));

@@ -156,18 +156,25 @@ __device__ __forceinline__ void orow_stage(const ORowArgs& a, int64_t n, typenam
   using S = typename Traits<CPLX>::S;
   const int h = a.hidden, nv = a.n_vis;
   const int OX = 2 + h * (MODEL == MODEL_MLP ? 2 : 1);
-  const char* trow = reinterpret_cast<const char*>(a.T) + (size_t)n * h * sizeof(S);
-  const int tchunks = (int)((size_t)h * sizeof(S) / 16);
-  for (int c = tid; c < tchunks; c += nthreads) {
-    const uint32_t d = smem_addr(reinterpret_cast<char*>(tab + 2) + 16 * c);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(trow + 16 * c) : "memory");
-  }
-  if constexpr (MODEL == MODEL_MLP) {
-    const char* grow = reinterpret_cast<const char*>(a.G + (size_t)n * h);
-    for (int c = tid; c < h / 2; c += nthreads) {
-      const uint32_t d = smem_addr(reinterpret_cast<char*>(tab + 2 + h) + 16 * c);
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(grow + 16 * c) : "memory");
+  const S* trow = reinterpret_cast<const S*>(a.T) + (size_t)n * h;
+  if (CPLX || (h & 1) == 0) {  // rows 16-B aligned: async copy
+    const int tchunks = (int)((size_t)h * sizeof(S) / 16);
+    for (int c = tid; c < tchunks; c += nthreads) {
+      const uint32_t d = smem_addr(reinterpret_cast<char*>(tab + 2) + 16 * c);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(reinterpret_cast<const char*>(trow) + 16 * c)
+                   : "memory");
     }
+    if constexpr (MODEL == MODEL_MLP) {
+      const char* grow = reinterpret_cast<const char*>(a.G + (size_t)n * h);
+      for (int c = tid; c < h / 2; c += nthreads) {
+        const uint32_t d = smem_addr(reinterpret_cast<char*>(tab + 2 + h) + 16 * c);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(grow + 16 * c) : "memory");
+      }
+    }
+  } else {  // odd hidden width (real): plain loads
+    for (int j = tid; j < h; j += nthreads) tab[2 + j] = trow[j];
+    if constexpr (MODEL == MODEL_MLP)
+      for (int j = tid; j < h; j += nthreads) tab[2 + h + j] = a.G[(size_t)n * h + j];
   }
   for (int i = tid; i < nv; i += nthreads) {
     const double xv = a.x[n * nv + i] ? 1.0 : 0.0;
@@ -185,7 +192,8 @@ __global__ void __launch_bounds__(512) k_orows(const ORowArgs a) {
   const int tid = threadIdx.x;
   const int rank = blockIdx.x % a.C, blk = blockIdx.x / a.C;
   const int64_t lo = (a.n_rows * blk) / a.nb, hi = (a.n_rows * (blk + 1)) / a.nb;
-  const int64_t col0 = (int64_t)rank * a.W;
+  const int64_t col0 = (a.ld_u * rank) / a.C;  // uneven split: any tile count
+  const int W = (int)((a.ld_u * (rank + 1)) / a.C - col0);
   constexpr int E = Traits<CPLX>::kElemsPerUnit;
   const int TL = (orow_tab_len<MODEL>(a.n_vis, a.hidden) + 1) & ~1;
   S* tabs = reinterpret_cast<S*>(smem_r);  // [2][TL]
@@ -197,7 +205,7 @@ __global__ void __launch_bounds__(512) k_orows(const ORowArgs a) {
     const int idx = tid + k * NT;
     const int64_t u = col0 + idx;
 #pragma unroll
-    for (int e = 0; e < E; ++e) pr[k][e] = (idx < a.W) ? elem_pair<MODEL>(u * E + e, a.n_vis, a.hidden, a.p) : 1u;
+    for (int e = 0; e < E; ++e) pr[k][e] = (idx < W) ? elem_pair<MODEL>(u * E + e, a.n_vis, a.hidden, a.p) : 1u;
     acc0[k] = make_double2(0.0, 0.0);
     acc1[k] = make_double2(0.0, 0.0);
   }
@@ -230,7 +238,7 @@ __global__ void __launch_bounds__(512) k_orows(const ORowArgs a) {
 #pragma unroll
     for (int k = 0; k < PPT; ++k) {
       const int idx = tid + k * NT;
-      if (idx < a.W) {
+      if (idx < W) {
         double2 u;
         if constexpr (CPLX) {
           u = T::mul(tab[pr[k][0] >> 16], tab[pr[k][0] & 0xffffu]);
@@ -253,7 +261,7 @@ __global__ void __launch_bounds__(512) k_orows(const ORowArgs a) {
 #pragma unroll
   for (int k = 0; k < PPT; ++k) {
     const int idx = tid + k * NT;
-    if (idx < a.W) {
+    if (idx < W) {
       a.part0[(int64_t)blk * a.ld_u + col0 + idx] = acc0[k];
       a.part1[(int64_t)blk * a.ld_u + col0 + idx] = acc1[k];
     }
