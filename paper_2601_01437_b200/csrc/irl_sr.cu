@@ -473,11 +473,11 @@ int colstats_impl(bool cplx, const double* O, int64_t n, int64_t ld, const doubl
 struct OPlan {
   int C, W, PPT, NT, nb;
   size_t smem;
-  void (*fn)(ORowArgs);
+  void (*fn)(ORowArgs, int);
 };
 
 template <bool CPLX, int MODEL>
-void (*pick_orows(int ppt))(ORowArgs) {
+void (*pick_orows(int ppt))(ORowArgs, int) {
   switch (ppt) {
     case 1: return k_orows<CPLX, MODEL, 1>;
     case 2: return k_orows<CPLX, MODEL, 2>;
@@ -491,8 +491,8 @@ int make_oplan(int64_t ld_u, bool cplx, int model, OPlan& p) {
   IRL_TRY(dev_info(d));
   // write-bound: prefer few units per thread (low registers, several CTAs per
   // SM with independent row barriers); column tiles may be uneven
-  for (int ppt : {2, 4, 8}) {
-    for (int64_t C = std::max<int64_t>(1, cdiv(ld_u, (int64_t)512 * ppt)); C <= 4096; ++C) {
+  for (int64_t C = 1; C <= 4096; ++C) {
+    for (int ppt : {1, 2, 4, 8}) {
       const int64_t W = cdiv(ld_u, C);
       int64_t nt = rup(cdiv(W, ppt), 32);
       if (nt > 512) continue;
@@ -598,14 +598,17 @@ int obuild_impl(bool cplx, int model, const uint8_t* x, int64_t n, int n_vis, in
   a.C = p.C;
   a.nb = p.nb;
   const int tab_len = model == MODEL_MLP ? orow_tab_len<MODEL_MLP>(n_vis, hidden) : orow_tab_len<MODEL_RBM>(n_vis, hidden);
-  const size_t smem = (size_t)2 * ((tab_len + 1) & ~1) * sS;
+  const size_t tab_bytes = (size_t)((tab_len + 1) & ~1) * sS;
+  // rows per staging group: amortise the per-group barrier, ~48 KB of tables
+  const int R = (int)std::max<size_t>(1, std::min<size_t>(8, (size_t)(24 * 1024) / tab_bytes));
+  const size_t smem = 2 * (size_t)R * tab_bytes;
   {
     DevInfo d;
     IRL_TRY(dev_info(d));
     if (smem > (size_t)d.smem_optin) return fail(IRL_ERR_ARG, "hidden layer too wide for the row table");
     IRL_TRY(ensure_fn_attrs((const void*)p.fn, d.smem_optin));
   }
-  p.fn<<<(unsigned)(p.nb * p.C), p.NT, smem, st>>>(a);
+  p.fn<<<(unsigned)(p.nb * p.C), p.NT, smem, st>>>(a, R);
   IRL_TRY(cuda_check(cudaGetLastError(), "orows launch"));
   const unsigned blocks = (unsigned)cdiv(ld_u, 32);
   if (cplx)

@@ -180,11 +180,10 @@ __device__ __forceinline__ void orow_stage(const ORowArgs& a, int64_t n, typenam
     const double xv = a.x[n * nv + i] ? 1.0 : 0.0;
     if constexpr (CPLX) tab[OX + i] = make_double2(xv, 0.0); else tab[OX + i] = xv;
   }
-  asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
 template <bool CPLX, int MODEL, int PPT>
-__global__ void __launch_bounds__(512) k_orows(const ORowArgs a) {
+__global__ void __launch_bounds__(512) k_orows(const ORowArgs a, int R) {
   using T = Traits<CPLX>;
   using S = typename T::S;
   extern __shared__ __align__(16) unsigned char smem_r[];
@@ -196,7 +195,7 @@ __global__ void __launch_bounds__(512) k_orows(const ORowArgs a) {
   const int W = (int)((a.ld_u * (rank + 1)) / a.C - col0);
   constexpr int E = Traits<CPLX>::kElemsPerUnit;
   const int TL = (orow_tab_len<MODEL>(a.n_vis, a.hidden) + 1) & ~1;
-  S* tabs = reinterpret_cast<S*>(smem_r);  // [2][TL]
+  S* tabs = reinterpret_cast<S*>(smem_r);  // [2][R][TL] factor tables, R rows per group
 
   uint32_t pr[PPT][E];
   double2 acc0[PPT], acc1[PPT];
@@ -209,54 +208,60 @@ __global__ void __launch_bounds__(512) k_orows(const ORowArgs a) {
     acc0[k] = make_double2(0.0, 0.0);
     acc1[k] = make_double2(0.0, 0.0);
   }
-  for (int b = 0; b < 2; ++b) {
-    if (tid == 0) {
-      if constexpr (CPLX) {
-        tabs[b * TL] = make_double2(0.0, 0.0);
-        tabs[b * TL + 1] = make_double2(1.0, 0.0);
-      } else {
-        tabs[b * TL] = 0.0;
-        tabs[b * TL + 1] = 1.0;
-      }
+  for (int e = tid; e < 2 * R; e += NT) {
+    if constexpr (CPLX) {
+      tabs[e * TL] = make_double2(0.0, 0.0);
+      tabs[e * TL + 1] = make_double2(1.0, 0.0);
+    } else {
+      tabs[e * TL] = 0.0;
+      tabs[e * TL + 1] = 1.0;
     }
   }
   const S* cf = reinterpret_cast<const S*>(a.coeff);
-  if (lo < hi) orow_stage<CPLX, MODEL>(a, lo, tabs, tid, NT);
-  for (int64_t n = lo; n < hi; ++n) {
-    const int buf = (int)((n - lo) & 1);
-    if (n + 1 < hi) {
-      orow_stage<CPLX, MODEL>(a, n + 1, tabs + (buf ^ 1) * TL, tid, NT);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-    }
-    __syncthreads();
-    const S* tab = tabs + buf * TL;
-    const double wn = __ldg(a.w + n);
-    const S cn = cf[n];
-    double2* orow = a.O + n * a.ld_u + col0;
+  const int G = (int)((hi - lo + R - 1) / R);
+  auto stage_group = [&](int g) {
+    const int64_t n0 = lo + (int64_t)g * R;
+    const int rows = (int)min((int64_t)R, hi - n0);
+    S* base = tabs + (size_t)(g & 1) * R * TL;
+    for (int r = 0; r < rows; ++r) orow_stage<CPLX, MODEL>(a, n0 + r, base + (size_t)r * TL, tid, NT);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  if (G > 0) stage_group(0);
+  for (int g = 0; g < G; ++g) {
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();  // group g staged; every thread is done with group g-1's buffer
+    if (g + 1 < G) stage_group(g + 1);
+    const int64_t n0 = lo + (int64_t)g * R;
+    const int rows = (int)min((int64_t)R, hi - n0);
+    const S* base = tabs + (size_t)(g & 1) * R * TL;
+    for (int r = 0; r < rows; ++r) {
+      const int64_t n = n0 + r;
+      const S* tab = base + (size_t)r * TL;
+      const double wn = __ldg(a.w + n);
+      const S cn = cf[n];
+      double2* orow = a.O + n * a.ld_u + col0;
 #pragma unroll
-    for (int k = 0; k < PPT; ++k) {
-      const int idx = tid + k * NT;
-      if (idx < W) {
-        double2 u;
-        if constexpr (CPLX) {
-          u = T::mul(tab[pr[k][0] >> 16], tab[pr[k][0] & 0xffffu]);
-          acc0[k].x = fma(wn, u.x, acc0[k].x);
-          acc0[k].y = fma(-wn, u.y, acc0[k].y);
-          T::axpy(acc1[k], u, cn);
-        } else {
-          u.x = tab[pr[k][0] >> 16] * tab[pr[k][0] & 0xffffu];
-          u.y = tab[pr[k][1] >> 16] * tab[pr[k][1] & 0xffffu];
-          acc0[k].x = fma(wn, u.x, acc0[k].x);
-          acc0[k].y = fma(wn, u.y, acc0[k].y);
-          acc1[k].x = fma(cn, u.x, acc1[k].x);
-          acc1[k].y = fma(cn, u.y, acc1[k].y);
+      for (int k = 0; k < PPT; ++k) {
+        const int idx = tid + k * NT;
+        if (idx < W) {
+          double2 u;
+          if constexpr (CPLX) {
+            u = T::mul(tab[pr[k][0] >> 16], tab[pr[k][0] & 0xffffu]);
+            acc0[k].x = fma(wn, u.x, acc0[k].x);
+            acc0[k].y = fma(-wn, u.y, acc0[k].y);
+            T::axpy(acc1[k], u, cn);
+          } else {
+            u.x = tab[pr[k][0] >> 16] * tab[pr[k][0] & 0xffffu];
+            u.y = tab[pr[k][1] >> 16] * tab[pr[k][1] & 0xffffu];
+            acc0[k].x = fma(wn, u.x, acc0[k].x);
+            acc0[k].y = fma(wn, u.y, acc0[k].y);
+            acc1[k].x = fma(cn, u.x, acc1[k].x);
+            acc1[k].y = fma(cn, u.y, acc1[k].y);
+          }
+          st_stream(orow + idx, u);
         }
-        st_stream(orow + idx, u);
       }
     }
-    __syncthreads();  // buffer `buf` is restaged two rows later
   }
 #pragma unroll
   for (int k = 0; k < PPT; ++k) {
