@@ -197,14 +197,19 @@ __global__ void __launch_bounds__(512) k_orows(const ORowArgs a, int R) {
   const int TL = (orow_tab_len<MODEL>(a.n_vis, a.hidden) + 1) & ~1;
   S* tabs = reinterpret_cast<S*>(smem_r);  // [2][R][TL] factor tables, R rows per group
 
+  // smem byte offsets of the two factors of each element (relative to the row table)
   uint32_t pr[PPT][E];
   double2 acc0[PPT], acc1[PPT];
+  const int kval = (W > tid) ? min(PPT, (W - tid + NT - 1) / NT) : 0;
 #pragma unroll
   for (int k = 0; k < PPT; ++k) {
     const int idx = tid + k * NT;
     const int64_t u = col0 + idx;
 #pragma unroll
-    for (int e = 0; e < E; ++e) pr[k][e] = (idx < W) ? elem_pair<MODEL>(u * E + e, a.n_vis, a.hidden, a.p) : 1u;
+    for (int e = 0; e < E; ++e) {
+      const uint32_t q = (idx < W) ? elem_pair<MODEL>(u * E + e, a.n_vis, a.hidden, a.p) : 1u;
+      pr[k][e] = (((q >> 16) * (uint32_t)sizeof(S)) << 16) | ((q & 0xffffu) * (uint32_t)sizeof(S));
+    }
     acc0[k] = make_double2(0.0, 0.0);
     acc1[k] = make_double2(0.0, 0.0);
   }
@@ -234,31 +239,34 @@ __global__ void __launch_bounds__(512) k_orows(const ORowArgs a, int R) {
     const int64_t n0 = lo + (int64_t)g * R;
     const int rows = (int)min((int64_t)R, hi - n0);
     const S* base = tabs + (size_t)(g & 1) * R * TL;
-    for (int r = 0; r < rows; ++r) {
+    double2* orow = a.O + n0 * a.ld_u + col0 + tid;
+    const char* tbase = reinterpret_cast<const char*>(base);
+    for (int r = 0; r < rows; ++r, orow += a.ld_u, tbase += (size_t)TL * sizeof(S)) {
       const int64_t n = n0 + r;
-      const S* tab = base + (size_t)r * TL;
       const double wn = __ldg(a.w + n);
       const S cn = cf[n];
-      double2* orow = a.O + n * a.ld_u + col0;
 #pragma unroll
       for (int k = 0; k < PPT; ++k) {
-        const int idx = tid + k * NT;
-        if (idx < W) {
+        if (k < kval) {
           double2 u;
           if constexpr (CPLX) {
-            u = T::mul(tab[pr[k][0] >> 16], tab[pr[k][0] & 0xffffu]);
+            const S fa = *reinterpret_cast<const S*>(tbase + (pr[k][0] >> 16));
+            const S fb = *reinterpret_cast<const S*>(tbase + (pr[k][0] & 0xffffu));
+            u = T::mul(fa, fb);
             acc0[k].x = fma(wn, u.x, acc0[k].x);
             acc0[k].y = fma(-wn, u.y, acc0[k].y);
             T::axpy(acc1[k], u, cn);
           } else {
-            u.x = tab[pr[k][0] >> 16] * tab[pr[k][0] & 0xffffu];
-            u.y = tab[pr[k][1] >> 16] * tab[pr[k][1] & 0xffffu];
+            u.x = *reinterpret_cast<const double*>(tbase + (pr[k][0] >> 16)) *
+                  *reinterpret_cast<const double*>(tbase + (pr[k][0] & 0xffffu));
+            u.y = *reinterpret_cast<const double*>(tbase + (pr[k][1] >> 16)) *
+                  *reinterpret_cast<const double*>(tbase + (pr[k][1] & 0xffffu));
             acc0[k].x = fma(wn, u.x, acc0[k].x);
             acc0[k].y = fma(wn, u.y, acc0[k].y);
             acc1[k].x = fma(cn, u.x, acc1[k].x);
             acc1[k].y = fma(cn, u.y, acc1[k].y);
           }
-          st_stream(orow + idx, u);
+          st_stream(orow + k * NT, u);
         }
       }
     }
