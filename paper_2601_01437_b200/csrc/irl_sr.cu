@@ -324,6 +324,8 @@ int launch_finish_mvp(const double2* part, int nb, int64_t ld_u, const void* ysu
                     "finish kernel launch");
 }
 
+constexpr int kAutoMaxCluster = 2;
+
 // MVP workspace layout for one plan
 struct MvpWs {
   double2* part;
@@ -368,7 +370,9 @@ int mvp_impl(bool cplx, const double* O, int64_t n, int64_t p, int64_t ld, const
   Plan pl;
   if (mode == IRL_MVP_AUTO || mode == IRL_MVP_FUSED) {
     int rc = make_plan(n, ld_u, cplx, MODE_FUSED, pl);
-    if (rc == IRL_OK) {
+    // AUTO: the per-row DSMEM exchange of wide clusters costs more than the
+    // second HBM pass (measured: C <= 2 wins, C >= 6 loses; tools/tune_cluster.py)
+    if (rc == IRL_OK && (mode == IRL_MVP_FUSED || pl.C <= kAutoMaxCluster)) {
       path = IRL_MVP_FUSED;
     } else if (mode == IRL_MVP_FUSED) {
       return rc;
@@ -806,7 +810,8 @@ int irl_mvp_plan(int64_t n, int64_t ld, int is_complex, int mode, int* out_path,
   Plan p;
   int path = IRL_MVP_TWO_PASS;
   if (mode == IRL_MVP_AUTO || mode == IRL_MVP_FUSED) {
-    if (make_plan(n, ld_u, is_complex != 0, MODE_FUSED, p) == IRL_OK) {
+    if (make_plan(n, ld_u, is_complex != 0, MODE_FUSED, p) == IRL_OK &&
+        (mode == IRL_MVP_FUSED || p.C <= kAutoMaxCluster)) {
       path = IRL_MVP_FUSED;
     } else if (mode == IRL_MVP_FUSED) {
       return IRL_ERR_DEVICE;
