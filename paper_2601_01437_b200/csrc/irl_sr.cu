@@ -95,8 +95,8 @@ template <bool CPLX, int MODE>
 StreamFn pick_stream(int ppt, int R) {
 #define IRL_CASE(P, RR) \
   if (ppt == P && R == RR) return k_stream<CPLX, P, RR, MODE>;
-  IRL_CASE(2, 1) IRL_CASE(2, 4) IRL_CASE(4, 1) IRL_CASE(4, 4)
-  IRL_CASE(8, 1) IRL_CASE(8, 4) IRL_CASE(16, 1) IRL_CASE(16, 4)
+  IRL_CASE(2, 1) IRL_CASE(2, 2) IRL_CASE(2, 4) IRL_CASE(4, 1) IRL_CASE(4, 2) IRL_CASE(4, 4)
+  IRL_CASE(8, 1) IRL_CASE(8, 2) IRL_CASE(8, 4) IRL_CASE(16, 1) IRL_CASE(16, 2) IRL_CASE(16, 4)
 #undef IRL_CASE
   return nullptr;
 }
@@ -119,7 +119,8 @@ struct Plan {
 
 size_t stream_extra_smem(bool cplx, int R, int C, int NS) {
   const size_t sS = cplx ? 16 : 8;
-  return (size_t)(2 * NS + kXchSlots) * 8 + (size_t)2 * R * 32 * sS + (size_t)kXchSlots * C * R * sS + sS + 8;
+  return (size_t)(2 * NS + kXchSlots) * 8 + (size_t)2 * R * 32 * sS + (size_t)kXchSlots * C * R * sS +
+         (size_t)kXchSlots * R * sS + sS + 8;
 }
 
 // Geometry for C column slices (uneven split, slot width Wmax = ceil(ld_u / C)).
@@ -142,7 +143,9 @@ bool choose_geom(int64_t ld_u, int C, bool cplx, int mode, int budget, Plan& p) 
   }
   if (!best_ppt) return false;
   const size_t slice = (size_t)W * 16;
-  const int R = (4 * slice <= 64 * 1024) ? 4 : 1;
+  // rows per stage: amortise the per-group reduction over up to 4 rows while
+  // keeping >= 3 stages in flight
+  const int R = (4 * slice <= 64 * 1024) ? 4 : (2 * slice <= 64 * 1024) ? 2 : 1;
   const size_t extra = stream_extra_smem(cplx, R, C, 8);
   if ((size_t)budget <= extra) return false;
   int NS = (int)std::min<size_t>(8, ((size_t)budget - extra) / (R * slice));

@@ -94,7 +94,8 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
   uint64_t* xbar = empty + NS;                       // [kXchSlots]
   S* red = reinterpret_cast<S*>(xbar + kXchSlots);   // [2][R][32]
   S* xch = red + 2 * R * 32;                         // [kXchSlots][C][R]
-  S* pro_s = xch + kXchSlots * C * R;                // [1] cluster-visible prologue slot
+  S* tslot = xch + kXchSlots * C * R;                // [kXchSlots][R] CTA-level t (C == 1)
+  S* pro_s = tslot + kXchSlots * R;                  // [1] cluster-visible prologue slot
   double* pro_g = reinterpret_cast<double*>(pro_s + 1);  // [1]
 
   const bool clustered = (MODE == MODE_FUSED) && (C > 1);
@@ -229,9 +230,10 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
   auto rows_of = [&](int g) -> int { return (int)min((int64_t)R, hi - (lo + (int64_t)g * R)); };
   auto stage_ptr = [&](int g) -> const double2* { return ring + (size_t)(g % NS) * R * WM; };
 
-  // dot + block reduction (+ DSMEM send) of group g; returns the CTA-level
-  // partial t for row `lane` (valid for lane < rows) in every warp.
-  auto dot_group = [&](int g) -> S {
+  // dot + block reduction (+ DSMEM send) of group g.  Only warp 0 reduces the
+  // per-warp partials; the result reaches the other warps through smem
+  // (tslot, C == 1), the DSMEM exchange (xch, C > 1) or global (tpart, DOT).
+  auto dot_group = [&](int g) {
     const int rows = rows_of(g);
     mbar_wait(&full[g % NS], (g / NS) & 1);
     const double2* st = stage_ptr(g);
@@ -255,38 +257,47 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
       for (int r = 0; r < R; ++r) rb[r * 32 + warp] = dp[r];
     }
     named_bar_sync(1, NT);
-    S t = T::zero();
+    if (warp == 0) {
+      S t = T::zero();
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const S tr = block_sum(rb + r * 32);
-      if (lane == r) t = tr;
-    }
-    if (clustered && warp == 0) {
+      for (int r = 0; r < R; ++r) {
+        const S tr = block_sum(rb + r * 32);
+        if (lane == r) t = tr;
+      }
       const int b = g % kXchSlots;
-      if (lane == 0) mbar_arrive_expect_tx(&xbar[b], (uint32_t)(C * rows * sizeof(S)));
-      if (lane < rows) {
-        const uint32_t la = smem_addr(&xch[(b * C + rank) * R + lane]);
-        const uint32_t lb = smem_addr(&xbar[b]);
-        for (int q = 0; q < C; ++q) st_async(map_to_rank(la, q), t, map_to_rank(lb, q));
+      if constexpr (MODE == MODE_DOT) {
+        if (lane < rows) reinterpret_cast<S*>(a.tpart)[(int64_t)rank * N + lo + (int64_t)g * R + lane] = t;
+      } else if (clustered) {
+        if (lane == 0) mbar_arrive_expect_tx(&xbar[b], (uint32_t)(C * rows * sizeof(S)));
+        if (lane < rows) {
+          const uint32_t la = smem_addr(&xch[(b * C + rank) * R + lane]);
+          const uint32_t lb = smem_addr(&xbar[b]);
+          for (int q = 0; q < C; ++q) st_async(map_to_rank(la, q), t, map_to_rank(lb, q));
+        }
+      } else {
+        if (lane < rows) tslot[b * R + lane] = t;
       }
     }
-    return t;
   };
 
   // finish group g: cluster-summed t -> y -> accumulate -> release the stage
   S ys = T::zero();
-  auto acc_group = [&](int g, S tcta, S cf0, S cf1) {
+  auto acc_group = [&](int g, S tin, S cf0, S cf1) {
     const int rows = rows_of(g);
     const double2* st = stage_ptr(g);
     S yv = T::zero();
     if constexpr (MODE == MODE_FUSED || MODE == MODE_ACC) {
-      S t = tcta;
-      if (clustered) {
+      S t = tin;
+      if constexpr (MODE == MODE_FUSED) {
         const int b = g % kXchSlots;
-        mbar_wait(&xbar[b], (g / kXchSlots) & 1);
-        t = T::zero();
-        if (lane < rows)
-          for (int q = 0; q < C; ++q) t = T::add(t, xch[(b * C + q) * R + lane]);
+        if (clustered) {
+          mbar_wait(&xbar[b], (g / kXchSlots) & 1);
+          t = T::zero();
+          if (lane < rows)
+            for (int q = 0; q < C; ++q) t = T::add(t, xch[(b * C + q) * R + lane]);
+        } else {
+          t = (lane < rows) ? tslot[b * R + lane] : T::zero();
+        }
       }
       if (lane < rows) yv = T::mul(cf0, T::sub(t, s_val));
     } else {
@@ -338,9 +349,7 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
 
   if constexpr (MODE == MODE_DOT) {
     for (int g = 0; g < G; ++g) {
-      const S t = dot_group(g);
-      const int rows = rows_of(g);
-      if (warp == 0 && lane < rows) reinterpret_cast<S*>(a.tpart)[(int64_t)rank * N + lo + (int64_t)g * R + lane] = t;
+      dot_group(g);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[g % NS]);
     }
@@ -348,15 +357,16 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
     if (G > 0) {
       S cf0, cf1, tin;
       load_coeffs(0, cf0, cf1, tin);
-      S t_cur = dot_group(0);
+      dot_group(0);
       for (int g = 0; g < G; ++g) {
-        S t_next = T::zero(), cn0 = T::zero(), cn1 = T::zero(), tn = T::zero();
+        S cn0 = T::zero(), cn1 = T::zero(), tn = T::zero();
         if (g + 1 < G) {
           load_coeffs(g + 1, cn0, cn1, tn);
-          t_next = dot_group(g + 1);  // lookahead: overlaps group g's exchange latency
+          dot_group(g + 1);  // lookahead: its barrier also publishes tslot[g] (C == 1)
+        } else if (!clustered) {
+          named_bar_sync(1, NT);  // publish the last group's tslot
         }
-        acc_group(g, t_cur, cf0, cf1);
-        t_cur = t_next;
+        acc_group(g, T::zero(), cf0, cf1);
         cf0 = cn0;
       }
     }
