@@ -120,7 +120,7 @@ struct Plan {
 size_t stream_extra_smem(bool cplx, int R, int C, int NS) {
   const size_t sS = cplx ? 16 : 8;
   return (size_t)(2 * NS + kXchSlots) * 8 + (size_t)2 * R * 32 * sS + (size_t)kXchSlots * C * R * sS +
-         (size_t)2 * kXchSlots * R * sS + sS + 8;
+         (size_t)kXchSlots * R * sS + sS + 8;
 }
 
 // Geometry for C column slices (uneven split, slot width Wmax = ceil(ld_u / C)).
@@ -303,12 +303,6 @@ int launch_stream(const Plan& p, const StreamArgs& a, cudaStream_t st) {
   args.C = p.C;
   args.nb = p.nb;
   args.stages = p.NS;
-  // lookahead: keep one stage prefetching beyond the L+1 held ones
-  {
-    const char* env = getenv("IRL_LOOKAHEAD");
-    int L = env ? atoi(env) : (p.C > 1 ? p.NS - 2 : 1);
-    args.lookahead = std::max(1, std::min(L, std::min(kMaxLookahead, p.NS - 1)));
-  }
   void* kargs[] = {&args};
   return cuda_check(cudaLaunchKernelExC(&cfg, (const void*)p.fn, kargs), "stream kernel launch");
 }

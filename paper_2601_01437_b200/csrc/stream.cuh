@@ -31,10 +31,7 @@ namespace irl {
 
 enum StreamMode { MODE_FUSED = 0, MODE_DOT = 1, MODE_ACC = 2, MODE_STATS = 3 };
 
-// DSMEM exchange ring depth: a lookahead of L groups needs 2L + 2 slots (a peer
-// can be at most L + 1 groups ahead of the slowest reader of a slot)
-constexpr int kXchSlots = 8;
-constexpr int kMaxLookahead = 3;
+constexpr int kXchSlots = 4;  // DSMEM exchange ring depth (lookahead 1 needs 4, see below)
 
 struct StreamArgs {
   const double2* O;  // units; row stride ld_u
@@ -44,7 +41,6 @@ struct StreamArgs {
   int C;       // column slices (cluster size in MODE_FUSED)
   int nb;      // row blocks (clusters in MODE_FUSED)
   int stages;  // ring depth
-  int lookahead;  // FUSED: row groups reduced ahead of the accumulate (1..kMaxLookahead)
   // input vectors (unit-indexed).  real: v_re is the f64 array viewed as units;
   // complex: planar re/im (im may be null = 0).
   const double* v_re;
@@ -99,8 +95,7 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
   S* red = reinterpret_cast<S*>(xbar + kXchSlots);   // [2][R][32]
   S* xch = red + 2 * R * 32;                         // [kXchSlots][C][R]
   S* tslot = xch + kXchSlots * C * R;                // [kXchSlots][R] CTA-level t (C == 1)
-  S* cfslot = tslot + kXchSlots * R;                 // [kXchSlots][R] row coefficients (FUSED)
-  S* pro_s = cfslot + kXchSlots * R;                 // [1] cluster-visible prologue slot
+  S* pro_s = tslot + kXchSlots * R;                  // [1] cluster-visible prologue slot
   double* pro_g = reinterpret_cast<double*>(pro_s + 1);  // [1]
 
   const bool clustered = (MODE == MODE_FUSED) && (C > 1);
@@ -273,7 +268,6 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
       if constexpr (MODE == MODE_DOT) {
         if (lane < rows) reinterpret_cast<S*>(a.tpart)[(int64_t)rank * N + lo + (int64_t)g * R + lane] = t;
       } else if (clustered) {
-        if (lane < rows) cfslot[b * R + lane] = reinterpret_cast<const S*>(a.coeff0)[lo + (int64_t)g * R + lane];
         if (lane == 0) mbar_arrive_expect_tx(&xbar[b], (uint32_t)(C * rows * sizeof(S)));
         if (lane < rows) {
           const uint32_t la = smem_addr(&xch[(b * C + rank) * R + lane]);
@@ -281,10 +275,7 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
           for (int q = 0; q < C; ++q) st_async(map_to_rank(la, q), t, map_to_rank(lb, q));
         }
       } else {
-        if (lane < rows) {
-          tslot[b * R + lane] = t;
-          cfslot[b * R + lane] = reinterpret_cast<const S*>(a.coeff0)[lo + (int64_t)g * R + lane];
-        }
+        if (lane < rows) tslot[b * R + lane] = t;
       }
     }
   };
@@ -307,7 +298,6 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
         } else {
           t = (lane < rows) ? tslot[b * R + lane] : T::zero();
         }
-        cf0 = (lane < rows) ? cfslot[b * R + lane] : T::zero();
       }
       if (lane < rows) yv = T::mul(cf0, T::sub(t, s_val));
     } else {
@@ -364,20 +354,21 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
       if (lane == 0) mbar_arrive(&empty[g % NS]);
     }
   } else if constexpr (MODE == MODE_FUSED) {
-    // lookahead L: group g+L is reduced (and its partial sent) before group g
-    // is accumulated; warp 0 parks t (C == 1) and the coefficients in smem
-    // slots, published to the other warps by the next group's barrier.
-    const int L = max(1, min(a.lookahead, kMaxLookahead));
-    for (int j = 0; j < min(L, G); ++j) dot_group(j);
-    bool tail_published = false;
-    for (int g = 0; g < G; ++g) {
-      if (g + L < G) {
-        dot_group(g + L);
-      } else if (!tail_published) {
-        named_bar_sync(1, NT);  // publish the remaining groups' slots
-        tail_published = true;
+    if (G > 0) {
+      S cf0, cf1, tin;
+      load_coeffs(0, cf0, cf1, tin);
+      dot_group(0);
+      for (int g = 0; g < G; ++g) {
+        S cn0 = T::zero(), cn1 = T::zero(), tn = T::zero();
+        if (g + 1 < G) {
+          load_coeffs(g + 1, cn0, cn1, tn);
+          dot_group(g + 1);  // lookahead: its barrier also publishes tslot[g] (C == 1)
+        } else if (!clustered) {
+          named_bar_sync(1, NT);  // publish the last group's tslot
+        }
+        acc_group(g, T::zero(), cf0, cf1);
+        cf0 = cn0;
       }
-      acc_group(g, T::zero(), T::zero(), T::zero());
     }
   } else {
     for (int g = 0; g < G; ++g) {
