@@ -1,7 +1,7 @@
 # Builds the sm_100a C-ABI library in-tree (the .so travels to the GPU box).
 NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisibility=hidden \
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisibility=hidden -Xcompiler -ffp-contract=off \
            --expt-relaxed-constexpr -Xptxas -warn-spills
 PKG := paper_2601_01437_b200
 SRC := $(PKG)/csrc/irl_sr.cu

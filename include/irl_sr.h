@@ -140,6 +140,18 @@ int irl_otf_mvp_mlp_f64(const uint64_t* xbits, const double* t, const double* g,
                         const double* half_f, const double* u0, double* out0, void* ws, size_t ws_bytes,
                         void* stream);
 
+/* ------------------------------------------------------ A13 / A16 ----
+ * IRL driver helpers.
+ * irl_lanczos_step_small: one Lanczos step (krylov.py:96-116) on device scalars
+ * for short vectors (L <= 4096): given W = A v_j, writes alpha_j, beta_j into
+ * ab[j], ab[m + j], reorthogonalises W twice against V rows 0..j (ldv stride)
+ * and stores V[j+1] = W / beta_j.  Single CTA, graph-capturable.
+ * irl_host_qr_sweeps: HOST function; nshift implicit-shift QR bulge chases
+ * (krylov.py:165-190, as applied by implicit_restart :225-227) on the dense
+ * row-major m x m tridiagonal T, accumulating Q (both in/out, host memory). */
+int irl_lanczos_step_small(double* V, int64_t ldv, double* W, int64_t L, int j, int m, double* ab, void* stream);
+int irl_host_qr_sweeps(int m, double* T, double* Q, const double* shifts, int nshift);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

@@ -13,6 +13,7 @@
 #include "../../include/irl_sr.h"
 #include "obuild.cuh"
 #include "otf.cuh"
+#include "lanczos.cuh"
 #include "stream.cuh"
 
 using namespace irl;
@@ -913,6 +914,48 @@ int irl_otf_mvp_mlp_f64(const uint64_t* xbits, const double* t, const double* g,
   k_otf_finish<<<(unsigned)cdiv(ld, 256), 256, 0, st>>>(wl.part, wl.partu, pl.nb, hidden, n_in, ld, wl.ypart, pl.ny,
                                                        obar, half_f, u0, wl.gpart, pl.ny, out, out0);
   return cuda_check(cudaGetLastError(), "otf finish launch");
+}
+
+int irl_lanczos_step_small(double* V, int64_t ldv, double* W, int64_t L, int j, int m, double* ab, void* stream) {
+  if (!V || !W || !ab || L < 1 || j < 0 || j >= m || j + 1 > 63 || ldv < L) return fail(IRL_ERR_ARG, "bad lanczos step");
+  k_lanczos_small<<<1, 1024, 0, (cudaStream_t)stream>>>(V, ldv, W, L, j, m, ab);
+  return cuda_check(cudaGetLastError(), "lanczos step launch");
+}
+
+int irl_host_qr_sweeps(int m, double* T, double* Q, const double* shifts, int nshift) {
+  if (m < 2 || !T || !Q || (nshift > 0 && !shifts)) return fail(IRL_ERR_ARG, "bad qr sweep arguments");
+  // kry:165-190 per shift, same operation order (full rows / columns, t <- G^T t G, q <- q G)
+  for (int sidx = 0; sidx < nshift; ++sidx) {
+    double x = T[0] - shifts[sidx], z = T[m];
+    for (int k = 0; k < m - 1; ++k) {
+      const double r = hypot(x, z);
+      double c = 1.0, s = 0.0;
+      if (r != 0.0) {
+        c = x / r;
+        s = z / r;
+      }
+      for (int col = 0; col < m; ++col) {
+        const double a0 = T[k * m + col], a1 = T[(k + 1) * m + col];
+        T[k * m + col] = c * a0 + s * a1;
+        T[(k + 1) * m + col] = -s * a0 + c * a1;
+      }
+      for (int row = 0; row < m; ++row) {
+        const double a0 = T[row * m + k], a1 = T[row * m + k + 1];
+        T[row * m + k] = c * a0 + s * a1;
+        T[row * m + k + 1] = -s * a0 + c * a1;
+      }
+      for (int row = 0; row < m; ++row) {
+        const double a0 = Q[row * m + k], a1 = Q[row * m + k + 1];
+        Q[row * m + k] = c * a0 + s * a1;
+        Q[row * m + k + 1] = -s * a0 + c * a1;
+      }
+      if (k < m - 2) {
+        x = T[(k + 1) * m + k];
+        z = T[(k + 2) * m + k];
+      }
+    }
+  }
+  return IRL_OK;
 }
 
 }  // extern "C"

@@ -1,0 +1,73 @@
+// Lanczos step for short vectors (kry:96-116) fused into ONE single-CTA kernel.
+//
+// On entry W = A v_j.  The kernel performs, on device scalars only:
+//   alpha_j = v_j . W ;  W -= alpha_j v_j + beta_{j-1} v_{j-1}
+//   twice:   h = V_{0..j} W ;  W -= V^T h          (full reorthogonalisation)
+//   beta_j = ||W|| ;  V[j+1] = W / max(beta_j, tiny)
+// and stores (alpha_j, beta_j) into ab[0][j], ab[1][j].  It replaces ~14
+// separate BLAS-1/2 launches per Lanczos step when L is small enough that one
+// SM streams V faster than the launch latency of the multi-kernel version.
+// All reductions are fixed-order (warp butterflies, warps in index order).
+#pragma once
+#include "common.cuh"
+
+namespace irl {
+
+__device__ __forceinline__ double block_sum_f64(double x, double* sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  x = warp_sum<false>(x);
+  __syncthreads();  // sh reuse
+  if (lane == 0) sh[warp] = x;
+  __syncthreads();
+  double t = (lane < nw) ? sh[lane] : 0.0;
+  return warp_sum<false>(t);
+}
+
+__global__ void __launch_bounds__(1024) k_lanczos_small(double* __restrict__ V, int64_t ldv, double* __restrict__ W,
+                                                         int64_t L, int j, int m, double* __restrict__ ab) {
+  __shared__ double sh[32];
+  __shared__ double hs[64];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const double* vj = V + (int64_t)j * ldv;
+  // alpha
+  double p = 0.0;
+  for (int64_t e = tid; e < L; e += blockDim.x) p = fma(vj[e], W[e], p);
+  const double alpha = block_sum_f64(p, sh);
+  const double bprev = j > 0 ? ab[m + j - 1] : 0.0;
+  const double* vp = j > 0 ? V + (int64_t)(j - 1) * ldv : nullptr;
+  for (int64_t e = tid; e < L; e += blockDim.x) {
+    double w = W[e] - alpha * vj[e];
+    if (vp) w -= bprev * vp[e];
+    W[e] = w;
+  }
+  __syncthreads();
+  for (int pass = 0; pass < 2; ++pass) {
+    // h_i = V_i . W, one warp per basis row
+    for (int i = warp; i <= j; i += nw) {
+      const double* vi = V + (int64_t)i * ldv;
+      double q = 0.0;
+      for (int64_t e = lane; e < L; e += 32) q = fma(vi[e], W[e], q);
+      q = warp_sum<false>(q);
+      if (lane == 0) hs[i] = q;
+    }
+    __syncthreads();
+    for (int64_t e = tid; e < L; e += blockDim.x) {
+      double acc = 0.0;
+      for (int i = 0; i <= j; ++i) acc = fma(hs[i], V[(int64_t)i * ldv + e], acc);
+      W[e] -= acc;
+    }
+    __syncthreads();
+  }
+  double nrm = 0.0;
+  for (int64_t e = tid; e < L; e += blockDim.x) nrm = fma(W[e], W[e], nrm);
+  const double beta = sqrt(block_sum_f64(nrm, sh));
+  const double inv = 1.0 / fmax(beta, 1e-300);
+  double* vn = V + (int64_t)(j + 1) * ldv;
+  for (int64_t e = tid; e < L; e += blockDim.x) vn[e] = W[e] * inv;
+  if (tid == 0) {
+    ab[j] = alpha;
+    ab[m + j] = beta;
+  }
+}
+
+}  // namespace irl
