@@ -130,15 +130,18 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
     if (clustered) cluster_arrive();  // prologue exchange barrier (no data needed here)
     if (lane == 0) {
       const uint32_t slice_bytes = (uint32_t)W * 16u;
-      for (int g = 0; g < G; ++g) {
-        const int s = g % NS;
-        if (g >= NS) mbar_wait(&empty[s], ((g / NS) - 1) & 1);
+      for (int g = 0, s = 0, ph = 0; g < G; ++g) {
+        if (g >= NS) mbar_wait(&empty[s], ph ^ 1);
         const int64_t r0 = lo + (int64_t)g * R;
         const int rows = (int)min((int64_t)R, hi - r0);
         mbar_arrive_expect_tx(&full[s], slice_bytes * rows);
         double2* dst = ring + (size_t)s * R * WM;
         const double2* src = a.O + r0 * a.ld_u + col0;
         for (int r = 0; r < rows; ++r) bulk_g2s(dst + (size_t)r * WM, src + r * a.ld_u, slice_bytes, &full[s]);
+        if (++s == NS) {
+          s = 0;
+          ph ^= 1;
+        }
       }
     }
     __syncwarp();
@@ -228,15 +231,24 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
   }
 
   auto rows_of = [&](int g) -> int { return (int)min((int64_t)R, hi - (lo + (int64_t)g * R)); };
-  auto stage_ptr = [&](int g) -> const double2* { return ring + (size_t)(g % NS) * R * WM; };
+  // ring position of a group: (stage s, phase parity ph), advanced incrementally
+  struct Pos {
+    int s, ph;
+  };
+  auto advance = [&](Pos& p) {
+    if (++p.s == NS) {
+      p.s = 0;
+      p.ph ^= 1;
+    }
+  };
 
   // dot + block reduction (+ DSMEM send) of group g.  Only warp 0 reduces the
   // per-warp partials; the result reaches the other warps through smem
   // (tslot, C == 1), the DSMEM exchange (xch, C > 1) or global (tpart, DOT).
-  auto dot_group = [&](int g) {
+  auto dot_group = [&](int g, Pos p) {
     const int rows = rows_of(g);
-    mbar_wait(&full[g % NS], (g / NS) & 1);
-    const double2* st = stage_ptr(g);
+    mbar_wait(&full[p.s], p.ph);
+    const double2* st = ring + (size_t)p.s * R * WM;
     S dp[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) dp[r] = T::zero();
@@ -282,9 +294,9 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
 
   // finish group g: cluster-summed t -> y -> accumulate -> release the stage
   S ys = T::zero();
-  auto acc_group = [&](int g, S tin, S cf0, S cf1) {
+  auto acc_group = [&](int g, Pos p, S tin, S cf0, S cf1) {
     const int rows = rows_of(g);
-    const double2* st = stage_ptr(g);
+    const double2* st = ring + (size_t)p.s * R * WM;
     S yv = T::zero();
     if constexpr (MODE == MODE_FUSED || MODE == MODE_ACC) {
       S t = tin;
@@ -303,7 +315,7 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
     } else {
       yv = cf0;
     }
-    if constexpr (MODE == MODE_ACC || MODE == MODE_STATS) mbar_wait(&full[g % NS], (g / NS) & 1);
+    if constexpr (MODE == MODE_ACC || MODE == MODE_STATS) mbar_wait(&full[p.s], p.ph);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       if (r < rows) {
@@ -322,7 +334,7 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
       }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[g % NS]);
+    if (lane == 0) mbar_arrive(&empty[p.s]);
   };
 
   // per-row coefficients for group g (lane r owns row r)
@@ -348,33 +360,39 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
   };
 
   if constexpr (MODE == MODE_DOT) {
-    for (int g = 0; g < G; ++g) {
-      dot_group(g);
+    Pos p{0, 0};
+    for (int g = 0; g < G; ++g, advance(p)) {
+      dot_group(g, p);
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[g % NS]);
+      if (lane == 0) mbar_arrive(&empty[p.s]);
     }
   } else if constexpr (MODE == MODE_FUSED) {
     if (G > 0) {
       S cf0, cf1, tin;
       load_coeffs(0, cf0, cf1, tin);
-      dot_group(0);
+      Pos pa{0, 0}, pd{0, 0};
+      dot_group(0, pd);
+      advance(pd);
       for (int g = 0; g < G; ++g) {
         S cn0 = T::zero(), cn1 = T::zero(), tn = T::zero();
         if (g + 1 < G) {
           load_coeffs(g + 1, cn0, cn1, tn);
-          dot_group(g + 1);  // lookahead: its barrier also publishes tslot[g] (C == 1)
+          dot_group(g + 1, pd);  // lookahead: its barrier also publishes tslot[g] (C == 1)
+          advance(pd);
         } else if (!clustered) {
           named_bar_sync(1, NT);  // publish the last group's tslot
         }
-        acc_group(g, T::zero(), cf0, cf1);
+        acc_group(g, pa, T::zero(), cf0, cf1);
+        advance(pa);
         cf0 = cn0;
       }
     }
   } else {
-    for (int g = 0; g < G; ++g) {
+    Pos p{0, 0};
+    for (int g = 0; g < G; ++g, advance(p)) {
       S cf0, cf1, tin;
       load_coeffs(g, cf0, cf1, tin);
-      acc_group(g, tin, cf0, cf1);
+      acc_group(g, p, tin, cf0, cf1);
     }
   }
 
