@@ -54,6 +54,40 @@ def dist_env():
     return world, rank, local
 
 
+class Replicas:
+    """One process per GPU, N independent replicas of the hot path:
+    the only communication is the barrier around the timed region and the
+    max-over-ranks of the elapsed times.  Backend nccl on GPUs, gloo in tests."""
+
+    def __init__(self, backend: str = "nccl", device=None):
+        self.world, self.rank, self.local = dist_env()
+        self.device = device
+        self.pg = None
+        if self.world > 1:
+            import torch.distributed as dist
+
+            kw = {"device_id": device} if backend == "nccl" and device is not None else {}
+            dist.init_process_group(backend, **kw)
+            self.pg = dist
+
+    def barrier(self):
+        if self.pg:
+            self.pg.barrier()
+
+    def max(self, x: float) -> float:
+        if not self.pg:
+            return float(x)
+        import torch
+
+        t = torch.tensor([float(x)], dtype=torch.float64, device=self.device if self.device is not None else "cpu")
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t)
+
+    def close(self):
+        if self.pg:
+            self.pg.destroy_process_group()
+
+
 def cpu_cores() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -232,14 +266,9 @@ def run_ours(args):
     import torch
 
     world, rank, local = dist_env()
-    if world > 1:
-        import torch.distributed as dist
-
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(0)
+    torch.cuda.set_device(local if world > 1 else 0)
     dev = torch.device("cuda", torch.cuda.current_device())
+    reps = Replicas("nccl", dev)
 
     from paper_2601_01437_b200 import _lib, ansatz as A, estimators as E, optimizer as OPT, synthetic as S
 
@@ -294,11 +323,7 @@ def run_ours(args):
         one(k % nvec, coef_h, 0)
         one((k + 1) % nvec, coef_s, 1)
 
-    def barrier():
-        if world > 1:
-            import torch.distributed as dist
-
-            dist.barrier()
+    barrier = reps.barrier
 
     for k in range(args.warmup):
         step(k)
@@ -325,14 +350,8 @@ def run_ours(args):
         t1.record(stream)
         torch.cuda.synchronize()
     barrier()
-    elapsed = t0.elapsed_time(t1) / 1e3
+    elapsed = reps.max(t0.elapsed_time(t1) / 1e3)
     mvp_ms = [a.elapsed_time(b) for a, b in per]
-    if world > 1:
-        import torch.distributed as dist
-
-        tt = torch.tensor([elapsed], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        elapsed = float(tt)
     mvps = 2 * args.steps
     value = world * mvps / elapsed
 
@@ -351,12 +370,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     e2e_time = time.perf_counter() - h0
     barrier()
-    if world > 1:
-        import torch.distributed as dist
-
-        tt = torch.tensor([e2e_time], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_time = float(tt)
+    e2e_time = reps.max(e2e_time)
     vbytes = P * (16 if herm else 8)
     e2e = {"value": world * 2 * e2e_steps / e2e_time, "unit": UNIT, "h2d_bytes_per_step": 2 * vbytes,
            "d2h_bytes_per_step": 2 * vbytes,
@@ -380,10 +394,7 @@ def run_ours(args):
                "m": cfg.m, "max_restarts": cfg.max_restarts}
 
     if rank != 0:
-        if world > 1:
-            import torch.distributed as dist
-
-            dist.destroy_process_group()
+        reps.close()
         return 0
 
     # ---- roofline of the dominant kernel (the streaming MVP launch)
@@ -436,10 +447,7 @@ def run_ours(args):
         "mvp_ms_per_product": elapsed / mvps * 1e3,
     }
     print(json.dumps(line))
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.destroy_process_group()
+    reps.close()
     return 0
 
 
