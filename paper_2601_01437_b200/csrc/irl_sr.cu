@@ -637,10 +637,10 @@ int make_otf_plan(int64_t n, int n_in, int hidden, OtfPlan& p) {
   IRL_TRY(dev_info(d));
   if (n_in < 1 || n_in > OTF_MAX_NIN) return fail(IRL_ERR_ARG, "on-the-fly mode supports n_in <= %d", OTF_MAX_NIN);
   p.jc = (int)cdiv(hidden, OTF_BJ);
-  p.nb = std::max(1, (int)((4LL * d.sms + p.jc / 2) / p.jc));  // ~2 waves at 2 CTAs/SM
+  p.nb = std::max(1, (int)((2LL * d.sms + p.jc / 2) / p.jc));
   p.nb = (int)std::min<int64_t>(p.nb, std::max<int64_t>(1, cdiv(n, OTF_BM)));
   p.ny = d.sms;
-  p.smem_dot = (size_t)(OTF_BJ * OTF_MAX_NIN + 2 * OTF_BJ + 2 * OTF_BM * OTF_BJ) * 8 + 2 * OTF_BM * OTF_XW * 8 +
+  p.smem_dot = (size_t)(OTF_BJ * OTF_MAX_NIN + 2 * OTF_BJ + 4 * OTF_BM * OTF_BJ) * 8 + 2 * OTF_BM * OTF_XW * 8 +
                4 * OTF_BM * 8;
   p.smem_acc = (size_t)4 * OTF_BM * OTF_BJ * 8 + 2 * OTF_BM * OTF_XW * 8 + 2 * OTF_BM * 8;
   IRL_TRY(ensure_fn_attrs((const void*)k_otf_dot, d.smem_optin));

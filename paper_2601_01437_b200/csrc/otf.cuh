@@ -20,7 +20,7 @@
 namespace irl {
 
 constexpr int OTF_BJ = 64;   // hidden units per CTA chunk
-constexpr int OTF_BM = 32;   // rows per tile (2 CTAs per SM fit in shared memory)
+constexpr int OTF_BM = 64;   // rows per tile
 constexpr int OTF_KC = 104;  // k columns of the acc GEMM: n_in (<=100) + ones column, padded to 13 n-tiles
 constexpr int OTF_MAX_NIN = 100;
 constexpr int OTF_XW = 2;    // 64-bit words per packed input row (n_in <= 128)
@@ -76,14 +76,14 @@ __global__ void k_pack_bits(const uint8_t* __restrict__ x, int64_t n, int n_in, 
 // Tile loader: G/T rows [r0, r0+BM) x columns [j0, j0+BJ) and the packed bits.
 __device__ __forceinline__ void otf_load_tile(const OtfArgs& a, int64_t r0, int64_t hi, int j0, double* gs, double* ts,
                                               uint64_t* xs, int tid, int nthreads) {
-  // BM rows x 64 doubles = 512 B per row = 32 x 16 B per row, for G (and T when ts != null)
+  // 64 rows x 64 doubles = 512 B per row = 32 x 16 B per row, for G and T
   for (int e = tid; e < OTF_BM * (OTF_BJ / 2); e += nthreads) {
     const int r = e / (OTF_BJ / 2), c = (e % (OTF_BJ / 2)) * 2;
     const int64_t row = r0 + r;
     const bool ok = row < hi && (j0 + c) < a.hidden;
     const int64_t off = ok ? row * a.hidden + j0 + c : 0;
     cp_async16(gs + r * OTF_BJ + c, a.G + off, ok);
-    if (ts) cp_async16(ts + r * OTF_BJ + c, a.T + off, ok);
+    cp_async16(ts + r * OTF_BJ + c, a.T + off, ok);
   }
   for (int e = tid; e < OTF_BM; e += nthreads) {
     const int64_t row = r0 + e;
@@ -92,26 +92,26 @@ __device__ __forceinline__ void otf_load_tile(const OtfArgs& a, int64_t r0, int6
   }
 }
 
-// grid (JC, nb), 256 threads, 2 CTAs/SM: t partials for hidden chunk jc over a
-// row block.  Warp (wr, wj) owns rows [16 wr, +16) x hidden units [16 wj, +16)
-// of each 32-row tile: 2 x 2 DMMA accumulator chains over K = n_in.
-__global__ void __launch_bounds__(256, 2) k_otf_dot(const OtfArgs a) {
+// grid (JC, nb), 256 threads: t partials for hidden chunk jc over row block
+__global__ void __launch_bounds__(256) k_otf_dot(const OtfArgs a) {
   extern __shared__ __align__(16) unsigned char smem_o[];
   double* vw = reinterpret_cast<double*>(smem_o);            // [BJ][OTF_MAX_NIN]
   double* vb = vw + OTF_BJ * OTF_MAX_NIN;                    // [BJ]
   double* vu = vb + OTF_BJ;                                  // [BJ]
   double* gs = vu + OTF_BJ;                                  // [2][BM][BJ]
-  uint64_t* xs = reinterpret_cast<uint64_t*>(gs + 2 * OTF_BM * OTF_BJ);  // [2][BM][XW]
+  double* ts = gs + 2 * OTF_BM * OTF_BJ;                     // [2][BM][BJ]
+  uint64_t* xs = reinterpret_cast<uint64_t*>(ts + 2 * OTF_BM * OTF_BJ);  // [2][BM][XW]
   double* red = reinterpret_cast<double*>(xs + 2 * OTF_BM * OTF_XW);     // [4][BM]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wr = warp >> 2, wj = warp & 3;
+  const int wr = warp >> 2, wj = warp & 3;  // rows [wr*32, +32), j [wj*16, +16)
   const int jc = blockIdx.x, j0 = jc * OTF_BJ;
   const int64_t N = a.n_rows;
   const int64_t lo = (N * blockIdx.y) / a.nb, hi = (N * (blockIdx.y + 1)) / a.nb;
   const int h = a.hidden, nin = a.n_in;
   const int64_t offb = (int64_t)h * nin, offu = offb + h;
 
+  // v_W chunk, v_b, v_u (zero beyond h / n_in)
   for (int e = tid; e < OTF_BJ * OTF_MAX_NIN; e += blockDim.x) {
     const int jj = e / OTF_MAX_NIN, k = e % OTF_MAX_NIN;
     vw[e] = (j0 + jj < h && k < nin) ? a.v[(int64_t)(j0 + jj) * nin + k] : 0.0;
@@ -121,64 +121,63 @@ __global__ void __launch_bounds__(256, 2) k_otf_dot(const OtfArgs a) {
     vu[e] = (j0 + e < h) ? a.v[offu + j0 + e] : 0.0;
   }
   const int ntiles = (int)((hi - lo + OTF_BM - 1) / OTF_BM);
-  if (ntiles > 0) otf_load_tile(a, lo, hi, j0, gs, nullptr, xs, tid, blockDim.x);
+  if (ntiles > 0) otf_load_tile(a, lo, hi, j0, gs, ts, xs, tid, blockDim.x);
   cp_async_commit();
   const int ksteps = (nin + 3) / 4;
-  const double* vrow0 = vw + (wj * 16 + (lane >> 2)) * OTF_MAX_NIN + (lane & 3);
 
   for (int it = 0; it < ntiles; ++it) {
     const int buf = it & 1;
     const int64_t r0 = lo + (int64_t)it * OTF_BM;
     if (it + 1 < ntiles)
-      otf_load_tile(a, r0 + OTF_BM, hi, j0, gs + (buf ^ 1) * OTF_BM * OTF_BJ, nullptr,
+      otf_load_tile(a, r0 + OTF_BM, hi, j0, gs + (buf ^ 1) * OTF_BM * OTF_BJ, ts + (buf ^ 1) * OTF_BM * OTF_BJ,
                     xs + (buf ^ 1) * OTF_BM * OTF_XW, tid, blockDim.x);
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
     const double* G = gs + buf * OTF_BM * OTF_BJ;
+    const double* Tt = ts + buf * OTF_BM * OTF_BJ;
     const uint64_t* X = xs + buf * OTF_BM * OTF_XW;
 
     // C = v_b (broadcast per column) + X V_W^T
-    double c[2][2][2];
+    double c[4][2][2];
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
       const int jl = wj * 16 + nt * 8 + (lane & 3) * 2;
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt) {
+      for (int mt = 0; mt < 4; ++mt) {
         c[mt][nt][0] = vb[jl];
         c[mt][nt][1] = vb[jl + 1];
       }
     }
-    uint64_t xr[2][OTF_XW];
+    uint64_t xr[4][OTF_XW];
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
+    for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-      for (int q = 0; q < OTF_XW; ++q) xr[mt][q] = X[(wr * 16 + mt * 8 + (lane >> 2)) * OTF_XW + q];
+      for (int q = 0; q < OTF_XW; ++q) xr[mt][q] = X[(wr * 32 + mt * 8 + (lane >> 2)) * OTF_XW + q];
+    const double* vrow0 = vw + (wj * 16 + (lane >> 2)) * OTF_MAX_NIN + (lane & 3);
     for (int kk = 0; kk < ksteps; ++kk) {
       const int k = kk * 4 + (lane & 3);
       const double b0 = vrow0[kk * 4];
       const double b1 = vrow0[kk * 4 + 8 * OTF_MAX_NIN];
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt) {
+      for (int mt = 0; mt < 4; ++mt) {
         const uint64_t word = (k < 64) ? xr[mt][0] : xr[mt][1];
         const double av = bit_to_double((uint32_t)(word >> (k & 63)) & 1u);
         dmma(c[mt][0][0], c[mt][0][1], av, b0);
         dmma(c[mt][1][0], c[mt][1][1], av, b1);
       }
     }
-    // epilogue: row sums of G (.) C + T (.) v_u  (T streamed from global, read once)
-    double rs[2];
+    // epilogue: row sums of G (.) C + T (.) v_u
+    double rs[4];
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt) {
-      const int rl = wr * 16 + mt * 8 + (lane >> 2);
-      const int64_t row = r0 + rl;
+    for (int mt = 0; mt < 4; ++mt) {
+      const int rl = wr * 32 + mt * 8 + (lane >> 2);
       double s = 0.0;
 #pragma unroll
       for (int nt = 0; nt < 2; ++nt) {
         const int jl = wj * 16 + nt * 8 + (lane & 3) * 2;
         const double2 g2 = *reinterpret_cast<const double2*>(G + rl * OTF_BJ + jl);
-        double2 t2 = make_double2(0.0, 0.0);
-        if (row < hi && j0 + jl < h) t2 = __ldg(reinterpret_cast<const double2*>(a.T + row * h + j0 + jl));
+        const double2 t2 = *reinterpret_cast<const double2*>(Tt + rl * OTF_BJ + jl);
         s = fma(g2.x, c[mt][nt][0], s);
         s = fma(g2.y, c[mt][nt][1], s);
         s = fma(t2.x, vu[jl], s);
@@ -190,7 +189,7 @@ __global__ void __launch_bounds__(256, 2) k_otf_dot(const OtfArgs a) {
     }
     if ((lane & 3) == 0) {
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt) red[wj * OTF_BM + wr * 16 + mt * 8 + (lane >> 2)] = rs[mt];
+      for (int mt = 0; mt < 4; ++mt) red[wj * OTF_BM + wr * 32 + mt * 8 + (lane >> 2)] = rs[mt];
     }
     __syncthreads();
     if (tid < OTF_BM) {
@@ -236,7 +235,7 @@ __global__ void __launch_bounds__(256) k_otf_y(const double* __restrict__ tpart,
 
 // grid (JC, nb), 256 threads (warp w owns hidden units j0 + 8w .. +7):
 // part[blk][j][kc] = sum_rows y g_j x_kc (kc = n_in is the ones column), partu = sum y t_j
-__global__ void __launch_bounds__(256, 2) k_otf_acc(const OtfArgs a) {
+__global__ void __launch_bounds__(256) k_otf_acc(const OtfArgs a) {
   extern __shared__ __align__(16) unsigned char smem_o[];
   double* gs = reinterpret_cast<double*>(smem_o);           // [2][BM][BJ]
   double* ts = gs + 2 * OTF_BM * OTF_BJ;                     // [2][BM][BJ]
