@@ -304,6 +304,10 @@ int launch_stream(const Plan& p, const StreamArgs& a, cudaStream_t st) {
   args.C = p.C;
   args.nb = p.nb;
   args.stages = p.NS;
+  {
+    static const int dbg = getenv("IRL_DEBUG") ? atoi(getenv("IRL_DEBUG")) : 0;
+    args.dbg = dbg;
+  }
   void* kargs[] = {&args};
   return cuda_check(cudaLaunchKernelExC(&cfg, (const void*)p.fn, kargs), "stream kernel launch");
 }

@@ -41,6 +41,7 @@ struct StreamArgs {
   int C;       // column slices (cluster size in MODE_FUSED)
   int nb;      // row blocks (clusters in MODE_FUSED)
   int stages;  // ring depth
+  int dbg;     // development flags (bit 0: skip the DSMEM exchange -- wrong results, timing only)
   // input vectors (unit-indexed).  real: v_re is the f64 array viewed as units;
   // complex: planar re/im (im may be null = 0).
   const double* v_re;
@@ -99,6 +100,7 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
   double* pro_g = reinterpret_cast<double*>(pro_s + 1);  // [1]
 
   const bool clustered = (MODE == MODE_FUSED) && (C > 1);
+  const bool xchg = clustered && !(a.dbg & 1);
   int rank, blk;
   if (MODE == MODE_FUSED) {
     rank = clustered ? (int)cluster_rank() : 0;
@@ -279,7 +281,7 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
       const int b = g % kXchSlots;
       if constexpr (MODE == MODE_DOT) {
         if (lane < rows) reinterpret_cast<S*>(a.tpart)[(int64_t)rank * N + lo + (int64_t)g * R + lane] = t;
-      } else if (clustered) {
+      } else if (xchg) {
         if (lane == 0) mbar_arrive_expect_tx(&xbar[b], (uint32_t)(C * rows * sizeof(S)));
         if (lane < rows) {
           const uint32_t la = smem_addr(&xch[(b * C + rank) * R + lane]);
@@ -302,7 +304,7 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
       S t = tin;
       if constexpr (MODE == MODE_FUSED) {
         const int b = g % kXchSlots;
-        if (clustered) {
+        if (xchg) {
           mbar_wait(&xbar[b], (g / kXchSlots) & 1);
           t = T::zero();
           if (lane < rows)
@@ -379,7 +381,7 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
           load_coeffs(g + 1, cn0, cn1, tn);
           dot_group(g + 1, pd);  // lookahead: its barrier also publishes tslot[g] (C == 1)
           advance(pd);
-        } else if (!clustered) {
+        } else if (!xchg) {
           named_bar_sync(1, NT);  // publish the last group's tslot
         }
         acc_group(g, pa, T::zero(), cf0, cf1);
