@@ -373,17 +373,13 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
     // g+1..g+L are reduced (and their partials sent) before group g is
     // accumulated; per-row coefficients ride in a 3-register rotation.
     const int L = (xchg && NS >= 4) ? 2 : 1;
-    S cf[2], dummy1, dummy2;
-    cf[0] = cf[1] = T::zero();
+    S cf[3], dummy1, dummy2;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) cf[q] = T::zero();
     Pos pa{0, 0}, pd{0, 0};
-    if (G > 0) {
-      load_coeffs(0, cf[0], dummy1, dummy2);
-      dot_group(0, pd);
-      advance(pd);
-    }
-    if (L == 2 && G > 1) {
-      load_coeffs(1, cf[1], dummy1, dummy2);
-      dot_group(1, pd);
+    for (int j = 0; j < L && j < G; ++j) {
+      load_coeffs(j, cf[j], dummy1, dummy2);
+      dot_group(j, pd);
       advance(pd);
     }
     for (int g = 0; g < G; ++g) {
@@ -397,12 +393,9 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
       }
       acc_group(g, pa, T::zero(), cf[0], T::zero());
       advance(pa);
-      if (L == 2) {  // coefficients of groups g+1.. shift down; the new one lands at L-1
-        cf[0] = cf[1];
-        cf[1] = cnew;
-      } else {
-        cf[0] = cnew;
-      }
+      cf[0] = cf[1];
+      cf[1] = cf[2];
+      cf[L] = cnew;
     }
   } else {
     Pos p{0, 0};
