@@ -369,33 +369,25 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
       if (lane == 0) mbar_arrive(&empty[p.s]);
     }
   } else if constexpr (MODE == MODE_FUSED) {
-    // lookahead L (1, or 2 for exchanged clusters with >= 4 stages): groups
-    // g+1..g+L are reduced (and their partials sent) before group g is
-    // accumulated; per-row coefficients ride in a 3-register rotation.
-    const int L = (xchg && NS >= 4) ? 2 : 1;
-    S cf[3], dummy1, dummy2;
-#pragma unroll
-    for (int q = 0; q < 3; ++q) cf[q] = T::zero();
-    Pos pa{0, 0}, pd{0, 0};
-    for (int j = 0; j < L && j < G; ++j) {
-      load_coeffs(j, cf[j], dummy1, dummy2);
-      dot_group(j, pd);
+    if (G > 0) {
+      S cf0, cf1, tin;
+      load_coeffs(0, cf0, cf1, tin);
+      Pos pa{0, 0}, pd{0, 0};
+      dot_group(0, pd);
       advance(pd);
-    }
-    for (int g = 0; g < G; ++g) {
-      S cnew = T::zero();
-      if (g + L < G) {
-        load_coeffs(g + L, cnew, dummy1, dummy2);
-        dot_group(g + L, pd);  // its barrier also publishes tslot[g] (C == 1)
-        advance(pd);
-      } else if (!xchg && g + 1 == G) {
-        named_bar_sync(1, NT);  // publish the last group's tslot
+      for (int g = 0; g < G; ++g) {
+        S cn0 = T::zero(), cn1 = T::zero(), tn = T::zero();
+        if (g + 1 < G) {
+          load_coeffs(g + 1, cn0, cn1, tn);
+          dot_group(g + 1, pd);  // lookahead: its barrier also publishes tslot[g] (C == 1)
+          advance(pd);
+        } else if (!xchg) {
+          named_bar_sync(1, NT);  // publish the last group's tslot
+        }
+        acc_group(g, pa, T::zero(), cf0, cf1);
+        advance(pa);
+        cf0 = cn0;
       }
-      acc_group(g, pa, T::zero(), cf[0], T::zero());
-      advance(pa);
-      cf[0] = cf[1];
-      cf[1] = cf[2];
-      cf[L] = cnew;
     }
   } else {
     Pos p{0, 0};
