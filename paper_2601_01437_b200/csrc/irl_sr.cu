@@ -503,8 +503,12 @@ int make_oplan(int64_t ld_u, bool cplx, int model, OPlan& p) {
   IRL_TRY(dev_info(d));
   // write-bound: prefer few units per thread (low registers, several CTAs per
   // SM with independent row barriers); column tiles may be uneven
-  for (int64_t C = 1; C <= 4096; ++C) {
+  const char* fc = getenv("IRL_OBUILD_C");     // tuning overrides
+  const char* fp = getenv("IRL_OBUILD_PPT");
+  const int c_force = fc ? atoi(fc) : 0, p_force = fp ? atoi(fp) : 0;
+  for (int64_t C = std::max(1, c_force); C <= 4096; ++C) {
     for (int ppt : {1, 2, 4, 8}) {
+      if (p_force && ppt != p_force) continue;
       const int64_t W = cdiv(ld_u, C);
       int64_t nt = rup(cdiv(W, ppt), 32);
       if (nt > 512) continue;
