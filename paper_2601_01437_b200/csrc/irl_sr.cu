@@ -125,7 +125,7 @@ size_t stream_extra_smem(bool cplx, int R, int C, int NS) {
 }
 
 // Geometry for C column slices (uneven split, slot width Wmax = ceil(ld_u / C)).
-bool choose_geom(int64_t ld_u, int C, bool cplx, int mode, int budget, Plan& p) {
+bool choose_geom(int64_t ld_u, int C, bool cplx, int mode, int budget, Plan& p, int ns_cap = 8) {
   if (C < 1 || C > ld_u) return false;
   const int64_t W = cdiv(ld_u, C);
   if (W > INT_MAX / 16) return false;
@@ -149,7 +149,7 @@ bool choose_geom(int64_t ld_u, int C, bool cplx, int mode, int budget, Plan& p) 
   const int R = (4 * slice <= 64 * 1024) ? 4 : (2 * slice <= 64 * 1024) ? 2 : 1;
   const size_t extra = stream_extra_smem(cplx, R, C, 8);
   if ((size_t)budget <= extra) return false;
-  int NS = (int)std::min<size_t>(8, ((size_t)budget - extra) / (R * slice));
+  int NS = (int)std::min<size_t>((size_t)ns_cap, ((size_t)budget - extra) / (R * slice));
   if (NS < 2) return false;
   p.mode = mode;
   p.C = C;
@@ -191,19 +191,19 @@ int active_clusters(const Plan& p, int sms) {
 }
 
 struct PlanKey {
-  int64_t ld_u;
+  int64_t n, ld_u;
   int cplx, mode, dev;
   bool operator==(const PlanKey& o) const {
-    return ld_u == o.ld_u && cplx == o.cplx && mode == o.mode && dev == o.dev;
+    return n == o.n && ld_u == o.ld_u && cplx == o.cplx && mode == o.mode && dev == o.dev;
   }
 };
 struct PlanKeyHash {
   size_t operator()(const PlanKey& k) const {
-    return std::hash<int64_t>()(k.ld_u * 131 + k.cplx * 17 + k.mode * 3 + k.dev * 7919);
+    return std::hash<int64_t>()(k.ld_u * 131 + k.n * 1000003 + k.cplx * 17 + k.mode * 3 + k.dev * 7919);
   }
 };
 
-int make_plan_uncached(int64_t ld_u, bool cplx, int mode, Plan& out) {
+int make_plan_uncached(int64_t n, int64_t ld_u, bool cplx, int mode, Plan& out) {
   DevInfo d;
   IRL_TRY(dev_info(d));
   const int budget = d.smem_optin;
@@ -225,6 +225,22 @@ int make_plan_uncached(int64_t ld_u, bool cplx, int mode, Plan& out) {
         IRL_TRY(occupancy_blocks(p, occ));
         p.nb = d.sms * occ;
         active = p.nb;
+        // short problems: each CTA would see only a few row groups, so trade
+        // ring depth for a second CTA per SM (twice the warps, half the chain)
+        if (occ == 1 && n < (int64_t)d.sms * 8 * p.R * p.NS) {
+          Plan q;
+          const size_t extra = stream_extra_smem(cplx, p.R, 1, 3);
+          const size_t stage = (size_t)p.R * p.W * 16;
+          const int ns2 = (int)(((size_t)budget / 2 - 1024 - extra) / stage);
+          if (ns2 >= 3 && choose_geom(ld_u, 1, cplx, mode, budget, q, ns2)) {
+            int occ2 = 0;
+            IRL_TRY(occupancy_blocks(q, occ2));
+            if (occ2 >= 2) {
+              q.nb = d.sms * occ2;
+              p = q;
+            }
+          }
+        }
       } else {
         p.nb = active_clusters(p, d.sms);
         active = p.nb * C;
@@ -254,7 +270,6 @@ int make_plan_uncached(int64_t ld_u, bool cplx, int mode, Plan& out) {
 }
 
 int make_plan(int64_t n, int64_t ld_u, bool cplx, int mode, Plan& p) {
-  (void)n;
   static std::mutex mu;
   struct Entry {
     int rc;
@@ -264,7 +279,7 @@ int make_plan(int64_t n, int64_t ld_u, bool cplx, int mode, Plan& p) {
   static std::unordered_map<PlanKey, Entry, PlanKeyHash> cache;
   int dev = 0;
   IRL_TRY(cuda_check(cudaGetDevice(&dev), "cudaGetDevice"));
-  PlanKey key{ld_u, cplx ? 1 : 0, mode, dev};
+  PlanKey key{n, ld_u, cplx ? 1 : 0, mode, dev};
   {
     std::lock_guard<std::mutex> lk(mu);
     auto it = cache.find(key);
@@ -275,7 +290,7 @@ int make_plan(int64_t n, int64_t ld_u, bool cplx, int mode, Plan& p) {
     }
   }
   Plan q;
-  const int rc = make_plan_uncached(ld_u, cplx, mode, q);
+  const int rc = make_plan_uncached(n, ld_u, cplx, mode, q);
   const std::string err = rc != IRL_OK ? g_err : std::string();
   std::lock_guard<std::mutex> lk(mu);
   cache[key] = Entry{rc, q, err};
@@ -322,12 +337,15 @@ int launch_finish_mvp(const double2* part, int nb, int64_t ld_u, const void* ysu
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.gridDim = dim3((unsigned)cdiv(ld_u, 32));
+  // units per block: 32 normally; narrow vectors spread the nb-way sums over
+  // more row groups per block so the grid still covers the SMs
+  const int upb = ld_u >= 32 * 148 ? 32 : (ld_u >= 16 * 148 ? 16 : 8);
+  cfg.gridDim = dim3((unsigned)cdiv(ld_u, upb));
   cfg.blockDim = dim3(256);
   cfg.stream = st;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cuda_check(cudaLaunchKernelEx(&cfg, k_finish_mvp<CPLX>, part, nb, ld_u, ysum, obar, hf_re, hf_im, u0,
+  return cuda_check(cudaLaunchKernelEx(&cfg, k_finish_mvp<CPLX>, part, nb, ld_u, upb, ysum, obar, hf_re, hf_im, u0,
                                        out_re, out_im, gpart, n_gpart, out0),
                     "finish kernel launch");
 }

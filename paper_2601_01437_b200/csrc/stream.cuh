@@ -419,7 +419,7 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
 //
 // out = sum_b part[b] - conj(obar) * sum_b ysum[b]  (+ u0 * hf)    ; out0 = sum gpart
 template <bool CPLX>
-__global__ void __launch_bounds__(256) k_finish_mvp(const double2* __restrict__ part, int nb, int64_t ld_u,
+__global__ void __launch_bounds__(256) k_finish_mvp(const double2* __restrict__ part, int nb, int64_t ld_u, int upb,
                                                     const void* ysum, const double2* __restrict__ obar,
                                                     const double* hf_re, const double* hf_im, const double* u0,
                                                     double* out_re, double* out_im, const double* gpart,
@@ -427,32 +427,37 @@ __global__ void __launch_bounds__(256) k_finish_mvp(const double2* __restrict__ 
   using T = Traits<CPLX>;
   using S = typename T::S;
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  __shared__ double2 sh[8][33];
-  __shared__ S shy[8];
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  // Y = sum_b ysum[b]: each warp a strided fixed-order partial, then 8 in order
-  const S* ysv = reinterpret_cast<const S*>(ysum);
-  S yp = T::zero();
-  for (int b = tx; b < nb; b += 32) yp = T::add(yp, ysv[b]);
-  yp = warp_sum<CPLX>(yp);
-  if (ty == 0 && tx == 0) shy[0] = yp;
-  const int64_t i = blockIdx.x * 32 + tx;
+  __shared__ double2 sh[256];
+  __shared__ S shy[1];
+  // upb units x (256 / upb) row groups per block
+  const int groups = 256 / upb;
+  const int tx = threadIdx.x % upb, ty = threadIdx.x / upb;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // Y = sum_b ysum[b]: warp 0, fixed-order strided partial + butterfly
+  if (warp == 0) {
+    const S* ysv = reinterpret_cast<const S*>(ysum);
+    S yp = T::zero();
+    for (int b = lane; b < nb; b += 32) yp = T::add(yp, ysv[b]);
+    yp = warp_sum<CPLX>(yp);
+    if (lane == 0) shy[0] = yp;
+  }
+  const int64_t i = blockIdx.x * (int64_t)upb + tx;
   double2 acc = make_double2(0.0, 0.0);
   if (i < ld_u) {
-    for (int b = ty; b < nb; b += 8) {
+    for (int b = ty; b < nb; b += groups) {
       const double2 p = part[(int64_t)b * ld_u + i];
       acc.x += p.x;
       acc.y += p.y;
     }
   }
-  sh[ty][tx] = acc;
+  sh[threadIdx.x] = acc;
   __syncthreads();
   if (ty == 0) {
     const S Y = shy[0];
-    acc = sh[0][tx];
-    for (int k = 1; k < 8; ++k) {
-      acc.x += sh[k][tx].x;
-      acc.y += sh[k][tx].y;
+    acc = sh[tx];
+    for (int k = 1; k < groups; ++k) {
+      acc.x += sh[k * upb + tx].x;
+      acc.y += sh[k * upb + tx].y;
     }
     if (i < ld_u) {
       if (obar) {
