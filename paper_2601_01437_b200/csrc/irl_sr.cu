@@ -554,16 +554,29 @@ size_t obuild_bytes(const OPlan& p, int model, int64_t n, int hidden, int64_t ld
   const size_t sS = cplx ? 16 : 8;
   size_t b = align256((size_t)n * hidden * sS);                    // t
   if (model == MODEL_MLP) b += align256((size_t)n * hidden * 8);    // g
+  b += align256((size_t)n * OTF_XW * 8);                           // packed inputs
   b += 2 * align256((size_t)p.nb * ld_u * 16);                     // partials
   return b;
 }
 
 template <bool CPLX, int MODEL>
-int launch_hidden(const uint8_t* x, int64_t n, int n_vis, int hidden, const void* Wm, const void* bvec,
-                  const double* uvec, void* T, double* G, cudaStream_t st) {
+int launch_hidden(const uint8_t* x, const uint64_t* xbits, int64_t n, int n_vis, int hidden, const void* Wm,
+                  const void* bvec, const double* uvec, void* T, double* G, cudaStream_t st) {
   using S = typename Traits<CPLX>::S;
   DevInfo d;
   IRL_TRY(dev_info(d));
+  if (xbits && n_vis <= OTF_MAX_NIN && (CPLX || (hidden & 1) == 0)) {
+    // FP64 tensor-core path (DMMA): PRE = X W^T + b, activation in the epilogue
+    auto fn = k_hidden_mma<CPLX, MODEL>;
+    const size_t smem = (size_t)(64 * OTF_MAX_NIN + 64) * 8;
+    IRL_TRY(ensure_fn_attrs((const void*)fn, d.smem_optin));
+    const int ncols = CPLX ? 2 * hidden : hidden;
+    const int jc = (int)cdiv(ncols, 64);
+    const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 64), cdiv((int64_t)d.sms * 4, jc)));
+    fn<<<dim3((unsigned)jc, (unsigned)nb), 256, smem, st>>>(xbits, n, n_vis, hidden, (const double*)Wm,
+                                                           (const double*)bvec, uvec, (double*)T, G, nb);
+    return cuda_check(cudaGetLastError(), "hidden (mma) kernel launch");
+  }
   const size_t smem = (size_t)n_vis * 32 * sizeof(S);
   if (smem > (size_t)d.smem_optin) return fail(IRL_ERR_ARG, "n_vis too large");
   auto fn = k_hidden<CPLX, MODEL>;
@@ -573,6 +586,13 @@ int launch_hidden(const uint8_t* x, int64_t n, int n_vis, int hidden, const void
   dim3 grid((unsigned)rb, (unsigned)jt);
   fn<<<grid, 256, smem, st>>>(x, n, n_vis, hidden, (const S*)Wm, (const S*)bvec, uvec, (S*)T, G);
   return cuda_check(cudaGetLastError(), "hidden kernel launch");
+}
+
+int pack_bits(const uint8_t* x, int64_t n, int n_vis, uint64_t* xbits, cudaStream_t st) {
+  DevInfo d;
+  IRL_TRY(dev_info(d));
+  k_pack_bits<<<(unsigned)std::min<int64_t>(cdiv(n, 256), 4 * d.sms), 256, 0, st>>>(x, n, n_vis, xbits);
+  return cuda_check(cudaGetLastError(), "pack bits launch");
 }
 
 int obuild_impl(bool cplx, int model, const uint8_t* x, int64_t n, int n_vis, int hidden, const double* theta,
@@ -601,18 +621,24 @@ int obuild_impl(bool cplx, int model, const uint8_t* x, int64_t n, int n_vis, in
   double2* part0 = reinterpret_cast<double2*>(base + off);
   off += align256((size_t)p.nb * ld_u * 16);
   double2* part1 = reinterpret_cast<double2*>(base + off);
+  off += align256((size_t)p.nb * ld_u * 16);
+  uint64_t* xbits = nullptr;
+  if (n_vis <= OTF_MAX_NIN) {
+    xbits = reinterpret_cast<uint64_t*>(base + off);
+    IRL_TRY(pack_bits(x, n, n_vis, xbits, st));
+  }
   if (model == MODEL_RBM) {
     const double* bvec = theta + (size_t)n_vis * (cplx ? 2 : 1);
     const double* Wm = theta + (size_t)(n_vis + hidden) * (cplx ? 2 : 1);
     if (cplx)
-      IRL_TRY((launch_hidden<true, MODEL_RBM>(x, n, n_vis, hidden, Wm, bvec, nullptr, T, nullptr, st)));
+      IRL_TRY((launch_hidden<true, MODEL_RBM>(x, xbits, n, n_vis, hidden, Wm, bvec, nullptr, T, nullptr, st)));
     else
-      IRL_TRY((launch_hidden<false, MODEL_RBM>(x, n, n_vis, hidden, Wm, bvec, nullptr, T, nullptr, st)));
+      IRL_TRY((launch_hidden<false, MODEL_RBM>(x, xbits, n, n_vis, hidden, Wm, bvec, nullptr, T, nullptr, st)));
   } else {
     const double* Wm = theta;
     const double* bvec = theta + (size_t)hidden * n_vis;
     const double* uvec = bvec + hidden;
-    IRL_TRY((launch_hidden<false, MODEL_MLP>(x, n, n_vis, hidden, Wm, bvec, uvec, T, G, st)));
+    IRL_TRY((launch_hidden<false, MODEL_MLP>(x, xbits, n, n_vis, hidden, Wm, bvec, uvec, T, G, st)));
   }
   ORowArgs a{};
   a.x = x;
@@ -798,14 +824,14 @@ int irl_obuild_mlp_f64(const uint8_t* x, int64_t n, int n_in, int hidden, const 
 int irl_hidden_rbm_f64(const uint8_t* x, int64_t n, int n_vis, int hidden, const double* theta, double* t,
                        void* stream) {
   if (!x || !theta || !t || n < 1 || n_vis < 1 || hidden < 1) return fail(IRL_ERR_ARG, "bad hidden arguments");
-  return launch_hidden<false, MODEL_RBM>(x, n, n_vis, hidden, theta + n_vis + hidden, theta + n_vis, nullptr, t,
-                                         nullptr, (cudaStream_t)stream);
+  return launch_hidden<false, MODEL_RBM>(x, nullptr, n, n_vis, hidden, theta + n_vis + hidden, theta + n_vis, nullptr,
+                                         t, nullptr, (cudaStream_t)stream);
 }
 
 int irl_hidden_rbm_c128(const uint8_t* x, int64_t n, int n_vis, int hidden, const double* theta, double* t,
                         void* stream) {
   if (!x || !theta || !t || n < 1 || n_vis < 1 || hidden < 1) return fail(IRL_ERR_ARG, "bad hidden arguments");
-  return launch_hidden<true, MODEL_RBM>(x, n, n_vis, hidden, theta + 2 * (n_vis + hidden), theta + 2 * n_vis,
+  return launch_hidden<true, MODEL_RBM>(x, nullptr, n, n_vis, hidden, theta + 2 * (n_vis + hidden), theta + 2 * n_vis,
                                         nullptr, t, nullptr, (cudaStream_t)stream);
 }
 
@@ -813,7 +839,7 @@ int irl_hidden_mlp_f64(const uint8_t* x, int64_t n, int n_in, int hidden, const 
                        double* g, void* stream) {
   if (!x || !theta || !t || !g || n < 1 || n_in < 1 || hidden < 1) return fail(IRL_ERR_ARG, "bad hidden arguments");
   const double* bvec = theta + (size_t)hidden * n_in;
-  return launch_hidden<false, MODEL_MLP>(x, n, n_in, hidden, theta, bvec, bvec + hidden, t, g,
+  return launch_hidden<false, MODEL_MLP>(x, nullptr, n, n_in, hidden, theta, bvec, bvec + hidden, t, g,
                                          (cudaStream_t)stream);
 }
 
@@ -868,10 +894,9 @@ int irl_otf_prepare_mlp_f64(const uint8_t* x, int64_t n, int n_in, int hidden, c
   cudaStream_t st = (cudaStream_t)stream;
   DevInfo d;
   IRL_TRY(dev_info(d));
-  k_pack_bits<<<(unsigned)std::min<int64_t>(cdiv(n, 256), 4 * d.sms), 256, 0, st>>>(x, n, n_in, xbits);
-  IRL_TRY(cuda_check(cudaGetLastError(), "pack bits launch"));
+  IRL_TRY(pack_bits(x, n, n_in, xbits, st));
   const double* bvec = theta + (size_t)hidden * n_in;
-  return launch_hidden<false, MODEL_MLP>(x, n, n_in, hidden, theta, bvec, bvec + hidden, t, g, st);
+  return launch_hidden<false, MODEL_MLP>(x, xbits, n, n_in, hidden, theta, bvec, bvec + hidden, t, g, st);
 }
 
 int irl_otf_colstats_mlp_f64(const uint64_t* xbits, const double* t, const double* g, int64_t n, int n_in, int hidden,

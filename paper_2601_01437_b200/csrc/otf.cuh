@@ -16,6 +16,7 @@
 // (est:167, est:156-163) without ever materialising O.
 #pragma once
 #include "common.cuh"
+#include "obuild.cuh"
 
 namespace irl {
 
@@ -408,6 +409,106 @@ __global__ void __launch_bounds__(256) k_vsum(const double* __restrict__ y, int6
     double t = 0.0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s[w];
     part[blockIdx.x] = t;
+  }
+}
+}  // namespace irl
+
+namespace irl {
+// Hidden layer on FP64 tensor cores (the MLP "forward contraction" of the north
+// star; also the RBM's theta = b + W x): PRE = X W^T + b for a 64-column chunk
+// of the (real) weight matrix, then the activation epilogue.
+//   real    : columns = hidden units;            T = tanh(PRE), MLP: G = u (1 - T^2)
+//   complex : columns (2j, 2j+1) = (Re, Im) of W row j, so each C fragment pair
+//             holds one complex theta_j;       T = tanh(theta) (complex)
+// grid (ceil(ncols/64), nb), 256 threads; X as packed bits (n_in <= 100).
+template <bool CPLX, int MODEL>
+__global__ void __launch_bounds__(256) k_hidden_mma(const uint64_t* __restrict__ xbits, int64_t n_rows, int n_in,
+                                                    int hidden, const double* __restrict__ Wm,
+                                                    const double* __restrict__ bvec, const double* __restrict__ uvec,
+                                                    double* __restrict__ Tout, double* __restrict__ Gout, int nb) {
+  extern __shared__ __align__(16) unsigned char smem_h2[];
+  double* ws = reinterpret_cast<double*>(smem_h2);  // [64][OTF_MAX_NIN] weight chunk (real columns)
+  double* bs = ws + 64 * OTF_MAX_NIN;              // [64]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wr = warp >> 2, wj = warp & 3;
+  const int ncols = CPLX ? 2 * hidden : hidden;
+  const int c0 = blockIdx.x * 64;
+  const int64_t lo = (n_rows * blockIdx.y) / nb, hi = (n_rows * (blockIdx.y + 1)) / nb;
+  // real column c <-> weight element: real: W[c][k]; complex: (Re|Im) W[c/2][k]
+  for (int e = tid; e < 64 * OTF_MAX_NIN; e += blockDim.x) {
+    const int cc = e / OTF_MAX_NIN, k = e % OTF_MAX_NIN;
+    const int col = c0 + cc;
+    double val = 0.0;
+    if (col < ncols && k < n_in) {
+      if constexpr (CPLX) val = Wm[((int64_t)(col >> 1) * n_in + k) * 2 + (col & 1)];
+      else val = Wm[(int64_t)col * n_in + k];
+    }
+    ws[e] = val;
+  }
+  for (int e = tid; e < 64; e += blockDim.x) {
+    const int col = c0 + e;
+    double bv = 0.0;
+    if (col < ncols) {
+      if constexpr (CPLX) bv = bvec[(col >> 1) * 2 + (col & 1)];
+      else bv = bvec[col];
+    }
+    bs[e] = bv;
+  }
+  __syncthreads();
+  const int ksteps = (n_in + 3) / 4;
+  const double* wrow0 = ws + (wj * 16 + (lane >> 2)) * OTF_MAX_NIN + (lane & 3);
+  for (int64_t r0 = lo; r0 < hi; r0 += 64) {
+    double c[4][2][2];
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      const int cl = wj * 16 + nt * 8 + (lane & 3) * 2;
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        c[mt][nt][0] = bs[cl];
+        c[mt][nt][1] = bs[cl + 1];
+      }
+    }
+    uint64_t xr[4][OTF_XW];
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {
+      const int64_t row = r0 + wr * 32 + mt * 8 + (lane >> 2);
+#pragma unroll
+      for (int q = 0; q < OTF_XW; ++q) xr[mt][q] = row < hi ? __ldg(xbits + row * OTF_XW + q) : 0ull;
+    }
+    for (int kk = 0; kk < ksteps; ++kk) {
+      const int k = kk * 4 + (lane & 3);
+      const double b0 = wrow0[kk * 4];
+      const double b1 = wrow0[kk * 4 + 8 * OTF_MAX_NIN];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        const uint64_t word = (k < 64) ? xr[mt][0] : xr[mt][1];
+        const double av = bit_to_double((uint32_t)(word >> (k & 63)) & 1u);
+        dmma(c[mt][0][0], c[mt][0][1], av, b0);
+        dmma(c[mt][1][0], c[mt][1][1], av, b1);
+      }
+    }
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {
+      const int64_t row = r0 + wr * 32 + mt * 8 + (lane >> 2);
+      if (row >= hi) continue;
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const int col = c0 + wj * 16 + nt * 8 + (lane & 3) * 2;
+        if (col >= ncols) continue;
+        if constexpr (CPLX) {
+          const double2 t = ctanh(make_double2(c[mt][nt][0], c[mt][nt][1]));
+          reinterpret_cast<double2*>(Tout)[row * hidden + (col >> 1)] = t;
+        } else {
+          const double t0 = tanh(c[mt][nt][0]), t1 = tanh(c[mt][nt][1]);
+          *reinterpret_cast<double2*>(Tout + row * hidden + col) = make_double2(t0, t1);
+          if (MODEL == MODEL_MLP) {
+            const double u0 = uvec[col], u1 = uvec[col + 1];
+            *reinterpret_cast<double2*>(Gout + row * hidden + col) =
+                make_double2(u0 * (1.0 - t0 * t0), u1 * (1.0 - t1 * t1));
+          }
+        }
+      }
+    }
   }
 }
 }  // namespace irl
