@@ -499,185 +499,6 @@ int colstats_impl(bool cplx, const double* O, int64_t n, int64_t ld, const doubl
   return cuda_check(cudaGetLastError(), "colstats finish launch");
 }
 
-// ------------------------------------------------------------ obuild ----
-struct OPlan {
-  int C, W, PPT, NT, nb;
-  size_t smem;
-  void (*fn)(ORowArgs, int);
-};
-
-template <bool CPLX, int MODEL>
-void (*pick_orows(int ppt))(ORowArgs, int) {
-  switch (ppt) {
-    case 1: return k_orows<CPLX, MODEL, 1>;
-    case 2: return k_orows<CPLX, MODEL, 2>;
-    case 4: return k_orows<CPLX, MODEL, 4>;
-    default: return k_orows<CPLX, MODEL, 8>;
-  }
-}
-
-int make_oplan(int64_t ld_u, bool cplx, int model, OPlan& p) {
-  DevInfo d;
-  IRL_TRY(dev_info(d));
-  // write-bound: prefer few units per thread (low registers, several CTAs per
-  // SM with independent row barriers); column tiles may be uneven
-  const char* fc = getenv("IRL_OBUILD_C");     // tuning overrides
-  const char* fp = getenv("IRL_OBUILD_PPT");
-  const int c_force = fc ? atoi(fc) : 0, p_force = fp ? atoi(fp) : 0;
-  for (int64_t C = std::max(1, c_force); C <= 4096; ++C) {
-    for (int ppt : {1, 2, 4, 8}) {
-      if (p_force && ppt != p_force) continue;
-      const int64_t W = cdiv(ld_u, C);
-      int64_t nt = rup(cdiv(W, ppt), 32);
-      if (nt > 512) continue;
-      if (nt < 64) nt = 64;
-      p.C = (int)C;
-      p.W = (int)W;
-      p.PPT = ppt;
-      p.NT = (int)nt;
-      if (cplx)
-        p.fn = pick_orows<true, MODEL_RBM>(ppt);
-      else
-        p.fn = model == MODEL_RBM ? pick_orows<false, MODEL_RBM>(ppt) : pick_orows<false, MODEL_MLP>(ppt);
-      p.smem = 0;
-      int occ = 0;
-      IRL_TRY(cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)p.fn, p.NT, 0), "occ"));
-      occ = std::max(occ, 1);
-      p.nb = std::max(1, (int)((d.sms * occ + C - 1) / C));
-      return IRL_OK;
-    }
-  }
-  return fail(IRL_ERR_DEVICE, "no O-build geometry");
-}
-
-size_t obuild_bytes(const OPlan& p, int model, int64_t n, int hidden, int64_t ld_u, bool cplx) {
-  const size_t sS = cplx ? 16 : 8;
-  size_t b = align256((size_t)n * hidden * sS);                    // t
-  if (model == MODEL_MLP) b += align256((size_t)n * hidden * 8);    // g
-  b += align256((size_t)n * OTF_XW * 8);                           // packed inputs
-  b += 2 * align256((size_t)p.nb * ld_u * 16);                     // partials
-  return b;
-}
-
-template <bool CPLX, int MODEL>
-int launch_hidden(const uint8_t* x, const uint64_t* xbits, int64_t n, int n_vis, int hidden, const void* Wm,
-                  const void* bvec, const double* uvec, void* T, double* G, cudaStream_t st) {
-  using S = typename Traits<CPLX>::S;
-  DevInfo d;
-  IRL_TRY(dev_info(d));
-  if (xbits && n_vis <= OTF_MAX_NIN && (CPLX || (hidden & 1) == 0)) {
-    // FP64 tensor-core path (DMMA): PRE = X W^T + b, activation in the epilogue
-    auto fn = k_hidden_mma<CPLX, MODEL>;
-    const size_t smem = (size_t)(64 * OTF_MAX_NIN + 64) * 8;
-    IRL_TRY(ensure_fn_attrs((const void*)fn, d.smem_optin));
-    const int ncols = CPLX ? 2 * hidden : hidden;
-    const int jc = (int)cdiv(ncols, 64);
-    const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 64), cdiv((int64_t)d.sms * 4, jc)));
-    fn<<<dim3((unsigned)jc, (unsigned)nb), 256, smem, st>>>(xbits, n, n_vis, hidden, (const double*)Wm,
-                                                           (const double*)bvec, uvec, (double*)T, G, nb);
-    return cuda_check(cudaGetLastError(), "hidden (mma) kernel launch");
-  }
-  const size_t smem = (size_t)n_vis * 32 * sizeof(S);
-  if (smem > (size_t)d.smem_optin) return fail(IRL_ERR_ARG, "n_vis too large");
-  auto fn = k_hidden<CPLX, MODEL>;
-  IRL_TRY(ensure_fn_attrs((const void*)fn, d.smem_optin));
-  const int jt = (int)cdiv(hidden, 32);
-  int64_t rb = std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 8), cdiv((int64_t)d.sms * 8, jt)));
-  dim3 grid((unsigned)rb, (unsigned)jt);
-  fn<<<grid, 256, smem, st>>>(x, n, n_vis, hidden, (const S*)Wm, (const S*)bvec, uvec, (S*)T, G);
-  return cuda_check(cudaGetLastError(), "hidden kernel launch");
-}
-
-int pack_bits(const uint8_t* x, int64_t n, int n_vis, uint64_t* xbits, cudaStream_t st) {
-  DevInfo d;
-  IRL_TRY(dev_info(d));
-  k_pack_bits<<<(unsigned)std::min<int64_t>(cdiv(n, 256), 4 * d.sms), 256, 0, st>>>(x, n, n_vis, xbits);
-  return cuda_check(cudaGetLastError(), "pack bits launch");
-}
-
-int obuild_impl(bool cplx, int model, const uint8_t* x, int64_t n, int n_vis, int hidden, const double* theta,
-                double* O, int64_t ld, const double* w, const double* coeff, double* obar, double* g, void* ws,
-                size_t ws_bytes, cudaStream_t st) {
-  if (!x || !theta || !O || !w || !coeff || !obar || !g) return fail(IRL_ERR_ARG, "null pointer");
-  if (n < 1 || n_vis < 1 || hidden < 1 || n_vis > 4095 || hidden > 65535) return fail(IRL_ERR_ARG, "bad shape");
-  const int64_t P = model == MODEL_RBM ? (int64_t)n_vis + hidden + (int64_t)hidden * n_vis
-                                       : (int64_t)hidden * n_vis + 2 * (int64_t)hidden + 1;
-  if (ld != irl_padded_ld(P, cplx)) return fail(IRL_ERR_ALIGN, "ld must equal irl_padded_ld(P=%lld)", (long long)P);
-  if (!aligned16(O) || !aligned16(obar) || !aligned16(g) || !aligned16(ws)) return fail(IRL_ERR_ALIGN, "alignment");
-  const int64_t ld_u = cplx ? ld : ld / 2;
-  OPlan p;
-  IRL_TRY(make_oplan(ld_u, cplx, model, p));
-  const size_t need = obuild_bytes(p, model, n, hidden, ld_u, cplx);
-  if (ws_bytes < need) return fail(IRL_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, need);
-  const size_t sS = cplx ? 16 : 8;
-  char* base = static_cast<char*>(ws);
-  void* T = base;
-  size_t off = align256((size_t)n * hidden * sS);
-  double* G = nullptr;
-  if (model == MODEL_MLP) {
-    G = reinterpret_cast<double*>(base + off);
-    off += align256((size_t)n * hidden * 8);
-  }
-  double2* part0 = reinterpret_cast<double2*>(base + off);
-  off += align256((size_t)p.nb * ld_u * 16);
-  double2* part1 = reinterpret_cast<double2*>(base + off);
-  off += align256((size_t)p.nb * ld_u * 16);
-  uint64_t* xbits = nullptr;
-  if (n_vis <= OTF_MAX_NIN) {
-    xbits = reinterpret_cast<uint64_t*>(base + off);
-    IRL_TRY(pack_bits(x, n, n_vis, xbits, st));
-  }
-  if (model == MODEL_RBM) {
-    const double* bvec = theta + (size_t)n_vis * (cplx ? 2 : 1);
-    const double* Wm = theta + (size_t)(n_vis + hidden) * (cplx ? 2 : 1);
-    if (cplx)
-      IRL_TRY((launch_hidden<true, MODEL_RBM>(x, xbits, n, n_vis, hidden, Wm, bvec, nullptr, T, nullptr, st)));
-    else
-      IRL_TRY((launch_hidden<false, MODEL_RBM>(x, xbits, n, n_vis, hidden, Wm, bvec, nullptr, T, nullptr, st)));
-  } else {
-    const double* Wm = theta;
-    const double* bvec = theta + (size_t)hidden * n_vis;
-    const double* uvec = bvec + hidden;
-    IRL_TRY((launch_hidden<false, MODEL_MLP>(x, xbits, n, n_vis, hidden, Wm, bvec, uvec, T, G, st)));
-  }
-  ORowArgs a{};
-  a.x = x;
-  a.n_rows = n;
-  a.n_vis = n_vis;
-  a.hidden = hidden;
-  a.p = P;
-  a.T = T;
-  a.G = G;
-  a.O = reinterpret_cast<double2*>(O);
-  a.ld_u = ld_u;
-  a.w = w;
-  a.coeff = coeff;
-  a.part0 = part0;
-  a.part1 = part1;
-  a.W = p.W;
-  a.C = p.C;
-  a.nb = p.nb;
-  const int tab_len = model == MODEL_MLP ? orow_tab_len<MODEL_MLP>(n_vis, hidden) : orow_tab_len<MODEL_RBM>(n_vis, hidden);
-  const size_t tab_bytes = (size_t)((tab_len + 1) & ~1) * sS;
-  // rows per staging group: amortise the per-group barrier, ~48 KB of tables
-  const int R = (int)std::max<size_t>(1, std::min<size_t>(8, (size_t)(24 * 1024) / tab_bytes));
-  const size_t smem = 2 * (size_t)R * tab_bytes;
-  {
-    DevInfo d;
-    IRL_TRY(dev_info(d));
-    if (smem > (size_t)d.smem_optin) return fail(IRL_ERR_ARG, "hidden layer too wide for the row table");
-    IRL_TRY(ensure_fn_attrs((const void*)p.fn, d.smem_optin));
-  }
-  p.fn<<<(unsigned)(p.nb * p.C), p.NT, smem, st>>>(a, R);
-  IRL_TRY(cuda_check(cudaGetLastError(), "orows launch"));
-  const unsigned blocks = (unsigned)cdiv(ld_u, 32);
-  if (cplx)
-    k_finish_stats<true><<<blocks, 256, 0, st>>>(part0, part1, p.nb, ld_u, (double2*)obar, (double2*)g);
-  else
-    k_finish_stats<false><<<blocks, 256, 0, st>>>(part0, part1, p.nb, ld_u, (double2*)obar, (double2*)g);
-  return cuda_check(cudaGetLastError(), "obuild finish launch");
-}
-
 // --------------------------------------------------------------- otf ----
 struct OtfPlan {
   int jc, nb, ny;
@@ -741,6 +562,236 @@ int otf_acc_launch(const OtfPlan& pl, OtfArgs& a, cudaStream_t st) {
   return cuda_check(cudaGetLastError(), "otf acc launch");
 }
 
+// ------------------------------------------------------------ obuild ----
+struct OPlan {
+  int C, W, PPT, NT, nb;
+  size_t smem;
+  void (*fn)(ORowArgs, int);
+};
+
+template <bool CPLX, int MODEL, bool STATS>
+void (*pick_orows(int ppt))(ORowArgs, int) {
+  switch (ppt) {
+    case 1: return k_orows<CPLX, MODEL, 1, STATS>;
+    case 2: return k_orows<CPLX, MODEL, 2, STATS>;
+    case 4: return k_orows<CPLX, MODEL, 4, STATS>;
+    default: return k_orows<CPLX, MODEL, 8, STATS>;
+  }
+}
+
+// real models with n_in <= 100 and an even hidden width take their column
+// statistics from the DMMA GEMM (k_otf_acc) instead of the row writer
+bool gemm_stats(bool cplx, int n_vis, int hidden) { return !cplx && n_vis <= OTF_MAX_NIN && (hidden & 1) == 0; }
+
+int make_oplan(int64_t ld_u, bool cplx, int model, OPlan& p, bool stats_in_writer) {
+  DevInfo d;
+  IRL_TRY(dev_info(d));
+  // write-bound: prefer few units per thread (low registers, several CTAs per
+  // SM with independent row barriers); column tiles may be uneven
+  const char* fc = getenv("IRL_OBUILD_C");     // tuning overrides
+  const char* fp = getenv("IRL_OBUILD_PPT");
+  const int c_force = fc ? atoi(fc) : 0, p_force = fp ? atoi(fp) : 0;
+  for (int64_t C = std::max(1, c_force); C <= 4096; ++C) {
+    for (int ppt : {1, 2, 4, 8}) {
+      if (p_force && ppt != p_force) continue;
+      const int64_t W = cdiv(ld_u, C);
+      int64_t nt = rup(cdiv(W, ppt), 32);
+      if (nt > 512) continue;
+      if (nt < 64) nt = 64;
+      p.C = (int)C;
+      p.W = (int)W;
+      p.PPT = ppt;
+      p.NT = (int)nt;
+      if (cplx)
+        p.fn = pick_orows<true, MODEL_RBM, true>(ppt);
+      else if (stats_in_writer)
+        p.fn = model == MODEL_RBM ? pick_orows<false, MODEL_RBM, true>(ppt) : pick_orows<false, MODEL_MLP, true>(ppt);
+      else
+        p.fn = model == MODEL_RBM ? pick_orows<false, MODEL_RBM, false>(ppt) : pick_orows<false, MODEL_MLP, false>(ppt);
+      p.smem = 0;
+      int occ = 0;
+      IRL_TRY(cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)p.fn, p.NT, 0), "occ"));
+      occ = std::max(occ, 1);
+      p.nb = std::max(1, (int)((d.sms * occ + C - 1) / C));
+      return IRL_OK;
+    }
+  }
+  return fail(IRL_ERR_DEVICE, "no O-build geometry");
+}
+
+size_t obuild_bytes(const OPlan& p, int model, int64_t n, int n_vis, int hidden, int64_t ld_u, bool cplx) {
+  const size_t sS = cplx ? 16 : 8;
+  size_t b = align256((size_t)n * hidden * sS);                    // t
+  if (model == MODEL_MLP) b += align256((size_t)n * hidden * 8);    // g
+  b += align256((size_t)n * OTF_XW * 8);                           // packed inputs
+  if (gemm_stats(cplx, n_vis, hidden)) {                           // DMMA stats scratch
+    OtfPlan op;
+    if (make_otf_plan(n, n_vis, hidden, op) == IRL_OK) b += otf_ws_layout(op, n, hidden, nullptr).bytes;
+    b += align256((size_t)148 * 4 * (n_vis + 1) * 8);             // x sums
+  }
+  b += 2 * align256((size_t)p.nb * ld_u * 16);                     // partials
+  return b;
+}
+
+template <bool CPLX, int MODEL>
+int launch_hidden(const uint8_t* x, const uint64_t* xbits, int64_t n, int n_vis, int hidden, const void* Wm,
+                  const void* bvec, const double* uvec, void* T, double* G, cudaStream_t st) {
+  using S = typename Traits<CPLX>::S;
+  DevInfo d;
+  IRL_TRY(dev_info(d));
+  if (xbits && n_vis <= OTF_MAX_NIN && (CPLX || (hidden & 1) == 0)) {
+    // FP64 tensor-core path (DMMA): PRE = X W^T + b, activation in the epilogue
+    auto fn = k_hidden_mma<CPLX, MODEL>;
+    const size_t smem = (size_t)(64 * OTF_MAX_NIN + 64) * 8;
+    IRL_TRY(ensure_fn_attrs((const void*)fn, d.smem_optin));
+    const int ncols = CPLX ? 2 * hidden : hidden;
+    const int jc = (int)cdiv(ncols, 64);
+    const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 64), cdiv((int64_t)d.sms * 4, jc)));
+    fn<<<dim3((unsigned)jc, (unsigned)nb), 256, smem, st>>>(xbits, n, n_vis, hidden, (const double*)Wm,
+                                                           (const double*)bvec, uvec, (double*)T, G, nb);
+    return cuda_check(cudaGetLastError(), "hidden (mma) kernel launch");
+  }
+  const size_t smem = (size_t)n_vis * 32 * sizeof(S);
+  if (smem > (size_t)d.smem_optin) return fail(IRL_ERR_ARG, "n_vis too large");
+  auto fn = k_hidden<CPLX, MODEL>;
+  IRL_TRY(ensure_fn_attrs((const void*)fn, d.smem_optin));
+  const int jt = (int)cdiv(hidden, 32);
+  int64_t rb = std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 8), cdiv((int64_t)d.sms * 8, jt)));
+  dim3 grid((unsigned)rb, (unsigned)jt);
+  fn<<<grid, 256, smem, st>>>(x, n, n_vis, hidden, (const S*)Wm, (const S*)bvec, uvec, (S*)T, G);
+  return cuda_check(cudaGetLastError(), "hidden kernel launch");
+}
+
+int pack_bits(const uint8_t* x, int64_t n, int n_vis, uint64_t* xbits, cudaStream_t st) {
+  DevInfo d;
+  IRL_TRY(dev_info(d));
+  k_pack_bits<<<(unsigned)std::min<int64_t>(cdiv(n, 256), 4 * d.sms), 256, 0, st>>>(x, n, n_vis, xbits);
+  return cuda_check(cudaGetLastError(), "pack bits launch");
+}
+
+int obuild_impl(bool cplx, int model, const uint8_t* x, int64_t n, int n_vis, int hidden, const double* theta,
+                double* O, int64_t ld, const double* w, const double* coeff, double* obar, double* g, void* ws,
+                size_t ws_bytes, cudaStream_t st) {
+  if (!x || !theta || !O || !w || !coeff || !obar || !g) return fail(IRL_ERR_ARG, "null pointer");
+  if (n < 1 || n_vis < 1 || hidden < 1 || n_vis > 4095 || hidden > 65535) return fail(IRL_ERR_ARG, "bad shape");
+  const int64_t P = model == MODEL_RBM ? (int64_t)n_vis + hidden + (int64_t)hidden * n_vis
+                                       : (int64_t)hidden * n_vis + 2 * (int64_t)hidden + 1;
+  if (ld != irl_padded_ld(P, cplx)) return fail(IRL_ERR_ALIGN, "ld must equal irl_padded_ld(P=%lld)", (long long)P);
+  if (!aligned16(O) || !aligned16(obar) || !aligned16(g) || !aligned16(ws)) return fail(IRL_ERR_ALIGN, "alignment");
+  const int64_t ld_u = cplx ? ld : ld / 2;
+  const bool gstats = gemm_stats(cplx, n_vis, hidden);
+  OPlan p;
+  IRL_TRY(make_oplan(ld_u, cplx, model, p, !gstats));
+  const size_t need = obuild_bytes(p, model, n, n_vis, hidden, ld_u, cplx);
+  if (ws_bytes < need) return fail(IRL_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, need);
+  const size_t sS = cplx ? 16 : 8;
+  char* base = static_cast<char*>(ws);
+  void* T = base;
+  size_t off = align256((size_t)n * hidden * sS);
+  double* G = nullptr;
+  if (model == MODEL_MLP) {
+    G = reinterpret_cast<double*>(base + off);
+    off += align256((size_t)n * hidden * 8);
+  }
+  double2* part0 = reinterpret_cast<double2*>(base + off);
+  off += align256((size_t)p.nb * ld_u * 16);
+  double2* part1 = reinterpret_cast<double2*>(base + off);
+  off += align256((size_t)p.nb * ld_u * 16);
+  uint64_t* xbits = nullptr;
+  if (n_vis <= OTF_MAX_NIN) {
+    xbits = reinterpret_cast<uint64_t*>(base + off);
+    IRL_TRY(pack_bits(x, n, n_vis, xbits, st));
+  }
+  off += align256((size_t)n * OTF_XW * 8);
+  if (model == MODEL_RBM) {
+    const double* bvec = theta + (size_t)n_vis * (cplx ? 2 : 1);
+    const double* Wm = theta + (size_t)(n_vis + hidden) * (cplx ? 2 : 1);
+    if (cplx)
+      IRL_TRY((launch_hidden<true, MODEL_RBM>(x, xbits, n, n_vis, hidden, Wm, bvec, nullptr, T, nullptr, st)));
+    else
+      IRL_TRY((launch_hidden<false, MODEL_RBM>(x, xbits, n, n_vis, hidden, Wm, bvec, nullptr, T, nullptr, st)));
+  } else {
+    const double* Wm = theta;
+    const double* bvec = theta + (size_t)hidden * n_vis;
+    const double* uvec = bvec + hidden;
+    IRL_TRY((launch_hidden<false, MODEL_MLP>(x, xbits, n, n_vis, hidden, Wm, bvec, uvec, T, G, st)));
+  }
+  ORowArgs a{};
+  a.x = x;
+  a.n_rows = n;
+  a.n_vis = n_vis;
+  a.hidden = hidden;
+  a.p = P;
+  a.T = T;
+  a.G = G;
+  a.O = reinterpret_cast<double2*>(O);
+  a.ld_u = ld_u;
+  a.w = w;
+  a.coeff = coeff;
+  a.part0 = part0;
+  a.part1 = part1;
+  a.W = p.W;
+  a.C = p.C;
+  a.nb = p.nb;
+  const int tab_len = model == MODEL_MLP ? orow_tab_len<MODEL_MLP>(n_vis, hidden) : orow_tab_len<MODEL_RBM>(n_vis, hidden);
+  const size_t tab_bytes = (size_t)((tab_len + 1) & ~1) * sS;
+  // rows per staging group: amortise the per-group barrier, ~48 KB of tables
+  const int R = (int)std::max<size_t>(1, std::min<size_t>(8, (size_t)(24 * 1024) / tab_bytes));
+  const size_t smem = 2 * (size_t)R * tab_bytes;
+  {
+    DevInfo d;
+    IRL_TRY(dev_info(d));
+    if (smem > (size_t)d.smem_optin) return fail(IRL_ERR_ARG, "hidden layer too wide for the row table");
+    IRL_TRY(ensure_fn_attrs((const void*)p.fn, d.smem_optin));
+  }
+  p.fn<<<(unsigned)(p.nb * p.C), p.NT, smem, st>>>(a, R);
+  IRL_TRY(cuda_check(cudaGetLastError(), "orows launch"));
+  if (gstats) {
+    // column statistics from the hidden activations and the packed inputs
+    OtfPlan op;
+    IRL_TRY(make_otf_plan(n, n_vis, hidden, op));
+    OtfWs wl = otf_ws_layout(op, n, hidden, base + off);
+    off += align256(wl.bytes);
+    double* xpart = reinterpret_cast<double*>(base + off);
+    OtfArgs oa{};
+    oa.xbits = xbits;
+    oa.T = reinterpret_cast<const double*>(T);
+    oa.G = model == MODEL_MLP ? G : reinterpret_cast<const double*>(T);
+    oa.n_rows = n;
+    oa.n_in = n_vis;
+    oa.hidden = hidden;
+    oa.part = wl.part;
+    oa.partu = wl.partu;
+    const double* ys[2] = {w, coeff};
+    double* outs[2] = {obar, g};
+    DevInfo d;
+    IRL_TRY(dev_info(d));
+    const int nbx = std::min<int>(4 * d.sms, (int)std::max<int64_t>(1, n / 64));
+    for (int q = 0; q < 2; ++q) {
+      oa.y = ys[q];
+      IRL_TRY(otf_acc_launch(op, oa, st));
+      if (model == MODEL_MLP) {
+        k_vsum<<<op.ny, 256, 0, st>>>(ys[q], n, wl.ypart);
+        k_otf_finish<<<(unsigned)cdiv(ld, 256), 256, 0, st>>>(wl.part, wl.partu, op.nb, hidden, n_vis, ld, wl.ypart,
+                                                             op.ny, nullptr, nullptr, nullptr, nullptr, 0, outs[q],
+                                                             nullptr);
+      } else {
+        k_xsum<<<nbx, 128, 0, st>>>(xbits, ys[q], n, n_vis, xpart, wl.ypart);
+        k_rbm_stats_finish<<<(unsigned)cdiv(ld, 256), 256, 0, st>>>(wl.part, op.nb, hidden, n_vis, xpart, nbx, ld,
+                                                                    outs[q]);
+      }
+      IRL_TRY(cuda_check(cudaGetLastError(), "gemm stats launch"));
+    }
+    return IRL_OK;
+  }
+  const unsigned blocks = (unsigned)cdiv(ld_u, 32);
+  if (cplx)
+    k_finish_stats<true><<<blocks, 256, 0, st>>>(part0, part1, p.nb, ld_u, (double2*)obar, (double2*)g);
+  else
+    k_finish_stats<false><<<blocks, 256, 0, st>>>(part0, part1, p.nb, ld_u, (double2*)obar, (double2*)g);
+  return cuda_check(cudaGetLastError(), "obuild finish launch");
+}
+
 }  // namespace
 
 // =================================================================== ABI ==
@@ -795,9 +846,8 @@ int irl_colstats_c128(const double* O, int64_t n, int64_t ld, const double* w, c
 size_t irl_obuild_workspace_bytes(int model, int64_t n, int n_vis, int hidden, int64_t ld, int is_complex) {
   const int64_t ld_u = is_complex ? ld : ld / 2;
   OPlan p;
-  if (make_oplan(ld_u, is_complex != 0, model, p) != IRL_OK) return 0;
-  (void)n_vis;
-  return obuild_bytes(p, model, n, hidden, ld_u, is_complex != 0);
+  if (make_oplan(ld_u, is_complex != 0, model, p, !gemm_stats(is_complex != 0, n_vis, hidden)) != IRL_OK) return 0;
+  return obuild_bytes(p, model, n, n_vis, hidden, ld_u, is_complex != 0);
 }
 
 int irl_obuild_rbm_f64(const uint8_t* x, int64_t n, int n_vis, int hidden, const double* theta, double* O,

@@ -182,7 +182,9 @@ __device__ __forceinline__ void orow_stage(const ORowArgs& a, int64_t n, typenam
   }
 }
 
-template <bool CPLX, int MODEL, int PPT>
+// STATS: accumulate the column statistics in the writer (complex RBM); real
+// models get them from the DMMA GEMMs of otf.cuh instead (lighter writer).
+template <bool CPLX, int MODEL, int PPT, bool STATS>
 __global__ void __launch_bounds__(512) k_orows(const ORowArgs a, int R) {
   using T = Traits<CPLX>;
   using S = typename T::S;
@@ -243,8 +245,12 @@ __global__ void __launch_bounds__(512) k_orows(const ORowArgs a, int R) {
     const char* tbase = reinterpret_cast<const char*>(base);
     for (int r = 0; r < rows; ++r, orow += a.ld_u, tbase += (size_t)TL * sizeof(S)) {
       const int64_t n = n0 + r;
-      const double wn = __ldg(a.w + n);
-      const S cn = cf[n];
+      double wn = 0.0;
+      S cn = T::zero();
+      if constexpr (STATS) {
+        wn = __ldg(a.w + n);
+        cn = cf[n];
+      }
 #pragma unroll
       for (int k = 0; k < PPT; ++k) {
         if (k < kval) {
@@ -253,30 +259,36 @@ __global__ void __launch_bounds__(512) k_orows(const ORowArgs a, int R) {
             const S fa = *reinterpret_cast<const S*>(tbase + (pr[k][0] >> 16));
             const S fb = *reinterpret_cast<const S*>(tbase + (pr[k][0] & 0xffffu));
             u = T::mul(fa, fb);
-            acc0[k].x = fma(wn, u.x, acc0[k].x);
-            acc0[k].y = fma(-wn, u.y, acc0[k].y);
-            T::axpy(acc1[k], u, cn);
+            if constexpr (STATS) {
+              acc0[k].x = fma(wn, u.x, acc0[k].x);
+              acc0[k].y = fma(-wn, u.y, acc0[k].y);
+              T::axpy(acc1[k], u, cn);
+            }
           } else {
             u.x = *reinterpret_cast<const double*>(tbase + (pr[k][0] >> 16)) *
                   *reinterpret_cast<const double*>(tbase + (pr[k][0] & 0xffffu));
             u.y = *reinterpret_cast<const double*>(tbase + (pr[k][1] >> 16)) *
                   *reinterpret_cast<const double*>(tbase + (pr[k][1] & 0xffffu));
-            acc0[k].x = fma(wn, u.x, acc0[k].x);
-            acc0[k].y = fma(wn, u.y, acc0[k].y);
-            acc1[k].x = fma(cn, u.x, acc1[k].x);
-            acc1[k].y = fma(cn, u.y, acc1[k].y);
+            if constexpr (STATS) {
+              acc0[k].x = fma(wn, u.x, acc0[k].x);
+              acc0[k].y = fma(wn, u.y, acc0[k].y);
+              acc1[k].x = fma(cn, u.x, acc1[k].x);
+              acc1[k].y = fma(cn, u.y, acc1[k].y);
+            }
           }
           st_stream(orow + k * NT, u);
         }
       }
     }
   }
+  if constexpr (STATS) {
 #pragma unroll
-  for (int k = 0; k < PPT; ++k) {
-    const int idx = tid + k * NT;
-    if (idx < W) {
-      a.part0[(int64_t)blk * a.ld_u + col0 + idx] = acc0[k];
-      a.part1[(int64_t)blk * a.ld_u + col0 + idx] = acc1[k];
+    for (int k = 0; k < PPT; ++k) {
+      const int idx = tid + k * NT;
+      if (idx < W) {
+        a.part0[(int64_t)blk * a.ld_u + col0 + idx] = acc0[k];
+        a.part1[(int64_t)blk * a.ld_u + col0 + idx] = acc1[k];
+      }
     }
   }
 }

@@ -512,3 +512,46 @@ __global__ void __launch_bounds__(256) k_hidden_mma(const uint64_t* __restrict__
   }
 }
 }  // namespace irl
+
+namespace irl {
+// xpart[blk][i] = sum_{rows of blk} y_r x_ri (thread i < n_in owns feature i; the
+// packed row words are broadcast), plus ypart[blk] = sum y_r.  Fixed order.
+__global__ void __launch_bounds__(128) k_xsum(const uint64_t* __restrict__ xbits, const double* __restrict__ y,
+                                              int64_t n, int n_in, double* xpart, double* ypart) {
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = blockIdx.x * per, hi = min(n, lo + per);
+  const int i = threadIdx.x;
+  double acc = 0.0, ys = 0.0;
+  for (int64_t r = lo; r < hi; ++r) {
+    const double yr = y[r];
+    if (i < n_in) {
+      const uint64_t w = __ldg(xbits + r * OTF_XW + (i >> 6));
+      if ((w >> (i & 63)) & 1ull) acc += yr;
+    }
+    ys += yr;
+  }
+  if (i < n_in) xpart[(int64_t)blockIdx.x * n_in + i] = acc;
+  if (i == 0) ypart[blockIdx.x] = ys;
+}
+
+// RBM real column statistics in the parameter layout [a (n), b (h), W (h x n)]:
+//   a_i = sum y x_i ; b_j = sum y t_j (ones column) ; W_ji = sum y t_j x_i
+__global__ void __launch_bounds__(256) k_rbm_stats_finish(const double* __restrict__ part, int nb, int hidden,
+                                                          int n_in, const double* __restrict__ xpart, int nbx,
+                                                          int64_t ld, double* out) {
+  const int64_t P = (int64_t)n_in + hidden + (int64_t)hidden * n_in;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < ld; p += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    if (p < n_in) {
+      for (int b = 0; b < nbx; ++b) acc += xpart[(int64_t)b * n_in + p];
+    } else if (p < n_in + hidden) {
+      const int64_t j = p - n_in;
+      for (int b = 0; b < nb; ++b) acc += part[((int64_t)b * hidden + j) * OTF_KC + n_in];
+    } else if (p < P) {
+      const int64_t q = p - n_in - hidden, j = q / n_in, i = q % n_in;
+      for (int b = 0; b < nb; ++b) acc += part[((int64_t)b * hidden + j) * OTF_KC + i];
+    }
+    out[p] = acc;
+  }
+}
+}  // namespace irl
