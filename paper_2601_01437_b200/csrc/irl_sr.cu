@@ -502,8 +502,25 @@ int colstats_impl(bool cplx, const double* O, int64_t n, int64_t ld, const doubl
 // --------------------------------------------------------------- otf ----
 struct OtfPlan {
   int jc, nb, ny;
-  size_t smem_dot, smem_acc;
+  int nkt, kc;  // n-tiles of the acc GEMM (k columns = n_in + ones column, padded to 8)
+  size_t smem_dot;
 };
+
+using AccFn = void (*)(OtfArgs);
+
+AccFn pick_acc(int nkt, int nyv, bool has_t) {
+#define IRL_ACC(NK, NYV, HT) \
+  if (nkt == NK && nyv == NYV && has_t == HT) return k_otf_acc<NK, NYV, HT>;
+  IRL_ACC(3, 1, true) IRL_ACC(3, 2, true) IRL_ACC(3, 1, false) IRL_ACC(3, 2, false)
+  IRL_ACC(6, 1, true) IRL_ACC(6, 2, true) IRL_ACC(6, 1, false) IRL_ACC(6, 2, false)
+  IRL_ACC(13, 1, true) IRL_ACC(13, 1, false)
+#undef IRL_ACC
+  return nullptr;
+}
+
+size_t acc_smem(int nyv, bool has_t) {
+  return ((size_t)2 * OTF_BM * OTF_BJ * (has_t ? 2 : 1) + 2 * OTF_BM * OTF_XW + (size_t)nyv * 2 * OTF_BM) * 8;
+}
 
 int make_otf_plan(int64_t n, int n_in, int hidden, OtfPlan& p) {
   DevInfo d;
@@ -515,9 +532,14 @@ int make_otf_plan(int64_t n, int n_in, int hidden, OtfPlan& p) {
   p.ny = d.sms;
   p.smem_dot = (size_t)(OTF_BJ * OTF_MAX_NIN + 2 * OTF_BJ + 4 * OTF_BM * OTF_BJ) * 8 + 2 * OTF_BM * OTF_XW * 8 +
                4 * OTF_BM * 8;
-  p.smem_acc = (size_t)4 * OTF_BM * OTF_BJ * 8 + 2 * OTF_BM * OTF_XW * 8 + 2 * OTF_BM * 8;
+  p.nkt = (n_in + 1 + 7) / 8 <= 3 ? 3 : (n_in + 1 + 7) / 8 <= 6 ? 6 : 13;
+  p.kc = 8 * p.nkt;
   IRL_TRY(ensure_fn_attrs((const void*)k_otf_dot, d.smem_optin));
-  IRL_TRY(ensure_fn_attrs((const void*)k_otf_acc, d.smem_optin));
+  for (int nyv = 1; nyv <= 2; ++nyv)
+    for (bool ht : {true, false}) {
+      AccFn f = pick_acc(p.nkt, nyv, ht);
+      if (f) IRL_TRY(ensure_fn_attrs((const void*)f, d.smem_optin));
+    }
   return IRL_OK;
 }
 
@@ -539,8 +561,8 @@ OtfWs otf_ws_layout(const OtfPlan& p, int64_t n, int hidden, void* base) {
   w.ypart = carve((size_t)p.ny * 8);
   w.dpart = carve((size_t)p.ny * 8);
   w.gpart = carve((size_t)p.ny * 8);
-  w.part = carve((size_t)p.nb * hidden * OTF_KC * 8);
-  w.partu = carve((size_t)p.nb * hidden * 8);
+  w.part = carve((size_t)2 * p.nb * hidden * p.kc * 8);
+  w.partu = carve((size_t)2 * p.nb * hidden * 8);
   w.bytes = off;
   return w;
 }
@@ -555,11 +577,47 @@ int otf_check(const uint64_t* xbits, const double* t, const double* g, int64_t n
   return IRL_OK;
 }
 
-int otf_acc_launch(const OtfPlan& pl, OtfArgs& a, cudaStream_t st) {
+int otf_acc_launch(const OtfPlan& pl, OtfArgs& a, cudaStream_t st, int nyv, bool has_t) {
+  AccFn f = pick_acc(pl.nkt, nyv, has_t);
+  if (!f) return fail(IRL_ERR_DEVICE, "no acc GEMM instance for nkt=%d ny=%d", pl.nkt, nyv);
   dim3 grid((unsigned)pl.jc, (unsigned)pl.nb);
   a.nb = pl.nb;
-  k_otf_acc<<<grid, 256, pl.smem_acc, st>>>(a);
+  f<<<grid, 256, acc_smem(nyv, has_t), st>>>(a);
   return cuda_check(cudaGetLastError(), "otf acc launch");
+}
+
+// column statistics (obar = sum w O, grad = sum c O) of a real model from the
+// hidden activations: one GEMM pass for both weight vectors when they fit
+int otf_stats(const OtfPlan& pl, OtfArgs a, const OtfWs& wl, int model, int64_t n, int n_in, int hidden,
+              int64_t ld, const double* w, const double* coeff, double* obar, double* grad, double* xpart, int nbx,
+              cudaStream_t st) {
+  const bool has_t = model == MODEL_MLP;
+  const double* ys[2] = {w, coeff};
+  double* outs[2] = {obar, grad};
+  a.part = wl.part;
+  a.partu = wl.partu;
+  const int nyv = pl.nkt <= 6 ? 2 : 1;
+  for (int q0 = 0; q0 < 2; q0 += nyv) {
+    a.y = ys[q0];
+    a.y2 = nyv == 2 ? ys[q0 + 1] : nullptr;
+    IRL_TRY(otf_acc_launch(pl, a, st, nyv, has_t));
+    for (int q = q0; q < q0 + nyv; ++q) {
+      const double* part = wl.part + (size_t)(q - q0) * pl.nb * hidden * pl.kc;
+      const double* partu = wl.partu + (size_t)(q - q0) * pl.nb * hidden;
+      if (model == MODEL_MLP) {
+        k_vsum<<<pl.ny, 256, 0, st>>>(ys[q], n, wl.ypart);
+        k_otf_finish<<<(unsigned)cdiv(ld, 256), 256, 0, st>>>(part, partu, pl.nb, hidden, n_in, pl.kc, ld, wl.ypart,
+                                                             pl.ny, nullptr, nullptr, nullptr, nullptr, 0, outs[q],
+                                                             nullptr);
+      } else {
+        k_xsum<<<nbx, 128, 0, st>>>(a.xbits, ys[q], n, n_in, xpart, wl.ypart);
+        k_rbm_stats_finish<<<(unsigned)cdiv(ld, 256), 256, 0, st>>>(part, pl.nb, hidden, n_in, pl.kc, xpart, nbx,
+                                                                    ld, outs[q]);
+      }
+      IRL_TRY(cuda_check(cudaGetLastError(), "stats finish launch"));
+    }
+  }
+  return IRL_OK;
 }
 
 // ------------------------------------------------------------ obuild ----
@@ -760,28 +818,10 @@ int obuild_impl(bool cplx, int model, const uint8_t* x, int64_t n, int n_vis, in
     oa.n_rows = n;
     oa.n_in = n_vis;
     oa.hidden = hidden;
-    oa.part = wl.part;
-    oa.partu = wl.partu;
-    const double* ys[2] = {w, coeff};
-    double* outs[2] = {obar, g};
     DevInfo d;
     IRL_TRY(dev_info(d));
     const int nbx = std::min<int>(4 * d.sms, (int)std::max<int64_t>(1, n / 64));
-    for (int q = 0; q < 2; ++q) {
-      oa.y = ys[q];
-      IRL_TRY(otf_acc_launch(op, oa, st));
-      if (model == MODEL_MLP) {
-        k_vsum<<<op.ny, 256, 0, st>>>(ys[q], n, wl.ypart);
-        k_otf_finish<<<(unsigned)cdiv(ld, 256), 256, 0, st>>>(wl.part, wl.partu, op.nb, hidden, n_vis, ld, wl.ypart,
-                                                             op.ny, nullptr, nullptr, nullptr, nullptr, 0, outs[q],
-                                                             nullptr);
-      } else {
-        k_xsum<<<nbx, 128, 0, st>>>(xbits, ys[q], n, n_vis, xpart, wl.ypart);
-        k_rbm_stats_finish<<<(unsigned)cdiv(ld, 256), 256, 0, st>>>(wl.part, op.nb, hidden, n_vis, xpart, nbx, ld,
-                                                                    outs[q]);
-      }
-      IRL_TRY(cuda_check(cudaGetLastError(), "gemm stats launch"));
-    }
+    IRL_TRY(otf_stats(op, oa, wl, model, n, n_vis, hidden, ld, w, coeff, obar, g, xpart, nbx, st));
     return IRL_OK;
   }
   const unsigned blocks = (unsigned)cdiv(ld_u, 32);
@@ -966,20 +1006,7 @@ int irl_otf_colstats_mlp_f64(const uint64_t* xbits, const double* t, const doubl
   a.n_rows = n;
   a.n_in = n_in;
   a.hidden = hidden;
-  a.part = wl.part;
-  a.partu = wl.partu;
-  const double* ys[2] = {w, coeff};
-  double* outs[2] = {obar, grad};
-  for (int q = 0; q < 2; ++q) {
-    a.y = ys[q];
-    IRL_TRY(otf_acc_launch(pl, a, st));
-    k_vsum<<<pl.ny, 256, 0, st>>>(ys[q], n, wl.ypart);
-    k_otf_finish<<<(unsigned)cdiv(ld, 256), 256, 0, st>>>(wl.part, wl.partu, pl.nb, hidden, n_in, ld, wl.ypart,
-                                                         pl.ny, nullptr, nullptr, nullptr, nullptr, 0, outs[q],
-                                                         nullptr);
-    IRL_TRY(cuda_check(cudaGetLastError(), "otf colstats launch"));
-  }
-  return IRL_OK;
+  return otf_stats(pl, a, wl, MODEL_MLP, n, n_in, hidden, ld, w, coeff, obar, grad, nullptr, 0, st);
 }
 
 int irl_otf_mvp_mlp_f64(const uint64_t* xbits, const double* t, const double* g, int64_t n, int n_in, int hidden,
@@ -1011,9 +1038,9 @@ int irl_otf_mvp_mlp_f64(const uint64_t* xbits, const double* t, const double* g,
   k_otf_dot<<<dim3((unsigned)pl.jc, (unsigned)pl.nb), 256, pl.smem_dot, st>>>(a);
   IRL_TRY(cuda_check(cudaGetLastError(), "otf dot launch"));
   k_otf_y<<<pl.ny, 256, 0, st>>>(wl.tpart, pl.jc, n, coeff, v, P - 1, wl.dpart, obar ? pl.ny : 0, wl.y, wl.ypart);
-  IRL_TRY(otf_acc_launch(pl, a, st));
-  k_otf_finish<<<(unsigned)cdiv(ld, 256), 256, 0, st>>>(wl.part, wl.partu, pl.nb, hidden, n_in, ld, wl.ypart, pl.ny,
-                                                       obar, half_f, u0, wl.gpart, pl.ny, out, out0);
+  IRL_TRY(otf_acc_launch(pl, a, st, 1, true));
+  k_otf_finish<<<(unsigned)cdiv(ld, 256), 256, 0, st>>>(wl.part, wl.partu, pl.nb, hidden, n_in, pl.kc, ld, wl.ypart,
+                                                       pl.ny, obar, half_f, u0, wl.gpart, pl.ny, out, out0);
   return cuda_check(cudaGetLastError(), "otf finish launch");
 }
 

@@ -38,8 +38,9 @@ struct OtfArgs {
   double* tpart;          // [JC][N]
   // acc
   const double* y;        // [N]
-  double* part;           // [nb][h][OTF_KC]
-  double* partu;          // [nb][h]
+  const double* y2;       // [N] second weight vector (NY = 2)
+  double* part;           // [NY][nb][h][KC]
+  double* partu;          // [NY][nb][h]
 };
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
@@ -235,13 +236,18 @@ __global__ void __launch_bounds__(256) k_otf_y(const double* __restrict__ tpart,
 }
 
 // grid (JC, nb), 256 threads (warp w owns hidden units j0 + 8w .. +7):
-// part[blk][j][kc] = sum_rows y g_j x_kc (kc = n_in is the ones column), partu = sum y t_j
+// part[y][blk][j][kc] = sum_rows y g_j x_kc (kc = n_in is the ones column),
+// partu[y][blk][j] = sum y t_j (HAS_T).  NKT n-tiles of 8 k columns cover
+// n_in + 1 (the MMA count follows n_in); NY weight vectors share one read of
+// the G/T tiles and the B fragments.
+template <int NKT, int NY, bool HAS_T>
 __global__ void __launch_bounds__(256) k_otf_acc(const OtfArgs a) {
   extern __shared__ __align__(16) unsigned char smem_o[];
   double* gs = reinterpret_cast<double*>(smem_o);           // [2][BM][BJ]
-  double* ts = gs + 2 * OTF_BM * OTF_BJ;                     // [2][BM][BJ]
-  uint64_t* xs = reinterpret_cast<uint64_t*>(ts + 2 * OTF_BM * OTF_BJ);  // [2][BM][XW]
-  double* ys = reinterpret_cast<double*>(xs + 2 * OTF_BM * OTF_XW);      // [2][BM]
+  double* ts = gs + 2 * OTF_BM * OTF_BJ;                     // [2][BM][BJ] (HAS_T)
+  uint64_t* xs = reinterpret_cast<uint64_t*>(ts + (HAS_T ? 2 * OTF_BM * OTF_BJ : 0));  // [2][BM][XW]
+  double* ys = reinterpret_cast<double*>(xs + 2 * OTF_BM * OTF_XW);      // [NY][2][BM]
+  constexpr int KC = 8 * NKT;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int jc = blockIdx.x, j0 = jc * OTF_BJ;
@@ -249,20 +255,28 @@ __global__ void __launch_bounds__(256) k_otf_acc(const OtfArgs a) {
   const int64_t lo = (N * blockIdx.y) / a.nb, hi = (N * (blockIdx.y + 1)) / a.nb;
   const int nin = a.n_in;
   const int ntiles = (int)((hi - lo + OTF_BM - 1) / OTF_BM);
+  const double* yv_src[2] = {a.y, a.y2};
 
-  auto load_y = [&](int64_t r0, double* dst) {
-    for (int e = tid; e < OTF_BM; e += blockDim.x) dst[e] = (r0 + e < hi) ? a.y[r0 + e] : 0.0;
+  auto load_y = [&](int64_t r0, int buf) {
+    for (int e = tid; e < NY * OTF_BM; e += blockDim.x) {
+      const int q = e / OTF_BM, r = e % OTF_BM;
+      ys[(q * 2 + buf) * OTF_BM + r] = (r0 + r < hi) ? yv_src[q][r0 + r] : 0.0;
+    }
   };
   if (ntiles > 0) {
-    otf_load_tile(a, lo, hi, j0, gs, ts, xs, tid, blockDim.x);
-    load_y(lo, ys);
+    otf_load_tile(a, lo, hi, j0, gs, HAS_T ? ts : nullptr, xs, tid, blockDim.x);
+    load_y(lo, 0);
   }
   cp_async_commit();
 
-  double c[13][2];
-  double cu[2] = {0.0, 0.0};
+  double c[NY][NKT][2];
+  double cu[NY][2];
 #pragma unroll
-  for (int nt = 0; nt < 13; ++nt) c[nt][0] = c[nt][1] = 0.0;
+  for (int q = 0; q < NY; ++q) {
+    cu[q][0] = cu[q][1] = 0.0;
+#pragma unroll
+    for (int nt = 0; nt < NKT; ++nt) c[q][nt][0] = c[q][nt][1] = 0.0;
+  }
   const int jl = warp * 8 + (lane >> 2);  // A row (hidden unit) of this lane
   const int sh_base = lane >> 2;          // B column offset within an n-tile
   const double one_b = (lane >> 2) == 0 ? 1.0 : 0.0;
@@ -271,9 +285,10 @@ __global__ void __launch_bounds__(256) k_otf_acc(const OtfArgs a) {
     const int buf = it & 1;
     const int64_t r0 = lo + (int64_t)it * OTF_BM;
     if (it + 1 < ntiles) {
-      otf_load_tile(a, r0 + OTF_BM, hi, j0, gs + (buf ^ 1) * OTF_BM * OTF_BJ, ts + (buf ^ 1) * OTF_BM * OTF_BJ,
-                    xs + (buf ^ 1) * OTF_BM * OTF_XW, tid, blockDim.x);
-      load_y(r0 + OTF_BM, ys + (buf ^ 1) * OTF_BM);
+      otf_load_tile(a, r0 + OTF_BM, hi, j0, gs + (buf ^ 1) * OTF_BM * OTF_BJ,
+                    HAS_T ? ts + (buf ^ 1) * OTF_BM * OTF_BJ : nullptr, xs + (buf ^ 1) * OTF_BM * OTF_XW, tid,
+                    blockDim.x);
+      load_y(r0 + OTF_BM, buf ^ 1);
     }
     cp_async_commit();
     cp_async_wait<1>();
@@ -281,42 +296,45 @@ __global__ void __launch_bounds__(256) k_otf_acc(const OtfArgs a) {
     const double* G = gs + buf * OTF_BM * OTF_BJ;
     const double* Tt = ts + buf * OTF_BM * OTF_BJ;
     const uint64_t* X = xs + buf * OTF_BM * OTF_XW;
-    const double* Y = ys + buf * OTF_BM;
 #pragma unroll 2
     for (int kk = 0; kk < OTF_BM / 4; ++kk) {
       const int rl = kk * 4 + (lane & 3);
-      const double yv = Y[rl];
-      const double av = G[rl * OTF_BJ + jl] * yv;
-      const double au = Tt[rl * OTF_BJ + jl] * yv;
+      const double gv = G[rl * OTF_BJ + jl];
+      const double tv = HAS_T ? Tt[rl * OTF_BJ + jl] : 0.0;
       const uint64_t w0 = X[rl * OTF_XW] >> sh_base, w1 = X[rl * OTF_XW + 1] >> sh_base;
+      double bv[NKT];
 #pragma unroll
-      for (int nt = 0; nt < 13; ++nt) {
+      for (int nt = 0; nt < NKT; ++nt) {
         const int kcol = nt * 8 + sh_base;
-        uint32_t bit;
-        if (nt < 8) {
-          bit = (uint32_t)(w0 >> (nt * 8)) & 1u;
-        } else {
-          bit = (uint32_t)(w1 >> ((nt - 8) * 8)) & 1u;
-        }
-        double bv = bit_to_double(bit);
-        if (nt * 8 + 7 >= nin) bv = (kcol < nin) ? bv : (kcol == nin ? 1.0 : 0.0);
-        dmma(c[nt][0], c[nt][1], av, bv);
+        const uint32_t bit = nt < 8 ? (uint32_t)(w0 >> (nt * 8)) & 1u : (uint32_t)(w1 >> ((nt - 8) * 8)) & 1u;
+        bv[nt] = bit_to_double(bit);
+        if (nt * 8 + 7 >= nin) bv[nt] = (kcol < nin) ? bv[nt] : (kcol == nin ? 1.0 : 0.0);
       }
-      dmma(cu[0], cu[1], au, one_b);
+#pragma unroll
+      for (int q = 0; q < NY; ++q) {
+        const double yq = ys[(q * 2 + buf) * OTF_BM + rl];
+        const double av = gv * yq;
+#pragma unroll
+        for (int nt = 0; nt < NKT; ++nt) dmma(c[q][nt][0], c[q][nt][1], av, bv[nt]);
+        if (HAS_T) dmma(cu[q][0], cu[q][1], tv * yq, one_b);
+      }
     }
     __syncthreads();
   }
-  // partials: C[j][kc] fragment -> part[blk][j][kc]
-  double* pb = a.part + ((int64_t)blockIdx.y * a.hidden + j0 + warp * 8 + (lane >> 2)) * OTF_KC;
-  const bool jok = (j0 + warp * 8 + (lane >> 2)) < a.hidden;
-  if (jok) {
+  // partials: C[j][kc] fragment -> part[q][blk][j][kc]
+  const int jrow = j0 + warp * 8 + (lane >> 2);
+  if (jrow < a.hidden) {
 #pragma unroll
-    for (int nt = 0; nt < 13; ++nt) {
-      const int kc = nt * 8 + (lane & 3) * 2;
-      pb[kc] = c[nt][0];
-      pb[kc + 1] = c[nt][1];
+    for (int q = 0; q < NY; ++q) {
+      double* pb = a.part + (((int64_t)q * a.nb + blockIdx.y) * a.hidden + jrow) * KC;
+#pragma unroll
+      for (int nt = 0; nt < NKT; ++nt) {
+        const int kc = nt * 8 + (lane & 3) * 2;
+        pb[kc] = c[q][nt][0];
+        pb[kc + 1] = c[q][nt][1];
+      }
+      if (HAS_T && (lane & 3) == 0) a.partu[((int64_t)q * a.nb + blockIdx.y) * a.hidden + jrow] = cu[q][0];
     }
-    if ((lane & 3) == 0) a.partu[(int64_t)blockIdx.y * a.hidden + j0 + warp * 8 + (lane >> 2)] = cu[0];
   }
 }
 
@@ -324,7 +342,7 @@ __global__ void __launch_bounds__(256) k_otf_acc(const OtfArgs a) {
 //   mode 0 (product): out = sum part - obar * Y (+ u0 hf), out0 = g0
 //   mode 1 (stats)  : out = sum part          (Y, obar unused)
 __global__ void __launch_bounds__(256) k_otf_finish(const double* __restrict__ part, const double* __restrict__ partu,
-                                                    int nb, int hidden, int n_in, int64_t ld,
+                                                    int nb, int hidden, int n_in, int kc, int64_t ld,
                                                     const double* __restrict__ ypart, int n_ypart,
                                                     const double* __restrict__ obar, const double* hf,
                                                     const double* u0, const double* dgpart, int n_dgpart,
@@ -338,10 +356,10 @@ __global__ void __launch_bounds__(256) k_otf_finish(const double* __restrict__ p
     double acc = 0.0;
     if (p < hn) {
       const int64_t j = p / n_in, k = p % n_in;
-      for (int b = 0; b < nb; ++b) acc += part[((int64_t)b * hidden + j) * OTF_KC + k];
+      for (int b = 0; b < nb; ++b) acc += part[((int64_t)b * hidden + j) * kc + k];
     } else if (p < hn + hidden) {
       const int64_t j = p - hn;
-      for (int b = 0; b < nb; ++b) acc += part[((int64_t)b * hidden + j) * OTF_KC + n_in];
+      for (int b = 0; b < nb; ++b) acc += part[((int64_t)b * hidden + j) * kc + n_in];
     } else if (p < hn + 2 * hidden) {
       const int64_t j = p - hn - hidden;
       for (int b = 0; b < nb; ++b) acc += partu[(int64_t)b * hidden + j];
@@ -537,7 +555,7 @@ __global__ void __launch_bounds__(128) k_xsum(const uint64_t* __restrict__ xbits
 // RBM real column statistics in the parameter layout [a (n), b (h), W (h x n)]:
 //   a_i = sum y x_i ; b_j = sum y t_j (ones column) ; W_ji = sum y t_j x_i
 __global__ void __launch_bounds__(256) k_rbm_stats_finish(const double* __restrict__ part, int nb, int hidden,
-                                                          int n_in, const double* __restrict__ xpart, int nbx,
+                                                          int n_in, int kc, const double* __restrict__ xpart, int nbx,
                                                           int64_t ld, double* out) {
   const int64_t P = (int64_t)n_in + hidden + (int64_t)hidden * n_in;
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < ld; p += (int64_t)gridDim.x * blockDim.x) {
@@ -546,10 +564,10 @@ __global__ void __launch_bounds__(256) k_rbm_stats_finish(const double* __restri
       for (int b = 0; b < nbx; ++b) acc += xpart[(int64_t)b * n_in + p];
     } else if (p < n_in + hidden) {
       const int64_t j = p - n_in;
-      for (int b = 0; b < nb; ++b) acc += part[((int64_t)b * hidden + j) * OTF_KC + n_in];
+      for (int b = 0; b < nb; ++b) acc += part[((int64_t)b * hidden + j) * kc + n_in];
     } else if (p < P) {
       const int64_t q = p - n_in - hidden, j = q / n_in, i = q % n_in;
-      for (int b = 0; b < nb; ++b) acc += part[((int64_t)b * hidden + j) * OTF_KC + i];
+      for (int b = 0; b < nb; ++b) acc += part[((int64_t)b * hidden + j) * kc + i];
     }
     out[p] = acc;
   }
