@@ -113,15 +113,24 @@ def _x_device(x, n_inputs: int, dev) -> torch.Tensor:
 
 
 def build_batch(params: AnsatzParameters, x, e_loc, weights=None, n_samples: int | None = None,
-                device=None) -> SampleBatch:
+                device=None, mode: str = "stored") -> SampleBatch:
     """Device SampleBatch with O built by the fused row kernel (K1/K2).
 
-    One launch sequence: k_energy (E, c = w (e - E)) -> k_hidden (tanh layer)
-    -> k_orows (O rows + fused sum w conj(O), sum c conj(O)) -> finisher.
-    ``weights`` defaults to 1/N (stochastic mode, est:99-100).
+    One launch sequence: k_energy (E, c = w (e - E)) -> hidden layer on FP64
+    tensor cores -> k_orows (O rows; column statistics fused or from the DMMA
+    GEMM) -> finisher.  ``weights`` defaults to 1/N (stochastic mode, est:99-100).
+
+    ``mode``: "stored" materialises O in HBM; "otf" keeps only the hidden
+    activations and regenerates O inside every product (MLP only, see
+    :func:`build_batch_otf`); "auto" picks "otf" for the MLP (faster and ~10x
+    less memory on every BASELINE MLP shape) and "stored" otherwise.
     """
-    dev = _device(device)
     arch = params.architecture
+    if mode not in ("stored", "otf", "auto"):
+        raise ValueError(f"unknown build mode {mode!r}")
+    if mode == "otf" or (mode == "auto" and arch.model == _lib.MODEL_MLP and arch.n_inputs <= 100):
+        return build_batch_otf(params, x, e_loc, weights=weights, n_samples=n_samples, device=device)
+    dev = _device(device)
     xt = _x_device(x, arch.n_inputs, dev)
     n = int(xt.shape[0])
     if n < 1:

@@ -639,7 +639,10 @@ void (*pick_orows(int ppt))(ORowArgs, int) {
 
 // real models with n_in <= 100 and an even hidden width take their column
 // statistics from the DMMA GEMM (k_otf_acc) instead of the row writer
-bool gemm_stats(bool cplx, int n_vis, int hidden) { return !cplx && n_vis <= OTF_MAX_NIN && (hidden & 1) == 0; }
+// (measured: for the narrow RBM hidden layers the fused writer statistics win)
+bool gemm_stats(bool cplx, int model, int n_vis, int hidden) {
+  return !cplx && model == MODEL_MLP && n_vis <= OTF_MAX_NIN && (hidden & 1) == 0;
+}
 
 int make_oplan(int64_t ld_u, bool cplx, int model, OPlan& p, bool stats_in_writer) {
   DevInfo d;
@@ -682,7 +685,7 @@ size_t obuild_bytes(const OPlan& p, int model, int64_t n, int n_vis, int hidden,
   size_t b = align256((size_t)n * hidden * sS);                    // t
   if (model == MODEL_MLP) b += align256((size_t)n * hidden * 8);    // g
   b += align256((size_t)n * OTF_XW * 8);                           // packed inputs
-  if (gemm_stats(cplx, n_vis, hidden)) {                           // DMMA stats scratch
+  if (gemm_stats(cplx, model, n_vis, hidden)) {                           // DMMA stats scratch
     OtfPlan op;
     if (make_otf_plan(n, n_vis, hidden, op) == IRL_OK) b += otf_ws_layout(op, n, hidden, nullptr).bytes;
     b += align256((size_t)148 * 4 * (n_vis + 1) * 8);             // x sums
@@ -737,7 +740,7 @@ int obuild_impl(bool cplx, int model, const uint8_t* x, int64_t n, int n_vis, in
   if (ld != irl_padded_ld(P, cplx)) return fail(IRL_ERR_ALIGN, "ld must equal irl_padded_ld(P=%lld)", (long long)P);
   if (!aligned16(O) || !aligned16(obar) || !aligned16(g) || !aligned16(ws)) return fail(IRL_ERR_ALIGN, "alignment");
   const int64_t ld_u = cplx ? ld : ld / 2;
-  const bool gstats = gemm_stats(cplx, n_vis, hidden);
+  const bool gstats = gemm_stats(cplx, model, n_vis, hidden);
   OPlan p;
   IRL_TRY(make_oplan(ld_u, cplx, model, p, !gstats));
   const size_t need = obuild_bytes(p, model, n, n_vis, hidden, ld_u, cplx);
@@ -886,7 +889,7 @@ int irl_colstats_c128(const double* O, int64_t n, int64_t ld, const double* w, c
 size_t irl_obuild_workspace_bytes(int model, int64_t n, int n_vis, int hidden, int64_t ld, int is_complex) {
   const int64_t ld_u = is_complex ? ld : ld / 2;
   OPlan p;
-  if (make_oplan(ld_u, is_complex != 0, model, p, !gemm_stats(is_complex != 0, n_vis, hidden)) != IRL_OK) return 0;
+  if (make_oplan(ld_u, is_complex != 0, model, p, !gemm_stats(is_complex != 0, model, n_vis, hidden)) != IRL_OK) return 0;
   return obuild_bytes(p, model, n, n_vis, hidden, ld_u, is_complex != 0);
 }
 
