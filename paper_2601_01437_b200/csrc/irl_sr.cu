@@ -518,9 +518,8 @@ AccFn pick_acc(int nkt, int nyv, bool has_t) {
   return nullptr;
 }
 
-size_t acc_smem(int nyv, bool has_t, int kc) {
-  return ((size_t)2 * OTF_BM * OTF_BJ * (has_t ? 2 : 1) + 2 * OTF_BM * OTF_XW + (size_t)nyv * 2 * OTF_BM +
-          (size_t)OTF_BM * kc) * 8;
+size_t acc_smem(int nyv, bool has_t) {
+  return ((size_t)2 * OTF_BM * OTF_BJ * (has_t ? 2 : 1) + 2 * OTF_BM * OTF_XW + (size_t)nyv * 2 * OTF_BM) * 8;
 }
 
 int make_otf_plan(int64_t n, int n_in, int hidden, OtfPlan& p) {
@@ -583,7 +582,7 @@ int otf_acc_launch(const OtfPlan& pl, OtfArgs& a, cudaStream_t st, int nyv, bool
   if (!f) return fail(IRL_ERR_DEVICE, "no acc GEMM instance for nkt=%d ny=%d", pl.nkt, nyv);
   dim3 grid((unsigned)pl.jc, (unsigned)pl.nb);
   a.nb = pl.nb;
-  f<<<grid, 256, acc_smem(nyv, has_t, pl.kc), st>>>(a);
+  f<<<grid, 256, acc_smem(nyv, has_t), st>>>(a);
   return cuda_check(cudaGetLastError(), "otf acc launch");
 }
 

@@ -248,7 +248,6 @@ __global__ void __launch_bounds__(256) k_otf_acc(const OtfArgs a) {
   uint64_t* xs = reinterpret_cast<uint64_t*>(ts + (HAS_T ? 2 * OTF_BM * OTF_BJ : 0));  // [2][BM][XW]
   double* ys = reinterpret_cast<double*>(xs + 2 * OTF_BM * OTF_XW);      // [NY][2][BM]
   constexpr int KC = 8 * NKT;
-  double* xd = ys + NY * 2 * OTF_BM;  // [BM][KC] B operand of the current tile (0/1 plus the ones column)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int jc = blockIdx.x, j0 = jc * OTF_BJ;
@@ -297,23 +296,20 @@ __global__ void __launch_bounds__(256) k_otf_acc(const OtfArgs a) {
     const double* G = gs + buf * OTF_BM * OTF_BJ;
     const double* Tt = ts + buf * OTF_BM * OTF_BJ;
     const uint64_t* X = xs + buf * OTF_BM * OTF_XW;
-    // expand the tile's bits once per CTA (instead of once per warp and k-step)
-    for (int e = tid; e < OTF_BM * KC; e += blockDim.x) {
-      const int r = e / KC, kc = e % KC;
-      double v = 0.0;
-      if (kc < nin) v = bit_to_double((uint32_t)(X[r * OTF_XW + (kc >> 6)] >> (kc & 63)) & 1u);
-      else if (kc == nin) v = 1.0;
-      xd[e] = v;
-    }
-    __syncthreads();
 #pragma unroll 2
     for (int kk = 0; kk < OTF_BM / 4; ++kk) {
       const int rl = kk * 4 + (lane & 3);
       const double gv = G[rl * OTF_BJ + jl];
       const double tv = HAS_T ? Tt[rl * OTF_BJ + jl] : 0.0;
+      const uint64_t w0 = X[rl * OTF_XW] >> sh_base, w1 = X[rl * OTF_XW + 1] >> sh_base;
       double bv[NKT];
 #pragma unroll
-      for (int nt = 0; nt < NKT; ++nt) bv[nt] = xd[rl * KC + nt * 8 + sh_base];
+      for (int nt = 0; nt < NKT; ++nt) {
+        const int kcol = nt * 8 + sh_base;
+        const uint32_t bit = nt < 8 ? (uint32_t)(w0 >> (nt * 8)) & 1u : (uint32_t)(w1 >> ((nt - 8) * 8)) & 1u;
+        bv[nt] = bit_to_double(bit);
+        if (nt * 8 + 7 >= nin) bv[nt] = (kcol < nin) ? bv[nt] : (kcol == nin ? 1.0 : 0.0);
+      }
 #pragma unroll
       for (int q = 0; q < NY; ++q) {
         const double yq = ys[(q * 2 + buf) * OTF_BM + rl];
