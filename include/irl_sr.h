@@ -135,6 +135,16 @@ int irl_otf_prepare_mlp_f64(const uint8_t* x, int64_t n, int n_in, int hidden, c
 int irl_otf_colstats_mlp_f64(const uint64_t* xbits, const double* t, const double* g, int64_t n, int n_in, int hidden,
                              int64_t ld, const double* w, const double* coeff, double* obar, double* grad, void* ws,
                              size_t ws_bytes, void* stream);
+/* RBM (real theta) on-the-fly mode, layout [a (n), b (h), W (h x n)]: the same
+ * products and statistics regenerated from the packed inputs and t = tanh(b + W x). */
+int irl_otf_prepare_rbm_f64(const uint8_t* x, int64_t n, int n_vis, int hidden, const double* theta, uint64_t* xbits,
+                            double* t, void* stream);
+int irl_otf_colstats_rbm_f64(const uint64_t* xbits, const double* t, int64_t n, int n_vis, int hidden, int64_t ld,
+                             const double* w, const double* coeff, double* obar, double* grad, void* ws,
+                             size_t ws_bytes, void* stream);
+int irl_otf_mvp_rbm_f64(const uint64_t* xbits, const double* t, int64_t n, int n_vis, int hidden, int64_t ld,
+                        const double* obar, const double* coeff, const double* v, double* out, const double* half_f,
+                        const double* u0, double* out0, void* ws, size_t ws_bytes, void* stream);
 int irl_otf_mvp_mlp_f64(const uint64_t* xbits, const double* t, const double* g, int64_t n, int n_in, int hidden,
                         int64_t ld, const double* obar, const double* coeff, const double* v, double* out,
                         const double* half_f, const double* u0, double* out0, void* ws, size_t ws_bytes,

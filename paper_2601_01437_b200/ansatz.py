@@ -227,16 +227,17 @@ def hidden_activations(params: AnsatzParameters, x, device=None):
 
 def build_batch_otf(params: AnsatzParameters, x, e_loc, weights=None, n_samples: int | None = None,
                     device=None) -> SampleBatch:
-    """MLP batch in on-the-fly mode (K6): O is never stored.
+    """Batch in on-the-fly mode (K6, SURVEY §2 mvp_onthefly_{mlp,rbm}): O is never stored.
 
-    Keeps the bit-packed inputs and the hidden activations t, g (N x h) in HBM;
-    every product regenerates O's contribution with FP64 tensor-core GEMMs.
+    O's big block is an outer product (MLP: g (x) x, RBM: t (x) x), so every
+    product is regenerated from the bit-packed inputs and the hidden
+    activations t (, g) with FP64 tensor-core GEMMs.  Real parameters only.
     Same SampleBatch interface (estimate_energy, energy_gradient, heff_matvec,
     qgt_matvec, solve_step) as a stored-O batch.
     """
     arch = params.architecture
-    if arch.model != _lib.MODEL_MLP:
-        raise ValueError("on-the-fly mode is implemented for the shallow MLP")
+    if arch.complex_params:
+        raise ValueError("on-the-fly mode is implemented for real parameters (RBM f64, MLP)")
     dev = _device(device)
     xt = _x_device(x, arch.n_inputs, dev)
     n = int(xt.shape[0])
@@ -255,9 +256,14 @@ def build_batch_otf(params: AnsatzParameters, x, e_loc, weights=None, n_samples:
     batch.o_matrix = placeholder
     xbits = torch.empty((n, 2), dtype=torch.int64, device=dev)
     t = torch.empty((n, arch.hidden), dtype=torch.float64, device=dev)
-    g = torch.empty((n, arch.hidden), dtype=torch.float64, device=dev)
     theta = _theta_device(params, dev)
-    _lib.call("irl_otf_prepare_mlp_f64", _lib.ptr(xt), n, arch.n_in, arch.hidden, _lib.ptr(theta), _lib.ptr(xbits),
-              _lib.ptr(t), _lib.ptr(g), _lib.stream_handle(dev))
-    batch.otf = {"xbits": xbits, "t": t, "g": g, "n_in": arch.n_in, "hidden": arch.hidden}
+    if arch.model == _lib.MODEL_RBM:
+        g = None
+        _lib.call("irl_otf_prepare_rbm_f64", _lib.ptr(xt), n, arch.n_visible, arch.hidden, _lib.ptr(theta),
+                  _lib.ptr(xbits), _lib.ptr(t), _lib.stream_handle(dev))
+    else:
+        g = torch.empty((n, arch.hidden), dtype=torch.float64, device=dev)
+        _lib.call("irl_otf_prepare_mlp_f64", _lib.ptr(xt), n, arch.n_in, arch.hidden, _lib.ptr(theta),
+                  _lib.ptr(xbits), _lib.ptr(t), _lib.ptr(g), _lib.stream_handle(dev))
+    batch.otf = {"xbits": xbits, "t": t, "g": g, "n_in": arch.n_inputs, "hidden": arch.hidden, "model": arch.model}
     return batch

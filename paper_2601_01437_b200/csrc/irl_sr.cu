@@ -544,7 +544,7 @@ int make_otf_plan(int64_t n, int n_in, int hidden, OtfPlan& p) {
 }
 
 struct OtfWs {
-  double *tpart, *y, *ypart, *dpart, *gpart, *part, *partu;
+  double *tpart, *y, *ypart, *dpart, *gpart, *part, *partu, *xpart, *ypart2;
   size_t bytes;
 };
 
@@ -563,6 +563,8 @@ OtfWs otf_ws_layout(const OtfPlan& p, int64_t n, int hidden, void* base) {
   w.gpart = carve((size_t)p.ny * 8);
   w.part = carve((size_t)2 * p.nb * hidden * p.kc * 8);
   w.partu = carve((size_t)2 * p.nb * hidden * 8);
+  w.xpart = carve((size_t)4 * 148 * (OTF_MAX_NIN + 1) * 8);
+  w.ypart2 = carve((size_t)4 * 148 * 8);
   w.bytes = off;
   return w;
 }
@@ -610,9 +612,10 @@ int otf_stats(const OtfPlan& pl, OtfArgs a, const OtfWs& wl, int model, int64_t 
                                                              pl.ny, nullptr, nullptr, nullptr, nullptr, 0, outs[q],
                                                              nullptr);
       } else {
-        k_xsum<<<nbx, 128, 0, st>>>(a.xbits, ys[q], n, n_in, xpart, wl.ypart);
-        k_rbm_stats_finish<<<(unsigned)cdiv(ld, 256), 256, 0, st>>>(part, pl.nb, hidden, n_in, pl.kc, xpart, nbx,
-                                                                    ld, outs[q]);
+        double* xp = xpart ? xpart : wl.xpart;
+        k_xsum<<<nbx, 128, 0, st>>>(a.xbits, ys[q], n, n_in, xp, wl.ypart2);
+        k_rbm_stats_finish<<<(unsigned)cdiv(ld, 256), 256, 0, st>>>(part, pl.nb, hidden, n_in, pl.kc, xp, nbx, ld,
+                                                                    outs[q]);
       }
       IRL_TRY(cuda_check(cudaGetLastError(), "stats finish launch"));
     }
@@ -1033,6 +1036,9 @@ int irl_otf_mvp_mlp_f64(const uint64_t* xbits, const double* t, const double* g,
   a.n_in = n_in;
   a.hidden = hidden;
   a.nb = pl.nb;
+  a.offW = 0;
+  a.offb = (int64_t)hidden * n_in;
+  a.offu = a.offb + hidden;
   a.v = v;
   a.tpart = wl.tpart;
   a.y = wl.y;
@@ -1040,11 +1046,90 @@ int irl_otf_mvp_mlp_f64(const uint64_t* xbits, const double* t, const double* g,
   a.partu = wl.partu;
   k_otf_dot<<<dim3((unsigned)pl.jc, (unsigned)pl.nb), 256, pl.smem_dot, st>>>(a);
   IRL_TRY(cuda_check(cudaGetLastError(), "otf dot launch"));
-  k_otf_y<<<pl.ny, 256, 0, st>>>(wl.tpart, pl.jc, n, coeff, v, P - 1, wl.dpart, obar ? pl.ny : 0, wl.y, wl.ypart);
+  k_otf_y<<<pl.ny, 256, 0, st>>>(wl.tpart, pl.jc, n, coeff, v, P - 1, wl.dpart, obar ? pl.ny : 0, wl.y, wl.ypart,
+                                 nullptr, -1, n_in);
   IRL_TRY(otf_acc_launch(pl, a, st, 1, true));
   k_otf_finish<<<(unsigned)cdiv(ld, 256), 256, 0, st>>>(wl.part, wl.partu, pl.nb, hidden, n_in, pl.kc, ld, wl.ypart,
                                                        pl.ny, obar, half_f, u0, wl.gpart, pl.ny, out, out0);
   return cuda_check(cudaGetLastError(), "otf finish launch");
+}
+
+int irl_otf_prepare_rbm_f64(const uint8_t* x, int64_t n, int n_vis, int hidden, const double* theta, uint64_t* xbits,
+                            double* t, void* stream) {
+  if (!x || !theta || !xbits || !t || n < 1 || n_vis < 1 || hidden < 1) return fail(IRL_ERR_ARG, "bad prepare arguments");
+  if (n_vis > OTF_MAX_NIN || (hidden & 1)) return fail(IRL_ERR_ARG, "on-the-fly RBM needs n_vis <= %d, even hidden", OTF_MAX_NIN);
+  cudaStream_t st = (cudaStream_t)stream;
+  IRL_TRY(pack_bits(x, n, n_vis, xbits, st));
+  return launch_hidden<false, MODEL_RBM>(x, xbits, n, n_vis, hidden, theta + n_vis + hidden, theta + n_vis, nullptr, t,
+                                         nullptr, st);
+}
+
+int irl_otf_colstats_rbm_f64(const uint64_t* xbits, const double* t, int64_t n, int n_vis, int hidden, int64_t ld,
+                             const double* w, const double* coeff, double* obar, double* grad, void* ws,
+                             size_t ws_bytes, void* stream) {
+  if (!xbits || !t || !w || !coeff || !obar || !grad || n < 1) return fail(IRL_ERR_ARG, "null pointer");
+  const int64_t P = (int64_t)n_vis + hidden + (int64_t)hidden * n_vis;
+  if (ld != irl_padded_ld(P, 0)) return fail(IRL_ERR_ALIGN, "ld must equal irl_padded_ld(P=%lld)", (long long)P);
+  OtfPlan pl;
+  IRL_TRY(make_otf_plan(n, n_vis, hidden, pl));
+  OtfWs wl = otf_ws_layout(pl, n, hidden, ws);
+  if (ws_bytes < wl.bytes) return fail(IRL_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, wl.bytes);
+  OtfArgs a{};
+  a.xbits = xbits;
+  a.T = t;
+  a.G = t;
+  a.n_rows = n;
+  a.n_in = n_vis;
+  a.hidden = hidden;
+  DevInfo d;
+  IRL_TRY(dev_info(d));
+  const int nbx = std::min<int>(4 * d.sms, (int)std::max<int64_t>(1, n / 64));
+  return otf_stats(pl, a, wl, MODEL_RBM, n, n_vis, hidden, ld, w, coeff, obar, grad, nullptr, nbx,
+                   (cudaStream_t)stream);
+}
+
+int irl_otf_mvp_rbm_f64(const uint64_t* xbits, const double* t, int64_t n, int n_vis, int hidden, int64_t ld,
+                        const double* obar, const double* coeff, const double* v, double* out, const double* half_f,
+                        const double* u0, double* out0, void* ws, size_t ws_bytes, void* stream) {
+  if (!xbits || !t || !coeff || !v || !out || n < 1) return fail(IRL_ERR_ARG, "null pointer");
+  const int64_t P = (int64_t)n_vis + hidden + (int64_t)hidden * n_vis;
+  if (ld != irl_padded_ld(P, 0)) return fail(IRL_ERR_ALIGN, "ld must equal irl_padded_ld(P=%lld)", (long long)P);
+  if (n_vis > OTF_MAX_NIN || (hidden & 1) || !aligned16(t)) return fail(IRL_ERR_ARG, "unsupported on-the-fly shape");
+  OtfPlan pl;
+  IRL_TRY(make_otf_plan(n, n_vis, hidden, pl));
+  OtfWs wl = otf_ws_layout(pl, n, hidden, ws);
+  if (ws_bytes < wl.bytes) return fail(IRL_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, wl.bytes);
+  cudaStream_t st = (cudaStream_t)stream;
+  DevInfo d;
+  IRL_TRY(dev_info(d));
+  k_vdot2<<<pl.ny, 256, 0, st>>>(obar, half_f, v, ld, wl.dpart, wl.gpart);
+  OtfArgs a{};
+  a.xbits = xbits;
+  a.T = t;
+  a.G = t;
+  a.n_rows = n;
+  a.n_in = n_vis;
+  a.hidden = hidden;
+  a.nb = pl.nb;
+  a.offW = (int64_t)n_vis + hidden;
+  a.offb = n_vis;
+  a.offu = -1;
+  a.v = v;
+  a.tpart = wl.tpart;
+  a.y = wl.y;
+  a.part = wl.part;
+  a.partu = wl.partu;
+  k_otf_dot<<<dim3((unsigned)pl.jc, (unsigned)pl.nb), 256, pl.smem_dot, st>>>(a);
+  IRL_TRY(cuda_check(cudaGetLastError(), "otf dot launch"));
+  k_otf_y<<<pl.ny, 256, 0, st>>>(wl.tpart, pl.jc, n, coeff, v, -1, wl.dpart, obar ? pl.ny : 0, wl.y, wl.ypart, xbits,
+                                 0, n_vis);
+  IRL_TRY(otf_acc_launch(pl, a, st, 1, false));
+  const int nbx = std::min<int>(4 * d.sms, (int)std::max<int64_t>(1, n / 64));
+  k_xsum<<<nbx, 128, 0, st>>>(xbits, wl.y, n, n_vis, wl.xpart, wl.ypart2);
+  k_rbm_otf_finish<<<(unsigned)cdiv(ld, 256), 256, 0, st>>>(wl.part, pl.nb, hidden, n_vis, pl.kc, wl.xpart, nbx,
+                                                           wl.ypart, pl.ny, ld, obar, half_f, u0, wl.gpart, pl.ny,
+                                                           out, out0);
+  return cuda_check(cudaGetLastError(), "otf rbm finish launch");
 }
 
 int irl_lanczos_step_small(double* V, int64_t ldv, double* W, int64_t L, int j, int m, double* ab, void* stream) {

@@ -33,8 +33,10 @@ struct OtfArgs {
   int64_t n_rows;
   int n_in, hidden;
   int nb;                 // row blocks
+  // parameter layout offsets (elements of v): W block, b, u (-1: none, RBM)
+  int64_t offW, offb, offu;
   // dot
-  const double* v;        // padded parameter vector (MLP layout)
+  const double* v;        // padded parameter vector
   double* tpart;          // [JC][N]
   // acc
   const double* y;        // [N]
@@ -111,16 +113,16 @@ __global__ void __launch_bounds__(256) k_otf_dot(const OtfArgs a) {
   const int64_t N = a.n_rows;
   const int64_t lo = (N * blockIdx.y) / a.nb, hi = (N * (blockIdx.y + 1)) / a.nb;
   const int h = a.hidden, nin = a.n_in;
-  const int64_t offb = (int64_t)h * nin, offu = offb + h;
+  const int64_t offW = a.offW, offb = a.offb, offu = a.offu;
 
-  // v_W chunk, v_b, v_u (zero beyond h / n_in)
+  // v_W chunk, v_b, v_u (zero beyond h / n_in; no u block for the RBM)
   for (int e = tid; e < OTF_BJ * OTF_MAX_NIN; e += blockDim.x) {
     const int jj = e / OTF_MAX_NIN, k = e % OTF_MAX_NIN;
-    vw[e] = (j0 + jj < h && k < nin) ? a.v[(int64_t)(j0 + jj) * nin + k] : 0.0;
+    vw[e] = (j0 + jj < h && k < nin) ? a.v[offW + (int64_t)(j0 + jj) * nin + k] : 0.0;
   }
   for (int e = tid; e < OTF_BJ; e += blockDim.x) {
     vb[e] = (j0 + e < h) ? a.v[offb + j0 + e] : 0.0;
-    vu[e] = (j0 + e < h) ? a.v[offu + j0 + e] : 0.0;
+    vu[e] = (j0 + e < h && offu >= 0) ? a.v[offu + j0 + e] : 0.0;
   }
   const int ntiles = (int)((hi - lo + OTF_BM - 1) / OTF_BM);
   if (ntiles > 0) otf_load_tile(a, lo, hi, j0, gs, ts, xs, tid, blockDim.x);
@@ -207,20 +209,38 @@ __global__ void __launch_bounds__(256) k_otf_dot(const OtfArgs a) {
 
 // y_n = c_n (sum_jc tpart + v_c - s) ; s, g0 from per-CTA partial dots (fixed order)
 // Y partials per CTA.
+// p_last >= 0: MLP constant parameter v_c; offa >= 0: RBM visible block, adds x_n . v_a
 __global__ void __launch_bounds__(256) k_otf_y(const double* __restrict__ tpart, int jc_count, int64_t n,
                                                const double* __restrict__ coeff, const double* v, int64_t p_last,
                                                const double* __restrict__ dpart, int n_dpart, double* y,
-                                               double* ypart) {
+                                               double* ypart, const uint64_t* __restrict__ xbits, int64_t offa,
+                                               int n_in) {
   __shared__ double sh[8];
+  __shared__ double va[OTF_MAX_NIN];
+  if (offa >= 0)
+    for (int i = threadIdx.x; i < n_in; i += blockDim.x) va[i] = v[offa + i];
+  __syncthreads();
   double s = 0.0;
   for (int q = 0; q < n_dpart; ++q) s += dpart[q];
-  const double vc = v[p_last];
+  const double vc = p_last >= 0 ? v[p_last] : 0.0;
   double acc = 0.0;
   const int64_t per = (n + gridDim.x - 1) / gridDim.x;
   const int64_t lo = blockIdx.x * per, hi = min(n, lo + per);
   for (int64_t r = lo + threadIdx.x; r < hi; r += blockDim.x) {
     double t = 0.0;
     for (int q = 0; q < jc_count; ++q) t += tpart[(int64_t)q * n + r];
+    if (offa >= 0) {
+      double xa = 0.0;
+      for (int w = 0; w < OTF_XW; ++w) {
+        uint64_t bits = xbits[r * OTF_XW + w];
+        while (bits) {
+          const int b = __ffsll((long long)bits) - 1;
+          bits &= bits - 1;
+          xa += va[w * 64 + b];
+        }
+      }
+      t += xa;
+    }
     const double yy = coeff[r] * ((t + vc) - s);
     y[r] = yy;
     acc += yy;
@@ -570,6 +590,47 @@ __global__ void __launch_bounds__(256) k_rbm_stats_finish(const double* __restri
       for (int b = 0; b < nb; ++b) acc += part[((int64_t)b * hidden + j) * kc + i];
     }
     out[p] = acc;
+  }
+}
+}  // namespace irl
+
+namespace irl {
+// RBM on-the-fly product assembled in the layout [a (n), b (h), W (h x n)]:
+//   out = sum_blocks (x / ones-column / W partials) - obar * Y (+ u0 hf) ; out0 = g0
+__global__ void __launch_bounds__(256) k_rbm_otf_finish(const double* __restrict__ part, int nb, int hidden,
+                                                        int n_in, int kc, const double* __restrict__ xpart, int nbx,
+                                                        const double* __restrict__ ypart, int n_ypart, int64_t ld,
+                                                        const double* __restrict__ obar, const double* hf,
+                                                        const double* u0, const double* dgpart, int n_dgpart,
+                                                        double* out, double* out0) {
+  double Y = 0.0;
+  for (int q = 0; q < n_ypart; ++q) Y += ypart[q];
+  const int64_t P = (int64_t)n_in + hidden + (int64_t)hidden * n_in;
+  const double uu = (hf && u0) ? *u0 : 0.0;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < ld; p += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    if (p < n_in) {
+      for (int b = 0; b < nbx; ++b) acc += xpart[(int64_t)b * n_in + p];
+    } else if (p < n_in + hidden) {
+      const int64_t j = p - n_in;
+      for (int b = 0; b < nb; ++b) acc += part[((int64_t)b * hidden + j) * kc + n_in];
+    } else if (p < P) {
+      const int64_t q = p - n_in - hidden, j = q / n_in, i = q % n_in;
+      for (int b = 0; b < nb; ++b) acc += part[((int64_t)b * hidden + j) * kc + i];
+    }
+    if (p < P) {
+      if (obar) acc = fma(-obar[p], Y, acc);
+      if (hf && u0) acc = fma(uu, hf[p], acc);
+    } else {
+      acc = 0.0;
+    }
+    out[p] = acc;
+  }
+  if (out0 && blockIdx.x == 0 && threadIdx.x == 0) {
+    double g = 0.0;
+    if (hf)
+      for (int q = 0; q < n_dgpart; ++q) g += dgpart[q];
+    *out0 = g;
   }
 }
 }  // namespace irl

@@ -248,9 +248,14 @@ class SampleBatch:
         obar = torch.empty(self.ld, dtype=torch.float64, device=self.device)
         g = torch.empty(self.ld, dtype=torch.float64, device=self.device)
         ws = self.mvp_workspace()
-        _lib.call("irl_otf_colstats_mlp_f64", _lib.ptr(o["xbits"]), _lib.ptr(o["t"]), _lib.ptr(o["g"]), n,
-                  o["n_in"], o["hidden"], self.ld, _lib.ptr(self.weights), _lib.ptr(c), _lib.ptr(obar), _lib.ptr(g),
-                  _lib.ptr(ws), ws.numel(), self._stream())
+        if o["model"] == _lib.MODEL_RBM:
+            _lib.call("irl_otf_colstats_rbm_f64", _lib.ptr(o["xbits"]), _lib.ptr(o["t"]), n, o["n_in"], o["hidden"],
+                      self.ld, _lib.ptr(self.weights), _lib.ptr(c), _lib.ptr(obar), _lib.ptr(g), _lib.ptr(ws),
+                      ws.numel(), self._stream())
+        else:
+            _lib.call("irl_otf_colstats_mlp_f64", _lib.ptr(o["xbits"]), _lib.ptr(o["t"]), _lib.ptr(o["g"]), n,
+                      o["n_in"], o["hidden"], self.ld, _lib.ptr(self.weights), _lib.ptr(c), _lib.ptr(obar),
+                      _lib.ptr(g), _lib.ptr(ws), ws.numel(), self._stream())
         self._colstats[key] = (obar, g)
         return obar, g
 
@@ -315,6 +320,11 @@ def _apply(batch: SampleBatch, coeff: torch.Tensor, v: torch.Tensor, out: torch.
     n = batch.n_rows
     if batch.otf is not None:
         o = batch.otf
+        if o["model"] == _lib.MODEL_RBM:
+            _lib.call("irl_otf_mvp_rbm_f64", _lib.ptr(o["xbits"]), _lib.ptr(o["t"]), n, o["n_in"], o["hidden"],
+                      batch.ld, _lib.ptr(obar), _lib.ptr(coeff), _lib.ptr(v), _lib.ptr(out), _lib.ptr(half_f),
+                      _lib.ptr(u0), _lib.ptr(out0), _lib.ptr(ws), ws.numel(), stream)
+            return
         _lib.call("irl_otf_mvp_mlp_f64", _lib.ptr(o["xbits"]), _lib.ptr(o["t"]), _lib.ptr(o["g"]), n, o["n_in"],
                   o["hidden"], batch.ld, _lib.ptr(obar), _lib.ptr(coeff), _lib.ptr(v), _lib.ptr(out),
                   _lib.ptr(half_f), _lib.ptr(u0), _lib.ptr(out0), _lib.ptr(ws), ws.numel(), stream)

@@ -336,3 +336,32 @@ def test_otf_mlp_matches_stored(pkg, rows, n_in, hidden):
     assert r1.n_matvec == r2.n_matvec
     assert abs(r1.lambda_min - r2.lambda_min) <= RITZ_TOL * abs(r1.lambda_min)
     assert rel(host(r2.direction), host(r1.direction)) < DIR_TOL
+
+
+@pytest.mark.parametrize("idx,rows", [(1, 8192), (2, 2048)])
+def test_otf_rbm_matches_stored(pkg, idx, rows):
+    """On-the-fly RBM (K6): products, stats and IRL == stored-O batch and the oracle."""
+    from paper_2601_01437_b200 import ansatz as A, estimators as E, optimizer as OPT, synthetic as S
+
+    cfg = S.CONFIGS[idx].with_rows(rows)
+    inp = S.make_inputs(cfg)
+    arch = A.RBMArchitecture(cfg.n_inputs, cfg.hidden)
+    params = A.AnsatzParameters(arch, inp.theta)
+    stored = A.build_batch(params, inp.x, inp.e_loc)
+    otf = A.build_batch(params, inp.x, inp.e_loc, mode="otf")
+    assert otf.otf is not None
+    es, eo = E.estimate_energy(stored), E.estimate_energy(otf)
+    P = arch.param_count
+    assert rel(host(E.energy_gradient(otf, eo)), host(E.energy_gradient(stored, es))) < 1e-12
+    assert rel(host(otf.obar()[:P]), host(stored.obar()[:P])) < 1e-13
+    o = nqs.rbm_rows(inp.theta, inp.x, cfg.n_inputs, cfg.hidden)
+    w = np.full(rows, 1.0 / rows)
+    v = np.random.default_rng(3).standard_normal(P)
+    assert rel(E.heff_matvec(otf, eo, v), oest.heff(w, inp.e_loc, o, es.mean, v)) < PROD_TOL
+    assert rel(E.qgt_matvec(otf, v), oest.qgt(w, o, v)) < PROD_TOL
+    conf = OPT.OptimizerConfig(m=cfg.m, max_restarts=3)
+    r1 = OPT.solve_step(stored, conf, seed=cfg.lanczos_seed)
+    r2 = OPT.solve_step(otf, conf, seed=cfg.lanczos_seed)
+    assert r1.n_matvec == r2.n_matvec
+    assert abs(r1.lambda_min - r2.lambda_min) <= RITZ_TOL * abs(r1.lambda_min)
+    assert rel(host(r2.direction), host(r1.direction)) < DIR_TOL
