@@ -55,7 +55,7 @@ def main():
         arch = (A.RBMArchitecture(cfg.n_inputs, cfg.hidden, cfg.complex_params) if cfg.model == "rbm"
                 else A.MLPArchitecture(cfg.n_inputs, cfg.hidden))
         params = A.AnsatzParameters(arch, inp.theta)
-        if args.otf and cfg.model == "mlp":
+        if args.otf and not cfg.complex_params:
             t0 = time.perf_counter()
             batch = A.build_batch_otf(params, inp.x, inp.e_loc)
             en = E.estimate_energy(batch)
