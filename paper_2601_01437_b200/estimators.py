@@ -124,7 +124,7 @@ class SampleBatch:
         # est:50-51 validation (one host sync, once per batch)
         wmin = float(w.min()) if n else 0.0
         wsum = float(w.sum()) if n else 0.0
-        if n and (wmin < 0 or abs(wsum - 1.0) > 1e-12):
+        if wmin < 0 or abs(wsum - 1.0) > 1e-12:  # an empty batch fails here, as in the reference
             raise ValueError("weights must be nonnegative and sum to 1")
         self.configs = None
         self.weights = w

@@ -1,0 +1,147 @@
+"""Edge cases on the device path (reference behaviour: T/test_estimators.py:156-166,
+:208-213; est:44-53, est:147-148, est:178-183): ragged and tiny shapes, exact-mode
+weights, error paths, determinism, ABI status codes."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+from oracle import estimators as oest
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.fixture(scope="module")
+def E(cuda):
+    from paper_2601_01437_b200 import estimators
+
+    return estimators
+
+
+def random_batch(rng, n, p, cplx=False, exact=False):
+    o = rng.normal(0.1, 0.7, (n, p))
+    e = rng.normal(-3.0, 0.3, n)
+    if cplx:
+        o = o + 1j * rng.normal(0, 0.5, (n, p))
+        e = e + 1j * rng.normal(0, 0.05, n)
+    w = rng.random(n) + 0.05 if exact else np.ones(n)
+    return o, e, w / w.sum()
+
+
+@pytest.mark.parametrize("n,p", [(1, 1), (1, 17), (3, 2), (37, 5), (1237, 17), (4099, 33), (513, 1031)])
+@pytest.mark.parametrize("mode", [1, 2])
+def test_ragged_shapes_real(E, n, p, mode):
+    rng = np.random.default_rng(n * 1000 + p)
+    o, e, w = random_batch(rng, n, p, exact=True)
+    b = E.SampleBatch(None, w, e, o, 0)
+    en = E.estimate_energy(b)
+    mean, var, _ = oest.energy(w, e, 0)
+    assert en.mean == pytest.approx(mean, abs=1e-12) and en.std_error == 0.0
+    assert rel(E.energy_gradient(b, en).cpu().numpy(), oest.gradient(w, e, o, mean)) < 1e-9
+    for _ in range(2):
+        v = rng.standard_normal(p)
+        assert rel(E.heff_matvec(b, en, v, mode=mode), oest.heff(w, e, o, mean, v)) < 1e-10
+        assert rel(E.qgt_matvec(b, v, mode=mode), oest.qgt(w, o, v)) < 1e-10
+
+
+@pytest.mark.parametrize("n,p", [(1, 3), (301, 7), (2050, 129)])
+def test_ragged_shapes_complex_raw(E, n, p):
+    rng = np.random.default_rng(n + p)
+    o, e, w = random_batch(rng, n, p, cplx=True, exact=True)
+    b = E.SampleBatch(None, w, e, o, 0)
+    with pytest.warns(UserWarning):
+        en = E.estimate_energy(b)
+    mean, _, _ = oest.energy(w, e, 0)
+    v = rng.standard_normal(p)
+    for mode in (1, 2):
+        assert rel(E.heff_matvec(b, en, v, mode=mode), oest.heff(w, e, o, mean, v)) < 1e-10
+
+
+def test_validation_errors(E):
+    rng = np.random.default_rng(0)
+    o, e, w = random_batch(rng, 10, 4)
+    with pytest.raises(ValueError):  # est:50-51
+        E.SampleBatch(None, w * 2, e, o, 10)
+    with pytest.raises(ValueError):
+        E.SampleBatch(None, -w, e, o, 10)
+    with pytest.raises(ValueError):  # empty batch: weights cannot sum to one
+        E.SampleBatch(None, np.zeros(0), np.zeros(0), np.zeros((0, 4)), 0)
+    with pytest.raises(ValueError):
+        E.SampleBatch(None, w, e[:5], o, 10)
+    b = E.SampleBatch(None, w, e, o, 10)
+    en = E.estimate_energy(b)
+    with pytest.raises(ValueError):  # est:178-181
+        E.heff_matvec(b, en, np.zeros(5))
+    bad = np.zeros(4)
+    bad[1] = np.inf
+    with pytest.raises(ValueError):  # est:182-183
+        E.heff_matvec(b, en, bad)
+    with pytest.raises(E.DensePCapError):  # est:324-325
+        E.dense_heff(b, en, cap=3)
+
+
+def test_host_tensor_inputs_and_outputs(E):
+    import torch
+
+    rng = np.random.default_rng(1)
+    o, e, w = random_batch(rng, 333, 21)
+    b = E.SampleBatch(None, w, e, o, 333)
+    en = E.estimate_energy(b)
+    v = rng.standard_normal(21)
+    ref = oest.heff(w, e, o, en.mean, v)
+    for t in (torch.as_tensor(v), torch.as_tensor(v).pin_memory()):
+        out = E.heff_matvec(b, en, t)
+        assert isinstance(out, torch.Tensor) and not out.is_cuda
+        assert rel(out.numpy(), ref) < 1e-10
+    out = E.heff_matvec(b, en, torch.as_tensor(v, device="cuda"))
+    assert out.is_cuda and rel(out.cpu().numpy(), ref) < 1e-10
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+def test_bitwise_determinism(E, mode):
+    import torch
+
+    rng = np.random.default_rng(2)
+    o, e, w = random_batch(rng, 5000, 300, cplx=True)
+    b = E.SampleBatch(None, w, e, o, 5000, kind="hermitian")
+    en = E.estimate_energy(b)
+    v = torch.as_tensor(rng.standard_normal(300) + 1j * rng.standard_normal(300), device="cuda")
+    first = E.heff_matvec(b, en, v, mode=mode)
+    for _ in range(3):
+        assert torch.equal(first, E.heff_matvec(b, en, v, mode=mode))
+
+
+def test_abi_status_codes(cuda):
+    import torch
+
+    from paper_2601_01437_b200 import _lib
+
+    lib = _lib.lib()
+    n, p = 64, 10
+    ld = _lib.padded_ld(p, False)
+    o = torch.zeros((n, ld), dtype=torch.float64, device="cuda")
+    v = torch.zeros(ld, dtype=torch.float64, device="cuda")
+    c = torch.zeros(n, dtype=torch.float64, device="cuda")
+    ws_bytes = int(lib.irl_mvp_workspace_bytes(n, ld, 0))
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+    st = _lib.stream_handle()
+    ok = lib.irl_mvp_f64(o.data_ptr(), n, p, ld, v.data_ptr(), c.data_ptr(), v.data_ptr(), v.data_ptr(), None, None,
+                         None, 0, ws.data_ptr(), ws_bytes, st)
+    assert ok == _lib.IRL_OK
+    assert lib.irl_mvp_f64(o.data_ptr(), n, p, ld + 16, None, c.data_ptr(), v.data_ptr(), v.data_ptr(), None, None,
+                           None, 0, ws.data_ptr(), ws_bytes, st) == _lib.IRL_ERR_ALIGN
+    assert lib.irl_mvp_f64(o.data_ptr(), n, p, ld, None, c.data_ptr(), v.data_ptr(), v.data_ptr(), None, None, None,
+                           0, ws.data_ptr(), 16, st) == _lib.IRL_ERR_WORKSPACE
+    assert lib.irl_mvp_f64(o.data_ptr() + 8, n, p, ld, None, c.data_ptr(), v.data_ptr(), v.data_ptr(), None, None,
+                           None, 0, ws.data_ptr(), ws_bytes, st) == _lib.IRL_ERR_ALIGN
+    assert lib.irl_mvp_f64(None, n, p, ld, None, c.data_ptr(), v.data_ptr(), v.data_ptr(), None, None, None, 0,
+                           ws.data_ptr(), ws_bytes, st) == _lib.IRL_ERR_ARG
+    assert lib.irl_mvp_f64(o.data_ptr(), n, p, ld, None, c.data_ptr(), v.data_ptr(), v.data_ptr(), None, None, None,
+                           7, ws.data_ptr(), ws_bytes, st) == _lib.IRL_ERR_ARG
+    assert b"bad mvp mode" in lib.irl_last_error()
+    torch.cuda.synchronize()
