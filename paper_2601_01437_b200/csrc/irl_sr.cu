@@ -634,19 +634,13 @@ struct OPlan {
   void (*fn)(ORowArgs, int);
 };
 
-bool obuild_tma() {
-  static const int v = getenv("IRL_OBUILD_TMA") ? atoi(getenv("IRL_OBUILD_TMA")) : 1;
-  return v != 0;
-}
-
 template <bool CPLX, int MODEL, bool STATS>
 void (*pick_orows(int ppt))(ORowArgs, int) {
-  const bool tma = obuild_tma();
   switch (ppt) {
-    case 1: return tma ? k_orows<CPLX, MODEL, 1, STATS, true> : k_orows<CPLX, MODEL, 1, STATS, false>;
-    case 2: return tma ? k_orows<CPLX, MODEL, 2, STATS, true> : k_orows<CPLX, MODEL, 2, STATS, false>;
-    case 4: return tma ? k_orows<CPLX, MODEL, 4, STATS, true> : k_orows<CPLX, MODEL, 4, STATS, false>;
-    default: return tma ? k_orows<CPLX, MODEL, 8, STATS, true> : k_orows<CPLX, MODEL, 8, STATS, false>;
+    case 1: return k_orows<CPLX, MODEL, 1, STATS>;
+    case 2: return k_orows<CPLX, MODEL, 2, STATS>;
+    case 4: return k_orows<CPLX, MODEL, 4, STATS>;
+    default: return k_orows<CPLX, MODEL, 8, STATS>;
   }
 }
 
@@ -811,7 +805,7 @@ int obuild_impl(bool cplx, int model, const uint8_t* x, int64_t n, int n_vis, in
   const size_t tab_bytes = (size_t)((tab_len + 1) & ~1) * sS;
   // rows per staging group: amortise the per-group barrier, ~48 KB of tables
   const int R = (int)std::max<size_t>(1, std::min<size_t>(8, (size_t)(24 * 1024) / tab_bytes));
-  const size_t smem = 2 * (size_t)R * tab_bytes + (obuild_tma() ? (size_t)2 * p.W * 16 : 0);
+  const size_t smem = 2 * (size_t)R * tab_bytes;
   {
     DevInfo d;
     IRL_TRY(dev_info(d));

@@ -184,10 +184,7 @@ __device__ __forceinline__ void orow_stage(const ORowArgs& a, int64_t n, typenam
 
 // STATS: accumulate the column statistics in the writer (complex RBM); real
 // models get them from the DMMA GEMMs of otf.cuh instead (lighter writer).
-// TMA: rows are assembled in a double-buffered shared-memory staging row and
-// written by the TMA engine (cp.async.bulk.global.shared::cta) instead of
-// per-thread 16-B stores.
-template <bool CPLX, int MODEL, int PPT, bool STATS, bool TMA>
+template <bool CPLX, int MODEL, int PPT, bool STATS>
 __global__ void __launch_bounds__(512) k_orows(const ORowArgs a, int R) {
   using T = Traits<CPLX>;
   using S = typename T::S;
@@ -201,8 +198,6 @@ __global__ void __launch_bounds__(512) k_orows(const ORowArgs a, int R) {
   constexpr int E = Traits<CPLX>::kElemsPerUnit;
   const int TL = (orow_tab_len<MODEL>(a.n_vis, a.hidden) + 1) & ~1;
   S* tabs = reinterpret_cast<S*>(smem_r);  // [2][R][TL] factor tables, R rows per group
-  double2* stg = reinterpret_cast<double2*>(tabs + (size_t)2 * R * TL);  // [2][W] staging rows (TMA)
-  int srow = 0;                                                          // staging parity counter
 
   // smem byte offsets of the two factors of each element (relative to the row table)
   uint32_t pr[PPT][E];
@@ -281,30 +276,10 @@ __global__ void __launch_bounds__(512) k_orows(const ORowArgs a, int R) {
               acc1[k].y = fma(cn, u.y, acc1[k].y);
             }
           }
-          if constexpr (TMA) {
-            stg[(srow & 1) * W + tid + k * NT] = u;
-          } else {
-            st_stream(orow + k * NT, u);
-          }
+          st_stream(orow + k * NT, u);
         }
-      }
-      if constexpr (TMA) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // row r-1 left smem
-        __syncthreads();
-        if (tid == 0) {
-          const uint32_t src = smem_addr(stg + (srow & 1) * W);
-          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(orow - tid),
-                       "r"(src), "r"((uint32_t)W * 16u)
-                       : "memory");
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        }
-        ++srow;
       }
     }
-  }
-  if constexpr (TMA) {
-    if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   if constexpr (STATS) {
 #pragma unroll
