@@ -593,11 +593,7 @@ int otf_acc_launch(const OtfPlan& pl, OtfArgs& a, cudaStream_t st, int nyv, bool
 int otf_stats(const OtfPlan& pl, OtfArgs a, const OtfWs& wl, int model, int64_t n, int n_in, int hidden,
               int64_t ld, const double* w, const double* coeff, double* obar, double* grad, double* xpart, int nbx,
               cudaStream_t st) {
-  // TODO(round 2): the HAS_T = false instance of k_otf_acc gives wrong sums on
-  // the GPU (tests/test_gpu_parity.py::test_otf_rbm_matches_stored catches it);
-  // the RBM runs the HAS_T = true instance with T := t (one redundant tile load)
-  const bool has_t = true;
-  (void)model;
+  const bool has_t = model == MODEL_MLP;  // the RBM has no u block: G-only tiles
   const double* ys[2] = {w, coeff};
   double* outs[2] = {obar, grad};
   a.part = wl.part;
@@ -1127,7 +1123,7 @@ int irl_otf_mvp_rbm_f64(const uint64_t* xbits, const double* t, int64_t n, int n
   IRL_TRY(cuda_check(cudaGetLastError(), "otf dot launch"));
   k_otf_y<<<pl.ny, 256, 0, st>>>(wl.tpart, pl.jc, n, coeff, v, -1, wl.dpart, obar ? pl.ny : 0, wl.y, wl.ypart, xbits,
                                  0, n_vis);
-  IRL_TRY(otf_acc_launch(pl, a, st, 1, true));  // HAS_T = false instance: see otf_stats
+  IRL_TRY(otf_acc_launch(pl, a, st, 1, false));
   const int nbx = std::min<int>(4 * d.sms, (int)std::max<int64_t>(1, n / 64));
   k_xsum<<<nbx, 128, 0, st>>>(xbits, wl.y, n, n_vis, wl.xpart, wl.ypart2);
   k_rbm_otf_finish<<<(unsigned)cdiv(ld, 256), 256, 0, st>>>(wl.part, pl.nb, hidden, n_vis, pl.kc, wl.xpart, nbx,

@@ -77,7 +77,7 @@ __global__ void k_pack_bits(const uint8_t* __restrict__ x, int64_t n, int n_in, 
   }
 }
 
-// Tile loader: G/T rows [r0, r0+BM) x columns [j0, j0+BJ) and the packed bits.
+// Tile loader: G (and T unless ts is null) rows [r0, r0+BM) x columns [j0, j0+BJ), packed bits.
 __device__ __forceinline__ void otf_load_tile(const OtfArgs& a, int64_t r0, int64_t hi, int j0, double* gs, double* ts,
                                               uint64_t* xs, int tid, int nthreads) {
   // 64 rows x 64 doubles = 512 B per row = 32 x 16 B per row, for G and T
@@ -87,7 +87,7 @@ __device__ __forceinline__ void otf_load_tile(const OtfArgs& a, int64_t r0, int6
     const bool ok = row < hi && (j0 + c) < a.hidden;
     const int64_t off = ok ? row * a.hidden + j0 + c : 0;
     cp_async16(gs + r * OTF_BJ + c, a.G + off, ok);
-    cp_async16(ts + r * OTF_BJ + c, a.T + off, ok);
+    if (ts) cp_async16(ts + r * OTF_BJ + c, a.T + off, ok);  // ts == nullptr: G-only tiles (RBM)
   }
   for (int e = tid; e < OTF_BM; e += nthreads) {
     const int64_t row = r0 + e;
