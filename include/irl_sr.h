@@ -149,6 +149,21 @@ int irl_otf_mvp_mlp_f64(const uint64_t* xbits, const double* t, const double* g,
                         int64_t ld, const double* obar, const double* coeff, const double* v, double* out,
                         const double* half_f, const double* u0, double* out0, void* ws, size_t ws_bytes,
                         void* stream);
+/* Complex-theta RBM on the fly (hermitian kind, cfg4): t = tanh(b + W x) complex
+ * (N x h interleaved c128), vectors in the planar real embedding of irl_mvp_c128
+ * (ld = irl_padded_ld(P, 1)); obar, coeff, grad interleaved c128.  Statistics:
+ * obar = sum w O, grad = sum c conj(O) (estimators.py:156-168); product as
+ * irl_mvp_c128 with a real coeff stored as c128. */
+size_t irl_otf_workspace_bytes_c128(int64_t n, int n_vis, int hidden);
+int irl_otf_prepare_rbm_c128(const uint8_t* x, int64_t n, int n_vis, int hidden, const double* theta,
+                             uint64_t* xbits, double* t, void* stream);
+int irl_otf_colstats_rbm_c128(const uint64_t* xbits, const double* t, int64_t n, int n_vis, int hidden, int64_t ld,
+                              const double* w, const double* coeff, double* obar, double* grad, void* ws,
+                              size_t ws_bytes, void* stream);
+int irl_otf_mvp_rbm_c128(const uint64_t* xbits, const double* t, int64_t n, int n_vis, int hidden, int64_t ld,
+                         const double* obar, const double* coeff, const double* v_re, const double* v_im,
+                         double* out_re, double* out_im, const double* half_f_re, const double* half_f_im,
+                         const double* u0, double* out0, void* ws, size_t ws_bytes, void* stream);
 
 /* ------------------------------------------------------ A13 / A16 ----
  * IRL driver helpers.

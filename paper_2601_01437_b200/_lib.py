@@ -64,6 +64,10 @@ SIGNATURES = {
     "irl_otf_prepare_rbm_f64": (_I, [_P, _I64, _I, _I, _P, _P, _P, _P]),
     "irl_otf_colstats_rbm_f64": (_I, [_P, _P, _I64, _I, _I, _I64, _P, _P, _P, _P, _P, _SZ, _P]),
     "irl_otf_mvp_rbm_f64": (_I, [_P, _P, _I64, _I, _I, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "irl_otf_workspace_bytes_c128": (_SZ, [_I64, _I, _I]),
+    "irl_otf_prepare_rbm_c128": (_I, [_P, _I64, _I, _I, _P, _P, _P, _P]),
+    "irl_otf_colstats_rbm_c128": (_I, [_P, _P, _I64, _I, _I, _I64, _P, _P, _P, _P, _P, _SZ, _P]),
+    "irl_otf_mvp_rbm_c128": (_I, [_P, _P, _I64, _I, _I, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
 }
 
 

@@ -236,8 +236,9 @@ def build_batch_otf(params: AnsatzParameters, x, e_loc, weights=None, n_samples:
     qgt_matvec, solve_step) as a stored-O batch.
     """
     arch = params.architecture
-    if arch.complex_params:
-        raise ValueError("on-the-fly mode is implemented for real parameters (RBM f64, MLP)")
+    cplx = bool(arch.complex_params)
+    if cplx and arch.model != _lib.MODEL_RBM:
+        raise ValueError("complex parameters are an RBM feature")
     dev = _device(device)
     xt = _x_device(x, arch.n_inputs, dev)
     n = int(xt.shape[0])
@@ -248,16 +249,22 @@ def build_batch_otf(params: AnsatzParameters, x, e_loc, weights=None, n_samples:
         if n_samples is None:
             n_samples = n
     p = arch.param_count
-    ld = _lib.padded_ld(p, False)
+    ld = _lib.padded_ld(p, cplx)
+    odt = torch.complex128 if cplx else torch.float64
     # a zero-width placeholder keeps SampleBatch's validation; O is not stored
-    placeholder = torch.empty((n, ld), dtype=torch.float64, device="meta")
+    placeholder = torch.empty((n, ld), dtype=odt, device="meta")
     batch = SampleBatch.__new__(SampleBatch)
-    SampleBatch._init_common(batch, weights, e_loc, n, n_samples or 0, KIND_REAL, p, ld, dev)
+    SampleBatch._init_common(batch, weights, e_loc, n, n_samples or 0, KIND_HERMITIAN if cplx else KIND_REAL, p, ld,
+                             dev)
     batch.o_matrix = placeholder
     xbits = torch.empty((n, 2), dtype=torch.int64, device=dev)
-    t = torch.empty((n, arch.hidden), dtype=torch.float64, device=dev)
+    t = torch.empty((n, arch.hidden), dtype=odt, device=dev)
     theta = _theta_device(params, dev)
-    if arch.model == _lib.MODEL_RBM:
+    if cplx:
+        g = None
+        _lib.call("irl_otf_prepare_rbm_c128", _lib.ptr(xt), n, arch.n_visible, arch.hidden, _lib.ptr(theta),
+                  _lib.ptr(xbits), _lib.ptr(t), _lib.stream_handle(dev))
+    elif arch.model == _lib.MODEL_RBM:
         g = None
         _lib.call("irl_otf_prepare_rbm_f64", _lib.ptr(xt), n, arch.n_visible, arch.hidden, _lib.ptr(theta),
                   _lib.ptr(xbits), _lib.ptr(t), _lib.stream_handle(dev))

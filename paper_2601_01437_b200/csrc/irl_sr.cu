@@ -623,6 +623,105 @@ int otf_stats(const OtfPlan& pl, OtfArgs a, const OtfWs& wl, int model, int64_t 
   return IRL_OK;
 }
 
+
+// complex-parameter RBM on the fly (hermitian kind): T viewed as N x 2h real
+struct OtfCPlan {
+  int jc, nb_dot, nb_acc, ny, nbx;
+  int nkt, kc;
+  size_t smem_dot, smem_acc;
+};
+
+using AccCFn = void (*)(OtfCArgs);
+
+AccCFn pick_acc_c(int nkt) {
+  switch (nkt) {
+    case 3: return k_otf_acc_c<3>;
+    case 6: return k_otf_acc_c<6>;
+    case 8: return k_otf_acc_c<8>;
+    case 13: return k_otf_acc_c<13>;
+    default: return nullptr;
+  }
+}
+
+int make_otfc_plan(int64_t n, int n_in, int hidden, OtfCPlan& p) {
+  DevInfo d;
+  IRL_TRY(dev_info(d));
+  if (n_in < 1 || n_in > OTF_MAX_NIN) return fail(IRL_ERR_ARG, "on-the-fly mode supports n_in <= %d", OTF_MAX_NIN);
+  p.jc = (int)cdiv(2LL * hidden, OTF_BJ);
+  const int k8 = (n_in + 1 + 7) / 8;
+  p.nkt = k8 <= 3 ? 3 : k8 <= 6 ? 6 : k8 <= 8 ? 8 : 13;
+  p.kc = 8 * p.nkt;
+  p.smem_dot = (size_t)(OTF_BJ * OTF_MAX_NIN + OTF_BJ + 2 * OTF_BM * OTF_BJ) * 8 + 2 * OTF_BM * OTF_XW * 8 +
+               4 * OTF_BM * 16;
+  p.smem_acc = (size_t)(2 * OTF_BM * OTF_BJ) * 8 + 2 * OTF_BM * OTF_XW * 8 + 2 * OTF_BM * 16;
+  AccCFn acc = pick_acc_c(p.nkt);
+  IRL_TRY(ensure_fn_attrs((const void*)k_otf_dot_c, d.smem_optin));
+  IRL_TRY(ensure_fn_attrs((const void*)acc, d.smem_optin));
+  int occ_d = 1, occ_a = 1;
+  IRL_TRY(cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_d, (const void*)k_otf_dot_c, 256, p.smem_dot),
+                     "occ"));
+  IRL_TRY(cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_a, (const void*)acc, 256, p.smem_acc), "occ"));
+  const int64_t tiles = std::max<int64_t>(1, cdiv(n, OTF_BM));
+  // one wave of CTAs (row blocks x column chunks), never more row blocks than row tiles
+  p.nb_dot = (int)std::min<int64_t>(tiles, std::max(1, d.sms * std::max(occ_d, 1) / p.jc));
+  p.nb_acc = (int)std::min<int64_t>(tiles, std::max(1, d.sms * std::max(occ_a, 1) / p.jc));
+  p.ny = d.sms;
+  p.nbx = std::min<int>(4 * d.sms, (int)std::max<int64_t>(1, n / 64));
+  return IRL_OK;
+}
+
+struct OtfCWs {
+  double2 *tpart, *y, *ypart, *dpart, *xpart;
+  double *gpart, *part;
+  size_t bytes;
+};
+
+OtfCWs otfc_ws_layout(const OtfCPlan& p, int64_t n, int n_in, int hidden, void* base) {
+  OtfCWs w{};
+  size_t off = 0;
+  auto carve = [&](size_t b) {
+    char* r = base ? static_cast<char*>(base) + off : nullptr;
+    off += align256(b);
+    return r;
+  };
+  w.tpart = reinterpret_cast<double2*>(carve((size_t)p.jc * n * 16));
+  w.y = reinterpret_cast<double2*>(carve((size_t)n * 16));
+  w.ypart = reinterpret_cast<double2*>(carve((size_t)p.ny * 16));
+  w.dpart = reinterpret_cast<double2*>(carve((size_t)p.ny * 16));
+  w.xpart = reinterpret_cast<double2*>(carve((size_t)p.nbx * n_in * 16));
+  w.gpart = reinterpret_cast<double*>(carve((size_t)p.ny * 8));
+  w.part = reinterpret_cast<double*>(carve((size_t)p.nb_acc * 2 * hidden * p.kc * 8));
+  w.bytes = off;
+  return w;
+}
+
+int otfc_check(const uint64_t* xbits, const double* t, int64_t n, int n_vis, int hidden, int64_t ld) {
+  if (!xbits || !t) return fail(IRL_ERR_ARG, "null pointer");
+  if (n < 1 || hidden < 1 || n_vis < 1) return fail(IRL_ERR_ARG, "bad shape");
+  if (n_vis > OTF_MAX_NIN) return fail(IRL_ERR_ARG, "on-the-fly mode supports n_vis <= %d", OTF_MAX_NIN);
+  const int64_t P = (int64_t)n_vis + hidden + (int64_t)hidden * n_vis;
+  if (ld != irl_padded_ld(P, 1)) return fail(IRL_ERR_ALIGN, "ld must equal irl_padded_ld(P=%lld, complex)", (long long)P);
+  if (!aligned16(xbits) || !aligned16(t)) return fail(IRL_ERR_ALIGN, "on-the-fly operands must be 16-byte aligned");
+  return IRL_OK;
+}
+
+// Sum_n conj(O_n) y_n for the complex RBM -> out_c (interleaved), conj'd when conj_out
+int otfc_colsum(const OtfCPlan& pl, OtfCArgs a, const OtfCWs& wl, int64_t ld, const double2* y, const double* yr,
+                double2* out_c, int conj_out, cudaStream_t st) {
+  a.y = y;
+  a.yr = yr;
+  a.part = wl.part;
+  a.nb = pl.nb_acc;
+  pick_acc_c(pl.nkt)<<<dim3((unsigned)pl.jc, (unsigned)pl.nb_acc), 256, pl.smem_acc, st>>>(a);
+  IRL_TRY(cuda_check(cudaGetLastError(), "otf acc (complex) launch"));
+  k_xsum_c<<<pl.nbx, 128, 0, st>>>(a.xbits, y, yr, a.n_rows, a.n_in, wl.xpart);
+  k_rbm_otf_finish_c<<<(unsigned)cdiv(ld, 256), 256, 0, st>>>(wl.part, pl.nb_acc, a.hidden, a.n_in, pl.kc, wl.xpart,
+                                                             pl.nbx, nullptr, 0, ld, nullptr, nullptr, nullptr,
+                                                             nullptr, nullptr, 0, nullptr, nullptr, nullptr, out_c,
+                                                             conj_out);
+  return cuda_check(cudaGetLastError(), "otf finish (complex) launch");
+}
+
 // ------------------------------------------------------------ obuild ----
 struct OPlan {
   int C, W, PPT, NT, nb;
@@ -1130,6 +1229,89 @@ int irl_otf_mvp_rbm_f64(const uint64_t* xbits, const double* t, int64_t n, int n
                                                            wl.ypart, pl.ny, ld, obar, half_f, u0, wl.gpart, pl.ny,
                                                            out, out0);
   return cuda_check(cudaGetLastError(), "otf rbm finish launch");
+}
+
+int irl_otf_prepare_rbm_c128(const uint8_t* x, int64_t n, int n_vis, int hidden, const double* theta,
+                             uint64_t* xbits, double* t, void* stream) {
+  if (!x || !theta || !xbits || !t || n < 1 || n_vis < 1 || hidden < 1) return fail(IRL_ERR_ARG, "bad prepare arguments");
+  if (n_vis > OTF_MAX_NIN) return fail(IRL_ERR_ARG, "on-the-fly RBM needs n_vis <= %d", OTF_MAX_NIN);
+  cudaStream_t st = (cudaStream_t)stream;
+  IRL_TRY(pack_bits(x, n, n_vis, xbits, st));
+  const double2* th = reinterpret_cast<const double2*>(theta);
+  return launch_hidden<true, MODEL_RBM>(x, xbits, n, n_vis, hidden, th + n_vis + hidden, th + n_vis, nullptr, t,
+                                        nullptr, st);
+}
+
+size_t irl_otf_workspace_bytes_c128(int64_t n, int n_vis, int hidden) {
+  OtfCPlan p;
+  if (make_otfc_plan(n, n_vis, hidden, p) != IRL_OK) return 0;
+  return otfc_ws_layout(p, n, n_vis, hidden, nullptr).bytes;
+}
+
+int irl_otf_colstats_rbm_c128(const uint64_t* xbits, const double* t, int64_t n, int n_vis, int hidden, int64_t ld,
+                              const double* w, const double* coeff, double* obar, double* grad, void* ws,
+                              size_t ws_bytes, void* stream) {
+  IRL_TRY(otfc_check(xbits, t, n, n_vis, hidden, ld));
+  if (!w || !coeff || !obar || !grad) return fail(IRL_ERR_ARG, "null pointer");
+  OtfCPlan pl;
+  IRL_TRY(make_otfc_plan(n, n_vis, hidden, pl));
+  OtfCWs wl = otfc_ws_layout(pl, n, n_vis, hidden, ws);
+  if (ws_bytes < wl.bytes) return fail(IRL_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, wl.bytes);
+  cudaStream_t st = (cudaStream_t)stream;
+  OtfCArgs a{};
+  a.xbits = xbits;
+  a.T = t;
+  a.n_rows = n;
+  a.n_in = n_vis;
+  a.hidden = hidden;
+  // obar = sum w O = conj(sum w conj(O)) ; grad = sum c conj(O)
+  IRL_TRY(otfc_colsum(pl, a, wl, ld, nullptr, w, reinterpret_cast<double2*>(obar), 1, st));
+  return otfc_colsum(pl, a, wl, ld, reinterpret_cast<const double2*>(coeff), nullptr,
+                     reinterpret_cast<double2*>(grad), 0, st);
+}
+
+int irl_otf_mvp_rbm_c128(const uint64_t* xbits, const double* t, int64_t n, int n_vis, int hidden, int64_t ld,
+                         const double* obar, const double* coeff, const double* v_re, const double* v_im,
+                         double* out_re, double* out_im, const double* half_f_re, const double* half_f_im,
+                         const double* u0, double* out0, void* ws, size_t ws_bytes, void* stream) {
+  IRL_TRY(otfc_check(xbits, t, n, n_vis, hidden, ld));
+  if (!coeff || !v_re || !v_im || !out_re || !out_im) return fail(IRL_ERR_ARG, "null pointer");
+  if ((half_f_re || u0 || out0) && !(half_f_re && half_f_im && u0 && out0))
+    return fail(IRL_ERR_ARG, "bordered product needs half_f_re, half_f_im, u0 and out0");
+  OtfCPlan pl;
+  IRL_TRY(make_otfc_plan(n, n_vis, hidden, pl));
+  OtfCWs wl = otfc_ws_layout(pl, n, n_vis, hidden, ws);
+  if (ws_bytes < wl.bytes) return fail(IRL_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, wl.bytes);
+  cudaStream_t st = (cudaStream_t)stream;
+  const double2* ob = reinterpret_cast<const double2*>(obar);
+  k_vdot_c<<<pl.ny, 256, 0, st>>>(ob, v_re, v_im, half_f_re, half_f_im, ld, wl.dpart, wl.gpart);
+  OtfCArgs a{};
+  a.xbits = xbits;
+  a.T = t;
+  a.n_rows = n;
+  a.n_in = n_vis;
+  a.hidden = hidden;
+  a.nb = pl.nb_dot;
+  a.offW = (int64_t)n_vis + hidden;
+  a.offb = n_vis;
+  a.v_re = v_re;
+  a.v_im = v_im;
+  a.tpart = wl.tpart;
+  k_otf_dot_c<<<dim3((unsigned)pl.jc, (unsigned)pl.nb_dot), 256, pl.smem_dot, st>>>(a);
+  IRL_TRY(cuda_check(cudaGetLastError(), "otf dot (complex) launch"));
+  k_otf_y_c<<<pl.ny, 256, 0, st>>>(wl.tpart, pl.jc, n, reinterpret_cast<const double2*>(coeff), v_re, v_im, 0, n_vis,
+                                   xbits, wl.dpart, obar ? pl.ny : 0, wl.y, wl.ypart);
+  a.y = wl.y;
+  a.yr = nullptr;
+  a.part = wl.part;
+  a.nb = pl.nb_acc;
+  pick_acc_c(pl.nkt)<<<dim3((unsigned)pl.jc, (unsigned)pl.nb_acc), 256, pl.smem_acc, st>>>(a);
+  IRL_TRY(cuda_check(cudaGetLastError(), "otf acc (complex) launch"));
+  k_xsum_c<<<pl.nbx, 128, 0, st>>>(xbits, wl.y, nullptr, n, n_vis, wl.xpart);
+  k_rbm_otf_finish_c<<<(unsigned)cdiv(ld, 256), 256, 0, st>>>(wl.part, pl.nb_acc, hidden, n_vis, pl.kc, wl.xpart,
+                                                             pl.nbx, wl.ypart, pl.ny, ld, ob, half_f_re, half_f_im,
+                                                             u0, wl.gpart, pl.ny, out_re, out_im, out0, nullptr, 0);
+  return cuda_check(cudaGetLastError(), "otf finish (complex) launch");
 }
 
 int irl_lanczos_step_small(double* V, int64_t ldv, double* W, int64_t L, int j, int m, double* ab, void* stream) {

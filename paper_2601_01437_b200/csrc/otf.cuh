@@ -634,3 +634,416 @@ __global__ void __launch_bounds__(256) k_rbm_otf_finish(const double* __restrict
   }
 }
 }  // namespace irl
+
+// ============================================================================
+// Complex-parameter (Hermitian, cfg4) RBM on the fly.  T (N x h complex) is
+// viewed as a real N x 2h matrix (Re/Im column pairs), so the same DMMA tiles
+// apply: the pair (2j, 2j+1) of every C fragment is one complex value.
+//   dot : A = X V_W^T + v_b (complex) ; t_n = x.v_a + sum_j T_nj A_nj
+//   acc : out[2j+p][kc] = sum_n (conj(T_nj) y_n)_p x_n,kc   (ones column kc = n_in)
+// ============================================================================
+namespace irl {
+
+struct OtfCArgs {
+  const uint64_t* xbits;
+  const double* T;   // [N][2h] real view of the complex activations
+  int64_t n_rows;
+  int n_in, hidden;  // hidden = complex units h
+  int nb;
+  int64_t offW, offb;  // complex parameter offsets (RBM layout [a, b, W])
+  const double* v_re;
+  const double* v_im;
+  double2* tpart;      // [JC][N]
+  const double2* y;    // [N] complex row weights, or
+  const double* yr;    // [N] real row weights (y == nullptr)
+  double* part;        // [nb][2h][KC]
+};
+
+__device__ __forceinline__ void otf_load_ctile(const OtfCArgs& a, int64_t r0, int64_t hi, int c0, double* gs,
+                                               uint64_t* xs, int tid, int nthreads) {
+  const int ncols = 2 * a.hidden;
+  for (int e = tid; e < OTF_BM * (OTF_BJ / 2); e += nthreads) {
+    const int r = e / (OTF_BJ / 2), c = (e % (OTF_BJ / 2)) * 2;
+    const int64_t row = r0 + r;
+    const bool ok = row < hi && (c0 + c) < ncols;
+    cp_async16(gs + r * OTF_BJ + c, a.T + (ok ? row * ncols + c0 + c : 0), ok);
+  }
+  for (int e = tid; e < OTF_BM; e += nthreads) {
+    const int64_t row = r0 + e;
+    const bool ok = row < hi;
+    cp_async16(xs + e * OTF_XW, a.xbits + (ok ? row * OTF_XW : 0), ok);
+  }
+}
+
+// grid (ceil(2h/64), nb), 256 threads
+__global__ void __launch_bounds__(256) k_otf_dot_c(const OtfCArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_c[];
+  double* vw = reinterpret_cast<double*>(smem_c);            // [64][OTF_MAX_NIN]
+  double* vb = vw + OTF_BJ * OTF_MAX_NIN;                    // [64]
+  double* gs = vb + OTF_BJ;                                  // [2][BM][64]
+  uint64_t* xs = reinterpret_cast<uint64_t*>(gs + 2 * OTF_BM * OTF_BJ);  // [2][BM][XW]
+  double2* red = reinterpret_cast<double2*>(xs + 2 * OTF_BM * OTF_XW);   // [4][BM]
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wr = warp >> 2, wj = warp & 3;
+  const int c0 = blockIdx.x * OTF_BJ;  // real column chunk
+  const int ncols = 2 * a.hidden, nin = a.n_in;
+  const int64_t N = a.n_rows;
+  const int64_t lo = (N * blockIdx.y) / a.nb, hi = (N * (blockIdx.y + 1)) / a.nb;
+  for (int e = tid; e < OTF_BJ * OTF_MAX_NIN; e += blockDim.x) {
+    const int cc = e / OTF_MAX_NIN, k = e % OTF_MAX_NIN;
+    const int col = c0 + cc;
+    double val = 0.0;
+    if (col < ncols && k < nin) {
+      const int64_t idx = a.offW + (int64_t)(col >> 1) * nin + k;
+      val = (col & 1) ? a.v_im[idx] : a.v_re[idx];
+    }
+    vw[e] = val;
+  }
+  for (int e = tid; e < OTF_BJ; e += blockDim.x) {
+    const int col = c0 + e;
+    vb[e] = col < ncols ? ((col & 1) ? a.v_im[a.offb + (col >> 1)] : a.v_re[a.offb + (col >> 1)]) : 0.0;
+  }
+  const int ntiles = (int)((hi - lo + OTF_BM - 1) / OTF_BM);
+  if (ntiles > 0) otf_load_ctile(a, lo, hi, c0, gs, xs, tid, blockDim.x);
+  cp_async_commit();
+  const int ksteps = (nin + 3) / 4;
+  const double* vrow0 = vw + (wj * 16 + (lane >> 2)) * OTF_MAX_NIN + (lane & 3);
+  for (int it = 0; it < ntiles; ++it) {
+    const int buf = it & 1;
+    const int64_t r0 = lo + (int64_t)it * OTF_BM;
+    if (it + 1 < ntiles)
+      otf_load_ctile(a, r0 + OTF_BM, hi, c0, gs + (buf ^ 1) * OTF_BM * OTF_BJ, xs + (buf ^ 1) * OTF_BM * OTF_XW, tid,
+                     blockDim.x);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const double* G = gs + buf * OTF_BM * OTF_BJ;
+    const uint64_t* X = xs + buf * OTF_BM * OTF_XW;
+    double c[4][2][2];
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      const int cl = wj * 16 + nt * 8 + (lane & 3) * 2;
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        c[mt][nt][0] = vb[cl];
+        c[mt][nt][1] = vb[cl + 1];
+      }
+    }
+    uint64_t xr[4][OTF_XW];
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int q = 0; q < OTF_XW; ++q) xr[mt][q] = X[(wr * 32 + mt * 8 + (lane >> 2)) * OTF_XW + q];
+    for (int kk = 0; kk < ksteps; ++kk) {
+      const int k = kk * 4 + (lane & 3);
+      const double b0 = vrow0[kk * 4];
+      const double b1 = vrow0[kk * 4 + 8 * OTF_MAX_NIN];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        const uint64_t word = (k < 64) ? xr[mt][0] : xr[mt][1];
+        const double av = bit_to_double((uint32_t)(word >> (k & 63)) & 1u);
+        dmma(c[mt][0][0], c[mt][0][1], av, b0);
+        dmma(c[mt][1][0], c[mt][1][1], av, b1);
+      }
+    }
+    // epilogue: complex row sums of T_nj A_nj over this chunk's units
+    double2 rs[4];
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {
+      const int rl = wr * 32 + mt * 8 + (lane >> 2);
+      double sre = 0.0, sim = 0.0;
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const int cl = wj * 16 + nt * 8 + (lane & 3) * 2;
+        const double2 t2 = *reinterpret_cast<const double2*>(G + rl * OTF_BJ + cl);
+        sre = fma(t2.x, c[mt][nt][0], sre);
+        sre = fma(-t2.y, c[mt][nt][1], sre);
+        sim = fma(t2.x, c[mt][nt][1], sim);
+        sim = fma(t2.y, c[mt][nt][0], sim);
+      }
+      sre += __shfl_xor_sync(0xffffffffu, sre, 1);
+      sim += __shfl_xor_sync(0xffffffffu, sim, 1);
+      sre += __shfl_xor_sync(0xffffffffu, sre, 2);
+      sim += __shfl_xor_sync(0xffffffffu, sim, 2);
+      rs[mt] = make_double2(sre, sim);
+    }
+    if ((lane & 3) == 0) {
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) red[wj * OTF_BM + wr * 32 + mt * 8 + (lane >> 2)] = rs[mt];
+    }
+    __syncthreads();
+    if (tid < OTF_BM) {
+      const int64_t row = r0 + tid;
+      if (row < hi) {
+        double2 t = red[tid];
+        for (int w = 1; w < 4; ++w) {
+          t.x += red[w * OTF_BM + tid].x;
+          t.y += red[w * OTF_BM + tid].y;
+        }
+        a.tpart[(int64_t)blockIdx.x * N + row] = t;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// s = sum obar_p v_p (complex, obar interleaved, v planar), g0 = sum hf_re v_re + hf_im v_im
+__global__ void __launch_bounds__(256) k_vdot_c(const double2* __restrict__ obar, const double* __restrict__ v_re,
+                                                const double* __restrict__ v_im, const double* __restrict__ h_re,
+                                                const double* __restrict__ h_im, int64_t len, double2* sp,
+                                                double* gp) {
+  __shared__ double sh[3][8];
+  double xr = 0.0, xi = 0.0, g = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x) {
+    const double vr = v_re[i], vi = v_im ? v_im[i] : 0.0;
+    if (obar) {
+      const double2 o = obar[i];
+      xr = fma(o.x, vr, fma(-o.y, vi, xr));
+      xi = fma(o.x, vi, fma(o.y, vr, xi));
+    }
+    if (h_re) g = fma(h_re[i], vr, fma(h_im ? h_im[i] : 0.0, vi, g));
+  }
+  xr = warp_sum<false>(xr);
+  xi = warp_sum<false>(xi);
+  g = warp_sum<false>(g);
+  if ((threadIdx.x & 31) == 0) {
+    sh[0][threadIdx.x >> 5] = xr;
+    sh[1][threadIdx.x >> 5] = xi;
+    sh[2][threadIdx.x >> 5] = g;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0, c = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      a += sh[0][w];
+      b += sh[1][w];
+      c += sh[2][w];
+    }
+    sp[blockIdx.x] = make_double2(a, b);
+    gp[blockIdx.x] = c;
+  }
+}
+
+// y_n = c_n (sum_jc tpart + x_n . v_a - s), complex; Y partials per CTA
+__global__ void __launch_bounds__(256) k_otf_y_c(const double2* __restrict__ tpart, int jc_count, int64_t n,
+                                                 const double2* __restrict__ coeff, const double* v_re,
+                                                 const double* v_im, int64_t offa, int n_in,
+                                                 const uint64_t* __restrict__ xbits, const double2* __restrict__ sp,
+                                                 int n_sp, double2* y, double2* ypart) {
+  __shared__ double2 va[OTF_MAX_NIN];
+  __shared__ double2 sh[8];
+  for (int i = threadIdx.x; i < n_in; i += blockDim.x)
+    va[i] = make_double2(v_re[offa + i], v_im ? v_im[offa + i] : 0.0);
+  __syncthreads();
+  double sr = 0.0, si = 0.0;
+  for (int q = 0; q < n_sp; ++q) {
+    sr += sp[q].x;
+    si += sp[q].y;
+  }
+  double ar = 0.0, ai = 0.0;
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = blockIdx.x * per, hi = min(n, lo + per);
+  for (int64_t r = lo + threadIdx.x; r < hi; r += blockDim.x) {
+    double tr = 0.0, ti = 0.0;
+    for (int q = 0; q < jc_count; ++q) {
+      const double2 p = tpart[(int64_t)q * n + r];
+      tr += p.x;
+      ti += p.y;
+    }
+    for (int w = 0; w < OTF_XW; ++w) {
+      uint64_t bits = xbits[r * OTF_XW + w];
+      while (bits) {
+        const int b = __ffsll((long long)bits) - 1;
+        bits &= bits - 1;
+        tr += va[w * 64 + b].x;
+        ti += va[w * 64 + b].y;
+      }
+    }
+    tr -= sr;
+    ti -= si;
+    const double2 c = coeff[r];
+    const double2 yy = make_double2(c.x * tr - c.y * ti, c.x * ti + c.y * tr);
+    y[r] = yy;
+    ar += yy.x;
+    ai += yy.y;
+  }
+  ar = warp_sum<false>(ar);
+  ai = warp_sum<false>(ai);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = make_double2(ar, ai);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double2 t = make_double2(0.0, 0.0);
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      t.x += sh[w].x;
+      t.y += sh[w].y;
+    }
+    ypart[blockIdx.x] = t;
+  }
+}
+
+// part[blk][2j+p][kc] = sum_rows (conj(T_nj) y_n)_p x_n,kc  (kc = n_in: ones column)
+template <int NKT>
+__global__ void __launch_bounds__(256) k_otf_acc_c(const OtfCArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_c[];
+  double* gs = reinterpret_cast<double*>(smem_c);                        // [2][BM][64]
+  uint64_t* xs = reinterpret_cast<uint64_t*>(gs + 2 * OTF_BM * OTF_BJ);  // [2][BM][XW]
+  double2* ys = reinterpret_cast<double2*>(xs + 2 * OTF_BM * OTF_XW);    // [2][BM]
+  constexpr int KC = 8 * NKT;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int c0 = blockIdx.x * OTF_BJ;
+  const int64_t N = a.n_rows;
+  const int64_t lo = (N * blockIdx.y) / a.nb, hi = (N * (blockIdx.y + 1)) / a.nb;
+  const int nin = a.n_in, ncols = 2 * a.hidden;
+  const int ntiles = (int)((hi - lo + OTF_BM - 1) / OTF_BM);
+  auto load_y = [&](int64_t r0, int buf) {
+    for (int e = tid; e < OTF_BM; e += blockDim.x)
+      ys[buf * OTF_BM + e] = (r0 + e >= hi) ? make_double2(0.0, 0.0)
+                             : a.y ? a.y[r0 + e] : make_double2(a.yr[r0 + e], 0.0);
+  };
+  if (ntiles > 0) {
+    otf_load_ctile(a, lo, hi, c0, gs, xs, tid, blockDim.x);
+    load_y(lo, 0);
+  }
+  cp_async_commit();
+  double c[NKT][2];
+#pragma unroll
+  for (int nt = 0; nt < NKT; ++nt) c[nt][0] = c[nt][1] = 0.0;
+  const int jl = warp * 8 + (lane >> 2);  // real row (2j + p) of this lane within the chunk
+  const int pj = jl & 1, jb = jl & ~1;
+  const int sh_base = lane >> 2;
+  for (int it = 0; it < ntiles; ++it) {
+    const int buf = it & 1;
+    const int64_t r0 = lo + (int64_t)it * OTF_BM;
+    if (it + 1 < ntiles) {
+      otf_load_ctile(a, r0 + OTF_BM, hi, c0, gs + (buf ^ 1) * OTF_BM * OTF_BJ, xs + (buf ^ 1) * OTF_BM * OTF_XW, tid,
+                     blockDim.x);
+      load_y(r0 + OTF_BM, buf ^ 1);
+    }
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const double* G = gs + buf * OTF_BM * OTF_BJ;
+    const uint64_t* X = xs + buf * OTF_BM * OTF_XW;
+#pragma unroll 2
+    for (int kk = 0; kk < OTF_BM / 4; ++kk) {
+      const int rl = kk * 4 + (lane & 3);
+      const double2 t = *reinterpret_cast<const double2*>(G + rl * OTF_BJ + jb);
+      const double2 yv = ys[buf * OTF_BM + rl];
+      // conj(t) y = (t.x y.x + t.y y.y) + i (t.x y.y - t.y y.x)
+      const double av = pj ? fma(t.x, yv.y, -t.y * yv.x) : fma(t.x, yv.x, t.y * yv.y);
+      const uint64_t w0 = X[rl * OTF_XW] >> sh_base, w1 = X[rl * OTF_XW + 1] >> sh_base;
+#pragma unroll
+      for (int nt = 0; nt < NKT; ++nt) {
+        const int kcol = nt * 8 + sh_base;
+        const uint32_t bit = nt < 8 ? (uint32_t)(w0 >> (nt * 8)) & 1u : (uint32_t)(w1 >> ((nt - 8) * 8)) & 1u;
+        double bv = bit_to_double(bit);
+        if (nt * 8 + 7 >= nin) bv = (kcol < nin) ? bv : (kcol == nin ? 1.0 : 0.0);
+        dmma(c[nt][0], c[nt][1], av, bv);
+      }
+    }
+    __syncthreads();
+  }
+  const int col = c0 + jl;
+  if (col < ncols) {
+    double* pb = a.part + ((int64_t)blockIdx.y * ncols + col) * KC;
+#pragma unroll
+    for (int nt = 0; nt < NKT; ++nt) {
+      const int kc = nt * 8 + (lane & 3) * 2;
+      pb[kc] = c[nt][0];
+      pb[kc + 1] = c[nt][1];
+    }
+  }
+}
+
+// xpart[blk][i] = sum y_r x_ri (complex y)
+__global__ void __launch_bounds__(128) k_xsum_c(const uint64_t* __restrict__ xbits, const double2* __restrict__ y,
+                                                const double* __restrict__ yr, int64_t n, int n_in, double2* xpart) {
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = blockIdx.x * per, hi = min(n, lo + per);
+  const int i = threadIdx.x;
+  double ar = 0.0, ai = 0.0;
+  if (i < n_in) {
+    for (int64_t r = lo; r < hi; ++r) {
+      const uint64_t w = __ldg(xbits + r * OTF_XW + (i >> 6));
+      if ((w >> (i & 63)) & 1ull) {
+        if (y) {
+          const double2 yy = y[r];
+          ar += yy.x;
+          ai += yy.y;
+        } else {
+          ar += yr[r];
+        }
+      }
+    }
+    xpart[(int64_t)blockIdx.x * n_in + i] = make_double2(ar, ai);
+  }
+}
+
+// Assemble the complex RBM vector [a, b, W] from the partials.
+//   product mode (out_re/out_im planar): out = R - conj(obar) Y (+ u0 hf) ; out0 = g0
+//   stats mode (out_c interleaved): out = R, or conj(R) when conj_out (obar from y = w)
+__global__ void __launch_bounds__(256) k_rbm_otf_finish_c(const double* __restrict__ part, int nb, int hidden,
+                                                          int n_in, int kc, const double2* __restrict__ xpart, int nbx,
+                                                          const double2* __restrict__ ypart, int n_ypart, int64_t ld,
+                                                          const double2* __restrict__ obar, const double* hf_re,
+                                                          const double* hf_im, const double* u0,
+                                                          const double* gpart, int n_gpart, double* out_re,
+                                                          double* out_im, double* out0, double2* out_c, int conj_out) {
+  double Yr = 0.0, Yi = 0.0;
+  for (int q = 0; q < n_ypart; ++q) {
+    Yr += ypart[q].x;
+    Yi += ypart[q].y;
+  }
+  const int ncols = 2 * hidden;
+  const int64_t P = (int64_t)n_in + hidden + (int64_t)hidden * n_in;
+  const double uu = (hf_re && u0) ? *u0 : 0.0;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < ld; p += (int64_t)gridDim.x * blockDim.x) {
+    double ar = 0.0, ai = 0.0;
+    if (p < n_in) {
+      for (int b = 0; b < nbx; ++b) {
+        const double2 q = xpart[(int64_t)b * n_in + p];
+        ar += q.x;
+        ai += q.y;
+      }
+    } else if (p < n_in + hidden) {
+      const int64_t j = p - n_in;
+      for (int b = 0; b < nb; ++b) {
+        ar += part[((int64_t)b * ncols + 2 * j) * kc + n_in];
+        ai += part[((int64_t)b * ncols + 2 * j + 1) * kc + n_in];
+      }
+    } else if (p < P) {
+      const int64_t q = p - n_in - hidden, j = q / n_in, i = q % n_in;
+      for (int b = 0; b < nb; ++b) {
+        ar += part[((int64_t)b * ncols + 2 * j) * kc + i];
+        ai += part[((int64_t)b * ncols + 2 * j + 1) * kc + i];
+      }
+    }
+    if (p >= P) ar = ai = 0.0;
+    if (out_c) {
+      out_c[p] = make_double2(ar, conj_out ? -ai : ai);
+      continue;
+    }
+    if (p < P) {
+      if (obar) {  // - conj(obar) Y
+        const double2 o = obar[p];
+        ar -= o.x * Yr + o.y * Yi;
+        ai -= o.x * Yi - o.y * Yr;
+      }
+      if (hf_re && u0) {
+        ar = fma(uu, hf_re[p], ar);
+        if (hf_im) ai = fma(uu, hf_im[p], ai);
+      }
+    }
+    out_re[p] = ar;
+    if (out_im) out_im[p] = ai;
+  }
+  if (out0 && blockIdx.x == 0 && threadIdx.x == 0) {
+    double g = 0.0;
+    if (hf_re)
+      for (int q = 0; q < n_gpart; ++q) g += gpart[q];
+    *out0 = g;
+  }
+}
+
+}  // namespace irl

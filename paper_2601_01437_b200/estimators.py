@@ -164,7 +164,8 @@ class SampleBatch:
     def mvp_workspace(self) -> torch.Tensor:
         if self._ws is None:
             if self.otf is not None:
-                nbytes = int(_lib.lib().irl_otf_workspace_bytes(self.n_rows, self.otf["n_in"], self.otf["hidden"]))
+                fn = "irl_otf_workspace_bytes_c128" if self.is_complex else "irl_otf_workspace_bytes"
+                nbytes = int(getattr(_lib.lib(), fn)(self.n_rows, self.otf["n_in"], self.otf["hidden"]))
             else:
                 nbytes = int(_lib.lib().irl_mvp_workspace_bytes(self.n_rows, self.ld, int(self.is_complex)))
             self._ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
@@ -245,10 +246,15 @@ class SampleBatch:
     def _otf_colstats(self, key: float, c: torch.Tensor):
         o = self.otf
         n = self.n_rows
-        obar = torch.empty(self.ld, dtype=torch.float64, device=self.device)
-        g = torch.empty(self.ld, dtype=torch.float64, device=self.device)
+        dt = torch.complex128 if self.is_complex else torch.float64
+        obar = torch.empty(self.ld, dtype=dt, device=self.device)
+        g = torch.empty(self.ld, dtype=dt, device=self.device)
         ws = self.mvp_workspace()
-        if o["model"] == _lib.MODEL_RBM:
+        if self.is_complex:
+            _lib.call("irl_otf_colstats_rbm_c128", _lib.ptr(o["xbits"]), _lib.ptr(o["t"]), n, o["n_in"],
+                      o["hidden"], self.ld, _lib.ptr(self.weights), _lib.ptr(c), _lib.ptr(obar), _lib.ptr(g),
+                      _lib.ptr(ws), ws.numel(), self._stream())
+        elif o["model"] == _lib.MODEL_RBM:
             _lib.call("irl_otf_colstats_rbm_f64", _lib.ptr(o["xbits"]), _lib.ptr(o["t"]), n, o["n_in"], o["hidden"],
                       self.ld, _lib.ptr(self.weights), _lib.ptr(c), _lib.ptr(obar), _lib.ptr(g), _lib.ptr(ws),
                       ws.numel(), self._stream())
@@ -320,6 +326,14 @@ def _apply(batch: SampleBatch, coeff: torch.Tensor, v: torch.Tensor, out: torch.
     n = batch.n_rows
     if batch.otf is not None:
         o = batch.otf
+        if batch.kind == KIND_HERMITIAN:
+            (v_re, v_im), (o_re, o_im) = v, out
+            h_re, h_im = half_f if half_f is not None else (None, None)
+            _lib.call("irl_otf_mvp_rbm_c128", _lib.ptr(o["xbits"]), _lib.ptr(o["t"]), n, o["n_in"], o["hidden"],
+                      batch.ld, _lib.ptr(obar), _lib.ptr(coeff), _lib.ptr(v_re), _lib.ptr(v_im), _lib.ptr(o_re),
+                      _lib.ptr(o_im), _lib.ptr(h_re), _lib.ptr(h_im), _lib.ptr(u0), _lib.ptr(out0), _lib.ptr(ws),
+                      ws.numel(), stream)
+            return
         if o["model"] == _lib.MODEL_RBM:
             _lib.call("irl_otf_mvp_rbm_f64", _lib.ptr(o["xbits"]), _lib.ptr(o["t"]), n, o["n_in"], o["hidden"],
                       batch.ld, _lib.ptr(obar), _lib.ptr(coeff), _lib.ptr(v), _lib.ptr(out), _lib.ptr(half_f),

@@ -365,3 +365,36 @@ def test_otf_rbm_matches_stored(pkg, idx, rows):
     assert r1.n_matvec == r2.n_matvec
     assert abs(r1.lambda_min - r2.lambda_min) <= RITZ_TOL * abs(r1.lambda_min)
     assert rel(host(r2.direction), host(r1.direction)) < DIR_TOL
+
+
+@pytest.mark.parametrize("rows", [512, 3000])
+def test_otf_hermitian_rbm_matches_stored(pkg, rows):
+    """Complex-theta RBM on the fly (cfg4 shapes): statistics, products (plain and
+    bordered through the IRL) == stored-O batch and the oracle."""
+    from paper_2601_01437_b200 import ansatz as A, estimators as E, optimizer as OPT, synthetic as S
+
+    cfg = S.CONFIGS[4].with_rows(rows)
+    inp = S.make_inputs(cfg)
+    arch = A.RBMArchitecture(cfg.n_inputs, cfg.hidden, complex_params=True)
+    params = A.AnsatzParameters(arch, inp.theta)
+    stored = A.build_batch(params, inp.x, inp.e_loc)
+    otf = A.build_batch(params, inp.x, inp.e_loc, mode="otf")
+    assert otf.otf is not None and otf.kind == E.KIND_HERMITIAN
+    es, eo = E.estimate_energy(stored), E.estimate_energy(otf)
+    assert eo.mean == es.mean
+    P = arch.param_count
+    assert rel(host(E.energy_gradient(otf, eo)), host(E.energy_gradient(stored, es))) < 1e-12
+    assert rel(host(otf.obar()[:P]), host(stored.obar()[:P])) < 1e-13
+    o = nqs.rbm_rows(inp.theta, inp.x, cfg.n_inputs, cfg.hidden)
+    w = np.full(rows, 1.0 / rows)
+    rng = np.random.default_rng(rows)
+    v = rng.standard_normal(P) + 1j * rng.standard_normal(P)
+    assert rel(E.heff_matvec(otf, eo, v), oest.heff_hermitian(w, inp.e_loc, o, es.mean, v)) < PROD_TOL
+    o_c = o - w @ o
+    assert rel(E.qgt_matvec(otf, v), (w * (o_c @ v)) @ o_c.conj()) < PROD_TOL
+    conf = OPT.OptimizerConfig(m=cfg.m, max_restarts=3)
+    r1 = OPT.solve_step(stored, conf, seed=cfg.lanczos_seed)
+    r2 = OPT.solve_step(otf, conf, seed=cfg.lanczos_seed)
+    assert r1.n_matvec == r2.n_matvec
+    assert abs(r1.lambda_min - r2.lambda_min) <= RITZ_TOL * abs(r1.lambda_min)
+    assert rel(host(r2.direction), host(r1.direction)) < DIR_TOL

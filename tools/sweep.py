@@ -55,7 +55,7 @@ def main():
         arch = (A.RBMArchitecture(cfg.n_inputs, cfg.hidden, cfg.complex_params) if cfg.model == "rbm"
                 else A.MLPArchitecture(cfg.n_inputs, cfg.hidden))
         params = A.AnsatzParameters(arch, inp.theta)
-        if args.otf and not cfg.complex_params:
+        if args.otf:
             t0 = time.perf_counter()
             batch = A.build_batch_otf(params, inp.x, inp.e_loc)
             en = E.estimate_energy(batch)
@@ -64,14 +64,18 @@ def main():
             prep = (time.perf_counter() - t0) * 1e3
             P, ld = batch.param_count, batch.ld
             coeff = batch.coefficients(en.mean)
-            vin = torch.randn(ld, dtype=torch.float64, device=dev)
-            vin[P:] = 0
-            vout = torch.empty(ld, dtype=torch.float64, device=dev)
-            E._apply(batch, coeff, vin, vout)
+            shape = (2, ld) if cfg.complex_params else (ld,)
+            vin = torch.randn(shape, dtype=torch.float64, device=dev)
+            vin[..., P:] = 0
+            vout = torch.empty(shape, dtype=torch.float64, device=dev)
+            vi, vo = ((vin[0], vin[1]), (vout[0], vout[1])) if cfg.complex_params else (vin, vout)
+            E._apply(batch, coeff, vi, vo)
             torch.cuda.synchronize()
-            ms = timed(lambda: E._apply(batch, coeff, vin, vout), args.reps)
+            ms = timed(lambda: E._apply(batch, coeff, vi, vo), args.reps)
             med = statistics.median(ms)
-            flops = 2.0 * batch.n_rows * cfg.hidden * (cfg.n_inputs + 104)
+            # useful DMMA flops: dot (n_in k-steps) + acc (n_in + 1 columns) per real hidden column
+            cols = cfg.hidden * (2 if cfg.complex_params else 1)
+            flops = 2.0 * batch.n_rows * cols * (2 * cfg.n_inputs + 1)
             out = {"config": cfg.name + "-otf", "prepare_ms": prep, "otf": {"ms": med, "mvp_s": 1e3 / med,
                    "tflops": flops / (med / 1e3) / 1e12}}
             if args.irl:
