@@ -500,11 +500,32 @@ int colstats_impl(bool cplx, const double* O, int64_t n, int64_t ld, const doubl
 }
 
 // --------------------------------------------------------------- otf ----
+// partial-reduction kernels: 32 outputs per CTA (blockDim (32, 8))
+unsigned fin_grid(int64_t ld) { return (unsigned)std::min<int64_t>(cdiv(ld, 32), 1 << 20); }
+
 struct OtfPlan {
-  int jc, nb, ny;
-  int nkt, kc;  // n-tiles of the acc GEMM (k columns = n_in + ones column, padded to 8)
-  size_t smem_dot;
+  int jc, nb, ny;  // nb: the largest row-block count of any acc variant (workspace bound)
+  int nkt, kc;     // n-tiles of the acc GEMM (k columns = n_in + ones column, padded to 8)
+  int nb_v[2][2];  // row blocks per acc variant [ny - 1][has_t]
 };
+
+// Row blocks for a (jc x nb) grid of equal CTAs: the wave count k in 1..3
+// whose floor(k * slots / jc) * jc fills the resident slots best.
+int best_row_blocks(int slots, int jc, int64_t n) {
+  const int64_t tiles = std::max<int64_t>(1, cdiv(n, OTF_BM));
+  int best = 1;
+  double best_eff = -1.0;
+  for (int k = 1; k <= 3; ++k) {
+    const int nb = (int)std::min<int64_t>(tiles, std::max(1, k * slots / jc));
+    const int64_t ctas = (int64_t)nb * jc;
+    const double eff = (double)ctas / (double)(cdiv(ctas, slots) * slots);
+    if (eff > best_eff + 0.02) {
+      best_eff = eff;
+      best = nb;
+    }
+  }
+  return best;
+}
 
 using AccFn = void (*)(OtfArgs);
 
@@ -519,28 +540,65 @@ AccFn pick_acc(int nkt, int nyv, bool has_t) {
 }
 
 size_t acc_smem(int nyv, bool has_t) {
-  return ((size_t)2 * OTF_BM * OTF_BJ * (has_t ? 2 : 1) + 2 * OTF_BM * OTF_XW + (size_t)nyv * 2 * OTF_BM) * 8;
+  const size_t st = OTF_ACC_STAGES;
+  return (st * OTF_BM * OTF_BJ * (has_t ? 2 : 1) + st * OTF_BM * OTF_XW + (size_t)nyv * st * OTF_BM) * 8;
 }
 
-int make_otf_plan(int64_t n, int n_in, int hidden, OtfPlan& p) {
+int make_otf_plan_uncached(int64_t n, int n_in, int hidden, OtfPlan& p) {
   DevInfo d;
   IRL_TRY(dev_info(d));
   if (n_in < 1 || n_in > OTF_MAX_NIN) return fail(IRL_ERR_ARG, "on-the-fly mode supports n_in <= %d", OTF_MAX_NIN);
   p.jc = (int)cdiv(hidden, OTF_BJ);
-  p.nb = std::max(1, (int)((2LL * d.sms + p.jc / 2) / p.jc));
-  p.nb = (int)std::min<int64_t>(p.nb, std::max<int64_t>(1, cdiv(n, OTF_BM)));
   p.ny = d.sms;
-  p.smem_dot = (size_t)(OTF_BJ * OTF_MAX_NIN + 2 * OTF_BJ + 4 * OTF_BM * OTF_BJ) * 8 + 2 * OTF_BM * OTF_XW * 8 +
-               4 * OTF_BM * 8;
   p.nkt = (n_in + 1 + 7) / 8 <= 3 ? 3 : (n_in + 1 + 7) / 8 <= 6 ? 6 : 13;
   p.kc = 8 * p.nkt;
-  IRL_TRY(ensure_fn_attrs((const void*)k_otf_dot, d.smem_optin));
+  p.nb = 1;
+  IRL_TRY(ensure_fn_attrs((const void*)k_otf_dot<true>, d.smem_optin));
+  IRL_TRY(ensure_fn_attrs((const void*)k_otf_dot<false>, d.smem_optin));
   for (int nyv = 1; nyv <= 2; ++nyv)
-    for (bool ht : {true, false}) {
-      AccFn f = pick_acc(p.nkt, nyv, ht);
-      if (f) IRL_TRY(ensure_fn_attrs((const void*)f, d.smem_optin));
+    for (int ht = 0; ht < 2; ++ht) {
+      p.nb_v[nyv - 1][ht] = 0;
+      AccFn f = pick_acc(p.nkt, nyv, ht != 0);
+      if (!f) continue;
+      IRL_TRY(ensure_fn_attrs((const void*)f, d.smem_optin));
+      int occ = 0;
+      IRL_TRY(cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)f, 256, acc_smem(nyv, ht != 0)),
+                         "occ"));
+      p.nb_v[nyv - 1][ht] = best_row_blocks(d.sms * std::max(occ, 1), p.jc, n);
+      p.nb = std::max(p.nb, p.nb_v[nyv - 1][ht]);
     }
   return IRL_OK;
+}
+
+int make_otf_plan(int64_t n, int n_in, int hidden, OtfPlan& p) {
+  struct Entry {
+    int rc;
+    OtfPlan plan;
+    std::string err;
+  };
+  static std::mutex mu;
+  static std::unordered_map<std::string, Entry> cache;
+  int dev = 0;
+  IRL_TRY(cuda_check(cudaGetDevice(&dev), "cudaGetDevice"));
+  char key[96];
+  snprintf(key, sizeof(key), "%lld/%d/%d/%d", (long long)n, n_in, hidden, dev);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      p = it->second.plan;
+      if (it->second.rc != IRL_OK) g_err = it->second.err;
+      return it->second.rc;
+    }
+  }
+  Entry e{};
+  e.rc = make_otf_plan_uncached(n, n_in, hidden, e.plan);
+  if (e.rc == IRL_ERR_CUDA) return e.rc;  // transient: do not cache
+  if (e.rc != IRL_OK) e.err = g_err;
+  p = e.plan;
+  std::lock_guard<std::mutex> lk(mu);
+  cache.emplace(key, e);
+  return e.rc;
 }
 
 struct OtfWs {
@@ -579,11 +637,57 @@ int otf_check(const uint64_t* xbits, const double* t, const double* g, int64_t n
   return IRL_OK;
 }
 
+size_t otf_dot_smem(int n_in, bool has_t, bool cplx) {
+  const int vs = otf_vstride(n_in);
+  const size_t tiles = (size_t)2 * OTF_BM * OTF_BJ * (has_t ? 2 : 1);
+  const size_t red = (size_t)4 * OTF_BM * (cplx ? 2 : 1);
+  return ((size_t)OTF_BJ * vs + OTF_BJ * (has_t ? 2 : 1) + tiles + red) * 8 + (size_t)2 * OTF_BM * OTF_XW * 8;
+}
+
+// persistent grid of the dot kernels: every resident CTA slot, occupancy cached per (kernel, n_in)
+int otf_dot_grid(const void* fn, size_t smem, int key, int& grid) {
+  static std::mutex mu;
+  static std::unordered_map<int, int> cache;
+  DevInfo d;
+  IRL_TRY(dev_info(d));
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int k = (key << 8) ^ dev;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(k);
+    if (it != cache.end()) {
+      grid = it->second;
+      return IRL_OK;
+    }
+  }
+  IRL_TRY(ensure_fn_attrs(fn, d.smem_optin));
+  int occ = 0;
+  IRL_TRY(cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, smem), "occ"));
+  grid = d.sms * std::max(occ, 1);
+  std::lock_guard<std::mutex> lk(mu);
+  cache[k] = grid;
+  return IRL_OK;
+}
+
+int otf_dot_launch(OtfArgs& a, bool has_t, cudaStream_t st) {
+  const void* fn = has_t ? (const void*)k_otf_dot<true> : (const void*)k_otf_dot<false>;
+  const size_t smem = otf_dot_smem(a.n_in, has_t, false);
+  int grid = 0;
+  IRL_TRY(otf_dot_grid(fn, smem, (a.n_in << 2) | (has_t ? 1 : 0), grid));
+  if (has_t)
+    k_otf_dot<true><<<grid, 256, smem, st>>>(a);
+  else
+    k_otf_dot<false><<<grid, 256, smem, st>>>(a);
+  return cuda_check(cudaGetLastError(), "otf dot launch");
+}
+
+// launches the acc GEMM variant; a.nb = its row-block count (the partial stride)
 int otf_acc_launch(const OtfPlan& pl, OtfArgs& a, cudaStream_t st, int nyv, bool has_t) {
   AccFn f = pick_acc(pl.nkt, nyv, has_t);
   if (!f) return fail(IRL_ERR_DEVICE, "no acc GEMM instance for nkt=%d ny=%d", pl.nkt, nyv);
-  dim3 grid((unsigned)pl.jc, (unsigned)pl.nb);
-  a.nb = pl.nb;
+  a.nb = pl.nb_v[nyv - 1][has_t ? 1 : 0];
+  dim3 grid((unsigned)pl.jc, (unsigned)a.nb);
   f<<<grid, 256, acc_smem(nyv, has_t), st>>>(a);
   return cuda_check(cudaGetLastError(), "otf acc launch");
 }
@@ -604,17 +708,17 @@ int otf_stats(const OtfPlan& pl, OtfArgs a, const OtfWs& wl, int model, int64_t 
     a.y2 = nyv == 2 ? ys[q0 + 1] : nullptr;
     IRL_TRY(otf_acc_launch(pl, a, st, nyv, has_t));
     for (int q = q0; q < q0 + nyv; ++q) {
-      const double* part = wl.part + (size_t)(q - q0) * pl.nb * hidden * pl.kc;
-      const double* partu = wl.partu + (size_t)(q - q0) * pl.nb * hidden;
+      const double* part = wl.part + (size_t)(q - q0) * a.nb * hidden * pl.kc;
+      const double* partu = wl.partu + (size_t)(q - q0) * a.nb * hidden;
       if (model == MODEL_MLP) {
         k_vsum<<<pl.ny, 256, 0, st>>>(ys[q], n, wl.ypart);
-        k_otf_finish<<<(unsigned)cdiv(ld, 256), 256, 0, st>>>(part, partu, pl.nb, hidden, n_in, pl.kc, ld, wl.ypart,
+        k_otf_finish<<<fin_grid(ld), dim3(32, 8), 0, st>>>(part, partu, a.nb, hidden, n_in, pl.kc, ld, wl.ypart,
                                                              pl.ny, nullptr, nullptr, nullptr, nullptr, 0, outs[q],
                                                              nullptr);
       } else {
         double* xp = xpart ? xpart : wl.xpart;
         k_xsum<<<nbx, 128, 0, st>>>(a.xbits, ys[q], n, n_in, xp, wl.ypart2);
-        k_rbm_stats_finish<<<(unsigned)cdiv(ld, 256), 256, 0, st>>>(part, pl.nb, hidden, n_in, pl.kc, xp, nbx, ld,
+        k_rbm_stats_finish<<<fin_grid(ld), dim3(32, 8), 0, st>>>(part, a.nb, hidden, n_in, pl.kc, xp, nbx, ld,
                                                                     outs[q]);
       }
       IRL_TRY(cuda_check(cudaGetLastError(), "stats finish launch"));
@@ -643,7 +747,7 @@ AccCFn pick_acc_c(int nkt) {
   }
 }
 
-int make_otfc_plan(int64_t n, int n_in, int hidden, OtfCPlan& p) {
+int make_otfc_plan_uncached(int64_t n, int n_in, int hidden, OtfCPlan& p) {
   DevInfo d;
   IRL_TRY(dev_info(d));
   if (n_in < 1 || n_in > OTF_MAX_NIN) return fail(IRL_ERR_ARG, "on-the-fly mode supports n_in <= %d", OTF_MAX_NIN);
@@ -651,9 +755,8 @@ int make_otfc_plan(int64_t n, int n_in, int hidden, OtfCPlan& p) {
   const int k8 = (n_in + 1 + 7) / 8;
   p.nkt = k8 <= 3 ? 3 : k8 <= 6 ? 6 : k8 <= 8 ? 8 : 13;
   p.kc = 8 * p.nkt;
-  p.smem_dot = (size_t)(OTF_BJ * OTF_MAX_NIN + OTF_BJ + 2 * OTF_BM * OTF_BJ) * 8 + 2 * OTF_BM * OTF_XW * 8 +
-               4 * OTF_BM * 16;
-  p.smem_acc = (size_t)(2 * OTF_BM * OTF_BJ) * 8 + 2 * OTF_BM * OTF_XW * 8 + 2 * OTF_BM * 16;
+  p.smem_dot = otf_dot_smem(n_in, false, true);
+  p.smem_acc = (size_t)OTF_ACC_STAGES * (OTF_BM * OTF_BJ * 8 + OTF_BM * OTF_XW * 8 + OTF_BM * 16);
   AccCFn acc = pick_acc_c(p.nkt);
   IRL_TRY(ensure_fn_attrs((const void*)k_otf_dot_c, d.smem_optin));
   IRL_TRY(ensure_fn_attrs((const void*)acc, d.smem_optin));
@@ -661,13 +764,42 @@ int make_otfc_plan(int64_t n, int n_in, int hidden, OtfCPlan& p) {
   IRL_TRY(cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_d, (const void*)k_otf_dot_c, 256, p.smem_dot),
                      "occ"));
   IRL_TRY(cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_a, (const void*)acc, 256, p.smem_acc), "occ"));
-  const int64_t tiles = std::max<int64_t>(1, cdiv(n, OTF_BM));
-  // one wave of CTAs (row blocks x column chunks), never more row blocks than row tiles
-  p.nb_dot = (int)std::min<int64_t>(tiles, std::max(1, d.sms * std::max(occ_d, 1) / p.jc));
-  p.nb_acc = (int)std::min<int64_t>(tiles, std::max(1, d.sms * std::max(occ_a, 1) / p.jc));
+  p.nb_dot = d.sms * std::max(occ_d, 1);  // persistent grid
+  p.nb_acc = best_row_blocks(d.sms * std::max(occ_a, 1), p.jc, n);
   p.ny = d.sms;
   p.nbx = std::min<int>(4 * d.sms, (int)std::max<int64_t>(1, n / 64));
   return IRL_OK;
+}
+
+int make_otfc_plan(int64_t n, int n_in, int hidden, OtfCPlan& p) {
+  struct Entry {
+    int rc;
+    OtfCPlan plan;
+    std::string err;
+  };
+  static std::mutex mu;
+  static std::unordered_map<std::string, Entry> cache;
+  int dev = 0;
+  IRL_TRY(cuda_check(cudaGetDevice(&dev), "cudaGetDevice"));
+  char key[96];
+  snprintf(key, sizeof(key), "%lld/%d/%d/%d", (long long)n, n_in, hidden, dev);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      p = it->second.plan;
+      if (it->second.rc != IRL_OK) g_err = it->second.err;
+      return it->second.rc;
+    }
+  }
+  Entry e{};
+  e.rc = make_otfc_plan_uncached(n, n_in, hidden, e.plan);
+  if (e.rc == IRL_ERR_CUDA) return e.rc;
+  if (e.rc != IRL_OK) e.err = g_err;
+  p = e.plan;
+  std::lock_guard<std::mutex> lk(mu);
+  cache.emplace(key, e);
+  return e.rc;
 }
 
 struct OtfCWs {
@@ -715,7 +847,7 @@ int otfc_colsum(const OtfCPlan& pl, OtfCArgs a, const OtfCWs& wl, int64_t ld, co
   pick_acc_c(pl.nkt)<<<dim3((unsigned)pl.jc, (unsigned)pl.nb_acc), 256, pl.smem_acc, st>>>(a);
   IRL_TRY(cuda_check(cudaGetLastError(), "otf acc (complex) launch"));
   k_xsum_c<<<pl.nbx, 128, 0, st>>>(a.xbits, y, yr, a.n_rows, a.n_in, wl.xpart);
-  k_rbm_otf_finish_c<<<(unsigned)cdiv(ld, 256), 256, 0, st>>>(wl.part, pl.nb_acc, a.hidden, a.n_in, pl.kc, wl.xpart,
+  k_rbm_otf_finish_c<<<fin_grid(ld), dim3(32, 8), 0, st>>>(wl.part, pl.nb_acc, a.hidden, a.n_in, pl.kc, wl.xpart,
                                                              pl.nbx, nullptr, 0, ld, nullptr, nullptr, nullptr,
                                                              nullptr, nullptr, 0, nullptr, nullptr, nullptr, out_c,
                                                              conj_out);
@@ -1143,12 +1275,11 @@ int irl_otf_mvp_mlp_f64(const uint64_t* xbits, const double* t, const double* g,
   a.y = wl.y;
   a.part = wl.part;
   a.partu = wl.partu;
-  k_otf_dot<<<dim3((unsigned)pl.jc, (unsigned)pl.nb), 256, pl.smem_dot, st>>>(a);
-  IRL_TRY(cuda_check(cudaGetLastError(), "otf dot launch"));
+  IRL_TRY(otf_dot_launch(a, true, st));
   k_otf_y<<<pl.ny, 256, 0, st>>>(wl.tpart, pl.jc, n, coeff, v, P - 1, wl.dpart, obar ? pl.ny : 0, wl.y, wl.ypart,
                                  nullptr, -1, n_in);
   IRL_TRY(otf_acc_launch(pl, a, st, 1, true));
-  k_otf_finish<<<(unsigned)cdiv(ld, 256), 256, 0, st>>>(wl.part, wl.partu, pl.nb, hidden, n_in, pl.kc, ld, wl.ypart,
+  k_otf_finish<<<fin_grid(ld), dim3(32, 8), 0, st>>>(wl.part, wl.partu, a.nb, hidden, n_in, pl.kc, ld, wl.ypart,
                                                        pl.ny, obar, half_f, u0, wl.gpart, pl.ny, out, out0);
   return cuda_check(cudaGetLastError(), "otf finish launch");
 }
@@ -1218,14 +1349,13 @@ int irl_otf_mvp_rbm_f64(const uint64_t* xbits, const double* t, int64_t n, int n
   a.y = wl.y;
   a.part = wl.part;
   a.partu = wl.partu;
-  k_otf_dot<<<dim3((unsigned)pl.jc, (unsigned)pl.nb), 256, pl.smem_dot, st>>>(a);
-  IRL_TRY(cuda_check(cudaGetLastError(), "otf dot launch"));
+  IRL_TRY(otf_dot_launch(a, false, st));
   k_otf_y<<<pl.ny, 256, 0, st>>>(wl.tpart, pl.jc, n, coeff, v, -1, wl.dpart, obar ? pl.ny : 0, wl.y, wl.ypart, xbits,
                                  0, n_vis);
   IRL_TRY(otf_acc_launch(pl, a, st, 1, false));
   const int nbx = std::min<int>(4 * d.sms, (int)std::max<int64_t>(1, n / 64));
   k_xsum<<<nbx, 128, 0, st>>>(xbits, wl.y, n, n_vis, wl.xpart, wl.ypart2);
-  k_rbm_otf_finish<<<(unsigned)cdiv(ld, 256), 256, 0, st>>>(wl.part, pl.nb, hidden, n_vis, pl.kc, wl.xpart, nbx,
+  k_rbm_otf_finish<<<fin_grid(ld), dim3(32, 8), 0, st>>>(wl.part, a.nb, hidden, n_vis, pl.kc, wl.xpart, nbx,
                                                            wl.ypart, pl.ny, ld, obar, half_f, u0, wl.gpart, pl.ny,
                                                            out, out0);
   return cuda_check(cudaGetLastError(), "otf rbm finish launch");
@@ -1297,7 +1427,7 @@ int irl_otf_mvp_rbm_c128(const uint64_t* xbits, const double* t, int64_t n, int 
   a.v_re = v_re;
   a.v_im = v_im;
   a.tpart = wl.tpart;
-  k_otf_dot_c<<<dim3((unsigned)pl.jc, (unsigned)pl.nb_dot), 256, pl.smem_dot, st>>>(a);
+  k_otf_dot_c<<<pl.nb_dot, 256, pl.smem_dot, st>>>(a);
   IRL_TRY(cuda_check(cudaGetLastError(), "otf dot (complex) launch"));
   k_otf_y_c<<<pl.ny, 256, 0, st>>>(wl.tpart, pl.jc, n, reinterpret_cast<const double2*>(coeff), v_re, v_im, 0, n_vis,
                                    xbits, wl.dpart, obar ? pl.ny : 0, wl.y, wl.ypart);
@@ -1308,7 +1438,7 @@ int irl_otf_mvp_rbm_c128(const uint64_t* xbits, const double* t, int64_t n, int 
   pick_acc_c(pl.nkt)<<<dim3((unsigned)pl.jc, (unsigned)pl.nb_acc), 256, pl.smem_acc, st>>>(a);
   IRL_TRY(cuda_check(cudaGetLastError(), "otf acc (complex) launch"));
   k_xsum_c<<<pl.nbx, 128, 0, st>>>(xbits, wl.y, nullptr, n, n_vis, wl.xpart);
-  k_rbm_otf_finish_c<<<(unsigned)cdiv(ld, 256), 256, 0, st>>>(wl.part, pl.nb_acc, hidden, n_vis, pl.kc, wl.xpart,
+  k_rbm_otf_finish_c<<<fin_grid(ld), dim3(32, 8), 0, st>>>(wl.part, pl.nb_acc, hidden, n_vis, pl.kc, wl.xpart,
                                                              pl.nbx, wl.ypart, pl.ny, ld, ob, half_f_re, half_f_im,
                                                              u0, wl.gpart, pl.ny, out_re, out_im, out0, nullptr, 0);
   return cuda_check(cudaGetLastError(), "otf finish (complex) launch");

@@ -25,6 +25,7 @@ constexpr int OTF_BM = 64;   // rows per tile
 constexpr int OTF_KC = 104;  // k columns of the acc GEMM: n_in (<=100) + ones column, padded to 13 n-tiles
 constexpr int OTF_MAX_NIN = 100;
 constexpr int OTF_XW = 2;    // 64-bit words per packed input row (n_in <= 128)
+constexpr int OTF_ACC_STAGES = 3;  // cp.async stages of the acc GEMMs (one barrier per tile)
 
 struct OtfArgs {
   const uint64_t* xbits;  // [N][OTF_XW]
@@ -96,47 +97,83 @@ __device__ __forceinline__ void otf_load_tile(const OtfArgs& a, int64_t r0, int6
   }
 }
 
-// grid (JC, nb), 256 threads: t partials for hidden chunk jc over row block
+// Row stride (doubles) of the v_W chunk in shared memory: >= n_in, a multiple
+// of 4 and == 4 (mod 16), so the B-fragment loads (8 rows x 4 k per half warp
+// pair) hit 16 distinct 8-byte bank pairs.
+__host__ __device__ __forceinline__ int otf_vstride(int nin) {
+  int vs = (nin + 3) & ~3;
+  while ((vs & 15) != 4) vs += 4;
+  return vs;
+}
+
+// Persistent tile range of CTA c: linear tiles t = jc * ntiles + row_tile,
+// split evenly over the grid (a range spans at most two hidden chunks while
+// JC < gridDim.x).
+__device__ __forceinline__ void otf_cta_range(int64_t total, int64_t& t0, int64_t& t1) {
+  t0 = (total * blockIdx.x) / gridDim.x;
+  t1 = (total * (blockIdx.x + 1)) / gridDim.x;
+}
+
+// grid (persistent, 1-D), 256 threads: t partials (tpart[jc][row]) for every
+// (hidden chunk, 64-row tile) of this CTA's range.  8 warps = 2 (32 rows) x 4
+// (16 hidden units).  HAS_T: MLP (G tile for X V_W^T, T tile for v_u);
+// RBM: G == T, G-only tiles, no u block.
+template <bool HAS_T>
 __global__ void __launch_bounds__(256) k_otf_dot(const OtfArgs a) {
   extern __shared__ __align__(16) unsigned char smem_o[];
-  double* vw = reinterpret_cast<double*>(smem_o);            // [BJ][OTF_MAX_NIN]
-  double* vb = vw + OTF_BJ * OTF_MAX_NIN;                    // [BJ]
-  double* vu = vb + OTF_BJ;                                  // [BJ]
-  double* gs = vu + OTF_BJ;                                  // [2][BM][BJ]
-  double* ts = gs + 2 * OTF_BM * OTF_BJ;                     // [2][BM][BJ]
-  uint64_t* xs = reinterpret_cast<uint64_t*>(ts + 2 * OTF_BM * OTF_BJ);  // [2][BM][XW]
-  double* red = reinterpret_cast<double*>(xs + 2 * OTF_BM * OTF_XW);     // [4][BM]
+  const int nin = a.n_in, vs = otf_vstride(nin);
+  double* vw = reinterpret_cast<double*>(smem_o);            // [BJ][vs]
+  double* vb = vw + OTF_BJ * vs;                             // [BJ]
+  double* vu = vb + OTF_BJ;                                  // [BJ] (HAS_T)
+  double* gs = vu + (HAS_T ? OTF_BJ : 0);                    // [2][BM][BJ]
+  double* ts = gs + 2 * OTF_BM * OTF_BJ;                     // [2][BM][BJ] (HAS_T)
+  uint64_t* xs = reinterpret_cast<uint64_t*>(ts + (HAS_T ? 2 * OTF_BM * OTF_BJ : 0));  // [2][BM][XW]
+  double* red = reinterpret_cast<double*>(xs + 2 * OTF_BM * OTF_XW);                   // [4][BM]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wr = warp >> 2, wj = warp & 3;  // rows [wr*32, +32), j [wj*16, +16)
-  const int jc = blockIdx.x, j0 = jc * OTF_BJ;
   const int64_t N = a.n_rows;
-  const int64_t lo = (N * blockIdx.y) / a.nb, hi = (N * (blockIdx.y + 1)) / a.nb;
-  const int h = a.hidden, nin = a.n_in;
-  const int64_t offW = a.offW, offb = a.offb, offu = a.offu;
+  const int64_t ntiles = (N + OTF_BM - 1) / OTF_BM;
+  const int jcount = (a.hidden + OTF_BJ - 1) / OTF_BJ;
+  int64_t t0, t1;
+  otf_cta_range(ntiles * jcount, t0, t1);
+  if (t0 >= t1) return;
+  const int h = a.hidden;
 
-  // v_W chunk, v_b, v_u (zero beyond h / n_in; no u block for the RBM)
-  for (int e = tid; e < OTF_BJ * OTF_MAX_NIN; e += blockDim.x) {
-    const int jj = e / OTF_MAX_NIN, k = e % OTF_MAX_NIN;
-    vw[e] = (j0 + jj < h && k < nin) ? a.v[offW + (int64_t)(j0 + jj) * nin + k] : 0.0;
-  }
-  for (int e = tid; e < OTF_BJ; e += blockDim.x) {
-    vb[e] = (j0 + e < h) ? a.v[offb + j0 + e] : 0.0;
-    vu[e] = (j0 + e < h && offu >= 0) ? a.v[offu + j0 + e] : 0.0;
-  }
-  const int ntiles = (int)((hi - lo + OTF_BM - 1) / OTF_BM);
-  if (ntiles > 0) otf_load_tile(a, lo, hi, j0, gs, ts, xs, tid, blockDim.x);
+  auto load_v = [&](int jc) {  // v_W chunk, v_b, v_u (zero beyond h / n_in)
+    const int j0 = jc * OTF_BJ;
+    for (int e = tid; e < OTF_BJ * vs; e += blockDim.x) {
+      const int jj = e / vs, k = e % vs;
+      vw[e] = (j0 + jj < h && k < nin) ? a.v[a.offW + (int64_t)(j0 + jj) * nin + k] : 0.0;
+    }
+    for (int e = tid; e < OTF_BJ; e += blockDim.x) {
+      vb[e] = (j0 + e < h) ? a.v[a.offb + j0 + e] : 0.0;
+      if (HAS_T) vu[e] = (j0 + e < h) ? a.v[a.offu + j0 + e] : 0.0;
+    }
+  };
+  auto load_tile = [&](int64_t t, int buf) {
+    const int jc = (int)(t / ntiles);
+    const int64_t r0 = (t % ntiles) * OTF_BM;
+    otf_load_tile(a, r0, min(N, r0 + OTF_BM), jc * OTF_BJ, gs + buf * OTF_BM * OTF_BJ,
+                  HAS_T ? ts + buf * OTF_BM * OTF_BJ : nullptr, xs + buf * OTF_BM * OTF_XW, tid, blockDim.x);
+  };
+  int cur_jc = (int)(t0 / ntiles);
+  load_v(cur_jc);
+  load_tile(t0, 0);
   cp_async_commit();
   const int ksteps = (nin + 3) / 4;
 
-  for (int it = 0; it < ntiles; ++it) {
-    const int buf = it & 1;
-    const int64_t r0 = lo + (int64_t)it * OTF_BM;
-    if (it + 1 < ntiles)
-      otf_load_tile(a, r0 + OTF_BM, hi, j0, gs + (buf ^ 1) * OTF_BM * OTF_BJ, ts + (buf ^ 1) * OTF_BM * OTF_BJ,
-                    xs + (buf ^ 1) * OTF_BM * OTF_XW, tid, blockDim.x);
+  for (int64_t t = t0; t < t1; ++t) {
+    const int buf = (int)((t - t0) & 1);
+    const int jc = (int)(t / ntiles);
+    const int64_t r0 = (t % ntiles) * OTF_BM;
+    if (t + 1 < t1) load_tile(t + 1, buf ^ 1);
     cp_async_commit();
     cp_async_wait<1>();
+    if (jc != cur_jc) {  // crossed into the next hidden chunk (the loop-end barrier fenced the old v)
+      load_v(jc);
+      cur_jc = jc;
+    }
     __syncthreads();
     const double* G = gs + buf * OTF_BM * OTF_BJ;
     const double* Tt = ts + buf * OTF_BM * OTF_BJ;
@@ -158,11 +195,11 @@ __global__ void __launch_bounds__(256) k_otf_dot(const OtfArgs a) {
     for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
       for (int q = 0; q < OTF_XW; ++q) xr[mt][q] = X[(wr * 32 + mt * 8 + (lane >> 2)) * OTF_XW + q];
-    const double* vrow0 = vw + (wj * 16 + (lane >> 2)) * OTF_MAX_NIN + (lane & 3);
+    const double* vrow0 = vw + (wj * 16 + (lane >> 2)) * vs + (lane & 3);
     for (int kk = 0; kk < ksteps; ++kk) {
       const int k = kk * 4 + (lane & 3);
       const double b0 = vrow0[kk * 4];
-      const double b1 = vrow0[kk * 4 + 8 * OTF_MAX_NIN];
+      const double b1 = vrow0[kk * 4 + 8 * vs];
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt) {
         const uint64_t word = (k < 64) ? xr[mt][0] : xr[mt][1];
@@ -171,7 +208,7 @@ __global__ void __launch_bounds__(256) k_otf_dot(const OtfArgs a) {
         dmma(c[mt][1][0], c[mt][1][1], av, b1);
       }
     }
-    // epilogue: row sums of G (.) C + T (.) v_u
+    // epilogue: row sums of G (.) C (+ T (.) v_u)
     double rs[4];
 #pragma unroll
     for (int mt = 0; mt < 4; ++mt) {
@@ -181,11 +218,13 @@ __global__ void __launch_bounds__(256) k_otf_dot(const OtfArgs a) {
       for (int nt = 0; nt < 2; ++nt) {
         const int jl = wj * 16 + nt * 8 + (lane & 3) * 2;
         const double2 g2 = *reinterpret_cast<const double2*>(G + rl * OTF_BJ + jl);
-        const double2 t2 = *reinterpret_cast<const double2*>(Tt + rl * OTF_BJ + jl);
         s = fma(g2.x, c[mt][nt][0], s);
         s = fma(g2.y, c[mt][nt][1], s);
-        s = fma(t2.x, vu[jl], s);
-        s = fma(t2.y, vu[jl + 1], s);
+        if (HAS_T) {
+          const double2 t2 = *reinterpret_cast<const double2*>(Tt + rl * OTF_BJ + jl);
+          s = fma(t2.x, vu[jl], s);
+          s = fma(t2.y, vu[jl + 1], s);
+        }
       }
       s += __shfl_xor_sync(0xffffffffu, s, 1);
       s += __shfl_xor_sync(0xffffffffu, s, 2);
@@ -198,9 +237,9 @@ __global__ void __launch_bounds__(256) k_otf_dot(const OtfArgs a) {
     __syncthreads();
     if (tid < OTF_BM) {
       const int64_t row = r0 + tid;
-      if (row < hi) {
-        const double t = ((red[tid] + red[OTF_BM + tid]) + red[2 * OTF_BM + tid]) + red[3 * OTF_BM + tid];
-        a.tpart[(int64_t)jc * N + row] = t;
+      if (row < N) {
+        const double tv = ((red[tid] + red[OTF_BM + tid]) + red[2 * OTF_BM + tid]) + red[3 * OTF_BM + tid];
+        a.tpart[(int64_t)jc * N + row] = tv;
       }
     }
     __syncthreads();
@@ -255,21 +294,25 @@ __global__ void __launch_bounds__(256) k_otf_y(const double* __restrict__ tpart,
   }
 }
 
-// grid (JC, nb), 256 threads (warp w owns hidden units j0 + 8w .. +7):
-// part[y][blk][j][kc] = sum_rows y g_j x_kc (kc = n_in is the ones column),
-// partu[y][blk][j] = sum y t_j (HAS_T).  NKT n-tiles of 8 k columns cover
-// n_in + 1 (the MMA count follows n_in); NY weight vectors share one read of
-// the G/T tiles and the B fragments.
+// grid (JC, nb), 256 threads.  part[y][blk][j][kc] = sum_rows y g_j x_kc
+// (kc = n_in is the ones column), partu[y][blk][j] = sum y t_j (HAS_T).
+// NKT n-tiles of 8 k columns cover n_in + 1; NY weight vectors share one read
+// of the G/T tiles and the B fragments.  Warp w: hidden units j0 + 16 (w & 3)
+// + {0..7, 8..15} (two A fragments per B fragment: every 0/1 input fragment
+// built from the bits feeds two DMMAs) over the row quads kk = w >> 2, +2, ...;
+// the two row halves are summed through shared memory at the end.
 template <int NKT, int NY, bool HAS_T>
 __global__ void __launch_bounds__(256) k_otf_acc(const OtfArgs a) {
   extern __shared__ __align__(16) unsigned char smem_o[];
-  double* gs = reinterpret_cast<double*>(smem_o);           // [2][BM][BJ]
-  double* ts = gs + 2 * OTF_BM * OTF_BJ;                     // [2][BM][BJ] (HAS_T)
-  uint64_t* xs = reinterpret_cast<uint64_t*>(ts + (HAS_T ? 2 * OTF_BM * OTF_BJ : 0));  // [2][BM][XW]
-  double* ys = reinterpret_cast<double*>(xs + 2 * OTF_BM * OTF_XW);      // [NY][2][BM]
+  constexpr int ST = OTF_ACC_STAGES;
+  double* gs = reinterpret_cast<double*>(smem_o);           // [ST][BM][BJ]
+  double* ts = gs + ST * OTF_BM * OTF_BJ;                    // [ST][BM][BJ] (HAS_T)
+  uint64_t* xs = reinterpret_cast<uint64_t*>(ts + (HAS_T ? ST * OTF_BM * OTF_BJ : 0));  // [ST][BM][XW]
+  double* ys = reinterpret_cast<double*>(xs + ST * OTF_BM * OTF_XW);     // [NY][ST][BM]
   constexpr int KC = 8 * NKT;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wj = warp & 3, wk = warp >> 2;
   const int jc = blockIdx.x, j0 = jc * OTF_BJ;
   const int64_t N = a.n_rows;
   const int64_t lo = (N * blockIdx.y) / a.nb, hi = (N * (blockIdx.y + 1)) / a.nb;
@@ -280,80 +323,139 @@ __global__ void __launch_bounds__(256) k_otf_acc(const OtfArgs a) {
   auto load_y = [&](int64_t r0, int buf) {
     for (int e = tid; e < NY * OTF_BM; e += blockDim.x) {
       const int q = e / OTF_BM, r = e % OTF_BM;
-      ys[(q * 2 + buf) * OTF_BM + r] = (r0 + r < hi) ? yv_src[q][r0 + r] : 0.0;
+      ys[(q * ST + buf) * OTF_BM + r] = (r0 + r < hi) ? yv_src[q][r0 + r] : 0.0;
     }
   };
-  if (ntiles > 0) {
-    otf_load_tile(a, lo, hi, j0, gs, HAS_T ? ts : nullptr, xs, tid, blockDim.x);
-    load_y(lo, 0);
-  }
-  cp_async_commit();
-
-  double c[NY][NKT][2];
-  double cu[NY][2];
-#pragma unroll
-  for (int q = 0; q < NY; ++q) {
-    cu[q][0] = cu[q][1] = 0.0;
-#pragma unroll
-    for (int nt = 0; nt < NKT; ++nt) c[q][nt][0] = c[q][nt][1] = 0.0;
-  }
-  const int jl = warp * 8 + (lane >> 2);  // A row (hidden unit) of this lane
-  const int sh_base = lane >> 2;          // B column offset within an n-tile
-  const double one_b = (lane >> 2) == 0 ? 1.0 : 0.0;
-
-  for (int it = 0; it < ntiles; ++it) {
-    const int buf = it & 1;
+  auto load_stage = [&](int it) {  // tile it -> stage it % ST
+    const int b = it % ST;
     const int64_t r0 = lo + (int64_t)it * OTF_BM;
-    if (it + 1 < ntiles) {
-      otf_load_tile(a, r0 + OTF_BM, hi, j0, gs + (buf ^ 1) * OTF_BM * OTF_BJ,
-                    HAS_T ? ts + (buf ^ 1) * OTF_BM * OTF_BJ : nullptr, xs + (buf ^ 1) * OTF_BM * OTF_XW, tid,
-                    blockDim.x);
-      load_y(r0 + OTF_BM, buf ^ 1);
-    }
+    otf_load_tile(a, r0, hi, j0, gs + b * OTF_BM * OTF_BJ, HAS_T ? ts + b * OTF_BM * OTF_BJ : nullptr,
+                  xs + b * OTF_BM * OTF_XW, tid, blockDim.x);
+    load_y(r0, b);
+  };
+  for (int it = 0; it < ST - 1; ++it) {  // prologue: ST - 1 tiles in flight
+    if (it < ntiles) load_stage(it);
     cp_async_commit();
-    cp_async_wait<1>();
+  }
+
+  double c[NY][2][NKT][2];
+  double cu[NY][2][2];
+#pragma unroll
+  for (int q = 0; q < NY; ++q)
+#pragma unroll
+    for (int f = 0; f < 2; ++f) {
+      cu[q][f][0] = cu[q][f][1] = 0.0;
+#pragma unroll
+      for (int nt = 0; nt < NKT; ++nt) c[q][f][nt][0] = c[q][f][nt][1] = 0.0;
+    }
+  const int jl = wj * 16 + (lane >> 2);  // A rows jl, jl + 8 (hidden units) of this lane
+  const int sh_base = lane >> 2;         // B column offset within an n-tile
+  const double one_b = (lane >> 2) == 0 ? 1.0 : 0.0;
+  // the ones column (k = n_in) is bit n_in of every packed row
+  const uint64_t one0 = nin < 64 ? (1ull << nin) : 0ull, one1 = nin >= 64 ? (1ull << (nin - 64)) : 0ull;
+
+  // one barrier per tile: after it, tile it is visible and every warp is done
+  // with tile it - 1, whose stage the load of tile it + ST - 1 reuses
+  for (int it = 0; it < ntiles; ++it) {
+    const int buf = it % ST;
+    cp_async_wait<ST - 2>();
     __syncthreads();
+    if (it + ST - 1 < ntiles) load_stage(it + ST - 1);
+    cp_async_commit();
     const double* G = gs + buf * OTF_BM * OTF_BJ;
     const double* Tt = ts + buf * OTF_BM * OTF_BJ;
     const uint64_t* X = xs + buf * OTF_BM * OTF_XW;
 #pragma unroll 2
-    for (int kk = 0; kk < OTF_BM / 4; ++kk) {
+    for (int kk = wk; kk < OTF_BM / 4; kk += 2) {
       const int rl = kk * 4 + (lane & 3);
-      const double gv = G[rl * OTF_BJ + jl];
-      const double tv = HAS_T ? Tt[rl * OTF_BJ + jl] : 0.0;
-      const uint64_t w0 = X[rl * OTF_XW] >> sh_base, w1 = X[rl * OTF_XW + 1] >> sh_base;
+      const double g0 = G[rl * OTF_BJ + jl], g1 = G[rl * OTF_BJ + jl + 8];
+      double t0 = 0.0, t1 = 0.0;
+      if (HAS_T) {
+        t0 = Tt[rl * OTF_BJ + jl];
+        t1 = Tt[rl * OTF_BJ + jl + 8];
+      }
+      const uint64_t w0 = (X[rl * OTF_XW] | one0) >> sh_base, w1 = (X[rl * OTF_XW + 1] | one1) >> sh_base;
       double bv[NKT];
 #pragma unroll
       for (int nt = 0; nt < NKT; ++nt) {
-        const int kcol = nt * 8 + sh_base;
         const uint32_t bit = nt < 8 ? (uint32_t)(w0 >> (nt * 8)) & 1u : (uint32_t)(w1 >> ((nt - 8) * 8)) & 1u;
         bv[nt] = bit_to_double(bit);
-        if (nt * 8 + 7 >= nin) bv[nt] = (kcol < nin) ? bv[nt] : (kcol == nin ? 1.0 : 0.0);
       }
 #pragma unroll
       for (int q = 0; q < NY; ++q) {
-        const double yq = ys[(q * 2 + buf) * OTF_BM + rl];
-        const double av = gv * yq;
+        const double yq = ys[(q * ST + buf) * OTF_BM + rl];
+        const double a0 = g0 * yq, a1 = g1 * yq;
 #pragma unroll
-        for (int nt = 0; nt < NKT; ++nt) dmma(c[q][nt][0], c[q][nt][1], av, bv[nt]);
-        if (HAS_T) dmma(cu[q][0], cu[q][1], tv * yq, one_b);
+        for (int nt = 0; nt < NKT; ++nt) {
+          dmma(c[q][0][nt][0], c[q][0][nt][1], a0, bv[nt]);
+          dmma(c[q][1][nt][0], c[q][1][nt][1], a1, bv[nt]);
+        }
+        if (HAS_T) {
+          dmma(cu[q][0][0], cu[q][0][1], t0 * yq, one_b);
+          dmma(cu[q][1][0], cu[q][1][1], t1 * yq, one_b);
+        }
       }
     }
-    __syncthreads();
+  }
+  cp_async_wait<0>();
+  __syncthreads();  // the exchange below reuses the stage buffers
+  // row halves: warps 4..7 hand their fragments to warps 0..3 (tile buffers are free now)
+  constexpr int NV = NY * 2 * (NKT + (HAS_T ? 1 : 0)) * 2;
+  static_assert(NV <= OTF_ACC_STAGES * OTF_BJ, "exchange must fit the G tile buffers");
+  double* xch = gs;  // [NV][128]
+  const int xl = wj * 32 + lane;
+  if (wk == 1) {
+    int v = 0;
+#pragma unroll
+    for (int q = 0; q < NY; ++q)
+#pragma unroll
+      for (int f = 0; f < 2; ++f) {
+#pragma unroll
+        for (int nt = 0; nt < NKT; ++nt) {
+          xch[(v++) * 128 + xl] = c[q][f][nt][0];
+          xch[(v++) * 128 + xl] = c[q][f][nt][1];
+        }
+        if (HAS_T) {
+          xch[(v++) * 128 + xl] = cu[q][f][0];
+          xch[(v++) * 128 + xl] = cu[q][f][1];
+        }
+      }
+  }
+  __syncthreads();
+  if (wk == 1) return;
+  {
+    int v = 0;
+#pragma unroll
+    for (int q = 0; q < NY; ++q)
+#pragma unroll
+      for (int f = 0; f < 2; ++f) {
+#pragma unroll
+        for (int nt = 0; nt < NKT; ++nt) {
+          c[q][f][nt][0] += xch[(v++) * 128 + xl];
+          c[q][f][nt][1] += xch[(v++) * 128 + xl];
+        }
+        if (HAS_T) {
+          cu[q][f][0] += xch[(v++) * 128 + xl];
+          cu[q][f][1] += xch[(v++) * 128 + xl];
+        }
+      }
+    (void)NV;
   }
   // partials: C[j][kc] fragment -> part[q][blk][j][kc]
-  const int jrow = j0 + warp * 8 + (lane >> 2);
-  if (jrow < a.hidden) {
+#pragma unroll
+  for (int f = 0; f < 2; ++f) {
+    const int jrow = j0 + jl + 8 * f;
+    if (jrow >= a.hidden) continue;
 #pragma unroll
     for (int q = 0; q < NY; ++q) {
       double* pb = a.part + (((int64_t)q * a.nb + blockIdx.y) * a.hidden + jrow) * KC;
 #pragma unroll
       for (int nt = 0; nt < NKT; ++nt) {
         const int kc = nt * 8 + (lane & 3) * 2;
-        pb[kc] = c[q][nt][0];
-        pb[kc + 1] = c[q][nt][1];
+        pb[kc] = c[q][f][nt][0];
+        pb[kc + 1] = c[q][f][nt][1];
       }
-      if (HAS_T && (lane & 3) == 0) a.partu[((int64_t)q * a.nb + blockIdx.y) * a.hidden + jrow] = cu[q][0];
+      if (HAS_T && (lane & 3) == 0) a.partu[((int64_t)q * a.nb + blockIdx.y) * a.hidden + jrow] = cu[q][f][0];
     }
   }
 }
@@ -361,44 +463,76 @@ __global__ void __launch_bounds__(256) k_otf_acc(const OtfArgs a) {
 // Assemble the MLP-layout parameter vector from the acc partials:
 //   mode 0 (product): out = sum part - obar * Y (+ u0 hf), out0 = g0
 //   mode 1 (stats)  : out = sum part          (Y, obar unused)
+// Fixed-order block sum of src[0..count) (every thread gets the total).
+__device__ __forceinline__ double block_sum_fixed(const double* __restrict__ src, int count, double* sh) {
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x, nt = blockDim.x * blockDim.y;
+  double v = 0.0;
+  for (int q = tid; q < count; q += nt) v += src[q];
+  v = warp_sum<false>(v);
+  if ((tid & 31) == 0) sh[tid >> 5] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int w = 0; w < (nt >> 5); ++w) t += sh[w];
+  __syncthreads();
+  return t;
+}
+
+// Column reduction of the row-block partials: blockDim (32, 8); lane x owns one
+// output, the 8 y-phases split the partial blocks (b = y, y + 8, ...), then a
+// fixed-order sum over y (valid on threadIdx.y == 0).
+__device__ __forceinline__ double ysum8(double v, double (*sm)[33]) {
+  sm[threadIdx.y][threadIdx.x] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.y == 0)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) t += sm[q][threadIdx.x];
+  __syncthreads();
+  return t;
+}
+
+// MLP assembly in the layout [W (h x n_in), b, u, c]; blockDim (32, 8)
 __global__ void __launch_bounds__(256) k_otf_finish(const double* __restrict__ part, const double* __restrict__ partu,
                                                     int nb, int hidden, int n_in, int kc, int64_t ld,
                                                     const double* __restrict__ ypart, int n_ypart,
                                                     const double* __restrict__ obar, const double* hf,
                                                     const double* u0, const double* dgpart, int n_dgpart,
                                                     double* out, double* out0) {
-  double Y = 0.0;
-  for (int q = 0; q < n_ypart; ++q) Y += ypart[q];
+  __shared__ double sh[8];
+  __shared__ double sm[8][33];
+  const double Y = block_sum_fixed(ypart, n_ypart, sh);
   const int64_t hn = (int64_t)hidden * n_in;
   const int64_t P = hn + 2 * hidden + 1;
   const double uu = (hf && u0) ? *u0 : 0.0;
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < ld; p += (int64_t)gridDim.x * blockDim.x) {
+  const int ty = threadIdx.y;
+  for (int64_t p0 = blockIdx.x * 32LL; p0 < ld; p0 += gridDim.x * 32LL) {
+    const int64_t p = p0 + threadIdx.x;
     double acc = 0.0;
     if (p < hn) {
       const int64_t j = p / n_in, k = p % n_in;
-      for (int b = 0; b < nb; ++b) acc += part[((int64_t)b * hidden + j) * kc + k];
+      for (int b = ty; b < nb; b += 8) acc += part[((int64_t)b * hidden + j) * kc + k];
     } else if (p < hn + hidden) {
       const int64_t j = p - hn;
-      for (int b = 0; b < nb; ++b) acc += part[((int64_t)b * hidden + j) * kc + n_in];
+      for (int b = ty; b < nb; b += 8) acc += part[((int64_t)b * hidden + j) * kc + n_in];
     } else if (p < hn + 2 * hidden) {
       const int64_t j = p - hn - hidden;
-      for (int b = 0; b < nb; ++b) acc += partu[(int64_t)b * hidden + j];
-    } else if (p == P - 1) {
-      acc = Y;
+      for (int b = ty; b < nb; b += 8) acc += partu[(int64_t)b * hidden + j];
     }
-    if (p < P) {
-      if (obar) acc = fma(-obar[p], Y, acc);
-      if (hf && u0) acc = fma(uu, hf[p], acc);
-    } else {
-      acc = 0.0;
+    acc = ysum8(acc, sm);
+    if (ty == 0 && p < ld) {
+      if (p == P - 1) acc = Y;
+      if (p < P) {
+        if (obar) acc = fma(-obar[p], Y, acc);
+        if (hf && u0) acc = fma(uu, hf[p], acc);
+      } else {
+        acc = 0.0;
+      }
+      out[p] = acc;
     }
-    out[p] = acc;
   }
-  if (out0 && blockIdx.x == 0 && threadIdx.x == 0) {
-    double g = 0.0;
-    if (hf)
-      for (int q = 0; q < n_dgpart; ++q) g += dgpart[q];
-    *out0 = g;
+  if (out0 && blockIdx.x == 0) {
+    const double g = hf ? block_sum_fixed(dgpart, n_dgpart, sh) : 0.0;
+    if (threadIdx.x == 0 && threadIdx.y == 0) *out0 = g;
   }
 }
 
@@ -556,20 +690,34 @@ namespace irl {
 // packed row words are broadcast), plus ypart[blk] = sum y_r.  Fixed order.
 __global__ void __launch_bounds__(128) k_xsum(const uint64_t* __restrict__ xbits, const double* __restrict__ y,
                                               int64_t n, int n_in, double* xpart, double* ypart) {
+  __shared__ uint64_t xb[128][OTF_XW];
+  __shared__ double yb[128];
+  __shared__ double sh[4];
   const int64_t per = (n + gridDim.x - 1) / gridDim.x;
   const int64_t lo = blockIdx.x * per, hi = min(n, lo + per);
   const int i = threadIdx.x;
+  const int wsel = i >> 6, sft = i & 63;
   double acc = 0.0, ys = 0.0;
-  for (int64_t r = lo; r < hi; ++r) {
-    const double yr = y[r];
-    if (i < n_in) {
-      const uint64_t w = __ldg(xbits + r * OTF_XW + (i >> 6));
-      if ((w >> (i & 63)) & 1ull) acc += yr;
+  for (int64_t r0 = lo; r0 < hi; r0 += 128) {  // stage 128 rows (coalesced), then scan them from smem
+    const int64_t r = r0 + i;
+    if (r < hi) {
+      xb[i][0] = xbits[r * OTF_XW];
+      xb[i][1] = xbits[r * OTF_XW + 1];
+      yb[i] = y[r];
+      ys += yb[i];
     }
-    ys += yr;
+    __syncthreads();
+    const int cnt = (int)min((int64_t)128, hi - r0);
+    if (i < n_in)
+      for (int q = 0; q < cnt; ++q)
+        if ((xb[q][wsel] >> sft) & 1ull) acc += yb[q];
+    __syncthreads();
   }
   if (i < n_in) xpart[(int64_t)blockIdx.x * n_in + i] = acc;
-  if (i == 0) ypart[blockIdx.x] = ys;
+  ys = warp_sum<false>(ys);
+  if ((i & 31) == 0) sh[i >> 5] = ys;
+  __syncthreads();
+  if (i == 0) ypart[blockIdx.x] = ((sh[0] + sh[1]) + sh[2]) + sh[3];
 }
 
 // RBM real column statistics in the parameter layout [a (n), b (h), W (h x n)]:
@@ -577,19 +725,23 @@ __global__ void __launch_bounds__(128) k_xsum(const uint64_t* __restrict__ xbits
 __global__ void __launch_bounds__(256) k_rbm_stats_finish(const double* __restrict__ part, int nb, int hidden,
                                                           int n_in, int kc, const double* __restrict__ xpart, int nbx,
                                                           int64_t ld, double* out) {
+  __shared__ double sm[8][33];
   const int64_t P = (int64_t)n_in + hidden + (int64_t)hidden * n_in;
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < ld; p += (int64_t)gridDim.x * blockDim.x) {
+  const int ty = threadIdx.y;
+  for (int64_t p0 = blockIdx.x * 32LL; p0 < ld; p0 += gridDim.x * 32LL) {
+    const int64_t p = p0 + threadIdx.x;
     double acc = 0.0;
     if (p < n_in) {
-      for (int b = 0; b < nbx; ++b) acc += xpart[(int64_t)b * n_in + p];
+      for (int b = ty; b < nbx; b += 8) acc += xpart[(int64_t)b * n_in + p];
     } else if (p < n_in + hidden) {
       const int64_t j = p - n_in;
-      for (int b = 0; b < nb; ++b) acc += part[((int64_t)b * hidden + j) * kc + n_in];
+      for (int b = ty; b < nb; b += 8) acc += part[((int64_t)b * hidden + j) * kc + n_in];
     } else if (p < P) {
       const int64_t q = p - n_in - hidden, j = q / n_in, i = q % n_in;
-      for (int b = 0; b < nb; ++b) acc += part[((int64_t)b * hidden + j) * kc + i];
+      for (int b = ty; b < nb; b += 8) acc += part[((int64_t)b * hidden + j) * kc + i];
     }
-    out[p] = acc;
+    acc = ysum8(acc, sm);
+    if (ty == 0 && p < ld) out[p] = acc;
   }
 }
 }  // namespace irl
@@ -603,34 +755,38 @@ __global__ void __launch_bounds__(256) k_rbm_otf_finish(const double* __restrict
                                                         const double* __restrict__ obar, const double* hf,
                                                         const double* u0, const double* dgpart, int n_dgpart,
                                                         double* out, double* out0) {
-  double Y = 0.0;
-  for (int q = 0; q < n_ypart; ++q) Y += ypart[q];
+  __shared__ double sh[8];
+  __shared__ double sm[8][33];
+  const double Y = block_sum_fixed(ypart, n_ypart, sh);
   const int64_t P = (int64_t)n_in + hidden + (int64_t)hidden * n_in;
   const double uu = (hf && u0) ? *u0 : 0.0;
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < ld; p += (int64_t)gridDim.x * blockDim.x) {
+  const int ty = threadIdx.y;
+  for (int64_t p0 = blockIdx.x * 32LL; p0 < ld; p0 += gridDim.x * 32LL) {
+    const int64_t p = p0 + threadIdx.x;
     double acc = 0.0;
     if (p < n_in) {
-      for (int b = 0; b < nbx; ++b) acc += xpart[(int64_t)b * n_in + p];
+      for (int b = ty; b < nbx; b += 8) acc += xpart[(int64_t)b * n_in + p];
     } else if (p < n_in + hidden) {
       const int64_t j = p - n_in;
-      for (int b = 0; b < nb; ++b) acc += part[((int64_t)b * hidden + j) * kc + n_in];
+      for (int b = ty; b < nb; b += 8) acc += part[((int64_t)b * hidden + j) * kc + n_in];
     } else if (p < P) {
       const int64_t q = p - n_in - hidden, j = q / n_in, i = q % n_in;
-      for (int b = 0; b < nb; ++b) acc += part[((int64_t)b * hidden + j) * kc + i];
+      for (int b = ty; b < nb; b += 8) acc += part[((int64_t)b * hidden + j) * kc + i];
     }
-    if (p < P) {
-      if (obar) acc = fma(-obar[p], Y, acc);
-      if (hf && u0) acc = fma(uu, hf[p], acc);
-    } else {
-      acc = 0.0;
+    acc = ysum8(acc, sm);
+    if (ty == 0 && p < ld) {
+      if (p < P) {
+        if (obar) acc = fma(-obar[p], Y, acc);
+        if (hf && u0) acc = fma(uu, hf[p], acc);
+      } else {
+        acc = 0.0;
+      }
+      out[p] = acc;
     }
-    out[p] = acc;
   }
-  if (out0 && blockIdx.x == 0 && threadIdx.x == 0) {
-    double g = 0.0;
-    if (hf)
-      for (int q = 0; q < n_dgpart; ++q) g += dgpart[q];
-    *out0 = g;
+  if (out0 && blockIdx.x == 0) {
+    const double g = hf ? block_sum_fixed(dgpart, n_dgpart, sh) : 0.0;
+    if (threadIdx.x == 0 && threadIdx.y == 0) *out0 = g;
   }
 }
 }  // namespace irl
@@ -675,48 +831,66 @@ __device__ __forceinline__ void otf_load_ctile(const OtfCArgs& a, int64_t r0, in
   }
 }
 
-// grid (ceil(2h/64), nb), 256 threads
+// grid (persistent, 1-D), 256 threads: complex t partials over this CTA's
+// range of (real column chunk, 64-row tile) pairs
 __global__ void __launch_bounds__(256) k_otf_dot_c(const OtfCArgs a) {
   extern __shared__ __align__(16) unsigned char smem_c[];
-  double* vw = reinterpret_cast<double*>(smem_c);            // [64][OTF_MAX_NIN]
-  double* vb = vw + OTF_BJ * OTF_MAX_NIN;                    // [64]
+  const int nin = a.n_in, vs = otf_vstride(nin);
+  double* vw = reinterpret_cast<double*>(smem_c);            // [64][vs]
+  double* vb = vw + OTF_BJ * vs;                             // [64]
   double* gs = vb + OTF_BJ;                                  // [2][BM][64]
   uint64_t* xs = reinterpret_cast<uint64_t*>(gs + 2 * OTF_BM * OTF_BJ);  // [2][BM][XW]
   double2* red = reinterpret_cast<double2*>(xs + 2 * OTF_BM * OTF_XW);   // [4][BM]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wr = warp >> 2, wj = warp & 3;
-  const int c0 = blockIdx.x * OTF_BJ;  // real column chunk
-  const int ncols = 2 * a.hidden, nin = a.n_in;
+  const int ncols = 2 * a.hidden;
   const int64_t N = a.n_rows;
-  const int64_t lo = (N * blockIdx.y) / a.nb, hi = (N * (blockIdx.y + 1)) / a.nb;
-  for (int e = tid; e < OTF_BJ * OTF_MAX_NIN; e += blockDim.x) {
-    const int cc = e / OTF_MAX_NIN, k = e % OTF_MAX_NIN;
-    const int col = c0 + cc;
-    double val = 0.0;
-    if (col < ncols && k < nin) {
-      const int64_t idx = a.offW + (int64_t)(col >> 1) * nin + k;
-      val = (col & 1) ? a.v_im[idx] : a.v_re[idx];
+  const int64_t ntiles = (N + OTF_BM - 1) / OTF_BM;
+  const int jcount = (ncols + OTF_BJ - 1) / OTF_BJ;
+  int64_t t0, t1;
+  otf_cta_range(ntiles * jcount, t0, t1);
+  if (t0 >= t1) return;
+
+  auto load_v = [&](int jc) {
+    const int c0 = jc * OTF_BJ;
+    for (int e = tid; e < OTF_BJ * vs; e += blockDim.x) {
+      const int cc = e / vs, k = e % vs;
+      const int col = c0 + cc;
+      double val = 0.0;
+      if (col < ncols && k < nin) {
+        const int64_t idx = a.offW + (int64_t)(col >> 1) * nin + k;
+        val = (col & 1) ? a.v_im[idx] : a.v_re[idx];
+      }
+      vw[e] = val;
     }
-    vw[e] = val;
-  }
-  for (int e = tid; e < OTF_BJ; e += blockDim.x) {
-    const int col = c0 + e;
-    vb[e] = col < ncols ? ((col & 1) ? a.v_im[a.offb + (col >> 1)] : a.v_re[a.offb + (col >> 1)]) : 0.0;
-  }
-  const int ntiles = (int)((hi - lo + OTF_BM - 1) / OTF_BM);
-  if (ntiles > 0) otf_load_ctile(a, lo, hi, c0, gs, xs, tid, blockDim.x);
+    for (int e = tid; e < OTF_BJ; e += blockDim.x) {
+      const int col = c0 + e;
+      vb[e] = col < ncols ? ((col & 1) ? a.v_im[a.offb + (col >> 1)] : a.v_re[a.offb + (col >> 1)]) : 0.0;
+    }
+  };
+  auto load_tile = [&](int64_t t, int buf) {
+    const int jc = (int)(t / ntiles);
+    const int64_t r0 = (t % ntiles) * OTF_BM;
+    otf_load_ctile(a, r0, min(N, r0 + OTF_BM), jc * OTF_BJ, gs + buf * OTF_BM * OTF_BJ, xs + buf * OTF_BM * OTF_XW,
+                   tid, blockDim.x);
+  };
+  int cur_jc = (int)(t0 / ntiles);
+  load_v(cur_jc);
+  load_tile(t0, 0);
   cp_async_commit();
   const int ksteps = (nin + 3) / 4;
-  const double* vrow0 = vw + (wj * 16 + (lane >> 2)) * OTF_MAX_NIN + (lane & 3);
-  for (int it = 0; it < ntiles; ++it) {
-    const int buf = it & 1;
-    const int64_t r0 = lo + (int64_t)it * OTF_BM;
-    if (it + 1 < ntiles)
-      otf_load_ctile(a, r0 + OTF_BM, hi, c0, gs + (buf ^ 1) * OTF_BM * OTF_BJ, xs + (buf ^ 1) * OTF_BM * OTF_XW, tid,
-                     blockDim.x);
+  for (int64_t t = t0; t < t1; ++t) {
+    const int buf = (int)((t - t0) & 1);
+    const int jc = (int)(t / ntiles);
+    const int64_t r0 = (t % ntiles) * OTF_BM;
+    if (t + 1 < t1) load_tile(t + 1, buf ^ 1);
     cp_async_commit();
     cp_async_wait<1>();
+    if (jc != cur_jc) {
+      load_v(jc);
+      cur_jc = jc;
+    }
     __syncthreads();
     const double* G = gs + buf * OTF_BM * OTF_BJ;
     const uint64_t* X = xs + buf * OTF_BM * OTF_XW;
@@ -735,10 +909,11 @@ __global__ void __launch_bounds__(256) k_otf_dot_c(const OtfCArgs a) {
     for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
       for (int q = 0; q < OTF_XW; ++q) xr[mt][q] = X[(wr * 32 + mt * 8 + (lane >> 2)) * OTF_XW + q];
+    const double* vrow0 = vw + (wj * 16 + (lane >> 2)) * vs + (lane & 3);
     for (int kk = 0; kk < ksteps; ++kk) {
       const int k = kk * 4 + (lane & 3);
       const double b0 = vrow0[kk * 4];
-      const double b1 = vrow0[kk * 4 + 8 * OTF_MAX_NIN];
+      const double b1 = vrow0[kk * 4 + 8 * vs];
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt) {
         const uint64_t word = (k < 64) ? xr[mt][0] : xr[mt][1];
@@ -775,13 +950,13 @@ __global__ void __launch_bounds__(256) k_otf_dot_c(const OtfCArgs a) {
     __syncthreads();
     if (tid < OTF_BM) {
       const int64_t row = r0 + tid;
-      if (row < hi) {
-        double2 t = red[tid];
+      if (row < N) {
+        double2 tv = red[tid];
         for (int w = 1; w < 4; ++w) {
-          t.x += red[w * OTF_BM + tid].x;
-          t.y += red[w * OTF_BM + tid].y;
+          tv.x += red[w * OTF_BM + tid].x;
+          tv.y += red[w * OTF_BM + tid].y;
         }
-        a.tpart[(int64_t)blockIdx.x * N + row] = t;
+        a.tpart[(int64_t)jc * N + row] = tv;
       }
     }
     __syncthreads();
@@ -882,15 +1057,19 @@ __global__ void __launch_bounds__(256) k_otf_y_c(const double2* __restrict__ tpa
   }
 }
 
-// part[blk][2j+p][kc] = sum_rows (conj(T_nj) y_n)_p x_n,kc  (kc = n_in: ones column)
+// part[blk][2j+p][kc] = sum_rows (conj(T_nj) y_n)_p x_n,kc  (kc = n_in: ones column).
+// Same warp layout as k_otf_acc: two A fragments (real rows jl, jl + 8) per
+// B fragment, row quads split over the two warp halves.
 template <int NKT>
 __global__ void __launch_bounds__(256) k_otf_acc_c(const OtfCArgs a) {
   extern __shared__ __align__(16) unsigned char smem_c[];
-  double* gs = reinterpret_cast<double*>(smem_c);                        // [2][BM][64]
-  uint64_t* xs = reinterpret_cast<uint64_t*>(gs + 2 * OTF_BM * OTF_BJ);  // [2][BM][XW]
-  double2* ys = reinterpret_cast<double2*>(xs + 2 * OTF_BM * OTF_XW);    // [2][BM]
+  constexpr int ST = OTF_ACC_STAGES;
+  double* gs = reinterpret_cast<double*>(smem_c);                         // [ST][BM][64]
+  uint64_t* xs = reinterpret_cast<uint64_t*>(gs + ST * OTF_BM * OTF_BJ);  // [ST][BM][XW]
+  double2* ys = reinterpret_cast<double2*>(xs + ST * OTF_BM * OTF_XW);    // [ST][BM]
   constexpr int KC = 8 * NKT;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wj = warp & 3, wk = warp >> 2;
   const int c0 = blockIdx.x * OTF_BJ;
   const int64_t N = a.n_rows;
   const int64_t lo = (N * blockIdx.y) / a.nb, hi = (N * (blockIdx.y + 1)) / a.nb;
@@ -901,83 +1080,116 @@ __global__ void __launch_bounds__(256) k_otf_acc_c(const OtfCArgs a) {
       ys[buf * OTF_BM + e] = (r0 + e >= hi) ? make_double2(0.0, 0.0)
                              : a.y ? a.y[r0 + e] : make_double2(a.yr[r0 + e], 0.0);
   };
-  if (ntiles > 0) {
-    otf_load_ctile(a, lo, hi, c0, gs, xs, tid, blockDim.x);
-    load_y(lo, 0);
+  auto load_stage = [&](int it) {
+    const int b = it % ST;
+    const int64_t r0 = lo + (int64_t)it * OTF_BM;
+    otf_load_ctile(a, r0, hi, c0, gs + b * OTF_BM * OTF_BJ, xs + b * OTF_BM * OTF_XW, tid, blockDim.x);
+    load_y(r0, b);
+  };
+  for (int it = 0; it < ST - 1; ++it) {
+    if (it < ntiles) load_stage(it);
+    cp_async_commit();
   }
-  cp_async_commit();
-  double c[NKT][2];
+  double c[2][NKT][2];
 #pragma unroll
-  for (int nt = 0; nt < NKT; ++nt) c[nt][0] = c[nt][1] = 0.0;
-  const int jl = warp * 8 + (lane >> 2);  // real row (2j + p) of this lane within the chunk
+  for (int f = 0; f < 2; ++f)
+#pragma unroll
+    for (int nt = 0; nt < NKT; ++nt) c[f][nt][0] = c[f][nt][1] = 0.0;
+  const int jl = wj * 16 + (lane >> 2);  // real rows (2j + p) jl and jl + 8 within the chunk
   const int pj = jl & 1, jb = jl & ~1;
   const int sh_base = lane >> 2;
+  const uint64_t one0 = nin < 64 ? (1ull << nin) : 0ull, one1 = nin >= 64 ? (1ull << (nin - 64)) : 0ull;
   for (int it = 0; it < ntiles; ++it) {
-    const int buf = it & 1;
-    const int64_t r0 = lo + (int64_t)it * OTF_BM;
-    if (it + 1 < ntiles) {
-      otf_load_ctile(a, r0 + OTF_BM, hi, c0, gs + (buf ^ 1) * OTF_BM * OTF_BJ, xs + (buf ^ 1) * OTF_BM * OTF_XW, tid,
-                     blockDim.x);
-      load_y(r0 + OTF_BM, buf ^ 1);
-    }
-    cp_async_commit();
-    cp_async_wait<1>();
+    const int buf = it % ST;
+    cp_async_wait<ST - 2>();
     __syncthreads();
+    if (it + ST - 1 < ntiles) load_stage(it + ST - 1);
+    cp_async_commit();
     const double* G = gs + buf * OTF_BM * OTF_BJ;
     const uint64_t* X = xs + buf * OTF_BM * OTF_XW;
 #pragma unroll 2
-    for (int kk = 0; kk < OTF_BM / 4; ++kk) {
+    for (int kk = wk; kk < OTF_BM / 4; kk += 2) {
       const int rl = kk * 4 + (lane & 3);
-      const double2 t = *reinterpret_cast<const double2*>(G + rl * OTF_BJ + jb);
+      const double2 ta = *reinterpret_cast<const double2*>(G + rl * OTF_BJ + jb);
+      const double2 tb = *reinterpret_cast<const double2*>(G + rl * OTF_BJ + jb + 8);
       const double2 yv = ys[buf * OTF_BM + rl];
       // conj(t) y = (t.x y.x + t.y y.y) + i (t.x y.y - t.y y.x)
-      const double av = pj ? fma(t.x, yv.y, -t.y * yv.x) : fma(t.x, yv.x, t.y * yv.y);
-      const uint64_t w0 = X[rl * OTF_XW] >> sh_base, w1 = X[rl * OTF_XW + 1] >> sh_base;
+      const double a0 = pj ? fma(ta.x, yv.y, -ta.y * yv.x) : fma(ta.x, yv.x, ta.y * yv.y);
+      const double a1 = pj ? fma(tb.x, yv.y, -tb.y * yv.x) : fma(tb.x, yv.x, tb.y * yv.y);
+      const uint64_t w0 = (X[rl * OTF_XW] | one0) >> sh_base, w1 = (X[rl * OTF_XW + 1] | one1) >> sh_base;
 #pragma unroll
       for (int nt = 0; nt < NKT; ++nt) {
-        const int kcol = nt * 8 + sh_base;
         const uint32_t bit = nt < 8 ? (uint32_t)(w0 >> (nt * 8)) & 1u : (uint32_t)(w1 >> ((nt - 8) * 8)) & 1u;
-        double bv = bit_to_double(bit);
-        if (nt * 8 + 7 >= nin) bv = (kcol < nin) ? bv : (kcol == nin ? 1.0 : 0.0);
-        dmma(c[nt][0], c[nt][1], av, bv);
+        const double bv = bit_to_double(bit);
+        dmma(c[0][nt][0], c[0][nt][1], a0, bv);
+        dmma(c[1][nt][0], c[1][nt][1], a1, bv);
       }
     }
-    __syncthreads();
   }
-  const int col = c0 + jl;
-  if (col < ncols) {
+  cp_async_wait<0>();
+  __syncthreads();
+  constexpr int NV = 2 * NKT * 2;
+  static_assert(NV <= OTF_ACC_STAGES * OTF_BJ, "exchange must fit the tile buffers");
+  double* xch = gs;  // [NV][128]
+  const int xl = wj * 32 + lane;
+  if (wk == 1) {
+#pragma unroll
+    for (int f = 0; f < 2; ++f)
+#pragma unroll
+      for (int nt = 0; nt < NKT; ++nt) {
+        xch[((f * NKT + nt) * 2) * 128 + xl] = c[f][nt][0];
+        xch[((f * NKT + nt) * 2 + 1) * 128 + xl] = c[f][nt][1];
+      }
+  }
+  __syncthreads();
+  if (wk == 1) return;
+#pragma unroll
+  for (int f = 0; f < 2; ++f) {
+    const int col = c0 + jl + 8 * f;
+#pragma unroll
+    for (int nt = 0; nt < NKT; ++nt) {
+      c[f][nt][0] += xch[((f * NKT + nt) * 2) * 128 + xl];
+      c[f][nt][1] += xch[((f * NKT + nt) * 2 + 1) * 128 + xl];
+    }
+    if (col >= ncols) continue;
     double* pb = a.part + ((int64_t)blockIdx.y * ncols + col) * KC;
 #pragma unroll
     for (int nt = 0; nt < NKT; ++nt) {
       const int kc = nt * 8 + (lane & 3) * 2;
-      pb[kc] = c[nt][0];
-      pb[kc + 1] = c[nt][1];
+      pb[kc] = c[f][nt][0];
+      pb[kc + 1] = c[f][nt][1];
     }
   }
 }
 
-// xpart[blk][i] = sum y_r x_ri (complex y)
+// xpart[blk][i] = sum y_r x_ri (complex y, or real yr); rows staged in smem
 __global__ void __launch_bounds__(128) k_xsum_c(const uint64_t* __restrict__ xbits, const double2* __restrict__ y,
                                                 const double* __restrict__ yr, int64_t n, int n_in, double2* xpart) {
+  __shared__ uint64_t xb[128][OTF_XW];
+  __shared__ double2 yb[128];
   const int64_t per = (n + gridDim.x - 1) / gridDim.x;
   const int64_t lo = blockIdx.x * per, hi = min(n, lo + per);
   const int i = threadIdx.x;
+  const int wsel = i >> 6, sft = i & 63;
   double ar = 0.0, ai = 0.0;
-  if (i < n_in) {
-    for (int64_t r = lo; r < hi; ++r) {
-      const uint64_t w = __ldg(xbits + r * OTF_XW + (i >> 6));
-      if ((w >> (i & 63)) & 1ull) {
-        if (y) {
-          const double2 yy = y[r];
-          ar += yy.x;
-          ai += yy.y;
-        } else {
-          ar += yr[r];
-        }
-      }
+  for (int64_t r0 = lo; r0 < hi; r0 += 128) {
+    const int64_t r = r0 + i;
+    if (r < hi) {
+      xb[i][0] = xbits[r * OTF_XW];
+      xb[i][1] = xbits[r * OTF_XW + 1];
+      yb[i] = y ? y[r] : make_double2(yr[r], 0.0);
     }
-    xpart[(int64_t)blockIdx.x * n_in + i] = make_double2(ar, ai);
+    __syncthreads();
+    const int cnt = (int)min((int64_t)128, hi - r0);
+    if (i < n_in)
+      for (int q = 0; q < cnt; ++q)
+        if ((xb[q][wsel] >> sft) & 1ull) {
+          ar += yb[q].x;
+          ai += yb[q].y;
+        }
+    __syncthreads();
   }
+  if (i < n_in) xpart[(int64_t)blockIdx.x * n_in + i] = make_double2(ar, ai);
 }
 
 // Assemble the complex RBM vector [a, b, W] from the partials.
@@ -990,35 +1202,56 @@ __global__ void __launch_bounds__(256) k_rbm_otf_finish_c(const double* __restri
                                                           const double* hf_im, const double* u0,
                                                           const double* gpart, int n_gpart, double* out_re,
                                                           double* out_im, double* out0, double2* out_c, int conj_out) {
+  __shared__ double sh[8];
+  __shared__ double sm[8][33];
+  // ypart as 2 n_ypart doubles (re, im interleaved): sum the two lanes separately
   double Yr = 0.0, Yi = 0.0;
-  for (int q = 0; q < n_ypart; ++q) {
-    Yr += ypart[q].x;
-    Yi += ypart[q].y;
+  if (ypart) {
+    const int tid = threadIdx.y * 32 + threadIdx.x;
+    for (int q = tid; q < n_ypart; q += 256) {
+      Yr += ypart[q].x;
+      Yi += ypart[q].y;
+    }
+    Yr = warp_sum<false>(Yr);
+    Yi = warp_sum<false>(Yi);
+    __shared__ double2 shy[8];
+    if ((tid & 31) == 0) shy[tid >> 5] = make_double2(Yr, Yi);
+    __syncthreads();
+    Yr = Yi = 0.0;
+    for (int w = 0; w < 8; ++w) {
+      Yr += shy[w].x;
+      Yi += shy[w].y;
+    }
   }
   const int ncols = 2 * hidden;
   const int64_t P = (int64_t)n_in + hidden + (int64_t)hidden * n_in;
   const double uu = (hf_re && u0) ? *u0 : 0.0;
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < ld; p += (int64_t)gridDim.x * blockDim.x) {
+  const int ty = threadIdx.y;
+  for (int64_t p0 = blockIdx.x * 32LL; p0 < ld; p0 += gridDim.x * 32LL) {
+    const int64_t p = p0 + threadIdx.x;
     double ar = 0.0, ai = 0.0;
     if (p < n_in) {
-      for (int b = 0; b < nbx; ++b) {
+      for (int b = ty; b < nbx; b += 8) {
         const double2 q = xpart[(int64_t)b * n_in + p];
         ar += q.x;
         ai += q.y;
       }
     } else if (p < n_in + hidden) {
       const int64_t j = p - n_in;
-      for (int b = 0; b < nb; ++b) {
+      for (int b = ty; b < nb; b += 8) {
         ar += part[((int64_t)b * ncols + 2 * j) * kc + n_in];
         ai += part[((int64_t)b * ncols + 2 * j + 1) * kc + n_in];
       }
     } else if (p < P) {
       const int64_t q = p - n_in - hidden, j = q / n_in, i = q % n_in;
-      for (int b = 0; b < nb; ++b) {
+      for (int b = ty; b < nb; b += 8) {
         ar += part[((int64_t)b * ncols + 2 * j) * kc + i];
         ai += part[((int64_t)b * ncols + 2 * j + 1) * kc + i];
       }
     }
+    ar = ysum8(ar, sm);
+    ai = ysum8(ai, sm);
+    if (ty != 0 || p >= ld) continue;
     if (p >= P) ar = ai = 0.0;
     if (out_c) {
       out_c[p] = make_double2(ar, conj_out ? -ai : ai);
@@ -1038,11 +1271,9 @@ __global__ void __launch_bounds__(256) k_rbm_otf_finish_c(const double* __restri
     out_re[p] = ar;
     if (out_im) out_im[p] = ai;
   }
-  if (out0 && blockIdx.x == 0 && threadIdx.x == 0) {
-    double g = 0.0;
-    if (hf_re)
-      for (int q = 0; q < n_gpart; ++q) g += gpart[q];
-    *out0 = g;
+  if (out0 && blockIdx.x == 0) {
+    const double g = hf_re ? block_sum_fixed(gpart, n_gpart, sh) : 0.0;
+    if (threadIdx.x == 0 && threadIdx.y == 0) *out0 = g;
   }
 }
 

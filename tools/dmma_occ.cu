@@ -1,46 +1,57 @@
-// DMMA throughput vs warps per SM and independent accumulator chains (development tool)
+// DMMA (mma.sync m8n8k4 f64) throughput vs resident warps and independent
+// accumulators per warp.  Development tool: what fraction of the FP64 tensor
+// peak is reachable at the occupancy the on-the-fly GEMMs run at.
 #include <cstdio>
 #include <cuda_runtime.h>
-template <int CH>
-__global__ void k(double* out, int iters) {
+
+template <int NACC>
+__global__ void k_dmma(double* out, int iters) {
   double a = threadIdx.x * 1e-3, b = 1.0 + threadIdx.x * 1e-4;
-  double c[CH][2];
-  for (int t = 0; t < CH; ++t) c[t][0] = c[t][1] = 0.0;
+  double c[NACC][2];
+#pragma unroll
+  for (int t = 0; t < NACC; ++t) c[t][0] = c[t][1] = 0.0;
   for (int i = 0; i < iters; ++i) {
 #pragma unroll
-    for (int t = 0; t < CH; ++t)
+    for (int t = 0; t < NACC; ++t)
       asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                   : "+d"(c[t][0]), "+d"(c[t][1]) : "d"(a), "d"(b));
+                   : "+d"(c[t][0]), "+d"(c[t][1])
+                   : "d"(a), "d"(b));
   }
   double s = 0;
-  for (int t = 0; t < CH; ++t) s += c[t][0] + c[t][1];
+#pragma unroll
+  for (int t = 0; t < NACC; ++t) s += c[t][0] + c[t][1];
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
-template <int CH>
-void run(int sms, int blocks_per_sm, int threads, double* out) {
+
+template <int NACC>
+void run(int sms, double* out, int warps_per_sm) {
+  const int threads = 256;
+  const int ctas = sms * warps_per_sm / 8;
+  const int iters = 4000;
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  const int iters = 4000;
-  k<CH><<<sms * blocks_per_sm, threads>>>(out, 10);
+  k_dmma<NACC><<<ctas, threads>>>(out, 10);
   cudaEventRecord(e0);
-  k<CH><<<sms * blocks_per_sm, threads>>>(out, iters);
+  k_dmma<NACC><<<ctas, threads>>>(out, iters);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms;
   cudaEventElapsedTime(&ms, e0, e1);
-  double flops = 2.0 * 256 * CH * iters * (double)(threads / 32) * sms * blocks_per_sm;
-  printf("chains=%2d warps/SM=%2d : %.1f TFLOP/s\n", CH, blocks_per_sm * threads / 32, flops / ms / 1e9);
+  const double flops = 512.0 * NACC * iters * (threads / 32) * (double)ctas;
+  printf("warps/SM=%2d acc/warp=%2d : %6.2f TFLOP/s\n", warps_per_sm, NACC, flops / ms / 1e9);
 }
+
 int main() {
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   double* out;
-  cudaMalloc(&out, sizeof(double) * sms * 4 * 1024);
-  for (int w : {4, 8, 12, 16}) {
-    run<4>(sms, 1, w * 32, out);
-    run<8>(sms, 1, w * 32, out);
-    run<16>(sms, 1, w * 32, out);
+  cudaMalloc(&out, sizeof(double) * sms * 64 * 32);
+  for (int w : {8, 16, 24, 32}) {
+    run<4>(sms, out, w);
+    run<8>(sms, out, w);
+    run<16>(sms, out, w);
+    run<26>(sms, out, w);
   }
   return 0;
 }
