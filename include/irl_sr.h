@@ -175,6 +175,9 @@ int irl_otf_mvp_rbm_c128(const uint64_t* xbits, const double* t, int64_t n, int 
  * (krylov.py:165-190, as applied by implicit_restart :225-227) on the dense
  * row-major m x m tridiagonal T, accumulating Q (both in/out, host memory). */
 int irl_lanczos_step_small(double* V, int64_t ldv, double* W, int64_t L, int j, int m, double* ab, void* stream);
+/* The same step on one thread-block cluster (2..16 CTAs, DSMEM reductions) for
+ * medium L; j + 1 <= 64. */
+int irl_lanczos_step_cluster(double* V, int64_t ldv, double* W, int64_t L, int j, int m, double* ab, void* stream);
 int irl_host_qr_sweeps(int m, double* T, double* Q, const double* shifts, int nshift);
 
 #if defined(__GNUC__)

@@ -56,6 +56,7 @@ SIGNATURES = {
     "irl_mvp_c128": (_I, [_P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P, _SZ, _P]),
     "irl_mvp_plan": (_I, [_I64, _I64, _I, _I, _P, _P]),
     "irl_lanczos_step_small": (_I, [_P, _I64, _P, _I64, _I, _I, _P, _P]),
+    "irl_lanczos_step_cluster": (_I, [_P, _I64, _P, _I64, _I, _I, _P, _P]),
     "irl_host_qr_sweeps": (_I, [_I, _P, _P, _P, _I]),
     "irl_otf_workspace_bytes": (_SZ, [_I64, _I, _I]),
     "irl_otf_prepare_mlp_f64": (_I, [_P, _I64, _I, _I, _P, _P, _P, _P, _P]),

@@ -1450,6 +1450,31 @@ int irl_lanczos_step_small(double* V, int64_t ldv, double* W, int64_t L, int j, 
   return cuda_check(cudaGetLastError(), "lanczos step launch");
 }
 
+int irl_lanczos_step_cluster(double* V, int64_t ldv, double* W, int64_t L, int j, int m, double* ab, void* stream) {
+  if (!V || !W || !ab || L < 1 || j < 0 || j >= m || j + 1 > LZ_MAXJ || ldv < L)
+    return fail(IRL_ERR_ARG, "bad lanczos step");
+  DevInfo d;
+  IRL_TRY(dev_info(d));
+  static std::once_flag once;  // static shared memory only; allow 16-CTA clusters
+  std::call_once(once, [] { cudaFuncSetAttribute((const void*)k_lanczos_cluster,
+                                                 cudaFuncAttributeNonPortableClusterSizeAllowed, 1); });
+  cudaGetLastError();
+  const int cs = (int)std::min<int64_t>(16, std::max<int64_t>(2, cdiv(L, 512)));
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(cs);
+  cfg.blockDim = dim3(512);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = (cudaStream_t)stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cuda_check(cudaLaunchKernelEx(&cfg, k_lanczos_cluster, V, ldv, W, L, j, m, ab), "lanczos cluster launch");
+}
+
 int irl_host_qr_sweeps(int m, double* T, double* Q, const double* shifts, int nshift) {
   if (m < 2 || !T || !Q || (nshift > 0 && !shifts)) return fail(IRL_ERR_ARG, "bad qr sweep arguments");
   // kry:165-190 per shift, same operation order (full rows / columns, t <- G^T t G, q <- q G)

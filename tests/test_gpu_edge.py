@@ -145,3 +145,46 @@ def test_abi_status_codes(cuda):
                            7, ws.data_ptr(), ws_bytes, st) == _lib.IRL_ERR_ARG
     assert b"bad mvp mode" in lib.irl_last_error()
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("L,j", [(866, 0), (866, 19), (6658, 7), (11282, 29), (60000, 39)])
+def test_lanczos_step_kernels(cuda, L, j):
+    """Fused Lanczos steps (single CTA, one cluster) == the BLAS-1/2 sequence
+    of kry:96-116 (alpha, three-term update, two reorthogonalisation passes,
+    beta, normalised next vector)."""
+    import torch
+    from paper_2601_01437_b200 import _lib
+
+    m = 41
+    gen = torch.Generator(device="cuda").manual_seed(L + j)
+    q, _ = torch.linalg.qr(torch.randn(L, j + 1, dtype=torch.float64, device="cuda", generator=gen))
+    V0 = torch.zeros((m + 1, L), dtype=torch.float64, device="cuda")
+    V0[: j + 1] = q.t()
+    W0 = torch.randn(L, dtype=torch.float64, device="cuda", generator=gen)
+    ab0 = torch.zeros((2, m), dtype=torch.float64, device="cuda")
+    if j > 0:
+        ab0[1, j - 1] = 0.37
+    # reference sequence (the driver's torch branch)
+    V, W, A = V0.clone(), W0.clone(), ab0.clone()
+    v = V[j]
+    a = torch.dot(v, W)
+    W -= a * v
+    if j > 0:
+        W -= A[1, j - 1] * V[j - 1]
+    vm = V[: j + 1]
+    for _ in range(2):
+        W -= vm.t() @ (vm @ W)
+    b = torch.linalg.vector_norm(W)
+    ref_v, ref_a, ref_b = (W / b), float(a), float(b)
+    kernels = ["irl_lanczos_step_cluster"] + (["irl_lanczos_step_small"] if L <= 4096 else [])
+    lib = _lib.lib()
+    for name in kernels:
+        V, W, A = V0.clone(), W0.clone(), ab0.clone()
+        _lib.check(name, getattr(lib, name)(V.data_ptr(), L, W.data_ptr(), L, j, m, A.data_ptr(),
+                                            _lib.stream_handle()))
+        torch.cuda.synchronize()
+        assert abs(float(A[0, j]) - ref_a) <= 1e-12 * max(1.0, abs(ref_a)), name
+        assert abs(float(A[1, j]) - ref_b) <= 1e-12 * ref_b, name
+        assert rel(V[j + 1].cpu().numpy(), ref_v.cpu().numpy()) < 1e-12, name
+        # rows 0..j untouched
+        assert torch.equal(V[: j + 1], V0[: j + 1]), name
