@@ -112,6 +112,15 @@ def _x_device(x, n_inputs: int, dev) -> torch.Tensor:
     return xt
 
 
+AUTO_OTF_MIN_BYTES = 256 << 20
+
+
+def otf_supported(arch) -> bool:
+    """On-the-fly kernels: n_inputs <= 100 packed bits per row; real models need
+    an even hidden width (16-byte tile rows)."""
+    return arch.n_inputs <= 100 and (bool(arch.complex_params) or arch.hidden % 2 == 0)
+
+
 def build_batch(params: AnsatzParameters, x, e_loc, weights=None, n_samples: int | None = None,
                 device=None, mode: str = "stored") -> SampleBatch:
     """Device SampleBatch with O built by the fused row kernel (K1/K2).
@@ -121,14 +130,22 @@ def build_batch(params: AnsatzParameters, x, e_loc, weights=None, n_samples: int
     GEMM) -> finisher.  ``weights`` defaults to 1/N (stochastic mode, est:99-100).
 
     ``mode``: "stored" materialises O in HBM; "otf" keeps only the hidden
-    activations and regenerates O inside every product (MLP only, see
-    :func:`build_batch_otf`); "auto" picks "otf" for the MLP (faster and ~10x
-    less memory on every BASELINE MLP shape) and "stored" otherwise.
+    activations and regenerates O inside every product (see
+    :func:`build_batch_otf`); "auto" picks "otf" whenever the model supports it
+    and the stored O would exceed ``AUTO_OTF_MIN_BYTES`` (measured on B200: the
+    DMMA regeneration beats streaming O from HBM 3.4x on cfg2, 3.6x on cfg3,
+    13x on cfg4, 12x on cfg5, while a small L2-resident O such as cfg1 streams
+    faster), and "stored" otherwise.
     """
     arch = params.architecture
     if mode not in ("stored", "otf", "auto"):
         raise ValueError(f"unknown build mode {mode!r}")
-    if mode == "otf" or (mode == "auto" and arch.model == _lib.MODEL_MLP and arch.n_inputs <= 100):
+    if mode == "auto" and otf_supported(arch):
+        n_rows = int(np.shape(x)[0]) if not isinstance(x, torch.Tensor) else int(x.shape[0])
+        o_bytes = n_rows * arch.param_count * (16 if arch.complex_params else 8)
+        if o_bytes >= AUTO_OTF_MIN_BYTES:
+            mode = "otf"
+    if mode == "otf":
         return build_batch_otf(params, x, e_loc, weights=weights, n_samples=n_samples, device=device)
     dev = _device(device)
     xt = _x_device(x, arch.n_inputs, dev)

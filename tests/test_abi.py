@@ -56,3 +56,14 @@ def test_errors_without_device_are_codes_not_crashes():
     rc = lib.irl_energy_f64(None, None, 0, None, None, None)
     assert rc == _lib.IRL_ERR_ARG
     assert b"bad energy" in lib.irl_last_error()
+
+
+def test_otf_support_rule():
+    """Which architectures the on-the-fly kernels take (ansatz.otf_supported)."""
+    from paper_2601_01437_b200 import ansatz as A
+
+    assert A.otf_supported(A.RBMArchitecture(40, 160))
+    assert A.otf_supported(A.RBMArchitecture(60, 481, complex_params=True))
+    assert not A.otf_supported(A.RBMArchitecture(40, 161))
+    assert not A.otf_supported(A.MLPArchitecture(101, 64))
+    assert A.otf_supported(A.MLPArchitecture(100, 2048))

@@ -398,3 +398,15 @@ def test_otf_hermitian_rbm_matches_stored(pkg, rows):
     assert r1.n_matvec == r2.n_matvec
     assert abs(r1.lambda_min - r2.lambda_min) <= RITZ_TOL * abs(r1.lambda_min)
     assert rel(host(r2.direction), host(r1.direction)) < DIR_TOL
+
+
+def test_auto_build_mode(pkg):
+    """mode="auto": stored O when it is small (cfg1), on-the-fly when O would be large."""
+    from paper_2601_01437_b200 import ansatz as A, synthetic as S
+
+    for idx, rows, want_otf in ((1, 8192, False), (4, 2048, True), (2, 4096, False)):
+        cfg = S.CONFIGS[idx].with_rows(rows)
+        inp = S.make_inputs(cfg)
+        arch = A.RBMArchitecture(cfg.n_inputs, cfg.hidden, cfg.complex_params)
+        b = A.build_batch(A.AnsatzParameters(arch, inp.theta), inp.x, inp.e_loc, mode="auto")
+        assert (b.otf is not None) == want_otf, idx
