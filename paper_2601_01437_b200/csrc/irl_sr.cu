@@ -10,6 +10,8 @@
 #include <unordered_map>
 #include <unordered_set>
 
+#include <cudaTypedefs.h>
+
 #include "../../include/irl_sr.h"
 #include "obuild.cuh"
 #include "otf.cuh"
@@ -527,7 +529,50 @@ int best_row_blocks(int slots, int jc, int64_t n) {
   return best;
 }
 
-using AccFn = void (*)(OtfArgs);
+using AccFn = void (*)(OtfArgs, CUtensorMap, CUtensorMap);
+
+// 2-D TMA descriptor of a row-major rows x cols f64 matrix, boxes of 64 rows x
+// 16 columns with the 128-byte swizzle (the acc GEMM tiles).  Cached per
+// (pointer, shape): encoding is host work on every product otherwise.
+int tile_map(CUtensorMap& m, const double* base, int64_t cols, int64_t rows) {
+  static std::once_flag once;
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  std::call_once(once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    cudaGetLastError();
+  });
+  if (!encode) return fail(IRL_ERR_DEVICE, "cuTensorMapEncodeTiled is unavailable");
+  struct Key {
+    const double* p;
+    int64_t c, r;
+  };
+  thread_local Key keys[16];
+  thread_local CUtensorMap maps[16];
+  thread_local int used = 0, next = 0;
+  for (int i = 0; i < used; ++i)
+    if (keys[i].p == base && keys[i].c == cols && keys[i].r == rows) {
+      m = maps[i];
+      return IRL_OK;
+    }
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || ((cols * 8) & 15))
+    return fail(IRL_ERR_ALIGN, "tile map needs 16-byte aligned rows");
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 8};
+  cuuint32_t box[2] = {16, (cuuint32_t)OTF_BM};
+  cuuint32_t es[2] = {1, 1};
+  const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, es,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(IRL_ERR_ARG, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  const int slot = used < 16 ? used++ : (next++ & 15);
+  keys[slot] = Key{base, cols, rows};
+  maps[slot] = m;
+  return IRL_OK;
+}
 
 AccFn pick_acc(int nkt, int nyv, bool has_t) {
 #define IRL_ACC(NK, NYV, HT) \
@@ -541,7 +586,7 @@ AccFn pick_acc(int nkt, int nyv, bool has_t) {
 
 size_t acc_smem(int nyv, bool has_t) {
   const size_t st = OTF_ACC_STAGES;
-  return (st * OTF_BM * OTF_BJ * (has_t ? 2 : 1) + st * OTF_BM * OTF_XW + (size_t)nyv * st * OTF_BM) * 8;
+  return 1024 + (st * OTF_TILE * (has_t ? 2 : 1) + st * OTF_BM * OTF_XW + (size_t)nyv * st * OTF_BM) * 8 + 2 * st * 8;
 }
 
 int make_otf_plan_uncached(int64_t n, int n_in, int hidden, OtfPlan& p) {
@@ -562,7 +607,7 @@ int make_otf_plan_uncached(int64_t n, int n_in, int hidden, OtfPlan& p) {
       if (!f) continue;
       IRL_TRY(ensure_fn_attrs((const void*)f, d.smem_optin));
       int occ = 0;
-      IRL_TRY(cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)f, 256, acc_smem(nyv, ht != 0)),
+      IRL_TRY(cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)f, 288, acc_smem(nyv, ht != 0)),
                          "occ"));
       p.nb_v[nyv - 1][ht] = best_row_blocks(d.sms * std::max(occ, 1), p.jc, n);
       p.nb = std::max(p.nb, p.nb_v[nyv - 1][ht]);
@@ -688,7 +733,13 @@ int otf_acc_launch(const OtfPlan& pl, OtfArgs& a, cudaStream_t st, int nyv, bool
   if (!f) return fail(IRL_ERR_DEVICE, "no acc GEMM instance for nkt=%d ny=%d", pl.nkt, nyv);
   a.nb = pl.nb_v[nyv - 1][has_t ? 1 : 0];
   dim3 grid((unsigned)pl.jc, (unsigned)a.nb);
-  f<<<grid, 256, acc_smem(nyv, has_t), st>>>(a);
+  CUtensorMap mg, mt;
+  IRL_TRY(tile_map(mg, a.G, a.hidden, a.n_rows));
+  if (has_t)
+    IRL_TRY(tile_map(mt, a.T, a.hidden, a.n_rows));
+  else
+    mt = mg;
+  f<<<grid, 288, acc_smem(nyv, has_t), st>>>(a, mg, mt);
   return cuda_check(cudaGetLastError(), "otf acc launch");
 }
 
@@ -735,7 +786,7 @@ struct OtfCPlan {
   size_t smem_dot, smem_acc;
 };
 
-using AccCFn = void (*)(OtfCArgs);
+using AccCFn = void (*)(OtfCArgs, CUtensorMap);
 
 AccCFn pick_acc_c(int nkt) {
   switch (nkt) {
@@ -756,14 +807,14 @@ int make_otfc_plan_uncached(int64_t n, int n_in, int hidden, OtfCPlan& p) {
   p.nkt = k8 <= 3 ? 3 : k8 <= 6 ? 6 : k8 <= 8 ? 8 : 13;
   p.kc = 8 * p.nkt;
   p.smem_dot = otf_dot_smem(n_in, false, true);
-  p.smem_acc = (size_t)OTF_ACC_STAGES * (OTF_BM * OTF_BJ * 8 + OTF_BM * OTF_XW * 8 + OTF_BM * 16);
+  p.smem_acc = 1024 + (size_t)OTF_ACC_STAGES * (OTF_TILE * 8 + OTF_BM * OTF_XW * 8 + OTF_BM * 16 + 16);
   AccCFn acc = pick_acc_c(p.nkt);
   IRL_TRY(ensure_fn_attrs((const void*)k_otf_dot_c, d.smem_optin));
   IRL_TRY(ensure_fn_attrs((const void*)acc, d.smem_optin));
   int occ_d = 1, occ_a = 1;
   IRL_TRY(cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_d, (const void*)k_otf_dot_c, 256, p.smem_dot),
                      "occ"));
-  IRL_TRY(cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_a, (const void*)acc, 256, p.smem_acc), "occ"));
+  IRL_TRY(cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_a, (const void*)acc, 288, p.smem_acc), "occ"));
   p.nb_dot = d.sms * std::max(occ_d, 1);  // persistent grid
   p.nb_acc = best_row_blocks(d.sms * std::max(occ_a, 1), p.jc, n);
   p.ny = d.sms;
@@ -844,7 +895,11 @@ int otfc_colsum(const OtfCPlan& pl, OtfCArgs a, const OtfCWs& wl, int64_t ld, co
   a.yr = yr;
   a.part = wl.part;
   a.nb = pl.nb_acc;
-  pick_acc_c(pl.nkt)<<<dim3((unsigned)pl.jc, (unsigned)pl.nb_acc), 256, pl.smem_acc, st>>>(a);
+  {
+    CUtensorMap mt;
+    IRL_TRY(tile_map(mt, a.T, 2LL * a.hidden, a.n_rows));
+    pick_acc_c(pl.nkt)<<<dim3((unsigned)pl.jc, (unsigned)pl.nb_acc), 288, pl.smem_acc, st>>>(a, mt);
+  }
   IRL_TRY(cuda_check(cudaGetLastError(), "otf acc (complex) launch"));
   k_xsum_c<<<pl.nbx, 128, 0, st>>>(a.xbits, y, yr, a.n_rows, a.n_in, wl.xpart);
   k_rbm_otf_finish_c<<<fin_grid(ld), dim3(32, 8), 0, st>>>(wl.part, pl.nb_acc, a.hidden, a.n_in, pl.kc, wl.xpart,
@@ -1435,7 +1490,11 @@ int irl_otf_mvp_rbm_c128(const uint64_t* xbits, const double* t, int64_t n, int 
   a.yr = nullptr;
   a.part = wl.part;
   a.nb = pl.nb_acc;
-  pick_acc_c(pl.nkt)<<<dim3((unsigned)pl.jc, (unsigned)pl.nb_acc), 256, pl.smem_acc, st>>>(a);
+  {
+    CUtensorMap mt;
+    IRL_TRY(tile_map(mt, a.T, 2LL * a.hidden, a.n_rows));
+    pick_acc_c(pl.nkt)<<<dim3((unsigned)pl.jc, (unsigned)pl.nb_acc), 288, pl.smem_acc, st>>>(a, mt);
+  }
   IRL_TRY(cuda_check(cudaGetLastError(), "otf acc (complex) launch"));
   k_xsum_c<<<pl.nbx, 128, 0, st>>>(xbits, wl.y, nullptr, n, n_vis, wl.xpart);
   k_rbm_otf_finish_c<<<fin_grid(ld), dim3(32, 8), 0, st>>>(wl.part, pl.nb_acc, hidden, n_vis, pl.kc, wl.xpart,

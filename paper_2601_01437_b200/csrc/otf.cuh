@@ -25,7 +25,7 @@ constexpr int OTF_BM = 64;   // rows per tile
 constexpr int OTF_KC = 104;  // k columns of the acc GEMM: n_in (<=100) + ones column, padded to 13 n-tiles
 constexpr int OTF_MAX_NIN = 100;
 constexpr int OTF_XW = 2;    // 64-bit words per packed input row (n_in <= 128)
-constexpr int OTF_ACC_STAGES = 3;  // cp.async stages of the acc GEMMs (one barrier per tile)
+constexpr int OTF_ACC_STAGES = 3;  // TMA ring stages of the acc GEMMs
 
 struct OtfArgs {
   const uint64_t* xbits;  // [N][OTF_XW]
@@ -294,49 +294,71 @@ __global__ void __launch_bounds__(256) k_otf_y(const double* __restrict__ tpart,
   }
 }
 
-// grid (JC, nb), 256 threads.  part[y][blk][j][kc] = sum_rows y g_j x_kc
-// (kc = n_in is the ones column), partu[y][blk][j] = sum y t_j (HAS_T).
-// NKT n-tiles of 8 k columns cover n_in + 1; NY weight vectors share one read
-// of the G/T tiles and the B fragments.  Warp w: hidden units j0 + 16 (w & 3)
-// + {0..7, 8..15} (two A fragments per B fragment: every 0/1 input fragment
-// built from the bits feeds two DMMAs) over the row quads kk = w >> 2, +2, ...;
-// the two row halves are summed through shared memory at the end.
+// Tiles of the acc GEMMs are 64 rows x 64 columns of doubles loaded by four
+// 2-D TMA boxes of 64 rows x 16 columns (128 bytes) with the 128-byte swizzle:
+// box b holds columns [16 b, 16 b + 16); row r's 16-byte chunk q sits at chunk
+// q ^ (r & 7).  Offset (in doubles) of element (r, c) of such a tile:
+__device__ __forceinline__ int swz64(int r, int c) {
+  return ((c >> 4) << 10) + (r << 4) + ((((c & 15) >> 1) ^ (r & 7)) << 1) + (c & 1);
+}
+constexpr int OTF_TILE = OTF_BM * OTF_BJ;  // doubles per swizzled tile (32 KB, 1024-byte aligned)
+
+// Dynamic shared memory, rounded up to the 1024-byte alignment the swizzle needs.
+__device__ __forceinline__ unsigned char* smem_1k(unsigned char* p) {
+  const uint32_t a = smem_addr(p);
+  return p + (((a + 1023u) & ~1023u) - a);
+}
+
+// grid (JC, nb), 288 threads = 8 consumer warps + 1 producer warp.
+// part[y][blk][j][kc] = sum_rows y g_j x_kc (kc = n_in is the ones column),
+// partu[y][blk][j] = sum y t_j (HAS_T).  NKT n-tiles of 8 k columns cover
+// n_in + 1; NY weight vectors share one read of the G/T tiles and the B
+// fragments.
+//
+// Pipeline: the producer warp fills an ST-stage ring (2-D TMA boxes of G/T,
+// a bulk copy of the packed bits and of y), completing on the stage's `full`
+// mbarrier; consumers release a stage through its `empty` mbarrier, so there
+// is no CTA-wide barrier in the main loop.
+//
+// Consumer warp w: hidden units j0 + 16 (w & 3) + {0..7, 8..15} (two A
+// fragments per B fragment: every 0/1 input fragment built from the bits
+// feeds two DMMAs) over the row quads kk = w >> 2, +2, ...; the two row halves
+// are summed through shared memory at the end.
 template <int NKT, int NY, bool HAS_T>
-__global__ void __launch_bounds__(256) k_otf_acc(const OtfArgs a) {
+__global__ void __launch_bounds__(288) __maxnreg__((NKT <= 8 && NY == 1 && !HAS_T) ? 96 : 168)
+    k_otf_acc(const OtfArgs a, const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmT) {
   extern __shared__ __align__(16) unsigned char smem_o[];
   constexpr int ST = OTF_ACC_STAGES;
-  double* gs = reinterpret_cast<double*>(smem_o);           // [ST][BM][BJ]
-  double* ts = gs + ST * OTF_BM * OTF_BJ;                    // [ST][BM][BJ] (HAS_T)
-  uint64_t* xs = reinterpret_cast<uint64_t*>(ts + (HAS_T ? ST * OTF_BM * OTF_BJ : 0));  // [ST][BM][XW]
-  double* ys = reinterpret_cast<double*>(xs + ST * OTF_BM * OTF_XW);     // [NY][ST][BM]
+  constexpr int NM = HAS_T ? 2 : 1;
   constexpr int KC = 8 * NKT;
+  double* tiles = reinterpret_cast<double*>(smem_1k(smem_o));                          // [ST][NM][TILE]
+  uint64_t* xs = reinterpret_cast<uint64_t*>(tiles + ST * NM * OTF_TILE);              // [ST][BM][XW]
+  double* ys = reinterpret_cast<double*>(xs + ST * OTF_BM * OTF_XW);                  // [ST][NY][BM]
+  uint64_t* full = reinterpret_cast<uint64_t*>(ys + ST * NY * OTF_BM);                // [ST]
+  uint64_t* empty = full + ST;                                                         // [ST]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wj = warp & 3, wk = warp >> 2;
   const int jc = blockIdx.x, j0 = jc * OTF_BJ;
   const int64_t N = a.n_rows;
-  const int64_t lo = (N * blockIdx.y) / a.nb, hi = (N * (blockIdx.y + 1)) / a.nb;
-  const int nin = a.n_in;
+  // row blocks start on even rows, so every tile's y slice is a 16-byte aligned bulk copy
+  const int64_t lo = ((N * blockIdx.y) / a.nb) & ~1LL;
+  const int64_t hi = blockIdx.y + 1 == (unsigned)a.nb ? N : ((N * (blockIdx.y + 1)) / a.nb) & ~1LL;
+  const int nin = a.n_in, h = a.hidden;
+  const int nbox = min(4, (h - j0 + 15) >> 4);  // boxes of this chunk inside [0, h)
   const int ntiles = (int)((hi - lo + OTF_BM - 1) / OTF_BM);
-  const double* yv_src[2] = {a.y, a.y2};
 
-  auto load_y = [&](int64_t r0, int buf) {
-    for (int e = tid; e < NY * OTF_BM; e += blockDim.x) {
-      const int q = e / OTF_BM, r = e % OTF_BM;
-      ys[(q * ST + buf) * OTF_BM + r] = (r0 + r < hi) ? yv_src[q][r0 + r] : 0.0;
+  // zero every stage once: boxes past h are never loaded and rows past the
+  // block keep finite data (their y is zero)
+  for (int e = tid; e < ST * NM * OTF_TILE; e += blockDim.x) tiles[e] = 0.0;
+  for (int e = tid; e < ST * OTF_BM * OTF_XW; e += blockDim.x) xs[e] = 0ull;
+  if (tid == 0) {
+    for (int q = 0; q < ST; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], 8);
     }
-  };
-  auto load_stage = [&](int it) {  // tile it -> stage it % ST
-    const int b = it % ST;
-    const int64_t r0 = lo + (int64_t)it * OTF_BM;
-    otf_load_tile(a, r0, hi, j0, gs + b * OTF_BM * OTF_BJ, HAS_T ? ts + b * OTF_BM * OTF_BJ : nullptr,
-                  xs + b * OTF_BM * OTF_XW, tid, blockDim.x);
-    load_y(r0, b);
-  };
-  for (int it = 0; it < ST - 1; ++it) {  // prologue: ST - 1 tiles in flight
-    if (it < ntiles) load_stage(it);
-    cp_async_commit();
+    fence_mbar_init();
   }
+  __syncthreads();
 
   double c[NY][2][NKT][2];
   double cu[NY][2][2];
@@ -348,63 +370,93 @@ __global__ void __launch_bounds__(256) k_otf_acc(const OtfArgs a) {
 #pragma unroll
       for (int nt = 0; nt < NKT; ++nt) c[q][f][nt][0] = c[q][f][nt][1] = 0.0;
     }
+  const int wj = warp & 3, wk = (warp >> 2) & 1;
   const int jl = wj * 16 + (lane >> 2);  // A rows jl, jl + 8 (hidden units) of this lane
-  const int sh_base = lane >> 2;         // B column offset within an n-tile
-  const double one_b = (lane >> 2) == 0 ? 1.0 : 0.0;
-  // the ones column (k = n_in) is bit n_in of every packed row
-  const uint64_t one0 = nin < 64 ? (1ull << nin) : 0ull, one1 = nin >= 64 ? (1ull << (nin - 64)) : 0ull;
 
-  // one barrier per tile: after it, tile it is visible and every warp is done
-  // with tile it - 1, whose stage the load of tile it + ST - 1 reuses
-  for (int it = 0; it < ntiles; ++it) {
-    const int buf = it % ST;
-    cp_async_wait<ST - 2>();
-    __syncthreads();
-    if (it + ST - 1 < ntiles) load_stage(it + ST - 1);
-    cp_async_commit();
-    const double* G = gs + buf * OTF_BM * OTF_BJ;
-    const double* Tt = ts + buf * OTF_BM * OTF_BJ;
-    const uint64_t* X = xs + buf * OTF_BM * OTF_XW;
+  if (warp == 8) {  // ---------------------------------------------- producer
+    const double* yv_src[2] = {a.y, a.y2};
+    for (int it = 0; it < ntiles; ++it) {
+      const int st = it % ST;
+      const uint32_t ph = (uint32_t)(it / ST) & 1u;
+      if (it >= ST) mbar_wait(&empty[st], ph ^ 1u);
+      const int64_t r0 = lo + (int64_t)it * OTF_BM;
+      const int nrows = (int)min((int64_t)OTF_BM, hi - r0);
+      // y: bulk copy of the even part; an odd last row (N odd) and the tail by plain stores
+      const int nev = nrows & ~1;
+      if (nrows < OTF_BM) {
+        for (int e = lane; e < NY * OTF_BM; e += 32) {
+          const int q = e / OTF_BM, r = e % OTF_BM;
+          if (r >= nev) ys[(st * NY + q) * OTF_BM + r] = r < nrows ? yv_src[q][r0 + r] : 0.0;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive_expect_tx(&full[st], (uint32_t)(nbox * NM * OTF_BM * 128) + (uint32_t)nrows * OTF_XW * 8u +
+                                             (uint32_t)(NY * nev * 8));
+        double* tg = tiles + (st * NM) * OTF_TILE;
+        for (int b = 0; b < nbox; ++b) {
+          tma_load_2d(tg + b * 1024, &tmG, j0 + 16 * b, (int)r0, &full[st]);
+          if (HAS_T) tma_load_2d(tg + OTF_TILE + b * 1024, &tmT, j0 + 16 * b, (int)r0, &full[st]);
+        }
+        bulk_g2s(xs + st * OTF_BM * OTF_XW, a.xbits + r0 * OTF_XW, (uint32_t)nrows * OTF_XW * 8u, &full[st]);
+      }
+      if (lane < NY && nev > 0) bulk_g2s(ys + (st * NY + lane) * OTF_BM, yv_src[lane] + r0, (uint32_t)nev * 8u, &full[st]);
+    }
+  } else {  // ---------------------------------------------------- consumers
+    const int sh_base = lane >> 2;  // B column offset within an n-tile
+    const double one_b = (lane >> 2) == 0 ? 1.0 : 0.0;
+    // the ones column (k = n_in) is bit n_in of every packed row
+    const uint64_t one0 = nin < 64 ? (1ull << nin) : 0ull, one1 = nin >= 64 ? (1ull << (nin - 64)) : 0ull;
+    for (int it = 0; it < ntiles; ++it) {
+      const int st = it % ST;
+      mbar_wait(&full[st], (uint32_t)(it / ST) & 1u);
+      const double* G = tiles + (st * NM) * OTF_TILE;
+      const double* Tt = G + OTF_TILE;
+      const uint64_t* X = xs + st * OTF_BM * OTF_XW;
+      const double* Y = ys + st * NY * OTF_BM;
 #pragma unroll 2
-    for (int kk = wk; kk < OTF_BM / 4; kk += 2) {
-      const int rl = kk * 4 + (lane & 3);
-      const double g0 = G[rl * OTF_BJ + jl], g1 = G[rl * OTF_BJ + jl + 8];
-      double t0 = 0.0, t1 = 0.0;
-      if (HAS_T) {
-        t0 = Tt[rl * OTF_BJ + jl];
-        t1 = Tt[rl * OTF_BJ + jl + 8];
-      }
-      const uint64_t w0 = (X[rl * OTF_XW] | one0) >> sh_base, w1 = (X[rl * OTF_XW + 1] | one1) >> sh_base;
-      double bv[NKT];
-#pragma unroll
-      for (int nt = 0; nt < NKT; ++nt) {
-        const uint32_t bit = nt < 8 ? (uint32_t)(w0 >> (nt * 8)) & 1u : (uint32_t)(w1 >> ((nt - 8) * 8)) & 1u;
-        bv[nt] = bit_to_double(bit);
-      }
-#pragma unroll
-      for (int q = 0; q < NY; ++q) {
-        const double yq = ys[(q * ST + buf) * OTF_BM + rl];
-        const double a0 = g0 * yq, a1 = g1 * yq;
+      for (int kk = wk; kk < OTF_BM / 4; kk += 2) {
+        const int rl = kk * 4 + (lane & 3);
+        const int o0 = swz64(rl, jl), o1 = swz64(rl, jl + 8);
+        const double g0 = G[o0], g1 = G[o1];
+        double t0 = 0.0, t1 = 0.0;
+        if (HAS_T) {
+          t0 = Tt[o0];
+          t1 = Tt[o1];
+        }
+        const uint64_t w0 = (X[rl * OTF_XW] | one0) >> sh_base, w1 = (X[rl * OTF_XW + 1] | one1) >> sh_base;
+        double bv[NKT];
 #pragma unroll
         for (int nt = 0; nt < NKT; ++nt) {
-          dmma(c[q][0][nt][0], c[q][0][nt][1], a0, bv[nt]);
-          dmma(c[q][1][nt][0], c[q][1][nt][1], a1, bv[nt]);
+          const uint32_t bit = nt < 8 ? (uint32_t)(w0 >> (nt * 8)) & 1u : (uint32_t)(w1 >> ((nt - 8) * 8)) & 1u;
+          bv[nt] = bit_to_double(bit);
         }
-        if (HAS_T) {
-          dmma(cu[q][0][0], cu[q][0][1], t0 * yq, one_b);
-          dmma(cu[q][1][0], cu[q][1][1], t1 * yq, one_b);
+#pragma unroll
+        for (int q = 0; q < NY; ++q) {
+          const double yq = Y[q * OTF_BM + rl];
+          const double a0 = g0 * yq, a1 = g1 * yq;
+#pragma unroll
+          for (int nt = 0; nt < NKT; ++nt) {
+            dmma(c[q][0][nt][0], c[q][0][nt][1], a0, bv[nt]);
+            dmma(c[q][1][nt][0], c[q][1][nt][1], a1, bv[nt]);
+          }
+          if (HAS_T) {
+            dmma(cu[q][0][0], cu[q][0][1], t0 * yq, one_b);
+            dmma(cu[q][1][0], cu[q][1][1], t1 * yq, one_b);
+          }
         }
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
     }
   }
-  cp_async_wait<0>();
-  __syncthreads();  // the exchange below reuses the stage buffers
-  // row halves: warps 4..7 hand their fragments to warps 0..3 (tile buffers are free now)
+  __syncthreads();  // every stage consumed and every copy landed: the tiles are free
+  // row halves: warps 4..7 hand their fragments to warps 0..3
   constexpr int NV = NY * 2 * (NKT + (HAS_T ? 1 : 0)) * 2;
-  static_assert(NV <= OTF_ACC_STAGES * OTF_BJ, "exchange must fit the G tile buffers");
-  double* xch = gs;  // [NV][128]
+  static_assert(NV * 128 <= ST * NM * OTF_TILE, "exchange must fit the tile buffers");
+  double* xch = tiles;  // [NV][128]
   const int xl = wj * 32 + lane;
-  if (wk == 1) {
+  if (warp >= 4 && warp < 8) {
     int v = 0;
 #pragma unroll
     for (int q = 0; q < NY; ++q)
@@ -422,7 +474,7 @@ __global__ void __launch_bounds__(256) k_otf_acc(const OtfArgs a) {
       }
   }
   __syncthreads();
-  if (wk == 1) return;
+  if (warp >= 4) return;
   {
     int v = 0;
 #pragma unroll
@@ -439,23 +491,22 @@ __global__ void __launch_bounds__(256) k_otf_acc(const OtfArgs a) {
           cu[q][f][1] += xch[(v++) * 128 + xl];
         }
       }
-    (void)NV;
   }
   // partials: C[j][kc] fragment -> part[q][blk][j][kc]
 #pragma unroll
   for (int f = 0; f < 2; ++f) {
     const int jrow = j0 + jl + 8 * f;
-    if (jrow >= a.hidden) continue;
+    if (jrow >= h) continue;
 #pragma unroll
     for (int q = 0; q < NY; ++q) {
-      double* pb = a.part + (((int64_t)q * a.nb + blockIdx.y) * a.hidden + jrow) * KC;
+      double* pb = a.part + (((int64_t)q * a.nb + blockIdx.y) * h + jrow) * KC;
 #pragma unroll
       for (int nt = 0; nt < NKT; ++nt) {
         const int kc = nt * 8 + (lane & 3) * 2;
         pb[kc] = c[q][f][nt][0];
         pb[kc + 1] = c[q][f][nt][1];
       }
-      if (HAS_T && (lane & 3) == 0) a.partu[((int64_t)q * a.nb + blockIdx.y) * a.hidden + jrow] = cu[q][f][0];
+      if (HAS_T && (lane & 3) == 0) a.partu[((int64_t)q * a.nb + blockIdx.y) * h + jrow] = cu[q][f][0];
     }
   }
 }
@@ -1058,81 +1109,107 @@ __global__ void __launch_bounds__(256) k_otf_y_c(const double2* __restrict__ tpa
 }
 
 // part[blk][2j+p][kc] = sum_rows (conj(T_nj) y_n)_p x_n,kc  (kc = n_in: ones column).
-// Same warp layout as k_otf_acc: two A fragments (real rows jl, jl + 8) per
-// B fragment, row quads split over the two warp halves.
+// Same structure as k_otf_acc (producer warp, 2-D swizzled TMA tiles of the
+// real N x 2h view of T, two A fragments per B fragment, row quads split over
+// two warp halves).
+// 9 warps per CTA: two resident CTAs put up to 5 warps on one SM sub-partition,
+// whose 16K-register slice then allows at most 96 registers per thread.
 template <int NKT>
-__global__ void __launch_bounds__(256) k_otf_acc_c(const OtfCArgs a) {
+__global__ void __launch_bounds__(288) __maxnreg__(NKT <= 8 ? 96 : 168)
+    k_otf_acc_c(const OtfCArgs a, const __grid_constant__ CUtensorMap tmT) {
   extern __shared__ __align__(16) unsigned char smem_c[];
   constexpr int ST = OTF_ACC_STAGES;
-  double* gs = reinterpret_cast<double*>(smem_c);                         // [ST][BM][64]
-  uint64_t* xs = reinterpret_cast<uint64_t*>(gs + ST * OTF_BM * OTF_BJ);  // [ST][BM][XW]
-  double2* ys = reinterpret_cast<double2*>(xs + ST * OTF_BM * OTF_XW);    // [ST][BM]
   constexpr int KC = 8 * NKT;
+  double* tiles = reinterpret_cast<double*>(smem_1k(smem_c));              // [ST][TILE]
+  uint64_t* xs = reinterpret_cast<uint64_t*>(tiles + ST * OTF_TILE);       // [ST][BM][XW]
+  double2* ys = reinterpret_cast<double2*>(xs + ST * OTF_BM * OTF_XW);     // [ST][BM]
+  uint64_t* full = reinterpret_cast<uint64_t*>(ys + ST * OTF_BM);          // [ST]
+  uint64_t* empty = full + ST;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wj = warp & 3, wk = warp >> 2;
   const int c0 = blockIdx.x * OTF_BJ;
   const int64_t N = a.n_rows;
   const int64_t lo = (N * blockIdx.y) / a.nb, hi = (N * (blockIdx.y + 1)) / a.nb;
   const int nin = a.n_in, ncols = 2 * a.hidden;
+  const int nbox = min(4, (ncols - c0 + 15) >> 4);
   const int ntiles = (int)((hi - lo + OTF_BM - 1) / OTF_BM);
-  auto load_y = [&](int64_t r0, int buf) {
-    for (int e = tid; e < OTF_BM; e += blockDim.x)
-      ys[buf * OTF_BM + e] = (r0 + e >= hi) ? make_double2(0.0, 0.0)
-                             : a.y ? a.y[r0 + e] : make_double2(a.yr[r0 + e], 0.0);
-  };
-  auto load_stage = [&](int it) {
-    const int b = it % ST;
-    const int64_t r0 = lo + (int64_t)it * OTF_BM;
-    otf_load_ctile(a, r0, hi, c0, gs + b * OTF_BM * OTF_BJ, xs + b * OTF_BM * OTF_XW, tid, blockDim.x);
-    load_y(r0, b);
-  };
-  for (int it = 0; it < ST - 1; ++it) {
-    if (it < ntiles) load_stage(it);
-    cp_async_commit();
+  for (int e = tid; e < ST * OTF_TILE; e += blockDim.x) tiles[e] = 0.0;
+  for (int e = tid; e < ST * OTF_BM * OTF_XW; e += blockDim.x) xs[e] = 0ull;
+  if (tid == 0) {
+    for (int q = 0; q < ST; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], 8);
+    }
+    fence_mbar_init();
   }
+  __syncthreads();
   double c[2][NKT][2];
 #pragma unroll
   for (int f = 0; f < 2; ++f)
 #pragma unroll
     for (int nt = 0; nt < NKT; ++nt) c[f][nt][0] = c[f][nt][1] = 0.0;
+  const int wj = warp & 3, wk = (warp >> 2) & 1;
   const int jl = wj * 16 + (lane >> 2);  // real rows (2j + p) jl and jl + 8 within the chunk
-  const int pj = jl & 1, jb = jl & ~1;
-  const int sh_base = lane >> 2;
-  const uint64_t one0 = nin < 64 ? (1ull << nin) : 0ull, one1 = nin >= 64 ? (1ull << (nin - 64)) : 0ull;
-  for (int it = 0; it < ntiles; ++it) {
-    const int buf = it % ST;
-    cp_async_wait<ST - 2>();
-    __syncthreads();
-    if (it + ST - 1 < ntiles) load_stage(it + ST - 1);
-    cp_async_commit();
-    const double* G = gs + buf * OTF_BM * OTF_BJ;
-    const uint64_t* X = xs + buf * OTF_BM * OTF_XW;
-#pragma unroll 2
-    for (int kk = wk; kk < OTF_BM / 4; kk += 2) {
-      const int rl = kk * 4 + (lane & 3);
-      const double2 ta = *reinterpret_cast<const double2*>(G + rl * OTF_BJ + jb);
-      const double2 tb = *reinterpret_cast<const double2*>(G + rl * OTF_BJ + jb + 8);
-      const double2 yv = ys[buf * OTF_BM + rl];
-      // conj(t) y = (t.x y.x + t.y y.y) + i (t.x y.y - t.y y.x)
-      const double a0 = pj ? fma(ta.x, yv.y, -ta.y * yv.x) : fma(ta.x, yv.x, ta.y * yv.y);
-      const double a1 = pj ? fma(tb.x, yv.y, -tb.y * yv.x) : fma(tb.x, yv.x, tb.y * yv.y);
-      const uint64_t w0 = (X[rl * OTF_XW] | one0) >> sh_base, w1 = (X[rl * OTF_XW + 1] | one1) >> sh_base;
-#pragma unroll
-      for (int nt = 0; nt < NKT; ++nt) {
-        const uint32_t bit = nt < 8 ? (uint32_t)(w0 >> (nt * 8)) & 1u : (uint32_t)(w1 >> ((nt - 8) * 8)) & 1u;
-        const double bv = bit_to_double(bit);
-        dmma(c[0][nt][0], c[0][nt][1], a0, bv);
-        dmma(c[1][nt][0], c[1][nt][1], a1, bv);
+
+  if (warp == 8) {  // producer
+    for (int it = 0; it < ntiles; ++it) {
+      const int st = it % ST;
+      const uint32_t ph = (uint32_t)(it / ST) & 1u;
+      if (it >= ST) mbar_wait(&empty[st], ph ^ 1u);
+      const int64_t r0 = lo + (int64_t)it * OTF_BM;
+      const int nrows = (int)min((int64_t)OTF_BM, hi - r0);
+      if (!a.y || nrows < OTF_BM)
+        for (int r = lane; r < OTF_BM; r += 32)
+          ys[st * OTF_BM + r] = r >= nrows ? make_double2(0.0, 0.0)
+                                : a.y ? a.y[r0 + r] : make_double2(a.yr[r0 + r], 0.0);
+      __syncwarp();
+      if (lane == 0) {
+        const bool ybulk = a.y && nrows == OTF_BM;
+        mbar_arrive_expect_tx(&full[st], (uint32_t)(nbox * OTF_BM * 128) + (uint32_t)nrows * OTF_XW * 8u +
+                                             (ybulk ? OTF_BM * 16u : 0u));
+        for (int b = 0; b < nbox; ++b)
+          tma_load_2d(tiles + st * OTF_TILE + b * 1024, &tmT, c0 + 16 * b, (int)r0, &full[st]);
+        bulk_g2s(xs + st * OTF_BM * OTF_XW, a.xbits + r0 * OTF_XW, (uint32_t)nrows * OTF_XW * 8u, &full[st]);
+        if (ybulk) bulk_g2s(ys + st * OTF_BM, a.y + r0, OTF_BM * 16u, &full[st]);
       }
     }
+  } else {  // consumers
+    const int pj = jl & 1, jb = jl & ~1;
+    const int sh_base = lane >> 2;
+    const uint64_t one0 = nin < 64 ? (1ull << nin) : 0ull, one1 = nin >= 64 ? (1ull << (nin - 64)) : 0ull;
+    for (int it = 0; it < ntiles; ++it) {
+      const int st = it % ST;
+      mbar_wait(&full[st], (uint32_t)(it / ST) & 1u);
+      const double* G = tiles + st * OTF_TILE;
+      const uint64_t* X = xs + st * OTF_BM * OTF_XW;
+      const double2* Y = ys + st * OTF_BM;
+#pragma unroll 2
+      for (int kk = wk; kk < OTF_BM / 4; kk += 2) {
+        const int rl = kk * 4 + (lane & 3);
+        const double2 ta = *reinterpret_cast<const double2*>(G + swz64(rl, jb));
+        const double2 tb = *reinterpret_cast<const double2*>(G + swz64(rl, jb + 8));
+        const double2 yv = Y[rl];
+        // conj(t) y = (t.x y.x + t.y y.y) + i (t.x y.y - t.y y.x)
+        const double a0 = pj ? fma(ta.x, yv.y, -ta.y * yv.x) : fma(ta.x, yv.x, ta.y * yv.y);
+        const double a1 = pj ? fma(tb.x, yv.y, -tb.y * yv.x) : fma(tb.x, yv.x, tb.y * yv.y);
+        const uint64_t w0 = (X[rl * OTF_XW] | one0) >> sh_base, w1 = (X[rl * OTF_XW + 1] | one1) >> sh_base;
+#pragma unroll
+        for (int nt = 0; nt < NKT; ++nt) {
+          const uint32_t bit = nt < 8 ? (uint32_t)(w0 >> (nt * 8)) & 1u : (uint32_t)(w1 >> ((nt - 8) * 8)) & 1u;
+          const double bv = bit_to_double(bit);
+          dmma(c[0][nt][0], c[0][nt][1], a0, bv);
+          dmma(c[1][nt][0], c[1][nt][1], a1, bv);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
   }
-  cp_async_wait<0>();
   __syncthreads();
   constexpr int NV = 2 * NKT * 2;
-  static_assert(NV <= OTF_ACC_STAGES * OTF_BJ, "exchange must fit the tile buffers");
-  double* xch = gs;  // [NV][128]
+  static_assert(NV * 128 <= ST * OTF_TILE, "exchange must fit the tile buffers");
+  double* xch = tiles;  // [NV][128]
   const int xl = wj * 32 + lane;
-  if (wk == 1) {
+  if (warp >= 4 && warp < 8) {
 #pragma unroll
     for (int f = 0; f < 2; ++f)
 #pragma unroll
@@ -1142,7 +1219,7 @@ __global__ void __launch_bounds__(256) k_otf_acc_c(const OtfCArgs a) {
       }
   }
   __syncthreads();
-  if (wk == 1) return;
+  if (warp >= 4) return;
 #pragma unroll
   for (int f = 0; f < 2; ++f) {
     const int col = c0 + jl + 8 * f;
