@@ -684,9 +684,10 @@ int otf_check(const uint64_t* xbits, const double* t, const double* g, int64_t n
 
 size_t otf_dot_smem(int n_in, bool has_t, bool cplx) {
   const int vs = otf_vstride(n_in);
-  const size_t tiles = (size_t)2 * OTF_BM * OTF_BJ * (has_t ? 2 : 1);
-  const size_t red = (size_t)4 * OTF_BM * (cplx ? 2 : 1);
-  return ((size_t)OTF_BJ * vs + OTF_BJ * (has_t ? 2 : 1) + tiles + red) * 8 + (size_t)2 * OTF_BM * OTF_XW * 8;
+  const size_t st = OTF_DOT_STAGES;
+  const size_t tiles = st * OTF_TILE * (has_t ? 2 : 1);
+  const size_t red = (size_t)2 * 4 * OTF_BM * (cplx ? 2 : 1);
+  return 1024 + (tiles + st * OTF_BM * OTF_XW + red + 2 * st + OTF_BJ * 2 + (size_t)OTF_BJ * vs) * 8;
 }
 
 // persistent grid of the dot kernels: every resident CTA slot, occupancy cached per (kernel, n_in)
@@ -708,7 +709,7 @@ int otf_dot_grid(const void* fn, size_t smem, int key, int& grid) {
   }
   IRL_TRY(ensure_fn_attrs(fn, d.smem_optin));
   int occ = 0;
-  IRL_TRY(cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, smem), "occ"));
+  IRL_TRY(cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 288, smem), "occ"));
   grid = d.sms * std::max(occ, 1);
   std::lock_guard<std::mutex> lk(mu);
   cache[k] = grid;
@@ -720,10 +721,16 @@ int otf_dot_launch(OtfArgs& a, bool has_t, cudaStream_t st) {
   const size_t smem = otf_dot_smem(a.n_in, has_t, false);
   int grid = 0;
   IRL_TRY(otf_dot_grid(fn, smem, (a.n_in << 2) | (has_t ? 1 : 0), grid));
+  CUtensorMap mg, mt;
+  IRL_TRY(tile_map(mg, a.G, a.hidden, a.n_rows));
   if (has_t)
-    k_otf_dot<true><<<grid, 256, smem, st>>>(a);
+    IRL_TRY(tile_map(mt, a.T, a.hidden, a.n_rows));
   else
-    k_otf_dot<false><<<grid, 256, smem, st>>>(a);
+    mt = mg;
+  if (has_t)
+    k_otf_dot<true><<<grid, 288, smem, st>>>(a, mg, mt);
+  else
+    k_otf_dot<false><<<grid, 288, smem, st>>>(a, mg, mt);
   return cuda_check(cudaGetLastError(), "otf dot launch");
 }
 
@@ -812,7 +819,7 @@ int make_otfc_plan_uncached(int64_t n, int n_in, int hidden, OtfCPlan& p) {
   IRL_TRY(ensure_fn_attrs((const void*)k_otf_dot_c, d.smem_optin));
   IRL_TRY(ensure_fn_attrs((const void*)acc, d.smem_optin));
   int occ_d = 1, occ_a = 1;
-  IRL_TRY(cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_d, (const void*)k_otf_dot_c, 256, p.smem_dot),
+  IRL_TRY(cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_d, (const void*)k_otf_dot_c, 288, p.smem_dot),
                      "occ"));
   IRL_TRY(cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_a, (const void*)acc, 288, p.smem_acc), "occ"));
   p.nb_dot = d.sms * std::max(occ_d, 1);  // persistent grid
@@ -1482,7 +1489,11 @@ int irl_otf_mvp_rbm_c128(const uint64_t* xbits, const double* t, int64_t n, int 
   a.v_re = v_re;
   a.v_im = v_im;
   a.tpart = wl.tpart;
-  k_otf_dot_c<<<pl.nb_dot, 256, pl.smem_dot, st>>>(a);
+  {
+    CUtensorMap mt;
+    IRL_TRY(tile_map(mt, t, 2LL * hidden, n));
+    k_otf_dot_c<<<pl.nb_dot, 288, pl.smem_dot, st>>>(a, mt);
+  }
   IRL_TRY(cuda_check(cudaGetLastError(), "otf dot (complex) launch"));
   k_otf_y_c<<<pl.ny, 256, 0, st>>>(wl.tpart, pl.jc, n, reinterpret_cast<const double2*>(coeff), v_re, v_im, 0, n_vis,
                                    xbits, wl.dpart, obar ? pl.ny : 0, wl.y, wl.ypart);

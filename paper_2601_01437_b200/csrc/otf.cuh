@@ -26,6 +26,7 @@ constexpr int OTF_KC = 104;  // k columns of the acc GEMM: n_in (<=100) + ones c
 constexpr int OTF_MAX_NIN = 100;
 constexpr int OTF_XW = 2;    // 64-bit words per packed input row (n_in <= 128)
 constexpr int OTF_ACC_STAGES = 3;  // TMA ring stages of the acc GEMMs
+constexpr int OTF_DOT_STAGES = 2;  // TMA ring stages of the dot GEMMs (v_W also lives in shared memory)
 
 struct OtfArgs {
   const uint64_t* xbits;  // [N][OTF_XW]
@@ -97,6 +98,21 @@ __device__ __forceinline__ void otf_load_tile(const OtfArgs& a, int64_t r0, int6
   }
 }
 
+// Tiles of the OTF GEMMs are 64 rows x 64 columns of doubles loaded by four
+// 2-D TMA boxes of 64 rows x 16 columns (128 bytes) with the 128-byte swizzle:
+// box b holds columns [16 b, 16 b + 16); row r's 16-byte chunk q sits at chunk
+// q ^ (r & 7).  Offset (in doubles) of element (r, c) of such a tile:
+__device__ __forceinline__ int swz64(int r, int c) {
+  return ((c >> 4) << 10) + (r << 4) + ((((c & 15) >> 1) ^ (r & 7)) << 1) + (c & 1);
+}
+constexpr int OTF_TILE = OTF_BM * OTF_BJ;  // doubles per swizzled tile (32 KB, 1024-byte aligned)
+
+// Dynamic shared memory, rounded up to the 1024-byte alignment the swizzle needs.
+__device__ __forceinline__ unsigned char* smem_1k(unsigned char* p) {
+  const uint32_t a = smem_addr(p);
+  return p + (((a + 1023u) & ~1023u) - a);
+}
+
 // Row stride (doubles) of the v_W chunk in shared memory: >= n_in, a multiple
 // of 4 and == 4 (mod 16), so the B-fragment loads (8 rows x 4 k per half warp
 // pair) hit 16 distinct 8-byte bank pairs.
@@ -114,70 +130,98 @@ __device__ __forceinline__ void otf_cta_range(int64_t total, int64_t& t0, int64_
   t1 = (total * (blockIdx.x + 1)) / gridDim.x;
 }
 
-// grid (persistent, 1-D), 256 threads: t partials (tpart[jc][row]) for every
-// (hidden chunk, 64-row tile) of this CTA's range.  8 warps = 2 (32 rows) x 4
-// (16 hidden units).  HAS_T: MLP (G tile for X V_W^T, T tile for v_u);
-// RBM: G == T, G-only tiles, no u block.
+// grid (persistent, 1-D), 288 threads = 8 consumer warps + 1 producer warp:
+// t partials (tpart[jc][row]) for every (hidden chunk, 64-row tile) of this
+// CTA's range.  Consumers: 2 (32 rows) x 4 (16 hidden units).  HAS_T: MLP
+// (G tile for X V_W^T, T tile for v_u); RBM: G == T, G-only tiles, no u block.
+// The producer streams the G/T tiles (2-D swizzled TMA boxes) and the packed
+// bits through a 2-stage mbarrier ring; the per-row cross-warp sums use a
+// double-buffered exchange and one named barrier of the consumers per tile.
 template <bool HAS_T>
-__global__ void __launch_bounds__(256) k_otf_dot(const OtfArgs a) {
+__global__ void __maxnreg__(HAS_T ? 224 : 96)
+    k_otf_dot(const OtfArgs a, const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmT) {
   extern __shared__ __align__(16) unsigned char smem_o[];
+  constexpr int ST = OTF_DOT_STAGES;
+  constexpr int NM = HAS_T ? 2 : 1;
   const int nin = a.n_in, vs = otf_vstride(nin);
-  double* vw = reinterpret_cast<double*>(smem_o);            // [BJ][vs]
-  double* vb = vw + OTF_BJ * vs;                             // [BJ]
-  double* vu = vb + OTF_BJ;                                  // [BJ] (HAS_T)
-  double* gs = vu + (HAS_T ? OTF_BJ : 0);                    // [2][BM][BJ]
-  double* ts = gs + 2 * OTF_BM * OTF_BJ;                     // [2][BM][BJ] (HAS_T)
-  uint64_t* xs = reinterpret_cast<uint64_t*>(ts + (HAS_T ? 2 * OTF_BM * OTF_BJ : 0));  // [2][BM][XW]
-  double* red = reinterpret_cast<double*>(xs + 2 * OTF_BM * OTF_XW);                   // [4][BM]
+  double* tiles = reinterpret_cast<double*>(smem_1k(smem_o));              // [ST][NM][TILE]
+  uint64_t* xs = reinterpret_cast<uint64_t*>(tiles + ST * NM * OTF_TILE);  // [ST][BM][XW]
+  double* red = reinterpret_cast<double*>(xs + ST * OTF_BM * OTF_XW);      // [2][4][BM]
+  uint64_t* full = reinterpret_cast<uint64_t*>(red + 2 * 4 * OTF_BM);      // [ST]
+  uint64_t* empty = full + ST;                                             // [ST]
+  double* vb = reinterpret_cast<double*>(empty + ST);                      // [BJ]
+  double* vu = vb + OTF_BJ;                                                // [BJ]
+  double* vw = vu + OTF_BJ;                                                // [BJ][vs]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wr = warp >> 2, wj = warp & 3;  // rows [wr*32, +32), j [wj*16, +16)
   const int64_t N = a.n_rows;
   const int64_t ntiles = (N + OTF_BM - 1) / OTF_BM;
-  const int jcount = (a.hidden + OTF_BJ - 1) / OTF_BJ;
+  const int h = a.hidden;
+  const int jcount = (h + OTF_BJ - 1) / OTF_BJ;
   int64_t t0, t1;
   otf_cta_range(ntiles * jcount, t0, t1);
   if (t0 >= t1) return;
-  const int h = a.hidden;
+  for (int e = tid; e < ST * NM * OTF_TILE; e += blockDim.x) tiles[e] = 0.0;
+  for (int e = tid; e < ST * OTF_BM * OTF_XW; e += blockDim.x) xs[e] = 0ull;
+  if (tid == 0) {
+    for (int q = 0; q < ST; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], 8);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
 
+  if (warp == 8) {  // ---------------------------------------------- producer
+    if (lane == 0) {
+      for (int64_t t = t0; t < t1; ++t) {
+        const int k = (int)(t - t0), st = k % ST;
+        if (k >= ST) mbar_wait(&empty[st], ((uint32_t)(k / ST) & 1u) ^ 1u);
+        const int jc = (int)(t / ntiles);
+        const int64_t r0 = (t % ntiles) * OTF_BM;
+        const int nrows = (int)min((int64_t)OTF_BM, N - r0);
+        const int j0 = jc * OTF_BJ;
+        const int nbox = min(4, (h - j0 + 15) >> 4);
+        mbar_arrive_expect_tx(&full[st], (uint32_t)(nbox * NM * OTF_BM * 128) + (uint32_t)nrows * OTF_XW * 8u);
+        double* tg = tiles + st * NM * OTF_TILE;
+        for (int b = 0; b < nbox; ++b) {
+          tma_load_2d(tg + b * 1024, &tmG, j0 + 16 * b, (int)r0, &full[st]);
+          if (HAS_T) tma_load_2d(tg + OTF_TILE + b * 1024, &tmT, j0 + 16 * b, (int)r0, &full[st]);
+        }
+        bulk_g2s(xs + st * OTF_BM * OTF_XW, a.xbits + r0 * OTF_XW, (uint32_t)nrows * OTF_XW * 8u, &full[st]);
+      }
+    }
+    return;
+  }
+  // ------------------------------------------------------------ consumers
+  const int wr = warp >> 2, wj = warp & 3;  // rows [wr*32, +32), j [wj*16, +16)
   auto load_v = [&](int jc) {  // v_W chunk, v_b, v_u (zero beyond h / n_in)
     const int j0 = jc * OTF_BJ;
-    for (int e = tid; e < OTF_BJ * vs; e += blockDim.x) {
+    for (int e = tid; e < OTF_BJ * vs; e += 256) {
       const int jj = e / vs, k = e % vs;
       vw[e] = (j0 + jj < h && k < nin) ? a.v[a.offW + (int64_t)(j0 + jj) * nin + k] : 0.0;
     }
-    for (int e = tid; e < OTF_BJ; e += blockDim.x) {
+    for (int e = tid; e < OTF_BJ; e += 256) {
       vb[e] = (j0 + e < h) ? a.v[a.offb + j0 + e] : 0.0;
       if (HAS_T) vu[e] = (j0 + e < h) ? a.v[a.offu + j0 + e] : 0.0;
     }
   };
-  auto load_tile = [&](int64_t t, int buf) {
-    const int jc = (int)(t / ntiles);
-    const int64_t r0 = (t % ntiles) * OTF_BM;
-    otf_load_tile(a, r0, min(N, r0 + OTF_BM), jc * OTF_BJ, gs + buf * OTF_BM * OTF_BJ,
-                  HAS_T ? ts + buf * OTF_BM * OTF_BJ : nullptr, xs + buf * OTF_BM * OTF_XW, tid, blockDim.x);
-  };
-  int cur_jc = (int)(t0 / ntiles);
-  load_v(cur_jc);
-  load_tile(t0, 0);
-  cp_async_commit();
   const int ksteps = (nin + 3) / 4;
-
+  int cur_jc = -1;
   for (int64_t t = t0; t < t1; ++t) {
-    const int buf = (int)((t - t0) & 1);
+    const int k = (int)(t - t0), st = k % ST;
     const int jc = (int)(t / ntiles);
     const int64_t r0 = (t % ntiles) * OTF_BM;
-    if (t + 1 < t1) load_tile(t + 1, buf ^ 1);
-    cp_async_commit();
-    cp_async_wait<1>();
-    if (jc != cur_jc) {  // crossed into the next hidden chunk (the loop-end barrier fenced the old v)
+    if (jc != cur_jc) {  // (re)load the B operand for this hidden chunk
+      named_bar_sync(1, 256);
       load_v(jc);
+      named_bar_sync(1, 256);
       cur_jc = jc;
     }
-    __syncthreads();
-    const double* G = gs + buf * OTF_BM * OTF_BJ;
-    const double* Tt = ts + buf * OTF_BM * OTF_BJ;
-    const uint64_t* X = xs + buf * OTF_BM * OTF_XW;
+    mbar_wait(&full[st], (uint32_t)(k / ST) & 1u);
+    const double* G = tiles + st * NM * OTF_TILE;
+    const double* Tt = G + OTF_TILE;
+    const uint64_t* X = xs + st * OTF_BM * OTF_XW;
 
     // C = v_b (broadcast per column) + X V_W^T
     double c[4][2][2];
@@ -197,13 +241,13 @@ __global__ void __launch_bounds__(256) k_otf_dot(const OtfArgs a) {
       for (int q = 0; q < OTF_XW; ++q) xr[mt][q] = X[(wr * 32 + mt * 8 + (lane >> 2)) * OTF_XW + q];
     const double* vrow0 = vw + (wj * 16 + (lane >> 2)) * vs + (lane & 3);
     for (int kk = 0; kk < ksteps; ++kk) {
-      const int k = kk * 4 + (lane & 3);
+      const int kq = kk * 4 + (lane & 3);
       const double b0 = vrow0[kk * 4];
       const double b1 = vrow0[kk * 4 + 8 * vs];
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt) {
-        const uint64_t word = (k < 64) ? xr[mt][0] : xr[mt][1];
-        const double av = bit_to_double((uint32_t)(word >> (k & 63)) & 1u);
+        const uint64_t word = (kq < 64) ? xr[mt][0] : xr[mt][1];
+        const double av = bit_to_double((uint32_t)(word >> (kq & 63)) & 1u);
         dmma(c[mt][0][0], c[mt][0][1], av, b0);
         dmma(c[mt][1][0], c[mt][1][1], av, b1);
       }
@@ -213,36 +257,39 @@ __global__ void __launch_bounds__(256) k_otf_dot(const OtfArgs a) {
 #pragma unroll
     for (int mt = 0; mt < 4; ++mt) {
       const int rl = wr * 32 + mt * 8 + (lane >> 2);
-      double s = 0.0;
+      double sacc = 0.0;
 #pragma unroll
       for (int nt = 0; nt < 2; ++nt) {
         const int jl = wj * 16 + nt * 8 + (lane & 3) * 2;
-        const double2 g2 = *reinterpret_cast<const double2*>(G + rl * OTF_BJ + jl);
-        s = fma(g2.x, c[mt][nt][0], s);
-        s = fma(g2.y, c[mt][nt][1], s);
+        const int o = swz64(rl, jl);
+        const double2 g2 = *reinterpret_cast<const double2*>(G + o);
+        sacc = fma(g2.x, c[mt][nt][0], sacc);
+        sacc = fma(g2.y, c[mt][nt][1], sacc);
         if (HAS_T) {
-          const double2 t2 = *reinterpret_cast<const double2*>(Tt + rl * OTF_BJ + jl);
-          s = fma(t2.x, vu[jl], s);
-          s = fma(t2.y, vu[jl + 1], s);
+          const double2 t2 = *reinterpret_cast<const double2*>(Tt + o);
+          sacc = fma(t2.x, vu[jl], sacc);
+          sacc = fma(t2.y, vu[jl + 1], sacc);
         }
       }
-      s += __shfl_xor_sync(0xffffffffu, s, 1);
-      s += __shfl_xor_sync(0xffffffffu, s, 2);
-      rs[mt] = s;
+      sacc += __shfl_xor_sync(0xffffffffu, sacc, 1);
+      sacc += __shfl_xor_sync(0xffffffffu, sacc, 2);
+      rs[mt] = sacc;
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done with the stage
+    double* rd = red + (k & 1) * 4 * OTF_BM;
     if ((lane & 3) == 0) {
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt) red[wj * OTF_BM + wr * 32 + mt * 8 + (lane >> 2)] = rs[mt];
+      for (int mt = 0; mt < 4; ++mt) rd[wj * OTF_BM + wr * 32 + mt * 8 + (lane >> 2)] = rs[mt];
     }
-    __syncthreads();
+    named_bar_sync(1, 256);
     if (tid < OTF_BM) {
       const int64_t row = r0 + tid;
       if (row < N) {
-        const double tv = ((red[tid] + red[OTF_BM + tid]) + red[2 * OTF_BM + tid]) + red[3 * OTF_BM + tid];
+        const double tv = ((rd[tid] + rd[OTF_BM + tid]) + rd[2 * OTF_BM + tid]) + rd[3 * OTF_BM + tid];
         a.tpart[(int64_t)jc * N + row] = tv;
       }
     }
-    __syncthreads();
   }
 }
 
@@ -294,21 +341,6 @@ __global__ void __launch_bounds__(256) k_otf_y(const double* __restrict__ tpart,
   }
 }
 
-// Tiles of the acc GEMMs are 64 rows x 64 columns of doubles loaded by four
-// 2-D TMA boxes of 64 rows x 16 columns (128 bytes) with the 128-byte swizzle:
-// box b holds columns [16 b, 16 b + 16); row r's 16-byte chunk q sits at chunk
-// q ^ (r & 7).  Offset (in doubles) of element (r, c) of such a tile:
-__device__ __forceinline__ int swz64(int r, int c) {
-  return ((c >> 4) << 10) + (r << 4) + ((((c & 15) >> 1) ^ (r & 7)) << 1) + (c & 1);
-}
-constexpr int OTF_TILE = OTF_BM * OTF_BJ;  // doubles per swizzled tile (32 KB, 1024-byte aligned)
-
-// Dynamic shared memory, rounded up to the 1024-byte alignment the swizzle needs.
-__device__ __forceinline__ unsigned char* smem_1k(unsigned char* p) {
-  const uint32_t a = smem_addr(p);
-  return p + (((a + 1023u) & ~1023u) - a);
-}
-
 // grid (JC, nb), 288 threads = 8 consumer warps + 1 producer warp.
 // part[y][blk][j][kc] = sum_rows y g_j x_kc (kc = n_in is the ones column),
 // partu[y][blk][j] = sum y t_j (HAS_T).  NKT n-tiles of 8 k columns cover
@@ -325,7 +357,7 @@ __device__ __forceinline__ unsigned char* smem_1k(unsigned char* p) {
 // feeds two DMMAs) over the row quads kk = w >> 2, +2, ...; the two row halves
 // are summed through shared memory at the end.
 template <int NKT, int NY, bool HAS_T>
-__global__ void __launch_bounds__(288) __maxnreg__((NKT <= 8 && NY == 1 && !HAS_T) ? 96 : 168)
+__global__ void __maxnreg__((NKT <= 8 && NY == 1 && !HAS_T) ? 96 : 224)
     k_otf_acc(const OtfArgs a, const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmT) {
   extern __shared__ __align__(16) unsigned char smem_o[];
   constexpr int ST = OTF_ACC_STAGES;
@@ -882,19 +914,22 @@ __device__ __forceinline__ void otf_load_ctile(const OtfCArgs& a, int64_t r0, in
   }
 }
 
-// grid (persistent, 1-D), 256 threads: complex t partials over this CTA's
-// range of (real column chunk, 64-row tile) pairs
-__global__ void __launch_bounds__(256) k_otf_dot_c(const OtfCArgs a) {
+// grid (persistent, 1-D), 288 threads: complex t partials over this CTA's
+// range of (real column chunk, 64-row tile) pairs; same pipeline as k_otf_dot.
+__global__ void __maxnreg__(96) k_otf_dot_c(const OtfCArgs a,
+                                                                  const __grid_constant__ CUtensorMap tmT) {
   extern __shared__ __align__(16) unsigned char smem_c[];
+  constexpr int ST = OTF_DOT_STAGES;
   const int nin = a.n_in, vs = otf_vstride(nin);
-  double* vw = reinterpret_cast<double*>(smem_c);            // [64][vs]
-  double* vb = vw + OTF_BJ * vs;                             // [64]
-  double* gs = vb + OTF_BJ;                                  // [2][BM][64]
-  uint64_t* xs = reinterpret_cast<uint64_t*>(gs + 2 * OTF_BM * OTF_BJ);  // [2][BM][XW]
-  double2* red = reinterpret_cast<double2*>(xs + 2 * OTF_BM * OTF_XW);   // [4][BM]
+  double* tiles = reinterpret_cast<double*>(smem_1k(smem_c));          // [ST][TILE]
+  uint64_t* xs = reinterpret_cast<uint64_t*>(tiles + ST * OTF_TILE);   // [ST][BM][XW]
+  double2* red = reinterpret_cast<double2*>(xs + ST * OTF_BM * OTF_XW);  // [2][4][BM]
+  uint64_t* full = reinterpret_cast<uint64_t*>(red + 2 * 4 * OTF_BM);  // [ST]
+  uint64_t* empty = full + ST;
+  double* vb = reinterpret_cast<double*>(empty + ST);  // [64]
+  double* vw = vb + OTF_BJ;                            // [64][vs]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wr = warp >> 2, wj = warp & 3;
   const int ncols = 2 * a.hidden;
   const int64_t N = a.n_rows;
   const int64_t ntiles = (N + OTF_BM - 1) / OTF_BM;
@@ -902,10 +937,39 @@ __global__ void __launch_bounds__(256) k_otf_dot_c(const OtfCArgs a) {
   int64_t t0, t1;
   otf_cta_range(ntiles * jcount, t0, t1);
   if (t0 >= t1) return;
+  for (int e = tid; e < ST * OTF_TILE; e += blockDim.x) tiles[e] = 0.0;
+  for (int e = tid; e < ST * OTF_BM * OTF_XW; e += blockDim.x) xs[e] = 0ull;
+  if (tid == 0) {
+    for (int q = 0; q < ST; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], 8);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
 
+  if (warp == 8) {  // producer
+    if (lane == 0) {
+      for (int64_t t = t0; t < t1; ++t) {
+        const int k = (int)(t - t0), st = k % ST;
+        if (k >= ST) mbar_wait(&empty[st], ((uint32_t)(k / ST) & 1u) ^ 1u);
+        const int jc = (int)(t / ntiles);
+        const int64_t r0 = (t % ntiles) * OTF_BM;
+        const int nrows = (int)min((int64_t)OTF_BM, N - r0);
+        const int c0 = jc * OTF_BJ;
+        const int nbox = min(4, (ncols - c0 + 15) >> 4);
+        mbar_arrive_expect_tx(&full[st], (uint32_t)(nbox * OTF_BM * 128) + (uint32_t)nrows * OTF_XW * 8u);
+        for (int b = 0; b < nbox; ++b)
+          tma_load_2d(tiles + st * OTF_TILE + b * 1024, &tmT, c0 + 16 * b, (int)r0, &full[st]);
+        bulk_g2s(xs + st * OTF_BM * OTF_XW, a.xbits + r0 * OTF_XW, (uint32_t)nrows * OTF_XW * 8u, &full[st]);
+      }
+    }
+    return;
+  }
+  const int wr = warp >> 2, wj = warp & 3;
   auto load_v = [&](int jc) {
     const int c0 = jc * OTF_BJ;
-    for (int e = tid; e < OTF_BJ * vs; e += blockDim.x) {
+    for (int e = tid; e < OTF_BJ * vs; e += 256) {
       const int cc = e / vs, k = e % vs;
       const int col = c0 + cc;
       double val = 0.0;
@@ -915,36 +979,26 @@ __global__ void __launch_bounds__(256) k_otf_dot_c(const OtfCArgs a) {
       }
       vw[e] = val;
     }
-    for (int e = tid; e < OTF_BJ; e += blockDim.x) {
+    for (int e = tid; e < OTF_BJ; e += 256) {
       const int col = c0 + e;
       vb[e] = col < ncols ? ((col & 1) ? a.v_im[a.offb + (col >> 1)] : a.v_re[a.offb + (col >> 1)]) : 0.0;
     }
   };
-  auto load_tile = [&](int64_t t, int buf) {
-    const int jc = (int)(t / ntiles);
-    const int64_t r0 = (t % ntiles) * OTF_BM;
-    otf_load_ctile(a, r0, min(N, r0 + OTF_BM), jc * OTF_BJ, gs + buf * OTF_BM * OTF_BJ, xs + buf * OTF_BM * OTF_XW,
-                   tid, blockDim.x);
-  };
-  int cur_jc = (int)(t0 / ntiles);
-  load_v(cur_jc);
-  load_tile(t0, 0);
-  cp_async_commit();
   const int ksteps = (nin + 3) / 4;
+  int cur_jc = -1;
   for (int64_t t = t0; t < t1; ++t) {
-    const int buf = (int)((t - t0) & 1);
+    const int k = (int)(t - t0), st = k % ST;
     const int jc = (int)(t / ntiles);
     const int64_t r0 = (t % ntiles) * OTF_BM;
-    if (t + 1 < t1) load_tile(t + 1, buf ^ 1);
-    cp_async_commit();
-    cp_async_wait<1>();
     if (jc != cur_jc) {
+      named_bar_sync(1, 256);
       load_v(jc);
+      named_bar_sync(1, 256);
       cur_jc = jc;
     }
-    __syncthreads();
-    const double* G = gs + buf * OTF_BM * OTF_BJ;
-    const uint64_t* X = xs + buf * OTF_BM * OTF_XW;
+    mbar_wait(&full[st], (uint32_t)(k / ST) & 1u);
+    const double* G = tiles + st * OTF_TILE;
+    const uint64_t* X = xs + st * OTF_BM * OTF_XW;
     double c[4][2][2];
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
@@ -962,13 +1016,13 @@ __global__ void __launch_bounds__(256) k_otf_dot_c(const OtfCArgs a) {
       for (int q = 0; q < OTF_XW; ++q) xr[mt][q] = X[(wr * 32 + mt * 8 + (lane >> 2)) * OTF_XW + q];
     const double* vrow0 = vw + (wj * 16 + (lane >> 2)) * vs + (lane & 3);
     for (int kk = 0; kk < ksteps; ++kk) {
-      const int k = kk * 4 + (lane & 3);
+      const int kq = kk * 4 + (lane & 3);
       const double b0 = vrow0[kk * 4];
       const double b1 = vrow0[kk * 4 + 8 * vs];
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt) {
-        const uint64_t word = (k < 64) ? xr[mt][0] : xr[mt][1];
-        const double av = bit_to_double((uint32_t)(word >> (k & 63)) & 1u);
+        const uint64_t word = (kq < 64) ? xr[mt][0] : xr[mt][1];
+        const double av = bit_to_double((uint32_t)(word >> (kq & 63)) & 1u);
         dmma(c[mt][0][0], c[mt][0][1], av, b0);
         dmma(c[mt][1][0], c[mt][1][1], av, b1);
       }
@@ -982,7 +1036,7 @@ __global__ void __launch_bounds__(256) k_otf_dot_c(const OtfCArgs a) {
 #pragma unroll
       for (int nt = 0; nt < 2; ++nt) {
         const int cl = wj * 16 + nt * 8 + (lane & 3) * 2;
-        const double2 t2 = *reinterpret_cast<const double2*>(G + rl * OTF_BJ + cl);
+        const double2 t2 = *reinterpret_cast<const double2*>(G + swz64(rl, cl));
         sre = fma(t2.x, c[mt][nt][0], sre);
         sre = fma(-t2.y, c[mt][nt][1], sre);
         sim = fma(t2.x, c[mt][nt][1], sim);
@@ -994,23 +1048,25 @@ __global__ void __launch_bounds__(256) k_otf_dot_c(const OtfCArgs a) {
       sim += __shfl_xor_sync(0xffffffffu, sim, 2);
       rs[mt] = make_double2(sre, sim);
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+    double2* rd = red + (k & 1) * 4 * OTF_BM;
     if ((lane & 3) == 0) {
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt) red[wj * OTF_BM + wr * 32 + mt * 8 + (lane >> 2)] = rs[mt];
+      for (int mt = 0; mt < 4; ++mt) rd[wj * OTF_BM + wr * 32 + mt * 8 + (lane >> 2)] = rs[mt];
     }
-    __syncthreads();
+    named_bar_sync(1, 256);
     if (tid < OTF_BM) {
       const int64_t row = r0 + tid;
       if (row < N) {
-        double2 tv = red[tid];
+        double2 tv = rd[tid];
         for (int w = 1; w < 4; ++w) {
-          tv.x += red[w * OTF_BM + tid].x;
-          tv.y += red[w * OTF_BM + tid].y;
+          tv.x += rd[w * OTF_BM + tid].x;
+          tv.y += rd[w * OTF_BM + tid].y;
         }
         a.tpart[(int64_t)jc * N + row] = tv;
       }
     }
-    __syncthreads();
   }
 }
 
@@ -1115,7 +1171,7 @@ __global__ void __launch_bounds__(256) k_otf_y_c(const double2* __restrict__ tpa
 // 9 warps per CTA: two resident CTAs put up to 5 warps on one SM sub-partition,
 // whose 16K-register slice then allows at most 96 registers per thread.
 template <int NKT>
-__global__ void __launch_bounds__(288) __maxnreg__(NKT <= 8 ? 96 : 168)
+__global__ void __maxnreg__(NKT <= 8 ? 96 : 224)
     k_otf_acc_c(const OtfCArgs a, const __grid_constant__ CUtensorMap tmT) {
   extern __shared__ __align__(16) unsigned char smem_c[];
   constexpr int ST = OTF_ACC_STAGES;
