@@ -1530,6 +1530,18 @@ int irl_lanczos_step_cluster(double* V, int64_t ldv, double* W, int64_t L, int j
                                                  cudaFuncAttributeNonPortableClusterSizeAllowed, 1); });
   cudaGetLastError();
   const int cs = (int)std::min<int64_t>(16, std::max<int64_t>(2, cdiv(L, 512)));
+  // shared-memory staged variant when this CTA's slice of rows 0..j (+ W) fits
+  const int64_t slice = 2 * cdiv(L / 2, cs);
+  const size_t stage_bytes = (size_t)(j + 2) * slice * 8;
+  static std::once_flag once_s;
+  std::call_once(once_s, [&] {
+    cudaFuncSetAttribute((const void*)k_lanczos_cluster_smem, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute((const void*)k_lanczos_cluster_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         d.smem_optin - 4096);
+  });
+  cudaGetLastError();
+  const bool staged = (L % 2 == 0) && (ldv % 2 == 0) && aligned16(V) && aligned16(W) &&
+                      stage_bytes + 4096 <= (size_t)d.smem_optin && getenv("IRL_LANCZOS_NOSTAGE") == nullptr;
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1538,10 +1550,13 @@ int irl_lanczos_step_cluster(double* V, int64_t ldv, double* W, int64_t L, int j
   attr[0].val.clusterDim.z = 1;
   cfg.gridDim = dim3(cs);
   cfg.blockDim = dim3(512);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = staged ? stage_bytes : 0;
   cfg.stream = (cudaStream_t)stream;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  if (staged)
+    return cuda_check(cudaLaunchKernelEx(&cfg, k_lanczos_cluster_smem, V, ldv, W, L, j, m, ab),
+                      "lanczos cluster launch");
   return cuda_check(cudaLaunchKernelEx(&cfg, k_lanczos_cluster, V, ldv, W, L, j, m, ab), "lanczos cluster launch");
 }
 

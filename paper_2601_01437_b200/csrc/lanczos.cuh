@@ -157,3 +157,93 @@ __global__ void __launch_bounds__(512) k_lanczos_cluster(double* __restrict__ V,
 }
 
 }  // namespace irl
+
+namespace irl {
+
+// The one-cluster step with the CTA's slice of V (rows 0..j) and W staged in
+// shared memory by TMA bulk copies at kernel start: the four passes over the
+// basis then read shared memory instead of L2, which removes three L2 round
+// trips from the step's critical path.  Slices are whole 16-byte units (L is
+// even for every bordered layout; the host checks).  Same arithmetic order as
+// k_lanczos_cluster.
+__global__ void __launch_bounds__(512) k_lanczos_cluster_smem(double* __restrict__ V, int64_t ldv,
+                                                               double* __restrict__ W, int64_t L, int j, int m,
+                                                               double* __restrict__ ab) {
+  extern __shared__ __align__(16) double lz_sm[];
+  __shared__ double sh[32];
+  __shared__ double p_alpha[1], p_beta[1], p_h0[LZ_MAXJ], p_h1[LZ_MAXJ];
+  __shared__ double s_alpha[1], s_beta[1], s_h[LZ_MAXJ];
+  __shared__ __align__(8) uint64_t bar;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int cs = (int)(gridDim.x * gridDim.y * gridDim.z);
+  const int rank = (int)cluster_rank();
+  const int64_t units = L >> 1;
+  const int64_t lo = 2 * (units * rank / cs), hi = 2 * (units * (rank + 1) / cs);
+  const int S = (int)(hi - lo);
+  double* vs = lz_sm;                           // [j+1][S]
+  double* ws = lz_sm + (int64_t)(j + 1) * S;    // [S]
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    mbar_arrive_expect_tx(&bar, (uint32_t)((j + 2) * S * 8));
+    for (int i = 0; i <= j; ++i) bulk_g2s(vs + (int64_t)i * S, V + (int64_t)i * ldv + lo, (uint32_t)S * 8u, &bar);
+    bulk_g2s(ws, W + lo, (uint32_t)S * 8u, &bar);
+  }
+  mbar_wait(&bar, 0);
+  const double* vj = vs + (int64_t)j * S;
+
+  double p = 0.0;
+  for (int e = tid; e < S; e += blockDim.x) p = fma(vj[e], ws[e], p);
+  p = block_sum_f64(p, sh);
+  if (tid == 0) p_alpha[0] = p;
+  lz_cluster_sum(p_alpha, s_alpha, 1, cs);
+  const double alpha = s_alpha[0];
+  const double bprev = j > 0 ? ab[m + j - 1] : 0.0;
+  const double* vp = j > 0 ? vs + (int64_t)(j - 1) * S : nullptr;
+  for (int e = tid; e < S; e += blockDim.x) {
+    double w = ws[e] - alpha * vj[e];
+    if (vp) w -= bprev * vp[e];
+    ws[e] = w;
+  }
+  __syncthreads();
+  for (int pass = 0; pass < 2; ++pass) {
+    double* ph = pass == 0 ? p_h0 : p_h1;
+    for (int i = warp; i <= j; i += nw) {
+      const double* vi = vs + (int64_t)i * S;
+      double q = 0.0;
+      for (int e = lane; e < S; e += 32) q = fma(vi[e], ws[e], q);
+      q = warp_sum<false>(q);
+      if (lane == 0) ph[i] = q;
+    }
+    lz_cluster_sum(ph, s_h, j + 1, cs);
+    for (int e = tid; e < S; e += blockDim.x) {
+      double acc = 0.0;
+      for (int i = 0; i <= j; ++i) acc = fma(s_h[i], vs[(int64_t)i * S + e], acc);
+      ws[e] -= acc;
+    }
+    __syncthreads();
+  }
+  double nrm = 0.0;
+  for (int e = tid; e < S; e += blockDim.x) nrm = fma(ws[e], ws[e], nrm);
+  nrm = block_sum_f64(nrm, sh);
+  if (tid == 0) p_beta[0] = nrm;
+  lz_cluster_sum(p_beta, s_beta, 1, cs);
+  const double beta = sqrt(s_beta[0]);
+  const double inv = 1.0 / fmax(beta, 1e-300);
+  double* vn = V + (int64_t)(j + 1) * ldv + lo;
+  for (int e = tid; e < S; e += blockDim.x) {
+    const double w = ws[e];
+    W[lo + e] = w;
+    vn[e] = w * inv;
+  }
+  if (rank == 0 && tid == 0) {
+    ab[j] = alpha;
+    ab[m + j] = beta;
+  }
+  cluster_sync();
+}
+
+}  // namespace irl

@@ -138,7 +138,7 @@ __device__ __forceinline__ void otf_cta_range(int64_t total, int64_t& t0, int64_
 // bits through a 2-stage mbarrier ring; the per-row cross-warp sums use a
 // double-buffered exchange and one named barrier of the consumers per tile.
 template <bool HAS_T>
-__global__ void __maxnreg__(HAS_T ? 224 : 96)
+__global__ void __maxnreg__(HAS_T ? 168 : 96)
     k_otf_dot(const OtfArgs a, const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmT) {
   extern __shared__ __align__(16) unsigned char smem_o[];
   constexpr int ST = OTF_DOT_STAGES;
@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(256) k_otf_y(const double* __restrict__ tpart,
 // feeds two DMMAs) over the row quads kk = w >> 2, +2, ...; the two row halves
 // are summed through shared memory at the end.
 template <int NKT, int NY, bool HAS_T>
-__global__ void __maxnreg__((NKT <= 8 && NY == 1 && !HAS_T) ? 96 : 224)
+__global__ void __maxnreg__((NKT <= 8 && NY == 1 && !HAS_T) ? 96 : 168)
     k_otf_acc(const OtfArgs a, const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmT) {
   extern __shared__ __align__(16) unsigned char smem_o[];
   constexpr int ST = OTF_ACC_STAGES;
@@ -1168,10 +1168,11 @@ __global__ void __launch_bounds__(256) k_otf_y_c(const double2* __restrict__ tpa
 // Same structure as k_otf_acc (producer warp, 2-D swizzled TMA tiles of the
 // real N x 2h view of T, two A fragments per B fragment, row quads split over
 // two warp halves).
-// 9 warps per CTA: two resident CTAs put up to 5 warps on one SM sub-partition,
-// whose 16K-register slice then allows at most 96 registers per thread.
+// Register caps of the 9-warp (288-thread) GEMM kernels: one SM sub-partition
+// holds a 16K-register slice and receives up to 3 warps of one CTA (168
+// registers per thread at most) or 5 warps of two CTAs (96).
 template <int NKT>
-__global__ void __maxnreg__(NKT <= 8 ? 96 : 224)
+__global__ void __maxnreg__(NKT <= 8 ? 96 : 168)
     k_otf_acc_c(const OtfCArgs a, const __grid_constant__ CUtensorMap tmT) {
   extern __shared__ __align__(16) unsigned char smem_c[];
   constexpr int ST = OTF_ACC_STAGES;

@@ -147,14 +147,17 @@ def test_abi_status_codes(cuda):
     torch.cuda.synchronize()
 
 
+@pytest.mark.parametrize("stage", [True, False])
 @pytest.mark.parametrize("L,j", [(866, 0), (866, 19), (6658, 7), (11282, 29), (60000, 39)])
-def test_lanczos_step_kernels(cuda, L, j):
+def test_lanczos_step_kernels(cuda, L, j, stage, monkeypatch):
     """Fused Lanczos steps (single CTA, one cluster) == the BLAS-1/2 sequence
     of kry:96-116 (alpha, three-term update, two reorthogonalisation passes,
     beta, normalised next vector)."""
     import torch
     from paper_2601_01437_b200 import _lib
 
+    if not stage:  # the global-memory cluster step instead of the shared-memory staged one
+        monkeypatch.setenv("IRL_LANCZOS_NOSTAGE", "1")
     m = 41
     gen = torch.Generator(device="cuda").manual_seed(L + j)
     q, _ = torch.linalg.qr(torch.randn(L, j + 1, dtype=torch.float64, device="cuda", generator=gen))
