@@ -302,7 +302,7 @@ def test_graph_sweeper_restarts_and_breakdown(pkg):
     assert abs(p2.value - 1.0) < 1e-12 and p2.n_matvec <= 5
 
 
-@pytest.mark.parametrize("rows,n_in,hidden", [(300, 20, 64), (257, 100, 130), (1024, 100, 2048)])
+@pytest.mark.parametrize("rows,n_in,hidden", [(300, 20, 64), (257, 100, 130), (1024, 100, 2048), (129, 37, 18), (4099, 64, 256)])
 def test_otf_mlp_matches_stored(pkg, rows, n_in, hidden):
     """On-the-fly (K6, DMMA) products, stats and IRL == stored-O batch and oracle."""
     from paper_2601_01437_b200 import ansatz as A, estimators as E, optimizer as OPT
@@ -338,7 +338,7 @@ def test_otf_mlp_matches_stored(pkg, rows, n_in, hidden):
     assert rel(host(r2.direction), host(r1.direction)) < DIR_TOL
 
 
-@pytest.mark.parametrize("idx,rows", [(1, 8192), (2, 2048)])
+@pytest.mark.parametrize("idx,rows", [(1, 8192), (2, 2048), (2, 4097), (1, 65)])
 def test_otf_rbm_matches_stored(pkg, idx, rows):
     """On-the-fly RBM (K6): products, stats and IRL == stored-O batch and the oracle."""
     from paper_2601_01437_b200 import ansatz as A, estimators as E, optimizer as OPT, synthetic as S
@@ -367,7 +367,7 @@ def test_otf_rbm_matches_stored(pkg, idx, rows):
     assert rel(host(r2.direction), host(r1.direction)) < DIR_TOL
 
 
-@pytest.mark.parametrize("rows", [512, 3000])
+@pytest.mark.parametrize("rows", [512, 3000, 1023])
 def test_otf_hermitian_rbm_matches_stored(pkg, rows):
     """Complex-theta RBM on the fly (cfg4 shapes): statistics, products (plain and
     bordered through the IRL) == stored-O batch and the oracle."""
