@@ -594,7 +594,7 @@ int make_otf_plan_uncached(int64_t n, int n_in, int hidden, OtfPlan& p) {
   IRL_TRY(dev_info(d));
   if (n_in < 1 || n_in > OTF_MAX_NIN) return fail(IRL_ERR_ARG, "on-the-fly mode supports n_in <= %d", OTF_MAX_NIN);
   p.jc = (int)cdiv(hidden, OTF_BJ);
-  p.ny = d.sms;
+  p.ny = 4 * d.sms;  // row-parallel helper kernels (y, dots): 4 CTAs per SM
   p.nkt = (n_in + 1 + 7) / 8 <= 3 ? 3 : (n_in + 1 + 7) / 8 <= 6 ? 6 : 13;
   p.kc = 8 * p.nkt;
   p.nb = 1;
@@ -824,7 +824,7 @@ int make_otfc_plan_uncached(int64_t n, int n_in, int hidden, OtfCPlan& p) {
   IRL_TRY(cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_a, (const void*)acc, 288, p.smem_acc), "occ"));
   p.nb_dot = d.sms * std::max(occ_d, 1);  // persistent grid
   p.nb_acc = best_row_blocks(d.sms * std::max(occ_a, 1), p.jc, n);
-  p.ny = d.sms;
+  p.ny = 4 * d.sms;  // row-parallel helper kernels (y, dots): 4 CTAs per SM
   p.nbx = std::min<int>(4 * d.sms, (int)std::max<int64_t>(1, n / 64));
   return IRL_OK;
 }

@@ -69,6 +69,34 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// Fixed-order block sum of src[0..count) (every thread gets the total).
+__device__ __forceinline__ double block_sum_fixed(const double* __restrict__ src, int count, double* sh) {
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x, nt = blockDim.x * blockDim.y;
+  double v = 0.0;
+  for (int q = tid; q < count; q += nt) v += src[q];
+  v = warp_sum<false>(v);
+  if ((tid & 31) == 0) sh[tid >> 5] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int w = 0; w < (nt >> 5); ++w) t += sh[w];
+  __syncthreads();
+  return t;
+}
+
+// Column reduction of the row-block partials: blockDim (32, 8); lane x owns one
+// output, the 8 y-phases split the partial blocks (b = y, y + 8, ...), then a
+// fixed-order sum over y (valid on threadIdx.y == 0).
+__device__ __forceinline__ double ysum8(double v, double (*sm)[33]) {
+  sm[threadIdx.y][threadIdx.x] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.y == 0)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) t += sm[q][threadIdx.x];
+  __syncthreads();
+  return t;
+}
+
 // x (N x n_in uint8) -> bit-packed rows
 __global__ void k_pack_bits(const uint8_t* __restrict__ x, int64_t n, int n_in, uint64_t* __restrict__ xbits) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
@@ -306,8 +334,7 @@ __global__ void __launch_bounds__(256) k_otf_y(const double* __restrict__ tpart,
   if (offa >= 0)
     for (int i = threadIdx.x; i < n_in; i += blockDim.x) va[i] = v[offa + i];
   __syncthreads();
-  double s = 0.0;
-  for (int q = 0; q < n_dpart; ++q) s += dpart[q];
+  const double s = block_sum_fixed(dpart, n_dpart, sh);  // same fixed order in every CTA
   const double vc = p_last >= 0 ? v[p_last] : 0.0;
   double acc = 0.0;
   const int64_t per = (n + gridDim.x - 1) / gridDim.x;
@@ -546,34 +573,6 @@ __global__ void __maxnreg__((NKT <= 8 && NY == 1 && !HAS_T) ? 96 : 168)
 // Assemble the MLP-layout parameter vector from the acc partials:
 //   mode 0 (product): out = sum part - obar * Y (+ u0 hf), out0 = g0
 //   mode 1 (stats)  : out = sum part          (Y, obar unused)
-// Fixed-order block sum of src[0..count) (every thread gets the total).
-__device__ __forceinline__ double block_sum_fixed(const double* __restrict__ src, int count, double* sh) {
-  const int tid = threadIdx.y * blockDim.x + threadIdx.x, nt = blockDim.x * blockDim.y;
-  double v = 0.0;
-  for (int q = tid; q < count; q += nt) v += src[q];
-  v = warp_sum<false>(v);
-  if ((tid & 31) == 0) sh[tid >> 5] = v;
-  __syncthreads();
-  double t = 0.0;
-  for (int w = 0; w < (nt >> 5); ++w) t += sh[w];
-  __syncthreads();
-  return t;
-}
-
-// Column reduction of the row-block partials: blockDim (32, 8); lane x owns one
-// output, the 8 y-phases split the partial blocks (b = y, y + 8, ...), then a
-// fixed-order sum over y (valid on threadIdx.y == 0).
-__device__ __forceinline__ double ysum8(double v, double (*sm)[33]) {
-  sm[threadIdx.y][threadIdx.x] = v;
-  __syncthreads();
-  double t = 0.0;
-  if (threadIdx.y == 0)
-#pragma unroll
-    for (int q = 0; q < 8; ++q) t += sm[q][threadIdx.x];
-  __syncthreads();
-  return t;
-}
-
 // MLP assembly in the layout [W (h x n_in), b, u, c]; blockDim (32, 8)
 __global__ void __launch_bounds__(256) k_otf_finish(const double* __restrict__ part, const double* __restrict__ partu,
                                                     int nb, int hidden, int n_in, int kc, int64_t ld,
@@ -1119,9 +1118,21 @@ __global__ void __launch_bounds__(256) k_otf_y_c(const double2* __restrict__ tpa
     va[i] = make_double2(v_re[offa + i], v_im ? v_im[offa + i] : 0.0);
   __syncthreads();
   double sr = 0.0, si = 0.0;
-  for (int q = 0; q < n_sp; ++q) {
-    sr += sp[q].x;
-    si += sp[q].y;
+  {  // fixed-order block sum of the complex partials (same order in every CTA)
+    __shared__ double2 shs[8];
+    double2 v = make_double2(0.0, 0.0);
+    for (int q = threadIdx.x; q < n_sp; q += blockDim.x) {
+      v.x += sp[q].x;
+      v.y += sp[q].y;
+    }
+    v.x = warp_sum<false>(v.x);
+    v.y = warp_sum<false>(v.y);
+    if ((threadIdx.x & 31) == 0) shs[threadIdx.x >> 5] = v;
+    __syncthreads();
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      sr += shs[w].x;
+      si += shs[w].y;
+    }
   }
   double ar = 0.0, ai = 0.0;
   const int64_t per = (n + gridDim.x - 1) / gridDim.x;
