@@ -484,24 +484,22 @@ __global__ void __maxnreg__((NKT <= 8 && NY == 1 && !HAS_T) ? 96 : 168)
           t1 = Tt[o1];
         }
         const uint64_t w0 = (X[rl * OTF_XW] | one0) >> sh_base, w1 = (X[rl * OTF_XW + 1] | one1) >> sh_base;
-        double bv[NKT];
-#pragma unroll
-        for (int nt = 0; nt < NKT; ++nt) {
-          const uint32_t bit = nt < 8 ? (uint32_t)(w0 >> (nt * 8)) & 1u : (uint32_t)(w1 >> ((nt - 8) * 8)) & 1u;
-          bv[nt] = bit_to_double(bit);
-        }
+        // the row weight rides on the B operand: B = x ? y : 0 (integer selects, no FP64
+        // multiply competing with the DMMA pipe)
 #pragma unroll
         for (int q = 0; q < NY; ++q) {
           const double yq = Y[q * OTF_BM + rl];
-          const double a0 = g0 * yq, a1 = g1 * yq;
 #pragma unroll
           for (int nt = 0; nt < NKT; ++nt) {
-            dmma(c[q][0][nt][0], c[q][0][nt][1], a0, bv[nt]);
-            dmma(c[q][1][nt][0], c[q][1][nt][1], a1, bv[nt]);
+            const uint32_t bit = nt < 8 ? (uint32_t)(w0 >> (nt * 8)) & 1u : (uint32_t)(w1 >> ((nt - 8) * 8)) & 1u;
+            const double bv = bit ? yq : 0.0;
+            dmma(c[q][0][nt][0], c[q][0][nt][1], g0, bv);
+            dmma(c[q][1][nt][0], c[q][1][nt][1], g1, bv);
           }
           if (HAS_T) {
-            dmma(cu[q][0][0], cu[q][0][1], t0 * yq, one_b);
-            dmma(cu[q][1][0], cu[q][1][1], t1 * yq, one_b);
+            const double yb = one_b != 0.0 ? yq : 0.0;
+            dmma(cu[q][0][0], cu[q][0][1], t0, yb);
+            dmma(cu[q][1][0], cu[q][1][1], t1, yb);
           }
         }
       }
@@ -1256,9 +1254,11 @@ __global__ void __maxnreg__(NKT <= 8 ? 96 : 168)
         const double2 ta = *reinterpret_cast<const double2*>(G + swz64(rl, jb));
         const double2 tb = *reinterpret_cast<const double2*>(G + swz64(rl, jb + 8));
         const double2 yv = Y[rl];
-        // conj(t) y = (t.x y.x + t.y y.y) + i (t.x y.y - t.y y.x)
-        const double a0 = pj ? fma(ta.x, yv.y, -ta.y * yv.x) : fma(ta.x, yv.x, ta.y * yv.y);
-        const double a1 = pj ? fma(tb.x, yv.y, -tb.y * yv.x) : fma(tb.x, yv.x, tb.y * yv.y);
+        // conj(t) y = (t.x y.x + t.y y.y) + i (t.x y.y - t.y y.x): the lane's part p
+        // is t.x u + t.y w with (u, w) selected once per row (no divergent FP64 paths)
+        const double u = pj ? yv.y : yv.x, w = pj ? -yv.x : yv.y;
+        const double a0 = fma(ta.x, u, ta.y * w);
+        const double a1 = fma(tb.x, u, tb.y * w);
         const uint64_t w0 = (X[rl * OTF_XW] | one0) >> sh_base, w1 = (X[rl * OTF_XW + 1] | one1) >> sh_base;
 #pragma unroll
         for (int nt = 0; nt < NKT; ++nt) {
