@@ -127,3 +127,41 @@ def test_krylov_restatement_matches_reference():
         assert abs(pair["value"] - float(g[f"value{i}"])) < 1e-12 * norm
         assert pair["residual"] <= 1e-12 * max(1.0, norm)
         assert abs(abs(pair["vector"] @ g[f"vector{i}"]) - 1.0) < 1e-10
+
+
+@pytest.mark.parametrize("idx,rows", [(1, 300), (2, 128), (3, 200), (4, 64), (5, 32)])
+def test_structured_oracle_matches_rows(idx, rows):
+    """oracle/structured.py (full-size CPU products from N x h / N x n factors)
+    equals the row-based restatement of est:171-186 on a row subset."""
+    from oracle import estimators as oest, nqs
+    from oracle.structured import MLPProducts, RBMProducts
+    from paper_2601_01437_b200 import synthetic as S
+
+    cfg = S.CONFIGS[idx].with_rows(rows)
+    inp = S.make_inputs(cfg)
+    n, h = cfg.n_inputs, cfg.hidden
+    w = np.full(rows, 1.0 / rows)
+    mean = float(np.sum(w * inp.e_loc).real)
+    rng = np.random.default_rng(idx)
+    if cfg.model == "rbm":
+        o = nqs.rbm_rows(inp.theta, inp.x, n, h)
+        sp = RBMProducts(inp.theta, inp.x, n, h, w)
+    else:
+        o = nqs.mlp_rows(inp.theta, inp.x, n, h)
+        sp = MLPProducts(inp.theta, inp.x, n, h, w)
+    P = o.shape[1]
+    assert sp.p == P
+    assert np.linalg.norm(sp.obar - w @ o) <= 1e-13 * np.linalg.norm(w @ o)
+    if cfg.complex_params:
+        v = rng.standard_normal(P) + 1j * rng.standard_normal(P)
+        ref = oest.heff_hermitian(w, inp.e_loc, o, mean, v)
+        got = sp.product(w * (inp.e_loc - mean).real, v)
+    else:
+        v = rng.standard_normal(P)
+        ref = oest.heff(w, inp.e_loc, o, mean, v)
+        got = sp.product(w * (inp.e_loc - mean), v)
+    assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(ref)
+    ref_s = oest.qgt(w, o, v.real) if not cfg.complex_params else None
+    if ref_s is not None:
+        got_s = sp.product(w, v)
+        assert np.linalg.norm(got_s - ref_s) <= 1e-12 * np.linalg.norm(ref_s)
