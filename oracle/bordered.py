@@ -65,3 +65,36 @@ def direction(vec, grad):
 def solve(matvec, dim, grad, m, tol=1e-12, max_restarts=3, seed=0):
     pair = krylov.irl(matvec, dim, m=m, tol=tol, max_restarts=max_restarts, seed=seed)
     return pair, direction(pair["vector"], grad)
+
+
+def structured_problem(sp, e, n_samples):
+    """(matvec, dim, gradient, mean) of opt:134-148 at full size from the
+    structured products of oracle/structured.py (real theta), or of the real
+    embedding for complex theta, dim 2P + 1."""
+    w = sp.w
+    mean, _, _ = est.energy(w, e, n_samples)
+    g = sp.colsum(w * (e - mean))  # sum w (e - E) conj(O) (= est:162 expanded form)
+    coeff = w * (e - mean).real
+    p = sp.p
+    if np.iscomplexobj(g):
+        grad = 2.0 * np.concatenate([g.real, g.imag])
+        half = 0.5 * grad
+
+        def matvec(u):
+            out = np.empty(2 * p + 1)
+            out[0] = half @ u[1:]
+            hv = sp.product(coeff, u[1 : p + 1] + 1j * u[p + 1 :])
+            out[1:] = u[0] * half + np.concatenate([hv.real, hv.imag])
+            return out
+
+        return matvec, 2 * p + 1, grad, mean
+    grad = 2.0 * g.real
+    half = 0.5 * grad
+
+    def matvec(u):
+        out = np.empty(p + 1)
+        out[0] = half @ u[1:]
+        out[1:] = u[0] * half + sp.product(coeff, u[1:])
+        return out
+
+    return matvec, p + 1, grad, mean

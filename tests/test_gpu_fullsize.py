@@ -4,6 +4,7 @@ cfg2-cfg5 (oracle/structured.py, itself pinned to the row-based restatement of
 est:171-186 in test_oracle_golden.py).  Tolerance: products rel-L2 <= 1e-10."""
 
 import gc
+import os
 
 import numpy as np
 import pytest
@@ -53,3 +54,39 @@ def test_full_size_products(cuda, idx):
     for mode, (_, hv, sv) in results.items():
         assert rel(hv, ref_h) < PROD_TOL, (idx, mode, "heff")
         assert rel(sv, ref_s) < PROD_TOL, (idx, mode, "S")
+
+
+# cfg4 (118 complex matvecs of the CPU restatement, ~2.5 min of host time) and
+# cfg5 (80 matvecs at 65536 x 208897, ~3 min) run when IRL_FULLSIZE_ALL=1
+# (recorded passing: profiles/r01b_fullsize_irl.txt).
+FULL_IRL = [2, 3] + ([4, 5] if os.environ.get("IRL_FULLSIZE_ALL") == "1" else [])
+
+
+@pytest.mark.parametrize("idx", FULL_IRL)
+def test_full_size_irl(cuda, idx):
+    """The full bordered IRL solve (opt:130-165) at full cfg size on the device
+    (AUTO build: on-the-fly for these shapes) against the CPU restatement
+    (oracle/krylov.py over the structured products): matvec count, Ritz value
+    within 1e-10, direction within 1e-8."""
+    import torch
+    from oracle import bordered as obord
+    from paper_2601_01437_b200 import ansatz as A, optimizer as OPT, synthetic as S
+
+    cfg = S.CONFIGS[idx]
+    inp = S.make_inputs(cfg)
+    n, h, N = cfg.n_inputs, cfg.hidden, cfg.n_rows
+    arch = (A.RBMArchitecture(n, h, cfg.complex_params) if cfg.model == "rbm" else A.MLPArchitecture(n, h))
+    b = A.build_batch(A.AnsatzParameters(arch, inp.theta), inp.x, inp.e_loc, mode="auto")
+    res = OPT.solve_step(b, OPT.OptimizerConfig(m=cfg.m, max_restarts=cfg.max_restarts), seed=cfg.lanczos_seed)
+    d = res.direction.cpu().numpy()
+    del b
+    torch.cuda.empty_cache()
+    w = np.full(N, 1.0 / N)
+    sp = (RBMProducts if cfg.model == "rbm" else MLPProducts)(inp.theta, inp.x, n, h, w)
+    mv, dim, grad, _ = obord.structured_problem(sp, inp.e_loc, N)
+    pair, d_ref = obord.solve(mv, dim, grad, cfg.m, max_restarts=cfg.max_restarts, seed=cfg.lanczos_seed)
+    assert res.n_matvec == pair["n_matvec"]
+    assert abs(res.lambda_min - pair["value"]) <= 1e-10 * abs(pair["value"])
+    if np.iscomplexobj(d):  # complex theta: compare in the real embedding [Re d, Im d]
+        d = np.concatenate([d.real, d.imag])
+    assert rel(d, d_ref) < 1e-8
