@@ -981,6 +981,7 @@ size_t obuild_bytes(const OPlan& p, int model, int64_t n, int n_vis, int hidden,
   size_t b = align256((size_t)n * hidden * sS);                    // t
   if (model == MODEL_MLP) b += align256((size_t)n * hidden * 8);    // g
   b += align256((size_t)n * OTF_XW * 8);                           // packed inputs
+  b += align256((size_t)n * (cplx ? n_vis : (n_vis + 1) & ~1) * sS);  // inputs as table entries
   if (gemm_stats(cplx, model, n_vis, hidden)) {                           // DMMA stats scratch
     OtfPlan op;
     if (make_otf_plan(n, n_vis, hidden, op) == IRL_OK) b += otf_ws_layout(op, n, hidden, nullptr).bytes;
@@ -1060,6 +1061,18 @@ int obuild_impl(bool cplx, int model, const uint8_t* x, int64_t n, int n_vis, in
     IRL_TRY(pack_bits(x, n, n_vis, xbits, st));
   }
   off += align256((size_t)n * OTF_XW * 8);
+  const int xrow = cplx ? n_vis : (n_vis + 1) & ~1;
+  void* xd = base + off;
+  off += align256((size_t)n * xrow * sS);
+  {
+    const int64_t total = n * xrow;
+    const unsigned grid = (unsigned)std::min<int64_t>(cdiv(total, 256), 4 * 148 * 8);
+    if (cplx)
+      k_x_expand<true><<<grid, 256, 0, st>>>(x, n, n_vis, xrow, reinterpret_cast<double2*>(xd));
+    else
+      k_x_expand<false><<<grid, 256, 0, st>>>(x, n, n_vis, xrow, reinterpret_cast<double*>(xd));
+    IRL_TRY(cuda_check(cudaGetLastError(), "x expand launch"));
+  }
   if (model == MODEL_RBM) {
     const double* bvec = theta + (size_t)n_vis * (cplx ? 2 : 1);
     const double* Wm = theta + (size_t)(n_vis + hidden) * (cplx ? 2 : 1);
@@ -1075,6 +1088,8 @@ int obuild_impl(bool cplx, int model, const uint8_t* x, int64_t n, int n_vis, in
   }
   ORowArgs a{};
   a.x = x;
+  a.xd = xd;
+  a.xrow = xrow;
   a.n_rows = n;
   a.n_vis = n_vis;
   a.hidden = hidden;
@@ -1092,16 +1107,17 @@ int obuild_impl(bool cplx, int model, const uint8_t* x, int64_t n, int n_vis, in
   a.nb = p.nb;
   const int tab_len = model == MODEL_MLP ? orow_tab_len<MODEL_MLP>(n_vis, hidden) : orow_tab_len<MODEL_RBM>(n_vis, hidden);
   const size_t tab_bytes = (size_t)((tab_len + 1) & ~1) * sS;
-  // rows per staging group: amortise the per-group barrier, ~48 KB of tables
-  const int R = (int)std::max<size_t>(1, std::min<size_t>(8, (size_t)(24 * 1024) / tab_bytes));
-  const size_t smem = 2 * (size_t)R * tab_bytes;
+  // per staging buffer: at least one full-width table (tiles spanning the short
+  // blocks), else 16 KB of compact per-tile tables (k_orows sizes its groups)
+  const size_t buf_bytes = rup(std::max<size_t>(tab_bytes, 16 * 1024), 16);
+  const size_t smem = ORW_NBUF * (buf_bytes + (size_t)ORW_RMAX * (8 + sS));
   {
     DevInfo d;
     IRL_TRY(dev_info(d));
     if (smem > (size_t)d.smem_optin) return fail(IRL_ERR_ARG, "hidden layer too wide for the row table");
     IRL_TRY(ensure_fn_attrs((const void*)p.fn, d.smem_optin));
   }
-  p.fn<<<(unsigned)(p.nb * p.C), p.NT, smem, st>>>(a, R);
+  p.fn<<<(unsigned)(p.nb * p.C), p.NT, smem, st>>>(a, (int)buf_bytes);
   IRL_TRY(cuda_check(cudaGetLastError(), "orows launch"));
   if (gstats) {
     // column statistics from the hidden activations and the packed inputs

@@ -20,6 +20,9 @@ namespace irl {
 
 enum { MODEL_RBM = 0, MODEL_MLP = 1 };
 
+constexpr int ORW_NBUF = 3;   // staging buffers of the O-row writer
+constexpr int ORW_RMAX = 32;  // rows per staging group at most
+
 // complex tanh: (sinh 2a + i sin 2b) / (cosh 2a + cos 2b)
 __device__ __forceinline__ double2 ctanh(double2 z) {
   const double d = cosh(2.0 * z.x) + cos(2.0 * z.y);
@@ -103,7 +106,23 @@ struct ORowArgs {
   double2* part0;     // [nb][ld_u]  sum w conj(O)
   double2* part1;     // [nb][ld_u]  sum c conj(O)
   int W, C, nb;
+  const void* xd;     // S[N][xrow]: the inputs as table entries (0/1), or null
+  int xrow;
 };
+
+// x (N x n uint8) -> S[N][xrow] 0/1 table entries (zero padded), for the
+// asynchronous row staging of the O-row writer
+template <bool CPLX>
+__global__ void k_x_expand(const uint8_t* __restrict__ x, int64_t n_rows, int n_vis, int xrow,
+                           typename Traits<CPLX>::S* __restrict__ xd) {
+  const int64_t total = n_rows * xrow;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / xrow;
+    const int i = (int)(e % xrow);
+    const double v = (i < n_vis && x[r * n_vis + i]) ? 1.0 : 0.0;
+    if constexpr (CPLX) xd[e] = make_double2(v, 0.0); else xd[e] = v;
+  }
+}
 
 // Per-row factor table (S-typed, in shared memory):
 //   [0] = 0, [1] = 1, [2, 2+h) = t_n, [2+h, 2+2h) = g_n (MLP), then x_n (0/1).
@@ -149,32 +168,97 @@ __device__ __forceinline__ uint32_t elem_pair(int64_t p, int n, int h, int64_t P
   return (ia << 16) | ib;
 }
 
-// stage the factor table of row n into tab (cp.async for t/g, direct for x)
+// Compact per-tile factor table.  A column tile only touches a contiguous
+// range of hidden units, so each CTA stages just that range:
+//   [0] = 0, [1] = 1, [2, 2+tl) = t[t_lo ..], [2+tl, 2+tl+gl) = g[g_lo ..], then x.
+struct TabRange {
+  int t_lo, tl, tn;  // first unit, table slots (even), units to stage (<= tl, inside [0, h))
+  int g_lo, gl, gn;
+  int len;           // table entries, even
+};
+
+template <int MODEL>
+__device__ __forceinline__ TabRange tab_range(int64_t e0, int64_t e1, int n, int h, int64_t P, bool even_align) {
+  // element range [e0, e1) of this tile (clipped to P) -> hidden-unit hulls
+  e1 = min(e1, P);
+  int tlo = h, thi = -1, glo = h, ghi = -1;
+  auto addt = [&](int64_t a, int64_t b) { if (a <= b) { tlo = min(tlo, (int)a); thi = max(thi, (int)b); } };
+  auto addg = [&](int64_t a, int64_t b) { if (a <= b) { glo = min(glo, (int)a); ghi = max(ghi, (int)b); } };
+  if (e0 < e1) {
+    if constexpr (MODEL == MODEL_RBM) {
+      const int64_t bb = n, wb = (int64_t)n + h;
+      addt(max(e0, bb) - bb, min(e1, wb) - 1 - bb);                               // b block: t_j
+      if (e1 > wb) addt((max(e0, wb) - wb) / n, (e1 - 1 - wb) / n);              // W block: t_j x_i
+    } else {
+      const int64_t hn = (int64_t)h * n;
+      if (e0 < hn) addg(e0 / n, (min(e1, hn) - 1) / n);                          // W block: g_j x_k
+      addg(max(e0, hn) - hn, min(e1, hn + h) - 1 - hn);                          // b block: g_j
+      addt(max(e0, hn + h) - hn - h, min(e1, hn + 2 * h) - 1 - hn - h);          // u block: t_j
+    }
+  }
+  TabRange r;
+  if (thi < tlo) { tlo = 0; thi = -1; }
+  if (ghi < glo) { glo = 0; ghi = -1; }
+  if (even_align) {  // 16-byte cp.async chunks of a real (8-byte) row
+    tlo &= ~1;
+    thi = (thi < 0) ? -1 : min(h - 1, thi | 1);
+    glo &= ~1;
+    ghi = (ghi < 0) ? -1 : min(h - 1, ghi | 1);
+  }
+  r.t_lo = tlo;
+  r.tn = thi - tlo + 1;
+  r.tl = (r.tn + 1) & ~1;  // even slot counts keep the x block 16-byte aligned
+  r.g_lo = glo;
+  r.gn = ghi - glo + 1;
+  r.gl = (r.gn + 1) & ~1;
+  r.len = (2 + r.tl + r.gl + n + 1) & ~1;
+  return r;
+}
+
+// full-layout factor index (elem_pair) -> compact index
+__device__ __forceinline__ uint32_t tab_remap(uint32_t ia, const TabRange& r, int h, int mlp) {
+  const uint32_t OT = 2, OG = 2 + h, OX = 2 + h * (mlp ? 2 : 1);
+  if (ia < OT) return ia;
+  if (ia < OT + h) return 2 + (ia - OT - r.t_lo);
+  if (mlp && ia < OG + h) return 2 + r.tl + (ia - OG - r.g_lo);
+  return 2 + r.tl + r.gl + (ia - OX);
+}
+
+// stage the compact factor table of row n into tab (cp.async for t/g, direct for x)
 template <bool CPLX, int MODEL>
-__device__ __forceinline__ void orow_stage(const ORowArgs& a, int64_t n, typename Traits<CPLX>::S* tab, int tid,
-                                           int nthreads) {
+__device__ __forceinline__ void orow_stage(const ORowArgs& a, int64_t n, const TabRange& rg,
+                                           typename Traits<CPLX>::S* tab, int tid, int nthreads) {
   using S = typename Traits<CPLX>::S;
   const int h = a.hidden, nv = a.n_vis;
-  const int OX = 2 + h * (MODEL == MODEL_MLP ? 2 : 1);
+  const int OX = 2 + rg.tl + rg.gl;
   const S* trow = reinterpret_cast<const S*>(a.T) + (size_t)n * h;
   if (CPLX || (h & 1) == 0) {  // rows 16-B aligned: async copy
-    const int tchunks = (int)((size_t)h * sizeof(S) / 16);
+    const int tchunks = (int)((size_t)rg.tn * sizeof(S) / 16);
+    const char* tsrc = reinterpret_cast<const char*>(trow + rg.t_lo);
     for (int c = tid; c < tchunks; c += nthreads) {
       const uint32_t d = smem_addr(reinterpret_cast<char*>(tab + 2) + 16 * c);
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(reinterpret_cast<const char*>(trow) + 16 * c)
-                   : "memory");
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(tsrc + 16 * c) : "memory");
     }
     if constexpr (MODEL == MODEL_MLP) {
-      const char* grow = reinterpret_cast<const char*>(a.G + (size_t)n * h);
-      for (int c = tid; c < h / 2; c += nthreads) {
-        const uint32_t d = smem_addr(reinterpret_cast<char*>(tab + 2 + h) + 16 * c);
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(grow + 16 * c) : "memory");
+      const char* gsrc = reinterpret_cast<const char*>(a.G + (size_t)n * h + rg.g_lo);
+      for (int c = tid; c < rg.gn / 2; c += nthreads) {
+        const uint32_t d = smem_addr(reinterpret_cast<char*>(tab + 2 + rg.tl) + 16 * c);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gsrc + 16 * c) : "memory");
       }
     }
   } else {  // odd hidden width (real): plain loads
-    for (int j = tid; j < h; j += nthreads) tab[2 + j] = trow[j];
+    for (int j = tid; j < rg.tn; j += nthreads) tab[2 + j] = trow[rg.t_lo + j];
     if constexpr (MODEL == MODEL_MLP)
-      for (int j = tid; j < h; j += nthreads) tab[2 + h + j] = a.G[(size_t)n * h + j];
+      for (int j = tid; j < rg.gn; j += nthreads) tab[2 + rg.tl + j] = a.G[(size_t)n * h + rg.g_lo + j];
+  }
+  if (a.xd) {  // expanded inputs: 16-byte asynchronous chunks
+    const int xchunks = (int)((size_t)a.xrow * sizeof(S) / 16);
+    const char* xsrc = reinterpret_cast<const char*>(reinterpret_cast<const S*>(a.xd) + (size_t)n * a.xrow);
+    for (int c = tid; c < xchunks; c += nthreads) {
+      const uint32_t d = smem_addr(reinterpret_cast<char*>(tab + OX) + 16 * c);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(xsrc + 16 * c) : "memory");
+    }
+    return;
   }
   for (int i = tid; i < nv; i += nthreads) {
     const double xv = a.x[n * nv + i] ? 1.0 : 0.0;
@@ -185,7 +269,7 @@ __device__ __forceinline__ void orow_stage(const ORowArgs& a, int64_t n, typenam
 // STATS: accumulate the column statistics in the writer (complex RBM); real
 // models get them from the DMMA GEMMs of otf.cuh instead (lighter writer).
 template <bool CPLX, int MODEL, int PPT, bool STATS>
-__global__ void __launch_bounds__(512) k_orows(const ORowArgs a, int R) {
+__global__ void __launch_bounds__(512) k_orows(const ORowArgs a, int buf_bytes) {
   using T = Traits<CPLX>;
   using S = typename T::S;
   extern __shared__ __align__(16) unsigned char smem_r[];
@@ -196,8 +280,15 @@ __global__ void __launch_bounds__(512) k_orows(const ORowArgs a, int R) {
   const int64_t col0 = (a.ld_u * rank) / a.C;  // uneven split: any tile count
   const int W = (int)((a.ld_u * (rank + 1)) / a.C - col0);
   constexpr int E = Traits<CPLX>::kElemsPerUnit;
-  const int TL = (orow_tab_len<MODEL>(a.n_vis, a.hidden) + 1) & ~1;
-  S* tabs = reinterpret_cast<S*>(smem_r);  // [2][R][TL] factor tables, R rows per group
+  const TabRange rg = tab_range<MODEL>(col0 * E, (col0 + W) * E, a.n_vis, a.hidden, a.p, !CPLX);
+  const int TL = rg.len;
+  // rows per staging group: as many compact tables as one buffer holds (<= ORW_RMAX)
+  const int R = max(1, min(ORW_RMAX, buf_bytes / (TL * (int)sizeof(S))));
+  // 3 staging buffers of R rows: factor tables, then the rows' w_n and c_n
+  constexpr int NBUF = ORW_NBUF;
+  S* tabs = reinterpret_cast<S*>(smem_r);                                   // [NBUF][R][TL]
+  double* wsm = reinterpret_cast<double*>(smem_r + (size_t)NBUF * buf_bytes); // [NBUF][RMAX]
+  S* csm = reinterpret_cast<S*>(wsm + NBUF * ORW_RMAX);                       // [NBUF][RMAX]
 
   // smem byte offsets of the two factors of each element (relative to the row table)
   uint32_t pr[PPT][E];
@@ -210,12 +301,14 @@ __global__ void __launch_bounds__(512) k_orows(const ORowArgs a, int R) {
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       const uint32_t q = (idx < W) ? elem_pair<MODEL>(u * E + e, a.n_vis, a.hidden, a.p) : 1u;
-      pr[k][e] = (((q >> 16) * (uint32_t)sizeof(S)) << 16) | ((q & 0xffffu) * (uint32_t)sizeof(S));
+      const uint32_t ia = tab_remap(q >> 16, rg, a.hidden, MODEL == MODEL_MLP);
+      const uint32_t ib = tab_remap(q & 0xffffu, rg, a.hidden, MODEL == MODEL_MLP);
+      pr[k][e] = ((ia * (uint32_t)sizeof(S)) << 16) | (ib * (uint32_t)sizeof(S));
     }
     acc0[k] = make_double2(0.0, 0.0);
     acc1[k] = make_double2(0.0, 0.0);
   }
-  for (int e = tid; e < 2 * R; e += NT) {
+  for (int e = tid; e < NBUF * R; e += NT) {
     if constexpr (CPLX) {
       tabs[e * TL] = make_double2(0.0, 0.0);
       tabs[e * TL + 1] = make_double2(1.0, 0.0);
@@ -229,55 +322,70 @@ __global__ void __launch_bounds__(512) k_orows(const ORowArgs a, int R) {
   auto stage_group = [&](int g) {
     const int64_t n0 = lo + (int64_t)g * R;
     const int rows = (int)min((int64_t)R, hi - n0);
-    S* base = tabs + (size_t)(g & 1) * R * TL;
-    for (int r = 0; r < rows; ++r) orow_stage<CPLX, MODEL>(a, n0 + r, base + (size_t)r * TL, tid, NT);
-    asm volatile("cp.async.commit_group;" ::: "memory");
+    const int b = g % NBUF;
+    S* base = tabs + (size_t)b * R * TL;
+    for (int r = 0; r < rows; ++r) orow_stage<CPLX, MODEL>(a, n0 + r, rg, base + (size_t)r * TL, tid, NT);
+    if constexpr (STATS) {
+      for (int r = tid; r < rows; r += NT) {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(wsm + b * ORW_RMAX + r)),
+                     "l"(a.w + n0 + r)
+                     : "memory");
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_addr(csm + b * ORW_RMAX + r)),
+                     "l"(cf + n0 + r), "n"(sizeof(S))
+                     : "memory");
+      }
+    }
   };
-  if (G > 0) stage_group(0);
+  // two groups in flight: group g is waited for at iteration g, with g + 1 still pending
+  for (int g = 0; g < NBUF - 1; ++g) {
+    if (g < G) stage_group(g);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
   for (int g = 0; g < G; ++g) {
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
     __syncthreads();  // group g staged; every thread is done with group g-1's buffer
-    if (g + 1 < G) stage_group(g + 1);
+    if (g + NBUF - 1 < G) stage_group(g + NBUF - 1);
+    asm volatile("cp.async.commit_group;" ::: "memory");
     const int64_t n0 = lo + (int64_t)g * R;
     const int rows = (int)min((int64_t)R, hi - n0);
-    const S* base = tabs + (size_t)(g & 1) * R * TL;
+    const int b = g % NBUF;
+    const S* base = tabs + (size_t)b * R * TL;
     double2* orow = a.O + n0 * a.ld_u + col0 + tid;
     const char* tbase = reinterpret_cast<const char*>(base);
     for (int r = 0; r < rows; ++r, orow += a.ld_u, tbase += (size_t)TL * sizeof(S)) {
-      const int64_t n = n0 + r;
       double wn = 0.0;
       S cn = T::zero();
       if constexpr (STATS) {
-        wn = __ldg(a.w + n);
-        cn = cf[n];
+        wn = wsm[b * ORW_RMAX + r];
+        cn = csm[b * ORW_RMAX + r];
       }
+      // every unit computed (invalid ones read the table's constant slots): only
+      // the store is predicated, so the table loads of all PPT units issue together
 #pragma unroll
       for (int k = 0; k < PPT; ++k) {
-        if (k < kval) {
-          double2 u;
-          if constexpr (CPLX) {
-            const S fa = *reinterpret_cast<const S*>(tbase + (pr[k][0] >> 16));
-            const S fb = *reinterpret_cast<const S*>(tbase + (pr[k][0] & 0xffffu));
-            u = T::mul(fa, fb);
-            if constexpr (STATS) {
-              acc0[k].x = fma(wn, u.x, acc0[k].x);
-              acc0[k].y = fma(-wn, u.y, acc0[k].y);
-              T::axpy(acc1[k], u, cn);
-            }
-          } else {
-            u.x = *reinterpret_cast<const double*>(tbase + (pr[k][0] >> 16)) *
-                  *reinterpret_cast<const double*>(tbase + (pr[k][0] & 0xffffu));
-            u.y = *reinterpret_cast<const double*>(tbase + (pr[k][1] >> 16)) *
-                  *reinterpret_cast<const double*>(tbase + (pr[k][1] & 0xffffu));
-            if constexpr (STATS) {
-              acc0[k].x = fma(wn, u.x, acc0[k].x);
-              acc0[k].y = fma(wn, u.y, acc0[k].y);
-              acc1[k].x = fma(cn, u.x, acc1[k].x);
-              acc1[k].y = fma(cn, u.y, acc1[k].y);
-            }
+        double2 u;
+        if constexpr (CPLX) {
+          const S fa = *reinterpret_cast<const S*>(tbase + (pr[k][0] >> 16));
+          const S fb = *reinterpret_cast<const S*>(tbase + (pr[k][0] & 0xffffu));
+          u = T::mul(fa, fb);
+          if constexpr (STATS) {
+            acc0[k].x = fma(wn, u.x, acc0[k].x);
+            acc0[k].y = fma(-wn, u.y, acc0[k].y);
+            T::axpy(acc1[k], u, cn);
           }
-          st_stream(orow + k * NT, u);
+        } else {
+          u.x = *reinterpret_cast<const double*>(tbase + (pr[k][0] >> 16)) *
+                *reinterpret_cast<const double*>(tbase + (pr[k][0] & 0xffffu));
+          u.y = *reinterpret_cast<const double*>(tbase + (pr[k][1] >> 16)) *
+                *reinterpret_cast<const double*>(tbase + (pr[k][1] & 0xffffu));
+          if constexpr (STATS) {
+            acc0[k].x = fma(wn, u.x, acc0[k].x);
+            acc0[k].y = fma(wn, u.y, acc0[k].y);
+            acc1[k].x = fma(cn, u.x, acc1[k].x);
+            acc1[k].y = fma(cn, u.y, acc1[k].y);
+          }
         }
+        if (k < kval) st_stream(orow + k * NT, u);
       }
     }
   }
