@@ -25,6 +25,7 @@ IRL_ERR_DEVICE = 5
 MVP_AUTO = 0
 MVP_FUSED = 1
 MVP_TWO_PASS = 2
+MVP_ROWS = 3
 
 MODEL_RBM = 0
 MODEL_MLP = 1
@@ -149,5 +150,5 @@ def mvp_plan(n: int, ld: int, is_complex: bool, mode: int = MVP_AUTO) -> dict:
     check("irl_mvp_plan", code)
     keys = ("cluster", "units_per_slice", "threads", "rows_per_stage", "stages", "row_blocks", "units_per_thread")
     out = dict(zip(keys, list(geom)))
-    out["path"] = {MVP_FUSED: "fused", MVP_TWO_PASS: "two_pass"}[path.value]
+    out["path"] = {MVP_FUSED: "fused", MVP_TWO_PASS: "two_pass", MVP_ROWS: "rows"}[path.value]
     return out

@@ -17,6 +17,7 @@
 #include "otf.cuh"
 #include "lanczos.cuh"
 #include "stream.cuh"
+#include "rows.cuh"
 
 using namespace irl;
 
@@ -76,7 +77,11 @@ int ensure_fn_attrs(const void* fn, int smem_optin) {
   static std::unordered_set<const void*> done;
   std::lock_guard<std::mutex> lk(mu);
   if (done.count(fn)) return IRL_OK;
-  IRL_TRY(cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin),
+  cudaFuncAttributes fa;
+  IRL_TRY(cuda_check(cudaFuncGetAttributes(&fa, fn), "cudaFuncGetAttributes"));
+  // dynamic + static shared memory must fit the opt-in limit
+  IRL_TRY(cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          smem_optin - (int)fa.sharedSizeBytes),
                      "cudaFuncSetAttribute(smem)"));
   // cluster size 16 is non-portable; harmless for non-cluster launches
   cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -382,6 +387,45 @@ MvpWs mvp_ws_layout(const Plan& p, int64_t n, int64_t ld_u, bool cplx, void* bas
   return w;
 }
 
+// warp-per-row path (rows.cuh): narrow rows only
+constexpr int64_t kRowsMaxUnits = 512;
+
+using RowsFn = void (*)(StreamArgs);
+RowsFn pick_rows(bool cplx, int64_t ld_u) {
+  const int upl = (int)cdiv(ld_u, 32);
+  if (upl <= 4) return cplx ? k_rows_mvp<true, 4> : k_rows_mvp<false, 4>;
+  if (upl <= 8) return cplx ? k_rows_mvp<true, 8> : k_rows_mvp<false, 8>;
+  if (upl <= 16) return cplx ? k_rows_mvp<true, 16> : k_rows_mvp<false, 16>;
+  return nullptr;
+}
+
+// rows plan: 2 CTAs per SM (or fewer for short problems); a Plan carrying the
+// partial count for the workspace layout
+int make_rows_plan(int64_t n, int64_t ld_u, Plan& p) {
+  if (ld_u > kRowsMaxUnits) return fail(IRL_ERR_DEVICE, "rows path needs ld <= %lld units", (long long)kRowsMaxUnits);
+  DevInfo d;
+  IRL_TRY(dev_info(d));
+  p = Plan{};
+  p.mode = MODE_FUSED;  // no tpart in the workspace
+  p.C = 1;
+  const int upl = (int)cdiv(ld_u, 32);
+  const int nw = upl <= 8 ? 8 : 12, per_sm = upl <= 8 ? 2 : 1;
+  p.nb = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm * d.sms, cdiv(n, 2 * nw)));
+  p.NT = nw * 32;
+  p.smem = (size_t)(nw + 1) * ld_u * 16;
+  return IRL_OK;
+}
+
+int launch_rows(const Plan& p, bool cplx, const StreamArgs& a, cudaStream_t st) {
+  RowsFn fn = pick_rows(cplx, a.ld_u);
+  if (!fn) return fail(IRL_ERR_DEVICE, "no rows instance for ld=%lld units", (long long)a.ld_u);
+  DevInfo d;
+  IRL_TRY(dev_info(d));
+  IRL_TRY(ensure_fn_attrs((const void*)fn, d.smem_optin));
+  fn<<<p.nb, p.NT, p.smem, st>>>(a);
+  return cuda_check(cudaGetLastError(), "rows kernel launch");
+}
+
 int mvp_impl(bool cplx, const double* O, int64_t n, int64_t p, int64_t ld, const double* obar, const double* coeff,
              const double* v_re, const double* v_im, double* out_re, double* out_im, const double* hf_re,
              const double* hf_im, const double* u0, double* out0, int mode, void* ws, size_t ws_bytes,
@@ -396,7 +440,10 @@ int mvp_impl(bool cplx, const double* O, int64_t n, int64_t p, int64_t ld, const
   const int64_t ld_u = cplx ? ld : ld / 2;
   int path = mode;
   Plan pl;
-  if (mode == IRL_MVP_AUTO || mode == IRL_MVP_FUSED) {
+  if ((mode == IRL_MVP_AUTO && ld_u <= kRowsMaxUnits) || mode == IRL_MVP_ROWS) {
+    IRL_TRY(make_rows_plan(n, ld_u, pl));
+    path = IRL_MVP_ROWS;
+  } else if (mode == IRL_MVP_AUTO || mode == IRL_MVP_FUSED) {
     int rc = make_plan(n, ld_u, cplx, MODE_FUSED, pl);
     // AUTO: the per-row DSMEM exchange of wide clusters costs more than the
     // second HBM pass (measured: C <= 2 wins, C >= 6 loses; tools/tune_cluster.py)
@@ -420,14 +467,19 @@ int mvp_impl(bool cplx, const double* O, int64_t n, int64_t p, int64_t ld, const
   a.hf_im = hf_im;
   a.obar = reinterpret_cast<const double2*>(obar);
   a.coeff0 = coeff;
-  if (path == IRL_MVP_FUSED) {
+  if (path == IRL_MVP_FUSED || path == IRL_MVP_ROWS) {
     MvpWs w = mvp_ws_layout(pl, n, ld_u, cplx, ws);
     if (ws_bytes < w.bytes) return fail(IRL_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, w.bytes);
     a.part0 = w.part;
     a.ysum = w.ysum;
     a.spart = w.spart;
     a.gpart = w.gpart;
-    IRL_TRY(launch_stream(pl, a, st));
+    if (path == IRL_MVP_ROWS) {
+      a.n_rows = n;
+      IRL_TRY(launch_rows(pl, cplx, a, st));
+    } else {
+      IRL_TRY(launch_stream(pl, a, st));
+    }
     if (cplx)
       return launch_finish_mvp<true>(w.part, pl.nb, ld_u, w.ysum, a.obar, hf_re, hf_im, u0, out_re, out_im, w.gpart, 1,
                                      out0, st);
@@ -462,6 +514,7 @@ size_t mvp_ws_bytes(int64_t n, int64_t ld, bool cplx) {
   size_t best = 0;
   Plan p;
   if (make_plan(n, ld_u, cplx, MODE_FUSED, p) == IRL_OK) best = std::max(best, mvp_ws_layout(p, n, ld_u, cplx, nullptr).bytes);
+  if (make_rows_plan(n, ld_u, p) == IRL_OK) best = std::max(best, mvp_ws_layout(p, n, ld_u, cplx, nullptr).bytes);
   Plan p1, p2;
   if (make_plan(n, ld_u, cplx, MODE_DOT, p1) == IRL_OK && make_plan(n, ld_u, cplx, MODE_ACC, p2) == IRL_OK) {
     p1.nb = std::max(p1.nb, p2.nb);
@@ -1270,7 +1323,10 @@ int irl_mvp_plan(int64_t n, int64_t ld, int is_complex, int mode, int* out_path,
   const int64_t ld_u = is_complex ? ld : ld / 2;
   Plan p;
   int path = IRL_MVP_TWO_PASS;
-  if (mode == IRL_MVP_AUTO || mode == IRL_MVP_FUSED) {
+  if ((mode == IRL_MVP_AUTO && ld_u <= kRowsMaxUnits) || mode == IRL_MVP_ROWS) {
+    IRL_TRY(make_rows_plan(n, ld_u, p));
+    path = IRL_MVP_ROWS;
+  } else if (mode == IRL_MVP_AUTO || mode == IRL_MVP_FUSED) {
     if (make_plan(n, ld_u, is_complex != 0, MODE_FUSED, p) == IRL_OK &&
         (mode == IRL_MVP_FUSED || p.C <= kAutoMaxCluster)) {
       path = IRL_MVP_FUSED;
