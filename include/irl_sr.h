@@ -45,6 +45,7 @@ extern "C" {
 #define IRL_MVP_FUSED 1     /* one HBM pass, column slices over a CTA cluster (DSMEM exchange) */
 #define IRL_MVP_TWO_PASS 2  /* t = O v pass, then O^H y pass */
 #define IRL_MVP_ROWS 3      /* one HBM pass, a warp per row (narrow rows: ld <= 512 16-byte units) */
+#define IRL_MVP_WIDE 4      /* one HBM pass + one L2 pass, persistent column-sliced grid (very wide rows) */
 
 #define IRL_MODEL_RBM 0
 #define IRL_MODEL_MLP 1
@@ -118,7 +119,7 @@ int irl_mvp_c128(const double* O, int64_t n, int64_t p, int64_t ld, const double
                  const double* v_re, const double* v_im, double* out_re, double* out_im, const double* hf_re,
                  const double* hf_im, const double* u0, double* out0, int mode, void* ws, size_t ws_bytes,
                  void* stream);
-/* Which path (IRL_MVP_FUSED / IRL_MVP_TWO_PASS / IRL_MVP_ROWS) AUTO takes, and its launch
+/* Which path (IRL_MVP_FUSED / IRL_MVP_TWO_PASS / IRL_MVP_ROWS / IRL_MVP_WIDE) AUTO takes, and its launch
  * geometry (cluster size, units per slice, threads, rows per stage, stages,
  * row blocks); for benches and tests.  Returns IRL_OK or an error. */
 int irl_mvp_plan(int64_t n, int64_t ld, int is_complex, int mode, int* out_path, int* out_geom7);

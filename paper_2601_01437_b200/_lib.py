@@ -26,6 +26,7 @@ MVP_AUTO = 0
 MVP_FUSED = 1
 MVP_TWO_PASS = 2
 MVP_ROWS = 3
+MVP_WIDE = 4
 
 MODEL_RBM = 0
 MODEL_MLP = 1
@@ -150,5 +151,5 @@ def mvp_plan(n: int, ld: int, is_complex: bool, mode: int = MVP_AUTO) -> dict:
     check("irl_mvp_plan", code)
     keys = ("cluster", "units_per_slice", "threads", "rows_per_stage", "stages", "row_blocks", "units_per_thread")
     out = dict(zip(keys, list(geom)))
-    out["path"] = {MVP_FUSED: "fused", MVP_TWO_PASS: "two_pass", MVP_ROWS: "rows"}[path.value]
+    out["path"] = {MVP_FUSED: "fused", MVP_TWO_PASS: "two_pass", MVP_ROWS: "rows", MVP_WIDE: "wide"}[path.value]
     return out

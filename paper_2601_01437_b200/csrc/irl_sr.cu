@@ -18,6 +18,7 @@
 #include "lanczos.cuh"
 #include "stream.cuh"
 #include "rows.cuh"
+#include "wide.cuh"
 
 using namespace irl;
 
@@ -426,6 +427,85 @@ int launch_rows(const Plan& p, bool cplx, const StreamArgs& a, cudaStream_t st) 
   return cuda_check(cudaGetLastError(), "rows kernel launch");
 }
 
+// ----------------------------------------------------------------- wide ---
+// AUTO does not take the wide path yet: at cfg4 / cfg5 it reads O once from HBM
+// (ncu: 62.4 GB of 61.5) but its consumers are latency-bound per row block
+// (30 / 35 ms against 17.4 / 30.5 ms for the two-pass path); IRL_MVP_WIDE
+// selects it explicitly.
+constexpr int64_t kWideMinUnits = INT64_MAX;
+
+struct WidePlan {
+  int G, R, NS, RB, WM, ppt;
+  size_t smem, ws;
+};
+
+using WideFn = void (*)(WideArgs);
+WideFn pick_wide(bool cplx, int upl) {
+  switch (upl) {
+    case 8: return cplx ? k_wide<true, 8> : k_wide<false, 8>;
+    case 16: return cplx ? k_wide<true, 16> : k_wide<false, 16>;
+    case 24: return cplx ? k_wide<true, 24> : k_wide<false, 24>;
+    default: return nullptr;
+  }
+}
+
+int make_wide_plan(int64_t n, int64_t ld_u, bool cplx, WidePlan& p) {
+  DevInfo d;
+  IRL_TRY(dev_info(d));
+  p.G = d.sms;
+  p.WM = (int)cdiv(ld_u, p.G);
+  const int need = (int)cdiv(p.WM, 32);  // units per lane (warp per row slice)
+  p.ppt = need <= 8 ? 8 : need <= 16 ? 16 : need <= 24 ? 24 : 0;
+  if (!p.ppt) return fail(IRL_ERR_DEVICE, "wide path needs ld <= %d units per SM slice", 24 * 32);
+  const size_t sS = cplx ? 16 : 8;
+  const int64_t row_bytes = ld_u * 16;
+  p.RB = WIDE_NW;  // one row slice per consumer warp per stage
+  const int64_t target = (getenv("IRL_WIDE_MB") ? atoll(getenv("IRL_WIDE_MB")) : 24) << 20;
+  p.R = (int)std::max<int64_t>(p.RB, std::min<int64_t>(512, target / row_bytes));
+  p.R = (int)std::min<int64_t>(rup(p.R, p.RB), std::max<int64_t>(rup(n, p.RB), p.RB));
+  const size_t fixed = (size_t)p.R * sS + (size_t)p.WM * 16 + 64;
+  const size_t budget = (size_t)std::min(d.smem_optin - 4096, 210 * 1024);
+  p.NS = (int)std::min<int64_t>(16, (int64_t)((budget - fixed) / ((size_t)p.RB * p.WM * 16 + 16)));
+  if (p.NS < 2) return fail(IRL_ERR_DEVICE, "wide path: row slices too wide for the ring");
+  p.smem = (size_t)p.NS * p.RB * p.WM * 16 + (size_t)2 * p.NS * 8 + fixed;
+  p.ws = align256((size_t)3 * p.R * p.G * sS) + align256((size_t)p.G * 8) + 256;
+  return IRL_OK;
+}
+
+int launch_wide(const WidePlan& p, bool cplx, WideArgs a, void* ws, cudaStream_t st) {
+  WideFn fn = pick_wide(cplx, p.ppt);
+  DevInfo d;
+  IRL_TRY(dev_info(d));
+  IRL_TRY(ensure_fn_attrs((const void*)fn, d.smem_optin));
+  char* base = static_cast<char*>(ws);
+  const size_t sS = cplx ? 16 : 8;
+  a.tpart = base;
+  size_t off = align256((size_t)3 * p.R * p.G * sS);
+  a.gpart = reinterpret_cast<double*>(base + off);
+  off += align256((size_t)p.G * 8);
+  a.counter = reinterpret_cast<unsigned int*>(base + off);
+  a.error = reinterpret_cast<int*>(base + off + 4);
+  a.R = p.R;
+  a.NS = p.NS;
+  a.RB = p.RB;
+  a.WM = p.WM;
+  IRL_TRY(cuda_check(cudaMemsetAsync(a.counter, 0, 8, st), "wide counter reset"));
+  int occ = 0;
+  IRL_TRY(cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)fn, WIDE_NT + 32, p.smem), "occ"));
+  if (occ < 1) return fail(IRL_ERR_DEVICE, "wide kernel does not fit on an SM");
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // all G CTAs co-resident: the grid counter cannot deadlock
+  attr[0].val.cooperative = 1;
+  cfg.gridDim = dim3(p.G);
+  cfg.blockDim = dim3(WIDE_NT + 32);
+  cfg.dynamicSmemBytes = p.smem;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cuda_check(cudaLaunchKernelEx(&cfg, fn, a), "wide kernel launch");
+}
+
 int mvp_impl(bool cplx, const double* O, int64_t n, int64_t p, int64_t ld, const double* obar, const double* coeff,
              const double* v_re, const double* v_im, double* out_re, double* out_im, const double* hf_re,
              const double* hf_im, const double* u0, double* out0, int mode, void* ws, size_t ws_bytes,
@@ -440,9 +520,29 @@ int mvp_impl(bool cplx, const double* O, int64_t n, int64_t p, int64_t ld, const
   const int64_t ld_u = cplx ? ld : ld / 2;
   int path = mode;
   Plan pl;
+  WidePlan wp{};
   if ((mode == IRL_MVP_AUTO && ld_u <= kRowsMaxUnits) || mode == IRL_MVP_ROWS) {
     IRL_TRY(make_rows_plan(n, ld_u, pl));
     path = IRL_MVP_ROWS;
+  } else if ((mode == IRL_MVP_AUTO && ld_u >= kWideMinUnits && make_wide_plan(n, ld_u, cplx, wp) == IRL_OK) ||
+             mode == IRL_MVP_WIDE) {
+    IRL_TRY(make_wide_plan(n, ld_u, cplx, wp));
+    if (ws_bytes < wp.ws) return fail(IRL_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, wp.ws);
+    WideArgs wa{};
+    wa.O = reinterpret_cast<const double2*>(O);
+    wa.n_rows = n;
+    wa.ld_u = ld_u;
+    wa.v_re = v_re;
+    wa.v_im = v_im;
+    wa.hf_re = hf_re;
+    wa.hf_im = hf_im;
+    wa.obar = reinterpret_cast<const double2*>(obar);
+    wa.coeff = coeff;
+    wa.u0 = u0;
+    wa.out_re = out_re;
+    wa.out_im = out_im;
+    wa.out0 = out0;
+    return launch_wide(wp, cplx, wa, ws, st);
   } else if (mode == IRL_MVP_AUTO || mode == IRL_MVP_FUSED) {
     int rc = make_plan(n, ld_u, cplx, MODE_FUSED, pl);
     // AUTO: the per-row DSMEM exchange of wide clusters costs more than the
@@ -515,6 +615,8 @@ size_t mvp_ws_bytes(int64_t n, int64_t ld, bool cplx) {
   Plan p;
   if (make_plan(n, ld_u, cplx, MODE_FUSED, p) == IRL_OK) best = std::max(best, mvp_ws_layout(p, n, ld_u, cplx, nullptr).bytes);
   if (make_rows_plan(n, ld_u, p) == IRL_OK) best = std::max(best, mvp_ws_layout(p, n, ld_u, cplx, nullptr).bytes);
+  WidePlan wp;
+  if (make_wide_plan(n, ld_u, cplx, wp) == IRL_OK) best = std::max(best, wp.ws);
   Plan p1, p2;
   if (make_plan(n, ld_u, cplx, MODE_DOT, p1) == IRL_OK && make_plan(n, ld_u, cplx, MODE_ACC, p2) == IRL_OK) {
     p1.nb = std::max(p1.nb, p2.nb);
@@ -1323,9 +1425,17 @@ int irl_mvp_plan(int64_t n, int64_t ld, int is_complex, int mode, int* out_path,
   const int64_t ld_u = is_complex ? ld : ld / 2;
   Plan p;
   int path = IRL_MVP_TWO_PASS;
+  WidePlan wp{};
   if ((mode == IRL_MVP_AUTO && ld_u <= kRowsMaxUnits) || mode == IRL_MVP_ROWS) {
     IRL_TRY(make_rows_plan(n, ld_u, p));
     path = IRL_MVP_ROWS;
+  } else if ((mode == IRL_MVP_AUTO && ld_u >= kWideMinUnits && make_wide_plan(n, ld_u, is_complex != 0, wp) == IRL_OK) ||
+             mode == IRL_MVP_WIDE) {
+    IRL_TRY(make_wide_plan(n, ld_u, is_complex != 0, wp));
+    *out_path = IRL_MVP_WIDE;
+    int g[7] = {wp.G, wp.WM, WIDE_NT, wp.RB, wp.NS, wp.R, wp.ppt};  // slices, units/slice, threads, rows/stage, stages, rows/block, ppt
+    memcpy(out_geom7, g, sizeof(g));
+    return IRL_OK;
   } else if (mode == IRL_MVP_AUTO || mode == IRL_MVP_FUSED) {
     if (make_plan(n, ld_u, is_complex != 0, MODE_FUSED, p) == IRL_OK &&
         (mode == IRL_MVP_FUSED || p.C <= kAutoMaxCluster)) {

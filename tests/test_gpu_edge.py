@@ -60,7 +60,7 @@ def test_ragged_shapes_complex_raw(E, n, p):
         en = E.estimate_energy(b)
     mean, _, _ = oest.energy(w, e, 0)
     v = rng.standard_normal(p)
-    for mode in (1, 2, 3):
+    for mode in (1, 2, 3, 4):
         assert rel(E.heff_matvec(b, en, v, mode=mode), oest.heff(w, e, o, mean, v)) < 1e-10
 
 
@@ -104,7 +104,7 @@ def test_host_tensor_inputs_and_outputs(E):
     assert out.is_cuda and rel(out.cpu().numpy(), ref) < 1e-10
 
 
-@pytest.mark.parametrize("mode", [1, 2, 3])
+@pytest.mark.parametrize("mode", [1, 2, 3, 4])
 def test_bitwise_determinism(E, mode):
     import torch
 

@@ -116,7 +116,7 @@ def main():
             vi, vo = vin, vout
         out = {"config": cfg.name, "gen_s": gen_s, "obuild_ms": min(ob),
                "obuild_gbs": N * P * b_el / (min(ob) / 1e3) / 1e9}
-        for mode, name, passes in ((1, "fused", 1), (2, "two_pass", 2), (3, "rows", 1)):
+        for mode, name, passes in ((1, "fused", 1), (2, "two_pass", 2), (3, "rows", 1), (4, "wide", 1)):
             try:
                 plan = _lib.mvp_plan(N, ld, batch.is_complex, mode)
                 E._apply(batch, coeff, vi, vo, mode=mode)
