@@ -459,7 +459,9 @@ int make_wide_plan(int64_t n, int64_t ld_u, bool cplx, WidePlan& p) {
   if (!p.ppt) return fail(IRL_ERR_DEVICE, "wide path needs ld <= %d units per SM slice", 24 * 32);
   const size_t sS = cplx ? 16 : 8;
   const int64_t row_bytes = ld_u * 16;
-  p.RB = WIDE_NW;  // one row slice per consumer warp per stage
+  // one or two row slices per consumer warp per stage (two when >= 3 stages still fit)
+  p.RB = (size_t)3 * 2 * WIDE_NW * p.WM * 16 <= (size_t)160 * 1024 ? 2 * WIDE_NW : WIDE_NW;
+  if (getenv("IRL_WIDE_RPW")) p.RB = WIDE_NW * std::max(1, std::min(2, atoi(getenv("IRL_WIDE_RPW"))));
   const int64_t target = (getenv("IRL_WIDE_MB") ? atoll(getenv("IRL_WIDE_MB")) : 24) << 20;
   p.R = (int)std::max<int64_t>(p.RB, std::min<int64_t>(512, target / row_bytes));
   p.R = (int)std::min<int64_t>(rup(p.R, p.RB), std::max<int64_t>(rup(n, p.RB), p.RB));

@@ -87,7 +87,8 @@ __global__ void __launch_bounds__(WIDE_NT + 32, 1) k_wide(const WideArgs a) {
   using S = typename T::S;
   extern __shared__ __align__(16) unsigned char smem_w[];
   const int NS = a.NS, WM = a.WM, R = a.R;
-  constexpr int RB = WIDE_NW;
+  const int RB = a.RB;  // WIDE_NW * rpw row slices per stage
+  const int rpw = RB / WIDE_NW;
   double2* ring = reinterpret_cast<double2*>(smem_w);                          // [NS][RB][WM]
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)NS * RB * WM);  // [NS]
   uint64_t* empty = full + NS;                                                 // [NS]
@@ -193,16 +194,30 @@ __global__ void __launch_bounds__(WIDE_NT + 32, 1) k_wide(const WideArgs a) {
     S* tp = tpart + ((size_t)(b % 3) * R) * G;
     for (int r = 0; r < rows; r += RB) {
       mbar_wait_bounded(&full[s], ph, a.error);
-      if (r + warp < rows) {
-        const double2* row = ring + ((size_t)s * RB + warp) * WM;
-        S t = T::zero();
+      // this warp's rows of the stage: warp, warp + NW (rpw <= 2); two partial
+      // accumulators per row keep the FMA chains short
+      S t[2][2];
 #pragma unroll
-        for (int k = 0; k < UPL; ++k) {
-          const int u = lane + 32 * k;
-          if (u < W) T::dot_acc(t, row[u], vs[u]);
+      for (int i = 0; i < 2; ++i) t[i][0] = t[i][1] = T::zero();
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int rr = warp + i * WIDE_NW;
+        if (i < rpw && r + rr < rows) {
+          const double2* row = ring + ((size_t)s * RB + rr) * WM;
+#pragma unroll
+          for (int k = 0; k < UPL; ++k) {
+            const int u = lane + 32 * k;
+            if (u < W) T::dot_acc(t[i][k & 1], row[u], vs[u]);
+          }
         }
-        t = warp_sum<CPLX>(t);
-        if (lane == 0) tp[(size_t)(r + warp) * G + c] = T::sub(t, s_c);
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int rr = warp + i * WIDE_NW;
+        if (i < rpw && r + rr < rows) {
+          const S tt = warp_sum<CPLX>(T::add(t[i][0], t[i][1]));
+          if (lane == 0) tp[(size_t)(r + rr) * G + c] = T::sub(tt, s_c);
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
@@ -251,13 +266,17 @@ __global__ void __launch_bounds__(WIDE_NT + 32, 1) k_wide(const WideArgs a) {
     named_bar_sync(1, WIDE_NT);
     for (int r = 0; r < rows; r += RB) {
       mbar_wait_bounded(&full[s], ph, a.error);
-      if (r + warp < rows) {
-        const double2* row = ring + ((size_t)s * RB + warp) * WM;
-        const S y = ys[r + warp];
 #pragma unroll
-        for (int k = 0; k < UPL; ++k) {
-          const int u = lane + 32 * k;
-          if (u < W) T::axpy(acc[k], row[u], y);
+      for (int i = 0; i < 2; ++i) {
+        const int rr = warp + i * WIDE_NW;
+        if (i < rpw && r + rr < rows) {
+          const double2* row = ring + ((size_t)s * RB + rr) * WM;
+          const S y = ys[r + rr];
+#pragma unroll
+          for (int k = 0; k < UPL; ++k) {
+            const int u = lane + 32 * k;
+            if (u < W) T::axpy(acc[k], row[u], y);
+          }
         }
       }
       __syncwarp();
