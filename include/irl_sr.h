@@ -182,6 +182,46 @@ int irl_lanczos_step_small(double* V, int64_t ldv, double* W, int64_t L, int j, 
 int irl_lanczos_step_cluster(double* V, int64_t ldv, double* W, int64_t L, int j, int m, double* ab, void* stream);
 int irl_host_qr_sweeps(int m, double* T, double* Q, const double* shifts, int nshift);
 
+/* ------------------------------------------------ §8(f) 1: completion ----
+ * Connected (two-configuration) product: heff_matvec + heff_offdiag_matvec
+ * (estimators.py:171-186 + :254-294, summed as the optimizer closure does,
+ * optimizer.py:144-147), with the optional bordered row/column of irl_mvp_*:
+ *   out = O_c^H (w corr + coeff (O_c v))        (real / raw complex: real part)
+ *   corr_n = sum_{e in seg(dist_index[n])} pcoeff_e (q_part[partner_row_e] - q_n)
+ *   q = O_c v,  q_part = (partner_O - obar) v
+ * The cache arrays mirror ConnectedCache (estimators.py:189-218): dist_index
+ * (N, int64) indexes the CSR segments indptr (n_dist + 1, int64); partner_row
+ * (nnz, int64) indexes rows of partner_O (n_partner x ld, padded like O);
+ * pcoeff (nnz, S) = <x|H|y> psi(y)/psi(x) (f64: its real part, which is exact
+ * for real O).  coeff may be NULL: the completion alone (heff_offdiag_matvec).
+ * All indices must be in range (the Python wrapper validates once per cache). */
+size_t irl_connected_workspace_bytes(int64_t n, int64_t n_partner, int64_t ld, int is_complex);
+int irl_connected_mvp_f64(const double* O, int64_t n, int64_t p, int64_t ld, const double* obar, const double* w,
+                          const double* coeff, const int64_t* dist_index, const int64_t* indptr,
+                          const int64_t* partner_row, const double* pcoeff, const double* partner_O,
+                          int64_t n_partner, const double* v, double* out, const double* half_f, const double* u0,
+                          double* out0, int mode, void* ws, size_t ws_bytes, void* stream);
+int irl_connected_mvp_c128(const double* O, int64_t n, int64_t p, int64_t ld, const double* obar, const double* w,
+                           const double* coeff, const int64_t* dist_index, const int64_t* indptr,
+                           const int64_t* partner_row, const double* pcoeff, const double* partner_O,
+                           int64_t n_partner, const double* v_re, const double* v_im, double* out_re,
+                           double* out_im, const double* hf_re, const double* hf_im, const double* u0, double* out0,
+                           int mode, void* ws, size_t ws_bytes, void* stream);
+
+/* Batched log psi of the shallow NQS (role of ansatz.log_amplitude,
+ * ansatz.py:200-247, for the BASELINE RBM / MLP), for the partner amplitude
+ * ratios psi(y)/psi(x) of the connected cache (estimators.py:248-252):
+ *   RBM  log psi = a.x + sum_j log cosh(b_j + W_j.x)   (c128: complex theta, complex out)
+ *   MLP  log psi = u.tanh(b + W x) + c
+ * x: N x n_vis uint8 (0/1); logpsi: N doubles (c128: N interleaved complex). */
+size_t irl_logamp_workspace_bytes(int64_t n, int hidden, int is_complex);
+int irl_logamp_rbm_f64(const uint8_t* x, int64_t n, int n_vis, int hidden, const double* theta, double* logpsi,
+                       void* ws, size_t ws_bytes, void* stream);
+int irl_logamp_rbm_c128(const uint8_t* x, int64_t n, int n_vis, int hidden, const double* theta, double* logpsi,
+                        void* ws, size_t ws_bytes, void* stream);
+int irl_logamp_mlp_f64(const uint8_t* x, int64_t n, int n_in, int hidden, const double* theta, double* logpsi,
+                       void* ws, size_t ws_bytes, void* stream);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

@@ -73,3 +73,42 @@ def dense_qgt(w, o):
     o_c = o - w @ o
     mat = ((o_c.conj().T * w) @ o_c).real
     return (mat + mat.T) / 2
+
+
+def heff_offdiag(w, o, dist_index, indptr, partner_row, coeff, partner_o, v):
+    """est:254-294 (real v): two-configuration completion, restated operation by operation.
+
+    q = (O - Obar) v, q_part = (O_part - Obar) v; corr per distinct config by
+    a segment sum (est:283-290); out = Re((w corr) @ conj(O_c)).
+    """
+    o_bar = w @ o
+    q_batch = (o - o_bar) @ v
+    q_part = (partner_o - o_bar) @ v if len(partner_o) else np.zeros(0)
+    n_dist = len(indptr) - 1
+    q_dist = np.zeros(n_dist, dtype=complex)
+    q_dist[dist_index] = q_batch
+    seg = np.repeat(np.arange(n_dist), np.diff(indptr))
+    corr_dist = np.zeros(n_dist, dtype=complex)
+    if len(seg):
+        np.add.at(corr_dist, seg, coeff * (q_part[partner_row] - q_dist[seg]))
+    corr = corr_dist[dist_index]
+    o_c = o - o_bar
+    return ((w * corr) @ o_c.conj()).real
+
+
+def heff_offdiag_hermitian(w, o, dist_index, indptr, partner_row, coeff, partner_o, v):
+    """Complex-parameter completion: the reference's est:254-294 on the real
+    embedding [O, iO] equals [Re z, Im z] with
+    z = sum_n w_n corr_n conj(O_c,n), q = O_c v for complex v."""
+    o_bar = w @ o
+    q_batch = (o - o_bar) @ v
+    q_part = (partner_o - o_bar) @ v if len(partner_o) else np.zeros(0, dtype=complex)
+    n_dist = len(indptr) - 1
+    q_dist = np.zeros(n_dist, dtype=complex)
+    q_dist[dist_index] = q_batch
+    seg = np.repeat(np.arange(n_dist), np.diff(indptr))
+    corr_dist = np.zeros(n_dist, dtype=complex)
+    if len(seg):
+        np.add.at(corr_dist, seg, coeff * (q_part[partner_row] - q_dist[seg]))
+    corr = corr_dist[dist_index]
+    return (w * corr) @ (o - o_bar).conj()

@@ -206,17 +206,161 @@ def case_krylov(seed=100, count=4):
     return out
 
 
+def bordered_connected(batch, energy, grad, cache):
+    """The reference optimizer's full operator, opt:140-148 WITH heff_offdiag_matvec (opt:146)."""
+    p = batch.param_count
+    half = 0.5 * grad
+
+    def matvec(u):
+        out = np.empty(p + 1)
+        out[0] = half @ u[1:]
+        out[1:] = u[0] * half + est.heff_matvec(batch, energy, u[1:]) + est.heff_offdiag_matvec(batch, cache, u[1:])
+        return out
+
+    return matvec
+
+
+def _cache_arrays(cache):
+    return dict(dist_index=np.array(cache.dist_index), indptr=np.array(cache.indptr),
+                partner_row=np.array(cache.partner_row), coeff=np.array(cache.coeff),
+                partner_o=np.array(cache.partner_o))
+
+
+def case_h2_connected(m=20):
+    """The reference's own connected completion (T/test_estimators.py:170-193):
+    H2 generic complex state, exact batch and a stochastic batch with duplicate
+    configurations (n_samples=64, seed=13, :71-80); both products, the sandwich
+    oracle and the full optimizer operator's IRL solve (opt:134-165)."""
+    from irlnqs.hamiltonian import build_dense_hamiltonian
+    from irlnqs.hilbert import enumerate_sector
+
+    with open(os.path.join(REF, "tests", "data", "h2_sto3g.fcidump")) as fh:
+        integrals = parse_fcidump(fh.read())
+    sector = integrals.sector()
+    arch = ans.Architecture(sector.n_orbitals, 3)
+    init = ans.init_parameters(arch, seed=9)
+    rng = np.random.default_rng(41)
+    params = ans.AnsatzParameters(arch, init.theta + 0.1 * rng.standard_normal(arch.param_count))
+    out = {}
+    for tag, kw in (("exact", {}), ("stoch", dict(n_samples=64, seed=13))):
+        batch = est.build_batch(params, integrals, sector, **kw)
+        energy = est.estimate_energy(batch)
+        grad = est.energy_gradient(batch, energy)
+        cache = est.build_connected_cache(params, integrals, sector, batch)
+        vs = np.random.default_rng(88).standard_normal((6, batch.param_count))
+        off = np.array([est.heff_offdiag_matvec(batch, cache, v) for v in vs])
+        full = np.array([est.heff_matvec(batch, energy, v) + est.heff_offdiag_matvec(batch, cache, v) for v in vs])
+        pair = kry.irl_smallest(bordered_connected(batch, energy, grad, cache), batch.param_count + 1, m=m,
+                                tol=1e-12, max_restarts=3, seed=5)
+        d = {"o": np.array(batch.o_matrix), "e": np.array(batch.e_loc), "w": np.array(batch.weights),
+             "n_samples": batch.n_samples, "mean": energy.mean, "grad": grad, "vs": vs, "off": off, "full": full,
+             "lam": pair.value, "vec": pair.vector, "n_matvec": pair.n_matvec,
+             "direction": direction(pair.vector, grad), **_cache_arrays(cache)}
+        if tag == "exact":
+            hmat = build_dense_hamiltonian(integrals, sector)
+            amps = np.array([np.exp(ans.log_amplitude(params, x, sector).value) for x in enumerate_sector(sector)])
+            psi = amps / np.linalg.norm(amps)
+            o_bar = batch.weights @ batch.o_matrix
+            tangent = psi[:, None] * (batch.o_matrix - o_bar)
+            d["sandwich"] = (tangent.conj().T @ (hmat - energy.mean * np.eye(len(psi))) @ tangent).real
+        out.update({f"{tag}_{k}": v for k, v in d.items()})
+    out["m"] = m
+    out["seed"] = 5
+    return out
+
+
+def rbm_log_psi_np(theta, x, n, h):
+    xf = x.astype(float)
+    a, b, w = theta[:n], theta[n : n + h], theta[n + h :].reshape(h, n)
+    return xf @ a + np.sum(np.log(np.cosh(b + xf @ w.T)), axis=-1)
+
+
+def _rbm_partner_case(seed, n, h, N, per_row, complex_params):
+    rng = np.random.default_rng(seed)
+    x = np.zeros((N, n), dtype=np.uint8)
+    occ = np.argsort(rng.random((N, n)), axis=1)[:, : n // 2]
+    x[np.arange(N)[:, None], occ] = 1
+    x[N // 2 :] = x[: N - N // 2]  # duplicate configurations (stochastic batches repeat samples)
+    P = n + h + h * n
+    theta = rng.normal(0, 0.2, P)
+    if complex_params:
+        theta = theta + 1j * rng.normal(0, 0.2, P)
+    # distinct configurations, first-occurrence order (est:228-233)
+    keys = [bytes(r) for r in x]
+    first = {}
+    for i, k in enumerate(keys):
+        first.setdefault(k, len(first))
+    dist_index = np.array([first[k] for k in keys])
+    reps = np.array([keys.index(k) for k in first])
+    # partners: random particle-conserving single excitations (the data shape of ham:260-264)
+    partners, elements, indptr = [], [], [0]
+    for r in reps:
+        cnt = int(rng.integers(0, per_row + 1))
+        for _ in range(cnt):
+            y = x[r].copy()
+            y[rng.choice(np.flatnonzero(y == 1))] = 0
+            y[rng.choice(np.flatnonzero(x[r] == 0))] = 1
+            partners.append(y)
+            elements.append(rng.normal(0.0, 0.3))
+        indptr.append(len(partners))
+    partners = np.array(partners, dtype=np.uint8).reshape(-1, n)
+    elements = np.array(elements)
+    uniq, inv = np.unique(partners, axis=0, return_inverse=True)
+    inv = inv.reshape(-1)
+    seg = np.repeat(np.arange(len(reps)), np.diff(indptr))
+    coeff = elements * np.exp(rbm_log_psi_np(theta, partners, n, h) - rbm_log_psi_np(theta, x[reps], n, h)[seg])
+    o = rbm_rows_np(theta, x, n, h)
+    po = rbm_rows_np(theta, uniq, n, h)
+    w = rng.random(N) + 0.2
+    w = w / w.sum()
+    return dict(x=x, theta=theta, n=n, h=h, w=w, o=o, partners=partners, elements=elements, indptr=np.array(indptr),
+                dist_index=dist_index, partner_row=inv, partner_o=po, uniq=uniq, coeff=coeff.astype(complex),
+                logpsi_x=rbm_log_psi_np(theta, x, n, h), logpsi_p=rbm_log_psi_np(theta, partners, n, h))
+
+
+def case_rbm_connected(seed=21, n=6, h=4, N=40, per_row=5):
+    """Real RBM batch with a partner cache through the reference heff_offdiag_matvec (est:254-294)."""
+    d = _rbm_partner_case(seed, n, h, N, per_row, False)
+    batch = placeholder_batch(d["w"], np.zeros(N), d["o"].astype(complex), N)
+    cache = est.ConnectedCache(d["dist_index"], d["indptr"], d["partner_row"], d["coeff"],
+                               d["partner_o"].astype(complex))
+    vs = np.random.default_rng(seed + 1).standard_normal((4, d["o"].shape[1]))
+    d["vs"] = vs
+    d["off"] = np.array([est.heff_offdiag_matvec(batch, cache, v) for v in vs])
+    return d
+
+
+def case_hermitian_connected(seed=23, n=6, h=4, N=40, per_row=5):
+    """Complex-theta RBM completion through the real embedding [O, iO]."""
+    d = _rbm_partner_case(seed, n, h, N, per_row, True)
+    o, po = d["o"], d["partner_o"]
+    batch = placeholder_batch(d["w"], np.zeros(N), np.concatenate([o, 1j * o], axis=1), N)
+    cache = est.ConnectedCache(d["dist_index"], d["indptr"], d["partner_row"], d["coeff"],
+                               np.concatenate([po, 1j * po], axis=1))
+    vs = np.random.default_rng(seed + 1).standard_normal((4, 2 * o.shape[1]))
+    d["vs"] = vs
+    d["off"] = np.array([est.heff_offdiag_matvec(batch, cache, v) for v in vs])
+    return d
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
+    only = set(sys.argv[1:])
     cases = {
-        "real_rbm": case_real(),
-        "complex_raw": case_complex_raw(),
-        "hermitian_rbm": case_hermitian(),
-        "h2_exact": case_h2(),
-        "mlp_phase_head": case_mlp_phase_head(),
-        "krylov": case_krylov(),
+        "real_rbm": case_real,
+        "complex_raw": case_complex_raw,
+        "hermitian_rbm": case_hermitian,
+        "h2_exact": case_h2,
+        "mlp_phase_head": case_mlp_phase_head,
+        "krylov": case_krylov,
+        "h2_connected": case_h2_connected,
+        "rbm_connected": case_rbm_connected,
+        "hermitian_connected": case_hermitian_connected,
     }
     for name, data in cases.items():
+        if only and name not in only:
+            continue
+        data = data()
         path = os.path.join(OUT, f"{name}.npz")
         np.savez_compressed(path, **data)
         print(f"wrote {path} ({os.path.getsize(path)} bytes)")

@@ -71,6 +71,15 @@ SIGNATURES = {
     "irl_otf_prepare_rbm_c128": (_I, [_P, _I64, _I, _I, _P, _P, _P, _P]),
     "irl_otf_colstats_rbm_c128": (_I, [_P, _P, _I64, _I, _I, _I64, _P, _P, _P, _P, _P, _SZ, _P]),
     "irl_otf_mvp_rbm_c128": (_I, [_P, _P, _I64, _I, _I, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "irl_connected_workspace_bytes": (_SZ, [_I64, _I64, _I64, _I]),
+    "irl_connected_mvp_f64": (_I, [_P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _P, _P, _P,
+                                   _I, _P, _SZ, _P]),
+    "irl_connected_mvp_c128": (_I, [_P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _P, _P, _P,
+                                    _P, _P, _P, _I, _P, _SZ, _P]),
+    "irl_logamp_workspace_bytes": (_SZ, [_I64, _I, _I]),
+    "irl_logamp_rbm_f64": (_I, [_P, _I64, _I, _I, _P, _P, _P, _SZ, _P]),
+    "irl_logamp_rbm_c128": (_I, [_P, _I64, _I, _I, _P, _P, _P, _SZ, _P]),
+    "irl_logamp_mlp_f64": (_I, [_P, _I64, _I, _I, _P, _P, _P, _SZ, _P]),
 }
 
 

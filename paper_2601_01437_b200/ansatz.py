@@ -6,7 +6,8 @@ seam* — ``Architecture.param_count`` (``ans:26-38``), ``AnsatzParameters``
 (``ans:41-53``), ``log_derivative(params, x, sector)`` (``ans:249-290``) — and
 adds the batched form the hot path needs, ``log_derivative_batch`` and
 ``build_batch`` (the role of ``estimators.build_batch``, ``est:79-133``, with
-synthetic E_loc instead of a Hamiltonian).
+synthetic E_loc instead of a Hamiltonian), ``log_amplitude_batch`` (``ans:200``)
+and ``build_connected_cache`` (``est:221-251``, partners given as input).
 
 Encodings: inputs are 0/1 occupations (``sigma_i = x_i``), not
 the reference's +-1 encodings (``ans:156-162``, ``ans:243-246``).
@@ -29,7 +30,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .estimators import KIND_HERMITIAN, KIND_REAL, SampleBatch, _as_tensor, _device
+from .estimators import KIND_HERMITIAN, KIND_REAL, ConnectedCache, SampleBatch, _as_tensor, _device
 
 
 @dataclass(frozen=True)
@@ -291,3 +292,94 @@ def build_batch_otf(params: AnsatzParameters, x, e_loc, weights=None, n_samples:
                   _lib.ptr(xbits), _lib.ptr(t), _lib.ptr(g), _lib.stream_handle(dev))
     batch.otf = {"xbits": xbits, "t": t, "g": g, "n_in": arch.n_inputs, "hidden": arch.hidden, "model": arch.model}
     return batch
+
+
+def log_amplitude_batch(params: AnsatzParameters, x, device=None) -> torch.Tensor:
+    """log psi for every row of x (role of ``ans.log_amplitude``, ans:200-247):
+    RBM ``a.x + sum_j log cosh(b_j + W_j.x)`` (complex for complex theta), MLP
+    ``u.tanh(W x + b) + c``.  Device tensor (N,), float64 or complex128."""
+    dev = _device(device)
+    arch = params.architecture
+    xt = _x_device(x, arch.n_inputs, dev)
+    n = int(xt.shape[0])
+    cplx = bool(arch.complex_params)
+    out = torch.empty(n, dtype=torch.complex128 if cplx else torch.float64, device=dev)
+    if n == 0:
+        return out
+    theta = _theta_device(params, dev)
+    nbytes = int(_lib.lib().irl_logamp_workspace_bytes(n, arch.hidden, int(cplx)))
+    ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=dev)
+    if arch.model == _lib.MODEL_RBM:
+        fn = "irl_logamp_rbm_c128" if cplx else "irl_logamp_rbm_f64"
+    else:
+        fn = "irl_logamp_mlp_f64"
+    _lib.call(fn, _lib.ptr(xt), n, arch.n_inputs, arch.hidden, _lib.ptr(theta), _lib.ptr(out), _lib.ptr(ws),
+              ws.numel(), _lib.stream_handle(dev))
+    return out
+
+
+def log_amplitude(params: AnsatzParameters, x, sector=None):
+    """Single-sample log psi (ans:200 signature; ``sector`` unused)."""
+    xa = np.asarray(x, dtype=np.uint8).reshape(1, -1)
+    v = log_amplitude_batch(params, xa)[0].item()
+    return complex(v)
+
+
+def build_connected_cache(params: AnsatzParameters, batch: SampleBatch, x, partners, elements, indptr,
+                          dist_index=None, device=None) -> ConnectedCache:
+    """``est.build_connected_cache`` (est:221-251) for the shallow NQS.
+
+    The Hamiltonian side (which partners, and their <x|H|y>) is an input here:
+    ``partners`` (nnz, n) holds the connected configurations of distinct
+    configuration k in the CSR slice ``indptr[k]:indptr[k+1]``, with
+    ``elements`` their matrix elements; ``dist_index`` maps batch rows to
+    distinct configurations (default: every row distinct).  On device: log psi
+    of the representatives and of the distinct partners (``k_logamp``),
+    coefficients ``element * exp(log psi(y) - log psi(x))`` (est:246-248) and
+    the partner O rows (the K1/K2 row kernel), deduplicated as the reference's
+    ``o_row`` table is (est:236-242).
+    """
+    dev = _device(device) if device is not None else batch.device
+    arch = params.architecture
+    xa = np.asarray(x.cpu() if isinstance(x, torch.Tensor) else x, dtype=np.uint8)
+    pa = np.asarray(partners.cpu() if isinstance(partners, torch.Tensor) else partners, dtype=np.uint8)
+    ip = np.asarray(indptr, dtype=np.int64)
+    n = xa.shape[0]
+    if n != batch.n_rows:
+        raise ValueError("x rows do not match the batch")
+    di = np.arange(n, dtype=np.int64) if dist_index is None else np.asarray(dist_index, dtype=np.int64)
+    n_dist = len(ip) - 1
+    if di.shape != (n,) or (n and (di.min() < 0 or di.max() >= n_dist)):
+        raise ValueError("dist_index does not match indptr")
+    nnz = int(ip[-1])
+    if pa.shape[0] != nnz or np.shape(elements) != (nnz,):
+        raise ValueError("partners / elements must have indptr[-1] rows")
+    # representative batch row of each distinct configuration (first occurrence, est:228-233)
+    reps = np.full(n_dist, -1, dtype=np.int64)
+    order = np.arange(n)[::-1]
+    reps[di[order]] = order
+    if np.any(reps < 0):
+        raise ValueError("a distinct configuration has no batch row")
+    if nnz:
+        uniq, inv = np.unique(pa, axis=0, return_inverse=True)
+        inv = inv.reshape(-1)
+    else:
+        uniq, inv = np.zeros((0, arch.n_inputs), dtype=np.uint8), np.zeros(0, dtype=np.int64)
+    m = uniq.shape[0]
+    cplx = bool(arch.complex_params)
+    odt = torch.complex128 if cplx else torch.float64
+    po = torch.zeros((m, batch.ld), dtype=odt, device=dev)
+    if m:
+        ut = _x_device(uniq, arch.n_inputs, dev)
+        w = torch.full((m,), 1.0 / m, dtype=torch.float64, device=dev)
+        scratch = [torch.empty(batch.ld, dtype=odt, device=dev) for _ in range(2)]
+        fill_o_rows(params, ut, po, w, torch.zeros(m, dtype=odt, device=dev), scratch[0], scratch[1])
+        lp = log_amplitude_batch(params, ut, device=dev)
+    lx = log_amplitude_batch(params, xa[reps], device=dev)
+    if nnz:
+        seg = torch.as_tensor(np.repeat(np.arange(n_dist), np.diff(ip)), device=dev)
+        ratio = torch.exp(lp[torch.as_tensor(inv, device=dev)].to(torch.complex128) - lx[seg].to(torch.complex128))
+        coeff = torch.as_tensor(np.asarray(elements), dtype=torch.complex128, device=dev) * ratio
+    else:
+        coeff = torch.zeros(0, dtype=torch.complex128, device=dev)
+    return ConnectedCache(di, ip, inv, coeff, po, batch=batch)

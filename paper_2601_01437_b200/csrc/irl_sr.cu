@@ -19,6 +19,7 @@
 #include "stream.cuh"
 #include "rows.cuh"
 #include "wide.cuh"
+#include "connected.cuh"
 
 using namespace irl;
 
@@ -509,7 +510,7 @@ int launch_wide(const WidePlan& p, bool cplx, WideArgs a, void* ws, cudaStream_t
 }
 
 int mvp_impl(bool cplx, const double* O, int64_t n, int64_t p, int64_t ld, const double* obar, const double* coeff,
-             const double* v_re, const double* v_im, double* out_re, double* out_im, const double* hf_re,
+             const void* yadd, const double* v_re, const double* v_im, double* out_re, double* out_im, const double* hf_re,
              const double* hf_im, const double* u0, double* out0, int mode, void* ws, size_t ws_bytes,
              cudaStream_t st) {
   if (!O || !coeff || !v_re || !out_re) return fail(IRL_ERR_ARG, "null required pointer");
@@ -540,6 +541,7 @@ int mvp_impl(bool cplx, const double* O, int64_t n, int64_t p, int64_t ld, const
     wa.hf_im = hf_im;
     wa.obar = reinterpret_cast<const double2*>(obar);
     wa.coeff = coeff;
+    wa.yadd = yadd;
     wa.u0 = u0;
     wa.out_re = out_re;
     wa.out_im = out_im;
@@ -569,6 +571,7 @@ int mvp_impl(bool cplx, const double* O, int64_t n, int64_t p, int64_t ld, const
   a.hf_im = hf_im;
   a.obar = reinterpret_cast<const double2*>(obar);
   a.coeff0 = coeff;
+  a.yadd = yadd;
   if (path == IRL_MVP_FUSED || path == IRL_MVP_ROWS) {
     MvpWs w = mvp_ws_layout(pl, n, ld_u, cplx, ws);
     if (ws_bytes < w.bytes) return fail(IRL_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, w.bytes);
@@ -1304,6 +1307,134 @@ int obuild_impl(bool cplx, int model, const uint8_t* x, int64_t n, int n_vis, in
   return cuda_check(cudaGetLastError(), "obuild finish launch");
 }
 
+// ------------------------------------------------------------ connected ---
+// Full connected product (est:171-186 + est:254-294, summed as opt:144-147):
+// partner DOT pass -> per-row (a_n, d_n) -> one ordinary product over the batch
+// O with coefficient a and additive row term d (connected.cuh).
+struct ConnWs {
+  size_t mvp, tpart, spart, gpart, a, d, bytes;
+};
+
+ConnWs conn_ws_layout(int64_t n, int64_t m, int64_t ld, bool cplx, const Plan* pp) {
+  const size_t sS = cplx ? 16 : 8;
+  ConnWs w{};
+  size_t off = 0;
+  auto carve = [&](size_t b) {
+    const size_t r = off;
+    off += align256(std::max<size_t>(b, 1));
+    return r;
+  };
+  w.mvp = carve(mvp_ws_bytes(n, ld, cplx));
+  const int C = pp ? std::max(pp->C, 1) : 1;
+  w.tpart = carve((size_t)C * std::max<int64_t>(m, 1) * sS);
+  w.spart = carve((size_t)C * sS);
+  w.gpart = carve((size_t)C * 8);
+  w.a = carve((size_t)n * sS);
+  w.d = carve((size_t)n * sS);
+  w.bytes = off;
+  return w;
+}
+
+size_t connected_ws_bytes(int64_t n, int64_t m, int64_t ld, bool cplx) {
+  const int64_t ld_u = cplx ? ld : ld / 2;
+  Plan pp;
+  const bool ok = m > 0 && make_plan(m, ld_u, cplx, MODE_DOT, pp) == IRL_OK;
+  g_err.clear();
+  return conn_ws_layout(n, m, ld, cplx, ok ? &pp : nullptr).bytes;
+}
+
+int connected_impl(bool cplx, const double* O, int64_t n, int64_t p, int64_t ld, const double* obar, const double* w,
+                   const double* coeff, const int64_t* dist_index, const int64_t* indptr, const int64_t* prow,
+                   const double* pcoeff, const double* Op, int64_t m, const double* v_re, const double* v_im,
+                   double* out_re, double* out_im, const double* hf_re, const double* hf_im, const double* u0,
+                   double* out0, int mode, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (!O || !w || !dist_index || !indptr || !v_re || !out_re) return fail(IRL_ERR_ARG, "null required pointer");
+  if (m < 0 || (m > 0 && (!Op || !prow || !pcoeff))) return fail(IRL_ERR_ARG, "bad partner arguments");
+  if (n < 1 || p < 1 || ld < p) return fail(IRL_ERR_ARG, "bad shape n=%lld p=%lld ld=%lld", (long long)n,
+                                            (long long)p, (long long)ld);
+  if (ld != irl_padded_ld(p, cplx)) return fail(IRL_ERR_ALIGN, "ld must equal irl_padded_ld(p)");
+  if (!aligned16(O) || !aligned16(Op) || !aligned16(obar) || !aligned16(ws))
+    return fail(IRL_ERR_ALIGN, "pointers must be 16-byte aligned");
+  const int64_t ld_u = cplx ? ld : ld / 2;
+  Plan pp{};
+  if (m > 0) IRL_TRY(make_plan(m, ld_u, cplx, MODE_DOT, pp));
+  const ConnWs wl = conn_ws_layout(n, m, ld, cplx, m > 0 ? &pp : nullptr);
+  if (ws_bytes < wl.bytes) return fail(IRL_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, wl.bytes);
+  char* base = static_cast<char*>(ws);
+  if (m > 0) {
+    StreamArgs a{};
+    a.O = reinterpret_cast<const double2*>(Op);
+    a.n_rows = m;
+    a.ld_u = ld_u;
+    a.v_re = v_re;
+    a.v_im = v_im;
+    a.obar = reinterpret_cast<const double2*>(obar);
+    a.tpart = base + wl.tpart;
+    a.spart = base + wl.spart;
+    a.gpart = reinterpret_cast<double*>(base + wl.gpart);
+    IRL_TRY(launch_stream(pp, a, st));
+  }
+  DevInfo d;
+  IRL_TRY(dev_info(d));
+  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 8), (int64_t)d.sms * 8));
+  if (cplx) {
+    k_connected_rows<true><<<blocks, 256, 0, st>>>(
+        dist_index, indptr, prow, reinterpret_cast<const double2*>(pcoeff),
+        reinterpret_cast<const double2*>(base + wl.tpart), std::max(pp.C, 1), m,
+        reinterpret_cast<const double2*>(base + wl.spart), w, reinterpret_cast<const double2*>(coeff), n,
+        reinterpret_cast<double2*>(base + wl.a), reinterpret_cast<double2*>(base + wl.d));
+  } else {
+    k_connected_rows<false><<<blocks, 256, 0, st>>>(
+        dist_index, indptr, prow, pcoeff, reinterpret_cast<const double*>(base + wl.tpart), std::max(pp.C, 1), m,
+        reinterpret_cast<const double*>(base + wl.spart), w, coeff, n, reinterpret_cast<double*>(base + wl.a),
+        reinterpret_cast<double*>(base + wl.d));
+  }
+  IRL_TRY(cuda_check(cudaGetLastError(), "connected rows launch"));
+  return mvp_impl(cplx, O, n, p, ld, obar, reinterpret_cast<const double*>(base + wl.a), base + wl.d, v_re, v_im,
+                  out_re, out_im, hf_re, hf_im, u0, out0, mode, base + wl.mvp, wl.a - wl.mvp, st);
+}
+
+// ------------------------------------------------------------- log psi ---
+size_t logamp_ws_bytes(int64_t n, int hidden, bool cplx) {
+  return align256((size_t)cdiv(hidden, 32) * std::max<int64_t>(n, 1) * (cplx ? 16 : 8));
+}
+
+template <bool CPLX, int MODEL>
+int logamp_impl(const uint8_t* x, int64_t n, int n_vis, int hidden, const double* theta, double* out, void* ws,
+                size_t ws_bytes, cudaStream_t st) {
+  using S = typename Traits<CPLX>::S;
+  if (!x || !theta || !out || n < 1 || n_vis < 1 || hidden < 1) return fail(IRL_ERR_ARG, "bad log-amplitude arguments");
+  if (ws_bytes < logamp_ws_bytes(n, hidden, CPLX)) return fail(IRL_ERR_WORKSPACE, "workspace too small");
+  const size_t smem = (size_t)n_vis * 32 * sizeof(S);
+  DevInfo d;
+  IRL_TRY(dev_info(d));
+  if (smem > (size_t)d.smem_optin) return fail(IRL_ERR_ARG, "n_vis too large");
+  const S* th = reinterpret_cast<const S*>(theta);
+  const S *avec, *bvec, *Wm;
+  const double *uvec = nullptr, *cval = nullptr;
+  if (MODEL == MODEL_RBM) {
+    avec = th;
+    bvec = th + n_vis;
+    Wm = th + n_vis + hidden;
+  } else {
+    Wm = th;
+    bvec = th + (size_t)hidden * n_vis;
+    uvec = theta + (size_t)hidden * n_vis + hidden;
+    cval = uvec + hidden;
+    avec = nullptr;
+  }
+  auto fn = k_logamp_part<CPLX, MODEL>;
+  IRL_TRY(ensure_fn_attrs((const void*)fn, d.smem_optin));
+  const int jt = (int)cdiv(hidden, 32);
+  const int64_t rb = std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 8), cdiv((int64_t)d.sms * 8, jt)));
+  S* part = static_cast<S*>(ws);
+  fn<<<dim3((unsigned)rb, (unsigned)jt), 256, smem, st>>>(x, n, n_vis, hidden, Wm, bvec, uvec, part);
+  IRL_TRY(cuda_check(cudaGetLastError(), "log-amplitude kernel launch"));
+  k_logamp_finish<CPLX, MODEL><<<(unsigned)cdiv(n, 256), 256, 0, st>>>(x, n, n_vis, jt, avec, cval, part,
+                                                                       reinterpret_cast<S*>(out));
+  return cuda_check(cudaGetLastError(), "log-amplitude finish launch");
+}
+
 }  // namespace
 
 // =================================================================== ABI ==
@@ -1410,7 +1541,7 @@ size_t irl_mvp_workspace_bytes(int64_t n, int64_t ld, int is_complex) { return m
 int irl_mvp_f64(const double* O, int64_t n, int64_t p, int64_t ld, const double* obar, const double* coeff,
                 const double* v, double* out, const double* half_f, const double* u0, double* out0, int mode,
                 void* ws, size_t ws_bytes, void* stream) {
-  return mvp_impl(false, O, n, p, ld, obar, coeff, v, nullptr, out, nullptr, half_f, nullptr, u0, out0, mode, ws,
+  return mvp_impl(false, O, n, p, ld, obar, coeff, nullptr, v, nullptr, out, nullptr, half_f, nullptr, u0, out0, mode, ws,
                   ws_bytes, (cudaStream_t)stream);
 }
 
@@ -1418,7 +1549,7 @@ int irl_mvp_c128(const double* O, int64_t n, int64_t p, int64_t ld, const double
                  const double* v_re, const double* v_im, double* out_re, double* out_im, const double* hf_re,
                  const double* hf_im, const double* u0, double* out0, int mode, void* ws, size_t ws_bytes,
                  void* stream) {
-  return mvp_impl(true, O, n, p, ld, obar, coeff, v_re, v_im, out_re, out_im, hf_re, hf_im, u0, out0, mode, ws,
+  return mvp_impl(true, O, n, p, ld, obar, coeff, nullptr, v_re, v_im, out_re, out_im, hf_re, hf_im, u0, out0, mode, ws,
                   ws_bytes, (cudaStream_t)stream);
 }
 
@@ -1778,6 +1909,50 @@ int irl_host_qr_sweeps(int m, double* T, double* Q, const double* shifts, int ns
     }
   }
   return IRL_OK;
+}
+
+size_t irl_connected_workspace_bytes(int64_t n, int64_t n_partner, int64_t ld, int is_complex) {
+  return connected_ws_bytes(n, n_partner, ld, is_complex != 0);
+}
+
+int irl_connected_mvp_f64(const double* O, int64_t n, int64_t p, int64_t ld, const double* obar, const double* w,
+                          const double* coeff, const int64_t* dist_index, const int64_t* indptr,
+                          const int64_t* partner_row, const double* pcoeff, const double* partner_O,
+                          int64_t n_partner, const double* v, double* out, const double* half_f, const double* u0,
+                          double* out0, int mode, void* ws, size_t ws_bytes, void* stream) {
+  return connected_impl(false, O, n, p, ld, obar, w, coeff, dist_index, indptr, partner_row, pcoeff, partner_O,
+                        n_partner, v, nullptr, out, nullptr, half_f, nullptr, u0, out0, mode, ws, ws_bytes,
+                        (cudaStream_t)stream);
+}
+
+int irl_connected_mvp_c128(const double* O, int64_t n, int64_t p, int64_t ld, const double* obar, const double* w,
+                           const double* coeff, const int64_t* dist_index, const int64_t* indptr,
+                           const int64_t* partner_row, const double* pcoeff, const double* partner_O,
+                           int64_t n_partner, const double* v_re, const double* v_im, double* out_re,
+                           double* out_im, const double* hf_re, const double* hf_im, const double* u0, double* out0,
+                           int mode, void* ws, size_t ws_bytes, void* stream) {
+  return connected_impl(true, O, n, p, ld, obar, w, coeff, dist_index, indptr, partner_row, pcoeff, partner_O,
+                        n_partner, v_re, v_im, out_re, out_im, hf_re, hf_im, u0, out0, mode, ws, ws_bytes,
+                        (cudaStream_t)stream);
+}
+
+size_t irl_logamp_workspace_bytes(int64_t n, int hidden, int is_complex) {
+  return logamp_ws_bytes(n, hidden, is_complex != 0);
+}
+
+int irl_logamp_rbm_f64(const uint8_t* x, int64_t n, int n_vis, int hidden, const double* theta, double* logpsi,
+                       void* ws, size_t ws_bytes, void* stream) {
+  return logamp_impl<false, MODEL_RBM>(x, n, n_vis, hidden, theta, logpsi, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int irl_logamp_rbm_c128(const uint8_t* x, int64_t n, int n_vis, int hidden, const double* theta, double* logpsi,
+                        void* ws, size_t ws_bytes, void* stream) {
+  return logamp_impl<true, MODEL_RBM>(x, n, n_vis, hidden, theta, logpsi, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int irl_logamp_mlp_f64(const uint8_t* x, int64_t n, int n_in, int hidden, const double* theta, double* logpsi,
+                       void* ws, size_t ws_bytes, void* stream) {
+  return logamp_impl<false, MODEL_MLP>(x, n, n_in, hidden, theta, logpsi, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 }  // extern "C"

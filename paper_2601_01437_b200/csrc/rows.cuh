@@ -68,6 +68,7 @@ __global__ void __launch_bounds__(RowsGeom<UPL>::NW * 32, RowsGeom<UPL>::MINB) k
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   const S* coeff = reinterpret_cast<const S*>(a.coeff0);
+  const S* yadd = reinterpret_cast<const S*>(a.yadd);
   double2 acc[UPL];
 #pragma unroll
   for (int k = 0; k < UPL; ++k) acc[k] = make_double2(0.0, 0.0);
@@ -88,7 +89,8 @@ __global__ void __launch_bounds__(RowsGeom<UPL>::NW * 32, RowsGeom<UPL>::MINB) k
       if (u < ld_u) T::dot_acc(t, o[k], vs[u]);
     }
     t = warp_sum<CPLX>(t);  // butterfly: every lane holds t_n
-    const S y = T::mul(coeff[r], T::sub(t, s_val));
+    S y = T::mul(coeff[r], T::sub(t, s_val));
+    if (yadd) y = T::add(y, yadd[r]);  // connected completion term
 #pragma unroll
     for (int k = 0; k < UPL; ++k) T::axpy(acc[k], o[k], y);
     ys = T::add(ys, y);

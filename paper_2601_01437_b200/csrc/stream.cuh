@@ -51,6 +51,7 @@ struct StreamArgs {
   const double2* obar;  // centring vector (units); null = uncentred
   const void* coeff0;   // FUSED/ACC: S[N] ; STATS: double[N] (weights)
   const void* coeff1;   // STATS: S[N]
+  const void* yadd;     // FUSED/ACC: S[N] additive row term, y_n += yadd_n (connected completion); null = none
   // outputs / workspace
   double2* part0;  // [nb][ld_u]
   double2* part1;  // [nb][ld_u]   (STATS)
@@ -313,7 +314,7 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
           t = (lane < rows) ? tslot[b * R + lane] : T::zero();
         }
       }
-      if (lane < rows) yv = T::mul(cf0, T::sub(t, s_val));
+      if (lane < rows) yv = T::add(T::mul(cf0, T::sub(t, s_val)), cf1);  // cf1 = yadd_n (0 without)
     } else {
       yv = cf0;
     }
@@ -353,6 +354,7 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
         cf1 = reinterpret_cast<const S*>(a.coeff1)[r0 + lane];
       } else if constexpr (MODE != MODE_DOT) {
         cf0 = reinterpret_cast<const S*>(a.coeff0)[r0 + lane];
+        if (a.yadd) cf1 = reinterpret_cast<const S*>(a.yadd)[r0 + lane];
       }
       if constexpr (MODE == MODE_ACC) {
         for (int c = 0; c < C; ++c)
@@ -387,6 +389,7 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
         acc_group(g, pa, T::zero(), cf0, cf1);
         advance(pa);
         cf0 = cn0;
+        cf1 = cn1;
       }
     }
   } else {

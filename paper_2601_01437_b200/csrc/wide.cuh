@@ -37,6 +37,7 @@ struct WideArgs {
   const double* hf_im;
   const double2* obar;
   const void* coeff;  // S[N]
+  const void* yadd;   // S[N] additive row term (connected completion); null = none
   const double* u0;
   double* out_re;
   double* out_im;
@@ -256,7 +257,8 @@ __global__ void __launch_bounds__(WIDE_NT + 32, 1) k_wide(const WideArgs a) {
       for (int i = 0; i < 4; ++i) {
         if (r + i >= rows) break;
         const S tt = warp_sum<CPLX>(t[i]);
-        const S y = T::mul(coeff[r0 + r + i], tt);
+        S y = T::mul(coeff[r0 + r + i], tt);
+        if (a.yadd) y = T::add(y, reinterpret_cast<const S*>(a.yadd)[r0 + r + i]);
         if (lane == 0) {
           ys[r + i] = y;
           ysum = T::add(ysum, y);

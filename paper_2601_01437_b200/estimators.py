@@ -10,6 +10,9 @@ Mirrors the reference entry points on the hot path:
 * :func:`energy_gradient`   — ``estimators.py:156-163``  (fused column stats)
 * :func:`heff_matvec`       — ``estimators.py:171-186``  (single-pass fused MVP)
 * :func:`qgt_matvec`        — matrix-free form of ``dense_qgt`` (``:335-344``)
+* :class:`ConnectedCache`, :func:`heff_offdiag_matvec` — ``estimators.py:189-294``
+  (two-configuration completion); :func:`connected_heff_matvec`
+  applies both terms of the optimizer's operator (``optimizer.py:144-147``)
 * :func:`dense_heff`, :func:`dense_qgt`, :class:`DensePCapError` — ``:319-344``
 
 Three parameter/O conventions are supported:
@@ -313,17 +316,22 @@ def energy_gradient(batch: SampleBatch, energy: EnergyEstimate) -> torch.Tensor:
     return 2.0 * (g.real if batch.is_complex else g)
 
 
-def _apply(batch: SampleBatch, coeff: torch.Tensor, v: torch.Tensor, out: torch.Tensor, *,
-           mode: int = _lib.MVP_AUTO, half_f=None, u0=None, out0=None) -> None:
+def _apply(batch: SampleBatch, coeff: torch.Tensor | None, v: torch.Tensor, out: torch.Tensor, *,
+           mode: int = _lib.MVP_AUTO, half_f=None, u0=None, out0=None, cache: "ConnectedCache | None" = None) -> None:
     """Raw device product on padded vectors; no validation (driver fast path).
 
     real/complex_raw: v, out, half_f are real padded vectors (ld,) (views OK).
     hermitian: v, out, half_f are (re, im) tuples of real padded vectors.
+    With ``cache`` the two-configuration completion (est:254-294) is added in
+    the same launch sequence; ``coeff=None`` then gives the completion alone.
     """
     obar = batch.obar()
     stream = batch._stream()
-    ws = batch.mvp_workspace()
     n = batch.n_rows
+    if cache is not None:
+        _apply_connected(batch, cache, coeff, obar, v, out, mode, half_f, u0, out0, stream)
+        return
+    ws = batch.mvp_workspace()
     if batch.otf is not None:
         o = batch.otf
         if batch.kind == KIND_HERMITIAN:
@@ -360,7 +368,31 @@ def _apply(batch: SampleBatch, coeff: torch.Tensor, v: torch.Tensor, out: torch.
               _lib.ptr(h_im), _lib.ptr(u0), _lib.ptr(out0), int(mode), _lib.ptr(ws), ws.numel(), stream)
 
 
-def _product(batch: SampleBatch, coeff: torch.Tensor, v, mode: int):
+def _apply_connected(batch, cache, coeff, obar, v, out, mode, half_f, u0, out0, stream) -> None:
+    if batch.otf is not None:
+        raise ValueError("the connected completion needs a stored-O batch (build_batch(mode='stored'))")
+    cache._check_batch(batch)
+    ws = cache.workspace(batch)
+    n = batch.n_rows
+    common = (_lib.ptr(batch.o_matrix), n, batch.param_count, batch.ld, _lib.ptr(obar), _lib.ptr(batch.weights),
+              _lib.ptr(coeff), _lib.ptr(cache.dist_index), _lib.ptr(cache.indptr), _lib.ptr(cache.partner_row),
+              _lib.ptr(cache.coeff), _lib.ptr(cache.partner_o), cache.n_partner)
+    if not batch.is_complex:
+        _lib.call("irl_connected_mvp_f64", *common, _lib.ptr(v), _lib.ptr(out), _lib.ptr(half_f), _lib.ptr(u0),
+                  _lib.ptr(out0), int(mode), _lib.ptr(ws), ws.numel(), stream)
+        return
+    if batch.kind == KIND_HERMITIAN:
+        (v_re, v_im), (o_re, o_im) = v, out
+        h_re, h_im = half_f if half_f is not None else (None, None)
+    else:
+        v_re, v_im, o_re, o_im = v, None, out, None
+        h_re, h_im = half_f, None
+    _lib.call("irl_connected_mvp_c128", *common, _lib.ptr(v_re), _lib.ptr(v_im), _lib.ptr(o_re), _lib.ptr(o_im),
+              _lib.ptr(h_re), _lib.ptr(h_im), _lib.ptr(u0), _lib.ptr(out0), int(mode), _lib.ptr(ws), ws.numel(),
+              stream)
+
+
+def _product(batch: SampleBatch, coeff: torch.Tensor | None, v, mode: int, cache: "ConnectedCache | None" = None):
     p = batch.param_count
     as_numpy = not isinstance(v, torch.Tensor)
     if as_numpy:
@@ -384,7 +416,7 @@ def _product(batch: SampleBatch, coeff: torch.Tensor, v, mode: int):
         vin[0, :p] = vt.real
         vin[1, :p] = vt.imag
         vout = torch.empty((2, ld), dtype=torch.float64, device=dev)
-        _apply(batch, coeff, (vin[0], vin[1]), (vout[0], vout[1]), mode=mode)
+        _apply(batch, coeff, (vin[0], vin[1]), (vout[0], vout[1]), mode=mode, cache=cache)
         res = torch.complex(vout[0, :p], vout[1, :p])
     else:
         if (not as_numpy) and torch.is_complex(v):
@@ -395,7 +427,7 @@ def _product(batch: SampleBatch, coeff: torch.Tensor, v, mode: int):
         else:
             vin[:p] = _as_tensor(v, torch.float64, dev)
         vout = torch.empty(ld, dtype=torch.float64, device=dev)
-        _apply(batch, coeff, vin, vout, mode=mode)
+        _apply(batch, coeff, vin, vout, mode=mode, cache=cache)
         res = vout[:p]
     if on_host:
         dst = torch.empty(res.shape, dtype=res.dtype, pin_memory=v.is_pinned())
@@ -416,6 +448,111 @@ def heff_matvec(batch: SampleBatch, energy: EnergyEstimate, v, *, mode: int = _l
 def qgt_matvec(batch: SampleBatch, v, *, mode: int = _lib.MVP_AUTO):
     """S v = O_c^H (w (O_c v)) — matrix-free ``dense_qgt`` (est:335-344)."""
     return _product(batch, batch.weights if not batch.is_complex else batch.weights.to(torch.complex128), v, mode)
+
+
+class ConnectedCache:
+    """Device-resident off-diagonal couplings of a batch (est:189-218).
+
+    Same fields as the reference dataclass: batch row n maps to distinct
+    configuration ``dist_index[n]``; the partners of distinct configuration k
+    are the CSR slice ``indptr[k]:indptr[k+1]`` of ``partner_row`` / ``coeff``;
+    ``coeff`` holds <x|H|y> psi(y)/psi(x) and ``partner_row`` indexes rows of
+    ``partner_o``.  Arrays may be numpy (uploaded once) or device tensors;
+    ``partner_o`` may be host (M, P) or an already padded device tensor
+    (M, ld).  Real batches keep ``Re(coeff)``: with real O the reference's
+    ``Re((w corr) @ conj(O_c))`` only sees the real part.  Indices are checked
+    once here (the reference indexes without checks; an out-of-range index
+    would raise IndexError there).
+    """
+
+    def __init__(self, dist_index, indptr, partner_row, coeff, partner_o, *, batch: SampleBatch):
+        dev = batch.device
+        kind_c = batch.is_complex
+        cdt = torch.complex128 if kind_c else torch.float64
+        di = np.asarray(dist_index.cpu() if isinstance(dist_index, torch.Tensor) else dist_index, dtype=np.int64)
+        ip = np.asarray(indptr.cpu() if isinstance(indptr, torch.Tensor) else indptr, dtype=np.int64)
+        pr = np.asarray(partner_row.cpu() if isinstance(partner_row, torch.Tensor) else partner_row, dtype=np.int64)
+        n = batch.n_rows
+        if di.shape != (n,):
+            raise ValueError("dist_index must have one entry per batch row")
+        if ip.ndim != 1 or len(ip) < 1 or ip[0] != 0 or np.any(np.diff(ip) < 0):
+            raise ValueError("indptr must start at 0 and be non-decreasing")
+        n_dist = len(ip) - 1
+        if n and (di.min() < 0 or di.max() >= n_dist):
+            raise IndexError("dist_index out of range")
+        nnz = int(ip[-1])
+        if pr.shape != (nnz,):
+            raise ValueError("partner_row length must equal indptr[-1]")
+        ld, p = batch.ld, batch.param_count
+        if isinstance(partner_o, torch.Tensor) and partner_o.is_cuda and partner_o.ndim == 2 \
+                and partner_o.shape[1] == ld and partner_o.dtype == cdt:
+            po = partner_o.contiguous()
+        else:
+            src = partner_o
+            if not isinstance(src, torch.Tensor):
+                src = np.asarray(src)
+                if not kind_c and np.iscomplexobj(src):
+                    imax = float(np.max(np.abs(src.imag))) if src.size else 0.0
+                    if imax > 0.0:
+                        raise ValueError("complex partner_o needs a complex batch kind")
+                    src = src.real
+            m = int(src.shape[0]) if src.ndim == 2 else 0
+            if m and src.shape[1] != p:
+                raise ValueError("partner_o width does not match param_count")
+            po = torch.zeros((max(m, 0), ld), dtype=cdt, device=dev)
+            if m:
+                po[:, :p] = _as_tensor(src, cdt, dev)
+        m = int(po.shape[0])
+        if nnz and (pr.min() < 0 or pr.max() >= m):
+            raise IndexError("partner_row out of range")
+        c = coeff.detach().cpu().numpy() if isinstance(coeff, torch.Tensor) else np.asarray(coeff)
+        if c.shape != (nnz,):
+            raise ValueError("coeff length must equal indptr[-1]")
+        if not kind_c:
+            c = np.real(c)
+        self.dist_index = torch.as_tensor(di, device=dev)
+        self.indptr = torch.as_tensor(ip, device=dev)
+        self.partner_row = torch.as_tensor(pr, device=dev)
+        self.coeff = torch.as_tensor(np.ascontiguousarray(c), dtype=cdt, device=dev)
+        self.partner_o = po
+        self.n_partner = m
+        self.n_dist = n_dist
+        self._batch_id = id(batch)
+        self._ws: torch.Tensor | None = None
+
+    @classmethod
+    def from_reference(cls, cache, batch: SampleBatch) -> "ConnectedCache":
+        """Upload a reference ``irlnqs.estimators.ConnectedCache`` (or any object with its fields)."""
+        return cls(cache.dist_index, cache.indptr, cache.partner_row, cache.coeff, cache.partner_o, batch=batch)
+
+    def _check_batch(self, batch: SampleBatch) -> None:
+        if self._batch_id != id(batch):
+            raise ValueError("connected cache was built for another batch")
+
+    def workspace(self, batch: SampleBatch) -> torch.Tensor:
+        if self._ws is None:
+            nbytes = int(_lib.lib().irl_connected_workspace_bytes(batch.n_rows, self.n_partner, batch.ld,
+                                                                   int(batch.is_complex)))
+            self._ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=batch.device)
+        return self._ws
+
+
+def heff_offdiag_matvec(batch: SampleBatch, cache: ConnectedCache, v, *, mode: int = _lib.MVP_AUTO):
+    """est:254-294: two-configuration completion of the H_eff product.
+
+    ``Re(((w corr) @ conj(O_c)))`` with ``corr_n = sum_y coeff (q(y) - q(x_n))``,
+    ``q = (O - Obar) v``; one partner dot pass, a per-row CSR kernel and one
+    streaming pass over the batch O (``irl_connected_mvp_*`` with no diagonal
+    coefficient).  Hermitian batches return the complex product of the
+    reference's real embedding.
+    """
+    return _product(batch, None, v, mode, cache=cache)
+
+
+def connected_heff_matvec(batch: SampleBatch, energy: EnergyEstimate, cache: ConnectedCache, v, *,
+                          mode: int = _lib.MVP_AUTO):
+    """``heff_matvec + heff_offdiag_matvec`` (the optimizer's operator, opt:144-147) in one product."""
+    return _product(batch, batch.coefficients(energy.mean), v, mode, cache=cache)
 
 
 def _dense_from_products(batch: SampleBatch, coeff: torch.Tensor, cap: int) -> np.ndarray:

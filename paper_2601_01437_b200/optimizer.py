@@ -6,7 +6,10 @@ The data-parallel part of ``irlnqs.optimizer.outer_step`` (``opt:130-165``):
       A([u0; u]) = [ (F/2).u ; u0 F/2 + H_eff u ]
   — here ONE fused device launch (+ finisher) per product: the F/2 row and
   column are folded into the streaming kernel's prologue and epilogue;
-  ``heff_offdiag_matvec`` is absent for synthetic E_loc (SURVEY §8(f) row 1);
+  ``heff_offdiag_matvec`` (``opt:146``) is added when a
+  :class:`~.estimators.ConnectedCache` is given (``connected=``): one partner
+  dot pass and a per-row CSR kernel before the same streaming product; it is
+  absent for synthetic E_loc (SURVEY §8(a) A10);
 * ``krylov.irl_smallest`` on it with the reference's seed rule
   ``_batch_seed`` (``opt:100-101``);
 * the direction ``d = c[1:]/c0`` (``opt:160-165``).
@@ -30,6 +33,7 @@ import torch
 from . import _lib, krylov
 from .estimators import (
     KIND_HERMITIAN,
+    ConnectedCache,
     EnergyEstimate,
     SampleBatch,
     _apply,
@@ -99,8 +103,9 @@ class BorderedOperator:
     """opt:140-148 on the device: one fused streaming launch per product."""
 
     def __init__(self, batch: SampleBatch, energy: EnergyEstimate, gradient: torch.Tensor | None = None,
-                 mode: int = _lib.MVP_AUTO, use_graph: bool = True):
+                 mode: int = _lib.MVP_AUTO, use_graph: bool = True, connected: ConnectedCache | None = None):
         self.batch = batch
+        self.connected = connected
         self.energy = energy
         self.layout = BorderedLayout(batch)
         self.mode = mode
@@ -140,7 +145,8 @@ class BorderedOperator:
             out = torch.zeros(self.layout.length, dtype=torch.float64, device=u.device)
         u0, uin = self.layout.parts(u)
         out0, uout = self.layout.parts(out)
-        _apply(self.batch, self.coeff, uin, uout, mode=self.mode, half_f=self.half_f, u0=u0, out0=out0)
+        _apply(self.batch, self.coeff, uin, uout, mode=self.mode, half_f=self.half_f, u0=u0, out0=out0,
+               cache=self.connected)
         self.count += 1
         return out
 
@@ -173,17 +179,21 @@ def direction_from_vector(vec: torch.Tensor, gradient: torch.Tensor, p: int, her
 
 def solve_step(batch: SampleBatch, config: OptimizerConfig = OptimizerConfig(), step: int = 0, *,
                energy: EnergyEstimate | None = None, mode: int = _lib.MVP_AUTO, seed: int | None = None,
-               use_graph: bool = True) -> StepResult:
-    """The IRL-SR hot path of one outer step (opt:134-165) on a device batch."""
+               use_graph: bool = True, connected: ConnectedCache | None = None) -> StepResult:
+    """The IRL-SR hot path of one outer step (opt:134-165) on a device batch.
+
+    ``connected`` adds ``heff_offdiag_matvec`` to the operator as ``opt:146`` does.
+    """
     if energy is None:
         energy = estimate_energy(batch)
     # the operator (and its captured Lanczos graphs) is cached on the batch
-    cache = batch.__dict__.setdefault("_bordered_ops", {})
-    key = (float(energy.mean), int(mode), use_graph)
-    op = cache.get(key)
+    ops = batch.__dict__.setdefault("_bordered_ops", {})
+    key = (float(energy.mean), int(mode), use_graph, id(connected) if connected is not None else None)
+    op = ops.get(key)
     if op is None:
-        op = BorderedOperator(batch, energy, energy_gradient(batch, energy), mode=mode, use_graph=use_graph)
-        cache[key] = op
+        op = BorderedOperator(batch, energy, energy_gradient(batch, energy), mode=mode, use_graph=use_graph,
+                              connected=connected)
+        ops[key] = op
     gradient = op.gradient
     s = _batch_seed(config, step) if seed is None else seed
     lay = op.layout

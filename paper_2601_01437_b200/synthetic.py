@@ -95,3 +95,30 @@ def make_inputs(cfg: SyntheticConfig) -> SyntheticInputs:
     if cfg.complex_params:
         e = e + 1j * rng_e.normal(0.0, cfg.e_imag_std, N)
     return SyntheticInputs(cfg, x, theta, e)
+
+
+def connected_partners(x: np.ndarray, per_row: int, seed: int, element_std: float = 0.05):
+    """Seeded synthetic stand-in for ``connected_configurations`` (ham:238-287).
+
+    For every row of ``x`` (treated as distinct: dist_index = arange(N)), draw
+    ``per_row`` spin-conserving-free single excitations (one occupied orbital
+    emptied, one empty orbital filled: the partner keeps the particle number,
+    like the reference's singles) with off-diagonal elements N(0, element_std^2).
+    No Hamiltonian stands behind them; they exercise the completion's data path
+    at BASELINE shapes.  Returns (partners (N*per_row, n) uint8, elements,
+    indptr (N+1,), dist_index (N,)).
+    """
+    rng = np.random.default_rng(seed)
+    N, n = x.shape
+    occ = np.argsort(-x.astype(np.int8) + rng.random((N, n)) * 0.5, axis=1)  # occupied first, shuffled
+    k = int(x[0].sum())
+    holes = occ[:, :k][np.arange(N)[:, None], rng.integers(0, k, (N, per_row))]
+    parts = occ[:, k:][np.arange(N)[:, None], rng.integers(0, n - k, (N, per_row))]
+    partners = np.repeat(x, per_row, axis=0).reshape(N, per_row, n).copy()
+    ri = np.arange(N)[:, None]
+    ci = np.arange(per_row)[None, :]
+    partners[ri, ci, holes] = 0
+    partners[ri, ci, parts] = 1
+    elements = rng.normal(0.0, element_std, N * per_row)
+    indptr = np.arange(0, N * per_row + 1, per_row, dtype=np.int64)
+    return partners.reshape(N * per_row, n), elements, indptr, np.arange(N, dtype=np.int64)
