@@ -397,6 +397,8 @@ RowsFn pick_rows(bool cplx, int64_t ld_u) {
   const int upl = (int)cdiv(ld_u, 32);
   if (upl <= 4) return cplx ? k_rows_mvp<true, 4> : k_rows_mvp<false, 4>;
   if (upl <= 8) return cplx ? k_rows_mvp<true, 8> : k_rows_mvp<false, 8>;
+  if (upl <= 12) return cplx ? k_rows_mvp<true, 12> : k_rows_mvp<false, 12>;
+  if (upl <= 14) return cplx ? k_rows_mvp<true, 14> : k_rows_mvp<false, 14>;
   if (upl <= 16) return cplx ? k_rows_mvp<true, 16> : k_rows_mvp<false, 16>;
   return nullptr;
 }
@@ -411,10 +413,11 @@ int make_rows_plan(int64_t n, int64_t ld_u, Plan& p) {
   p.mode = MODE_FUSED;  // no tpart in the workspace
   p.C = 1;
   const int upl = (int)cdiv(ld_u, 32);
-  const int nw = upl <= 8 ? 8 : 12, per_sm = upl <= 8 ? 2 : 1;
+  const int nw = 8, per_sm = upl <= 4 ? 2 : 1;  // RowsGeom<UPL>
   p.nb = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm * d.sms, cdiv(n, 2 * nw)));
   p.NT = nw * 32;
-  p.smem = (size_t)(nw + 1) * ld_u * 16;
+  const int upl_t = upl <= 4 ? 4 : upl <= 8 ? 8 : upl <= 12 ? 12 : upl <= 14 ? 14 : 16;  // pick_rows' instance
+  p.smem = ((size_t)nw * ld_u + 32 * upl_t) * 16;
   return IRL_OK;
 }
 

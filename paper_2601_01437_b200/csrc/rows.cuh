@@ -14,12 +14,16 @@
 
 namespace irl {
 
-// UPL <= 8: 8 warps per CTA, 2 CTAs per SM; UPL = 16 (up to 512 units, ~160
-// registers): 12 warps per CTA, one CTA per SM.
+// Every warp keeps two rows in flight: the loads of row r + stride are issued
+// before row r is reduced and accumulated, and the first row's loads are
+// issued before the prologue (v staging, Obar.v), so HBM latency overlaps the
+// butterflies instead of adding to them row after row.
+// UPL <= 4: 8 warps per CTA, 2 CTAs per SM; larger UPL (two row buffers +
+// accumulators, up to ~210 registers at UPL = 16): 8 warps, one CTA per SM.
 template <int UPL>
 struct RowsGeom {
-  static constexpr int NW = UPL <= 8 ? 8 : 12;
-  static constexpr int MINB = UPL <= 8 ? 2 : 1;
+  static constexpr int NW = 8;
+  static constexpr int MINB = UPL <= 4 ? 2 : 1;
 };
 
 template <bool CPLX, int UPL>
@@ -29,15 +33,41 @@ __global__ void __launch_bounds__(RowsGeom<UPL>::NW * 32, RowsGeom<UPL>::MINB) k
   using S = typename T::S;
   extern __shared__ __align__(16) unsigned char smem_rw[];
   const int64_t ld_u = a.ld_u;
-  double2* vs = reinterpret_cast<double2*>(smem_rw);  // [ld_u] v units
-  double2* red = vs + ld_u;                           // [NW][ld_u] warp partials
+  double2* vs = reinterpret_cast<double2*>(smem_rw);  // [32 UPL] v units, zero past ld_u
+  double2* red = vs + 32 * UPL;                       // [NW][ld_u] warp partials
   __shared__ S shs[NW], shy[NW];
   __shared__ double shg[NW];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t nw = (int64_t)gridDim.x * NW;
+
+  const S* coeff = reinterpret_cast<const S*>(a.coeff0);
+  const S* yadd = reinterpret_cast<const S*>(a.yadd);
+  // row r's O units and its coefficient / additive term, all issued at once
+  auto load_row = [&](int64_t r, double2 (&o)[UPL], S& c, S& d) {
+    c = T::zero();
+    d = T::zero();
+    if (r < a.n_rows) {
+      c = coeff[r];
+      if (yadd) d = yadd[r];
+    }
+    const double2* orow = a.O + r * ld_u + lane;
+    // units read per lane: all 32 UPL except on the last row (units past ld_u
+    // read into the next row -- finite O entries -- and meet v = 0 in the dot;
+    // their accumulators are never stored); none past the last row
+    const int lim = (r + 1 < a.n_rows) ? 32 * UPL : (r < a.n_rows ? (int)ld_u : 0);
+#pragma unroll
+    for (int k = 0; k < UPL; ++k) o[k] = (lane + 32 * k < lim) ? __ldg(orow + 32 * k) : make_double2(0.0, 0.0);
+  };
+  // first row in flight before the prologue
+  double2 o0[UPL], o1[UPL];
+  S c0, c1, d0, d1;
+  int64_t r = (int64_t)blockIdx.x * NW + warp;
+  load_row(r, o0, c0, d0);
 
   // prologue: v -> shared memory; s = Obar . v and g = (F/2) . v in a fixed order
   S sp = T::zero();
   double gp = 0.0;
+  for (int64_t u = ld_u + tid; u < 32 * UPL; u += blockDim.x) vs[u] = make_double2(0.0, 0.0);
   for (int64_t u = tid; u < ld_u; u += blockDim.x) {
     const double2 v = load_vec_unit<CPLX>(a.v_re, a.v_im, u);
     vs[u] = v;
@@ -67,33 +97,31 @@ __global__ void __launch_bounds__(RowsGeom<UPL>::NW * 32, RowsGeom<UPL>::MINB) k
   }
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
-  const S* coeff = reinterpret_cast<const S*>(a.coeff0);
-  const S* yadd = reinterpret_cast<const S*>(a.yadd);
   double2 acc[UPL];
 #pragma unroll
   for (int k = 0; k < UPL; ++k) acc[k] = make_double2(0.0, 0.0);
   S ys = T::zero();
-  const int64_t nw = (int64_t)gridDim.x * NW;
-  for (int64_t r = (int64_t)blockIdx.x * NW + warp; r < a.n_rows; r += nw) {
-    const double2* orow = a.O + r * ld_u;
-    double2 o[UPL];
-#pragma unroll
-    for (int k = 0; k < UPL; ++k) {
-      const int64_t u = lane + 32 * k;
-      o[k] = (u < ld_u) ? __ldg(orow + u) : make_double2(0.0, 0.0);
-    }
+  auto row_step = [&](const double2 (&o)[UPL], S c, S d) {
     S t = T::zero();
 #pragma unroll
-    for (int k = 0; k < UPL; ++k) {
-      const int64_t u = lane + 32 * k;
-      if (u < ld_u) T::dot_acc(t, o[k], vs[u]);
-    }
+    for (int k = 0; k < UPL; ++k)
+      if (lane + 32 * k < ld_u) T::dot_acc(t, o[k], vs[lane + 32 * k]);
     t = warp_sum<CPLX>(t);  // butterfly: every lane holds t_n
-    S y = T::mul(coeff[r], T::sub(t, s_val));
-    if (yadd) y = T::add(y, yadd[r]);  // connected completion term
+    const S y = T::add(T::mul(c, T::sub(t, s_val)), d);  // d: connected completion term (0 without)
 #pragma unroll
     for (int k = 0; k < UPL; ++k) T::axpy(acc[k], o[k], y);
     ys = T::add(ys, y);
+  };
+  // two row buffers, alternating: the next row's loads are in flight while
+  // the current row is reduced and accumulated
+  while (r < a.n_rows) {
+    load_row(r + nw, o1, c1, d1);
+    row_step(o0, c0, d0);
+    r += nw;
+    if (r >= a.n_rows) break;
+    load_row(r + nw, o0, c0, d0);
+    row_step(o1, c1, d1);
+    r += nw;
   }
   // epilogue: the warp partials, summed in warp order
 #pragma unroll

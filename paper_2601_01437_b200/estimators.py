@@ -392,13 +392,29 @@ def _apply_connected(batch, cache, coeff, obar, v, out, mode, half_f, u0, out0, 
               stream)
 
 
+def _staging(batch: SampleBatch, shape) -> torch.Tensor:
+    """Zero-padded device input buffer reused across calls on one stream.
+
+    Only the first P entries of a row are ever written, so the padding stays
+    zero; reuse is safe because every use is ordered on the same stream.
+    """
+    key = (_lib.stream_handle(batch.device), tuple(shape))
+    st = batch.__dict__.setdefault("_stage", {})
+    buf = st.get(key)
+    if buf is None:
+        buf = torch.zeros(shape, dtype=torch.float64, device=batch.device)
+        st[key] = buf
+    return buf
+
+
 def _product(batch: SampleBatch, coeff: torch.Tensor | None, v, mode: int, cache: "ConnectedCache | None" = None):
     p = batch.param_count
     as_numpy = not isinstance(v, torch.Tensor)
-    if as_numpy:
-        v_arr = np.asarray(v)
+    on_host = (not as_numpy) and not v.is_cuda
+    if as_numpy or on_host:
+        v_arr = np.asarray(v) if as_numpy else v.detach().numpy()
         shape = v_arr.shape
-        finite = bool(np.all(np.isfinite(v_arr))) if shape == (p,) else True
+        finite = bool(np.isfinite(v_arr).all()) if shape == (p,) else True
     else:
         shape = tuple(v.shape)
         finite = bool(torch.isfinite(v).all()) if shape == (p,) else True
@@ -409,24 +425,23 @@ def _product(batch: SampleBatch, coeff: torch.Tensor | None, v, mode: int, cache
     dev = batch.device
     ld = batch.ld
     # host tensors (pinned for async copies) in -> host tensor out: the e2e path
-    on_host = (not as_numpy) and not v.is_cuda
     if batch.kind == KIND_HERMITIAN:
         vt = _as_tensor(v, torch.complex128, dev) if not on_host else v.to(torch.complex128).to(dev, non_blocking=True)
-        vin = torch.zeros((2, ld), dtype=torch.float64, device=dev)
+        vin = _staging(batch, (2, ld))
         vin[0, :p] = vt.real
         vin[1, :p] = vt.imag
-        vout = torch.empty((2, ld), dtype=torch.float64, device=dev)
+        vout = _staging(batch, (3, ld))[1:] if on_host else torch.empty((2, ld), dtype=torch.float64, device=dev)
         _apply(batch, coeff, (vin[0], vin[1]), (vout[0], vout[1]), mode=mode, cache=cache)
         res = torch.complex(vout[0, :p], vout[1, :p])
     else:
         if (not as_numpy) and torch.is_complex(v):
             raise ValueError("complex vector needs a hermitian batch")
-        vin = torch.zeros(ld, dtype=torch.float64, device=dev)
+        vin = _staging(batch, (ld,))
         if on_host:
-            vin[:p].copy_(v, non_blocking=True)
+            vin[:p].copy_(v if v.dtype == torch.float64 else v.to(torch.float64), non_blocking=True)
         else:
             vin[:p] = _as_tensor(v, torch.float64, dev)
-        vout = torch.empty(ld, dtype=torch.float64, device=dev)
+        vout = _staging(batch, (1, ld))[0] if on_host else torch.empty(ld, dtype=torch.float64, device=dev)
         _apply(batch, coeff, vin, vout, mode=mode, cache=cache)
         res = vout[:p]
     if on_host:
