@@ -222,6 +222,32 @@ int irl_logamp_rbm_c128(const uint8_t* x, int64_t n, int n_vis, int hidden, cons
 int irl_logamp_mlp_f64(const uint8_t* x, int64_t n, int n_in, int hidden, const double* theta, double* logpsi,
                        void* ws, size_t ws_bytes, void* stream);
 
+/* ------------------------------------------- §8(f) 2: local energies ----
+ * Molecular Hamiltonian from FCIDUMP integrals (hamiltonian.py): samples are
+ * bitmasks over M = 2 n_spatial <= 64 spin-orbitals (blocked: spin up first,
+ * hilbert.py:1-5); h1 (n_spatial^2) and g2 (n_spatial^4, chemists' (ij|kl), 8-fold
+ * symmetry expanded) are device arrays; theta is the shallow-NQS parameter
+ * vector (model IRL_MODEL_RBM / IRL_MODEL_MLP, layouts as irl_obuild_*).
+ *   irl_ham_local_energy     E_loc(x) = sum_y <x|H|y> psi(y)/psi(x)       (ham:290-302)
+ *   irl_ham_connected_count  number of kept off-diagonal partners per sample
+ *   irl_ham_connected_fill   their bitmasks, elements <y|H|x> and coefficients
+ *                            element * psi(y)/psi(x) at offsets[n]        (ham:238-287, est:243-249)
+ * Spin-conserving singles and doubles with the Slater-Condon rules and the
+ * fermionic sign of classify_excitation (ham:180-235, hilbert.py:137-158);
+ * |element| <= drop is dropped (ham:282-285).  eloc / coeff: double (c128:
+ * interleaved complex).  Workspace: irl_ham_workspace_bytes. */
+size_t irl_ham_workspace_bytes(int n_spatial, int hidden, int is_complex);
+int irl_ham_local_energy(int model, int is_complex, const uint64_t* xbits, int64_t n, int n_spatial, double e_core,
+                         const double* h1, const double* g2, double drop, int hidden, const double* theta,
+                         double* eloc, void* ws, size_t ws_bytes, void* stream);
+int irl_ham_connected_count(int model, int is_complex, const uint64_t* xbits, int64_t n, int n_spatial, double e_core,
+                            const double* h1, const double* g2, double drop, int hidden, const double* theta,
+                            int64_t* counts, void* ws, size_t ws_bytes, void* stream);
+int irl_ham_connected_fill(int model, int is_complex, const uint64_t* xbits, int64_t n, int n_spatial, double e_core,
+                           const double* h1, const double* g2, double drop, int hidden, const double* theta,
+                           const int64_t* offsets, uint64_t* partner_bits, double* elements, double* coeff, void* ws,
+                           size_t ws_bytes, void* stream);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

@@ -343,6 +343,73 @@ def case_hermitian_connected(seed=23, n=6, h=4, N=40, per_row=5):
     return d
 
 
+def case_hamiltonian():
+    """Local energies and connected configurations of the reference Hamiltonian
+    path (ham:94-302) on a seeded synthetic FCIDUMP (5 spatial orbitals, 3 up +
+    2 down) for the RBM (real, complex) and MLP log psi, plus H2 (its real
+    FCIDUMP, T/data/h2_sto3g.fcidump)."""
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from irlnqs.hamiltonian import build_dense_hamiltonian, connected_configurations, local_energy
+    from irlnqs.hilbert import enumerate_sector
+    from oracle import hamiltonian as oham
+    from oracle import nqs
+
+    text = oham.random_fcidump(31, 5, 5, ms2=1)
+    ints = parse_fcidump(text)
+    sector = ints.sector()
+    configs = enumerate_sector(sector)
+    bits = np.array([c.bits for c in configs], dtype=np.uint64)
+    M = ints.n_spin_orbitals
+    xocc = ((bits[:, None] >> np.arange(M, dtype=np.uint64)[None, :]) & np.uint64(1)).astype(np.uint8)
+    rng = np.random.default_rng(32)
+    n, hr, hm = M, 6, 7
+    th_rbm = rng.normal(0, 0.3, n + hr + hr * n)
+    th_rbmc = rng.normal(0, 0.3, n + hr + hr * n) + 1j * rng.normal(0, 0.3, n + hr + hr * n)
+    th_mlp = np.concatenate([rng.normal(0, np.sqrt(1 / n), hm * n + hm), rng.normal(0, np.sqrt(1 / hm), hm + 1)])
+    occ_of = {int(b): xocc[k] for k, b in enumerate(bits)}
+
+    def occ(x):
+        b = x.bits
+        return ((b >> np.arange(M)) & 1).astype(np.uint8)[None, :]
+
+    lps = {
+        "rbm": lambda x: nqs.rbm_log_psi(th_rbm, occ(x), n, hr)[0],
+        "rbmc": lambda x: nqs.rbm_log_psi(th_rbmc, occ(x), n, hr)[0],
+        "mlp": lambda x: nqs.mlp_log_psi(th_mlp, occ(x), n, hm)[0],
+    }
+    out = dict(fcidump=np.array(text), e_core=ints.e_core, h=ints.h, g=ints.g, ns=ints.n_spatial,
+               n_up=sector.n_up, n_down=sector.n_down, bits=bits, theta_rbm=th_rbm, theta_rbmc=th_rbmc,
+               theta_mlp=th_mlp, hidden_rbm=hr, hidden_mlp=hm,
+               dense=build_dense_hamiltonian(ints, sector))
+    for name, lp in lps.items():
+        out[f"eloc_{name}"] = np.array([local_energy(lp, ints, x) for x in configs])
+    pb, pe, ip = [], [], [0]
+    for x in configs:
+        ent = connected_configurations(ints, x)
+        out.setdefault("diag", []).append(ent[0].element)
+        pb += [e.config.bits for e in ent[1:]]
+        pe += [e.element for e in ent[1:]]
+        ip.append(len(pb))
+    out["diag"] = np.array(out["diag"])
+    out["partner_bits"] = np.array(pb, dtype=np.uint64)
+    out["partner_elem"] = np.array(pe)
+    out["partner_indptr"] = np.array(ip)
+    # H2 from its own FCIDUMP
+    with open(os.path.join(REF, "tests", "data", "h2_sto3g.fcidump")) as fh:
+        h2 = parse_fcidump(fh.read())
+    h2s = h2.sector()
+    out["h2_e_core"] = h2.e_core
+    out["h2_h"] = h2.h
+    out["h2_g"] = h2.g
+    out["h2_ns"] = h2.n_spatial
+    out["h2_n_up"] = h2s.n_up
+    out["h2_n_down"] = h2s.n_down
+    out["h2_bits"] = np.array([c.bits for c in enumerate_sector(h2s)], dtype=np.uint64)
+    out["h2_dense"] = build_dense_hamiltonian(h2, h2s)
+    out["h2_fci"] = -1.1372930376796802  # T/test_optimizer.py:16
+    return out
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     only = set(sys.argv[1:])
@@ -356,6 +423,7 @@ def main():
         "h2_connected": case_h2_connected,
         "rbm_connected": case_rbm_connected,
         "hermitian_connected": case_hermitian_connected,
+        "hamiltonian": case_hamiltonian,
     }
     for name, data in cases.items():
         if only and name not in only:

@@ -35,6 +35,7 @@ _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
 _I = ctypes.c_int
 _SZ = ctypes.c_size_t
+_D = ctypes.c_double
 
 # name -> (restype, argtypes); every symbol declared in include/irl_sr.h
 SIGNATURES = {
@@ -80,6 +81,10 @@ SIGNATURES = {
     "irl_logamp_rbm_f64": (_I, [_P, _I64, _I, _I, _P, _P, _P, _SZ, _P]),
     "irl_logamp_rbm_c128": (_I, [_P, _I64, _I, _I, _P, _P, _P, _SZ, _P]),
     "irl_logamp_mlp_f64": (_I, [_P, _I64, _I, _I, _P, _P, _P, _SZ, _P]),
+    "irl_ham_workspace_bytes": (_SZ, [_I, _I, _I]),
+    "irl_ham_local_energy": (_I, [_I, _I, _P, _I64, _I, _D, _P, _P, _D, _I, _P, _P, _P, _SZ, _P]),
+    "irl_ham_connected_count": (_I, [_I, _I, _P, _I64, _I, _D, _P, _P, _D, _I, _P, _P, _P, _SZ, _P]),
+    "irl_ham_connected_fill": (_I, [_I, _I, _P, _I64, _I, _D, _P, _P, _D, _I, _P, _P, _P, _P, _P, _P, _SZ, _P]),
 }
 
 

@@ -20,6 +20,7 @@
 #include "rows.cuh"
 #include "wide.cuh"
 #include "connected.cuh"
+#include "hamiltonian.cuh"
 
 using namespace irl;
 
@@ -1438,6 +1439,87 @@ int logamp_impl(const uint8_t* x, int64_t n, int n_vis, int hidden, const double
   return cuda_check(cudaGetLastError(), "log-amplitude finish launch");
 }
 
+// ---------------------------------------------------------- hamiltonian ---
+size_t ham_ws_bytes(int n_vis, int hidden, bool cplx) {
+  return align256((size_t)n_vis * std::max(hidden, 1) * (cplx ? 16 : 8));
+}
+
+template <bool CPLX, int MODEL, int MODE>
+int ham_launch(const HamArgs& a, size_t smem, cudaStream_t st) {
+  auto fn = k_local_energy<CPLX, MODEL, MODE>;
+  DevInfo d;
+  IRL_TRY(dev_info(d));
+  if (smem > (size_t)d.smem_optin - 8192) return fail(IRL_ERR_ARG, "hidden width too large for the local-energy kernel");
+  IRL_TRY(ensure_fn_attrs((const void*)fn, d.smem_optin));
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(a.n, (int64_t)d.sms * 16));
+  fn<<<grid, HAM_NT, smem, st>>>(a);
+  return cuda_check(cudaGetLastError(), "local-energy kernel launch");
+}
+
+int ham_impl(int model, bool cplx, int mode, const uint64_t* xbits, int64_t n, int ns, double e_core, const double* h1,
+             const double* g2, double drop, int hidden, const double* theta, void* out, int64_t* counts,
+             const int64_t* offsets, uint64_t* pbits, double* pelem, double* pcoeff, void* ws, size_t ws_bytes,
+             cudaStream_t st) {
+  if (!xbits || !h1 || !g2 || !theta || n < 0 || ns < 1 || ns > 32 || hidden < 1)
+    return fail(IRL_ERR_ARG, "bad local-energy arguments");
+  if (model != MODEL_RBM && model != MODEL_MLP) return fail(IRL_ERR_ARG, "unknown model %d", model);
+  if (cplx && model != MODEL_RBM) return fail(IRL_ERR_ARG, "complex parameters are an RBM feature");
+  if (mode == HAM_ELOC && !out) return fail(IRL_ERR_ARG, "null output");
+  if (mode == HAM_COUNT && !counts) return fail(IRL_ERR_ARG, "null counts");
+  if (mode == HAM_FILL && (!offsets || !pbits || !pelem || !pcoeff)) return fail(IRL_ERR_ARG, "null fill outputs");
+  const int M = 2 * ns;
+  if (ws_bytes < ham_ws_bytes(M, hidden, cplx)) return fail(IRL_ERR_WORKSPACE, "workspace too small");
+  if (n == 0) return IRL_OK;
+  const size_t sS = cplx ? 16 : 8;
+  HamArgs a{};
+  a.xbits = xbits;
+  a.n = n;
+  a.ns = ns;
+  a.hidden = hidden;
+  a.e_core = e_core;
+  a.h1 = h1;
+  a.g2 = g2;
+  a.drop = drop;
+  const char* th = reinterpret_cast<const char*>(theta);
+  const char* Wm;
+  if (model == MODEL_RBM) {
+    a.avec = th;
+    a.bvec = th + (size_t)M * sS;
+    Wm = th + (size_t)(M + hidden) * sS;
+  } else {
+    Wm = th;
+    a.bvec = th + (size_t)hidden * M * sS;
+    a.uvec = theta + (size_t)hidden * M + hidden;
+  }
+  a.WT = ws;
+  a.out = out;
+  a.counts = counts;
+  a.offsets = offsets;
+  a.pbits = pbits;
+  a.pelem = pelem;
+  a.pcoeff = pcoeff;
+  const int64_t ne = (int64_t)hidden * M;
+  if (cplx)
+    k_transpose_w<true><<<(unsigned)cdiv(ne, 256), 256, 0, st>>>((const double2*)Wm, hidden, M, (double2*)ws);
+  else
+    k_transpose_w<false><<<(unsigned)cdiv(ne, 256), 256, 0, st>>>((const double*)Wm, hidden, M, (double*)ws);
+  IRL_TRY(cuda_check(cudaGetLastError(), "transpose launch"));
+  const size_t smem = (size_t)3 * hidden * sS;
+#define IRL_HAM(C, MD, MO) \
+  if (cplx == C && model == MD && mode == MO) return ham_launch<C, MD, MO>(a, smem, st);
+  IRL_HAM(false, MODEL_RBM, HAM_ELOC)
+  IRL_HAM(false, MODEL_RBM, HAM_COUNT)
+  IRL_HAM(false, MODEL_RBM, HAM_FILL)
+  IRL_HAM(true, MODEL_RBM, HAM_ELOC)
+  IRL_HAM(true, MODEL_RBM, HAM_COUNT)
+  IRL_HAM(true, MODEL_RBM, HAM_FILL)
+  IRL_HAM(false, MODEL_MLP, HAM_ELOC)
+  IRL_HAM(false, MODEL_MLP, HAM_COUNT)
+  IRL_HAM(false, MODEL_MLP, HAM_FILL)
+#undef IRL_HAM
+  return fail(IRL_ERR_ARG, "unsupported local-energy variant");
+}
+
 }  // namespace
 
 // =================================================================== ABI ==
@@ -1956,6 +2038,32 @@ int irl_logamp_rbm_c128(const uint8_t* x, int64_t n, int n_vis, int hidden, cons
 int irl_logamp_mlp_f64(const uint8_t* x, int64_t n, int n_in, int hidden, const double* theta, double* logpsi,
                        void* ws, size_t ws_bytes, void* stream) {
   return logamp_impl<false, MODEL_MLP>(x, n, n_in, hidden, theta, logpsi, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+size_t irl_ham_workspace_bytes(int n_spatial, int hidden, int is_complex) {
+  return ham_ws_bytes(2 * n_spatial, hidden, is_complex != 0);
+}
+
+int irl_ham_local_energy(int model, int is_complex, const uint64_t* xbits, int64_t n, int n_spatial, double e_core,
+                         const double* h1, const double* g2, double drop, int hidden, const double* theta,
+                         double* eloc, void* ws, size_t ws_bytes, void* stream) {
+  return ham_impl(model, is_complex != 0, HAM_ELOC, xbits, n, n_spatial, e_core, h1, g2, drop, hidden, theta, eloc,
+                  nullptr, nullptr, nullptr, nullptr, nullptr, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int irl_ham_connected_count(int model, int is_complex, const uint64_t* xbits, int64_t n, int n_spatial, double e_core,
+                            const double* h1, const double* g2, double drop, int hidden, const double* theta,
+                            int64_t* counts, void* ws, size_t ws_bytes, void* stream) {
+  return ham_impl(model, is_complex != 0, HAM_COUNT, xbits, n, n_spatial, e_core, h1, g2, drop, hidden, theta,
+                  nullptr, counts, nullptr, nullptr, nullptr, nullptr, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int irl_ham_connected_fill(int model, int is_complex, const uint64_t* xbits, int64_t n, int n_spatial, double e_core,
+                           const double* h1, const double* g2, double drop, int hidden, const double* theta,
+                           const int64_t* offsets, uint64_t* partner_bits, double* elements, double* coeff, void* ws,
+                           size_t ws_bytes, void* stream) {
+  return ham_impl(model, is_complex != 0, HAM_FILL, xbits, n, n_spatial, e_core, h1, g2, drop, hidden, theta, nullptr,
+                  nullptr, offsets, partner_bits, elements, coeff, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 }  // extern "C"
