@@ -410,6 +410,87 @@ def case_hamiltonian():
     return out
 
 
+def case_outer_step(step=1):
+    """The reference outer step (opt:118-195) assembled from reference
+    primitives for the RBM on the synthetic FCIDUMP of case_hamiltonian:
+    exact batch (local_energy, |psi|^2), est.energy_gradient, a ConnectedCache
+    from connected_configurations (first-appearance o_row order, est:236-249),
+    kry.irl_smallest on the full bordered operator with _batch_seed, the
+    direction, and the line search by exact energy re-evaluation (opt:104-115)."""
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from irlnqs.hamiltonian import connected_configurations, local_energy
+    from irlnqs.hilbert import enumerate_sector
+    from irlnqs.optimizer import OptimizerConfig, _batch_seed
+    from oracle import hamiltonian as oham
+    from oracle import nqs
+
+    ints = parse_fcidump(oham.random_fcidump(31, 5, 5, ms2=1))
+    sector = ints.sector()
+    configs = enumerate_sector(sector)
+    M, h = ints.n_spin_orbitals, 6
+    theta = np.random.default_rng(33).normal(0, 0.3, M + h + h * M)
+
+    def occ(b):
+        return ((b >> np.arange(M)) & 1).astype(np.uint8)[None, :]
+
+    def batch_at(th):
+        lp = lambda x: nqs.rbm_log_psi(th, occ(x.bits), M, h)[0]  # noqa: E731
+        lps = np.array([lp(x) for x in configs])
+        w = np.exp(2 * (lps - lps.max()))
+        w = w / w.sum()
+        e = np.array([local_energy(lp, ints, x) for x in configs])
+        xo = np.concatenate([occ(x.bits) for x in configs])
+        o = rbm_rows_np(th, xo, M, h).astype(complex)
+        return est.SampleBatch(configs=tuple(configs), weights=w, e_loc=e, o_matrix=o, n_samples=0), lp
+
+    batch, lp = batch_at(theta)
+    energy = est.estimate_energy(batch)
+    grad = est.energy_gradient(batch, energy)
+    o_rows, o_list, indptr, prow, coeff = {}, [], [0], [], []
+    for x in configs:
+        lx = lp(x)
+        for ent in connected_configurations(ints, x)[1:]:
+            b = ent.config.bits
+            if b not in o_rows:
+                o_rows[b] = len(o_list)
+                o_list.append(rbm_rows_np(theta, occ(b), M, h)[0].astype(complex))
+            prow.append(o_rows[b])
+            coeff.append(ent.element * np.exp(lp(ent.config) - lx))
+        indptr.append(len(prow))
+    cache = est.ConnectedCache(np.arange(len(configs)), np.array(indptr), np.array(prow), np.array(coeff, dtype=complex),
+                               np.array(o_list))
+    config = OptimizerConfig()
+    p = batch.param_count
+    pair = kry.irl_smallest(bordered_connected(batch, energy, grad, cache), p + 1, m=config.m, tol=config.tol,
+                            max_restarts=config.max_restarts, seed=_batch_seed(config, step))
+    d = direction(pair.vector, grad)
+
+    def energy_at(th):
+        return est.estimate_energy(batch_at(th)[0]).mean
+
+    scan = []
+
+    def line_search(dd, best):
+        best_scale, best_energy = best
+        best_d = dd
+        for scale in config.line_search:
+            e_new = energy_at(theta + scale * dd)
+            scan.append(e_new)
+            if np.isfinite(e_new) and e_new < best_energy:
+                best_energy, best_scale, best_d = e_new, scale, dd
+        return best_scale, best_energy, best_d
+
+    best_scale, best_energy, best_d = line_search(d, (0.0, energy.mean))
+    if best_scale == 0.0:
+        norm = float(np.linalg.norm(grad))
+        if norm > 0.0:
+            best_scale, best_energy, best_d = line_search(-grad / norm, (0.0, energy.mean))
+    theta_new = theta + best_scale * best_d if best_scale > 0 else theta
+    return dict(theta=theta, hidden=h, step=step, energy=energy.mean, grad=grad, lam=pair.value,
+                n_matvec=pair.n_matvec, converged=pair.converged, direction=d, best_scale=best_scale,
+                best_energy=best_energy, theta_new=theta_new, scan=np.array(scan))
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     only = set(sys.argv[1:])
@@ -424,6 +505,7 @@ def main():
         "rbm_connected": case_rbm_connected,
         "hermitian_connected": case_hermitian_connected,
         "hamiltonian": case_hamiltonian,
+        "outer_step": case_outer_step,
     }
     for name, data in cases.items():
         if only and name not in only:

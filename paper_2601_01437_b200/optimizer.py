@@ -14,8 +14,11 @@ The data-parallel part of ``irlnqs.optimizer.outer_step`` (``opt:130-165``):
   ``_batch_seed`` (``opt:100-101``);
 * the direction ``d = c[1:]/c0`` (``opt:160-165``).
 
-Line search, Adam and the run loop (``opt:167-269``) need the energy
-re-evaluated from a Hamiltonian and are out of scope.
+With a molecular Hamiltonian (:mod:`.hamiltonian`) the whole reference
+outer step runs on the device: :func:`outer_step` (``opt:118-195``: exact
+batch, connected cache, the solve, the line search over ``config.line_search``
+with the steepest-descent fallback) and :func:`energy_at` (``opt:104-115``).
+Adam and the run loop (``opt:198-269``) are out of scope.
 
 Complex-parameter (Hermitian, cfg4) batches use the reference's real
 embedding ``[u0, Re c, Im c]`` (dimension 2P+1), so the driver,
@@ -42,9 +45,12 @@ from .estimators import (
 )
 
 
+DEFAULT_LINE_SEARCH_GRID = tuple(2.0**k for k in range(-6, 2))  # opt:29
+
+
 @dataclass(frozen=True)
 class OptimizerConfig:
-    """Solver subset of ``opt:41-57`` (defaults identical)."""
+    """``opt:41-57`` minus Adam (defaults identical)."""
 
     method: str = "irl"  # irl | sl
     m: int = 20
@@ -52,6 +58,10 @@ class OptimizerConfig:
     max_restarts: int = 300
     sl_budget: int = 100
     seed: int = 111
+    max_outer_steps: int = 50
+    convergence_eps: float = 1e-10
+    line_search: tuple = DEFAULT_LINE_SEARCH_GRID
+    n_samples: int = 0  # 0 = exact enumeration
 
     def __post_init__(self):
         if self.method not in ("irl", "sl"):
@@ -205,3 +215,79 @@ def solve_step(batch: SampleBatch, config: OptimizerConfig = OptimizerConfig(), 
     d = direction_from_vector(pair.vector, gradient, batch.param_count, lay.hermitian)
     return StepResult(direction=d, lambda_min=float(pair.value), n_matvec=pair.n_matvec,
                       converged=pair.converged, pair=pair, energy=energy)
+
+
+def energy_at(params, integrals, sector, config: OptimizerConfig = OptimizerConfig(), step: int = 0) -> float:
+    """opt:104-115: the batch energy at ``params`` (exact enumeration).
+
+    Only log psi (weights |psi|^2) and the local energies are needed -- no O rows.
+    """
+    from . import ansatz as A, hamiltonian as H
+
+    if config.n_samples != 0:
+        raise NotImplementedError("stochastic energies need an RBM/MLP sampler (exact mode only)")
+    bits = H.enumerate_sector(sector)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    xb = torch.as_tensor(bits.view(np.int64), device=dev)
+    e = H.local_energies(params, integrals, xb, device=dev)
+    lp = A.log_amplitude_batch(params, H.bits_to_occupations(bits, params.architecture.n_inputs), device=dev)
+    lr = lp.real if torch.is_complex(lp) else lp
+    w = torch.exp(2.0 * (lr - lr.max()))
+    w = w / w.sum()
+    val = (w.to(e.dtype) * e).sum()
+    return float(val.real if torch.is_complex(val) else val)
+
+
+@dataclass(frozen=True)
+class OuterStep:
+    params: object
+    lambda_min: float
+    step_scale: float
+    matvecs: int
+    converged: bool
+    energy: float  # energy of the batch the step was solved on
+    best_energy: float  # line-search energy at the accepted scale (= energy if none)
+
+
+def outer_step(params, integrals, sector, config: OptimizerConfig = OptimizerConfig(), step: int = 0, *,
+               mode: int = _lib.MVP_AUTO) -> OuterStep:
+    """opt:118-195 on the device for the shallow NQS (exact mode).
+
+    Batch (E_loc, |psi|^2 weights, O rows), energy, gradient, connected cache,
+    the bordered IRL / SL solve with ``heff_matvec + heff_offdiag_matvec``,
+    the direction ``c[1:]/c0``, then the line search over ``config.line_search``
+    by exact energy re-evaluation, falling back to the normalised steepest
+    descent ``-F/|F|`` when no scale lowers the energy (opt:167-190).
+    """
+    from . import ansatz as A, hamiltonian as H
+
+    if config.n_samples != 0:
+        raise NotImplementedError("stochastic batches need an RBM/MLP sampler (exact mode only)")
+    batch = H.build_batch(params, integrals, sector)
+    energy = estimate_energy(batch)
+    cache = H.build_connected_cache(params, integrals, sector, batch)
+    res = solve_step(batch, config, step, energy=energy, mode=mode, connected=cache)
+    grad = energy_gradient(batch, energy).detach().cpu().numpy()
+    d0 = res.direction.detach().cpu().numpy()
+    theta = np.asarray(params.theta)
+
+    def line_search(d, best):
+        best_scale, best_energy = best
+        best_d = d
+        for scale in config.line_search:
+            cand = A.AnsatzParameters(params.architecture, theta + scale * d)
+            e_new = energy_at(cand, integrals, sector, config, step)
+            if np.isfinite(e_new) and e_new < best_energy:
+                best_energy, best_scale, best_d = e_new, scale, d
+        return best_scale, best_energy, best_d
+
+    best_scale, best_energy, best_d = line_search(d0, (0.0, energy.mean))
+    if best_scale == 0.0:
+        norm = float(np.linalg.norm(grad))
+        if norm > 0.0:
+            best_scale, best_energy, best_d = line_search(-grad / norm, (0.0, energy.mean))
+    new = params
+    if best_scale > 0.0:
+        new = A.AnsatzParameters(params.architecture, theta + best_scale * best_d)
+    return OuterStep(params=new, lambda_min=res.lambda_min, step_scale=best_scale, matvecs=res.n_matvec,
+                     converged=res.converged, energy=energy.mean, best_energy=best_energy)

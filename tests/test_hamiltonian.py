@@ -255,3 +255,27 @@ def test_exact_batch_and_connected_step(cuda, g, name):
     assert res.n_matvec == pair["n_matvec"]
     assert abs(res.lambda_min - pair["value"]) <= 1e-10 * abs(pair["value"])
     assert rel(host(res.direction), d) < 1e-8
+
+
+@pytest.mark.gpu
+def test_outer_step_golden(cuda, g):
+    """The reference outer step (opt:118-195, assembled from reference
+    primitives in oracle/make_golden.py::case_outer_step) on the device: same
+    matvec count, Ritz value, direction, accepted line-search scale and energy."""
+    from paper_2601_01437_b200 import ansatz as A, optimizer as OPT
+
+    o = golden("outer_step")
+    ints = device_integrals(g)
+    M = ints.n_spin_orbitals
+    params = A.AnsatzParameters(A.RBMArchitecture(M, int(o["hidden"])), o["theta"])
+    cfg = OPT.OptimizerConfig()
+    res = OPT.outer_step(params, ints, ints.sector(), cfg, int(o["step"]))
+    assert abs(res.energy - float(o["energy"])) < 1e-10 * abs(float(o["energy"]))
+    assert res.matvecs == int(o["n_matvec"])
+    assert abs(res.lambda_min - float(o["lam"])) <= 1e-10 * abs(float(o["lam"]))
+    assert res.step_scale == float(o["best_scale"])
+    assert abs(res.best_energy - float(o["best_energy"])) < 1e-10 * abs(float(o["best_energy"]))
+    assert rel(res.params.theta, o["theta_new"]) < 1e-8
+    scan = [OPT.energy_at(A.AnsatzParameters(params.architecture, o["theta"] + s * o["direction"]), ints,
+                          ints.sector()) for s in cfg.line_search]
+    assert rel(scan, o["scan"][: len(scan)]) < 1e-10
