@@ -45,6 +45,7 @@ struct HamArgs {
   const void* avec;  // RBM a (M), S
   const void* bvec;  // b (h), S
   const void* WT;    // (M x h) transposed W, S
+  const void* EX;    // (M x h x 2) {exp(W^T), exp(-W^T)}, S (RBM)
   const double* uvec;  // MLP u (h)
   void* out;         // ELOC: S[n]
   int64_t* counts;   // COUNT: [n]
@@ -77,8 +78,10 @@ __device__ __forceinline__ double2 ham_exp<true>(double2 z) {
   return make_double2(m * c, m * s);
 }
 
-template <bool CPLX, int MODEL, int MODE>
-__global__ void __launch_bounds__(HAM_NT) k_local_energy(const HamArgs a) {
+// SMT: the RBM exp table lives in shared memory (rows padded by one entry so
+// lanes on different orbitals hit different banks); one CTA of NT threads per SM.
+template <bool CPLX, int MODEL, int MODE, int NT = HAM_NT, bool SMT = false>
+__global__ void __launch_bounds__(NT) k_local_energy(const HamArgs a) {
   using T = Traits<CPLX>;
   using S = typename T::S;
   extern __shared__ __align__(16) unsigned char smem_hm[];
@@ -86,14 +89,25 @@ __global__ void __launch_bounds__(HAM_NT) k_local_energy(const HamArgs a) {
   S* th = reinterpret_cast<S*>(smem_hm);  // [h] theta_j(x)
   S* fp = th + h;                         // [h] RBM P_j / MLP tanh theta_j
   S* fq = fp + h;                         // [h] RBM Q_j
+  // SMT: [M][h + 1][2] exp table, 16-B aligned for the paired loads
+  S* ex_s = reinterpret_cast<S*>(smem_hm + ((3 * (size_t)h * sizeof(S) + 15) & ~(size_t)15));
   __shared__ int occ_l[4][32];            // occ up, vir up, occ down, vir down
   __shared__ int cnt_l[4];
   __shared__ int occ_all[64];
   __shared__ int n_occ_all;
   __shared__ unsigned short pairs[4][HAM_MAXPAIR];
-  __shared__ S red[HAM_NT / 32];
-  __shared__ int64_t scan[HAM_NT];
+  __shared__ S red[NT / 32];
+  __shared__ int64_t scan[NT];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ex_ld = SMT ? h + 1 : h;  // table row stride (entries)
+  if constexpr (SMT) {
+    const S* src = reinterpret_cast<const S*>(a.EX);
+    for (int64_t e = tid; e < (int64_t)M * h; e += NT) {
+      const int row = (int)(e / h), j = (int)(e % h);
+      ex_s[2 * ((int64_t)row * ex_ld + j)] = src[2 * e];
+      ex_s[2 * ((int64_t)row * ex_ld + j) + 1] = src[2 * e + 1];
+    }
+  }
 
   for (int64_t r = blockIdx.x; r < a.n; r += gridDim.x) {
     const uint64_t x = a.xbits[r];
@@ -117,7 +131,7 @@ __global__ void __launch_bounds__(HAM_NT) k_local_energy(const HamArgs a) {
     }
     // theta_j(x) and the ratio factors
     const S* WT = reinterpret_cast<const S*>(a.WT);
-    for (int j = tid; j < h; j += HAM_NT) {
+    for (int j = tid; j < h; j += NT) {
       S acc = reinterpret_cast<const S*>(a.bvec)[j];
       uint64_t bits = x;
       while (bits) {
@@ -145,7 +159,7 @@ __global__ void __launch_bounds__(HAM_NT) k_local_energy(const HamArgs a) {
     const int64_t D_d = (int64_t)(nod * (nod - 1) / 2) * (nvd * (nvd - 1) / 2);
     const int64_t D_o = (int64_t)nou * nod * nvu * nvd;
     const int64_t Tot = S_u + S_d + D_u + D_d + D_o;
-    const int64_t lo = Tot * tid / HAM_NT, hi = Tot * (tid + 1) / HAM_NT;
+    const int64_t lo = Tot * tid / NT, hi = Tot * (tid + 1) / NT;
     const double* g = a.g2;
     auto G = [&](int p, int q, int s, int t) { return __ldg(g + (((int64_t)p * ns + q) * ns + s) * ns + t); };
 
@@ -218,24 +232,47 @@ __global__ void __launch_bounds__(HAM_NT) k_local_energy(const HamArgs a) {
       const S* wn = n >= 0 ? WT + (int64_t)n * h : nullptr;
       const S* wq = n >= 0 ? WT + (int64_t)q * h : nullptr;
       if constexpr (MODEL == MODEL_RBM) {
+        // e^{D_j} = e^{W_jp} e^{W_jq} e^{-W_jm} e^{-W_jn} from the exp table: no exp, no
+        // division; {e^{W}, e^{-W}} of one (orbital, unit) share a 16-B (32-B complex) entry
+        const S* EX = SMT ? ex_s : reinterpret_cast<const S*>(a.EX);  // [M][ex_ld][2]
         const S* av = reinterpret_cast<const S*>(a.avec);
         S lin = T::sub(av[p], av[m]);
         if (n >= 0) lin = T::add(lin, T::sub(av[q], av[n]));
         S prod;
         if constexpr (CPLX) prod = make_double2(1.0, 0.0); else prod = 1.0;
-        for (int j = 0; j < h; ++j) {
-          S d = T::sub(__ldg(wp + j), __ldg(wm + j));
-          if (n >= 0) d = T::add(d, T::sub(__ldg(wq + j), __ldg(wn + j)));
-          const S e = ham_exp<CPLX>(d);
-          S f;
+        const S* tp = EX + (int64_t)p * ex_ld * 2;
+        const S* tm = EX + (int64_t)m * ex_ld * 2;
+        auto ld2 = [](const S* t, int j, S& plus, S& minus) {
           if constexpr (CPLX) {
-            const double den = e.x * e.x + e.y * e.y;
-            const double2 ei = make_double2(e.x / den, -e.y / den);
-            f = T::add(T::mul(fp[j], e), T::mul(fq[j], ei));
+            plus = SMT ? t[2 * j] : __ldg(t + 2 * j);
+            minus = SMT ? t[2 * j + 1] : __ldg(t + 2 * j + 1);
           } else {
-            f = fp[j] * e + fq[j] / e;
+            const double2 v = SMT ? reinterpret_cast<const double2*>(t)[j] : __ldg(reinterpret_cast<const double2*>(t) + j);
+            plus = v.x;
+            minus = v.y;
           }
-          prod = T::mul(prod, f);
+        };
+        if (n < 0) {
+          for (int j = 0; j < h; ++j) {
+            S pp, ip, pm, im;
+            ld2(tp, j, pp, ip);
+            ld2(tm, j, im, pm);
+            const S e = T::mul(pp, pm), ei = T::mul(ip, im);
+            prod = T::mul(prod, T::add(T::mul(fp[j], e), T::mul(fq[j], ei)));
+          }
+        } else {
+          const S* tq = EX + (int64_t)q * ex_ld * 2;
+          const S* tn = EX + (int64_t)n * ex_ld * 2;
+          for (int j = 0; j < h; ++j) {
+            S pp, ip, pm, im, pq, iq, pn, in_;
+            ld2(tp, j, pp, ip);
+            ld2(tm, j, im, pm);
+            ld2(tq, j, pq, iq);
+            ld2(tn, j, in_, pn);
+            const S e = T::mul(T::mul(pp, pm), T::mul(pq, pn));
+            const S ei = T::mul(T::mul(ip, im), T::mul(iq, in_));
+            prod = T::mul(prod, T::add(T::mul(fp[j], e), T::mul(fq[j], ei)));
+          }
         }
         return T::mul(ham_exp<CPLX>(lin), prod);
       } else {
@@ -250,8 +287,10 @@ __global__ void __launch_bounds__(HAM_NT) k_local_energy(const HamArgs a) {
     };
 
     if constexpr (MODE == HAM_ELOC) {
+      // strided: neighbouring lanes share holes and walk the particles, so
+      // their table rows coincide or sit close in L1
       S acc = T::zero();
-      for (int64_t idx = lo; idx < hi; ++idx) {
+      for (int64_t idx = tid; idx < Tot; idx += NT) {
         int m, n, p, q;
         decode(idx, m, n, p, q);
         const double el = element(m, n, p, q);
@@ -282,7 +321,7 @@ __global__ void __launch_bounds__(HAM_NT) k_local_energy(const HamArgs a) {
       __syncthreads();
       if (tid == 0) {
         S e = red[0];
-        for (int w = 1; w < HAM_NT / 32; ++w) e = T::add(e, red[w]);
+        for (int w = 1; w < NT / 32; ++w) e = T::add(e, red[w]);
         reinterpret_cast<S*>(a.out)[r] = e;
       }
     } else {
@@ -297,7 +336,7 @@ __global__ void __launch_bounds__(HAM_NT) k_local_energy(const HamArgs a) {
         __syncthreads();
         if (tid == 0) {
           int64_t s = 0;
-          for (int t = 0; t < HAM_NT; ++t) s += scan[t];
+          for (int t = 0; t < NT; ++t) s += scan[t];
           a.counts[r] = s;
         }
       } else {
@@ -305,7 +344,7 @@ __global__ void __launch_bounds__(HAM_NT) k_local_energy(const HamArgs a) {
         __syncthreads();
         if (tid == 0) {
           int64_t s = 0;
-          for (int t = 0; t < HAM_NT; ++t) {
+          for (int t = 0; t < NT; ++t) {
             const int64_t c = scan[t];
             scan[t] = s;
             s += c;
@@ -333,14 +372,21 @@ __global__ void __launch_bounds__(HAM_NT) k_local_energy(const HamArgs a) {
   }
 }
 
-// W (h x M, row-major) -> WT (M x h)
+// W (h x M, row-major) -> WT (M x h) and, for the RBM ratio, EX = {exp(W^T), exp(-W^T)}
 template <bool CPLX>
 __global__ void k_transpose_w(const typename Traits<CPLX>::S* __restrict__ W, int h, int M,
-                              typename Traits<CPLX>::S* __restrict__ WT) {
+                              typename Traits<CPLX>::S* __restrict__ WT, typename Traits<CPLX>::S* __restrict__ EX) {
+  using S = typename Traits<CPLX>::S;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)h * M) return;
   const int j = (int)(e / M), i = (int)(e % M);
-  WT[(int64_t)i * h + j] = W[e];
+  const S w = W[e];
+  const int64_t o = (int64_t)i * h + j;
+  WT[o] = w;
+  if (EX) {
+    EX[2 * o] = ham_exp<CPLX>(w);
+    if constexpr (CPLX) EX[2 * o + 1] = ham_exp<CPLX>(make_double2(-w.x, -w.y)); else EX[2 * o + 1] = ham_exp<CPLX>(-w);
+  }
 }
 
 }  // namespace irl

@@ -1441,15 +1441,26 @@ int logamp_impl(const uint8_t* x, int64_t n, int n_vis, int hidden, const double
 
 // ---------------------------------------------------------- hamiltonian ---
 size_t ham_ws_bytes(int n_vis, int hidden, bool cplx) {
-  return align256((size_t)n_vis * std::max(hidden, 1) * (cplx ? 16 : 8));
+  return 3 * align256((size_t)n_vis * std::max(hidden, 1) * (cplx ? 16 : 8));  // W^T, exp(W^T), exp(-W^T)
 }
 
 template <bool CPLX, int MODEL, int MODE>
 int ham_launch(const HamArgs& a, size_t smem, cudaStream_t st) {
-  auto fn = k_local_energy<CPLX, MODEL, MODE>;
   DevInfo d;
   IRL_TRY(dev_info(d));
   if (smem > (size_t)d.smem_optin - 8192) return fail(IRL_ERR_ARG, "hidden width too large for the local-energy kernel");
+  // E_loc of the RBM: the exp table in shared memory when it fits (one 512-thread CTA per SM)
+  if constexpr (MODE == HAM_ELOC && MODEL == MODEL_RBM) {
+    const size_t tab = (size_t)2 * a.ns * (a.hidden + 1) * 2 * (CPLX ? 16 : 8);
+    if (!getenv("IRL_HAM_NO_SMT") && rup(smem, 16) + tab <= (size_t)d.smem_optin - 16384) {
+      auto fn = k_local_energy<CPLX, MODEL, MODE, 512, true>;
+      IRL_TRY(ensure_fn_attrs((const void*)fn, d.smem_optin));
+      const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(a.n, (int64_t)d.sms));
+      fn<<<grid, 512, rup(smem, 16) + tab, st>>>(a);
+      return cuda_check(cudaGetLastError(), "local-energy kernel launch");
+    }
+  }
+  auto fn = k_local_energy<CPLX, MODEL, MODE>;
   IRL_TRY(ensure_fn_attrs((const void*)fn, d.smem_optin));
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(a.n, (int64_t)d.sms * 16));
   fn<<<grid, HAM_NT, smem, st>>>(a);
@@ -1491,7 +1502,10 @@ int ham_impl(int model, bool cplx, int mode, const uint64_t* xbits, int64_t n, i
     a.bvec = th + (size_t)hidden * M * sS;
     a.uvec = theta + (size_t)hidden * M + hidden;
   }
+  const size_t tab = align256((size_t)M * hidden * sS);
   a.WT = ws;
+  void* EX = model == MODEL_RBM ? static_cast<char*>(ws) + tab : nullptr;
+  a.EX = EX;
   a.out = out;
   a.counts = counts;
   a.offsets = offsets;
@@ -1500,9 +1514,11 @@ int ham_impl(int model, bool cplx, int mode, const uint64_t* xbits, int64_t n, i
   a.pcoeff = pcoeff;
   const int64_t ne = (int64_t)hidden * M;
   if (cplx)
-    k_transpose_w<true><<<(unsigned)cdiv(ne, 256), 256, 0, st>>>((const double2*)Wm, hidden, M, (double2*)ws);
+    k_transpose_w<true><<<(unsigned)cdiv(ne, 256), 256, 0, st>>>((const double2*)Wm, hidden, M, (double2*)ws,
+                                                                 (double2*)EX);
   else
-    k_transpose_w<false><<<(unsigned)cdiv(ne, 256), 256, 0, st>>>((const double*)Wm, hidden, M, (double*)ws);
+    k_transpose_w<false><<<(unsigned)cdiv(ne, 256), 256, 0, st>>>((const double*)Wm, hidden, M, (double*)ws,
+                                                                  (double*)EX);
   IRL_TRY(cuda_check(cudaGetLastError(), "transpose launch"));
   const size_t smem = (size_t)3 * hidden * sS;
 #define IRL_HAM(C, MD, MO) \
