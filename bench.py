@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--no-otf", action="store_true")
     ap.add_argument("--no-connected", action="store_true")
     ap.add_argument("--partners", type=int, default=4, help="synthetic connected partners per row")
+    ap.add_argument("--no-eloc", action="store_true")
     return ap.parse_args()
 
 
@@ -470,6 +471,15 @@ def run_ours(args):
                          "seeded synthetic single-excitation partners, not a Hamiltonian")}
         del cache
 
+    # ---- local energies: cfg2-shaped RBM on a seeded synthetic molecule
+    eloc = None
+    if not args.no_eloc:
+        sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "tools"))
+        import eloc_bench
+
+        eloc = eloc_bench.run(n_samples=cfg.n_rows if cfg.model == "rbm" else 65536, cpu_samples=1,
+                              with_cpu=(rank == 0 and not args.no_cpu))
+
     if rank != 0:
         reps.close()
         return 0
@@ -521,6 +531,7 @@ def run_ours(args):
         "irl_solve": irl,
         "otf_mode": otf,
         "connected_mode": conn,
+        "local_energy_mode": eloc,
         "obuild_ms": obuild_ms,
         "obuild_write_gbs": N * P * b_el / (obuild_ms / 1e3) / 1e9,
         "mvp_ms_per_product": elapsed / mvps * 1e3,

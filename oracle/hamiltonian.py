@@ -143,21 +143,8 @@ def dense_hamiltonian(e_core, h, g, configs, ns):
 
 
 def random_fcidump(seed, ns, n_elec, ms2=0, scale=0.3):
-    """Seeded synthetic FCIDUMP text with 8-fold symmetric integrals (one line per unique quadruple)."""
-    rng = np.random.default_rng(seed)
-    lines = [f"&FCI NORB={ns},NELEC={n_elec},MS2={ms2},", " ORBSYM=" + ",".join(["1"] * ns) + ",", " ISYM=1,", "&END"]
-    seen = set()
-    for i in range(1, ns + 1):
-        for j in range(1, i + 1):
-            for k in range(1, ns + 1):
-                for l in range(1, k + 1):
-                    key = tuple(sorted([(i, j), (k, l)]))
-                    if key in seen:
-                        continue
-                    seen.add(key)
-                    lines.append(f"{rng.normal(0.0, scale):.16e} {i} {j} {k} {l}")
-    for i in range(1, ns + 1):
-        for j in range(1, i + 1):
-            lines.append(f"{rng.normal(-1.0 if i == j else 0.0, scale):.16e} {i} {j} 0 0")
-    lines.append(f"{rng.normal(0.5, 0.1):.16e} 0 0 0 0")
-    return "\n".join(lines) + "\n"
+    """Seeded synthetic FCIDUMP text (input generator; lives with the other
+    synthetic inputs in paper_2601_01437_b200/synthetic.py)."""
+    from paper_2601_01437_b200.synthetic import molecule_fcidump
+
+    return molecule_fcidump(seed, ns, n_elec, ms2=ms2, scale=scale)

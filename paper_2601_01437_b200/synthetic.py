@@ -122,3 +122,26 @@ def connected_partners(x: np.ndarray, per_row: int, seed: int, element_std: floa
     elements = rng.normal(0.0, element_std, N * per_row)
     indptr = np.arange(0, N * per_row + 1, per_row, dtype=np.int64)
     return partners.reshape(N * per_row, n), elements, indptr, np.arange(N, dtype=np.int64)
+
+
+def molecule_fcidump(seed, ns, n_elec, ms2=0, scale=0.3):
+    """Seeded synthetic FCIDUMP text with 8-fold symmetric integrals (one line per
+    unique quadruple; diagonal h around -1, core energy around 0.5).  No molecule
+    stands behind it: it feeds the local-energy path at chosen sizes."""
+    rng = np.random.default_rng(seed)
+    lines = [f"&FCI NORB={ns},NELEC={n_elec},MS2={ms2},", " ORBSYM=" + ",".join(["1"] * ns) + ",", " ISYM=1,", "&END"]
+    seen = set()
+    for i in range(1, ns + 1):
+        for j in range(1, i + 1):
+            for k in range(1, ns + 1):
+                for l in range(1, k + 1):
+                    key = tuple(sorted([(i, j), (k, l)]))
+                    if key in seen:
+                        continue
+                    seen.add(key)
+                    lines.append(f"{rng.normal(0.0, scale):.16e} {i} {j} {k} {l}")
+    for i in range(1, ns + 1):
+        for j in range(1, i + 1):
+            lines.append(f"{rng.normal(-1.0 if i == j else 0.0, scale):.16e} {i} {j} 0 0")
+    lines.append(f"{rng.normal(0.5, 0.1):.16e} 0 0 0 0")
+    return "\n".join(lines) + "\n"

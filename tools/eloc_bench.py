@@ -31,11 +31,9 @@ def sector_samples(rng, ns, n_up, n_dn, count):
 
 
 def run(n_samples=8192, cpu_samples=2, ns=20, n_elec=20, hidden=160, seed=7, with_cpu=True):
-    from oracle import hamiltonian as oham
-    from oracle import nqs
-    from paper_2601_01437_b200 import ansatz as A, hamiltonian as H
+    from paper_2601_01437_b200 import ansatz as A, hamiltonian as H, synthetic as S
 
-    ints = H.parse_fcidump(oham.random_fcidump(seed, ns, n_elec, scale=0.05))
+    ints = H.parse_fcidump(S.molecule_fcidump(seed, ns, n_elec, scale=0.05))
     sec = ints.sector()
     rng = np.random.default_rng(seed + 1)
     M = 2 * ns
@@ -61,6 +59,9 @@ def run(n_samples=8192, cpu_samples=2, ns=20, n_elec=20, hidden=160, seed=7, wit
            "partners_kept": nnz, "partners_per_sample": nnz / n_samples,
            "partner_evals_per_s": nnz / (ms / 1e3), "connected_csr_ms": cache_ms}
     if with_cpu:
+        from oracle import hamiltonian as oham  # the CPU baseline leg only
+        from oracle import nqs
+
         def lp(b):
             x = ((np.uint64(b) >> np.arange(M, dtype=np.uint64)) & np.uint64(1)).astype(np.uint8)[None, :]
             return nqs.rbm_log_psi(theta, x, M, hidden)[0]
