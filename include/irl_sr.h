@@ -248,6 +248,35 @@ int irl_ham_connected_fill(int model, int is_complex, const uint64_t* xbits, int
                            const int64_t* offsets, uint64_t* partner_bits, double* elements, double* coeff, void* ws,
                            size_t ws_bytes, void* stream);
 
+/* ------------------------------- §8(f) 4: the reference's own ansatz ----
+ * Autoregressive NQS of ansatz.py (ans:1-290), flat theta in the reference
+ * layout [W1 (h x 2M), b1, W2 (2 x h), b2, Wp (h x M), bp, up, w_lin, c];
+ * configurations are uint64 bitmasks in the sector (n_up, n_down); h <= 64.
+ *   irl_ar_logamp  ln psi = (ln p / 2, phase) per configuration, -inf outside
+ *                  the sector (log_amplitude, ans:229-247); logpsi interleaved c128
+ *   irl_ar_rows    O rows d ln psi / d theta into N x ld complex (log_derivative,
+ *                  ans:249-290; *error = 1 for a configuration outside the sector)
+ *   irl_ar_sample  exact ancestral sampling (sample, ans:215-236): rng_states
+ *                  (n x 4 uint64: state hi, lo, inc hi, lo) are numpy PCG64
+ *                  streams of SeedSequence(seed).spawn(n), replayed bit for bit
+ * Local energies with this ansatz (ham:290-302) combine the Hamiltonian-only
+ * enumeration (irl_ham_diagonal_and_count, irl_ham_partners_fill: <x|H|x>,
+ * kept partners and elements), irl_ar_logamp on the partners, and
+ * irl_eloc_combine: E_loc = diag + sum element exp(ln psi(y) - ln psi(x)). */
+int irl_ar_logamp(const uint64_t* xbits, int64_t n, int n_orbitals, int hidden, int n_up, int n_down,
+                  const double* theta, double* logpsi, int* error, void* stream);
+int irl_ar_rows(const uint64_t* xbits, int64_t n, int n_orbitals, int hidden, int n_up, int n_down,
+                const double* theta, double* O, int64_t ld, int* error, void* stream);
+int irl_ar_sample(const uint64_t* rng_states, int64_t n, int n_orbitals, int hidden, int n_up, int n_down,
+                  const double* theta, uint64_t* out_bits, int* error, void* stream);
+int irl_ham_diagonal_and_count(const uint64_t* xbits, int64_t n, int n_spatial, double e_core, const double* h1,
+                               const double* g2, double drop, double* diag, int64_t* counts, void* stream);
+int irl_ham_partners_fill(const uint64_t* xbits, int64_t n, int n_spatial, double e_core, const double* h1,
+                          const double* g2, double drop, const int64_t* offsets, uint64_t* partner_bits,
+                          double* elements, void* stream);
+int irl_eloc_combine(const int64_t* indptr, const double* elements, const double* logpsi_partner,
+                     const double* logpsi_x, const double* diag, int64_t n, double* eloc, void* stream);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

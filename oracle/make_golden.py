@@ -491,6 +491,59 @@ def case_outer_step(step=1):
                 best_energy=best_energy, theta_new=theta_new, scan=np.array(scan))
 
 
+def case_autoregressive():
+    """The reference's own ansatz (ans:1-290) on H2 and on a seeded synthetic
+    FCIDUMP (5 spatial orbitals, 3 up + 2 down): log amplitudes (in and out of
+    the sector), log-derivative rows, exact samples, local energies, a
+    stochastic build_batch, and the reference outer_step itself (opt:118-195)
+    in exact and stochastic mode."""
+    import warnings
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from irlnqs import optimizer as opt
+    from irlnqs.hamiltonian import local_energy
+    from irlnqs.hilbert import OccupationVector, enumerate_sector
+    from paper_2601_01437_b200.synthetic import molecule_fcidump
+
+    out = {}
+    with open(os.path.join(REF, "tests", "data", "h2_sto3g.fcidump")) as fh:
+        h2 = parse_fcidump(fh.read())
+    syn = parse_fcidump(molecule_fcidump(31, 5, 5, ms2=1))
+    for tag, ints, hidden, seed in (("h2", h2, 3, 9), ("syn", syn, 6, 5)):
+        sector = ints.sector()
+        arch = ans.Architecture(sector.n_orbitals, hidden)
+        init = ans.init_parameters(arch, seed=seed)
+        rng = np.random.default_rng(41)
+        params = ans.AnsatzParameters(arch, init.theta + 0.1 * rng.standard_normal(arch.param_count))
+        configs = enumerate_sector(sector)
+        M = sector.n_orbitals
+        bits = np.array([c.bits for c in configs], dtype=np.uint64)
+        outside = np.array([3, (1 << M) - 1, 0], dtype=np.uint64)
+        la = [ans.log_amplitude(params, OccupationVector(int(b), M), sector) for b in np.concatenate([bits, outside])]
+        rows = np.array([ans.log_derivative(params, c, sector) for c in configs[:24]])
+        samples = np.array([x.bits for x in ans.sample(params, sector, 64, seed=13)], dtype=np.uint64)
+        lp = lambda x: ans.log_amplitude(params, x, sector).value  # noqa: E731
+        eloc = np.array([local_energy(lp, ints, c) for c in configs[:40]])
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            sb = est.build_batch(params, ints, sector, n_samples=64, seed=13)
+        d = dict(theta=params.theta, hidden=hidden, n_up=sector.n_up, n_down=sector.n_down, M=M, bits=bits,
+                 outside=outside, log_prob_half=np.array([a.log_prob_half for a in la]),
+                 phase=np.array([a.phase for a in la]), rows=rows, samples=samples, eloc=eloc,
+                 sb_e=np.array(sb.e_loc), sb_w=np.array(sb.weights), sb_o=np.array(sb.o_matrix),
+                 sb_bits=np.array([x.bits for x in sb.configs], dtype=np.uint64),
+                 e_core=ints.e_core, h=ints.h, g=ints.g, ns=ints.n_spatial)
+        for mode, ns_ in (("exact", 0), ("stoch", 64)):
+            config = opt.OptimizerConfig(n_samples=ns_, max_restarts=300)
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore")
+                new, lam, scale, matvecs, conv = opt.outer_step(params, ints, sector, config, 1)
+            d.update({f"{mode}_theta_new": new.theta, f"{mode}_lam": lam, f"{mode}_scale": scale,
+                      f"{mode}_matvecs": matvecs, f"{mode}_converged": conv})
+        out.update({f"{tag}_{k}": v for k, v in d.items()})
+    return out
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     only = set(sys.argv[1:])
@@ -506,6 +559,7 @@ def main():
         "hermitian_connected": case_hermitian_connected,
         "hamiltonian": case_hamiltonian,
         "outer_step": case_outer_step,
+        "autoregressive": case_autoregressive,
     }
     for name, data in cases.items():
         if only and name not in only:

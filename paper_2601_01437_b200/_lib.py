@@ -85,6 +85,12 @@ SIGNATURES = {
     "irl_ham_local_energy": (_I, [_I, _I, _P, _I64, _I, _D, _P, _P, _D, _I, _P, _P, _P, _SZ, _P]),
     "irl_ham_connected_count": (_I, [_I, _I, _P, _I64, _I, _D, _P, _P, _D, _I, _P, _P, _P, _SZ, _P]),
     "irl_ham_connected_fill": (_I, [_I, _I, _P, _I64, _I, _D, _P, _P, _D, _I, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "irl_ar_logamp": (_I, [_P, _I64, _I, _I, _I, _I, _P, _P, _P, _P]),
+    "irl_ar_rows": (_I, [_P, _I64, _I, _I, _I, _I, _P, _P, _I64, _P, _P]),
+    "irl_ar_sample": (_I, [_P, _I64, _I, _I, _I, _I, _P, _P, _P, _P]),
+    "irl_ham_diagonal_and_count": (_I, [_P, _I64, _I, _D, _P, _P, _D, _P, _P, _P]),
+    "irl_ham_partners_fill": (_I, [_P, _I64, _I, _D, _P, _P, _D, _P, _P, _P, _P]),
+    "irl_eloc_combine": (_I, [_P, _P, _P, _P, _P, _I64, _P, _P]),
 }
 
 

@@ -49,6 +49,7 @@ struct HamArgs {
   const double* uvec;  // MLP u (h)
   void* out;         // ELOC: S[n]
   int64_t* counts;   // COUNT: [n]
+  double* diag;      // COUNT (optional): [n] diagonal elements <x|H|x>
   const int64_t* offsets;  // FILL: [n] start of each sample's partners
   uint64_t* pbits;   // FILL
   double* pelem;     // FILL
@@ -131,7 +132,7 @@ __global__ void __launch_bounds__(NT) k_local_energy(const HamArgs a) {
     }
     // theta_j(x) and the ratio factors
     const S* WT = reinterpret_cast<const S*>(a.WT);
-    for (int j = tid; j < h; j += NT) {
+    for (int j = tid; j < (MODEL == MODEL_NONE ? 0 : h); j += NT) {
       S acc = reinterpret_cast<const S*>(a.bvec)[j];
       uint64_t bits = x;
       while (bits) {
@@ -227,6 +228,11 @@ __global__ void __launch_bounds__(NT) k_local_energy(const HamArgs a) {
     };
     // psi(y) / psi(x) for the excitation (m, n) -> (p, q)
     auto ratio = [&](int m, int n, int p, int q) -> S {
+      if constexpr (MODEL == MODEL_NONE) {
+        S one;
+        if constexpr (CPLX) one = make_double2(1.0, 0.0); else one = 1.0;
+        return one;
+      }
       const S* wm = WT + (int64_t)m * h;
       const S* wp = WT + (int64_t)p * h;
       const S* wn = n >= 0 ? WT + (int64_t)n * h : nullptr;
@@ -286,6 +292,25 @@ __global__ void __launch_bounds__(NT) k_local_energy(const HamArgs a) {
       }
     };
 
+    // diagonal element <x|H|x> (ham:190-201)
+    auto diag_element = [&]() -> double {
+      double val = a.e_core;
+      const int no = n_occ_all;
+      for (int k = 0; k < no; ++k) {
+        const int i = occ_all[k], si = ham_spatial(i, ns);
+        val += __ldg(a.h1 + si * ns + si);
+      }
+      for (int k = 0; k < no; ++k) {
+        const int i = occ_all[k], si = ham_spatial(i, ns);
+        for (int l = k + 1; l < no; ++l) {
+          const int j = occ_all[l], sj = ham_spatial(j, ns);
+          val += G(si, si, sj, sj);
+          if (ham_same(i, j, ns)) val -= G(si, sj, sj, si);
+        }
+      }
+      return val;
+    };
+
     if constexpr (MODE == HAM_ELOC) {
       // strided: neighbouring lanes share holes and walk the particles, so
       // their table rows coincide or sit close in L1
@@ -299,21 +324,7 @@ __global__ void __launch_bounds__(NT) k_local_energy(const HamArgs a) {
         if constexpr (CPLX) acc = make_double2(fma(el, rt.x, acc.x), fma(el, rt.y, acc.y)); else acc = fma(el, rt, acc);
       }
       if (tid == 0) {
-        // diagonal element (ham:190-201), ratio 1
-        double val = a.e_core;
-        const int no = n_occ_all;
-        for (int k = 0; k < no; ++k) {
-          const int i = occ_all[k], si = ham_spatial(i, ns);
-          val += __ldg(a.h1 + si * ns + si);
-        }
-        for (int k = 0; k < no; ++k) {
-          const int i = occ_all[k], si = ham_spatial(i, ns);
-          for (int l = k + 1; l < no; ++l) {
-            const int j = occ_all[l], sj = ham_spatial(j, ns);
-            val += G(si, si, sj, sj);
-            if (ham_same(i, j, ns)) val -= G(si, sj, sj, si);
-          }
-        }
+        const double val = diag_element();  // ratio 1
         if constexpr (CPLX) acc.x += val; else acc += val;
       }
       acc = warp_sum<CPLX>(acc);
@@ -338,6 +349,7 @@ __global__ void __launch_bounds__(NT) k_local_energy(const HamArgs a) {
           int64_t s = 0;
           for (int t = 0; t < NT; ++t) s += scan[t];
           a.counts[r] = s;
+          if (a.diag) a.diag[r] = diag_element();
         }
       } else {
         scan[tid] = kept;

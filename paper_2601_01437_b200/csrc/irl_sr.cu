@@ -21,6 +21,7 @@
 #include "wide.cuh"
 #include "connected.cuh"
 #include "hamiltonian.cuh"
+#include "autoreg.cuh"
 
 using namespace irl;
 
@@ -1470,16 +1471,22 @@ int ham_launch(const HamArgs& a, size_t smem, cudaStream_t st) {
 int ham_impl(int model, bool cplx, int mode, const uint64_t* xbits, int64_t n, int ns, double e_core, const double* h1,
              const double* g2, double drop, int hidden, const double* theta, void* out, int64_t* counts,
              const int64_t* offsets, uint64_t* pbits, double* pelem, double* pcoeff, void* ws, size_t ws_bytes,
-             cudaStream_t st) {
-  if (!xbits || !h1 || !g2 || !theta || n < 0 || ns < 1 || ns > 32 || hidden < 1)
+             cudaStream_t st, double* diag = nullptr) {
+  const bool none = model == MODEL_NONE;
+  if (!xbits || !h1 || !g2 || (!none && !theta) || n < 0 || ns < 1 || ns > 32 || (!none && hidden < 1))
     return fail(IRL_ERR_ARG, "bad local-energy arguments");
-  if (model != MODEL_RBM && model != MODEL_MLP) return fail(IRL_ERR_ARG, "unknown model %d", model);
+  if (model != MODEL_RBM && model != MODEL_MLP && !none) return fail(IRL_ERR_ARG, "unknown model %d", model);
+  if (none) {
+    if (mode == HAM_ELOC) return fail(IRL_ERR_ARG, "local energies need an ansatz");
+    cplx = false;
+    hidden = 0;
+  }
   if (cplx && model != MODEL_RBM) return fail(IRL_ERR_ARG, "complex parameters are an RBM feature");
   if (mode == HAM_ELOC && !out) return fail(IRL_ERR_ARG, "null output");
   if (mode == HAM_COUNT && !counts) return fail(IRL_ERR_ARG, "null counts");
   if (mode == HAM_FILL && (!offsets || !pbits || !pelem || !pcoeff)) return fail(IRL_ERR_ARG, "null fill outputs");
   const int M = 2 * ns;
-  if (ws_bytes < ham_ws_bytes(M, hidden, cplx)) return fail(IRL_ERR_WORKSPACE, "workspace too small");
+  if (!none && ws_bytes < ham_ws_bytes(M, hidden, cplx)) return fail(IRL_ERR_WORKSPACE, "workspace too small");
   if (n == 0) return IRL_OK;
   const size_t sS = cplx ? 16 : 8;
   HamArgs a{};
@@ -1491,6 +1498,17 @@ int ham_impl(int model, bool cplx, int mode, const uint64_t* xbits, int64_t n, i
   a.h1 = h1;
   a.g2 = g2;
   a.drop = drop;
+  a.diag = diag;
+  a.out = out;
+  a.counts = counts;
+  a.offsets = offsets;
+  a.pbits = pbits;
+  a.pelem = pelem;
+  a.pcoeff = pcoeff;
+  if (none) {
+    if (mode == HAM_COUNT) return ham_launch<false, MODEL_NONE, HAM_COUNT>(a, 0, st);
+    return ham_launch<false, MODEL_NONE, HAM_FILL>(a, 0, st);
+  }
   const char* th = reinterpret_cast<const char*>(theta);
   const char* Wm;
   if (model == MODEL_RBM) {
@@ -1534,6 +1552,27 @@ int ham_impl(int model, bool cplx, int mode, const uint64_t* xbits, int64_t n, i
   IRL_HAM(false, MODEL_MLP, HAM_FILL)
 #undef IRL_HAM
   return fail(IRL_ERR_ARG, "unsupported local-energy variant");
+}
+
+// ------------------------------------------------------- autoregressive ---
+int ar_check(int64_t n, int M, int h, int n_up, int n_down, const double* theta) {
+  if (n < 0 || M < 2 || M > 64 || (M & 1) || h < 1 || h > 64 || !theta) return fail(IRL_ERR_ARG, "bad autoregressive shape");
+  if (n_up < 0 || n_down < 0 || n_up > M / 2 || n_down > M / 2) return fail(IRL_ERR_ARG, "bad sector");
+  return IRL_OK;
+}
+
+template <int MODE>
+int ar_launch(ArArgs& a, cudaStream_t st) {
+  if (a.n == 0) return IRL_OK;
+  DevInfo d;
+  IRL_TRY(dev_info(d));
+  const int hpl = a.h <= 32 ? 1 : 2;
+  const size_t smem = MODE == AR_ROWS ? (size_t)AR_WARPS * a.M * 32 * hpl * 8 : 0;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(a.n, AR_WARPS), (int64_t)d.sms * 16));
+  auto fn = hpl == 1 ? k_autoreg<1, MODE> : k_autoreg<2, MODE>;
+  IRL_TRY(ensure_fn_attrs((const void*)fn, d.smem_optin));
+  fn<<<grid, AR_WARPS * 32, smem, st>>>(a);
+  return cuda_check(cudaGetLastError(), "autoregressive kernel launch");
 }
 
 }  // namespace
@@ -2080,6 +2119,84 @@ int irl_ham_connected_fill(int model, int is_complex, const uint64_t* xbits, int
                            size_t ws_bytes, void* stream) {
   return ham_impl(model, is_complex != 0, HAM_FILL, xbits, n, n_spatial, e_core, h1, g2, drop, hidden, theta, nullptr,
                   nullptr, offsets, partner_bits, elements, coeff, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int irl_ham_diagonal_and_count(const uint64_t* xbits, int64_t n, int n_spatial, double e_core, const double* h1,
+                               const double* g2, double drop, double* diag, int64_t* counts, void* stream) {
+  return ham_impl(MODEL_NONE, false, HAM_COUNT, xbits, n, n_spatial, e_core, h1, g2, drop, 0, nullptr, nullptr, counts,
+                  nullptr, nullptr, nullptr, nullptr, nullptr, 256, (cudaStream_t)stream, diag);
+}
+
+int irl_ham_partners_fill(const uint64_t* xbits, int64_t n, int n_spatial, double e_core, const double* h1,
+                          const double* g2, double drop, const int64_t* offsets, uint64_t* partner_bits,
+                          double* elements, void* stream) {
+  return ham_impl(MODEL_NONE, false, HAM_FILL, xbits, n, n_spatial, e_core, h1, g2, drop, 0, nullptr, nullptr, nullptr,
+                  offsets, partner_bits, elements, elements, nullptr, 256, (cudaStream_t)stream);
+}
+
+int irl_ar_logamp(const uint64_t* xbits, int64_t n, int n_orbitals, int hidden, int n_up, int n_down,
+                  const double* theta, double* logpsi, int* error, void* stream) {
+  IRL_TRY(ar_check(n, n_orbitals, hidden, n_up, n_down, theta));
+  if (!xbits || !logpsi || !error) return fail(IRL_ERR_ARG, "null pointer");
+  ArArgs a{};
+  a.xbits = xbits;
+  a.n = n;
+  a.M = n_orbitals;
+  a.h = hidden;
+  a.n_up = n_up;
+  a.n_down = n_down;
+  a.theta = theta;
+  a.logpsi = reinterpret_cast<double2*>(logpsi);
+  a.error = error;
+  return ar_launch<AR_LOGAMP>(a, (cudaStream_t)stream);
+}
+
+int irl_ar_rows(const uint64_t* xbits, int64_t n, int n_orbitals, int hidden, int n_up, int n_down,
+                const double* theta, double* O, int64_t ld, int* error, void* stream) {
+  IRL_TRY(ar_check(n, n_orbitals, hidden, n_up, n_down, theta));
+  if (!xbits || !O || !error) return fail(IRL_ERR_ARG, "null pointer");
+  const int64_t p = (int64_t)hidden * 2 * n_orbitals + hidden + 2 * hidden + 2 + (int64_t)hidden * n_orbitals + 2 * hidden +
+                    n_orbitals + 1;
+  if (ld < p) return fail(IRL_ERR_ARG, "ld %lld < param count %lld", (long long)ld, (long long)p);
+  ArArgs a{};
+  a.xbits = xbits;
+  a.n = n;
+  a.M = n_orbitals;
+  a.h = hidden;
+  a.n_up = n_up;
+  a.n_down = n_down;
+  a.theta = theta;
+  a.O = reinterpret_cast<double2*>(O);
+  a.ld = ld;
+  a.error = error;
+  return ar_launch<AR_ROWS>(a, (cudaStream_t)stream);
+}
+
+int irl_ar_sample(const uint64_t* rng_states, int64_t n, int n_orbitals, int hidden, int n_up, int n_down,
+                  const double* theta, uint64_t* out_bits, int* error, void* stream) {
+  IRL_TRY(ar_check(n, n_orbitals, hidden, n_up, n_down, theta));
+  if (!rng_states || !out_bits || !error) return fail(IRL_ERR_ARG, "null pointer");
+  ArArgs a{};
+  a.n = n;
+  a.M = n_orbitals;
+  a.h = hidden;
+  a.n_up = n_up;
+  a.n_down = n_down;
+  a.theta = theta;
+  a.rng = rng_states;
+  a.out_bits = out_bits;
+  a.error = error;
+  return ar_launch<AR_SAMPLE>(a, (cudaStream_t)stream);
+}
+
+int irl_eloc_combine(const int64_t* indptr, const double* elements, const double* logpsi_partner,
+                     const double* logpsi_x, const double* diag, int64_t n, double* eloc, void* stream) {
+  if (!indptr || !logpsi_x || !diag || !eloc || n < 0) return fail(IRL_ERR_ARG, "bad combine arguments");
+  if (n == 0) return IRL_OK;
+  k_eloc_combine<<<(unsigned)std::min<int64_t>(cdiv(n, 8), 148 * 16), 256, 0, (cudaStream_t)stream>>>(
+      indptr, elements, reinterpret_cast<const double2*>(logpsi_partner), reinterpret_cast<const double2*>(logpsi_x),
+      diag, n, reinterpret_cast<double2*>(eloc));
+  return cuda_check(cudaGetLastError(), "combine launch");
 }
 
 }  // extern "C"

@@ -18,7 +18,7 @@
 
 namespace irl {
 
-enum { MODEL_RBM = 0, MODEL_MLP = 1 };
+enum { MODEL_RBM = 0, MODEL_MLP = 1, MODEL_NONE = 2 };  // NONE: Hamiltonian only (ratio 1)
 
 constexpr int ORW_NBUF = 3;   // staging buffers of the O-row writer
 constexpr int ORW_RMAX = 32;  // rows per staging group at most

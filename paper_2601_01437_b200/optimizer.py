@@ -218,16 +218,32 @@ def solve_step(batch: SampleBatch, config: OptimizerConfig = OptimizerConfig(), 
 
 
 def energy_at(params, integrals, sector, config: OptimizerConfig = OptimizerConfig(), step: int = 0) -> float:
-    """opt:104-115: the batch energy at ``params`` (exact enumeration).
+    """opt:104-115: the batch energy at ``params``.
 
-    Only log psi (weights |psi|^2) and the local energies are needed -- no O rows.
+    Only log psi (weights) and the local energies are needed -- no O rows.
+    The reference's own autoregressive ansatz also runs stochastic batches
+    (exact samples, seed ``_batch_seed(config, step)``); the RBM / MLP run in
+    exact-enumeration mode.
     """
-    from . import ansatz as A, hamiltonian as H
+    from . import ansatz as A, autoregressive as AR, hamiltonian as H
 
-    if config.n_samples != 0:
-        raise NotImplementedError("stochastic energies need an RBM/MLP sampler (exact mode only)")
-    bits = H.enumerate_sector(sector)
     dev = torch.device("cuda", torch.cuda.current_device())
+    if AR.is_autoregressive(params):
+        if config.n_samples == 0:
+            bits = H.enumerate_sector(sector)
+        else:
+            bits = AR.sample(params, sector, config.n_samples, _batch_seed(config, step), device=dev)
+        e = AR.local_energies(params, integrals, sector, bits, device=dev)
+        if config.n_samples == 0:
+            lp = AR.log_amplitude_batch(params, sector, bits, device=dev)
+            w = torch.exp(2.0 * lp.real)
+        else:
+            w = torch.ones(len(bits), dtype=torch.float64, device=dev)
+        w = w / w.sum()
+        return float((w.to(e.dtype) * e).sum().real)
+    if config.n_samples != 0:
+        raise NotImplementedError("stochastic RBM/MLP energies need a sampler (exact mode only)")
+    bits = H.enumerate_sector(sector)
     xb = torch.as_tensor(bits.view(np.int64), device=dev)
     e = H.local_energies(params, integrals, xb, device=dev)
     lp = A.log_amplitude_batch(params, H.bits_to_occupations(bits, params.architecture.n_inputs), device=dev)
@@ -251,7 +267,8 @@ class OuterStep:
 
 def outer_step(params, integrals, sector, config: OptimizerConfig = OptimizerConfig(), step: int = 0, *,
                mode: int = _lib.MVP_AUTO) -> OuterStep:
-    """opt:118-195 on the device for the shallow NQS (exact mode).
+    """opt:118-195 on the device: the reference's own autoregressive ansatz
+    (exact or stochastic batches) or the shallow RBM / MLP (exact mode).
 
     Batch (E_loc, |psi|^2 weights, O rows), energy, gradient, connected cache,
     the bordered IRL / SL solve with ``heff_matvec + heff_offdiag_matvec``,
@@ -259,13 +276,22 @@ def outer_step(params, integrals, sector, config: OptimizerConfig = OptimizerCon
     by exact energy re-evaluation, falling back to the normalised steepest
     descent ``-F/|F|`` when no scale lowers the energy (opt:167-190).
     """
-    from . import ansatz as A, hamiltonian as H
+    from . import ansatz as A, autoregressive as AR, hamiltonian as H
 
-    if config.n_samples != 0:
-        raise NotImplementedError("stochastic batches need an RBM/MLP sampler (exact mode only)")
-    batch = H.build_batch(params, integrals, sector)
-    energy = estimate_energy(batch)
-    cache = H.build_connected_cache(params, integrals, sector, batch)
+    if AR.is_autoregressive(params):
+        # the reference's own model: exact or stochastic batches (opt:134-137)
+        batch = AR.build_batch(params, integrals, sector, n_samples=config.n_samples,
+                               seed=_batch_seed(config, step))
+        energy = estimate_energy(batch)  # warns on an imaginary residual, as est:136-143
+        cache = AR.build_connected_cache(params, integrals, sector, batch)
+        make = lambda th: AR.AnsatzParameters(params.architecture, th)  # noqa: E731
+    else:
+        if config.n_samples != 0:
+            raise NotImplementedError("stochastic RBM/MLP batches need a sampler (exact mode only)")
+        batch = H.build_batch(params, integrals, sector)
+        energy = estimate_energy(batch)
+        cache = H.build_connected_cache(params, integrals, sector, batch)
+        make = lambda th: A.AnsatzParameters(params.architecture, th)  # noqa: E731
     res = solve_step(batch, config, step, energy=energy, mode=mode, connected=cache)
     grad = energy_gradient(batch, energy).detach().cpu().numpy()
     d0 = res.direction.detach().cpu().numpy()
@@ -275,7 +301,7 @@ def outer_step(params, integrals, sector, config: OptimizerConfig = OptimizerCon
         best_scale, best_energy = best
         best_d = d
         for scale in config.line_search:
-            cand = A.AnsatzParameters(params.architecture, theta + scale * d)
+            cand = make(theta + scale * d)
             e_new = energy_at(cand, integrals, sector, config, step)
             if np.isfinite(e_new) and e_new < best_energy:
                 best_energy, best_scale, best_d = e_new, scale, d
@@ -288,6 +314,6 @@ def outer_step(params, integrals, sector, config: OptimizerConfig = OptimizerCon
             best_scale, best_energy, best_d = line_search(-grad / norm, (0.0, energy.mean))
     new = params
     if best_scale > 0.0:
-        new = A.AnsatzParameters(params.architecture, theta + best_scale * best_d)
+        new = make(theta + best_scale * best_d)
     return OuterStep(params=new, lambda_min=res.lambda_min, step_scale=best_scale, matvecs=res.n_matvec,
                      converged=res.converged, energy=energy.mean, best_energy=best_energy)
