@@ -276,6 +276,10 @@ int irl_ham_partners_fill(const uint64_t* xbits, int64_t n, int n_spatial, doubl
                           double* elements, void* stream);
 int irl_eloc_combine(const int64_t* indptr, const double* elements, const double* logpsi_partner,
                      const double* logpsi_x, const double* diag, int64_t n, double* eloc, void* stream);
+/* Binary search of queries in ascending keys: out = index or -1 (partner rows
+ * that are batch rows reuse the batch's O, est:236-242's o_row table). */
+int irl_sorted_lookup(const uint64_t* keys, int64_t n_keys, const uint64_t* queries, int64_t n_queries, int64_t* out,
+                      void* stream);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

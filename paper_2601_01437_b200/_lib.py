@@ -91,6 +91,7 @@ SIGNATURES = {
     "irl_ham_diagonal_and_count": (_I, [_P, _I64, _I, _D, _P, _P, _D, _P, _P, _P]),
     "irl_ham_partners_fill": (_I, [_P, _I64, _I, _D, _P, _P, _D, _P, _P, _P, _P]),
     "irl_eloc_combine": (_I, [_P, _P, _P, _P, _P, _I64, _P, _P]),
+    "irl_sorted_lookup": (_I, [_P, _I64, _P, _I64, _P, _P]),
 }
 
 

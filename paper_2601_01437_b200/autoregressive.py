@@ -31,7 +31,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .estimators import KIND_COMPLEX_RAW, ConnectedCache, SampleBatch, _device
+from .estimators import KIND_COMPLEX_RAW, ConnectedCache, SampleBatch, _device, partner_rows_in_batch
 
 
 @dataclass(frozen=True)
@@ -208,6 +208,28 @@ def hamiltonian_partners(integrals, xbits, *, drop_tolerance: float = 1e-14, dev
     return diag, indptr, pbits[:nnz], elem[:nnz]
 
 
+def _partner_logamp(params, sector, xb: torch.Tensor, lp_x: torch.Tensor, pbits: torch.Tensor) -> torch.Tensor:
+    """ln psi of the partners: looked up among the configurations already
+    evaluated (every partner in exact mode: the batch is the whole sector),
+    the network run only on the rest."""
+    dev = xb.device
+    if pbits.numel() == 0:
+        return lp_x[:0]
+    xh = xb.cpu().numpy().view(np.uint64)
+    uniq, first = np.unique(xh, return_index=True)
+    keys = torch.as_tensor(uniq.view(np.int64), device=dev)
+    idx = torch.empty(pbits.numel(), dtype=torch.int64, device=dev)
+    _lib.call("irl_sorted_lookup", _lib.ptr(keys), keys.numel(), _lib.ptr(pbits), pbits.numel(), _lib.ptr(idx),
+              _lib.stream_handle(dev))
+    lp_keys = lp_x[torch.as_tensor(first, device=dev)]
+    found = idx >= 0
+    lp_y = lp_keys[idx.clamp_min(0)]
+    if not bool(found.all()):
+        miss = ~found
+        lp_y[miss] = log_amplitude_batch(params, sector, pbits[miss], device=dev)
+    return lp_y
+
+
 def local_energies(params, integrals, sector, xbits, device=None) -> torch.Tensor:
     """E_loc (ham:290-302) for this ansatz: diag + sum element psi(y)/psi(x), complex (N,)."""
     dev = _device(device)
@@ -216,7 +238,7 @@ def local_energies(params, integrals, sector, xbits, device=None) -> torch.Tenso
     lp_x = log_amplitude_batch(params, sector, xb, device=dev)
     if not bool(torch.isfinite(lp_x.real).all()):
         raise ValueError("log-amplitude is not finite at the reference configuration")  # ham:295-296
-    lp_y = log_amplitude_batch(params, sector, pbits, device=dev) if pbits.numel() else lp_x[:0]
+    lp_y = _partner_logamp(params, sector, xb, lp_x, pbits)
     out = torch.empty(int(xb.shape[0]), dtype=torch.complex128, device=dev)
     _lib.call("irl_eloc_combine", _lib.ptr(indptr), _lib.ptr(elem), _lib.ptr(lp_y) if pbits.numel() else None,
               _lib.ptr(lp_x), _lib.ptr(diag), int(xb.shape[0]), _lib.ptr(out), _lib.stream_handle(dev))
@@ -261,20 +283,26 @@ def build_connected_cache(params, integrals, sector, batch: SampleBatch) -> Conn
     dev = batch.device
     uniq, dist_index = np.unique(np.asarray(bits, dtype=np.uint64), return_inverse=True)
     _, indptr, pbits, elem = hamiltonian_partners(integrals, uniq, device=dev)
-    lp_x = log_amplitude_batch(params, sector, uniq, device=dev)
-    ip = indptr.cpu().numpy()
+    ub = _bits(uniq, dev)
+    lp_x = log_amplitude_batch(params, sector, ub, device=dev)
+    nnz = pbits.numel()
+    lp_y = _partner_logamp(params, sector, ub, lp_x, pbits)
+    seg = torch.repeat_interleave(torch.arange(len(uniq), device=dev), indptr[1:] - indptr[:-1])
+    coeff = elem.to(torch.complex128) * torch.exp(lp_y - lp_x[seg])
+    keep = torch.isfinite(lp_y.real)  # est:246-247 skips zero-amplitude partners
+    if nnz and not bool(keep.all()):
+        counts = torch.bincount(seg[keep], minlength=len(uniq))
+        indptr = torch.zeros(len(uniq) + 1, dtype=torch.int64, device=dev)
+        torch.cumsum(counts, 0, out=indptr[1:])
+        pbits, coeff = pbits[keep], coeff[keep]
+    reps = np.full(len(uniq), -1, dtype=np.int64)
+    order = np.arange(len(bits))[::-1]
+    reps[dist_index.reshape(-1)[order]] = order
+    rows = partner_rows_in_batch(uniq, reps, pbits) if pbits.numel() else None
+    if rows is not None:
+        return ConnectedCache(dist_index.reshape(-1), indptr, rows, coeff, batch.o_matrix, batch=batch)
     pb = pbits.cpu().numpy().view(np.uint64)
-    lp_y = log_amplitude_batch(params, sector, pb, device=dev) if len(pb) else lp_x[:0]
-    seg = torch.as_tensor(np.repeat(np.arange(len(uniq)), np.diff(ip)), device=dev)
-    keep = torch.isfinite(lp_y.real) if len(pb) else torch.zeros(0, dtype=torch.bool, device=dev)  # est:246-247
-    coeff = elem.to(torch.complex128) * torch.exp(lp_y - lp_x[seg]) if len(pb) else lp_y
-    if len(pb) and not bool(keep.all()):
-        k = keep.cpu().numpy()
-        counts = np.bincount(np.repeat(np.arange(len(uniq)), np.diff(ip))[k], minlength=len(uniq))
-        ip = np.concatenate([[0], np.cumsum(counts)])
-        pb = pb[k]
-        coeff = coeff[keep]
     pu, pinv = np.unique(pb, return_inverse=True) if len(pb) else (pb, np.zeros(0, dtype=np.int64))
     po = log_derivative_batch(params, sector, pu, ld=batch.ld, device=dev) if len(pu) else \
         torch.zeros((0, batch.ld), dtype=torch.complex128, device=dev)
-    return ConnectedCache(dist_index.reshape(-1), ip, pinv.reshape(-1), coeff, po, batch=batch)
+    return ConnectedCache(dist_index.reshape(-1), indptr, pinv.reshape(-1), coeff, po, batch=batch)

@@ -166,4 +166,21 @@ __global__ void __launch_bounds__(256) k_logamp_finish(const uint8_t* __restrict
   out[r] = T::add(lin, h);
 }
 
+// Row lookup of partner configurations among the batch's sorted distinct
+// configurations (binary search): out[q] = index of queries[q] in keys, or -1.
+// In exact mode every partner lies in the batch, so the partner rows are the
+// batch's own O rows and no partner O is built or stored.
+__global__ void k_sorted_lookup(const uint64_t* __restrict__ keys, int64_t nk, const uint64_t* __restrict__ q,
+                                int64_t nq, int64_t* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nq; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t v = q[i];
+    int64_t lo = 0, hi = nk;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (keys[mid] < v) lo = mid + 1; else hi = mid;
+    }
+    out[i] = (lo < nk && keys[lo] == v) ? lo : -1;
+  }
+}
+
 }  // namespace irl

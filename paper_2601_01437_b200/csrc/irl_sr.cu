@@ -2199,4 +2199,14 @@ int irl_eloc_combine(const int64_t* indptr, const double* elements, const double
   return cuda_check(cudaGetLastError(), "combine launch");
 }
 
+int irl_sorted_lookup(const uint64_t* keys, int64_t n_keys, const uint64_t* queries, int64_t n_queries, int64_t* out,
+                      void* stream) {
+  if ((!keys && n_keys) || (!queries && n_queries) || (!out && n_queries) || n_keys < 0 || n_queries < 0)
+    return fail(IRL_ERR_ARG, "bad lookup arguments");
+  if (n_queries == 0) return IRL_OK;
+  const unsigned blocks = (unsigned)std::min<int64_t>(cdiv(n_queries, 256), 148 * 32);
+  k_sorted_lookup<<<blocks, 256, 0, (cudaStream_t)stream>>>(keys, n_keys, queries, n_queries, out);
+  return cuda_check(cudaGetLastError(), "lookup launch");
+}
+
 }  // extern "C"

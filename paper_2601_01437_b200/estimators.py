@@ -484,24 +484,28 @@ class ConnectedCache:
         dev = batch.device
         kind_c = batch.is_complex
         cdt = torch.complex128 if kind_c else torch.float64
-        di = np.asarray(dist_index.cpu() if isinstance(dist_index, torch.Tensor) else dist_index, dtype=np.int64)
-        ip = np.asarray(indptr.cpu() if isinstance(indptr, torch.Tensor) else indptr, dtype=np.int64)
-        pr = np.asarray(partner_row.cpu() if isinstance(partner_row, torch.Tensor) else partner_row, dtype=np.int64)
+
+        def idx(a):  # int64 device tensor; validation runs where the data lives
+            if isinstance(a, torch.Tensor):
+                return a.to(device=dev, dtype=torch.int64).contiguous()
+            return torch.as_tensor(np.asarray(a, dtype=np.int64), device=dev)
+
+        di, ip, pr = idx(dist_index), idx(indptr), idx(partner_row)
         n = batch.n_rows
-        if di.shape != (n,):
+        if tuple(di.shape) != (n,):
             raise ValueError("dist_index must have one entry per batch row")
-        if ip.ndim != 1 or len(ip) < 1 or ip[0] != 0 or np.any(np.diff(ip) < 0):
+        if ip.dim() != 1 or ip.numel() < 1 or int(ip[0]) != 0 or (ip.numel() > 1 and bool((ip[1:] < ip[:-1]).any())):
             raise ValueError("indptr must start at 0 and be non-decreasing")
-        n_dist = len(ip) - 1
-        if n and (di.min() < 0 or di.max() >= n_dist):
+        n_dist = ip.numel() - 1
+        if n and (int(di.min()) < 0 or int(di.max()) >= n_dist):
             raise IndexError("dist_index out of range")
         nnz = int(ip[-1])
-        if pr.shape != (nnz,):
+        if tuple(pr.shape) != (nnz,):
             raise ValueError("partner_row length must equal indptr[-1]")
         ld, p = batch.ld, batch.param_count
         if isinstance(partner_o, torch.Tensor) and partner_o.is_cuda and partner_o.ndim == 2 \
                 and partner_o.shape[1] == ld and partner_o.dtype == cdt:
-            po = partner_o.contiguous()
+            po = partner_o.contiguous()  # e.g. the batch's own O (partners that are batch rows)
         else:
             src = partner_o
             if not isinstance(src, torch.Tensor):
@@ -518,17 +522,20 @@ class ConnectedCache:
             if m:
                 po[:, :p] = _as_tensor(src, cdt, dev)
         m = int(po.shape[0])
-        if nnz and (pr.min() < 0 or pr.max() >= m):
+        if nnz and (int(pr.min()) < 0 or int(pr.max()) >= m):
             raise IndexError("partner_row out of range")
-        c = coeff.detach().cpu().numpy() if isinstance(coeff, torch.Tensor) else np.asarray(coeff)
-        if c.shape != (nnz,):
+        if isinstance(coeff, torch.Tensor):
+            c = coeff.detach().to(dev)
+        else:
+            c = torch.as_tensor(np.asarray(coeff), device=dev)
+        if tuple(c.shape) != (nnz,):
             raise ValueError("coeff length must equal indptr[-1]")
-        if not kind_c:
-            c = np.real(c)
-        self.dist_index = torch.as_tensor(di, device=dev)
-        self.indptr = torch.as_tensor(ip, device=dev)
-        self.partner_row = torch.as_tensor(pr, device=dev)
-        self.coeff = torch.as_tensor(np.ascontiguousarray(c), dtype=cdt, device=dev)
+        if not kind_c and torch.is_complex(c):
+            c = c.real
+        self.dist_index = di
+        self.indptr = ip
+        self.partner_row = pr
+        self.coeff = c.to(cdt).contiguous()
         self.partner_o = po
         self.n_partner = m
         self.n_dist = n_dist
@@ -550,6 +557,27 @@ class ConnectedCache:
                                                                    int(batch.is_complex)))
             self._ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=batch.device)
         return self._ws
+
+
+def partner_rows_in_batch(uniq_bits: np.ndarray, reps: np.ndarray, partner_bits: torch.Tensor):
+    """Batch O rows of partner configurations, when every partner is a batch row.
+
+    ``uniq_bits``: the batch's distinct configurations (ascending uint64),
+    ``reps``: a batch row of each; ``partner_bits``: device int64 view of the
+    partners' uint64 bitmasks.  Returns the batch row of every partner (device
+    int64), or None when some partner is not in the batch.  In exact mode the
+    batch is the whole sector, which every connected partner lies in, so the
+    cache points into the batch's own O (the reference's o_row table,
+    est:236-242, without a second copy of the rows).
+    """
+    dev = partner_bits.device
+    keys = torch.as_tensor(np.ascontiguousarray(uniq_bits, dtype=np.uint64).view(np.int64), device=dev)
+    out = torch.empty(partner_bits.numel(), dtype=torch.int64, device=dev)
+    _lib.call("irl_sorted_lookup", _lib.ptr(keys), keys.numel(), _lib.ptr(partner_bits), partner_bits.numel(),
+              _lib.ptr(out), _lib.stream_handle(dev))
+    if out.numel() and bool((out < 0).any()):
+        return None
+    return torch.as_tensor(np.asarray(reps, dtype=np.int64), device=dev)[out]
 
 
 def heff_offdiag_matvec(batch: SampleBatch, cache: ConnectedCache, v, *, mode: int = _lib.MVP_AUTO):

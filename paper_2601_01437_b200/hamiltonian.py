@@ -38,14 +38,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from .ansatz import (
-    AnsatzParameters,
-    _theta_device,
-    build_connected_cache as _cache_from_partners,
-    fill_o_rows,
-    log_amplitude_batch,
-)
-from .estimators import KIND_HERMITIAN, KIND_REAL, ConnectedCache, SampleBatch, _device
+from .ansatz import AnsatzParameters, _theta_device, fill_o_rows, log_amplitude_batch
+from .estimators import KIND_HERMITIAN, KIND_REAL, ConnectedCache, SampleBatch, _device, partner_rows_in_batch
 
 DROP_TOLERANCE = 1e-14  # ham:24
 MAX_ORBITALS = 64  # hilbert.py:14
@@ -311,23 +305,36 @@ def build_batch(params: AnsatzParameters, integrals: MolecularIntegrals, sector:
 def build_connected_cache(params: AnsatzParameters, integrals: MolecularIntegrals, sector: Sector,
                           batch: SampleBatch) -> ConnectedCache:
     """``est.build_connected_cache`` (est:221-251): distinct configurations of
-    the batch, their kept partners and coefficients (device enumeration), and
-    the partner O rows (row kernel, deduplicated as the reference's o_row table)."""
+    the batch, their kept partners and coefficients element * psi(y)/psi(x)
+    (device enumeration), and the partner O rows: the batch's own rows when
+    every partner is a batch configuration (exact mode), else the row kernel on
+    the distinct partners (the reference's o_row table, est:236-242)."""
     bits = getattr(batch, "xbits", None)
     if bits is None:
         raise ValueError("batch has no sample bitmasks (build it with hamiltonian.build_batch)")
     dev = batch.device
-    uniq, dist_index = np.unique(np.asarray(bits, dtype=np.uint64), return_inverse=True)
+    bits = np.asarray(bits, dtype=np.uint64)
+    uniq, dist_index = np.unique(bits, return_inverse=True)
+    dist_index = dist_index.reshape(-1)
     indptr, pbits, elem, coeff = connected_partners(params, integrals, uniq, device=dev)
-    arch = params.architecture
-    partners = bits_to_occupations(pbits.cpu().numpy().view(np.uint64), arch.n_inputs)
-    # partner rows and coefficients: the coefficient is already element * psi(y)/psi(x)
-    ip = indptr.cpu().numpy()
-    x_rows = bits_to_occupations(np.asarray(bits, dtype=np.uint64), arch.n_inputs)
-    cache = _cache_from_partners(params, batch, x_rows, partners, np.ones(len(partners)), ip,
-                                 dist_index=dist_index.reshape(-1), device=dev)
-    # replace the ratio-only coefficients by the kernel's element * ratio (same values)
-    c = coeff if batch.is_complex else coeff.real if torch.is_complex(coeff) else coeff
-    cache.coeff = c.to(cache.coeff.dtype).contiguous()
+    reps = np.full(len(uniq), -1, dtype=np.int64)
+    order = np.arange(len(bits))[::-1]
+    reps[dist_index[order]] = order
+    rows = partner_rows_in_batch(uniq, reps, pbits) if pbits.numel() else None
+    if rows is not None:
+        cache = ConnectedCache(dist_index, indptr, rows, coeff, batch.o_matrix, batch=batch)
+    else:
+        arch = params.architecture
+        pb = pbits.cpu().numpy().view(np.uint64)
+        pu, pinv = np.unique(pb, return_inverse=True)
+        cdt = torch.complex128 if arch.complex_params else torch.float64
+        po = torch.zeros((len(pu), batch.ld), dtype=cdt, device=dev)
+        if len(pu):
+            xt = torch.as_tensor(bits_to_occupations(pu, arch.n_inputs), device=dev)
+            m = len(pu)
+            w = torch.full((m,), 1.0 / m, dtype=torch.float64, device=dev)
+            scratch = [torch.empty(batch.ld, dtype=cdt, device=dev) for _ in range(2)]
+            fill_o_rows(params, xt, po, w, torch.zeros(m, dtype=cdt, device=dev), scratch[0], scratch[1])
+        cache = ConnectedCache(dist_index, indptr, pinv.reshape(-1), coeff, po, batch=batch)
     cache.elements = elem
     return cache
