@@ -1348,6 +1348,70 @@ size_t connected_ws_bytes(int64_t n, int64_t m, int64_t ld, bool cplx) {
   return conn_ws_layout(n, m, ld, cplx, ok ? &pp : nullptr).bytes;
 }
 
+// Partners that are the batch's own rows (partner_O == O, exact mode): the
+// product's first pass already gives q at every row, so the completion costs no
+// extra read of O -- DOT pass over O, the per-row CSR kernel on those partial
+// dots, then the ACC pass with coefficient a and additive term d (two passes
+// instead of a partner pass plus the fused pass).
+int connected_self_impl(bool cplx, const double* O, int64_t n, int64_t ld, const double* obar, const double* w,
+                        const double* coeff, const int64_t* dist_index, const int64_t* indptr, const int64_t* prow,
+                        const double* pcoeff, const double* v_re, const double* v_im, double* out_re, double* out_im,
+                        const double* hf_re, const double* hf_im, const double* u0, double* out0, void* ws,
+                        size_t ws_bytes, cudaStream_t st) {
+  const int64_t ld_u = cplx ? ld : ld / 2;
+  Plan p1, p2;
+  IRL_TRY(make_plan(n, ld_u, cplx, MODE_DOT, p1));
+  IRL_TRY(make_plan(n, ld_u, cplx, MODE_ACC, p2));
+  if (p1.C != p2.C) return fail(IRL_ERR_DEVICE, "two-pass plans disagree on column split");
+  const ConnWs wl = conn_ws_layout(n, 0, ld, cplx, nullptr);
+  if (ws_bytes < wl.bytes) return fail(IRL_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, wl.bytes);
+  char* base = static_cast<char*>(ws);
+  Plan pw = p1;
+  pw.nb = std::max(p1.nb, p2.nb);
+  MvpWs mw = mvp_ws_layout(pw, n, ld_u, cplx, base + wl.mvp);
+  if ((size_t)(wl.a - wl.mvp) < mw.bytes) return fail(IRL_ERR_WORKSPACE, "connected workspace layout");
+  StreamArgs a{};
+  a.O = reinterpret_cast<const double2*>(O);
+  a.n_rows = n;
+  a.ld_u = ld_u;
+  a.v_re = v_re;
+  a.v_im = v_im;
+  a.hf_re = hf_re;
+  a.hf_im = hf_im;
+  a.obar = reinterpret_cast<const double2*>(obar);
+  a.part0 = mw.part;
+  a.ysum = mw.ysum;
+  a.tpart = mw.tpart;
+  a.spart = mw.spart;
+  a.gpart = mw.gpart;
+  IRL_TRY(launch_stream(p1, a, st));
+  DevInfo d;
+  IRL_TRY(dev_info(d));
+  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 8), (int64_t)d.sms * 8));
+  void* av = base + wl.a;
+  void* dv = base + wl.d;
+  if (cplx)
+    k_connected_rows<true><<<blocks, 256, 0, st>>>(dist_index, indptr, prow, reinterpret_cast<const double2*>(pcoeff),
+                                                   reinterpret_cast<const double2*>(mw.tpart), p1.C, n,
+                                                   reinterpret_cast<const double2*>(mw.spart), w,
+                                                   reinterpret_cast<const double2*>(coeff), n,
+                                                   reinterpret_cast<double2*>(av), reinterpret_cast<double2*>(dv));
+  else
+    k_connected_rows<false><<<blocks, 256, 0, st>>>(dist_index, indptr, prow, pcoeff,
+                                                    reinterpret_cast<const double*>(mw.tpart), p1.C, n,
+                                                    reinterpret_cast<const double*>(mw.spart), w, coeff, n,
+                                                    reinterpret_cast<double*>(av), reinterpret_cast<double*>(dv));
+  IRL_TRY(cuda_check(cudaGetLastError(), "connected rows launch"));
+  a.coeff0 = av;
+  a.yadd = dv;
+  IRL_TRY(launch_stream(p2, a, st));
+  if (cplx)
+    return launch_finish_mvp<true>(mw.part, p2.nb, ld_u, mw.ysum, a.obar, hf_re, hf_im, u0, out_re, out_im, mw.gpart,
+                                   p1.C, out0, st);
+  return launch_finish_mvp<false>(mw.part, p2.nb, ld_u, mw.ysum, a.obar, hf_re, hf_im, u0, out_re, out_im, mw.gpart,
+                                  p1.C, out0, st);
+}
+
 int connected_impl(bool cplx, const double* O, int64_t n, int64_t p, int64_t ld, const double* obar, const double* w,
                    const double* coeff, const int64_t* dist_index, const int64_t* indptr, const int64_t* prow,
                    const double* pcoeff, const double* Op, int64_t m, const double* v_re, const double* v_im,
@@ -1361,6 +1425,9 @@ int connected_impl(bool cplx, const double* O, int64_t n, int64_t p, int64_t ld,
   if (!aligned16(O) || !aligned16(Op) || !aligned16(obar) || !aligned16(ws))
     return fail(IRL_ERR_ALIGN, "pointers must be 16-byte aligned");
   const int64_t ld_u = cplx ? ld : ld / 2;
+  if (Op == O && m == n) return connected_self_impl(cplx, O, n, ld, obar, w, coeff, dist_index, indptr, prow, pcoeff,
+                                                    v_re, v_im, out_re, out_im, hf_re, hf_im, u0, out0, ws,
+                                                    ws_bytes, st);
   Plan pp{};
   if (m > 0) IRL_TRY(make_plan(m, ld_u, cplx, MODE_DOT, pp));
   const ConnWs wl = conn_ws_layout(n, m, ld, cplx, m > 0 ? &pp : nullptr);
