@@ -31,6 +31,7 @@ raises :class:`~paper_2601_01437_b200._lib.NativeUnavailable`.
 
 from __future__ import annotations
 
+import os
 import warnings
 from dataclasses import dataclass
 
@@ -407,6 +408,53 @@ def _staging(batch: SampleBatch, shape) -> torch.Tensor:
     return buf
 
 
+_E2E_GRAPHS = os.environ.get("IRL_E2E_GRAPH", "1") != "0"
+
+
+def _host_product_graph(batch: SampleBatch, coeff, v: torch.Tensor, mode: int, cache) -> torch.Tensor:
+    """Host vector in -> host vector out as ONE CUDA graph replay: the H2D copy
+    from a pinned staging vector, the product's launches and the D2H copy are
+    captured once per (batch, coefficient, mode, cache, stream); a call copies
+    v into the staging vector, replays, synchronises and returns a fresh copy."""
+    import gc
+
+    dev = batch.device
+    p, ld = batch.param_count, batch.ld
+    key = (_lib.stream_handle(dev), id(coeff), int(mode), id(cache) if cache is not None else None)
+    graphs = batch.__dict__.setdefault("_e2e_graphs", {})
+    hit = graphs.get(key)
+    if hit is None:
+        vin = torch.zeros(ld, dtype=torch.float64, device=dev)
+        vout = torch.empty(ld, dtype=torch.float64, device=dev)
+        hin = torch.zeros(p, dtype=torch.float64, pin_memory=True)
+        hout = torch.empty(p, dtype=torch.float64, pin_memory=True)
+
+        def body():
+            vin[:p].copy_(hin, non_blocking=True)
+            _apply(batch, coeff, vin, vout, mode=mode, cache=cache)
+            hout.copy_(vout[:p], non_blocking=True)
+
+        body()  # eager once: plans, workspaces
+        torch.cuda.synchronize(dev)
+        g = torch.cuda.CUDAGraph()
+        gc.collect()
+        was = gc.isenabled()
+        gc.disable()
+        try:
+            with torch.cuda.graph(g, capture_error_mode="thread_local"):
+                body()
+        finally:
+            if was:
+                gc.enable()
+        hit = (g, hin, hout, coeff, cache)  # keep coeff / cache alive with the graph
+        graphs[key] = hit
+    g, hin, hout = hit[0], hit[1], hit[2]
+    hin.copy_(v if v.dtype == torch.float64 else v.to(torch.float64))
+    g.replay()
+    torch.cuda.current_stream(dev).synchronize()
+    return hout.clone()
+
+
 def _product(batch: SampleBatch, coeff: torch.Tensor | None, v, mode: int, cache: "ConnectedCache | None" = None):
     p = batch.param_count
     as_numpy = not isinstance(v, torch.Tensor)
@@ -436,6 +484,8 @@ def _product(batch: SampleBatch, coeff: torch.Tensor | None, v, mode: int, cache
     else:
         if (not as_numpy) and torch.is_complex(v):
             raise ValueError("complex vector needs a hermitian batch")
+        if on_host and _E2E_GRAPHS:
+            return _host_product_graph(batch, coeff, v, mode, cache)
         vin = _staging(batch, (ld,))
         if on_host:
             vin[:p].copy_(v if v.dtype == torch.float64 else v.to(torch.float64), non_blocking=True)
@@ -460,9 +510,20 @@ def heff_matvec(batch: SampleBatch, energy: EnergyEstimate, v, *, mode: int = _l
     return _product(batch, batch.coefficients(energy.mean), v, mode)
 
 
+def _qgt_coeff(batch: SampleBatch) -> torch.Tensor:
+    """Coefficient w of S v (cached: the complex kinds need it as c128)."""
+    if not batch.is_complex:
+        return batch.weights
+    c = batch.__dict__.get("_wc")
+    if c is None:
+        c = batch.weights.to(torch.complex128)
+        batch._wc = c
+    return c
+
+
 def qgt_matvec(batch: SampleBatch, v, *, mode: int = _lib.MVP_AUTO):
     """S v = O_c^H (w (O_c v)) — matrix-free ``dense_qgt`` (est:335-344)."""
-    return _product(batch, batch.weights if not batch.is_complex else batch.weights.to(torch.complex128), v, mode)
+    return _product(batch, _qgt_coeff(batch), v, mode)
 
 
 class ConnectedCache:
