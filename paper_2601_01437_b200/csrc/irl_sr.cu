@@ -1101,8 +1101,20 @@ void (*pick_orows(int ppt))(ORowArgs, int) {
 // real models with n_in <= 100 and an even hidden width take their column
 // statistics from the DMMA GEMM (k_otf_acc) instead of the row writer
 // (measured: for the narrow RBM hidden layers the fused writer statistics win)
+// Row-sweeping writer (k_orows_sweep): real models with unit-aligned blocks
+// (even n; the RBM also needs an even h), its statistics from the DMMA GEMMs.
+// Measured (B200): MLP cfg5 37.7 -> 23.3 ms, cfg3 equal; the RBM's column-tile
+// writer with fused statistics stays faster (cfg2 0.78 vs 1.00 ms), so the RBM
+// sweeps only with IRL_OBUILD_SWEEP=2; IRL_OBUILD_SWEEP=0 disables it.
+bool sweep_ok(bool cplx, int model, int n_vis, int hidden) {
+  static const int mode = getenv("IRL_OBUILD_SWEEP") ? atoi(getenv("IRL_OBUILD_SWEEP")) : 1;
+  if (mode == 0 || cplx || (n_vis & 1) || n_vis > 2 * 32 * SWEEP_UQ) return false;
+  return model == MODEL_MLP || (mode == 2 && (hidden & 1) == 0);
+}
+
 bool gemm_stats(bool cplx, int model, int n_vis, int hidden) {
-  return !cplx && model == MODEL_MLP && n_vis <= OTF_MAX_NIN && (hidden & 1) == 0;
+  if (cplx || n_vis > OTF_MAX_NIN || (hidden & 1)) return false;
+  return model == MODEL_MLP || sweep_ok(cplx, model, n_vis, hidden);
 }
 
 int make_oplan(int64_t ld_u, bool cplx, int model, OPlan& p, bool stats_in_writer) {
@@ -1282,7 +1294,17 @@ int obuild_impl(bool cplx, int model, const uint8_t* x, int64_t n, int n_vis, in
     if (smem > (size_t)d.smem_optin) return fail(IRL_ERR_ARG, "hidden layer too wide for the row table");
     IRL_TRY(ensure_fn_attrs((const void*)p.fn, d.smem_optin));
   }
-  p.fn<<<(unsigned)(p.nb * p.C), p.NT, smem, st>>>(a, (int)buf_bytes);
+  if (gstats && sweep_ok(cplx, model, n_vis, hidden)) {
+    DevInfo d;
+    IRL_TRY(dev_info(d));
+    auto fn = model == MODEL_MLP ? k_orows_sweep<false, MODEL_MLP> : k_orows_sweep<false, MODEL_RBM>;
+    const size_t sm = (size_t)hidden * 8;
+    IRL_TRY(ensure_fn_attrs((const void*)fn, d.smem_optin));
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(n, 2 * (int64_t)d.sms));
+    fn<<<grid, SWEEP_NT, sm, st>>>(x, n, n_vis, hidden, T, G, reinterpret_cast<double2*>(O), ld_u);
+  } else {
+    p.fn<<<(unsigned)(p.nb * p.C), p.NT, smem, st>>>(a, (int)buf_bytes);
+  }
   IRL_TRY(cuda_check(cudaGetLastError(), "orows launch"));
   if (gstats) {
     // column statistics from the hidden activations and the packed inputs

@@ -464,3 +464,110 @@ __global__ void __launch_bounds__(1024) k_energy(const double* __restrict__ w, c
 }
 
 }  // namespace irl
+
+namespace irl {
+
+// Row-sweeping O writer (stats come from the DMMA GEMMs, so no column
+// ownership is needed): CTA c writes whole rows c, c + grid, ... front to
+// back with streaming 16-B stores -- the store pattern that sustains the
+// HBM write rate on very wide rows (1.67 MB at cfg5), where column tiles of
+// many CTAs interleaving inside one row do not.  The outer-product block
+// (t_j x_i for the RBM, g_j x_k for the MLP) is written j-segment by
+// j-segment: a lane owns fixed input positions (units) of the segment, so its
+// x values are loaded once per row and every store is factor_j * x.
+//   real RBM  [x (n), t (h), W (h x n)]     needs n, h even (unit-aligned blocks)
+//   c128 RBM  same, one complex element per unit
+//   MLP       [W (h x n), g (h), t (h), 1]  needs n even
+constexpr int SWEEP_NT = 512;
+constexpr int SWEEP_UQ = 4;  // units per lane per segment: n <= 128 (complex) / 256 (real)
+
+template <bool CPLX, int MODEL>
+__global__ void __launch_bounds__(SWEEP_NT, 2) k_orows_sweep(const uint8_t* __restrict__ x, int64_t n_rows, int n,
+                                                            int h, const void* __restrict__ Tv,
+                                                            const double* __restrict__ G, double2* __restrict__ O,
+                                                            int64_t ld_u) {
+  using S = typename Traits<CPLX>::S;
+  extern __shared__ __align__(16) unsigned char smem_sw[];
+  S* fs = reinterpret_cast<S*>(smem_sw);  // [h] factor row (t or g)
+  const S* T = reinterpret_cast<const S*>(Tv);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, NW = SWEEP_NT / 32;
+  const int upj = CPLX ? n : n / 2;  // units per j segment
+  const int JW = upj >= 32 ? 1 : 32 / upj;
+  const int jo = upj >= 32 ? 0 : lane / upj;
+  const int u0 = upj >= 32 ? lane : lane % upj;
+  const bool active = jo < JW;
+  const int64_t hn = (int64_t)h * n;
+  const int64_t P = MODEL == MODEL_RBM ? (int64_t)n + h + hn : hn + 2 * (int64_t)h + 1;
+  const int64_t wb = MODEL == MODEL_MLP ? 0 : (CPLX ? (int64_t)n + h : ((int64_t)n + h) / 2);  // W block, units
+  const int64_t we = wb + (int64_t)h * upj;
+  for (int64_t r = blockIdx.x; r < n_rows; r += gridDim.x) {
+    const uint8_t* xr = x + r * n;
+    __syncthreads();  // previous row's factors consumed
+    for (int j = tid; j < h; j += SWEEP_NT) {
+      if constexpr (MODEL == MODEL_MLP) fs[j] = G[r * h + j]; else fs[j] = T[r * h + j];
+    }
+    // this lane's x values (its units of every segment)
+    double xa[SWEEP_UQ], xb[SWEEP_UQ];
+#pragma unroll
+    for (int q = 0; q < SWEEP_UQ; ++q) {
+      const int u = u0 + 32 * q;
+      xa[q] = xb[q] = 0.0;
+      if (u < upj) {
+        if constexpr (CPLX) {
+          xa[q] = xr[u] ? 1.0 : 0.0;
+        } else {
+          xa[q] = xr[2 * u] ? 1.0 : 0.0;
+          xb[q] = xr[2 * u + 1] ? 1.0 : 0.0;
+        }
+      }
+    }
+    __syncthreads();
+    double2* orow = O + r * ld_u;
+    if (active) {
+      for (int j = warp * JW + jo; j < h; j += NW * JW) {
+        const S f = fs[j];
+        double2* seg = orow + wb + (int64_t)j * upj;
+#pragma unroll
+        for (int q = 0; q < SWEEP_UQ; ++q) {
+          const int u = u0 + 32 * q;
+          if (u < upj) {
+            if constexpr (CPLX) st_stream(seg + u, make_double2(f.x * xa[q], f.y * xa[q]));
+            else st_stream(seg + u, make_double2(f * xa[q], f * xb[q]));
+          }
+        }
+      }
+    }
+    // the short blocks and the padding, element by element
+    auto elem = [&](int64_t e) -> S {
+      S v = Traits<CPLX>::zero();
+      if (e >= P) return v;
+      if constexpr (MODEL == MODEL_RBM) {
+        if (e < n) {
+          if constexpr (CPLX) v.x = xr[e] ? 1.0 : 0.0; else v = xr[e] ? 1.0 : 0.0;
+        } else if (e < (int64_t)n + h) {
+          v = fs[e - n];
+        }
+      } else {
+        if (e >= hn && e < hn + h) {
+          v = G[r * h + (e - hn)];
+        } else if (e >= hn + h && e < hn + 2 * h) {
+          if constexpr (!CPLX) v = reinterpret_cast<const double*>(Tv)[r * h + (e - hn - h)];
+        } else if (e == hn + 2 * h) {
+          if constexpr (!CPLX) v = 1.0;
+        }
+      }
+      return v;
+    };
+    for (int64_t u = tid; u < ld_u - (we - wb); u += SWEEP_NT) {
+      const int64_t uu = u < wb ? u : u + (we - wb);  // skip the W block
+      if constexpr (CPLX) {
+        st_stream(orow + uu, elem(uu));
+      } else {
+        const double lo = elem(2 * uu), hi = elem(2 * uu + 1);
+        st_stream(orow + uu, make_double2(lo, hi));
+      }
+    }
+  }
+}
+
+}  // namespace irl
