@@ -1108,12 +1108,16 @@ void (*pick_orows(int ppt))(ORowArgs, int) {
 // sweeps only with IRL_OBUILD_SWEEP=2; IRL_OBUILD_SWEEP=0 disables it.
 bool sweep_ok(bool cplx, int model, int n_vis, int hidden) {
   static const int mode = getenv("IRL_OBUILD_SWEEP") ? atoi(getenv("IRL_OBUILD_SWEEP")) : 1;
-  if (mode == 0 || cplx || (n_vis & 1) || n_vis > 2 * 32 * SWEEP_UQ) return false;
+  if (mode == 0) return false;
+  if (cplx)  // complex-theta RBM (cfg4: 470 KB rows): statistics from the complex DMMA colsums
+    return model == MODEL_RBM && n_vis <= OTF_MAX_NIN && n_vis <= 32 * SWEEP_UQ;
+  if ((n_vis & 1) || n_vis > 2 * 32 * SWEEP_UQ) return false;
   return model == MODEL_MLP || (mode == 2 && (hidden & 1) == 0);
 }
 
 bool gemm_stats(bool cplx, int model, int n_vis, int hidden) {
-  if (cplx || n_vis > OTF_MAX_NIN || (hidden & 1)) return false;
+  if (cplx) return sweep_ok(cplx, model, n_vis, hidden);
+  if (n_vis > OTF_MAX_NIN || (hidden & 1)) return false;
   return model == MODEL_MLP || sweep_ok(cplx, model, n_vis, hidden);
 }
 
@@ -1160,8 +1164,13 @@ size_t obuild_bytes(const OPlan& p, int model, int64_t n, int n_vis, int hidden,
   b += align256((size_t)n * OTF_XW * 8);                           // packed inputs
   b += align256((size_t)n * (cplx ? n_vis : (n_vis + 1) & ~1) * sS);  // inputs as table entries
   if (gemm_stats(cplx, model, n_vis, hidden)) {                           // DMMA stats scratch
-    OtfPlan op;
-    if (make_otf_plan(n, n_vis, hidden, op) == IRL_OK) b += otf_ws_layout(op, n, hidden, nullptr).bytes;
+    if (cplx) {
+      OtfCPlan op;
+      if (make_otfc_plan(n, n_vis, hidden, op) == IRL_OK) b += otfc_ws_layout(op, n, n_vis, hidden, nullptr).bytes;
+    } else {
+      OtfPlan op;
+      if (make_otf_plan(n, n_vis, hidden, op) == IRL_OK) b += otf_ws_layout(op, n, hidden, nullptr).bytes;
+    }
     b += align256((size_t)148 * 4 * (n_vis + 1) * 8);             // x sums
   }
   b += 2 * align256((size_t)p.nb * ld_u * 16);                     // partials
@@ -1297,8 +1306,9 @@ int obuild_impl(bool cplx, int model, const uint8_t* x, int64_t n, int n_vis, in
   if (gstats && sweep_ok(cplx, model, n_vis, hidden)) {
     DevInfo d;
     IRL_TRY(dev_info(d));
-    auto fn = model == MODEL_MLP ? k_orows_sweep<false, MODEL_MLP> : k_orows_sweep<false, MODEL_RBM>;
-    const size_t sm = (size_t)hidden * 8;
+    auto fn = cplx ? k_orows_sweep<true, MODEL_RBM>
+                   : (model == MODEL_MLP ? k_orows_sweep<false, MODEL_MLP> : k_orows_sweep<false, MODEL_RBM>);
+    const size_t sm = (size_t)hidden * (cplx ? 16 : 8);
     IRL_TRY(ensure_fn_attrs((const void*)fn, d.smem_optin));
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(n, 2 * (int64_t)d.sms));
     fn<<<grid, SWEEP_NT, sm, st>>>(x, n, n_vis, hidden, T, G, reinterpret_cast<double2*>(O), ld_u);
@@ -1306,6 +1316,22 @@ int obuild_impl(bool cplx, int model, const uint8_t* x, int64_t n, int n_vis, in
     p.fn<<<(unsigned)(p.nb * p.C), p.NT, smem, st>>>(a, (int)buf_bytes);
   }
   IRL_TRY(cuda_check(cudaGetLastError(), "orows launch"));
+  if (gstats && cplx) {
+    // complex theta: obar = conj(sum w conj(O)), grad = sum c conj(O) from the
+    // real N x 2h view of T (as irl_otf_colstats_rbm_c128)
+    OtfCPlan op;
+    IRL_TRY(make_otfc_plan(n, n_vis, hidden, op));
+    OtfCWs wl = otfc_ws_layout(op, n, n_vis, hidden, base + off);
+    OtfCArgs oa{};
+    oa.xbits = xbits;
+    oa.T = reinterpret_cast<const double*>(T);
+    oa.n_rows = n;
+    oa.n_in = n_vis;
+    oa.hidden = hidden;
+    IRL_TRY(otfc_colsum(op, oa, wl, ld, nullptr, w, reinterpret_cast<double2*>(obar), 1, st));
+    return otfc_colsum(op, oa, wl, ld, reinterpret_cast<const double2*>(coeff), nullptr,
+                       reinterpret_cast<double2*>(g), 0, st);
+  }
   if (gstats) {
     // column statistics from the hidden activations and the packed inputs
     OtfPlan op;
