@@ -13,7 +13,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libirlsr.so")
+LIB_PATH = os.environ.get("IRL_LIB_PATH") or os.path.join(_HERE, "libirlsr.so")  # override: A/B builds
 
 IRL_OK = 0
 IRL_ERR_ARG = 1
@@ -123,6 +123,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
             )
         lib = ctypes.CDLL(path)
         for name, (res, args) in SIGNATURES.items():
+            if os.environ.get("IRL_LIB_PATH") and not hasattr(lib, name):
+                continue  # an older A/B build lacks newer entry points
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args

@@ -103,10 +103,10 @@ bool aligned16(const void* p) { return p == nullptr || (reinterpret_cast<uintptr
 // ----------------------------------------------------------- kernels ----
 using StreamFn = void (*)(StreamArgs);
 
-template <bool CPLX, int MODE>
+template <bool CPLX, int MODE, bool ADD = false>
 StreamFn pick_stream(int ppt, int R) {
 #define IRL_CASE(P, RR) \
-  if (ppt == P && R == RR) return k_stream<CPLX, P, RR, MODE>;
+  if (ppt == P && R == RR) return k_stream<CPLX, P, RR, MODE, ADD>;
   IRL_CASE(2, 1) IRL_CASE(2, 2) IRL_CASE(2, 4) IRL_CASE(4, 1) IRL_CASE(4, 2) IRL_CASE(4, 4)
   IRL_CASE(8, 1) IRL_CASE(8, 2) IRL_CASE(8, 4) IRL_CASE(16, 1) IRL_CASE(16, 2) IRL_CASE(16, 4)
 #undef IRL_CASE
@@ -127,6 +127,7 @@ struct Plan {
   int C = 0, W = 0, PPT = 0, R = 0, NT = 0, NS = 0, nb = 0;
   size_t smem = 0;
   StreamFn fn = nullptr;
+  StreamFn fn_add = nullptr;  // MODE_FUSED with the additive row term (connected product)
 };
 
 size_t stream_extra_smem(bool cplx, int R, int C, int NS) {
@@ -171,6 +172,8 @@ bool choose_geom(int64_t ld_u, int C, bool cplx, int mode, int budget, Plan& p, 
   p.NS = NS;
   p.smem = (size_t)NS * R * slice + stream_extra_smem(cplx, R, C, NS);
   p.fn = pick_stream_any(cplx, mode, best_ppt, R);
+  if (mode == MODE_FUSED)
+    p.fn_add = cplx ? pick_stream<true, MODE_FUSED, true>(best_ppt, R) : pick_stream<false, MODE_FUSED, true>(best_ppt, R);
   return p.fn != nullptr;
 }
 
@@ -230,6 +233,7 @@ int make_plan_uncached(int64_t n, int64_t ld_u, bool cplx, int mode, Plan& out) 
       Plan p;
       if (!choose_geom(ld_u, C, cplx, mode, budget, p)) continue;
       IRL_TRY(ensure_fn_attrs((const void*)p.fn, budget));
+      if (p.fn_add) IRL_TRY(ensure_fn_attrs((const void*)p.fn_add, budget));
       int active = 0;
       if (C == 1) {
         int occ = 0;
@@ -270,6 +274,7 @@ int make_plan_uncached(int64_t n, int64_t ld_u, bool cplx, int mode, Plan& out) 
     Plan p;
     if (!choose_geom(ld_u, C, cplx, mode, budget, p)) continue;
     IRL_TRY(ensure_fn_attrs((const void*)p.fn, budget));
+    if (p.fn_add) IRL_TRY(ensure_fn_attrs((const void*)p.fn_add, budget));
     int occ = 0;
     IRL_TRY(occupancy_blocks(p, occ));
     // ~2 waves of CTAs over the SMs
@@ -335,7 +340,9 @@ int launch_stream(const Plan& p, const StreamArgs& a, cudaStream_t st) {
     args.dbg = dbg;
   }
   void* kargs[] = {&args};
-  return cuda_check(cudaLaunchKernelExC(&cfg, (const void*)p.fn, kargs), "stream kernel launch");
+  const StreamFn fn = (args.yadd && p.mode == MODE_FUSED) ? p.fn_add : p.fn;
+  if (!fn) return fail(IRL_ERR_DEVICE, "no stream kernel instance");
+  return cuda_check(cudaLaunchKernelExC(&cfg, (const void*)fn, kargs), "stream kernel launch");
 }
 
 // finisher launched with programmatic dependent launch (overlaps its launch

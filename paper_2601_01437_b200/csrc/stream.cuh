@@ -78,8 +78,13 @@ __host__ __device__ constexpr int stream_max_nt(int ppt) {
   return ppt <= 2 ? 992 : ppt <= 4 ? 768 : ppt <= 8 ? 480 : 320;
 }
 
-template <bool CPLX, int PPT, int R, int MODE>
+// ADD (MODE_FUSED only): the additive row term yadd is compiled in only for the
+// connected product, so the plain fused product keeps its exact schedule
+// (a runtime test cost the clustered cfg3 product 2.15 -> 2.72 ms).  MODE_ACC
+// tests yadd at run time (no measurable cost there).
+template <bool CPLX, int PPT, int R, int MODE, bool ADD = false>
 __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const StreamArgs a) {
+  constexpr bool kAdd = (MODE == MODE_FUSED && ADD) || MODE == MODE_ACC;
   using T = Traits<CPLX>;
   using S = typename T::S;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -314,7 +319,10 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
           t = (lane < rows) ? tslot[b * R + lane] : T::zero();
         }
       }
-      if (lane < rows) yv = T::add(T::mul(cf0, T::sub(t, s_val)), cf1);  // cf1 = yadd_n (0 without)
+      if (lane < rows) {
+        yv = T::mul(cf0, T::sub(t, s_val));
+        if constexpr (kAdd) yv = T::add(yv, cf1);  // cf1 = yadd_n (0 without)
+      }
     } else {
       yv = cf0;
     }
@@ -354,7 +362,9 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
         cf1 = reinterpret_cast<const S*>(a.coeff1)[r0 + lane];
       } else if constexpr (MODE != MODE_DOT) {
         cf0 = reinterpret_cast<const S*>(a.coeff0)[r0 + lane];
-        if (a.yadd) cf1 = reinterpret_cast<const S*>(a.yadd)[r0 + lane];
+        if constexpr (kAdd) {
+          if (a.yadd) cf1 = reinterpret_cast<const S*>(a.yadd)[r0 + lane];
+        }
       }
       if constexpr (MODE == MODE_ACC) {
         for (int c = 0; c < C; ++c)
@@ -389,7 +399,7 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
         acc_group(g, pa, T::zero(), cf0, cf1);
         advance(pa);
         cf0 = cn0;
-        cf1 = cn1;
+        if constexpr (kAdd) cf1 = cn1;
       }
     }
   } else {

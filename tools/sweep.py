@@ -34,6 +34,34 @@ def flush_l2(buf):
     buf.add_(1.0)
 
 
+def _peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"])
+    except (OSError, KeyError, ValueError):
+        return 8000.0 * 0.8
+
+
+PEAK = _peak()
+DMMA_PEAK_TFLOPS = 37.0  # measured FP64 tensor (DMMA) peak on this B200 pool, tools/fp64_peak.cu
+
+
+def cpu_leg(cfg, budget_bytes: float = 1.5e9):
+    """The reference's arithmetic (oracle port of est.heff_matvec, with its
+    per-call centring copy) on a row sample sized to ~1.5 GB of O, extrapolated
+    linearly in N_s ("extrapolated" when not the full N)."""
+    sys.path.insert(0, ROOT)
+    import bench
+
+    b = 16 if cfg.complex_params else 8
+    width = cfg.param_count * (2 if cfg.complex_params else 1)
+    n_sub = int(max(256, min(cfg.n_rows, budget_bytes // (width * b))))
+    sec = bench.cpu_reference_sample(cfg, n_sub, reps=3)
+    full = sec * cfg.n_rows / n_sub
+    return {"mvp_s": 1.0 / full, "cores": bench.cpu_cores(), "kind": "port", "rows_timed": n_sub,
+            "extrapolated_x": cfg.n_rows / n_sub}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="1,2,3,4,5")
@@ -41,6 +69,7 @@ def main():
     ap.add_argument("--rows", type=int, default=0)
     ap.add_argument("--irl", type=int, default=1)
     ap.add_argument("--otf", type=int, default=0, help="MLP configs in on-the-fly mode (O not stored)")
+    ap.add_argument("--cpu", type=int, default=0, help="also time the CPU oracle port on a row sample (same run)")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     dev = torch.device("cuda", 0)
@@ -76,8 +105,11 @@ def main():
             # useful DMMA flops: dot (n_in k-steps) + acc (n_in + 1 columns) per real hidden column
             cols = cfg.hidden * (2 if cfg.complex_params else 1)
             flops = 2.0 * batch.n_rows * cols * (2 * cfg.n_inputs + 1)
+            tf = flops / (med / 1e3) / 1e12
             out = {"config": cfg.name + "-otf", "prepare_ms": prep, "otf": {"ms": med, "mvp_s": 1e3 / med,
-                   "tflops": flops / (med / 1e3) / 1e12}}
+                   "tflops": tf, "frac_dmma_measured": tf / DMMA_PEAK_TFLOPS}}
+            if args.cpu:
+                out["cpu_baseline"] = cpu_leg(cfg)
             if args.irl:
                 conf = OPT.OptimizerConfig(m=cfg.m, max_restarts=cfg.max_restarts)
                 OPT.solve_step(batch, conf, seed=cfg.lanczos_seed, energy=en)
@@ -140,6 +172,17 @@ def main():
             torch.cuda.synchronize()
             out["irl"] = {"wall_ms": (time.perf_counter() - t0) * 1e3, "n_matvec": res.n_matvec,
                           "lambda": res.lambda_min, "converged": res.converged}
+        # roofline fractions of the AUTO path against the measured copy peak and the 8 TB/s spec
+        auto = {"fused": "fused", "two_pass": "two_pass", "rows": "rows", "wide": "wide"}[
+            _lib.mvp_plan(N, ld, batch.is_complex, 0)["path"]]
+        if "ms" in out.get(auto, {}):
+            ms = out[auto]["ms"]
+            one, two = N * P * b_el / (ms / 1e3) / 1e9, 2 * N * P * b_el / (ms / 1e3) / 1e9
+            out["roofline"] = {"auto_path": auto, "mvp_s": 1e3 / ms, "gbs_one_read": one, "gbs_two_pass": two,
+                               "frac_measured_one_read": one / PEAK, "frac_measured_two_pass": two / PEAK,
+                               "frac_spec_two_pass": two / 8000.0, "peak_measured_gbs": PEAK}
+        if args.cpu:
+            out["cpu_baseline"] = cpu_leg(cfg)
         print(json.dumps(out), flush=True)
         del batch, inp, xt, obar, g, gc, coeff
         torch.cuda.empty_cache()
