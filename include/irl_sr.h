@@ -281,6 +281,33 @@ int irl_eloc_combine(const int64_t* indptr, const double* elements, const double
 int irl_sorted_lookup(const uint64_t* keys, int64_t n_keys, const uint64_t* queries, int64_t n_queries, int64_t* out,
                       void* stream);
 
+/* Connected completion on an on-the-fly batch (O never stored; the products of
+ * irl_otf_mvp_*): the same cache arrays as irl_connected_mvp_*; partner_O
+ * holds stored partner rows (n_partner x ld), or is NULL when partner_row
+ * indexes the batch's own rows (exact mode: the partner dots are the batch's
+ * centred dots of the same product).  coeff may be NULL (completion only). */
+size_t irl_otf_connected_workspace_bytes(int model, int64_t n, int64_t n_partner, int n_in, int hidden, int64_t ld,
+                                         int is_complex);
+int irl_otf_connected_mvp_rbm_f64(const uint64_t* xbits, const double* t, int64_t n, int n_vis, int hidden,
+                                  int64_t ld, const double* obar, const double* w, const double* coeff,
+                                  const int64_t* dist_index, const int64_t* indptr, const int64_t* partner_row,
+                                  const double* pcoeff, const double* partner_O, int64_t n_partner, const double* v,
+                                  double* out, const double* half_f, const double* u0, double* out0, void* ws,
+                                  size_t ws_bytes, void* stream);
+int irl_otf_connected_mvp_mlp_f64(const uint64_t* xbits, const double* t, const double* g, int64_t n, int n_in,
+                                  int hidden, int64_t ld, const double* obar, const double* w, const double* coeff,
+                                  const int64_t* dist_index, const int64_t* indptr, const int64_t* partner_row,
+                                  const double* pcoeff, const double* partner_O, int64_t n_partner, const double* v,
+                                  double* out, const double* half_f, const double* u0, double* out0, void* ws,
+                                  size_t ws_bytes, void* stream);
+int irl_otf_connected_mvp_rbm_c128(const uint64_t* xbits, const double* t, int64_t n, int n_vis, int hidden,
+                                   int64_t ld, const double* obar, const double* w, const double* coeff,
+                                   const int64_t* dist_index, const int64_t* indptr, const int64_t* partner_row,
+                                   const double* pcoeff, const double* partner_O, int64_t n_partner,
+                                   const double* v_re, const double* v_im, double* out_re, double* out_im,
+                                   const double* hf_re, const double* hf_im, const double* u0, double* out0, void* ws,
+                                   size_t ws_bytes, void* stream);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

@@ -300,7 +300,7 @@ def build_connected_cache(params, integrals, sector, batch: SampleBatch) -> Conn
     reps[dist_index.reshape(-1)[order]] = order
     rows = partner_rows_in_batch(uniq, reps, pbits) if pbits.numel() else None
     if rows is not None:
-        return ConnectedCache(dist_index.reshape(-1), indptr, rows, coeff, batch.o_matrix, batch=batch)
+        return ConnectedCache(dist_index.reshape(-1), indptr, rows, coeff, None, batch=batch)
     pb = pbits.cpu().numpy().view(np.uint64)
     pu, pinv = np.unique(pb, return_inverse=True) if len(pb) else (pb, np.zeros(0, dtype=np.int64))
     po = log_derivative_batch(params, sector, pu, ld=batch.ld, device=dev) if len(pu) else \

@@ -44,8 +44,8 @@ __global__ void __launch_bounds__(256) k_connected_rows(
   const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   // s = Obar . v, summed over the DOT pass's column slices in order (as MODE_ACC does)
-  S s = T::zero();
-  if (m > 0)
+  S s = T::zero();  // spart == nullptr: tpart_p already holds centred dots
+  if (m > 0 && spart)
     for (int c = 0; c < C; ++c) s = T::add(s, spart[c]);
   for (int64_t r = warp0; r < n; r += nwarps) {
     const int64_t k = dist_index[r];

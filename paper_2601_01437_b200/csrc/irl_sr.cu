@@ -1697,6 +1697,86 @@ int ar_launch(ArArgs& a, cudaStream_t st) {
   return cuda_check(cudaGetLastError(), "autoregressive kernel launch");
 }
 
+// ------------------------------------------------ connected, on the fly ---
+// The completion on an on-the-fly batch (O never stored): partner dots from
+// stored partner rows (a k_stream DOT pass) or, when the partners are batch
+// rows (partner_O == NULL, exact mode), from the batch's own centred dots (a
+// first k_otf_y pass with unit coefficient); then k_connected_rows, and the
+// product's y pass takes coefficient a and additive term d.
+struct OtfConn {
+  const int64_t* dist_index;
+  const int64_t* indptr;
+  const int64_t* prow;
+  const void* pcoeff;
+  const double* w;
+  const void* cdiag;
+  const double* partner_O;  // null: partners are batch rows
+  int64_t m;
+  Plan pp;
+  void* tpart_p;
+  void* spart_p;
+  double* gpart_p;
+  void* q;
+  void* qpart;
+  void* a;
+  void* d;
+};
+
+size_t otf_conn_carve(OtfConn& cx, int64_t n, int64_t m, bool cplx, bool stored, void* base) {
+  const size_t sS = cplx ? 16 : 8;
+  size_t off = 0;
+  auto carve = [&](size_t b) {
+    void* r = base ? static_cast<char*>(base) + off : nullptr;
+    off += align256(std::max<size_t>(b, 1));
+    return r;
+  };
+  const int C = stored ? std::max(cx.pp.C, 1) : 1;
+  cx.tpart_p = carve(stored ? (size_t)C * std::max<int64_t>(m, 1) * sS : 0);
+  cx.spart_p = carve((size_t)C * sS);
+  cx.gpart_p = reinterpret_cast<double*>(carve((size_t)C * 8));
+  cx.q = carve(stored ? 0 : (size_t)n * sS);
+  cx.qpart = carve((size_t)4 * 148 * sS);
+  cx.a = carve((size_t)n * sS);
+  cx.d = carve((size_t)n * sS);
+  return off;
+}
+
+int otf_conn_partner_dot(OtfConn& cx, bool cplx, int64_t ld, const double* v_re, const double* v_im,
+                         const double* obar, cudaStream_t st) {
+  if (!cx.partner_O || cx.m == 0) return IRL_OK;
+  StreamArgs a{};
+  a.O = reinterpret_cast<const double2*>(cx.partner_O);
+  a.n_rows = cx.m;
+  a.ld_u = cplx ? ld : ld / 2;
+  a.v_re = v_re;
+  a.v_im = v_im;
+  a.obar = reinterpret_cast<const double2*>(obar);
+  a.tpart = cx.tpart_p;
+  a.spart = cx.spart_p;
+  a.gpart = cx.gpart_p;
+  return launch_stream(cx.pp, a, st);
+}
+
+int otf_conn_rows(OtfConn& cx, bool cplx, int64_t n, cudaStream_t st) {
+  DevInfo d;
+  IRL_TRY(dev_info(d));
+  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 8), (int64_t)d.sms * 8));
+  const bool stored = cx.partner_O != nullptr;
+  const void* tp = stored ? cx.tpart_p : cx.q;
+  const int C = stored ? std::max(cx.pp.C, 1) : 1;
+  const int64_t m = stored ? cx.m : n;
+  const void* sp = stored ? cx.spart_p : nullptr;
+  if (cplx)
+    k_connected_rows<true><<<blocks, 256, 0, st>>>(cx.dist_index, cx.indptr, cx.prow, (const double2*)cx.pcoeff,
+                                                   (const double2*)tp, C, m, (const double2*)sp, cx.w,
+                                                   (const double2*)cx.cdiag, n, (double2*)cx.a, (double2*)cx.d);
+  else
+    k_connected_rows<false><<<blocks, 256, 0, st>>>(cx.dist_index, cx.indptr, cx.prow, (const double*)cx.pcoeff,
+                                                    (const double*)tp, C, m, (const double*)sp, cx.w,
+                                                    (const double*)cx.cdiag, n, (double*)cx.a, (double*)cx.d);
+  return cuda_check(cudaGetLastError(), "connected rows launch");
+}
+
 }  // namespace
 
 // =================================================================== ABI ==
@@ -1885,12 +1965,12 @@ int irl_otf_colstats_mlp_f64(const uint64_t* xbits, const double* t, const doubl
   return otf_stats(pl, a, wl, MODEL_MLP, n, n_in, hidden, ld, w, coeff, obar, grad, nullptr, 0, st);
 }
 
-int irl_otf_mvp_mlp_f64(const uint64_t* xbits, const double* t, const double* g, int64_t n, int n_in, int hidden,
+static int otf_mvp_mlp_core(const uint64_t* xbits, const double* t, const double* g, int64_t n, int n_in, int hidden,
                         int64_t ld, const double* obar, const double* coeff, const double* v, double* out,
                         const double* half_f, const double* u0, double* out0, void* ws, size_t ws_bytes,
-                        void* stream) {
+                        void* stream, const OtfConn* cx) {
   IRL_TRY(otf_check(xbits, t, g, n, n_in, hidden, ld));
-  if (!coeff || !v || !out) return fail(IRL_ERR_ARG, "null pointer");
+  if ((!coeff && !cx) || !v || !out) return fail(IRL_ERR_ARG, "null pointer");
   OtfPlan pl;
   IRL_TRY(make_otf_plan(n, n_in, hidden, pl));
   OtfWs wl = otf_ws_layout(pl, n, hidden, ws);
@@ -1914,13 +1994,31 @@ int irl_otf_mvp_mlp_f64(const uint64_t* xbits, const double* t, const double* g,
   a.y = wl.y;
   a.part = wl.part;
   a.partu = wl.partu;
+  if (cx) IRL_TRY(otf_conn_partner_dot(*const_cast<OtfConn*>(cx), false, ld, v, nullptr, obar, st));
   IRL_TRY(otf_dot_launch(a, true, st));
-  k_otf_y<<<pl.ny, 256, 0, st>>>(wl.tpart, pl.jc, n, coeff, v, P - 1, wl.dpart, obar ? pl.ny : 0, wl.y, wl.ypart,
-                                 nullptr, -1, n_in);
+  const double* ceff = coeff;
+  const double* yadd = nullptr;
+  if (cx) {
+    if (!cx->partner_O)
+      k_otf_y<<<pl.ny, 256, 0, st>>>(wl.tpart, pl.jc, n, nullptr, v, P - 1, wl.dpart, obar ? pl.ny : 0,
+                                     (double*)cx->q, (double*)cx->qpart, nullptr, -1, n_in);
+    IRL_TRY(otf_conn_rows(*const_cast<OtfConn*>(cx), false, n, st));
+    ceff = (const double*)cx->a;
+    yadd = (const double*)cx->d;
+  }
+  k_otf_y<<<pl.ny, 256, 0, st>>>(wl.tpart, pl.jc, n, ceff, v, P - 1, wl.dpart, obar ? pl.ny : 0, wl.y, wl.ypart,
+                                 nullptr, -1, n_in, yadd);
   IRL_TRY(otf_acc_launch(pl, a, st, 1, true));
   k_otf_finish<<<fin_grid(ld), dim3(32, 8), 0, st>>>(wl.part, wl.partu, a.nb, hidden, n_in, pl.kc, ld, wl.ypart,
                                                        pl.ny, obar, half_f, u0, wl.gpart, pl.ny, out, out0);
   return cuda_check(cudaGetLastError(), "otf finish launch");
+}
+
+int irl_otf_mvp_mlp_f64(const uint64_t* xbits, const double* t, const double* g, int64_t n, int n_in, int hidden,
+                        int64_t ld, const double* obar, const double* coeff, const double* v, double* out,
+                        const double* half_f, const double* u0, double* out0, void* ws, size_t ws_bytes,
+                        void* stream) {
+  return otf_mvp_mlp_core(xbits, t, g, n, n_in, hidden, ld, obar, coeff, v, out, half_f, u0, out0, ws, ws_bytes, stream, nullptr);
 }
 
 int irl_otf_prepare_rbm_f64(const uint8_t* x, int64_t n, int n_vis, int hidden, const double* theta, uint64_t* xbits,
@@ -1957,10 +2055,10 @@ int irl_otf_colstats_rbm_f64(const uint64_t* xbits, const double* t, int64_t n, 
                    (cudaStream_t)stream);
 }
 
-int irl_otf_mvp_rbm_f64(const uint64_t* xbits, const double* t, int64_t n, int n_vis, int hidden, int64_t ld,
+static int otf_mvp_rbm_core(const uint64_t* xbits, const double* t, int64_t n, int n_vis, int hidden, int64_t ld,
                         const double* obar, const double* coeff, const double* v, double* out, const double* half_f,
-                        const double* u0, double* out0, void* ws, size_t ws_bytes, void* stream) {
-  if (!xbits || !t || !coeff || !v || !out || n < 1) return fail(IRL_ERR_ARG, "null pointer");
+                        const double* u0, double* out0, void* ws, size_t ws_bytes, void* stream, const OtfConn* cx) {
+  if (!xbits || !t || (!coeff && !cx) || !v || !out || n < 1) return fail(IRL_ERR_ARG, "null pointer");
   const int64_t P = (int64_t)n_vis + hidden + (int64_t)hidden * n_vis;
   if (ld != irl_padded_ld(P, 0)) return fail(IRL_ERR_ALIGN, "ld must equal irl_padded_ld(P=%lld)", (long long)P);
   if (n_vis > OTF_MAX_NIN || (hidden & 1) || !aligned16(t)) return fail(IRL_ERR_ARG, "unsupported on-the-fly shape");
@@ -1988,9 +2086,20 @@ int irl_otf_mvp_rbm_f64(const uint64_t* xbits, const double* t, int64_t n, int n
   a.y = wl.y;
   a.part = wl.part;
   a.partu = wl.partu;
+  if (cx) IRL_TRY(otf_conn_partner_dot(*const_cast<OtfConn*>(cx), false, ld, v, nullptr, obar, st));
   IRL_TRY(otf_dot_launch(a, false, st));
-  k_otf_y<<<pl.ny, 256, 0, st>>>(wl.tpart, pl.jc, n, coeff, v, -1, wl.dpart, obar ? pl.ny : 0, wl.y, wl.ypart, xbits,
-                                 0, n_vis);
+  const double* ceff = coeff;
+  const double* yadd = nullptr;
+  if (cx) {
+    if (!cx->partner_O)
+      k_otf_y<<<pl.ny, 256, 0, st>>>(wl.tpart, pl.jc, n, nullptr, v, -1, wl.dpart, obar ? pl.ny : 0,
+                                     (double*)cx->q, (double*)cx->qpart, xbits, 0, n_vis);
+    IRL_TRY(otf_conn_rows(*const_cast<OtfConn*>(cx), false, n, st));
+    ceff = (const double*)cx->a;
+    yadd = (const double*)cx->d;
+  }
+  k_otf_y<<<pl.ny, 256, 0, st>>>(wl.tpart, pl.jc, n, ceff, v, -1, wl.dpart, obar ? pl.ny : 0, wl.y, wl.ypart, xbits,
+                                 0, n_vis, yadd);
   IRL_TRY(otf_acc_launch(pl, a, st, 1, false));
   const int nbx = std::min<int>(4 * d.sms, (int)std::max<int64_t>(1, n / 64));
   k_xsum<<<nbx, 128, 0, st>>>(xbits, wl.y, n, n_vis, wl.xpart, wl.ypart2);
@@ -1998,6 +2107,12 @@ int irl_otf_mvp_rbm_f64(const uint64_t* xbits, const double* t, int64_t n, int n
                                                            wl.ypart, pl.ny, ld, obar, half_f, u0, wl.gpart, pl.ny,
                                                            out, out0);
   return cuda_check(cudaGetLastError(), "otf rbm finish launch");
+}
+
+int irl_otf_mvp_rbm_f64(const uint64_t* xbits, const double* t, int64_t n, int n_vis, int hidden, int64_t ld,
+                        const double* obar, const double* coeff, const double* v, double* out, const double* half_f,
+                        const double* u0, double* out0, void* ws, size_t ws_bytes, void* stream) {
+  return otf_mvp_rbm_core(xbits, t, n, n_vis, hidden, ld, obar, coeff, v, out, half_f, u0, out0, ws, ws_bytes, stream, nullptr);
 }
 
 int irl_otf_prepare_rbm_c128(const uint8_t* x, int64_t n, int n_vis, int hidden, const double* theta,
@@ -2039,12 +2154,12 @@ int irl_otf_colstats_rbm_c128(const uint64_t* xbits, const double* t, int64_t n,
                      reinterpret_cast<double2*>(grad), 0, st);
 }
 
-int irl_otf_mvp_rbm_c128(const uint64_t* xbits, const double* t, int64_t n, int n_vis, int hidden, int64_t ld,
+static int otf_mvp_rbmc_core(const uint64_t* xbits, const double* t, int64_t n, int n_vis, int hidden, int64_t ld,
                          const double* obar, const double* coeff, const double* v_re, const double* v_im,
                          double* out_re, double* out_im, const double* half_f_re, const double* half_f_im,
-                         const double* u0, double* out0, void* ws, size_t ws_bytes, void* stream) {
+                         const double* u0, double* out0, void* ws, size_t ws_bytes, void* stream, const OtfConn* cx) {
   IRL_TRY(otfc_check(xbits, t, n, n_vis, hidden, ld));
-  if (!coeff || !v_re || !v_im || !out_re || !out_im) return fail(IRL_ERR_ARG, "null pointer");
+  if ((!coeff && !cx) || !v_re || !v_im || !out_re || !out_im) return fail(IRL_ERR_ARG, "null pointer");
   if ((half_f_re || u0 || out0) && !(half_f_re && half_f_im && u0 && out0))
     return fail(IRL_ERR_ARG, "bordered product needs half_f_re, half_f_im, u0 and out0");
   OtfCPlan pl;
@@ -2054,6 +2169,7 @@ int irl_otf_mvp_rbm_c128(const uint64_t* xbits, const double* t, int64_t n, int 
   cudaStream_t st = (cudaStream_t)stream;
   const double2* ob = reinterpret_cast<const double2*>(obar);
   k_vdot_c<<<pl.ny, 256, 0, st>>>(ob, v_re, v_im, half_f_re, half_f_im, ld, wl.dpart, wl.gpart);
+  if (cx) IRL_TRY(otf_conn_partner_dot(*const_cast<OtfConn*>(cx), true, ld, v_re, v_im, obar, st));
   OtfCArgs a{};
   a.xbits = xbits;
   a.T = t;
@@ -2072,8 +2188,18 @@ int irl_otf_mvp_rbm_c128(const uint64_t* xbits, const double* t, int64_t n, int 
     k_otf_dot_c<<<pl.nb_dot, 288, pl.smem_dot, st>>>(a, mt);
   }
   IRL_TRY(cuda_check(cudaGetLastError(), "otf dot (complex) launch"));
-  k_otf_y_c<<<pl.ny, 256, 0, st>>>(wl.tpart, pl.jc, n, reinterpret_cast<const double2*>(coeff), v_re, v_im, 0, n_vis,
-                                   xbits, wl.dpart, obar ? pl.ny : 0, wl.y, wl.ypart);
+  const double2* ceff = reinterpret_cast<const double2*>(coeff);
+  const double2* yadd = nullptr;
+  if (cx) {
+    if (!cx->partner_O)
+      k_otf_y_c<<<pl.ny, 256, 0, st>>>(wl.tpart, pl.jc, n, nullptr, v_re, v_im, 0, n_vis, xbits, wl.dpart,
+                                       obar ? pl.ny : 0, (double2*)cx->q, (double2*)cx->qpart);
+    IRL_TRY(otf_conn_rows(*const_cast<OtfConn*>(cx), true, n, st));
+    ceff = (const double2*)cx->a;
+    yadd = (const double2*)cx->d;
+  }
+  k_otf_y_c<<<pl.ny, 256, 0, st>>>(wl.tpart, pl.jc, n, ceff, v_re, v_im, 0, n_vis, xbits, wl.dpart,
+                                   obar ? pl.ny : 0, wl.y, wl.ypart, yadd);
   a.y = wl.y;
   a.yr = nullptr;
   a.part = wl.part;
@@ -2089,6 +2215,13 @@ int irl_otf_mvp_rbm_c128(const uint64_t* xbits, const double* t, int64_t n, int 
                                                              pl.nbx, wl.ypart, pl.ny, ld, ob, half_f_re, half_f_im,
                                                              u0, wl.gpart, pl.ny, out_re, out_im, out0, nullptr, 0);
   return cuda_check(cudaGetLastError(), "otf finish (complex) launch");
+}
+
+int irl_otf_mvp_rbm_c128(const uint64_t* xbits, const double* t, int64_t n, int n_vis, int hidden, int64_t ld,
+                         const double* obar, const double* coeff, const double* v_re, const double* v_im,
+                         double* out_re, double* out_im, const double* half_f_re, const double* half_f_im,
+                         const double* u0, double* out0, void* ws, size_t ws_bytes, void* stream) {
+  return otf_mvp_rbmc_core(xbits, t, n, n_vis, hidden, ld, obar, coeff, v_re, v_im, out_re, out_im, half_f_re, half_f_im, u0, out0, ws, ws_bytes, stream, nullptr);
 }
 
 int irl_lanczos_step_small(double* V, int64_t ldv, double* W, int64_t L, int j, int m, double* ab, void* stream) {
@@ -2329,6 +2462,88 @@ int irl_sorted_lookup(const uint64_t* keys, int64_t n_keys, const uint64_t* quer
   const unsigned blocks = (unsigned)std::min<int64_t>(cdiv(n_queries, 256), 148 * 32);
   k_sorted_lookup<<<blocks, 256, 0, (cudaStream_t)stream>>>(keys, n_keys, queries, n_queries, out);
   return cuda_check(cudaGetLastError(), "lookup launch");
+}
+
+// ---- connected completion on on-the-fly batches (partner_O: stored partner
+// rows, or NULL when partner_row indexes batch rows)
+static int otf_conn_setup(OtfConn& cx, bool cplx, int64_t n, int64_t ld, const double* w, const double* coeff,
+                          const int64_t* dist_index, const int64_t* indptr, const int64_t* partner_row,
+                          const double* pcoeff, const double* partner_O, int64_t n_partner, void* ws,
+                          size_t ws_bytes, size_t base_bytes) {
+  if (!w || !dist_index || !indptr) return fail(IRL_ERR_ARG, "null cache pointer");
+  if (n_partner < 0 || (n_partner > 0 && (!partner_row || !pcoeff))) return fail(IRL_ERR_ARG, "bad partner arguments");
+  if (partner_O && !aligned16(partner_O)) return fail(IRL_ERR_ALIGN, "partner_O must be 16-byte aligned");
+  cx = OtfConn{};
+  cx.dist_index = dist_index;
+  cx.indptr = indptr;
+  cx.prow = partner_row;
+  cx.pcoeff = pcoeff;
+  cx.w = w;
+  cx.cdiag = coeff;
+  cx.partner_O = partner_O;
+  cx.m = partner_O ? n_partner : n;
+  const bool stored = partner_O != nullptr;
+  if (stored && n_partner > 0) IRL_TRY(make_plan(n_partner, cplx ? ld : ld / 2, cplx, MODE_DOT, cx.pp));
+  const size_t need = align256(base_bytes) + otf_conn_carve(cx, n, cx.m, cplx, stored, nullptr);
+  if (ws_bytes < need) return fail(IRL_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, need);
+  otf_conn_carve(cx, n, cx.m, cplx, stored, static_cast<char*>(ws) + align256(base_bytes));
+  return IRL_OK;
+}
+
+size_t irl_otf_connected_workspace_bytes(int model, int64_t n, int64_t n_partner, int n_in, int hidden, int64_t ld,
+                                         int is_complex) {
+  const bool cplx = is_complex != 0;
+  const size_t base = cplx ? irl_otf_workspace_bytes_c128(n, n_in, hidden) : irl_otf_workspace_bytes(n, n_in, hidden);
+  (void)model;
+  OtfConn cx{};
+  size_t extra = otf_conn_carve(cx, n, n, cplx, false, nullptr);
+  if (n_partner > 0 && make_plan(n_partner, cplx ? ld : ld / 2, cplx, MODE_DOT, cx.pp) == IRL_OK)
+    extra = std::max(extra, otf_conn_carve(cx, n, n_partner, cplx, true, nullptr));
+  g_err.clear();
+  return align256(base) + extra;
+}
+
+int irl_otf_connected_mvp_rbm_f64(const uint64_t* xbits, const double* t, int64_t n, int n_vis, int hidden,
+                                  int64_t ld, const double* obar, const double* w, const double* coeff,
+                                  const int64_t* dist_index, const int64_t* indptr, const int64_t* partner_row,
+                                  const double* pcoeff, const double* partner_O, int64_t n_partner, const double* v,
+                                  double* out, const double* half_f, const double* u0, double* out0, void* ws,
+                                  size_t ws_bytes, void* stream) {
+  const size_t base = irl_otf_workspace_bytes(n, n_vis, hidden);
+  OtfConn cx;
+  IRL_TRY(otf_conn_setup(cx, false, n, ld, w, coeff, dist_index, indptr, partner_row, pcoeff, partner_O, n_partner,
+                         ws, ws_bytes, base));
+  return otf_mvp_rbm_core(xbits, t, n, n_vis, hidden, ld, obar, coeff, v, out, half_f, u0, out0, ws, base, stream,
+                          &cx);
+}
+
+int irl_otf_connected_mvp_mlp_f64(const uint64_t* xbits, const double* t, const double* g, int64_t n, int n_in,
+                                  int hidden, int64_t ld, const double* obar, const double* w, const double* coeff,
+                                  const int64_t* dist_index, const int64_t* indptr, const int64_t* partner_row,
+                                  const double* pcoeff, const double* partner_O, int64_t n_partner, const double* v,
+                                  double* out, const double* half_f, const double* u0, double* out0, void* ws,
+                                  size_t ws_bytes, void* stream) {
+  const size_t base = irl_otf_workspace_bytes(n, n_in, hidden);
+  OtfConn cx;
+  IRL_TRY(otf_conn_setup(cx, false, n, ld, w, coeff, dist_index, indptr, partner_row, pcoeff, partner_O, n_partner,
+                         ws, ws_bytes, base));
+  return otf_mvp_mlp_core(xbits, t, g, n, n_in, hidden, ld, obar, coeff, v, out, half_f, u0, out0, ws, base, stream,
+                          &cx);
+}
+
+int irl_otf_connected_mvp_rbm_c128(const uint64_t* xbits, const double* t, int64_t n, int n_vis, int hidden,
+                                   int64_t ld, const double* obar, const double* w, const double* coeff,
+                                   const int64_t* dist_index, const int64_t* indptr, const int64_t* partner_row,
+                                   const double* pcoeff, const double* partner_O, int64_t n_partner,
+                                   const double* v_re, const double* v_im, double* out_re, double* out_im,
+                                   const double* hf_re, const double* hf_im, const double* u0, double* out0, void* ws,
+                                   size_t ws_bytes, void* stream) {
+  const size_t base = irl_otf_workspace_bytes_c128(n, n_vis, hidden);
+  OtfConn cx;
+  IRL_TRY(otf_conn_setup(cx, true, n, ld, w, coeff, dist_index, indptr, partner_row, pcoeff, partner_O, n_partner,
+                         ws, ws_bytes, base));
+  return otf_mvp_rbmc_core(xbits, t, n, n_vis, hidden, ld, obar, coeff, v_re, v_im, out_re, out_im, hf_re, hf_im, u0,
+                           out0, ws, base, stream, &cx);
 }
 
 }  // extern "C"

@@ -328,7 +328,8 @@ __global__ void __launch_bounds__(256) k_otf_y(const double* __restrict__ tpart,
                                                const double* __restrict__ coeff, const double* v, int64_t p_last,
                                                const double* __restrict__ dpart, int n_dpart, double* y,
                                                double* ypart, const uint64_t* __restrict__ xbits, int64_t offa,
-                                               int n_in) {
+                                               int n_in, const double* __restrict__ yadd = nullptr) {
+  // coeff == nullptr: y = q (the centred row dot itself; connected completion)
   __shared__ double sh[8];
   __shared__ double va[OTF_MAX_NIN];
   if (offa >= 0)
@@ -354,7 +355,8 @@ __global__ void __launch_bounds__(256) k_otf_y(const double* __restrict__ tpart,
       }
       t += xa;
     }
-    const double yy = coeff[r] * ((t + vc) - s);
+    double yy = (coeff ? coeff[r] : 1.0) * ((t + vc) - s);
+    if (yadd) yy += yadd[r];
     y[r] = yy;
     acc += yy;
   }
@@ -1109,7 +1111,8 @@ __global__ void __launch_bounds__(256) k_otf_y_c(const double2* __restrict__ tpa
                                                  const double2* __restrict__ coeff, const double* v_re,
                                                  const double* v_im, int64_t offa, int n_in,
                                                  const uint64_t* __restrict__ xbits, const double2* __restrict__ sp,
-                                                 int n_sp, double2* y, double2* ypart) {
+                                                 int n_sp, double2* y, double2* ypart,
+                                                 const double2* __restrict__ yadd = nullptr) {
   __shared__ double2 va[OTF_MAX_NIN];
   __shared__ double2 sh[8];
   for (int i = threadIdx.x; i < n_in; i += blockDim.x)
@@ -1153,8 +1156,12 @@ __global__ void __launch_bounds__(256) k_otf_y_c(const double2* __restrict__ tpa
     }
     tr -= sr;
     ti -= si;
-    const double2 c = coeff[r];
-    const double2 yy = make_double2(c.x * tr - c.y * ti, c.x * ti + c.y * tr);
+    const double2 c = coeff ? coeff[r] : make_double2(1.0, 0.0);
+    double2 yy = make_double2(c.x * tr - c.y * ti, c.x * ti + c.y * tr);
+    if (yadd) {
+      yy.x += yadd[r].x;
+      yy.y += yadd[r].y;
+    }
     y[r] = yy;
     ar += yy.x;
     ai += yy.y;

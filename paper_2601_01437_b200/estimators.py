@@ -370,14 +370,36 @@ def _apply(batch: SampleBatch, coeff: torch.Tensor | None, v: torch.Tensor, out:
 
 
 def _apply_connected(batch, cache, coeff, obar, v, out, mode, half_f, u0, out0, stream) -> None:
-    if batch.otf is not None:
-        raise ValueError("the connected completion needs a stored-O batch (build_batch(mode='stored'))")
     cache._check_batch(batch)
     ws = cache.workspace(batch)
     n = batch.n_rows
-    common = (_lib.ptr(batch.o_matrix), n, batch.param_count, batch.ld, _lib.ptr(obar), _lib.ptr(batch.weights),
-              _lib.ptr(coeff), _lib.ptr(cache.dist_index), _lib.ptr(cache.indptr), _lib.ptr(cache.partner_row),
-              _lib.ptr(cache.coeff), _lib.ptr(cache.partner_o), cache.n_partner)
+    tail = (_lib.ptr(batch.weights), _lib.ptr(coeff), _lib.ptr(cache.dist_index), _lib.ptr(cache.indptr),
+            _lib.ptr(cache.partner_row), _lib.ptr(cache.coeff))
+    if batch.otf is not None:
+        # on-the-fly batch: partner dots from the stored partner rows, or (in-batch
+        # partners) from the product's own centred dots
+        o = batch.otf
+        po = _lib.ptr(cache.partner_o)
+        if batch.kind == KIND_HERMITIAN:
+            (v_re, v_im), (o_re, o_im) = v, out
+            h_re, h_im = half_f if half_f is not None else (None, None)
+            _lib.call("irl_otf_connected_mvp_rbm_c128", _lib.ptr(o["xbits"]), _lib.ptr(o["t"]), n, o["n_in"],
+                      o["hidden"], batch.ld, _lib.ptr(obar), *tail, po, cache.n_partner, _lib.ptr(v_re),
+                      _lib.ptr(v_im), _lib.ptr(o_re), _lib.ptr(o_im), _lib.ptr(h_re), _lib.ptr(h_im), _lib.ptr(u0),
+                      _lib.ptr(out0), _lib.ptr(ws), ws.numel(), stream)
+        elif o["model"] == _lib.MODEL_RBM:
+            _lib.call("irl_otf_connected_mvp_rbm_f64", _lib.ptr(o["xbits"]), _lib.ptr(o["t"]), n, o["n_in"],
+                      o["hidden"], batch.ld, _lib.ptr(obar), *tail, po, cache.n_partner, _lib.ptr(v), _lib.ptr(out),
+                      _lib.ptr(half_f), _lib.ptr(u0), _lib.ptr(out0), _lib.ptr(ws), ws.numel(), stream)
+        else:
+            _lib.call("irl_otf_connected_mvp_mlp_f64", _lib.ptr(o["xbits"]), _lib.ptr(o["t"]), _lib.ptr(o["g"]), n,
+                      o["n_in"], o["hidden"], batch.ld, _lib.ptr(obar), *tail, po, cache.n_partner, _lib.ptr(v),
+                      _lib.ptr(out), _lib.ptr(half_f), _lib.ptr(u0), _lib.ptr(out0), _lib.ptr(ws), ws.numel(),
+                      stream)
+        return
+    po = batch.o_matrix if cache.in_batch else cache.partner_o
+    common = (_lib.ptr(batch.o_matrix), n, batch.param_count, batch.ld, _lib.ptr(obar), *tail, _lib.ptr(po),
+              cache.n_partner)
     if not batch.is_complex:
         _lib.call("irl_connected_mvp_f64", *common, _lib.ptr(v), _lib.ptr(out), _lib.ptr(half_f), _lib.ptr(u0),
                   _lib.ptr(out0), int(mode), _lib.ptr(ws), ws.numel(), stream)
@@ -564,9 +586,11 @@ class ConnectedCache:
         if tuple(pr.shape) != (nnz,):
             raise ValueError("partner_row length must equal indptr[-1]")
         ld, p = batch.ld, batch.param_count
-        if isinstance(partner_o, torch.Tensor) and partner_o.is_cuda and partner_o.ndim == 2 \
+        if partner_o is None or partner_o is batch.o_matrix:
+            po = None  # partners are batch rows (exact mode): partner_row indexes the batch
+        elif isinstance(partner_o, torch.Tensor) and partner_o.is_cuda and partner_o.ndim == 2 \
                 and partner_o.shape[1] == ld and partner_o.dtype == cdt:
-            po = partner_o.contiguous()  # e.g. the batch's own O (partners that are batch rows)
+            po = partner_o.contiguous()
         else:
             src = partner_o
             if not isinstance(src, torch.Tensor):
@@ -582,7 +606,7 @@ class ConnectedCache:
             po = torch.zeros((max(m, 0), ld), dtype=cdt, device=dev)
             if m:
                 po[:, :p] = _as_tensor(src, cdt, dev)
-        m = int(po.shape[0])
+        m = n if po is None else int(po.shape[0])
         if nnz and (int(pr.min()) < 0 or int(pr.max()) >= m):
             raise IndexError("partner_row out of range")
         if isinstance(coeff, torch.Tensor):
@@ -612,10 +636,21 @@ class ConnectedCache:
         if self._batch_id != id(batch):
             raise ValueError("connected cache was built for another batch")
 
+    @property
+    def in_batch(self) -> bool:
+        """Partners are the batch's own rows (no separate partner O)."""
+        return self.partner_o is None
+
     def workspace(self, batch: SampleBatch) -> torch.Tensor:
         if self._ws is None:
-            nbytes = int(_lib.lib().irl_connected_workspace_bytes(batch.n_rows, self.n_partner, batch.ld,
-                                                                   int(batch.is_complex)))
+            if batch.otf is not None:
+                o = batch.otf
+                nbytes = int(_lib.lib().irl_otf_connected_workspace_bytes(
+                    int(o["model"]), batch.n_rows, 0 if self.in_batch else self.n_partner, o["n_in"], o["hidden"],
+                    batch.ld, int(batch.is_complex)))
+            else:
+                nbytes = int(_lib.lib().irl_connected_workspace_bytes(batch.n_rows, self.n_partner, batch.ld,
+                                                                       int(batch.is_complex)))
             self._ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=batch.device)
         return self._ws
 

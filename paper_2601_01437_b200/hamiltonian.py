@@ -254,7 +254,8 @@ def connected_partners(params: AnsatzParameters, integrals: MolecularIntegrals, 
 
 
 def build_batch(params: AnsatzParameters, integrals: MolecularIntegrals, sector: Sector, n_samples: int = 0,
-                seed: int = 0, *, configs=None, device=None, enumeration_cap: int = 10**6) -> SampleBatch:
+                seed: int = 0, *, configs=None, device=None, enumeration_cap: int = 10**6,
+                mode: str = "stored") -> SampleBatch:
     """``est.build_batch`` (est:79-133) for the shallow NQS on the device.
 
     Exact mode (``n_samples == 0``): the whole sector, weights ``|psi|^2``
@@ -286,6 +287,14 @@ def build_batch(params: AnsatzParameters, integrals: MolecularIntegrals, sector:
         w = w / float(w.sum())
     else:
         w = torch.full((len(bits),), 1.0 / n_samples, dtype=torch.float64, device=dev)
+    if mode == "otf":  # O regenerated inside every product (ansatz.build_batch_otf)
+        from .ansatz import build_batch_otf
+
+        batch = build_batch_otf(params, x, e_loc, weights=w, n_samples=n_samples, device=dev)
+        batch.xbits = bits
+        return batch
+    if mode != "stored":
+        raise ValueError(f"unknown build mode {mode!r}")
     kind = KIND_HERMITIAN if arch.complex_params else KIND_REAL
     p = arch.param_count
     ld = _lib.padded_ld(p, arch.complex_params)
@@ -322,7 +331,7 @@ def build_connected_cache(params: AnsatzParameters, integrals: MolecularIntegral
     reps[dist_index[order]] = order
     rows = partner_rows_in_batch(uniq, reps, pbits) if pbits.numel() else None
     if rows is not None:
-        cache = ConnectedCache(dist_index, indptr, rows, coeff, batch.o_matrix, batch=batch)
+        cache = ConnectedCache(dist_index, indptr, rows, coeff, None, batch=batch)
     else:
         arch = params.architecture
         pb = pbits.cpu().numpy().view(np.uint64)

@@ -198,8 +198,9 @@ def test_hermitian_connected_golden(pkg, mode):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("build", ["stored", "otf"])
 @pytest.mark.parametrize("idx,rows", [(1, 8192), (2, 2048), (3, 512), (4, 128)])
-def test_config_connected_vs_oracle(pkg, idx, rows):
+def test_config_connected_vs_oracle(pkg, idx, rows, build):
     """BASELINE shapes (row subsets) with seeded synthetic partners: the device
     completion and the full connected product against the oracle."""
     from paper_2601_01437_b200 import ansatz as A, estimators as E, synthetic
@@ -209,7 +210,7 @@ def test_config_connected_vs_oracle(pkg, idx, rows):
     arch = (A.RBMArchitecture(c.n_inputs, c.hidden, c.complex_params) if c.model == "rbm"
             else A.MLPArchitecture(c.n_inputs, c.hidden))
     params = A.AnsatzParameters(arch, inp.theta)
-    b = A.build_batch(params, inp.x, inp.e_loc)
+    b = A.build_batch(params, inp.x, inp.e_loc, mode=build)  # otf: O regenerated, partner rows stored
     partners, elements, indptr, dist = synthetic.connected_partners(inp.x, 4, seed=100 + idx)
     cache = A.build_connected_cache(params, b, inp.x, partners, elements, indptr, dist_index=dist)
     # oracle: rows and coefficients from the numpy restatement

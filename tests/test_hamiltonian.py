@@ -279,3 +279,36 @@ def test_outer_step_golden(cuda, g):
     scan = [OPT.energy_at(A.AnsatzParameters(params.architecture, o["theta"] + s * o["direction"]), ints,
                           ints.sector()) for s in cfg.line_search]
     assert rel(scan, o["scan"][: len(scan)]) < 1e-10
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["rbm", "rbmc"])
+def test_otf_batch_in_batch_partners(cuda, g, name):
+    """Exact batch with O regenerated on the fly: the partners are batch rows, so
+    the completion takes its partner dots from the product's own centred dots
+    (no partner O at all); products and the solve match the stored-O batch."""
+    from paper_2601_01437_b200 import estimators as E, hamiltonian as H, optimizer as OPT
+
+    ints = device_integrals(g)
+    params = device_params(g, name)
+    bs = H.build_batch(params, ints, ints.sector())
+    bo = H.build_batch(params, ints, ints.sector(), mode="otf")
+    cs = H.build_connected_cache(params, ints, ints.sector(), bs)
+    co = H.build_connected_cache(params, ints, ints.sector(), bo)
+    assert co.in_batch and cs.in_batch
+    ens, eno = E.estimate_energy(bs), E.estimate_energy(bo)
+    P = bs.param_count
+    rng = np.random.default_rng(5)
+    for _ in range(2):
+        v = rng.standard_normal(P) + (1j * rng.standard_normal(P) if name == "rbmc" else 0.0)
+        a = E.heff_offdiag_matvec(bs, cs, v)
+        b = E.heff_offdiag_matvec(bo, co, v)
+        assert rel(b, a) < 1e-10
+        a = E.connected_heff_matvec(bs, ens, cs, v)
+        b = E.connected_heff_matvec(bo, eno, co, v)
+        assert rel(b, a) < 1e-10
+    conf = OPT.OptimizerConfig(m=20, max_restarts=3)
+    rs = OPT.solve_step(bs, conf, energy=ens, seed=3, connected=cs)
+    ro = OPT.solve_step(bo, conf, energy=eno, seed=3, connected=co)
+    assert ro.n_matvec == rs.n_matvec
+    assert abs(ro.lambda_min - rs.lambda_min) <= 1e-10 * abs(rs.lambda_min)
