@@ -285,19 +285,25 @@ int irl_sorted_lookup(const uint64_t* keys, int64_t n_keys, const uint64_t* quer
  * irl_otf_mvp_*): the same cache arrays as irl_connected_mvp_*; partner_O
  * holds stored partner rows (n_partner x ld), or is NULL when partner_row
  * indexes the batch's own rows (exact mode: the partner dots are the batch's
- * centred dots of the same product).  coeff may be NULL (completion only). */
+ * centred dots of the same product).  Real models may instead pass the
+ * partners' packed inputs and hidden activations (partner_xbits, partner_t,
+ * MLP partner_g from irl_otf_prepare_*): the partner dots are then regenerated
+ * by the same DMMA GEMM, no partner O is stored.  coeff may be NULL
+ * (completion only). */
 size_t irl_otf_connected_workspace_bytes(int model, int64_t n, int64_t n_partner, int n_in, int hidden, int64_t ld,
                                          int is_complex);
 int irl_otf_connected_mvp_rbm_f64(const uint64_t* xbits, const double* t, int64_t n, int n_vis, int hidden,
                                   int64_t ld, const double* obar, const double* w, const double* coeff,
                                   const int64_t* dist_index, const int64_t* indptr, const int64_t* partner_row,
-                                  const double* pcoeff, const double* partner_O, int64_t n_partner, const double* v,
+                                  const double* pcoeff, const double* partner_O, const uint64_t* partner_xbits,
+                                  const double* partner_t, const double* partner_g, int64_t n_partner, const double* v,
                                   double* out, const double* half_f, const double* u0, double* out0, void* ws,
                                   size_t ws_bytes, void* stream);
 int irl_otf_connected_mvp_mlp_f64(const uint64_t* xbits, const double* t, const double* g, int64_t n, int n_in,
                                   int hidden, int64_t ld, const double* obar, const double* w, const double* coeff,
                                   const int64_t* dist_index, const int64_t* indptr, const int64_t* partner_row,
-                                  const double* pcoeff, const double* partner_O, int64_t n_partner, const double* v,
+                                  const double* pcoeff, const double* partner_O, const uint64_t* partner_xbits,
+                                  const double* partner_t, const double* partner_g, int64_t n_partner, const double* v,
                                   double* out, const double* half_f, const double* u0, double* out0, void* ws,
                                   size_t ws_bytes, void* stream);
 int irl_otf_connected_mvp_rbm_c128(const uint64_t* xbits, const double* t, int64_t n, int n_vis, int hidden,

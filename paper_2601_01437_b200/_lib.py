@@ -93,10 +93,10 @@ SIGNATURES = {
     "irl_eloc_combine": (_I, [_P, _P, _P, _P, _P, _I64, _P, _P]),
     "irl_sorted_lookup": (_I, [_P, _I64, _P, _I64, _P, _P]),
     "irl_otf_connected_workspace_bytes": (_SZ, [_I, _I64, _I64, _I, _I, _I64, _I]),
-    "irl_otf_connected_mvp_rbm_f64": (_I, [_P, _P, _I64, _I, _I, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _P, _P,
-                                           _P, _P, _P, _P, _SZ, _P]),
-    "irl_otf_connected_mvp_mlp_f64": (_I, [_P, _P, _P, _I64, _I, _I, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _P,
-                                           _P, _P, _P, _P, _P, _SZ, _P]),
+    "irl_otf_connected_mvp_rbm_f64": (_I, [_P, _P, _I64, _I, _I, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
+                                           _I64, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "irl_otf_connected_mvp_mlp_f64": (_I, [_P, _P, _P, _I64, _I, _I, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
+                                           _P, _I64, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "irl_otf_connected_mvp_rbm_c128": (_I, [_P, _P, _I64, _I, _I, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _P,
                                             _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
 }

@@ -368,8 +368,27 @@ def build_connected_cache(params: AnsatzParameters, batch: SampleBatch, x, partn
     m = uniq.shape[0]
     cplx = bool(arch.complex_params)
     odt = torch.complex128 if cplx else torch.float64
-    po = torch.zeros((m, batch.ld), dtype=odt, device=dev)
-    if m:
+    regen = batch.otf is not None and not cplx and m > 0
+    po = torch.zeros((0 if regen else m, batch.ld), dtype=odt, device=dev)
+    partner_otf = None
+    if regen:
+        # on-the-fly batch: the partner dots are regenerated from the partners'
+        # packed inputs and hidden activations (no partner O stored)
+        ut = _x_device(uniq, arch.n_inputs, dev)
+        pxb = torch.empty((m, 2), dtype=torch.int64, device=dev)
+        pt = torch.empty((m, arch.hidden), dtype=torch.float64, device=dev)
+        theta_d = _theta_device(params, dev)
+        if arch.model == _lib.MODEL_RBM:
+            pg = None
+            _lib.call("irl_otf_prepare_rbm_f64", _lib.ptr(ut), m, arch.n_visible, arch.hidden, _lib.ptr(theta_d),
+                      _lib.ptr(pxb), _lib.ptr(pt), _lib.stream_handle(dev))
+        else:
+            pg = torch.empty((m, arch.hidden), dtype=torch.float64, device=dev)
+            _lib.call("irl_otf_prepare_mlp_f64", _lib.ptr(ut), m, arch.n_in, arch.hidden, _lib.ptr(theta_d),
+                      _lib.ptr(pxb), _lib.ptr(pt), _lib.ptr(pg), _lib.stream_handle(dev))
+        partner_otf = {"xbits": pxb, "t": pt, "g": pg}
+        lp = log_amplitude_batch(params, uniq, device=dev)
+    elif m:
         ut = _x_device(uniq, arch.n_inputs, dev)
         w = torch.full((m,), 1.0 / m, dtype=torch.float64, device=dev)
         scratch = [torch.empty(batch.ld, dtype=odt, device=dev) for _ in range(2)]
@@ -382,4 +401,4 @@ def build_connected_cache(params: AnsatzParameters, batch: SampleBatch, x, partn
         coeff = torch.as_tensor(np.asarray(elements), dtype=torch.complex128, device=dev) * ratio
     else:
         coeff = torch.zeros(0, dtype=torch.complex128, device=dev)
-    return ConnectedCache(di, ip, inv, coeff, po, batch=batch)
+    return ConnectedCache(di, ip, inv, coeff, po, batch=batch, partner_otf=partner_otf)

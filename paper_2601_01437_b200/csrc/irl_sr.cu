@@ -1710,9 +1710,14 @@ struct OtfConn {
   const void* pcoeff;
   const double* w;
   const void* cdiag;
-  const double* partner_O;  // null: partners are batch rows
+  const double* partner_O;  // null: partners are batch rows (or regenerated, below)
+  const uint64_t* pxbits;   // partners regenerated on the fly: packed inputs, t (and MLP g)
+  const double* pt;
+  const double* pg;
   int64_t m;
   Plan pp;
+  OtfPlan ppl;
+  OtfWs pwl;
   void* tpart_p;
   void* spart_p;
   double* gpart_p;
@@ -1722,7 +1727,8 @@ struct OtfConn {
   void* d;
 };
 
-size_t otf_conn_carve(OtfConn& cx, int64_t n, int64_t m, bool cplx, bool stored, void* base) {
+size_t otf_conn_carve(OtfConn& cx, int64_t n, int64_t m, bool cplx, bool stored, void* base, bool regen = false,
+                      int hidden = 0) {
   const size_t sS = cplx ? 16 : 8;
   size_t off = 0;
   auto carve = [&](size_t b) {
@@ -1734,7 +1740,12 @@ size_t otf_conn_carve(OtfConn& cx, int64_t n, int64_t m, bool cplx, bool stored,
   cx.tpart_p = carve(stored ? (size_t)C * std::max<int64_t>(m, 1) * sS : 0);
   cx.spart_p = carve((size_t)C * sS);
   cx.gpart_p = reinterpret_cast<double*>(carve((size_t)C * 8));
-  cx.q = carve(stored ? 0 : (size_t)n * sS);
+  cx.q = carve(stored ? 0 : (size_t)(regen ? m : n) * sS);
+  if (regen) {
+    const size_t pb = otf_ws_layout(cx.ppl, m, hidden, nullptr).bytes;
+    void* pbase = carve(pb);
+    cx.pwl = otf_ws_layout(cx.ppl, m, hidden, pbase);
+  }
   cx.qpart = carve((size_t)4 * 148 * sS);
   cx.a = carve((size_t)n * sS);
   cx.d = carve((size_t)n * sS);
@@ -1764,7 +1775,7 @@ int otf_conn_rows(OtfConn& cx, bool cplx, int64_t n, cudaStream_t st) {
   const bool stored = cx.partner_O != nullptr;
   const void* tp = stored ? cx.tpart_p : cx.q;
   const int C = stored ? std::max(cx.pp.C, 1) : 1;
-  const int64_t m = stored ? cx.m : n;
+  const int64_t m = (stored || cx.pxbits) ? cx.m : n;
   const void* sp = stored ? cx.spart_p : nullptr;
   if (cplx)
     k_connected_rows<true><<<blocks, 256, 0, st>>>(cx.dist_index, cx.indptr, cx.prow, (const double2*)cx.pcoeff,
@@ -1775,6 +1786,25 @@ int otf_conn_rows(OtfConn& cx, bool cplx, int64_t n, cudaStream_t st) {
                                                     (const double*)tp, C, m, (const double*)sp, cx.w,
                                                     (const double*)cx.cdiag, n, (double*)cx.a, (double*)cx.d);
   return cuda_check(cudaGetLastError(), "connected rows launch");
+}
+
+// Partner dots regenerated from the partners' packed inputs and hidden
+// activations with the batch's own DMMA dot GEMM: q_p = O_p v - Obar.v.
+int otf_conn_regen_dots(OtfConn& cx, const OtfArgs& batch_args, bool has_t, int64_t p_last, int64_t offa,
+                        const double* dpart, int n_dpart, cudaStream_t st) {
+  if (!cx.pxbits || cx.m == 0) return IRL_OK;
+  OtfArgs ap = batch_args;
+  ap.xbits = cx.pxbits;
+  ap.T = cx.pt;
+  ap.G = has_t ? cx.pg : cx.pt;
+  ap.n_rows = cx.m;
+  ap.nb = cx.ppl.nb;
+  ap.tpart = cx.pwl.tpart;
+  IRL_TRY(otf_dot_launch(ap, has_t, st));
+  k_otf_y<<<cx.ppl.ny, 256, 0, st>>>(cx.pwl.tpart, cx.ppl.jc, cx.m, nullptr, batch_args.v, p_last, dpart, n_dpart,
+                                     (double*)cx.q, cx.pwl.ypart, offa >= 0 ? cx.pxbits : nullptr, offa,
+                                     batch_args.n_in);
+  return cuda_check(cudaGetLastError(), "partner dot launch");
 }
 
 }  // namespace
@@ -1999,7 +2029,9 @@ static int otf_mvp_mlp_core(const uint64_t* xbits, const double* t, const double
   const double* ceff = coeff;
   const double* yadd = nullptr;
   if (cx) {
-    if (!cx->partner_O)
+    if (cx->pxbits)
+      IRL_TRY(otf_conn_regen_dots(*const_cast<OtfConn*>(cx), a, true, P - 1, -1, wl.dpart, obar ? pl.ny : 0, st));
+    else if (!cx->partner_O)
       k_otf_y<<<pl.ny, 256, 0, st>>>(wl.tpart, pl.jc, n, nullptr, v, P - 1, wl.dpart, obar ? pl.ny : 0,
                                      (double*)cx->q, (double*)cx->qpart, nullptr, -1, n_in);
     IRL_TRY(otf_conn_rows(*const_cast<OtfConn*>(cx), false, n, st));
@@ -2091,7 +2123,9 @@ static int otf_mvp_rbm_core(const uint64_t* xbits, const double* t, int64_t n, i
   const double* ceff = coeff;
   const double* yadd = nullptr;
   if (cx) {
-    if (!cx->partner_O)
+    if (cx->pxbits)
+      IRL_TRY(otf_conn_regen_dots(*const_cast<OtfConn*>(cx), a, false, -1, 0, wl.dpart, obar ? pl.ny : 0, st));
+    else if (!cx->partner_O)
       k_otf_y<<<pl.ny, 256, 0, st>>>(wl.tpart, pl.jc, n, nullptr, v, -1, wl.dpart, obar ? pl.ny : 0,
                                      (double*)cx->q, (double*)cx->qpart, xbits, 0, n_vis);
     IRL_TRY(otf_conn_rows(*const_cast<OtfConn*>(cx), false, n, st));
@@ -2469,7 +2503,8 @@ int irl_sorted_lookup(const uint64_t* keys, int64_t n_keys, const uint64_t* quer
 static int otf_conn_setup(OtfConn& cx, bool cplx, int64_t n, int64_t ld, const double* w, const double* coeff,
                           const int64_t* dist_index, const int64_t* indptr, const int64_t* partner_row,
                           const double* pcoeff, const double* partner_O, int64_t n_partner, void* ws,
-                          size_t ws_bytes, size_t base_bytes) {
+                          size_t ws_bytes, size_t base_bytes, const uint64_t* pxbits = nullptr,
+                          const double* pt = nullptr, const double* pg = nullptr, int n_in = 0, int hidden = 0) {
   if (!w || !dist_index || !indptr) return fail(IRL_ERR_ARG, "null cache pointer");
   if (n_partner < 0 || (n_partner > 0 && (!partner_row || !pcoeff))) return fail(IRL_ERR_ARG, "bad partner arguments");
   if (partner_O && !aligned16(partner_O)) return fail(IRL_ERR_ALIGN, "partner_O must be 16-byte aligned");
@@ -2481,12 +2516,21 @@ static int otf_conn_setup(OtfConn& cx, bool cplx, int64_t n, int64_t ld, const d
   cx.w = w;
   cx.cdiag = coeff;
   cx.partner_O = partner_O;
-  cx.m = partner_O ? n_partner : n;
+  cx.pxbits = pxbits;
+  cx.pt = pt;
+  cx.pg = pg;
+  const bool regen = pxbits != nullptr;
+  if (regen && (partner_O || cplx || !pt)) return fail(IRL_ERR_ARG, "bad regenerated-partner arguments");
+  cx.m = (partner_O || regen) ? n_partner : n;
   const bool stored = partner_O != nullptr;
   if (stored && n_partner > 0) IRL_TRY(make_plan(n_partner, cplx ? ld : ld / 2, cplx, MODE_DOT, cx.pp));
-  const size_t need = align256(base_bytes) + otf_conn_carve(cx, n, cx.m, cplx, stored, nullptr);
+  if (regen && n_partner > 0) IRL_TRY(make_otf_plan(n_partner, n_in, hidden, cx.ppl));
+  const size_t need =
+      align256(base_bytes) + otf_conn_carve(cx, n, cx.m, cplx, stored, nullptr, regen && n_partner > 0, hidden);
   if (ws_bytes < need) return fail(IRL_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, need);
-  otf_conn_carve(cx, n, cx.m, cplx, stored, static_cast<char*>(ws) + align256(base_bytes));
+  otf_conn_carve(cx, n, cx.m, cplx, stored, static_cast<char*>(ws) + align256(base_bytes), regen && n_partner > 0,
+                 hidden);
+  if (regen && n_partner == 0) cx.pxbits = nullptr;
   return IRL_OK;
 }
 
@@ -2499,6 +2543,8 @@ size_t irl_otf_connected_workspace_bytes(int model, int64_t n, int64_t n_partner
   size_t extra = otf_conn_carve(cx, n, n, cplx, false, nullptr);
   if (n_partner > 0 && make_plan(n_partner, cplx ? ld : ld / 2, cplx, MODE_DOT, cx.pp) == IRL_OK)
     extra = std::max(extra, otf_conn_carve(cx, n, n_partner, cplx, true, nullptr));
+  if (n_partner > 0 && !cplx && make_otf_plan(n_partner, n_in, hidden, cx.ppl) == IRL_OK)
+    extra = std::max(extra, otf_conn_carve(cx, n, n_partner, cplx, false, nullptr, true, hidden));
   g_err.clear();
   return align256(base) + extra;
 }
@@ -2506,13 +2552,14 @@ size_t irl_otf_connected_workspace_bytes(int model, int64_t n, int64_t n_partner
 int irl_otf_connected_mvp_rbm_f64(const uint64_t* xbits, const double* t, int64_t n, int n_vis, int hidden,
                                   int64_t ld, const double* obar, const double* w, const double* coeff,
                                   const int64_t* dist_index, const int64_t* indptr, const int64_t* partner_row,
-                                  const double* pcoeff, const double* partner_O, int64_t n_partner, const double* v,
+                                  const double* pcoeff, const double* partner_O, const uint64_t* partner_xbits,
+                                  const double* partner_t, const double* partner_g, int64_t n_partner, const double* v,
                                   double* out, const double* half_f, const double* u0, double* out0, void* ws,
                                   size_t ws_bytes, void* stream) {
   const size_t base = irl_otf_workspace_bytes(n, n_vis, hidden);
   OtfConn cx;
   IRL_TRY(otf_conn_setup(cx, false, n, ld, w, coeff, dist_index, indptr, partner_row, pcoeff, partner_O, n_partner,
-                         ws, ws_bytes, base));
+                         ws, ws_bytes, base, partner_xbits, partner_t, partner_g, n_vis, hidden));
   return otf_mvp_rbm_core(xbits, t, n, n_vis, hidden, ld, obar, coeff, v, out, half_f, u0, out0, ws, base, stream,
                           &cx);
 }
@@ -2520,13 +2567,14 @@ int irl_otf_connected_mvp_rbm_f64(const uint64_t* xbits, const double* t, int64_
 int irl_otf_connected_mvp_mlp_f64(const uint64_t* xbits, const double* t, const double* g, int64_t n, int n_in,
                                   int hidden, int64_t ld, const double* obar, const double* w, const double* coeff,
                                   const int64_t* dist_index, const int64_t* indptr, const int64_t* partner_row,
-                                  const double* pcoeff, const double* partner_O, int64_t n_partner, const double* v,
+                                  const double* pcoeff, const double* partner_O, const uint64_t* partner_xbits,
+                                  const double* partner_t, const double* partner_g, int64_t n_partner, const double* v,
                                   double* out, const double* half_f, const double* u0, double* out0, void* ws,
                                   size_t ws_bytes, void* stream) {
   const size_t base = irl_otf_workspace_bytes(n, n_in, hidden);
   OtfConn cx;
   IRL_TRY(otf_conn_setup(cx, false, n, ld, w, coeff, dist_index, indptr, partner_row, pcoeff, partner_O, n_partner,
-                         ws, ws_bytes, base));
+                         ws, ws_bytes, base, partner_xbits, partner_t, partner_g, n_in, hidden));
   return otf_mvp_mlp_core(xbits, t, g, n, n_in, hidden, ld, obar, coeff, v, out, half_f, u0, out0, ws, base, stream,
                           &cx);
 }

@@ -380,6 +380,8 @@ def _apply_connected(batch, cache, coeff, obar, v, out, mode, half_f, u0, out0, 
         # partners) from the product's own centred dots
         o = batch.otf
         po = _lib.ptr(cache.partner_o)
+        pr = cache.partner_otf or {}
+        regen = (_lib.ptr(pr.get("xbits")), _lib.ptr(pr.get("t")), _lib.ptr(pr.get("g")))
         if batch.kind == KIND_HERMITIAN:
             (v_re, v_im), (o_re, o_im) = v, out
             h_re, h_im = half_f if half_f is not None else (None, None)
@@ -389,11 +391,13 @@ def _apply_connected(batch, cache, coeff, obar, v, out, mode, half_f, u0, out0, 
                       _lib.ptr(out0), _lib.ptr(ws), ws.numel(), stream)
         elif o["model"] == _lib.MODEL_RBM:
             _lib.call("irl_otf_connected_mvp_rbm_f64", _lib.ptr(o["xbits"]), _lib.ptr(o["t"]), n, o["n_in"],
-                      o["hidden"], batch.ld, _lib.ptr(obar), *tail, po, cache.n_partner, _lib.ptr(v), _lib.ptr(out),
+                      o["hidden"], batch.ld, _lib.ptr(obar), *tail, po, *regen, cache.n_partner, _lib.ptr(v),
+                      _lib.ptr(out),
                       _lib.ptr(half_f), _lib.ptr(u0), _lib.ptr(out0), _lib.ptr(ws), ws.numel(), stream)
         else:
             _lib.call("irl_otf_connected_mvp_mlp_f64", _lib.ptr(o["xbits"]), _lib.ptr(o["t"]), _lib.ptr(o["g"]), n,
-                      o["n_in"], o["hidden"], batch.ld, _lib.ptr(obar), *tail, po, cache.n_partner, _lib.ptr(v),
+                      o["n_in"], o["hidden"], batch.ld, _lib.ptr(obar), *tail, po, *regen, cache.n_partner,
+                      _lib.ptr(v),
                       _lib.ptr(out), _lib.ptr(half_f), _lib.ptr(u0), _lib.ptr(out0), _lib.ptr(ws), ws.numel(),
                       stream)
         return
@@ -563,7 +567,8 @@ class ConnectedCache:
     would raise IndexError there).
     """
 
-    def __init__(self, dist_index, indptr, partner_row, coeff, partner_o, *, batch: SampleBatch):
+    def __init__(self, dist_index, indptr, partner_row, coeff, partner_o, *, batch: SampleBatch,
+                 partner_otf: dict | None = None):
         dev = batch.device
         kind_c = batch.is_complex
         cdt = torch.complex128 if kind_c else torch.float64
@@ -586,7 +591,12 @@ class ConnectedCache:
         if tuple(pr.shape) != (nnz,):
             raise ValueError("partner_row length must equal indptr[-1]")
         ld, p = batch.ld, batch.param_count
-        if partner_o is None or partner_o is batch.o_matrix:
+        if partner_otf is not None:
+            # partners regenerated on the fly (real models): packed inputs + hidden activations
+            if batch.otf is None or batch.is_complex:
+                raise ValueError("regenerated partners need a real on-the-fly batch")
+            po = None
+        elif partner_o is None or partner_o is batch.o_matrix:
             po = None  # partners are batch rows (exact mode): partner_row indexes the batch
         elif isinstance(partner_o, torch.Tensor) and partner_o.is_cuda and partner_o.ndim == 2 \
                 and partner_o.shape[1] == ld and partner_o.dtype == cdt:
@@ -606,7 +616,10 @@ class ConnectedCache:
             po = torch.zeros((max(m, 0), ld), dtype=cdt, device=dev)
             if m:
                 po[:, :p] = _as_tensor(src, cdt, dev)
-        m = n if po is None else int(po.shape[0])
+        if partner_otf is not None:
+            m = int(partner_otf["t"].shape[0])
+        else:
+            m = n if po is None else int(po.shape[0])
         if nnz and (int(pr.min()) < 0 or int(pr.max()) >= m):
             raise IndexError("partner_row out of range")
         if isinstance(coeff, torch.Tensor):
@@ -622,6 +635,7 @@ class ConnectedCache:
         self.partner_row = pr
         self.coeff = c.to(cdt).contiguous()
         self.partner_o = po
+        self.partner_otf = partner_otf
         self.n_partner = m
         self.n_dist = n_dist
         self._batch_id = id(batch)
@@ -639,7 +653,7 @@ class ConnectedCache:
     @property
     def in_batch(self) -> bool:
         """Partners are the batch's own rows (no separate partner O)."""
-        return self.partner_o is None
+        return self.partner_o is None and self.partner_otf is None
 
     def workspace(self, batch: SampleBatch) -> torch.Tensor:
         if self._ws is None:
