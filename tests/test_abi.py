@@ -67,3 +67,22 @@ def test_otf_support_rule():
     assert not A.otf_supported(A.RBMArchitecture(40, 161))
     assert not A.otf_supported(A.MLPArchitecture(101, 64))
     assert A.otf_supported(A.MLPArchitecture(100, 2048))
+
+
+def test_new_entry_points_validate_before_any_cuda_call():
+    """Connected completion, local energies and the autoregressive ansatz
+    return IRL_ERR_ARG for bad arguments without touching a device."""
+    lib = _lib.load()
+    # connected product: null batch pointers
+    rc = lib.irl_connected_mvp_f64(None, 4, 3, 32, None, None, None, None, None, None, None, None, 0, None, None,
+                                   None, None, None, 0, None, 0, None)
+    assert rc == _lib.IRL_ERR_ARG
+    # local energy: unknown model
+    rc = lib.irl_ham_local_energy(7, 0, None, 1, 2, 0.0, None, None, 1e-14, 3, None, None, None, 0, None)
+    assert rc == _lib.IRL_ERR_ARG
+    # autoregressive ansatz: odd orbital count
+    rc = lib.irl_ar_logamp(None, 1, 5, 3, 1, 1, None, None, None, None)
+    assert rc == _lib.IRL_ERR_ARG
+    assert b"autoregressive" in lib.irl_last_error()
+    # sorted lookup: negative sizes
+    assert lib.irl_sorted_lookup(None, -1, None, 0, None, None) == _lib.IRL_ERR_ARG
