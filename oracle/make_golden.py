@@ -544,6 +544,29 @@ def case_autoregressive():
     return out
 
 
+def case_ar_edges():
+    """The autoregressive ansatz on edge sectors (empty / full spin channels,
+    ans:130-153 masking): log amplitudes, rows and exact samples."""
+    from irlnqs.hilbert import Sector, enumerate_sector
+
+    out = {}
+    for tag, (m, nu, nd, hidden) in {"e1": (8, 0, 2, 5), "e2": (8, 4, 1, 5), "e3": (2, 1, 0, 3)}.items():
+        sector = Sector(m, nu, nd)
+        arch = ans.Architecture(m, hidden)
+        rng = np.random.default_rng(len(tag) + m + nu)
+        params = ans.AnsatzParameters(arch, ans.init_parameters(arch, seed=3).theta
+                                      + 0.2 * rng.standard_normal(arch.param_count))
+        configs = enumerate_sector(sector)
+        la = [ans.log_amplitude(params, c, sector) for c in configs]
+        out.update({f"{tag}_theta": params.theta, f"{tag}_shape": np.array([m, nu, nd, hidden]),
+                    f"{tag}_bits": np.array([c.bits for c in configs], dtype=np.uint64),
+                    f"{tag}_lp": np.array([a.log_prob_half for a in la]), f"{tag}_ph": np.array([a.phase for a in la]),
+                    f"{tag}_rows": np.array([ans.log_derivative(params, c, sector) for c in configs]),
+                    f"{tag}_samples": np.array([x.bits for x in ans.sample(params, sector, 32, seed=5)],
+                                               dtype=np.uint64)})
+    return out
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     only = set(sys.argv[1:])
@@ -560,6 +583,7 @@ def main():
         "hamiltonian": case_hamiltonian,
         "outer_step": case_outer_step,
         "autoregressive": case_autoregressive,
+        "ar_edges": case_ar_edges,
     }
     for name, data in cases.items():
         if only and name not in only:

@@ -161,3 +161,22 @@ def test_reference_outer_step_stochastic(cuda, tag):
     assert abs(res.lambda_min - float(d["stoch_lam"])) <= 1e-8 * abs(float(d["stoch_lam"]))
     assert res.step_scale == float(d["stoch_scale"])
     assert rel(res.params.theta, d["stoch_theta_new"]) < 1e-6
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tag", ["e1", "e2", "e3"])
+def test_edge_sectors_golden(cuda, tag):
+    """Empty and full spin channels (the masking of ans:130-153): log
+    amplitudes, rows and exact samples against the reference."""
+    from paper_2601_01437_b200 import autoregressive as AR, hamiltonian as H
+
+    g = golden("ar_edges")
+    m, nu, nd, hidden = (int(v) for v in g[f"{tag}_shape"])
+    params = AR.AnsatzParameters(AR.Architecture(m, hidden), g[f"{tag}_theta"])
+    sector = H.Sector(m, nu, nd)
+    lp = AR.log_amplitude_batch(params, sector, g[f"{tag}_bits"]).cpu().numpy()
+    assert np.max(np.abs(lp.real - g[f"{tag}_lp"])) < 1e-12
+    assert np.max(np.abs(lp.imag - g[f"{tag}_ph"])) < 1e-12
+    rows = AR.log_derivative_batch(params, sector, g[f"{tag}_bits"]).cpu().numpy()
+    assert np.max(np.abs(rows[:, : params.architecture.param_count] - g[f"{tag}_rows"])) < 1e-12
+    assert np.array_equal(AR.sample(params, sector, 32, seed=5), g[f"{tag}_samples"])

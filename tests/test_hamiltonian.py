@@ -312,3 +312,42 @@ def test_otf_batch_in_batch_partners(cuda, g, name):
     ro = OPT.solve_step(bo, conf, energy=eno, seed=3, connected=co)
     assert ro.n_matvec == rs.n_matvec
     assert abs(ro.lambda_min - rs.lambda_min) <= 1e-10 * abs(rs.lambda_min)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("ns,n_up,n_dn,hidden,seed", [
+    (1, 1, 0, 2, 1),    # two spin-orbitals, one electron: no partners of one spin
+    (3, 0, 2, 4, 2),    # empty spin-up channel
+    (4, 4, 1, 2, 3),    # full spin-up channel: no up particles
+    (5, 2, 3, 6, 4),
+    (6, 3, 3, 4, 5),
+])
+def test_local_energy_sector_edges(cuda, ns, n_up, n_dn, hidden, seed):
+    """Edge sectors (empty / full spin channels, a single orbital) of the
+    device enumeration against the oracle restatement (ham:238-302): kept
+    partner sets and elements, local energies for the real and complex RBM."""
+    from paper_2601_01437_b200 import ansatz as A, hamiltonian as H, synthetic as S
+
+    ints = H.parse_fcidump(S.molecule_fcidump(seed, ns, n_up + n_dn, ms2=n_up - n_dn))
+    sec = ints.sector()
+    assert (sec.n_up, sec.n_down) == (n_up, n_dn)
+    bits = H.enumerate_sector(sec)
+    M = 2 * ns
+    rng = np.random.default_rng(seed)
+    for cplx in (False, True):
+        P = M + hidden + hidden * M
+        theta = rng.normal(0, 0.3, P) + (1j * rng.normal(0, 0.3, P) if cplx else 0.0)
+        params = A.AnsatzParameters(A.RBMArchitecture(M, hidden, complex_params=cplx), theta)
+        e = host(H.local_energies(params, ints, bits))
+        lp = lambda b: nqs.rbm_log_psi(theta, occ([b], M), M, hidden)[0]  # noqa: E731
+        ref = np.array([oham.local_energy(lp, ints.e_core, ints.h, ints.g, int(b), ns) for b in bits])
+        if not cplx:
+            ref = ref.real
+        assert np.max(np.abs(e - ref) / np.maximum(1.0, np.abs(ref))) < ELOC_TOL
+        indptr, pbits, elem, _ = H.connected_partners(params, ints, bits)
+        ip, pb, el = host(indptr), host(pbits).view(np.uint64), host(elem)
+        for k, b in enumerate(bits):
+            want = oham.connected(ints.e_core, ints.h, ints.g, int(b), ns)[1:]
+            order = np.argsort(pb[ip[k]:ip[k + 1]])
+            assert np.array_equal(pb[ip[k]:ip[k + 1]][order], np.array([y for y, _ in want], dtype=np.uint64))
+            assert np.allclose(el[ip[k]:ip[k + 1]][order], [x for _, x in want], atol=1e-13, rtol=0)
