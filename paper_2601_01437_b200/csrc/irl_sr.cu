@@ -1572,8 +1572,9 @@ int ham_launch(const HamArgs& a, size_t smem, cudaStream_t st) {
   DevInfo d;
   IRL_TRY(dev_info(d));
   if (smem > (size_t)d.smem_optin - 8192) return fail(IRL_ERR_ARG, "hidden width too large for the local-energy kernel");
-  // E_loc of the RBM: the exp table in shared memory when it fits (one 512-thread CTA per SM)
-  if constexpr (MODE == HAM_ELOC && MODEL == MODEL_RBM) {
+  // E_loc and the partner coefficients of the RBM: the exp table in shared
+  // memory when it fits (one 512-thread CTA per SM)
+  if constexpr ((MODE == HAM_ELOC || MODE == HAM_FILL) && MODEL == MODEL_RBM) {
     const size_t tab = (size_t)2 * a.ns * (a.hidden + 1) * 2 * (CPLX ? 16 : 8);
     if (!getenv("IRL_HAM_NO_SMT") && rup(smem, 16) + tab <= (size_t)d.smem_optin - 16384) {
       auto fn = k_local_energy<CPLX, MODEL, MODE, 512, true>;
