@@ -28,6 +28,7 @@ embedded operator.
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -266,7 +267,7 @@ class OuterStep:
 
 
 def outer_step(params, integrals, sector, config: OptimizerConfig = OptimizerConfig(), step: int = 0, *,
-               mode: int = _lib.MVP_AUTO) -> OuterStep:
+               mode: int = _lib.MVP_AUTO, use_graph: bool | None = None) -> OuterStep:
     """opt:118-195 on the device: the reference's own autoregressive ansatz
     (exact or stochastic batches) or the shallow RBM / MLP (exact mode).
 
@@ -292,7 +293,13 @@ def outer_step(params, integrals, sector, config: OptimizerConfig = OptimizerCon
         energy = estimate_energy(batch)
         cache = H.build_connected_cache(params, integrals, sector, batch)
         make = lambda th: A.AnsatzParameters(params.architecture, th)  # noqa: E731
-    res = solve_step(batch, config, step, energy=energy, mode=mode, connected=cache)
+    if use_graph is None:
+        # every outer step builds a new batch: capturing a sweep that runs once
+        # costs more than it saves (syn6 70-160 -> 11-17 ms, syn10 280 -> 153 ms
+        # eager); capturing recurring restart orders only ("lazy") did not help
+        # the long stochastic restart sequences either (670-930 vs 730 ms)
+        use_graph = {"1": True, "lazy": "lazy"}.get(os.environ.get("IRL_OUTER_GRAPH", ""), False)
+    res = solve_step(batch, config, step, energy=energy, mode=mode, connected=cache, use_graph=use_graph)
     grad = energy_gradient(batch, energy).detach().cpu().numpy()
     d0 = res.direction.detach().cpu().numpy()
     theta = np.asarray(params.theta)
