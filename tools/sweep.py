@@ -2,7 +2,8 @@
 """Per-config performance sweep (one JSON line per config) — development tool.
 
 For each BASELINE config: O-build time (warm), fused / two-pass MVP time and
-GB/s (one O read per fused product, two per two-pass), IRL solve wall time.
+GB/s (one O read per fused product, two per two-pass; device time per product
+after an L2 write flush, from CUDA-graph replays), IRL solve wall time.
 """
 
 import argparse
@@ -32,6 +33,45 @@ def timed(fn, reps):
 
 def flush_l2(buf):
     buf.add_(1.0)
+
+
+def graph_timed(fn, l2buf, k=10, reps=5):
+    """Per-call device time of fn() after a write flush of L2, free of host
+    launch overhead: CUDA graphs of k x (flush, fn) and k x flush, replayed
+    under events; the difference over k.  (Event-timing one eager call after a
+    flush measures the Python/ctypes launch path when the product is short,
+    e.g. cfg1: 25.6 us eager vs 17.5 us on the device.)"""
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        fn()
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+
+    def build(with_fn):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(k):
+                flush_l2(l2buf)
+                if with_fn:
+                    fn()
+        return g
+
+    def run(g):
+        out = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            g.replay()
+            b.record()
+            torch.cuda.synchronize()
+            out.append(a.elapsed_time(b))
+        return statistics.median(out)
+
+    g_both, g_flush = build(True), build(False)
+    t = (run(g_both) - run(g_flush)) / k
+    del g_both, g_flush
+    return t
 
 
 def _peak():
@@ -156,11 +196,8 @@ def main():
             except Exception as exc:  # noqa: BLE001
                 out[name] = {"error": str(exc)[:200]}
                 continue
-            ms = []
-            for _ in range(args.reps):
-                flush_l2(l2buf)
-                ms += timed(lambda: E._apply(batch, coeff, vi, vo, mode=mode), 1)
-            med = statistics.median(ms)
+            med = graph_timed(lambda: E._apply(batch, coeff, vi, vo, mode=mode), l2buf,
+                              k=10 if N * ld < 1e9 else 3)
             out[name] = {"ms": med, "mvp_s": 1e3 / med, "gbs_one_read": N * P * b_el / (med / 1e3) / 1e9,
                          "gbs_traffic": passes * N * ld * b_el / (med / 1e3) / 1e9, "plan": plan}
         if args.irl:
