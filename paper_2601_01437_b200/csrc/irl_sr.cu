@@ -335,10 +335,7 @@ int launch_stream(const Plan& p, const StreamArgs& a, cudaStream_t st) {
   args.C = p.C;
   args.nb = p.nb;
   args.stages = p.NS;
-  {
-    static const int dbg = getenv("IRL_DEBUG") ? atoi(getenv("IRL_DEBUG")) : 0;
-    args.dbg = dbg;
-  }
+  args.dbg = 0;
   void* kargs[] = {&args};
   const StreamFn fn = (args.yadd && p.mode == MODE_FUSED) ? p.fn_add : p.fn;
   if (!fn) return fail(IRL_ERR_DEVICE, "no stream kernel instance");

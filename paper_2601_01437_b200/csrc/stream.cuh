@@ -41,7 +41,7 @@ struct StreamArgs {
   int C;       // column slices (cluster size in MODE_FUSED)
   int nb;      // row blocks (clusters in MODE_FUSED)
   int stages;  // ring depth
-  int dbg;     // development flags (bit 0: skip the DSMEM exchange -- wrong results, timing only)
+  int dbg;     // reserved (0)
   // input vectors (unit-indexed).  real: v_re is the f64 array viewed as units;
   // complex: planar re/im (im may be null = 0).
   const double* v_re;
@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
   double* pro_g = reinterpret_cast<double*>(pro_s + 1);  // [1]
 
   const bool clustered = (MODE == MODE_FUSED) && (C > 1);
-  const bool xchg = clustered && !(a.dbg & 1);
+  const bool xchg = clustered;
   int rank, blk;
   if (MODE == MODE_FUSED) {
     rank = clustered ? (int)cluster_rank() : 0;
