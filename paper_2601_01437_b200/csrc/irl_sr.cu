@@ -18,6 +18,7 @@
 #include "lanczos.cuh"
 #include "stream.cuh"
 #include "rows.cuh"
+#include <utility>
 #include "wide.cuh"
 #include "connected.cuh"
 #include "hamiltonian.cuh"
@@ -885,6 +886,24 @@ int otf_dot_grid(const void* fn, size_t smem, int key, int& grid) {
   return IRL_OK;
 }
 
+// Launch with programmatic stream serialisation (the kernel must begin its
+// global-memory work with griddepcontrol.wait: pdl_enter() in otf.cuh).
+template <typename... KArgs, typename... Args>
+int launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, const char* what,
+               Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cuda_check(cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...), what);
+}
+
 int otf_dot_launch(OtfArgs& a, bool has_t, cudaStream_t st) {
   const void* fn = has_t ? (const void*)k_otf_dot<true> : (const void*)k_otf_dot<false>;
   const size_t smem = otf_dot_smem(a.n_in, has_t, false);
@@ -896,11 +915,8 @@ int otf_dot_launch(OtfArgs& a, bool has_t, cudaStream_t st) {
     IRL_TRY(tile_map(mt, a.T, a.hidden, a.n_rows));
   else
     mt = mg;
-  if (has_t)
-    k_otf_dot<true><<<grid, 288, smem, st>>>(a, mg, mt);
-  else
-    k_otf_dot<false><<<grid, 288, smem, st>>>(a, mg, mt);
-  return cuda_check(cudaGetLastError(), "otf dot launch");
+  if (has_t) return launch_pdl(k_otf_dot<true>, dim3(grid), dim3(288), smem, st, "otf dot launch", a, mg, mt);
+  return launch_pdl(k_otf_dot<false>, dim3(grid), dim3(288), smem, st, "otf dot launch", a, mg, mt);
 }
 
 // launches the acc GEMM variant; a.nb = its row-block count (the partial stride)
@@ -915,8 +931,7 @@ int otf_acc_launch(const OtfPlan& pl, OtfArgs& a, cudaStream_t st, int nyv, bool
     IRL_TRY(tile_map(mt, a.T, a.hidden, a.n_rows));
   else
     mt = mg;
-  f<<<grid, 288, acc_smem(nyv, has_t), st>>>(a, mg, mt);
-  return cuda_check(cudaGetLastError(), "otf acc launch");
+  return launch_pdl(f, grid, dim3(288), acc_smem(nyv, has_t), st, "otf acc launch", a, mg, mt);
 }
 
 // column statistics (obar = sum w O, grad = sum c O) of a real model from the
@@ -2005,7 +2020,8 @@ static int otf_mvp_mlp_core(const uint64_t* xbits, const double* t, const double
   if (ws_bytes < wl.bytes) return fail(IRL_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, wl.bytes);
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t P = (int64_t)hidden * n_in + 2 * (int64_t)hidden + 1;
-  k_vdot2<<<pl.ny, 256, 0, st>>>(obar, half_f, v, ld, wl.dpart, wl.gpart);
+  IRL_TRY(launch_pdl(k_vdot2, dim3(pl.ny), dim3(256), 0, st, "otf vdot launch", obar, half_f, v, (int64_t)ld,
+                     wl.dpart, wl.gpart));
   OtfArgs a{};
   a.xbits = xbits;
   a.T = t;
@@ -2036,12 +2052,14 @@ static int otf_mvp_mlp_core(const uint64_t* xbits, const double* t, const double
     ceff = (const double*)cx->a;
     yadd = (const double*)cx->d;
   }
-  k_otf_y<<<pl.ny, 256, 0, st>>>(wl.tpart, pl.jc, n, ceff, v, P - 1, wl.dpart, obar ? pl.ny : 0, wl.y, wl.ypart,
-                                 nullptr, -1, n_in, yadd);
+  IRL_TRY(launch_pdl(k_otf_y, dim3(pl.ny), dim3(256), 0, st, "otf y launch", (const double*)wl.tpart, (int)pl.jc,
+                     (int64_t)n, ceff, v, (int64_t)(P - 1), (const double*)wl.dpart, obar ? pl.ny : 0, wl.y,
+                     wl.ypart, (const uint64_t*)nullptr, (int64_t)-1, n_in, yadd));
   IRL_TRY(otf_acc_launch(pl, a, st, 1, true));
-  k_otf_finish<<<fin_grid(ld), dim3(32, 8), 0, st>>>(wl.part, wl.partu, a.nb, hidden, n_in, pl.kc, ld, wl.ypart,
-                                                       pl.ny, obar, half_f, u0, wl.gpart, pl.ny, out, out0);
-  return cuda_check(cudaGetLastError(), "otf finish launch");
+  return launch_pdl(k_otf_finish, fin_grid(ld), dim3(32, 8), 0, st, "otf finish launch", (const double*)wl.part,
+                    (const double*)wl.partu, (int)a.nb, hidden, n_in, (int)pl.kc, (int64_t)ld,
+                    (const double*)wl.ypart, (int)pl.ny, obar, half_f, u0, (const double*)wl.gpart, (int)pl.ny, out,
+                    out0);
 }
 
 int irl_otf_mvp_mlp_f64(const uint64_t* xbits, const double* t, const double* g, int64_t n, int n_in, int hidden,
@@ -2099,7 +2117,8 @@ static int otf_mvp_rbm_core(const uint64_t* xbits, const double* t, int64_t n, i
   cudaStream_t st = (cudaStream_t)stream;
   DevInfo d;
   IRL_TRY(dev_info(d));
-  k_vdot2<<<pl.ny, 256, 0, st>>>(obar, half_f, v, ld, wl.dpart, wl.gpart);
+  IRL_TRY(launch_pdl(k_vdot2, dim3(pl.ny), dim3(256), 0, st, "otf vdot launch", obar, half_f, v, (int64_t)ld,
+                     wl.dpart, wl.gpart));
   OtfArgs a{};
   a.xbits = xbits;
   a.T = t;
@@ -2130,15 +2149,17 @@ static int otf_mvp_rbm_core(const uint64_t* xbits, const double* t, int64_t n, i
     ceff = (const double*)cx->a;
     yadd = (const double*)cx->d;
   }
-  k_otf_y<<<pl.ny, 256, 0, st>>>(wl.tpart, pl.jc, n, ceff, v, -1, wl.dpart, obar ? pl.ny : 0, wl.y, wl.ypart, xbits,
-                                 0, n_vis, yadd);
+  IRL_TRY(launch_pdl(k_otf_y, dim3(pl.ny), dim3(256), 0, st, "otf y launch", (const double*)wl.tpart, (int)pl.jc,
+                     (int64_t)n, ceff, v, (int64_t)-1, (const double*)wl.dpart, obar ? pl.ny : 0, wl.y, wl.ypart,
+                     xbits, (int64_t)0, n_vis, yadd));
   IRL_TRY(otf_acc_launch(pl, a, st, 1, false));
   const int nbx = std::min<int>(4 * d.sms, (int)std::max<int64_t>(1, n / 64));
-  k_xsum<<<nbx, 128, 0, st>>>(xbits, wl.y, n, n_vis, wl.xpart, wl.ypart2);
-  k_rbm_otf_finish<<<fin_grid(ld), dim3(32, 8), 0, st>>>(wl.part, a.nb, hidden, n_vis, pl.kc, wl.xpart, nbx,
-                                                           wl.ypart, pl.ny, ld, obar, half_f, u0, wl.gpart, pl.ny,
-                                                           out, out0);
-  return cuda_check(cudaGetLastError(), "otf rbm finish launch");
+  IRL_TRY(launch_pdl(k_xsum, dim3(nbx), dim3(128), 0, st, "otf xsum launch", xbits, (const double*)wl.y, (int64_t)n,
+                     n_vis, wl.xpart, wl.ypart2));
+  return launch_pdl(k_rbm_otf_finish, fin_grid(ld), dim3(32, 8), 0, st, "otf rbm finish launch",
+                    (const double*)wl.part, (int)a.nb, hidden, n_vis, (int)pl.kc, (const double*)wl.xpart, nbx,
+                    (const double*)wl.ypart, (int)pl.ny, (int64_t)ld, obar, half_f, u0, (const double*)wl.gpart,
+                    (int)pl.ny, out, out0);
 }
 
 int irl_otf_mvp_rbm_f64(const uint64_t* xbits, const double* t, int64_t n, int n_vis, int hidden, int64_t ld,

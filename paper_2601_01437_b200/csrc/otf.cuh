@@ -53,6 +53,17 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                : "d"(a), "d"(b));
 }
 
+// Programmatic dependent launch: the product chain (vdot -> dot -> y -> acc ->
+// xsum -> finish) is launched with programmatic stream serialisation, so a
+// kernel's CTAs are set up while its predecessor drains.  Every kernel of the
+// chain waits for its predecessor's completion (and memory) before touching
+// global memory and lets its own successor launch right away; without the
+// launch attribute both instructions are no-ops.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // 0/1 -> 0.0/1.0 without a conversion instruction (1.0 = 0x3FF00000:00000000)
 __device__ __forceinline__ double bit_to_double(uint32_t bit) {
   return __hiloint2double((int)((0u - bit) & 0x3FF00000u), 0);
@@ -199,6 +210,7 @@ __global__ void __maxnreg__(HAS_T ? 168 : 96)
     fence_mbar_init();
   }
   __syncthreads();
+  pdl_enter();
 
   if (warp == 8) {  // ---------------------------------------------- producer
     if (lane == 0) {
@@ -268,7 +280,10 @@ __global__ void __maxnreg__(HAS_T ? 168 : 96)
 #pragma unroll
       for (int q = 0; q < OTF_XW; ++q) xr[mt][q] = X[(wr * 32 + mt * 8 + (lane >> 2)) * OTF_XW + q];
     const double* vrow0 = vw + (wj * 16 + (lane >> 2)) * vs + (lane & 3);
-    for (int kk = 0; kk < ksteps; ++kk) {
+    // a warp whose 16 hidden units all lie past h (tail chunk, e.g. h = 160)
+    // skips its GEMM: c stays v_b = 0 there and meets zero v_u
+    const int kend = (jc * OTF_BJ + wj * 16 < h) ? ksteps : 0;
+    for (int kk = 0; kk < kend; ++kk) {
       const int kq = kk * 4 + (lane & 3);
       const double b0 = vrow0[kk * 4];
       const double b1 = vrow0[kk * 4 + 8 * vs];
@@ -329,6 +344,7 @@ __global__ void __launch_bounds__(256) k_otf_y(const double* __restrict__ tpart,
                                                const double* __restrict__ dpart, int n_dpart, double* y,
                                                double* ypart, const uint64_t* __restrict__ xbits, int64_t offa,
                                                int n_in, const double* __restrict__ yadd = nullptr) {
+  pdl_enter();
   // coeff == nullptr: y = q (the centred row dot itself; connected completion)
   __shared__ double sh[8];
   __shared__ double va[OTF_MAX_NIN];
@@ -420,6 +436,7 @@ __global__ void __maxnreg__((NKT <= 8 && NY == 1 && !HAS_T) ? 96 : 168)
     fence_mbar_init();
   }
   __syncthreads();
+  pdl_enter();
 
   double c[NY][2][NKT][2];
   double cu[NY][2][2];
@@ -475,8 +492,10 @@ __global__ void __maxnreg__((NKT <= 8 && NY == 1 && !HAS_T) ? 96 : 168)
       const double* Tt = G + OTF_TILE;
       const uint64_t* X = xs + st * OTF_BM * OTF_XW;
       const double* Y = ys + st * NY * OTF_BM;
+      // warps whose 16 hidden units all lie past h never store: skip the GEMM
+      const int kk_end = (j0 + wj * 16 < h) ? OTF_BM / 4 : 0;
 #pragma unroll 2
-      for (int kk = wk; kk < OTF_BM / 4; kk += 2) {
+      for (int kk = wk; kk < kk_end; kk += 2) {
         const int rl = kk * 4 + (lane & 3);
         const int o0 = swz64(rl, jl), o1 = swz64(rl, jl + 8);
         const double g0 = G[o0], g1 = G[o1];
@@ -580,6 +599,7 @@ __global__ void __launch_bounds__(256) k_otf_finish(const double* __restrict__ p
                                                     const double* __restrict__ obar, const double* hf,
                                                     const double* u0, const double* dgpart, int n_dgpart,
                                                     double* out, double* out0) {
+  pdl_enter();
   __shared__ double sh[8];
   __shared__ double sm[8][33];
   const double Y = block_sum_fixed(ypart, n_ypart, sh);
@@ -621,6 +641,7 @@ __global__ void __launch_bounds__(256) k_otf_finish(const double* __restrict__ p
 // per-CTA partial dots s = obar . v and g0 = hf . v over the padded vector
 __global__ void __launch_bounds__(256) k_vdot2(const double* __restrict__ a1, const double* __restrict__ a2,
                                                const double* __restrict__ v, int64_t len, double* p1, double* p2) {
+  pdl_enter();
   __shared__ double s1[8], s2[8];
   double x1 = 0.0, x2 = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x) {
@@ -772,6 +793,7 @@ namespace irl {
 // packed row words are broadcast), plus ypart[blk] = sum y_r.  Fixed order.
 __global__ void __launch_bounds__(128) k_xsum(const uint64_t* __restrict__ xbits, const double* __restrict__ y,
                                               int64_t n, int n_in, double* xpart, double* ypart) {
+  pdl_enter();
   __shared__ uint64_t xb[128][OTF_XW];
   __shared__ double yb[128];
   __shared__ double sh[4];
@@ -837,6 +859,7 @@ __global__ void __launch_bounds__(256) k_rbm_otf_finish(const double* __restrict
                                                         const double* __restrict__ obar, const double* hf,
                                                         const double* u0, const double* dgpart, int n_dgpart,
                                                         double* out, double* out0) {
+  pdl_enter();
   __shared__ double sh[8];
   __shared__ double sm[8][33];
   const double Y = block_sum_fixed(ypart, n_ypart, sh);
