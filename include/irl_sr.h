@@ -151,6 +151,14 @@ int irl_otf_mvp_mlp_f64(const uint64_t* xbits, const double* t, const double* g,
                         int64_t ld, const double* obar, const double* coeff, const double* v, double* out,
                         const double* half_f, const double* u0, double* out0, void* ws, size_t ws_bytes,
                         void* stream);
+/* Same product with G = u (1 - t^2) formed inside the GEMM kernels from t and
+ * the output weights u (length hidden) instead of read from a stored G: half
+ * the activation traffic per product (the small-n_in products are HBM-bound on
+ * t and g).  Same arguments as irl_otf_mvp_mlp_f64 with u in place of g. */
+int irl_otf_mvp_mlp_u_f64(const uint64_t* xbits, const double* t, const double* u, int64_t n, int n_in, int hidden,
+                          int64_t ld, const double* obar, const double* coeff, const double* v, double* out,
+                          const double* half_f, const double* u0, double* out0, void* ws, size_t ws_bytes,
+                          void* stream);
 /* Complex-theta RBM on the fly (hermitian kind, cfg4): t = tanh(b + W x) complex
  * (N x h interleaved c128), vectors in the planar real embedding of irl_mvp_c128
  * (ld = irl_padded_ld(P, 1)); obar, coeff, grad interleaved c128.  Statistics:

@@ -65,6 +65,7 @@ SIGNATURES = {
     "irl_otf_prepare_mlp_f64": (_I, [_P, _I64, _I, _I, _P, _P, _P, _P, _P]),
     "irl_otf_colstats_mlp_f64": (_I, [_P, _P, _P, _I64, _I, _I, _I64, _P, _P, _P, _P, _P, _SZ, _P]),
     "irl_otf_mvp_mlp_f64": (_I, [_P, _P, _P, _I64, _I, _I, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "irl_otf_mvp_mlp_u_f64": (_I, [_P, _P, _P, _I64, _I, _I, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "irl_otf_prepare_rbm_f64": (_I, [_P, _I64, _I, _I, _P, _P, _P, _P]),
     "irl_otf_colstats_rbm_f64": (_I, [_P, _P, _I64, _I, _I, _I64, _P, _P, _P, _P, _P, _SZ, _P]),
     "irl_otf_mvp_rbm_f64": (_I, [_P, _P, _I64, _I, _I, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),

@@ -291,6 +291,11 @@ def build_batch_otf(params: AnsatzParameters, x, e_loc, weights=None, n_samples:
         _lib.call("irl_otf_prepare_mlp_f64", _lib.ptr(xt), n, arch.n_in, arch.hidden, _lib.ptr(theta),
                   _lib.ptr(xbits), _lib.ptr(t), _lib.ptr(g), _lib.stream_handle(dev))
     batch.otf = {"xbits": xbits, "t": t, "g": g, "n_in": arch.n_inputs, "hidden": arch.hidden, "model": arch.model}
+    if g is not None:
+        # MLP output weights u (theta layout [W, b, u, c], ans:67-83): the product
+        # can form G = u (1 - t^2) from t instead of reading g
+        off = arch.hidden * arch.n_in + arch.hidden
+        batch.otf["u"] = theta[off:off + arch.hidden].contiguous()
     return batch
 
 

@@ -857,7 +857,7 @@ size_t otf_dot_smem(int n_in, bool has_t, bool cplx) {
   const size_t st = OTF_DOT_STAGES;
   const size_t tiles = st * OTF_TILE * (has_t ? 2 : 1);
   const size_t red = (size_t)2 * 4 * OTF_BM * (cplx ? 2 : 1);
-  return 1024 + (tiles + st * OTF_BM * OTF_XW + red + 2 * st + OTF_BJ * 2 + (size_t)OTF_BJ * vs) * 8;
+  return 1024 + (tiles + st * OTF_BM * OTF_XW + red + 2 * st + OTF_BJ * 3 + (size_t)OTF_BJ * vs) * 8;
 }
 
 // persistent grid of the dot kernels: every resident CTA slot, occupancy cached per (kernel, n_in)
@@ -2011,7 +2011,8 @@ int irl_otf_colstats_mlp_f64(const uint64_t* xbits, const double* t, const doubl
 static int otf_mvp_mlp_core(const uint64_t* xbits, const double* t, const double* g, int64_t n, int n_in, int hidden,
                         int64_t ld, const double* obar, const double* coeff, const double* v, double* out,
                         const double* half_f, const double* u0, double* out0, void* ws, size_t ws_bytes,
-                        void* stream, const OtfConn* cx) {
+                        void* stream, const OtfConn* cx, const double* uvec = nullptr) {
+  // uvec: G = u (1 - T^2) formed in the GEMM kernels from T (g unused; any valid pointer)
   IRL_TRY(otf_check(xbits, t, g, n, n_in, hidden, ld));
   if ((!coeff && !cx) || !v || !out) return fail(IRL_ERR_ARG, "null pointer");
   OtfPlan pl;
@@ -2038,6 +2039,7 @@ static int otf_mvp_mlp_core(const uint64_t* xbits, const double* t, const double
   a.y = wl.y;
   a.part = wl.part;
   a.partu = wl.partu;
+  a.u = cx ? nullptr : uvec;
   if (cx) IRL_TRY(otf_conn_partner_dot(*const_cast<OtfConn*>(cx), false, ld, v, nullptr, obar, st));
   IRL_TRY(otf_dot_launch(a, true, st));
   const double* ceff = coeff;
@@ -2067,6 +2069,15 @@ int irl_otf_mvp_mlp_f64(const uint64_t* xbits, const double* t, const double* g,
                         const double* half_f, const double* u0, double* out0, void* ws, size_t ws_bytes,
                         void* stream) {
   return otf_mvp_mlp_core(xbits, t, g, n, n_in, hidden, ld, obar, coeff, v, out, half_f, u0, out0, ws, ws_bytes, stream, nullptr);
+}
+
+int irl_otf_mvp_mlp_u_f64(const uint64_t* xbits, const double* t, const double* u, int64_t n, int n_in, int hidden,
+                          int64_t ld, const double* obar, const double* coeff, const double* v, double* out,
+                          const double* half_f, const double* u0, double* out0, void* ws, size_t ws_bytes,
+                          void* stream) {
+  if (!u) return fail(IRL_ERR_ARG, "null pointer");
+  return otf_mvp_mlp_core(xbits, t, t, n, n_in, hidden, ld, obar, coeff, v, out, half_f, u0, out0, ws, ws_bytes, stream,
+                          nullptr, u);
 }
 
 int irl_otf_prepare_rbm_f64(const uint8_t* x, int64_t n, int n_vis, int hidden, const double* theta, uint64_t* xbits,

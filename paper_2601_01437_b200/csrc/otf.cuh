@@ -45,6 +45,10 @@ struct OtfArgs {
   const double* y2;       // [N] second weight vector (NY = 2)
   double* part;           // [NY][nb][h][KC]
   double* partu;          // [NY][nb][h]
+  // MLP only: output weights u (length h).  Non-null: G = u (1 - T^2) is formed
+  // from the T tile in registers and G is never read (half the activation
+  // traffic; the on-the-fly MLP product at small n_in is HBM-bound on T and G)
+  const double* u;
 };
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
@@ -191,6 +195,8 @@ __global__ void __maxnreg__(HAS_T ? 168 : 96)
   double* vb = reinterpret_cast<double*>(empty + ST);                      // [BJ]
   double* vu = vb + OTF_BJ;                                                // [BJ]
   double* vw = vu + OTF_BJ;                                                // [BJ][vs]
+  double* uw = vw + OTF_BJ * vs;                                           // [BJ] u chunk (gu)
+  const bool gu = HAS_T && a.u != nullptr;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t N = a.n_rows;
@@ -222,10 +228,10 @@ __global__ void __maxnreg__(HAS_T ? 168 : 96)
         const int nrows = (int)min((int64_t)OTF_BM, N - r0);
         const int j0 = jc * OTF_BJ;
         const int nbox = min(4, (h - j0 + 15) >> 4);
-        mbar_arrive_expect_tx(&full[st], (uint32_t)(nbox * NM * OTF_BM * 128) + (uint32_t)nrows * OTF_XW * 8u);
+        mbar_arrive_expect_tx(&full[st], (uint32_t)(nbox * (gu ? 1 : NM) * OTF_BM * 128) + (uint32_t)nrows * OTF_XW * 8u);
         double* tg = tiles + st * NM * OTF_TILE;
         for (int b = 0; b < nbox; ++b) {
-          tma_load_2d(tg + b * 1024, &tmG, j0 + 16 * b, (int)r0, &full[st]);
+          if (!gu) tma_load_2d(tg + b * 1024, &tmG, j0 + 16 * b, (int)r0, &full[st]);
           if (HAS_T) tma_load_2d(tg + OTF_TILE + b * 1024, &tmT, j0 + 16 * b, (int)r0, &full[st]);
         }
         bulk_g2s(xs + st * OTF_BM * OTF_XW, a.xbits + r0 * OTF_XW, (uint32_t)nrows * OTF_XW * 8u, &full[st]);
@@ -244,6 +250,7 @@ __global__ void __maxnreg__(HAS_T ? 168 : 96)
     for (int e = tid; e < OTF_BJ; e += 256) {
       vb[e] = (j0 + e < h) ? a.v[a.offb + j0 + e] : 0.0;
       if (HAS_T) vu[e] = (j0 + e < h) ? a.v[a.offu + j0 + e] : 0.0;
+      if (gu) uw[e] = (j0 + e < h) ? a.u[j0 + e] : 0.0;
     }
   };
   const int ksteps = (nin + 3) / 4;
@@ -305,7 +312,13 @@ __global__ void __maxnreg__(HAS_T ? 168 : 96)
       for (int nt = 0; nt < 2; ++nt) {
         const int jl = wj * 16 + nt * 8 + (lane & 3) * 2;
         const int o = swz64(rl, jl);
-        const double2 g2 = *reinterpret_cast<const double2*>(G + o);
+        double2 g2;
+        if (HAS_T && gu) {
+          const double2 t2 = *reinterpret_cast<const double2*>(Tt + o);
+          g2 = make_double2(uw[jl] * (1.0 - t2.x * t2.x), uw[jl + 1] * (1.0 - t2.y * t2.y));
+        } else {
+          g2 = *reinterpret_cast<const double2*>(G + o);
+        }
         sacc = fma(g2.x, c[mt][nt][0], sacc);
         sacc = fma(g2.y, c[mt][nt][1], sacc);
         if (HAS_T) {
@@ -450,6 +463,9 @@ __global__ void __maxnreg__((NKT <= 8 && NY == 1 && !HAS_T) ? 96 : 168)
     }
   const int wj = warp & 3, wk = (warp >> 2) & 1;
   const int jl = wj * 16 + (lane >> 2);  // A rows jl, jl + 8 (hidden units) of this lane
+  const bool gu = HAS_T && a.u != nullptr;
+  const double u_lo = (gu && j0 + jl < h) ? a.u[j0 + jl] : 0.0;
+  const double u_hi = (gu && j0 + jl + 8 < h) ? a.u[j0 + jl + 8] : 0.0;
 
   if (warp == 8) {  // ---------------------------------------------- producer
     const double* yv_src[2] = {a.y, a.y2};
@@ -469,11 +485,11 @@ __global__ void __maxnreg__((NKT <= 8 && NY == 1 && !HAS_T) ? 96 : 168)
       }
       __syncwarp();
       if (lane == 0) {
-        mbar_arrive_expect_tx(&full[st], (uint32_t)(nbox * NM * OTF_BM * 128) + (uint32_t)nrows * OTF_XW * 8u +
-                                             (uint32_t)(NY * nev * 8));
+        mbar_arrive_expect_tx(&full[st], (uint32_t)(nbox * (gu ? 1 : NM) * OTF_BM * 128) +
+                                             (uint32_t)nrows * OTF_XW * 8u + (uint32_t)(NY * nev * 8));
         double* tg = tiles + (st * NM) * OTF_TILE;
         for (int b = 0; b < nbox; ++b) {
-          tma_load_2d(tg + b * 1024, &tmG, j0 + 16 * b, (int)r0, &full[st]);
+          if (!gu) tma_load_2d(tg + b * 1024, &tmG, j0 + 16 * b, (int)r0, &full[st]);
           if (HAS_T) tma_load_2d(tg + OTF_TILE + b * 1024, &tmT, j0 + 16 * b, (int)r0, &full[st]);
         }
         bulk_g2s(xs + st * OTF_BM * OTF_XW, a.xbits + r0 * OTF_XW, (uint32_t)nrows * OTF_XW * 8u, &full[st]);
@@ -498,11 +514,17 @@ __global__ void __maxnreg__((NKT <= 8 && NY == 1 && !HAS_T) ? 96 : 168)
       for (int kk = wk; kk < kk_end; kk += 2) {
         const int rl = kk * 4 + (lane & 3);
         const int o0 = swz64(rl, jl), o1 = swz64(rl, jl + 8);
-        const double g0 = G[o0], g1 = G[o1];
-        double t0 = 0.0, t1 = 0.0;
+        double g0, g1, t0 = 0.0, t1 = 0.0;
         if (HAS_T) {
           t0 = Tt[o0];
           t1 = Tt[o1];
+        }
+        if (HAS_T && gu) {
+          g0 = u_lo * (1.0 - t0 * t0);
+          g1 = u_hi * (1.0 - t1 * t1);
+        } else {
+          g0 = G[o0];
+          g1 = G[o1];
         }
         const uint64_t w0 = (X[rl * OTF_XW] | one0) >> sh_base, w1 = (X[rl * OTF_XW + 1] | one1) >> sh_base;
         // the row weight rides on the B operand: B = x ? y : 0 (integer selects, no FP64

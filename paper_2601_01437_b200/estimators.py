@@ -317,6 +317,15 @@ def energy_gradient(batch: SampleBatch, energy: EnergyEstimate) -> torch.Tensor:
     return 2.0 * (g.real if batch.is_complex else g)
 
 
+_OTF_FORM_G = os.environ.get("IRL_OTF_FORM_G", "1")
+
+
+def _otf_form_g(o: dict) -> bool:
+    """On-the-fly MLP product: form G = u (1 - t^2) inside the GEMM kernels
+    (irl_otf_mvp_mlp_u_f64) instead of reading the stored g."""
+    return o.get("u") is not None and _OTF_FORM_G != "0"
+
+
 def _apply(batch: SampleBatch, coeff: torch.Tensor | None, v: torch.Tensor, out: torch.Tensor, *,
            mode: int = _lib.MVP_AUTO, half_f=None, u0=None, out0=None, cache: "ConnectedCache | None" = None) -> None:
     """Raw device product on padded vectors; no validation (driver fast path).
@@ -348,7 +357,11 @@ def _apply(batch: SampleBatch, coeff: torch.Tensor | None, v: torch.Tensor, out:
                       batch.ld, _lib.ptr(obar), _lib.ptr(coeff), _lib.ptr(v), _lib.ptr(out), _lib.ptr(half_f),
                       _lib.ptr(u0), _lib.ptr(out0), _lib.ptr(ws), ws.numel(), stream)
             return
-        _lib.call("irl_otf_mvp_mlp_f64", _lib.ptr(o["xbits"]), _lib.ptr(o["t"]), _lib.ptr(o["g"]), n, o["n_in"],
+        if _otf_form_g(o):
+            fn, gv = "irl_otf_mvp_mlp_u_f64", o["u"]
+        else:
+            fn, gv = "irl_otf_mvp_mlp_f64", o["g"]
+        _lib.call(fn, _lib.ptr(o["xbits"]), _lib.ptr(o["t"]), _lib.ptr(gv), n, o["n_in"],
                   o["hidden"], batch.ld, _lib.ptr(obar), _lib.ptr(coeff), _lib.ptr(v), _lib.ptr(out),
                   _lib.ptr(half_f), _lib.ptr(u0), _lib.ptr(out0), _lib.ptr(ws), ws.numel(), stream)
         return
