@@ -678,7 +678,7 @@ unsigned fin_grid(int64_t ld) { return (unsigned)std::min<int64_t>(cdiv(ld, 32),
 struct OtfPlan {
   int jc, nb, ny;  // nb: the largest row-block count of any acc variant (workspace bound)
   int nkt, kc;     // n-tiles of the acc GEMM (k columns = n_in + ones column, padded to 8)
-  int nb_v[2][2];  // row blocks per acc variant [ny - 1][has_t]
+  int nb_v[2][3];  // row blocks per acc variant [ny - 1][0: RBM, 1: MLP (G and T), 2: MLP (G from T)]
 };
 
 // Row blocks for a (jc x nb) grid of equal CTAs: the wave count k in 1..3
@@ -754,9 +754,11 @@ AccFn pick_acc(int nkt, int nyv, bool has_t) {
   return nullptr;
 }
 
-size_t acc_smem(int nyv, bool has_t) {
+// gu: G formed from T inside the kernel (OtfArgs::u), one tile per stage
+size_t acc_smem(int nyv, bool has_t, bool gu = false) {
   const size_t st = OTF_ACC_STAGES;
-  return 1024 + (st * OTF_TILE * (has_t ? 2 : 1) + st * OTF_BM * OTF_XW + (size_t)nyv * st * OTF_BM) * 8 + 2 * st * 8;
+  return 1024 + (st * OTF_TILE * (has_t && !gu ? 2 : 1) + st * OTF_BM * OTF_XW + (size_t)nyv * st * OTF_BM) * 8 +
+         2 * st * 8;
 }
 
 int make_otf_plan_uncached(int64_t n, int n_in, int hidden, OtfPlan& p) {
@@ -771,13 +773,15 @@ int make_otf_plan_uncached(int64_t n, int n_in, int hidden, OtfPlan& p) {
   IRL_TRY(ensure_fn_attrs((const void*)k_otf_dot<true>, d.smem_optin));
   IRL_TRY(ensure_fn_attrs((const void*)k_otf_dot<false>, d.smem_optin));
   for (int nyv = 1; nyv <= 2; ++nyv)
-    for (int ht = 0; ht < 2; ++ht) {
+    for (int ht = 0; ht < 3; ++ht) {
       p.nb_v[nyv - 1][ht] = 0;
+      if (ht == 2 && nyv != 1) continue;  // G from T: product only
       AccFn f = pick_acc(p.nkt, nyv, ht != 0);
       if (!f) continue;
       IRL_TRY(ensure_fn_attrs((const void*)f, d.smem_optin));
       int occ = 0;
-      IRL_TRY(cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)f, 288, acc_smem(nyv, ht != 0)),
+      IRL_TRY(cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)f, 288,
+                                                                       acc_smem(nyv, ht != 0, ht == 2)),
                          "occ"));
       p.nb_v[nyv - 1][ht] = best_row_blocks(d.sms * std::max(occ, 1), p.jc, n);
       p.nb = std::max(p.nb, p.nb_v[nyv - 1][ht]);
@@ -852,10 +856,10 @@ int otf_check(const uint64_t* xbits, const double* t, const double* g, int64_t n
   return IRL_OK;
 }
 
-size_t otf_dot_smem(int n_in, bool has_t, bool cplx) {
+size_t otf_dot_smem(int n_in, bool has_t, bool cplx, bool gu = false) {
   const int vs = otf_vstride(n_in);
   const size_t st = OTF_DOT_STAGES;
-  const size_t tiles = st * OTF_TILE * (has_t ? 2 : 1);
+  const size_t tiles = st * OTF_TILE * (has_t && !gu ? 2 : 1);
   const size_t red = (size_t)2 * 4 * OTF_BM * (cplx ? 2 : 1);
   return 1024 + (tiles + st * OTF_BM * OTF_XW + red + 2 * st + OTF_BJ * 3 + (size_t)OTF_BJ * vs) * 8;
 }
@@ -906,9 +910,10 @@ int launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStre
 
 int otf_dot_launch(OtfArgs& a, bool has_t, cudaStream_t st) {
   const void* fn = has_t ? (const void*)k_otf_dot<true> : (const void*)k_otf_dot<false>;
-  const size_t smem = otf_dot_smem(a.n_in, has_t, false);
+  const bool gu = has_t && a.u != nullptr;
+  const size_t smem = otf_dot_smem(a.n_in, has_t, false, gu);
   int grid = 0;
-  IRL_TRY(otf_dot_grid(fn, smem, (a.n_in << 2) | (has_t ? 1 : 0), grid));
+  IRL_TRY(otf_dot_grid(fn, smem, (a.n_in << 3) | (gu ? 4 : 0) | (has_t ? 1 : 0), grid));
   CUtensorMap mg, mt;
   IRL_TRY(tile_map(mg, a.G, a.hidden, a.n_rows));
   if (has_t)
@@ -923,7 +928,8 @@ int otf_dot_launch(OtfArgs& a, bool has_t, cudaStream_t st) {
 int otf_acc_launch(const OtfPlan& pl, OtfArgs& a, cudaStream_t st, int nyv, bool has_t) {
   AccFn f = pick_acc(pl.nkt, nyv, has_t);
   if (!f) return fail(IRL_ERR_DEVICE, "no acc GEMM instance for nkt=%d ny=%d", pl.nkt, nyv);
-  a.nb = pl.nb_v[nyv - 1][has_t ? 1 : 0];
+  const bool gu = has_t && nyv == 1 && a.u != nullptr;
+  a.nb = pl.nb_v[nyv - 1][has_t ? (gu ? 2 : 1) : 0];
   dim3 grid((unsigned)pl.jc, (unsigned)a.nb);
   CUtensorMap mg, mt;
   IRL_TRY(tile_map(mg, a.G, a.hidden, a.n_rows));
@@ -931,7 +937,7 @@ int otf_acc_launch(const OtfPlan& pl, OtfArgs& a, cudaStream_t st, int nyv, bool
     IRL_TRY(tile_map(mt, a.T, a.hidden, a.n_rows));
   else
     mt = mg;
-  return launch_pdl(f, grid, dim3(288), acc_smem(nyv, has_t), st, "otf acc launch", a, mg, mt);
+  return launch_pdl(f, grid, dim3(288), acc_smem(nyv, has_t, gu), st, "otf acc launch", a, mg, mt);
 }
 
 // column statistics (obar = sum w O, grad = sum c O) of a real model from the

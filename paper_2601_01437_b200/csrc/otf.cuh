@@ -185,7 +185,10 @@ __global__ void __maxnreg__(HAS_T ? 168 : 96)
     k_otf_dot(const OtfArgs a, const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmT) {
   extern __shared__ __align__(16) unsigned char smem_o[];
   constexpr int ST = OTF_DOT_STAGES;
-  constexpr int NM = HAS_T ? 2 : 1;
+  // tiles per stage: G (+ T for the MLP); with G formed from T (a.u) only T,
+  // which then sits in the first slot -- half the shared memory, 2 CTAs per SM
+  const bool gu = HAS_T && a.u != nullptr;
+  const int NM = (HAS_T && !gu) ? 2 : 1;
   const int nin = a.n_in, vs = otf_vstride(nin);
   double* tiles = reinterpret_cast<double*>(smem_1k(smem_o));              // [ST][NM][TILE]
   uint64_t* xs = reinterpret_cast<uint64_t*>(tiles + ST * NM * OTF_TILE);  // [ST][BM][XW]
@@ -196,7 +199,6 @@ __global__ void __maxnreg__(HAS_T ? 168 : 96)
   double* vu = vb + OTF_BJ;                                                // [BJ]
   double* vw = vu + OTF_BJ;                                                // [BJ][vs]
   double* uw = vw + OTF_BJ * vs;                                           // [BJ] u chunk (gu)
-  const bool gu = HAS_T && a.u != nullptr;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t N = a.n_rows;
@@ -228,11 +230,11 @@ __global__ void __maxnreg__(HAS_T ? 168 : 96)
         const int nrows = (int)min((int64_t)OTF_BM, N - r0);
         const int j0 = jc * OTF_BJ;
         const int nbox = min(4, (h - j0 + 15) >> 4);
-        mbar_arrive_expect_tx(&full[st], (uint32_t)(nbox * (gu ? 1 : NM) * OTF_BM * 128) + (uint32_t)nrows * OTF_XW * 8u);
+        mbar_arrive_expect_tx(&full[st], (uint32_t)(nbox * NM * OTF_BM * 128) + (uint32_t)nrows * OTF_XW * 8u);
         double* tg = tiles + st * NM * OTF_TILE;
         for (int b = 0; b < nbox; ++b) {
           if (!gu) tma_load_2d(tg + b * 1024, &tmG, j0 + 16 * b, (int)r0, &full[st]);
-          if (HAS_T) tma_load_2d(tg + OTF_TILE + b * 1024, &tmT, j0 + 16 * b, (int)r0, &full[st]);
+          if (HAS_T) tma_load_2d(tg + (NM - 1) * OTF_TILE + b * 1024, &tmT, j0 + 16 * b, (int)r0, &full[st]);
         }
         bulk_g2s(xs + st * OTF_BM * OTF_XW, a.xbits + r0 * OTF_XW, (uint32_t)nrows * OTF_XW * 8u, &full[st]);
       }
@@ -267,7 +269,7 @@ __global__ void __maxnreg__(HAS_T ? 168 : 96)
     }
     mbar_wait(&full[st], (uint32_t)(k / ST) & 1u);
     const double* G = tiles + st * NM * OTF_TILE;
-    const double* Tt = G + OTF_TILE;
+    const double* Tt = G + (NM - 1) * OTF_TILE;
     const uint64_t* X = xs + st * OTF_BM * OTF_XW;
 
     // C = v_b (broadcast per column) + X V_W^T
@@ -419,8 +421,10 @@ __global__ void __maxnreg__((NKT <= 8 && NY == 1 && !HAS_T) ? 96 : 168)
     k_otf_acc(const OtfArgs a, const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmT) {
   extern __shared__ __align__(16) unsigned char smem_o[];
   constexpr int ST = OTF_ACC_STAGES;
-  constexpr int NM = HAS_T ? 2 : 1;
   constexpr int KC = 8 * NKT;
+  // G formed from T (a.u, product only): T alone per stage, in the first slot
+  const bool gu = HAS_T && NY == 1 && a.u != nullptr;
+  const int NM = (HAS_T && !gu) ? 2 : 1;
   double* tiles = reinterpret_cast<double*>(smem_1k(smem_o));                          // [ST][NM][TILE]
   uint64_t* xs = reinterpret_cast<uint64_t*>(tiles + ST * NM * OTF_TILE);              // [ST][BM][XW]
   double* ys = reinterpret_cast<double*>(xs + ST * OTF_BM * OTF_XW);                  // [ST][NY][BM]
@@ -463,7 +467,6 @@ __global__ void __maxnreg__((NKT <= 8 && NY == 1 && !HAS_T) ? 96 : 168)
     }
   const int wj = warp & 3, wk = (warp >> 2) & 1;
   const int jl = wj * 16 + (lane >> 2);  // A rows jl, jl + 8 (hidden units) of this lane
-  const bool gu = HAS_T && a.u != nullptr;
   const double u_lo = (gu && j0 + jl < h) ? a.u[j0 + jl] : 0.0;
   const double u_hi = (gu && j0 + jl + 8 < h) ? a.u[j0 + jl + 8] : 0.0;
 
@@ -485,12 +488,12 @@ __global__ void __maxnreg__((NKT <= 8 && NY == 1 && !HAS_T) ? 96 : 168)
       }
       __syncwarp();
       if (lane == 0) {
-        mbar_arrive_expect_tx(&full[st], (uint32_t)(nbox * (gu ? 1 : NM) * OTF_BM * 128) +
+        mbar_arrive_expect_tx(&full[st], (uint32_t)(nbox * NM * OTF_BM * 128) +
                                              (uint32_t)nrows * OTF_XW * 8u + (uint32_t)(NY * nev * 8));
         double* tg = tiles + (st * NM) * OTF_TILE;
         for (int b = 0; b < nbox; ++b) {
           if (!gu) tma_load_2d(tg + b * 1024, &tmG, j0 + 16 * b, (int)r0, &full[st]);
-          if (HAS_T) tma_load_2d(tg + OTF_TILE + b * 1024, &tmT, j0 + 16 * b, (int)r0, &full[st]);
+          if (HAS_T) tma_load_2d(tg + (NM - 1) * OTF_TILE + b * 1024, &tmT, j0 + 16 * b, (int)r0, &full[st]);
         }
         bulk_g2s(xs + st * OTF_BM * OTF_XW, a.xbits + r0 * OTF_XW, (uint32_t)nrows * OTF_XW * 8u, &full[st]);
       }
@@ -505,7 +508,7 @@ __global__ void __maxnreg__((NKT <= 8 && NY == 1 && !HAS_T) ? 96 : 168)
       const int st = it % ST;
       mbar_wait(&full[st], (uint32_t)(it / ST) & 1u);
       const double* G = tiles + (st * NM) * OTF_TILE;
-      const double* Tt = G + OTF_TILE;
+      const double* Tt = G + (NM - 1) * OTF_TILE;
       const uint64_t* X = xs + st * OTF_BM * OTF_XW;
       const double* Y = ys + st * NY * OTF_BM;
       // warps whose 16 hidden units all lie past h never store: skip the GEMM
@@ -553,7 +556,8 @@ __global__ void __maxnreg__((NKT <= 8 && NY == 1 && !HAS_T) ? 96 : 168)
   __syncthreads();  // every stage consumed and every copy landed: the tiles are free
   // row halves: warps 4..7 hand their fragments to warps 0..3
   constexpr int NV = NY * 2 * (NKT + (HAS_T ? 1 : 0)) * 2;
-  static_assert(NV * 128 <= ST * NM * OTF_TILE, "exchange must fit the tile buffers");
+  // (the G-from-T layout, one tile per stage, only occurs with NY == 1)
+  static_assert(NV * 128 <= ST * (HAS_T && NY != 1 ? 2 : 1) * OTF_TILE, "exchange must fit the tile buffers");
   double* xch = tiles;  // [NV][128]
   const int xl = wj * 32 + lane;
   if (warp >= 4 && warp < 8) {
