@@ -411,3 +411,31 @@ def test_auto_build_mode(pkg):
         arch = A.RBMArchitecture(cfg.n_inputs, cfg.hidden, cfg.complex_params)
         b = A.build_batch(A.AnsatzParameters(arch, inp.theta), inp.x, inp.e_loc, mode="auto")
         assert (b.otf is not None) == want_otf, idx
+
+
+@pytest.mark.parametrize("rows,n_in,hidden", [(257, 100, 130), (129, 37, 18), (2048, 20, 512)])
+def test_otf_mlp_formed_g_matches_stored_g(pkg, rows, n_in, hidden, monkeypatch):
+    """irl_otf_mvp_mlp_u_f64 (G = u (1 - t^2) formed in the GEMM kernels) ==
+    irl_otf_mvp_mlp_f64 (stored G) on the same batch, and both == the oracle."""
+    from paper_2601_01437_b200 import ansatz as A, estimators as E
+
+    rng = np.random.default_rng(3 * rows + hidden)
+    x = np.zeros((rows, n_in), dtype=np.uint8)
+    occ = np.argsort(rng.random((rows, n_in)), axis=1)[:, : n_in // 2]
+    x[np.arange(rows)[:, None], occ] = 1
+    arch = A.MLPArchitecture(n_in, hidden)
+    P = arch.param_count
+    theta = np.concatenate([rng.normal(0, np.sqrt(1 / n_in), hidden * n_in + hidden),
+                            rng.normal(0, np.sqrt(1 / hidden), hidden + 1)])
+    e = rng.normal(-10.0, 0.1, rows)
+    otf = A.build_batch_otf(A.AnsatzParameters(arch, theta), x, e)
+    en = E.estimate_energy(otf)
+    o = nqs.mlp_rows(theta, x, n_in, hidden)
+    w = np.full(rows, 1.0 / rows)
+    v = rng.standard_normal(P)
+    monkeypatch.setattr(E, "_OTF_FORM_G", "1")
+    formed = E.heff_matvec(otf, en, v)
+    monkeypatch.setattr(E, "_OTF_FORM_G", "0")
+    stored = E.heff_matvec(otf, en, v)
+    assert rel(formed, stored) < 1e-13
+    assert rel(formed, oest.heff(w, e, o, en.mean, v)) < PROD_TOL
