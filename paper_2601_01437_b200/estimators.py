@@ -485,7 +485,10 @@ def _host_product_graph(batch: SampleBatch, coeff, v: torch.Tensor, mode: int, c
         finally:
             if was:
                 gc.enable()
-        hit = (g, hin, hout, coeff, cache)  # keep coeff / cache alive with the graph
+        # the graph reads and writes these buffers on every replay: they must live
+        # as long as the graph (a freed vin / vout would be handed to other
+        # tensors by the caching allocator and overwritten by later replays)
+        hit = (g, hin, hout, coeff, cache, vin, vout, body)
         graphs[key] = hit
     g, hin, hout = hit[0], hit[1], hit[2]
     hin.copy_(v if v.dtype == torch.float64 else v.to(torch.float64))

@@ -193,3 +193,43 @@ def test_lanczos_step_kernels(cuda, L, j, stage, monkeypatch):
         assert rel(V[j + 1].cpu().numpy(), ref_v.cpu().numpy()) < 1e-12, name
         # rows 0..j untouched
         assert torch.equal(V[: j + 1], V0[: j + 1]), name
+
+
+def test_interleaved_batches_and_strided_inputs(E):
+    """Plans, workspaces and captured host-path graphs are per batch / shape:
+    alternating products on batches of different shapes and kinds stay exact;
+    strided, float32 and host inputs are accepted like numpy's matmul would."""
+    import torch
+
+    rng = np.random.default_rng(11)
+    shapes = [(700, 13, False), (4099, 260, False), (333, 21, True), (1500, 37, False)]
+    batches = []
+    for n, p, cplx in shapes:
+        o, e, w = random_batch(rng, n, p, cplx=cplx)
+        b = E.SampleBatch(None, w, e, o, n, kind="hermitian") if cplx else E.SampleBatch(None, w, e, o, n)
+        if cplx:
+            with pytest.warns(UserWarning):
+                en = E.estimate_energy(b)
+        else:
+            en = E.estimate_energy(b)
+        batches.append((b, en, o, e, w, p, cplx))
+    for rep in range(3):
+        for b, en, o, e, w, p, cplx in batches:
+            if cplx:
+                v = rng.standard_normal(p) + 1j * rng.standard_normal(p)
+                ref = oest.heff_hermitian(w, e, o, en.mean, v)
+                got = E.heff_matvec(b, en, torch.as_tensor(v, device="cuda"))
+                again = E.heff_matvec(b, en, torch.as_tensor(v).pin_memory())
+                assert rel(got.cpu().numpy(), again.numpy()) < 1e-14
+                assert rel(got.cpu().numpy(), ref) < 1e-10
+                continue
+            v = rng.standard_normal(p)
+            ref = oest.heff(w, e, o, en.mean, v)
+            big = torch.zeros(2 * p, dtype=torch.float64, device="cuda")
+            big[::2] = torch.as_tensor(v, device="cuda")
+            strided = big[::2]  # non-contiguous device view
+            assert rel(E.heff_matvec(b, en, strided).cpu().numpy(), ref) < 1e-10
+            assert rel(E.heff_matvec(b, en, torch.as_tensor(v).pin_memory()).numpy(), ref) < 1e-10
+            v32 = v.astype(np.float32)
+            ref32 = oest.heff(w, e, o, en.mean, v32.astype(np.float64))
+            assert rel(np.asarray(E.heff_matvec(b, en, v32)), ref32) < 1e-10
