@@ -233,3 +233,47 @@ def test_interleaved_batches_and_strided_inputs(E):
             v32 = v.astype(np.float32)
             ref32 = oest.heff(w, e, o, en.mean, v32.astype(np.float64))
             assert rel(np.asarray(E.heff_matvec(b, en, v32)), ref32) < 1e-10
+
+
+def test_interleaved_solves_are_bitwise_stable(E):
+    """IRL solves and products on several batches (stored and on-the-fly, RBM
+    and MLP, host and device vectors) in turn give bit-identical results to
+    each batch's first, isolated call: no cached plan, workspace, staging
+    buffer or captured graph leaks between batches."""
+    import torch
+
+    from paper_2601_01437_b200 import ansatz as A, optimizer as OPT
+
+    rng = np.random.default_rng(5)
+
+    def bits(n, k, rows):
+        x = np.zeros((rows, n), dtype=np.uint8)
+        occ = np.argsort(rng.random((rows, n)), axis=1)[:, :k]
+        x[np.arange(rows)[:, None], occ] = 1
+        return x
+
+    specs = [("rbm", 12, 24, 900, "stored"), ("mlp", 10, 64, 1300, "otf"), ("rbm", 16, 40, 2100, "otf"),
+             ("mlp", 14, 30, 700, "stored")]
+    cases = []
+    for model, n, h, rows, mode in specs:
+        arch = A.RBMArchitecture(n, h) if model == "rbm" else A.MLPArchitecture(n, h)
+        theta = rng.normal(0, 0.05, arch.param_count)
+        x = bits(n, n // 2, rows)
+        e = rng.normal(-5.0, 0.1, rows)
+        b = A.build_batch(A.AnsatzParameters(arch, theta), x, e, mode=mode)
+        en = E.estimate_energy(b)
+        v = rng.standard_normal(arch.param_count)
+        cases.append((b, en, v))
+    conf = OPT.OptimizerConfig(m=12, max_restarts=2)
+    first = []
+    for b, en, v in cases:
+        r = OPT.solve_step(b, conf, seed=1, energy=en)
+        first.append((E.heff_matvec(b, en, torch.as_tensor(v).pin_memory()).clone(),
+                      E.qgt_matvec(b, torch.as_tensor(v, device="cuda")).cpu(), r.lambda_min,
+                      r.direction.cpu().clone()))
+    for _ in range(2):
+        for (b, en, v), (h0, s0, lam0, d0) in zip(cases[::-1], first[::-1]):
+            r = OPT.solve_step(b, conf, seed=1, energy=en)
+            assert r.lambda_min == lam0 and torch.equal(r.direction.cpu(), d0)
+            assert torch.equal(E.heff_matvec(b, en, torch.as_tensor(v).pin_memory()), h0)
+            assert torch.equal(E.qgt_matvec(b, torch.as_tensor(v, device="cuda")).cpu(), s0)
