@@ -283,11 +283,15 @@ __global__ void __maxnreg__(HAS_T ? 168 : 96)
         c[mt][nt][1] = vb[jl + 1];
       }
     }
+    // m-tile mt holds tile rows wr*32 + mt + 4 i (i = lane >> 2): the 8 lanes of a
+    // quarter-warp then read rows of both parities, so the 128-byte TMA swizzle
+    // (chunk ^ row % 8) spreads their epilogue LDS.128 over all 8 chunks (the
+    // consecutive-row mapping hit 4 chunks twice: 2-way bank conflicts)
     uint64_t xr[4][OTF_XW];
 #pragma unroll
     for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-      for (int q = 0; q < OTF_XW; ++q) xr[mt][q] = X[(wr * 32 + mt * 8 + (lane >> 2)) * OTF_XW + q];
+      for (int q = 0; q < OTF_XW; ++q) xr[mt][q] = X[(wr * 32 + mt + 4 * (lane >> 2)) * OTF_XW + q];
     const double* vrow0 = vw + (wj * 16 + (lane >> 2)) * vs + (lane & 3);
     // a warp whose 16 hidden units all lie past h (tail chunk, e.g. h = 160)
     // skips its GEMM: c stays v_b = 0 there and meets zero v_u
@@ -308,7 +312,7 @@ __global__ void __maxnreg__(HAS_T ? 168 : 96)
     double rs[4];
 #pragma unroll
     for (int mt = 0; mt < 4; ++mt) {
-      const int rl = wr * 32 + mt * 8 + (lane >> 2);
+      const int rl = wr * 32 + mt + 4 * (lane >> 2);
       double sacc = 0.0;
 #pragma unroll
       for (int nt = 0; nt < 2; ++nt) {
@@ -338,7 +342,7 @@ __global__ void __maxnreg__(HAS_T ? 168 : 96)
     double* rd = red + (k & 1) * 4 * OTF_BM;
     if ((lane & 3) == 0) {
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt) rd[wj * OTF_BM + wr * 32 + mt * 8 + (lane >> 2)] = rs[mt];
+      for (int mt = 0; mt < 4; ++mt) rd[wj * OTF_BM + wr * 32 + mt + 4 * (lane >> 2)] = rs[mt];
     }
     named_bar_sync(1, 256);
     if (tid < OTF_BM) {
@@ -1061,7 +1065,7 @@ __global__ void __maxnreg__(96) k_otf_dot_c(const OtfCArgs a,
 #pragma unroll
     for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-      for (int q = 0; q < OTF_XW; ++q) xr[mt][q] = X[(wr * 32 + mt * 8 + (lane >> 2)) * OTF_XW + q];
+      for (int q = 0; q < OTF_XW; ++q) xr[mt][q] = X[(wr * 32 + mt + 4 * (lane >> 2)) * OTF_XW + q];
     const double* vrow0 = vw + (wj * 16 + (lane >> 2)) * vs + (lane & 3);
     for (int kk = 0; kk < ksteps; ++kk) {
       const int kq = kk * 4 + (lane & 3);
@@ -1079,7 +1083,7 @@ __global__ void __maxnreg__(96) k_otf_dot_c(const OtfCArgs a,
     double2 rs[4];
 #pragma unroll
     for (int mt = 0; mt < 4; ++mt) {
-      const int rl = wr * 32 + mt * 8 + (lane >> 2);
+      const int rl = wr * 32 + mt + 4 * (lane >> 2);
       double sre = 0.0, sim = 0.0;
 #pragma unroll
       for (int nt = 0; nt < 2; ++nt) {
@@ -1101,7 +1105,7 @@ __global__ void __maxnreg__(96) k_otf_dot_c(const OtfCArgs a,
     double2* rd = red + (k & 1) * 4 * OTF_BM;
     if ((lane & 3) == 0) {
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt) rd[wj * OTF_BM + wr * 32 + mt * 8 + (lane >> 2)] = rs[mt];
+      for (int mt = 0; mt < 4; ++mt) rd[wj * OTF_BM + wr * 32 + mt + 4 * (lane >> 2)] = rs[mt];
     }
     named_bar_sync(1, 256);
     if (tid < OTF_BM) {
