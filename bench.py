@@ -411,16 +411,20 @@ def run_ours(args):
         oo = torch.empty((2, ld), dtype=torch.float64, device=dev)
         for _ in range(3):
             E._apply(ob, co_h, vo[0], oo[0])
+        # the activations (cfg2: T = 84 MB) would stay L2-resident between steps:
+        # write a 256 MB buffer before every step and time only the two products
+        l2buf = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
         torch.cuda.synchronize()
-        o0 = torch.cuda.Event(enable_timing=True)
-        o1 = torch.cuda.Event(enable_timing=True)
-        o0.record()
+        oe = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
         for k in range(args.steps):
+            l2buf.fill_(float(k))
+            oe[k][0].record(stream)
             E._apply(ob, co_h, vo[k % 2], oo[0])
             E._apply(ob, co_s, vo[(k + 1) % 2], oo[1])
-        o1.record()
+            oe[k][1].record(stream)
         torch.cuda.synchronize()
-        otf_s = o0.elapsed_time(o1) / 1e3
+        otf_s = sum(a.elapsed_time(b) for a, b in oe) / 1e3
+        del l2buf
         conf = OPT.OptimizerConfig(m=cfg.m, max_restarts=cfg.max_restarts)
         OPT.solve_step(ob, conf, seed=cfg.lanczos_seed, energy=eo)
         torch.cuda.synchronize()
@@ -429,6 +433,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         otf = {"value": 2 * args.steps / otf_s, "unit": UNIT, "irl_wall_ms": (time.perf_counter() - i0) * 1e3,
                "n_matvec": ro.n_matvec, "lambda_min": ro.lambda_min,
+               "l2": "256 MB write before every step (the hidden activations fit in L2)",
                "note": "O regenerated inside every product from packed inputs + hidden activations (DMMA GEMMs); "
                        "not the headline: BASELINE cfg2 stores O in HBM"}
         del ob
