@@ -277,3 +277,60 @@ def test_interleaved_solves_are_bitwise_stable(E):
             assert r.lambda_min == lam0 and torch.equal(r.direction.cpu(), d0)
             assert torch.equal(E.heff_matvec(b, en, torch.as_tensor(v).pin_memory()), h0)
             assert torch.equal(E.qgt_matvec(b, torch.as_tensor(v, device="cuda")).cpu(), s0)
+
+
+@pytest.mark.parametrize("kind", ["real", "complex_raw", "hermitian", "otf_rbm", "otf_mlp", "otf_herm"])
+def test_workspace_and_output_canaries(E, kind):
+    """Kernels stay inside the caller's buffers (the ABI's ownership rule): the
+    workspace is handed over at exactly *_workspace_bytes() with a guard region
+    behind it, outputs are views followed by guard words; every product path
+    must leave the guards untouched.  (compute-sanitizer is not available on the
+    GPU pool; this is the bounds check of our own.)"""
+    import torch
+
+    from paper_2601_01437_b200 import _lib, ansatz as A
+
+    rng = np.random.default_rng(len(kind))
+    guard = 1 << 20
+    if kind.startswith("otf"):
+        n_in, hidden, rows = (37, 130, 517) if kind == "otf_mlp" else (12, 72, 611)
+        x = np.zeros((rows, n_in), dtype=np.uint8)
+        occ = np.argsort(rng.random((rows, n_in)), axis=1)[:, : n_in // 2]
+        x[np.arange(rows)[:, None], occ] = 1
+        arch = (A.MLPArchitecture(n_in, hidden) if kind == "otf_mlp"
+                else A.RBMArchitecture(n_in, hidden, kind == "otf_herm"))
+        theta = rng.normal(0, 0.05, arch.param_count)
+        if kind == "otf_herm":
+            theta = theta + 1j * rng.normal(0, 0.05, arch.param_count)
+        b = A.build_batch_otf(A.AnsatzParameters(arch, theta), x, rng.normal(-3, 0.1, rows))
+        modes = [0]
+    else:
+        o, e, w = random_batch(rng, 2311, 301, cplx=kind != "real")
+        b = (E.SampleBatch(None, w, e, o, 2311, kind="hermitian") if kind == "hermitian"
+             else E.SampleBatch(None, w, e, o, 2311))
+        modes = [1, 2, 3, 4]
+    import warnings
+
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        en = E.estimate_energy(b)
+    nbytes = b.mvp_workspace().numel()
+    big = torch.full((nbytes + guard,), 0xA5, dtype=torch.uint8, device="cuda")
+    b._ws = big[:nbytes]
+    ld, p = b.ld, b.param_count
+    herm = b.kind == E.KIND_HERMITIAN
+    rows_v = 2 if herm else 1
+    vin = torch.zeros((rows_v, ld), dtype=torch.float64, device="cuda")
+    vin[:, :p] = torch.as_tensor(rng.standard_normal((rows_v, p)), device="cuda")
+    outbuf = torch.full((rows_v, ld + 64), 7.25, dtype=torch.float64, device="cuda")
+    coeff = b.coefficients(en.mean)
+    for mode in modes:
+        if mode == 3 and ld // (1 if b.is_complex else 2) > 512:
+            continue
+        if herm:
+            E._apply(b, coeff, (vin[0], vin[1]), (outbuf[0, :ld], outbuf[1, :ld]), mode=mode)
+        else:
+            E._apply(b, coeff, vin[0], outbuf[0, :ld], mode=mode)
+        torch.cuda.synchronize()
+        assert bool((big[nbytes:] == 0xA5).all()), f"workspace overrun, mode {mode}"
+        assert bool((outbuf[:, ld:] == 7.25).all()), f"output overrun, mode {mode}"
