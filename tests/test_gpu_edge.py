@@ -334,3 +334,35 @@ def test_workspace_and_output_canaries(E, kind):
         torch.cuda.synchronize()
         assert bool((big[nbytes:] == 0xA5).all()), f"workspace overrun, mode {mode}"
         assert bool((outbuf[:, ld:] == 7.25).all()), f"output overrun, mode {mode}"
+
+
+@pytest.mark.parametrize("model,n_in,hidden,rows,cplx", [("rbm", 12, 24, 1001, False), ("mlp", 37, 130, 517, False),
+                                                          ("rbm", 10, 30, 333, True), ("mlp", 100, 512, 70, False)])
+def test_obuild_output_canaries(E, model, n_in, hidden, rows, cplx):
+    """The O-row writers (column tiles and row sweeps) and their fused
+    statistics write exactly N x ld of O and ld entries of Obar / F."""
+    import torch
+
+    from paper_2601_01437_b200 import _lib, ansatz as A
+
+    rng = np.random.default_rng(rows)
+    x = np.zeros((rows, n_in), dtype=np.uint8)
+    occ = np.argsort(rng.random((rows, n_in)), axis=1)[:, : n_in // 2]
+    x[np.arange(rows)[:, None], occ] = 1
+    arch = A.MLPArchitecture(n_in, hidden) if model == "mlp" else A.RBMArchitecture(n_in, hidden, cplx)
+    theta = rng.normal(0, 0.05, arch.param_count) + (1j * rng.normal(0, 0.05, arch.param_count) if cplx else 0)
+    params = A.AnsatzParameters(arch, theta)
+    ref = A.build_batch(params, x, rng.normal(-3, 0.1, rows))
+    ld = ref.ld
+    odt = torch.complex128 if cplx else torch.float64
+    guard = 4096
+    mark = complex(7.25, -3.5) if cplx else 7.25
+    obig = torch.full((rows * ld + guard,), mark, dtype=odt, device="cuda")
+    sbig = torch.full((2, ld + guard), mark, dtype=odt, device="cuda")
+    o = obig[: rows * ld].view(rows, ld)
+    xt = A._x_device(x, n_in, torch.device("cuda"))
+    A.fill_o_rows(params, xt, o, ref.weights, ref.gradient_coefficients(ref._stats_e), sbig[0, :ld], sbig[1, :ld])
+    torch.cuda.synchronize()
+    assert bool((obig[rows * ld:] == mark).all()), "O overrun"
+    assert bool((sbig[:, ld:] == mark).all()), "statistics overrun"
+    assert torch.equal(o[:, : ref.param_count], ref.o_matrix[:, : ref.param_count])
