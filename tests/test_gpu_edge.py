@@ -366,3 +366,31 @@ def test_obuild_output_canaries(E, model, n_in, hidden, rows, cplx):
     assert bool((obig[rows * ld:] == mark).all()), "O overrun"
     assert bool((sbig[:, ld:] == mark).all()), "statistics overrun"
     assert torch.equal(o[:, : ref.param_count], ref.o_matrix[:, : ref.param_count])
+
+
+@pytest.mark.parametrize("mode", ["stored", "otf"])
+def test_connected_workspace_canary(E, mode):
+    """The connected completion (partner dots, per-row CSR, additive row term)
+    stays inside its cache workspace."""
+    import torch
+
+    from paper_2601_01437_b200 import ansatz as A, synthetic as S
+
+    cfg = S.CONFIGS[1].with_rows(777)
+    inp = S.make_inputs(cfg)
+    arch = A.RBMArchitecture(cfg.n_inputs, cfg.hidden)
+    params = A.AnsatzParameters(arch, inp.theta)
+    batch = A.build_batch(params, inp.x, inp.e_loc, mode=mode)
+    en = E.estimate_energy(batch)
+    partners, elements, indptr, dist = S.connected_partners(inp.x, 3, seed=9)
+    cache = A.build_connected_cache(params, batch, inp.x, partners, elements, indptr, dist_index=dist)
+    v = np.random.default_rng(4).standard_normal(arch.param_count)
+    ref = np.asarray(E.connected_heff_matvec(batch, en, cache, v))
+    nbytes = cache.workspace(batch).numel()
+    guard = 1 << 20
+    big = torch.full((nbytes + guard,), 0x5A, dtype=torch.uint8, device="cuda")
+    cache._ws = big[:nbytes]
+    got = np.asarray(E.connected_heff_matvec(batch, en, cache, v))
+    torch.cuda.synchronize()
+    assert bool((big[nbytes:] == 0x5A).all()), "connected workspace overrun"
+    assert np.array_equal(got, ref)
