@@ -481,7 +481,7 @@ int make_wide_plan(int64_t n, int64_t ld_u, bool cplx, WidePlan& p) {
   p.NS = (int)std::min<int64_t>(16, (int64_t)((budget - fixed) / ((size_t)p.RB * p.WM * 16 + 16)));
   if (p.NS < 2) return fail(IRL_ERR_DEVICE, "wide path: row slices too wide for the ring");
   p.smem = (size_t)p.NS * p.RB * p.WM * 16 + (size_t)2 * p.NS * 8 + fixed;
-  p.ws = align256((size_t)3 * p.R * p.G * sS) + align256((size_t)p.G * 8) + 256;
+  p.ws = align256((size_t)4 * p.R * p.G * sS) + align256((size_t)p.G * 8) + 256 + align256((size_t)cdiv(n, p.R) * 4);
   return IRL_OK;
 }
 
@@ -493,16 +493,17 @@ int launch_wide(const WidePlan& p, bool cplx, WideArgs a, void* ws, cudaStream_t
   char* base = static_cast<char*>(ws);
   const size_t sS = cplx ? 16 : 8;
   a.tpart = base;
-  size_t off = align256((size_t)3 * p.R * p.G * sS);
+  size_t off = align256((size_t)4 * p.R * p.G * sS);
   a.gpart = reinterpret_cast<double*>(base + off);
   off += align256((size_t)p.G * 8);
-  a.counter = reinterpret_cast<unsigned int*>(base + off);
-  a.error = reinterpret_cast<int*>(base + off + 4);
+  a.error = reinterpret_cast<int*>(base + off);
+  a.counter = reinterpret_cast<unsigned int*>(base + off + 256);  // [NB] per-block arrivals
+  const size_t nblk = (size_t)cdiv(a.n_rows, p.R);
   a.R = p.R;
   a.NS = p.NS;
   a.RB = p.RB;
   a.WM = p.WM;
-  IRL_TRY(cuda_check(cudaMemsetAsync(a.counter, 0, 8, st), "wide counter reset"));
+  IRL_TRY(cuda_check(cudaMemsetAsync(a.error, 0, 256 + nblk * 4, st), "wide counter reset"));
   int occ = 0;
   IRL_TRY(cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)fn, WIDE_NT + 32, p.smem), "occ"));
   if (occ < 1) return fail(IRL_ERR_DEVICE, "wide kernel does not fit on an SM");

@@ -9,7 +9,7 @@
 //     slice of the output needs no cross-CTA reduction at all;
 //   * rows go in blocks of R (~30 MB per block).  Phase D(b): stream the slice
 //     of block b through a TMA ring, per-row partial dots (minus the slice's
-//     share of Obar.v) -> tpart[b % 3][r][c]; arrive on a grid counter.
+//     share of Obar.v) -> tpart[b % 4][r][c]; arrive on block b's counter.
 //   * Phase A(b), one block later: wait until all G CTAs have arrived for b,
 //     every CTA forms y_r = c_r sum_c tpart[..][r][c] in the same fixed order,
 //     then streams its slice of block b again -- now from L2, the block was
@@ -17,9 +17,13 @@
 //
 // The producer warp streams D(0), D(1), A(0), D(2), A(1), ..., so the barrier
 // of block b is hidden behind D(b+1) and the ring keeps prefetching A(b) while
-// consumers wait.  HBM reads O once; L2 serves the second pass.  tpart is
-// triple-buffered: a CTA can only overwrite block b's partials after every CTA
-// has finished A(b) (they arrived for b+2).  All sums are fixed-order.
+// consumers wait.  HBM reads O once; L2 serves the second pass.  Each block
+// has its own arrival counter (a shared running total could be satisfied by a
+// fast CTA's later arrivals while a slow CTA had not yet published block b).
+// tpart has four buffers: a CTA writes block b+1's partials (into b-3's
+// buffer) only after its A(b-1), i.e. after every CTA arrived for b-1 and so
+// finished A(b-3); with three buffers a slow CTA could still be reading A(b-2)
+// (seen as a rare 1e-7 error on cfg5).  All sums are fixed-order.
 #pragma once
 #include "stream.cuh"
 
@@ -42,9 +46,9 @@ struct WideArgs {
   double* out_re;
   double* out_im;
   double* out0;
-  void* tpart;              // S[3][R][G]
+  void* tpart;              // S[4][R][G]
   double* gpart;            // [G]
-  unsigned int* counter;    // zero at launch
+  unsigned int* counter;    // [NB] per-block arrival counters, zero at launch
   int* error;               // set on a barrier timeout (never expected)
   int R;                    // rows per block
   int NS;                   // ring stages
@@ -192,7 +196,7 @@ __global__ void __launch_bounds__(WIDE_NT + 32, 1) k_wide(const WideArgs a) {
   auto phase_d = [&](int b) {
     const int64_t r0 = (int64_t)b * R;
     const int rows = (int)min((int64_t)R, N - r0);
-    S* tp = tpart + ((size_t)(b % 3) * R) * G;
+    S* tp = tpart + ((size_t)(b & 3) * R) * G;
     for (int r = 0; r < rows; r += RB) {
       mbar_wait_bounded(&full[s], ph, a.error);
       // this warp's rows of the stage: warp, warp + NW (rpw <= 2); two partial
@@ -225,16 +229,19 @@ __global__ void __launch_bounds__(WIDE_NT + 32, 1) k_wide(const WideArgs a) {
       advance();
     }
     named_bar_sync(1, WIDE_NT);  // every warp's partials written
-    if (tid == 0) red_release_add(a.counter, 1u);
+    if (tid == 0) red_release_add(a.counter + b, 1u);
   };
 
   auto phase_a = [&](int b) {
     const int64_t r0 = (int64_t)b * R;
     const int rows = (int)min((int64_t)R, N - r0);
     if (tid == 0) {  // wait until every CTA has published block b
-      const unsigned int target = (unsigned int)G * (unsigned int)(b + 1);
+      // one counter per block: a single running total could reach G (b + 1)
+      // with a fast CTA's later arrivals standing in for a slow CTA's missing
+      // one, and block b's partials would be read before they were all written
+      const unsigned int target = (unsigned int)G;
       const long long t0 = clock64();
-      while (ld_acquire_u32(a.counter) < target) {
+      while (ld_acquire_u32(a.counter + b) < target) {
         if (clock64() - t0 > (1LL << 36)) {  // ~30 s: never expected; no hang
           atomicExch(a.error, 1);
           break;
@@ -242,7 +249,7 @@ __global__ void __launch_bounds__(WIDE_NT + 32, 1) k_wide(const WideArgs a) {
       }
     }
     named_bar_sync(1, WIDE_NT);
-    const S* tp = tpart + ((size_t)(b % 3) * R) * G;
+    const S* tp = tpart + ((size_t)(b & 3) * R) * G;
     // 4 rows per warp at a time: their partial loads are independent (in flight together)
     for (int r = warp * 4; r < rows; r += WIDE_NW * 4) {
       S t[4];

@@ -394,3 +394,25 @@ def test_connected_workspace_canary(E, mode):
     torch.cuda.synchronize()
     assert bool((big[nbytes:] == 0x5A).all()), "connected workspace overrun"
     assert np.array_equal(got, ref)
+
+
+def test_wide_path_many_blocks_bitwise_stable(E):
+    """The single-read wide path (IRL_MVP_WIDE) synchronises its persistent
+    grid once per row block through per-block counters and a 4-deep partials
+    buffer; with many blocks, repeated products must be bit-identical and match
+    the oracle (a missed arrival shows up as a small, varying error)."""
+    import torch
+
+    from paper_2601_01437_b200 import ansatz as A, synthetic as S
+
+    cfg = S.CONFIGS[5].with_rows(1536)
+    inp = S.make_inputs(cfg)
+    arch = A.MLPArchitecture(cfg.n_inputs, cfg.hidden)
+    b = A.build_batch(A.AnsatzParameters(arch, inp.theta), inp.x, inp.e_loc)
+    en = E.estimate_energy(b)
+    v = torch.as_tensor(np.random.default_rng(8).standard_normal(arch.param_count), device="cuda")
+    first = E.heff_matvec(b, en, v, mode=4)
+    two = E.heff_matvec(b, en, v, mode=2)
+    assert rel(first.cpu().numpy(), two.cpu().numpy()) < 1e-12
+    for _ in range(12):
+        assert torch.equal(E.heff_matvec(b, en, v, mode=4), first)
