@@ -416,3 +416,31 @@ def test_wide_path_many_blocks_bitwise_stable(E):
     assert rel(first.cpu().numpy(), two.cpu().numpy()) < 1e-12
     for _ in range(12):
         assert torch.equal(E.heff_matvec(b, en, v, mode=4), first)
+
+
+def test_two_streams_two_batches(E):
+    """Re-entrancy (include/irl_sr.h: every entry takes a stream, no global
+    mutable state): products on two batches issued alternately on two CUDA
+    streams without host synchronisation equal the serial results bit for bit."""
+    import torch
+
+    rng = np.random.default_rng(21)
+    cases = []
+    for n, p in ((3001, 157), (2048, 611)):
+        o, e, w = random_batch(rng, n, p)
+        b = E.SampleBatch(None, w, e, o, n)
+        en = E.estimate_energy(b)
+        vs = [torch.as_tensor(rng.standard_normal(p), device="cuda") for _ in range(4)]
+        cases.append((b, en, vs))
+    serial = [[E.heff_matvec(b, en, v).clone() for v in vs] for b, en, vs in cases]
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = [[None] * 4, [None] * 4]
+    for k in range(4):
+        for i, (b, en, vs) in enumerate(cases):
+            with torch.cuda.stream(streams[i]):
+                outs[i][k] = E.heff_matvec(b, en, vs[k])
+    torch.cuda.synchronize()
+    for i in range(2):
+        for k in range(4):
+            assert torch.equal(outs[i][k], serial[i][k])
