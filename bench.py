@@ -293,7 +293,7 @@ def run_ours(args):
     ob0 = torch.cuda.Event(enable_timing=True)
     ob1 = torch.cuda.Event(enable_timing=True)
     ob0.record()
-    A.fill_o_rows(params, xt, batch.o_matrix, batch.weights, ob_c, ob_bar, ob_g)
+    A.fill_o_rows(params, xt, batch.o_padded, batch.weights, ob_c, ob_bar, ob_g)
     ob1.record()
     torch.cuda.synchronize()
     obuild_ms = ob0.elapsed_time(ob1)

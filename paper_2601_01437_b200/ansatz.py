@@ -274,7 +274,7 @@ def build_batch_otf(params: AnsatzParameters, x, e_loc, weights=None, n_samples:
     batch = SampleBatch.__new__(SampleBatch)
     SampleBatch._init_common(batch, weights, e_loc, n, n_samples or 0, KIND_HERMITIAN if cplx else KIND_REAL, p, ld,
                              dev)
-    batch.o_matrix = placeholder
+    batch.o_padded = placeholder
     xbits = torch.empty((n, 2), dtype=torch.int64, device=dev)
     t = torch.empty((n, arch.hidden), dtype=odt, device=dev)
     theta = _theta_device(params, dev)
@@ -296,6 +296,7 @@ def build_batch_otf(params: AnsatzParameters, x, e_loc, weights=None, n_samples:
         # can form G = u (1 - t^2) from t instead of reading g
         off = arch.hidden * arch.n_in + arch.hidden
         batch.otf["u"] = theta[off:off + arch.hidden].contiguous()
+    batch._seal()
     return batch
 
 

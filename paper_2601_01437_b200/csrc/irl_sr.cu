@@ -6,6 +6,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <set>
 #include <string>
 #include <unordered_map>
 #include <unordered_set>
@@ -77,11 +78,16 @@ int dev_info(DevInfo& d) {
   return IRL_OK;
 }
 
+// Function attributes are per device: the cache is keyed by (device, function)
+// so a process that launches on a second GPU sets them there too.
 int ensure_fn_attrs(const void* fn, int smem_optin) {
   static std::mutex mu;
-  static std::unordered_set<const void*> done;
+  static std::set<std::pair<int, const void*>> done;
+  int dev = 0;
+  IRL_TRY(cuda_check(cudaGetDevice(&dev), "cudaGetDevice"));
+  const std::pair<int, const void*> key(dev, fn);
   std::lock_guard<std::mutex> lk(mu);
-  if (done.count(fn)) return IRL_OK;
+  if (done.count(key)) return IRL_OK;
   cudaFuncAttributes fa;
   IRL_TRY(cuda_check(cudaFuncGetAttributes(&fa, fn), "cudaFuncGetAttributes"));
   // dynamic + static shared memory must fit the opt-in limit
@@ -91,7 +97,7 @@ int ensure_fn_attrs(const void* fn, int smem_optin) {
   // cluster size 16 is non-portable; harmless for non-cluster launches
   cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaGetLastError();
-  done.insert(fn);
+  done.insert(key);
   return IRL_OK;
 }
 
@@ -2306,21 +2312,13 @@ int irl_lanczos_step_cluster(double* V, int64_t ldv, double* W, int64_t L, int j
     return fail(IRL_ERR_ARG, "bad lanczos step");
   DevInfo d;
   IRL_TRY(dev_info(d));
-  static std::once_flag once;  // static shared memory only; allow 16-CTA clusters
-  std::call_once(once, [] { cudaFuncSetAttribute((const void*)k_lanczos_cluster,
-                                                 cudaFuncAttributeNonPortableClusterSizeAllowed, 1); });
-  cudaGetLastError();
+  // static shared memory only; allow 16-CTA clusters (per device, via ensure_fn_attrs)
+  IRL_TRY(ensure_fn_attrs((const void*)k_lanczos_cluster, d.smem_optin));
   const int cs = (int)std::min<int64_t>(16, std::max<int64_t>(2, cdiv(L, 512)));
   // shared-memory staged variant when this CTA's slice of rows 0..j (+ W) fits
   const int64_t slice = 2 * cdiv(L / 2, cs);
   const size_t stage_bytes = (size_t)(j + 2) * slice * 8;
-  static std::once_flag once_s;
-  std::call_once(once_s, [&] {
-    cudaFuncSetAttribute((const void*)k_lanczos_cluster_smem, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute((const void*)k_lanczos_cluster_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         d.smem_optin - 4096);
-  });
-  cudaGetLastError();
+  IRL_TRY(ensure_fn_attrs((const void*)k_lanczos_cluster_smem, d.smem_optin));
   const bool staged = (L % 2 == 0) && (ldv % 2 == 0) && aligned16(V) && aligned16(W) &&
                       stage_bytes + 4096 <= (size_t)d.smem_optin && getenv("IRL_LANCZOS_NOSTAGE") == nullptr;
   cudaLaunchConfig_t cfg = {};

@@ -51,10 +51,12 @@ __global__ void __launch_bounds__(RowsGeom<UPL>::NW * 32, RowsGeom<UPL>::MINB) k
       if (yadd) d = yadd[r];
     }
     const double2* orow = a.O + r * ld_u + lane;
-    // units read per lane: all 32 UPL except on the last row (units past ld_u
-    // read into the next row -- finite O entries -- and meet v = 0 in the dot;
-    // their accumulators are never stored); none past the last row
-    const int lim = (r + 1 < a.n_rows) ? 32 * UPL : (r < a.n_rows ? (int)ld_u : 0);
+    // units read per lane: up to 32 UPL (units past ld_u read into the
+    // following rows -- finite O entries -- and meet v = 0 in the dot; their
+    // accumulators are never stored), but never past the end of the last row:
+    // O may sit at the very end of the caller's allocation
+    const int64_t left = (r < a.n_rows) ? (a.n_rows - r) * ld_u : 0;
+    const int lim = (int)min((int64_t)(32 * UPL), left);
 #pragma unroll
     for (int k = 0; k < UPL; ++k) o[k] = (lane + 32 * k < lim) ? __ldg(orow + 32 * k) : make_double2(0.0, 0.0);
   };

@@ -3,9 +3,11 @@
 Mirrors the reference entry points on the hot path:
 
 * :class:`SampleBatch` — ``estimators.py:30-61`` (same constructor and
-  validation: shapes, ``w >= 0``, ``sum w = 1 +- 1e-12``), but the caches
-  live in HBM: ``o_matrix`` is an N x ld row-major device tensor with a
-  padded leading dimension (``irl_padded_ld``), padding columns zero.
+  validation: shapes, ``w >= 0``, ``sum w = 1 +- 1e-12``; frozen fields as
+  the reference's frozen dataclass), but the caches live in HBM: the kernels
+  stream ``o_padded``, an N x ld row-major device tensor with a padded leading
+  dimension (``irl_padded_ld``, padding columns zero); ``o_matrix`` is its
+  (N, P) view, so ``o_matrix.shape[1] == param_count`` as in ``est:55-57``.
 * :func:`estimate_energy`   — ``estimators.py:146-153``  (k_energy)
 * :func:`energy_gradient`   — ``estimators.py:156-163``  (fused column stats)
 * :func:`heff_matvec`       — ``estimators.py:171-186``  (single-pass fused MVP)
@@ -113,7 +115,28 @@ class SampleBatch:
             o = torch.zeros((n, ld), dtype=cdt, device=dev)
             o[:, :p] = _as_tensor(o_matrix, cdt, dev)
         self.configs = tuple(configs) if configs is not None else None
-        self.o_matrix = o
+        self.o_padded = o
+        self._seal()
+
+    # est:30 is a frozen dataclass: its fields cannot be rebound after
+    # construction (dataclasses.FrozenInstanceError).  The device caches below
+    # are private and keep being filled lazily.
+    _FROZEN = ("configs", "weights", "e_loc", "o_matrix", "o_padded", "n_samples", "kind", "otf")
+
+    def _seal(self) -> None:
+        object.__setattr__(self, "_sealed", True)
+
+    def __setattr__(self, name, value):
+        if name in SampleBatch._FROZEN and self.__dict__.get("_sealed"):
+            import dataclasses
+
+            raise dataclasses.FrozenInstanceError(f"cannot assign to field {name!r}")
+        object.__setattr__(self, name, value)
+
+    @property
+    def o_matrix(self) -> torch.Tensor:
+        """The (N, P) log-derivative matrix (est:33): a view of the padded device buffer."""
+        return self.o_padded[:, : self._p]
 
     def _init_common(self, weights, e_loc, n, n_samples, kind, p, ld, dev) -> None:
         """Weights / E_loc validation of est:44-53 and the device caches."""
@@ -141,7 +164,7 @@ class SampleBatch:
         self._coeff: dict = {}
         self._gcoeff: dict = {}
         self._colstats: dict = {}
-        self._ws: torch.Tensor | None = None
+        self._ws: dict = {}  # stream handle -> product workspace
         self._stats_e: float | None = None
 
     # -- reference properties (est:55-61)
@@ -166,14 +189,19 @@ class SampleBatch:
         return _lib.stream_handle(self.device)
 
     def mvp_workspace(self) -> torch.Tensor:
-        if self._ws is None:
+        """Product workspace of the current stream: products on one batch issued
+        on two streams must not share partials (one buffer per stream handle)."""
+        key = self._stream()
+        ws = self._ws.get(key)
+        if ws is None:
             if self.otf is not None:
                 fn = "irl_otf_workspace_bytes_c128" if self.is_complex else "irl_otf_workspace_bytes"
                 nbytes = int(getattr(_lib.lib(), fn)(self.n_rows, self.otf["n_in"], self.otf["hidden"]))
             else:
                 nbytes = int(_lib.lib().irl_mvp_workspace_bytes(self.n_rows, self.ld, int(self.is_complex)))
-            self._ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
-        return self._ws
+            ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
+            self._ws[key] = ws
+        return ws
 
     def coefficients(self, mean: float) -> torch.Tensor:
         """Product coefficient c_n = w_n (e_n - E): est:166-168, est:186
@@ -234,12 +262,12 @@ class SampleBatch:
         n = self.n_rows
         if self.otf is not None:
             return self._otf_colstats(key, c)
-        obar = torch.empty(self.ld, dtype=self.o_matrix.dtype, device=self.device)
-        g = torch.empty(self.ld, dtype=self.o_matrix.dtype, device=self.device)
+        obar = torch.empty(self.ld, dtype=self.o_padded.dtype, device=self.device)
+        g = torch.empty(self.ld, dtype=self.o_padded.dtype, device=self.device)
         nbytes = int(_lib.lib().irl_colstats_workspace_bytes(n, self.ld, int(self.is_complex)))
         ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
         fn = "irl_colstats_c128" if self.is_complex else "irl_colstats_f64"
-        _lib.call(fn, _lib.ptr(self.o_matrix), n, self.ld, _lib.ptr(self.weights), _lib.ptr(c),
+        _lib.call(fn, _lib.ptr(self.o_padded), n, self.ld, _lib.ptr(self.weights), _lib.ptr(c),
                   _lib.ptr(obar), _lib.ptr(g), _lib.ptr(ws), ws.numel(), self._stream())
         self._colstats[key] = (obar, g)
         return obar, g
@@ -366,7 +394,7 @@ def _apply(batch: SampleBatch, coeff: torch.Tensor | None, v: torch.Tensor, out:
                   _lib.ptr(half_f), _lib.ptr(u0), _lib.ptr(out0), _lib.ptr(ws), ws.numel(), stream)
         return
     if not batch.is_complex:
-        _lib.call("irl_mvp_f64", _lib.ptr(batch.o_matrix), n, batch.param_count, batch.ld, _lib.ptr(obar),
+        _lib.call("irl_mvp_f64", _lib.ptr(batch.o_padded), n, batch.param_count, batch.ld, _lib.ptr(obar),
                   _lib.ptr(coeff), _lib.ptr(v), _lib.ptr(out), _lib.ptr(half_f), _lib.ptr(u0), _lib.ptr(out0),
                   int(mode), _lib.ptr(ws), ws.numel(), stream)
         return
@@ -377,7 +405,7 @@ def _apply(batch: SampleBatch, coeff: torch.Tensor | None, v: torch.Tensor, out:
     else:
         v_re, v_im, o_re, o_im = v, None, out, None
         h_re, h_im = half_f, None
-    _lib.call("irl_mvp_c128", _lib.ptr(batch.o_matrix), n, batch.param_count, batch.ld, _lib.ptr(obar),
+    _lib.call("irl_mvp_c128", _lib.ptr(batch.o_padded), n, batch.param_count, batch.ld, _lib.ptr(obar),
               _lib.ptr(coeff), _lib.ptr(v_re), _lib.ptr(v_im), _lib.ptr(o_re), _lib.ptr(o_im), _lib.ptr(h_re),
               _lib.ptr(h_im), _lib.ptr(u0), _lib.ptr(out0), int(mode), _lib.ptr(ws), ws.numel(), stream)
 
@@ -414,8 +442,8 @@ def _apply_connected(batch, cache, coeff, obar, v, out, mode, half_f, u0, out0, 
                       _lib.ptr(out), _lib.ptr(half_f), _lib.ptr(u0), _lib.ptr(out0), _lib.ptr(ws), ws.numel(),
                       stream)
         return
-    po = batch.o_matrix if cache.in_batch else cache.partner_o
-    common = (_lib.ptr(batch.o_matrix), n, batch.param_count, batch.ld, _lib.ptr(obar), *tail, _lib.ptr(po),
+    po = batch.o_padded if cache.in_batch else cache.partner_o
+    common = (_lib.ptr(batch.o_padded), n, batch.param_count, batch.ld, _lib.ptr(obar), *tail, _lib.ptr(po),
               cache.n_partner)
     if not batch.is_complex:
         _lib.call("irl_connected_mvp_f64", *common, _lib.ptr(v), _lib.ptr(out), _lib.ptr(half_f), _lib.ptr(u0),
@@ -612,7 +640,7 @@ class ConnectedCache:
             if batch.otf is None or batch.is_complex:
                 raise ValueError("regenerated partners need a real on-the-fly batch")
             po = None
-        elif partner_o is None or partner_o is batch.o_matrix:
+        elif partner_o is None or partner_o is batch.o_padded or _same_view(partner_o, batch):
             po = None  # partners are batch rows (exact mode): partner_row indexes the batch
         elif isinstance(partner_o, torch.Tensor) and partner_o.is_cuda and partner_o.ndim == 2 \
                 and partner_o.shape[1] == ld and partner_o.dtype == cdt:
@@ -655,7 +683,7 @@ class ConnectedCache:
         self.n_partner = m
         self.n_dist = n_dist
         self._batch_id = id(batch)
-        self._ws: torch.Tensor | None = None
+        self._ws: dict = {}  # stream handle -> workspace
 
     @classmethod
     def from_reference(cls, cache, batch: SampleBatch) -> "ConnectedCache":
@@ -672,7 +700,10 @@ class ConnectedCache:
         return self.partner_o is None and self.partner_otf is None
 
     def workspace(self, batch: SampleBatch) -> torch.Tensor:
-        if self._ws is None:
+        """Per-stream workspace (see SampleBatch.mvp_workspace)."""
+        key = batch._stream()
+        ws = self._ws.get(key)
+        if ws is None:
             if batch.otf is not None:
                 o = batch.otf
                 nbytes = int(_lib.lib().irl_otf_connected_workspace_bytes(
@@ -681,8 +712,18 @@ class ConnectedCache:
             else:
                 nbytes = int(_lib.lib().irl_connected_workspace_bytes(batch.n_rows, self.n_partner, batch.ld,
                                                                        int(batch.is_complex)))
-            self._ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=batch.device)
-        return self._ws
+            ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=batch.device)
+            self._ws[key] = ws
+        return ws
+
+
+def _same_view(partner_o, batch: SampleBatch) -> bool:
+    """``partner_o`` is the batch's own (N, P) ``o_matrix`` view."""
+    if not isinstance(partner_o, torch.Tensor) or batch.otf is not None:
+        return False
+    o = batch.o_padded
+    return (partner_o.is_cuda and partner_o.data_ptr() == o.data_ptr() and tuple(partner_o.shape) ==
+            (batch.n_rows, batch.param_count) and partner_o.stride() == o.stride())
 
 
 def partner_rows_in_batch(uniq_bits: np.ndarray, reps: np.ndarray, partner_bits: torch.Tensor):

@@ -30,6 +30,7 @@ from __future__ import annotations
 
 import os
 from dataclasses import dataclass
+from typing import NamedTuple
 
 import numpy as np
 import torch
@@ -255,15 +256,31 @@ def energy_at(params, integrals, sector, config: OptimizerConfig = OptimizerConf
     return float(val.real if torch.is_complex(val) else val)
 
 
-@dataclass(frozen=True)
-class OuterStep:
+class _OuterStepFields(NamedTuple):
     params: object
     lambda_min: float
     step_scale: float
     matvecs: int
     converged: bool
-    energy: float  # energy of the batch the step was solved on
-    best_energy: float  # line-search energy at the accepted scale (= energy if none)
+
+
+class OuterStep(_OuterStepFields):
+    """The reference's 5-tuple ``(new params, lambda_min, step scale, matvec
+    count, converged)`` (``opt:118-124``), so callers unpack it exactly as
+    ``run_optimization`` does (``opt:257``); the named fields read the same
+    values.  Two extra attributes (not tuple members): ``energy``, the batch
+    energy the step was solved on, and ``best_energy``, the line-search energy
+    at the accepted scale (= ``energy`` when no scale was accepted)."""
+
+    def __new__(cls, params, lambda_min, step_scale, matvecs, converged, *, energy=float("nan"),
+                best_energy=float("nan")):
+        self = super().__new__(cls, params, lambda_min, step_scale, matvecs, converged)
+        object.__setattr__(self, "energy", float(energy))
+        object.__setattr__(self, "best_energy", float(best_energy))
+        return self
+
+    def __setattr__(self, name, value):
+        raise AttributeError("OuterStep is immutable")
 
 
 def outer_step(params, integrals, sector, config: OptimizerConfig = OptimizerConfig(), step: int = 0, *,
@@ -322,5 +339,5 @@ def outer_step(params, integrals, sector, config: OptimizerConfig = OptimizerCon
     new = params
     if best_scale > 0.0:
         new = make(theta + best_scale * best_d)
-    return OuterStep(params=new, lambda_min=res.lambda_min, step_scale=best_scale, matvecs=res.n_matvec,
-                     converged=res.converged, energy=energy.mean, best_energy=best_energy)
+    return OuterStep(new, res.lambda_min, best_scale, res.n_matvec, res.converged, energy=energy.mean,
+                     best_energy=best_energy)

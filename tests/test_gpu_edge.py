@@ -444,3 +444,79 @@ def test_two_streams_two_batches(E):
     for i in range(2):
         for k in range(4):
             assert torch.equal(outs[i][k], serial[i][k])
+
+
+@pytest.mark.gpu
+def test_two_streams_one_batch(E):
+    """Products on ONE batch issued alternately on two streams (each stream gets
+    its own workspace and staging buffers) equal the serial results bit for bit,
+    stored rows / fused / two-pass shapes alike."""
+    import torch
+
+    rng = np.random.default_rng(22)
+    for n, p in ((3001, 157), (4096, 6600)):
+        o, e, w = random_batch(rng, n, p)
+        b = E.SampleBatch(None, w, e, o, n)
+        en = E.estimate_energy(b)
+        vs = [torch.as_tensor(rng.standard_normal(p), device="cuda") for _ in range(8)]
+        serial = [E.heff_matvec(b, en, v).clone() if k % 2 == 0 else E.qgt_matvec(b, v).clone()
+                  for k, v in enumerate(vs)]
+        torch.cuda.synchronize()
+        streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+        outs = [None] * 8
+        for k, v in enumerate(vs):
+            with torch.cuda.stream(streams[k % 2]):
+                outs[k] = E.heff_matvec(b, en, v) if k % 2 == 0 else E.qgt_matvec(b, v)
+        torch.cuda.synchronize()
+        for k in range(8):
+            assert torch.equal(outs[k], serial[k]), (n, p, k)
+
+
+@pytest.mark.parametrize("p", [20, 60, 90])
+def test_rows_path_o_at_end_of_allocation(E, p):
+    """Narrow rows (ld = 16-48 units, the warp-per-row kernel reads 128-unit
+    row windows): with O placed so that its last row ends exactly at the end of
+    a raw 2 MiB cudaMalloc block, the product reads nothing past O (a read past
+    the mapping would fault) and matches the oracle."""
+    import ctypes
+
+    import torch
+
+    from paper_2601_01437_b200 import _lib
+
+    rt = ctypes.CDLL("libcudart.so.12")
+    lib = _lib.lib()
+    ld = _lib.padded_ld(p, False)
+    n = 301
+    nbytes = n * ld * 8
+    block = 2 << 20
+    assert nbytes < block
+    base = ctypes.c_void_p()
+    assert rt.cudaMalloc(ctypes.byref(base), ctypes.c_size_t(block)) == 0
+    try:
+        rng = np.random.default_rng(p)
+        o, e, w = random_batch(rng, n, p)
+        opad = np.zeros((n, ld))
+        opad[:, :p] = o
+        src = torch.as_tensor(opad, device="cuda")
+        o_ptr = base.value + block - nbytes
+        assert rt.cudaMemcpy(ctypes.c_void_p(o_ptr), ctypes.c_void_p(src.data_ptr()), ctypes.c_size_t(nbytes),
+                             3) == 0  # device to device
+        mean, _, _ = oest.energy(w, e, n)
+        coeff = torch.as_tensor(w * (e - mean), device="cuda")
+        obar = torch.zeros(ld, dtype=torch.float64, device="cuda")
+        obar[:p] = torch.as_tensor(w @ o, device="cuda")
+        v = rng.standard_normal(p)
+        vd = torch.zeros(ld, dtype=torch.float64, device="cuda")
+        vd[:p] = torch.as_tensor(v, device="cuda")
+        out = torch.empty(ld, dtype=torch.float64, device="cuda")
+        ws_bytes = int(lib.irl_mvp_workspace_bytes(n, ld, 0))
+        ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+        rc = lib.irl_mvp_f64(ctypes.c_void_p(o_ptr), n, p, ld, obar.data_ptr(), coeff.data_ptr(), vd.data_ptr(),
+                             out.data_ptr(), None, None, None, 3, ws.data_ptr(), ws_bytes, _lib.stream_handle())
+        assert rc == _lib.IRL_OK, lib.irl_last_error()
+        torch.cuda.synchronize()
+        assert rel(out[:p].cpu().numpy(), oest.heff(w, e, o, mean, v)) < 1e-10
+    finally:
+        torch.cuda.synchronize()
+        rt.cudaFree(base)

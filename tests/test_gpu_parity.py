@@ -63,7 +63,7 @@ def test_real_golden_obuild_and_irl(pkg):
     params = A.AnsatzParameters(arch, g["theta"])
     b = A.build_batch(params, g["x"], g["e"])
     assert np.max(np.abs(host(b.o_matrix[:, : arch.param_count]) - g["o"])) < 1e-14
-    assert float(np.max(np.abs(host(b.o_matrix[:, arch.param_count:])))) == 0.0  # padding stays zero
+    assert float(np.max(np.abs(host(b.o_padded[:, arch.param_count:])))) == 0.0  # padding stays zero
     en = E.estimate_energy(b)
     assert rel(host(E.energy_gradient(b, en)), g["grad"]) < 1e-10
     res = OPT.solve_step(b, OPT.OptimizerConfig(m=int(g["m"]), max_restarts=3), seed=int(g["seed"]))

@@ -19,5 +19,5 @@ mean = b._stats_e
 obar, g = b.colstats(mean)
 gc = b.gradient_coefficients(mean)
 for _ in range(2):
-    A.fill_o_rows(params, xt, b.o_matrix, b.weights, gc, obar, g)
+    A.fill_o_rows(params, xt, b.o_padded, b.weights, gc, obar, g)
 torch.cuda.synchronize()

@@ -170,7 +170,7 @@ def main():
         mean = batch._stats_e
         obar, g = batch.colstats(mean)
         gc = batch.gradient_coefficients(mean)
-        ob = timed(lambda: A.fill_o_rows(params, xt, batch.o_matrix, batch.weights, gc, obar, g), 3)
+        ob = timed(lambda: A.fill_o_rows(params, xt, batch.o_padded, batch.weights, gc, obar, g), 3)
         en = E.estimate_energy(batch)
         N, P, ld = batch.n_rows, batch.param_count, batch.ld
         b_el = 16 if batch.is_complex else 8
