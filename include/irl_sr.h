@@ -45,7 +45,7 @@ extern "C" {
 #define IRL_MVP_FUSED 1     /* one HBM pass, column slices over a CTA cluster (DSMEM exchange) */
 #define IRL_MVP_TWO_PASS 2  /* t = O v pass, then O^H y pass */
 #define IRL_MVP_ROWS 3      /* one HBM pass, a warp per row (narrow rows: ld <= 512 16-byte units) */
-#define IRL_MVP_WIDE 4      /* one HBM pass + one L2 pass, persistent column-sliced grid (very wide rows) */
+#define IRL_MVP_WIDE 4      /* one HBM pass, persistent column-sliced grid, stages resident until their accumulate (very wide rows) */
 
 #define IRL_MODEL_RBM 0
 #define IRL_MODEL_MLP 1
@@ -53,6 +53,11 @@ extern "C" {
 /* Library identity / diagnostics. */
 int irl_version(void);
 const char* irl_last_error(void);
+
+/* Development only: copies up to `bytes` of the wide-path trace (per-CTA,
+ * per-block %globaltimer stamps recorded when IRL_WIDE_TRACE is set) to host
+ * memory; returns the bytes copied (0 when tracing is off). */
+size_t irl_debug_wide_trace(void* host, size_t bytes);
 
 /* Padded leading dimension (in elements: doubles for f64, complex for c128) for
  * P parameters.  Rows are padded to whole 16-B units and to a multiple of 16

@@ -41,6 +41,7 @@ _D = ctypes.c_double
 SIGNATURES = {
     "irl_version": (_I, []),
     "irl_last_error": (ctypes.c_char_p, []),
+    "irl_debug_wide_trace": (_SZ, [_P, _SZ]),
     "irl_padded_ld": (_I64, [_I64, _I]),
     "irl_energy_f64": (_I, [_P, _P, _I64, _P, _P, _P]),
     "irl_energy_c128": (_I, [_P, _P, _I64, _I, _P, _P, _P]),

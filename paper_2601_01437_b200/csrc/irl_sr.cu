@@ -445,80 +445,146 @@ int launch_rows(const Plan& p, bool cplx, const StreamArgs& a, cudaStream_t st) 
 }
 
 // ----------------------------------------------------------------- wide ---
-// AUTO does not take the wide path yet: at cfg4 / cfg5 it reads O once from HBM
-// (ncu: 62.4 GB of 61.5) but its consumers are latency-bound per row block
-// (30 / 35 ms against 17.4 / 30.5 ms for the two-pass path); IRL_MVP_WIDE
-// selects it explicitly.
-constexpr int64_t kWideMinUnits = INT64_MAX;
+// Rows of at least kWideMinUnits 16-byte units (cfg4, cfg5) take the
+// single-read wide kernel (wide.cuh): every SM owns a column slice of every
+// row, so O is read from HBM once with no cluster exchange.
+constexpr int64_t kWideMinUnits = 16384;
 
 struct WidePlan {
-  int G, R, NS, RB, WM, ppt;
-  size_t smem, ws;
+  int G, WM, RS, Q, PU, NS, K, upl, rpw;
+  size_t smem, ws, part_bytes, fin_bytes, ring_bytes, vsl_off;
 };
 
 using WideFn = void (*)(WideArgs);
-WideFn pick_wide(bool cplx, int upl) {
-  switch (upl) {
-    case 8: return cplx ? k_wide<true, 8> : k_wide<false, 8>;
-    case 16: return cplx ? k_wide<true, 16> : k_wide<false, 16>;
-    case 24: return cplx ? k_wide<true, 24> : k_wide<false, 24>;
-    default: return nullptr;
-  }
+// instances: units per lane x rows per warp-step <= 16 (register budget)
+constexpr bool wide_inst(int upl, int rpw) { return upl * rpw <= 16; }
+template <bool CPLX>
+WideFn pick_wide_c(int upl, int rpw) {
+#define WIDE_CASE(U, R) if (upl == U && rpw == R) return k_wide<CPLX, U, R>;
+  WIDE_CASE(2, 1) WIDE_CASE(2, 2) WIDE_CASE(2, 4) WIDE_CASE(4, 1) WIDE_CASE(4, 2) WIDE_CASE(4, 4)
+  WIDE_CASE(6, 1) WIDE_CASE(6, 2) WIDE_CASE(8, 1) WIDE_CASE(8, 2)
+#undef WIDE_CASE
+  return nullptr;
 }
+WideFn pick_wide(bool cplx, int upl, int rpw) { return cplx ? pick_wide_c<true>(upl, rpw) : pick_wide_c<false>(upl, rpw); }
+
+int wide_upl(int need) { return need <= 2 ? 2 : need <= 4 ? 4 : need <= 6 ? 6 : need <= 8 ? 8 : 0; }
 
 int make_wide_plan(int64_t n, int64_t ld_u, bool cplx, WidePlan& p) {
   DevInfo d;
   IRL_TRY(dev_info(d));
   p.G = d.sms;
+  if (p.G > WIDE_QPL * 32 * WIDE_AW) return fail(IRL_ERR_DEVICE, "wide path: %d SMs exceed the aggregator lanes", p.G);
   p.WM = (int)cdiv(ld_u, p.G);
-  const int need = (int)cdiv(p.WM, 32);  // units per lane (warp per row slice)
-  p.ppt = need <= 8 ? 8 : need <= 16 ? 16 : need <= 24 ? 24 : 0;
-  if (!p.ppt) return fail(IRL_ERR_DEVICE, "wide path needs ld <= %d units per SM slice", 24 * 32);
+  // fewest parts per row slice (most rows per block, the biggest TMA stages)
+  // whose per-lane share fits a kernel instance
+  p.Q = 0;
+  for (int q = 1; q <= WIDE_CW; q *= 2) {
+    const int upl = wide_upl((int)cdiv(cdiv(p.WM, q), 32));
+    if (upl) {
+      p.Q = q;
+      p.upl = upl;
+      break;
+    }
+  }
+  if (!p.Q) return fail(IRL_ERR_DEVICE, "wide path needs <= %d units per SM slice", 8 * 32 * WIDE_CW);
+  if (getenv("IRL_WIDE_Q")) {  // tuning: more parts per row = fewer rows per stage
+    const int q = atoi(getenv("IRL_WIDE_Q"));
+    if (q >= p.Q && q <= WIDE_CW && (WIDE_CW % q) == 0) {
+      p.Q = q;
+      p.upl = wide_upl((int)cdiv(cdiv(p.WM, q), 32));
+    }
+  }
+  // rows per warp-step: each consumer step has fixed latencies (barrier probes,
+  // butterfly, TMEM round trip), so a step should move ~5 KB or more
+  const int part_bytes_row = (int)cdiv(p.WM, p.Q) * 16;
+  p.rpw = 1;
+  while (p.rpw < 4 && part_bytes_row * p.rpw < 4096 && wide_inst(p.upl, 2 * p.rpw) &&
+         2 * p.rpw * WIDE_CW / p.Q <= WIDE_MAX_RS && 2 * p.rpw * wide_tm_words(p.upl) * 2 <= WIDE_TM_COLS_PER_WARP)
+    p.rpw *= 2;
+  if (getenv("IRL_WIDE_RPW")) {
+    const int r = atoi(getenv("IRL_WIDE_RPW"));
+    if ((r == 1 || r == 2 || r == 4) && wide_inst(p.upl, r) && r * WIDE_CW / p.Q <= WIDE_MAX_RS &&
+        r * wide_tm_words(p.upl) * 2 <= WIDE_TM_COLS_PER_WARP)
+      p.rpw = r;
+  }
+  p.RS = p.rpw * WIDE_CW / p.Q;
+  p.PU = (int)cdiv(p.WM, p.Q);
   const size_t sS = cplx ? 16 : 8;
-  const int64_t row_bytes = ld_u * 16;
-  // one or two row slices per consumer warp per stage (two when >= 3 stages still fit)
-  p.RB = (size_t)3 * 2 * WIDE_NW * p.WM * 16 <= (size_t)160 * 1024 ? 2 * WIDE_NW : WIDE_NW;
-  if (getenv("IRL_WIDE_RPW")) p.RB = WIDE_NW * std::max(1, std::min(2, atoi(getenv("IRL_WIDE_RPW"))));
-  const int64_t target = (getenv("IRL_WIDE_MB") ? atoll(getenv("IRL_WIDE_MB")) : 24) << 20;
-  p.R = (int)std::max<int64_t>(p.RB, std::min<int64_t>(512, target / row_bytes));
-  p.R = (int)std::min<int64_t>(rup(p.R, p.RB), std::max<int64_t>(rup(n, p.RB), p.RB));
-  const size_t fixed = (size_t)p.R * sS + (size_t)p.WM * 16 + 64;
-  const size_t budget = (size_t)std::min(d.smem_optin - 4096, 210 * 1024);
-  p.NS = (int)std::min<int64_t>(16, (int64_t)((budget - fixed) / ((size_t)p.RB * p.WM * 16 + 16)));
+  // TMEM slots per consumer warp: its half of the 512 columns over 4 UPL words a block
+  p.K = std::min(WIDE_MAX_K, WIDE_TM_COLS_PER_WARP / (p.rpw * wide_tm_words(p.upl)));
+  if (getenv("IRL_WIDE_K")) p.K = std::min(p.K, std::max(2, atoi(getenv("IRL_WIDE_K"))));
+  const size_t stage = (size_t)p.RS * p.WM * 16;
+  const size_t per_slot = 2 * 8 + (size_t)p.RS * p.Q * sS + (size_t)p.RS * sS;  // dotdone, ydone, pd, ys
+  const size_t budget = (size_t)d.smem_optin - 2048;  // static smem of the kernel
+  const size_t fixed = (size_t)p.K * per_slot;
+  const size_t vbytes = (size_t)(p.WM + 1) * 16 + 16;
+  p.NS = (int)std::min<size_t>(WIDE_MAX_NS, (budget - fixed - vbytes) / (stage + 16));
+  if (getenv("IRL_WIDE_NS")) p.NS = std::min(p.NS, std::max(2, atoi(getenv("IRL_WIDE_NS"))));
   if (p.NS < 2) return fail(IRL_ERR_DEVICE, "wide path: row slices too wide for the ring");
-  p.smem = (size_t)p.NS * p.RB * p.WM * 16 + (size_t)2 * p.NS * 8 + fixed;
-  p.ws = align256((size_t)4 * p.R * p.G * sS) + align256((size_t)p.G * 8) + 256 + align256((size_t)cdiv(n, p.R) * 4);
+  p.ring_bytes = std::max((size_t)p.NS * stage, (size_t)WIDE_CW * 32 * p.upl * 16);  // ring / epilogue scratch
+  p.vsl_off = p.ring_bytes + (size_t)p.NS * 16 + fixed;
+  p.vsl_off = (p.vsl_off + 15) / 16 * 16;
+  p.smem = p.vsl_off + (size_t)(p.WM + 1) * 16;
+  if (p.smem > budget) return fail(IRL_ERR_DEVICE, "wide path: shared memory");
+  const size_t rec = cplx ? 32 : 16;  // LL record bytes per scalar
+  p.part_bytes = align256((size_t)WIDE_NBUF * p.RS * p.G * rec);
+  p.fin_bytes = align256((size_t)WIDE_NBUF * p.RS * rec);
+  p.ws = p.part_bytes + p.fin_bytes + align256((size_t)p.G * 16);
+  (void)n;
   return IRL_OK;
 }
 
+// development tracing (IRL_WIDE_TRACE=1): per-block globaltimer stamps of
+// every CTA into one process-wide device buffer, read by irl_debug_wide_trace
+unsigned long long* g_wide_trace = nullptr;
+size_t g_wide_trace_bytes = 0;
+unsigned long long* wide_trace_buffer(int G) {
+  static const bool on = getenv("IRL_WIDE_TRACE") != nullptr;
+  if (!on) return nullptr;
+  const size_t bytes = (size_t)G * WIDE_TRACE_B * 8 * 8;
+  if (!g_wide_trace) {
+    if (cudaMalloc(&g_wide_trace, bytes) != cudaSuccess) return nullptr;
+    cudaMemset(g_wide_trace, 0, bytes);
+    g_wide_trace_bytes = bytes;
+  }
+  return g_wide_trace;
+}
+
 int launch_wide(const WidePlan& p, bool cplx, WideArgs a, void* ws, cudaStream_t st) {
-  WideFn fn = pick_wide(cplx, p.ppt);
+  WideFn fn = pick_wide(cplx, p.upl, p.rpw);
+  if (!fn) return fail(IRL_ERR_DEVICE, "no wide instance for %d units per lane, %d rows per warp", p.upl, p.rpw);
   DevInfo d;
   IRL_TRY(dev_info(d));
   IRL_TRY(ensure_fn_attrs((const void*)fn, d.smem_optin));
   char* base = static_cast<char*>(ws);
-  const size_t sS = cplx ? 16 : 8;
-  a.tpart = base;
-  size_t off = align256((size_t)4 * p.R * p.G * sS);
-  a.gpart = reinterpret_cast<double*>(base + off);
-  off += align256((size_t)p.G * 8);
-  a.error = reinterpret_cast<int*>(base + off);
-  a.counter = reinterpret_cast<unsigned int*>(base + off + 256);  // [NB] per-block arrivals
-  const size_t nblk = (size_t)cdiv(a.n_rows, p.R);
-  a.R = p.R;
+  a.part = reinterpret_cast<ulonglong2*>(base);
+  a.fin = reinterpret_cast<ulonglong2*>(base + p.part_bytes);
+  a.gpart = reinterpret_cast<ulonglong2*>(base + p.part_bytes + p.fin_bytes);
+  a.RS = p.RS;
+  a.Q = p.Q;
+  a.PU = p.PU;
   a.NS = p.NS;
-  a.RB = p.RB;
+  a.K = p.K;
   a.WM = p.WM;
-  IRL_TRY(cuda_check(cudaMemsetAsync(a.error, 0, 256 + nblk * 4, st), "wide counter reset"));
+  a.ring_bytes = p.ring_bytes;
+  a.vsl_off = p.vsl_off;
+  a.trace = wide_trace_buffer(p.G);
+  a.trace_stride = getenv("IRL_WIDE_TRACE") ? std::max(1, atoi(getenv("IRL_WIDE_TRACE"))) : 1;
+  a.poll_ns = getenv("IRL_WIDE_POLL_NS") ? atoi(getenv("IRL_WIDE_POLL_NS")) : 160;
+  a.rot = getenv("IRL_WIDE_ROT") ? atoi(getenv("IRL_WIDE_ROT")) % p.G : 0;
+  a.spin_ns = getenv("IRL_WIDE_SPIN_NS") ? atoi(getenv("IRL_WIDE_SPIN_NS")) : 32;
+  // tags are block numbers: zeroed records can never match a stale one
+  IRL_TRY(cuda_check(cudaMemsetAsync(base, 0, p.ws, st), "wide record reset"));
   int occ = 0;
-  IRL_TRY(cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)fn, WIDE_NT + 32, p.smem), "occ"));
+  IRL_TRY(cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)fn, WIDE_THREADS, p.smem), "occ"));
   if (occ < 1) return fail(IRL_ERR_DEVICE, "wide kernel does not fit on an SM");
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;  // all G CTAs co-resident: the grid counter cannot deadlock
+  attr[0].id = cudaLaunchAttributeCooperative;  // all G CTAs co-resident: the exchange cannot deadlock
   attr[0].val.cooperative = 1;
   cfg.gridDim = dim3(p.G);
-  cfg.blockDim = dim3(WIDE_NT + 32);
+  cfg.blockDim = dim3(WIDE_THREADS);
   cfg.dynamicSmemBytes = p.smem;
   cfg.stream = st;
   cfg.attrs = attr;
@@ -1842,6 +1908,13 @@ int irl_version(void) { return 100; }
 
 const char* irl_last_error(void) { return g_err.c_str(); }
 
+size_t irl_debug_wide_trace(void* host, size_t bytes) {
+  if (!g_wide_trace || !host) return 0;
+  const size_t n = bytes < g_wide_trace_bytes ? bytes : g_wide_trace_bytes;
+  if (cudaMemcpy(host, g_wide_trace, n, cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
+  return n;
+}
+
 int64_t irl_padded_ld(int64_t p, int is_complex) {
   if (p < 1) return 0;
   const int64_t E = is_complex ? 1 : 2;
@@ -1964,7 +2037,7 @@ int irl_mvp_plan(int64_t n, int64_t ld, int is_complex, int mode, int* out_path,
              mode == IRL_MVP_WIDE) {
     IRL_TRY(make_wide_plan(n, ld_u, is_complex != 0, wp));
     *out_path = IRL_MVP_WIDE;
-    int g[7] = {wp.G, wp.WM, WIDE_NT, wp.RB, wp.NS, wp.R, wp.ppt};  // slices, units/slice, threads, rows/stage, stages, rows/block, ppt
+    int g[7] = {wp.G, wp.WM, WIDE_THREADS, wp.RS, wp.NS, wp.K, wp.upl};  // slices, units/slice, threads, rows/stage, stages, TMEM slots, units/lane
     memcpy(out_geom7, g, sizeof(g));
     return IRL_OK;
   } else if (mode == IRL_MVP_AUTO || mode == IRL_MVP_FUSED) {

@@ -1,36 +1,85 @@
 // Single-HBM-read product for very wide rows (cfg4: 470 KB rows, cfg5: 1.67 MB).
 //
-// The fused cluster kernel needs a whole row slice per CTA in shared memory
-// while the row's dot is exchanged, which limits rows in flight when rows are
-// this wide; the two-pass path reads O twice from HBM.  Here the GPU runs one
-// persistent, cooperatively launched grid with one CTA per SM:
+// The fused cluster kernel (stream.cuh) splits a row over at most a few CTAs
+// of one cluster, and its per-row DSMEM exchange stops paying beyond C = 2; the
+// two-pass path reads O twice from HBM.  Here the whole GPU works on every
+// row at once: one persistent, cooperatively launched grid with one CTA per SM.
 //
 //   * CTA c owns the column slice c of EVERY row (G = #SMs slices), so its
-//     slice of the output needs no cross-CTA reduction at all;
-//   * rows go in blocks of R (~30 MB per block).  Phase D(b): stream the slice
-//     of block b through a TMA ring, per-row partial dots (minus the slice's
-//     share of Obar.v) -> tpart[b % 4][r][c]; arrive on block b's counter.
-//   * Phase A(b), one block later: wait until all G CTAs have arrived for b,
-//     every CTA forms y_r = c_r sum_c tpart[..][r][c] in the same fixed order,
-//     then streams its slice of block b again -- now from L2, the block was
-//     read one block earlier -- and accumulates conj(O_r) y_r in registers.
+//     slice of the output lives in registers for the whole product and needs
+//     no cross-CTA reduction at all.
+//   * Rows go in blocks of RS rows; a block is one stage of a shared-memory
+//     ring (TMA bulk copies, one per row slice).  O is read from HBM exactly
+//     once and never re-read (not even from L2): between its dot and its
+//     accumulate a block waits for the grid-wide exchange of its row dots, and
+//     during that wait it is parked in TENSOR MEMORY -- each consumer warp
+//     moves its part of the block from shared memory to registers for the dot
+//     and from there to its TMEM columns (tcgen05.st), and frees the stage at
+//     once.  Shared memory then only has to cover the HBM latency and the
+//     256 KB of TMEM cover the exchange latency: a 1-CTA-per-SM stream needs
+//     about (HBM latency + exchange latency) x 45 GB/s in flight, more than
+//     the 227 KB of shared memory alone.
+//   * Only the per-row dots cross CTAs.  Every exchanged value travels as a
+//     self-validating "LL" record: each 32-bit half of a double shares a 64-bit
+//     word with a 32-bit tag (block + 1), and aligned 64-bit accesses are
+//     single-copy atomic, so a reader that sees the tag sees the data -- no
+//     fences, no counters, no atomics on the hot path.  The records are zeroed
+//     before every launch, so a stale tag can never match.
 //
-// The producer warp streams D(0), D(1), A(0), D(2), A(1), ..., so the barrier
-// of block b is hidden behind D(b+1) and the ring keeps prefetching A(b) while
-// consumers wait.  HBM reads O once; L2 serves the second pass.  Each block
-// has its own arrival counter (a shared running total could be satisfied by a
-// fast CTA's later arrivals while a slow CTA had not yet published block b).
-// tpart has four buffers: a CTA writes block b+1's partials (into b-3's
-// buffer) only after its A(b-1), i.e. after every CTA arrived for b-1 and so
-// finished A(b-3); with three buffers a slow CTA could still be reading A(b-2)
-// (seen as a rare 1e-7 error on cfg5).  All sums are fixed-order.
+// Exchange of block b (RS rows):
+//   publish    every CTA writes its RS partial dots (minus its share of
+//              Obar.v) to part[b % NBUF][row][c];
+//   aggregate  CTA r % G polls the G partials of row r, sums them in a
+//              fixed order (the same order whichever CTA aggregates) and
+//              writes t_r to fin[b % NBUF][row];
+//   reduce     every CTA polls fin, forms y_row = c_row t_row (+ yadd) --
+//              bit-identical in every CTA -- and accumulates with it.
+//
+// Warp roles (one CTA, WIDE_THREADS threads):
+//   consumers (WIDE_CW warps)  warp w owns rows (w / Q) RPW ... + RPW - 1 of a
+//       stage, part w % Q of the slice (RS = RPW WIDE_CW / Q rows per block;
+//       several rows per warp-step hide the step's latencies).  D(b): part -> registers,
+//       arrive empty (the stage refills at once), partial dot -> smem, arrive
+//       dotdone, park the part in TMEM slot b % K.  A(b): part back from TMEM,
+//       y from smem, acc += conj(O) y.  Each warp runs A(b) as soon as block
+//       b's y is there and D(b') as soon as block b' landed and a slot is free
+//       (non-blocking mbarrier probes), so the lag between the two adapts to
+//       the grid's exchange latency.
+//   producer (1 warp)          lane 0 streams block after block into the ring.
+//   publisher (1 warp)         sums the Q part dots of each row, writes part.
+//   aggregators (WIDE_AW warps) the rows this CTA aggregates.
+//   reducers (WIDE_RW warps)   block b (b = k mod RW): fin -> y -> smem,
+//       arrive ydone; several warps keep several blocks' polls in flight.
+//
+// Slot reuse: a consumer warp parks at most K blocks, so CTA X publishes block
+// b only after its consumers ran A(b - K), i.e. after fin of b - K existed,
+// i.e. after every CTA published b - K; a CTA publishes b - K only after its
+// consumers ran A(b - 2 K), i.e. after its reducers finished every block
+// <= b - 2 K.  With NBUF >= 2 K + 2 no record is overwritten while some CTA
+// may still read it; tags are unique within a launch.
+//
+// Replaces est:184-186 (centring copy + the two GEMVs) for stored O.
 #pragma once
 #include "stream.cuh"
 
 namespace irl {
 
-constexpr int WIDE_NT = 256;  // consumer threads
-constexpr int WIDE_NW = WIDE_NT / 32;
+constexpr int WIDE_CW = 8;  // consumer warps
+constexpr int WIDE_AW = 3;  // aggregator warps
+constexpr int WIDE_RW = 3;  // reducer warps
+constexpr int WIDE_THREADS = (WIDE_CW + 2 + WIDE_AW + WIDE_RW) * 32;
+constexpr int WIDE_MAX_NS = 24;  // shared-memory stages
+constexpr int WIDE_MAX_K = 24;   // blocks parked in TMEM per consumer warp (pending exchange)
+constexpr int WIDE_NBUF = 64;    // exchange record ring (>= 2 K + 2)
+static_assert(WIDE_NBUF >= 2 * WIDE_MAX_K + 2, "exchange ring too short for the deepest pending ring");
+constexpr int WIDE_QPL = 2;  // partials per aggregator lane: 2 * 32 * WIDE_AW >= G
+static_assert(WIDE_QPL * 32 * WIDE_AW >= 160, "aggregator lanes must cover every SM");
+constexpr int WIDE_MAX_RS = 32;  // rows per block: one reducer lane each
+constexpr int WIDE_TMEM_COLS = 512;  // whole TMEM: one CTA per SM
+// TMEM words (32-bit columns) one consumer lane parks per block: UPL 16-byte units
+__host__ __device__ constexpr int wide_tm_words(int upl) { return 4 * upl; }
+// consumer warps w and w + 4 share a 32-lane quarter of TMEM, so each owns half the columns
+constexpr int WIDE_TM_COLS_PER_WARP = WIDE_TMEM_COLS / (WIDE_CW / 4);
 
 struct WideArgs {
   const double2* O;
@@ -46,278 +95,471 @@ struct WideArgs {
   double* out_re;
   double* out_im;
   double* out0;
-  void* tpart;              // S[4][R][G]
-  double* gpart;            // [G]
-  unsigned int* counter;    // [NB] per-block arrival counters, zero at launch
-  int* error;               // set on a barrier timeout (never expected)
-  int R;                    // rows per block
-  int NS;                   // ring stages
-  int RB;                   // row slices per stage (<= WIDE_RB)
-  int WM;                   // row slice width in the ring (units)
+  ulonglong2* part;  // LL records [NBUF][RS][G][S doubles]   (zeroed per launch)
+  ulonglong2* fin;   // LL records [NBUF][RS][S doubles]      (zeroed per launch)
+  ulonglong2* gpart;  // LL records [G]: each slice's (F/2) . v share   (zeroed per launch)
+  int RS;            // rows per block (= per stage), WIDE_CW / Q
+  int Q;             // parts per row slice
+  int PU;            // units per part (ceil(WM / Q))
+  int NS;            // ring stages
+  int K;             // TMEM slots per consumer warp (blocks in flight between dot and accumulate)
+  int WM;            // max slice width (units): ring row pitch
+  size_t ring_bytes;  // ring + epilogue scratch (>= both)
+  size_t vsl_off;     // shared-memory offset of the v slice
+  unsigned long long* trace;  // debug (IRL_WIDE_TRACE): [G][WIDE_TRACE_B][8] globaltimer stamps; null = off
+  int trace_stride;           // every trace_stride-th block is stamped
+  int poll_ns;                // reducer / aggregator poll back-off (ns)
+  int rot;                    // debug: CTA c takes column slice (c + rot) % G
+  int spin_ns;                // consumer back-off when no stage is ready (0 = spin)
 };
 
-constexpr int WIDE_RB = 8;
+constexpr int WIDE_TRACE_B = 512;  // traced blocks per CTA
+constexpr uint32_t WIDE_GPART_TAG = 0xffffffffu;
 
-__device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
-  unsigned int v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
 }
-__device__ __forceinline__ void red_release_add(unsigned int* p, unsigned int v) {
-  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
+#define WIDE_STAMP(b, k)                                                                      \
+  do {                                                                                        \
+    if (a.trace && ((b) % a.trace_stride) == 0 && (b) / a.trace_stride < WIDE_TRACE_B)        \
+      a.trace[((size_t)c * WIDE_TRACE_B + (b) / a.trace_stride) * 8 + (k)] = gtimer();        \
+  } while (0)
 
-// mbarrier wait that gives up (and flags the error) after ~30 s instead of
-// hanging the GPU if the ring ever desynchronised
-__device__ __forceinline__ void mbar_wait_bounded(uint64_t* bar, uint32_t parity, int* error) {
-  const uint32_t addr = smem_addr(bar);
-  if (mbar_try_wait(addr, parity)) return;
-  const long long t0 = clock64();
-  while (!mbar_try_wait(addr, parity)) {
-    if (clock64() - t0 > (1LL << 36)) {
-      atomicExch(error, 2);
-      return;
-    }
+// ------------------------------------------------------------- LL records --
+__device__ __forceinline__ void st_ll(ulonglong2* p, double d, uint32_t tag) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(d);
+  const unsigned long long t = (unsigned long long)tag << 32;
+  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(t | (u & 0xffffffffull)),
+               "l"(t | (u >> 32))
+               : "memory");
+}
+// returns true (and the value) when both halves carry `tag`
+__device__ __forceinline__ bool ld_ll(const ulonglong2* p, uint32_t tag, double& d) {
+  unsigned long long lo, hi;
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "l"(p) : "memory");
+  d = __longlong_as_double((long long)((hi << 32) | (lo & 0xffffffffull)));
+  return (uint32_t)(lo >> 32) == tag && (uint32_t)(hi >> 32) == tag;
+}
+template <bool CPLX>
+__device__ __forceinline__ void st_ll_s(ulonglong2* p, typename Traits<CPLX>::S v, uint32_t tag) {
+  if constexpr (CPLX) {
+    st_ll(p, v.x, tag);
+    st_ll(p + 1, v.y, tag);
+  } else {
+    st_ll(p, v, tag);
+  }
+}
+template <bool CPLX>
+__device__ __forceinline__ bool ld_ll_s(const ulonglong2* p, uint32_t tag, typename Traits<CPLX>::S& v) {
+  if constexpr (CPLX) {
+    const bool a = ld_ll(p, tag, v.x);
+    const bool b = ld_ll(p + 1, tag, v.y);
+    return a && b;
+  } else {
+    return ld_ll(p, tag, v);
   }
 }
 
-// Consumers work warp-per-row: a ring stage holds WIDE_NW row slices and warp w
-// takes slice w, so a row's partial dot over the CTA's slice is one warp
-// butterfly (no cross-warp reduction per row) and each lane owns the units
-// lane + 32 k (k < UPL) of the slice; v sits in shared memory.  The warps'
-// accumulators meet in shared memory once, at the end, in warp order.
-template <bool CPLX, int UPL>
-__global__ void __launch_bounds__(WIDE_NT + 32, 1) k_wide(const WideArgs a) {
+// ------------------------------------------------------------------ TMEM --
+// 32x32b shapes: thread t of the warp moves 32-bit words to / from TMEM lane
+// (lane quarter base + t), consecutive columns.
+#define TM_R8(p) "r"(p[0]), "r"(p[1]), "r"(p[2]), "r"(p[3]), "r"(p[4]), "r"(p[5]), "r"(p[6]), "r"(p[7])
+#define TM_W8(p) "=r"(p[0]), "=r"(p[1]), "=r"(p[2]), "=r"(p[3]), "=r"(p[4]), "=r"(p[5]), "=r"(p[6]), "=r"(p[7])
+__device__ __forceinline__ void tm_st8(uint32_t ta, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(ta), TM_R8(r)
+               : "memory");
+}
+__device__ __forceinline__ void tm_ld8(uint32_t ta, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : TM_W8(r)
+               : "r"(ta)
+               : "memory");
+}
+#undef TM_R8
+#undef TM_W8
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// park / fetch UPL units (4 UPL words, a multiple of 8) of one lane
+template <int UPL>
+__device__ __forceinline__ void tm_park(uint32_t ta, const double2 (&x)[UPL]) {
+  static_assert((4 * UPL) % 8 == 0, "TMEM chunks of 8 words");
+#pragma unroll
+  for (int c8 = 0; c8 < UPL / 2; ++c8) {
+    uint32_t r[8];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const double2 v = x[2 * c8 + h];
+      r[4 * h + 0] = (uint32_t)__double2loint(v.x);
+      r[4 * h + 1] = (uint32_t)__double2hiint(v.x);
+      r[4 * h + 2] = (uint32_t)__double2loint(v.y);
+      r[4 * h + 3] = (uint32_t)__double2hiint(v.y);
+    }
+    tm_st8(ta + 8 * c8, r);
+  }
+}
+template <int UPL>
+__device__ __forceinline__ void tm_fetch(uint32_t ta, double2 (&x)[UPL]) {
+  uint32_t r[UPL / 2][8];
+#pragma unroll
+  for (int c8 = 0; c8 < UPL / 2; ++c8) tm_ld8(ta + 8 * c8, r[c8]);
+  tm_wait_ld();
+#pragma unroll
+  for (int c8 = 0; c8 < UPL / 2; ++c8)
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      x[2 * c8 + h] = make_double2(__hiloint2double((int)r[c8][4 * h + 1], (int)r[c8][4 * h + 0]),
+                                   __hiloint2double((int)r[c8][4 * h + 3], (int)r[c8][4 * h + 2]));
+}
+
+template <bool CPLX, int UPL, int RPW>
+__global__ void __launch_bounds__(WIDE_THREADS, 1) k_wide(const WideArgs a) {
   using T = Traits<CPLX>;
   using S = typename T::S;
+  constexpr int SW = CPLX ? 2 : 1;  // LL records per scalar
+  constexpr int TMW = RPW * wide_tm_words(UPL);  // TMEM words a lane parks per block
   extern __shared__ __align__(16) unsigned char smem_w[];
-  const int NS = a.NS, WM = a.WM, R = a.R;
-  const int RB = a.RB;  // WIDE_NW * rpw row slices per stage
-  const int rpw = RB / WIDE_NW;
-  double2* ring = reinterpret_cast<double2*>(smem_w);                          // [NS][RB][WM]
-  uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)NS * RB * WM);  // [NS]
-  uint64_t* empty = full + NS;                                                 // [NS]
-  S* ys = reinterpret_cast<S*>(empty + NS);                                    // [R]
-  double2* vs = reinterpret_cast<double2*>(ys + R);                            // [WM] v slice
-  __shared__ S shs[WIDE_NW];
-  __shared__ double shg[WIDE_NW];
+  const int NS = a.NS, K = a.K, WM = a.WM, RS = a.RS, Q = a.Q, PU = a.PU;
+  double2* ring = reinterpret_cast<double2*>(smem_w);                    // [NS][RS][WM]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_w + a.ring_bytes);  // [NS]
+  uint64_t* empty = full + NS;                                           // [NS]
+  uint64_t* dotdone = empty + NS;                                        // [K]
+  uint64_t* ydone = dotdone + K;                                         // [K]
+  S* pd = reinterpret_cast<S*>(ydone + K);                               // [K][RS][Q] part dots
+  S* ys = pd + (size_t)K * RS * Q;                                       // [K][RS] y of the rows
+  double2* vsl = reinterpret_cast<double2*>(a.vsl_off + smem_w);         // [WM + 1] v slice (+ a zero unit)
+  __shared__ S shs[WIDE_CW];
+  __shared__ double shg[WIDE_CW];
+  __shared__ S shy[WIDE_RW];
+  __shared__ S shagg[WIDE_AW];
+  __shared__ S s_c_sh;
+  __shared__ volatile int published;  // blocks this CTA has published (paces its aggregator)
+  __shared__ uint32_t tmem_base_sh;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int G = gridDim.x, c = blockIdx.x;
   const int64_t N = a.n_rows;
-  const int64_t col0 = slice_lo(a.ld_u, G, c);
-  const int W = (int)(slice_lo(a.ld_u, G, c + 1) - col0);
-  const int NB = (int)((N + R - 1) / R);
-  S* tpart = reinterpret_cast<S*>(a.tpart);
+  const int sl = (c + a.rot) % G;  // column slice of this CTA
+  const int64_t col0 = slice_lo(a.ld_u, G, sl);
+  const int W = (int)(slice_lo(a.ld_u, G, sl + 1) - col0);
+  const int NB = (int)((N + RS - 1) / RS);
+  const S* coeff = reinterpret_cast<const S*>(a.coeff);
+  const S* yadd = reinterpret_cast<const S*>(a.yadd);
+  constexpr int W_PROD = WIDE_CW, W_PUB = WIDE_CW + 1, W_AGG = WIDE_CW + 2, W_RED = WIDE_CW + 2 + WIDE_AW;
+  constexpr int NTC = WIDE_CW * 32;
 
   if (tid == 0) {
+    if (a.trace) {
+      unsigned int smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      a.trace[(size_t)c * WIDE_TRACE_B * 8 + 7] = smid;
+    }
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], WIDE_NW);
+      mbar_init(&empty[s], WIDE_CW);
     }
+    for (int j = 0; j < K; ++j) {
+      mbar_init(&dotdone[j], WIDE_CW);
+      mbar_init(&ydone[j], 1);
+    }
+    published = 0;
     fence_mbar_init();
   }
+  if (warp == 0) {  // the whole TMEM (one CTA per SM); warp 0 also frees it
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&tmem_base_sh)),
+                 "n"(WIDE_TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+
+  // prologue (consumer warps): the v slice, this slice's shares of Obar . v and (F/2) . v
+  if (warp < WIDE_CW) {
+    for (int u = W + tid; u <= WM; u += NTC) vsl[u] = make_double2(0.0, 0.0);  // past the slice: 0
+    S sp = T::zero();
+    double gp = 0.0;
+    for (int u = tid; u < W; u += NTC) {
+      const double2 v = load_vec_unit<CPLX>(a.v_re, a.v_im, col0 + u);
+      vsl[u] = v;
+      if (a.obar) T::dot_acc(sp, a.obar[col0 + u], v);
+      if (a.hf_re) {
+        const double2 h = load_vec_unit<CPLX>(a.hf_re, a.hf_im, col0 + u);
+        gp = fma(h.x, v.x, gp);
+        gp = fma(h.y, v.y, gp);
+      }
+    }
+    sp = warp_sum<CPLX>(sp);
+    gp = warp_sum<false>(gp);
+    if (lane == 0) {
+      shs[warp] = sp;
+      shg[warp] = gp;
+    }
+    named_bar_sync(1, NTC);
+    if (tid == 0) {
+      S s_c = T::zero();
+      double g_c = 0.0;
+      for (int w = 0; w < WIDE_CW; ++w) {
+        s_c = T::add(s_c, shs[w]);
+        g_c += shg[w];
+      }
+      s_c_sh = s_c;
+      st_ll(a.gpart + c, g_c, WIDE_GPART_TAG);  // read by CTA 0 at the end
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
   // ------------------------------------------------------------ producer --
-  // item sequence: D(0), then for each b: D(b+1) (if any), A(b)
-  if (warp == WIDE_NW) {
+  if (warp == W_PROD) {
     if (lane == 0) {
       const uint32_t slice_bytes = (uint32_t)W * 16u;
-      int s = 0, ph = 0;
-      int64_t issued = 0;
-      auto stream_block = [&](int b) {
-        const int64_t r0 = (int64_t)b * R;
-        const int rows = (int)min((int64_t)R, N - r0);
-        for (int r = 0; r < rows; r += RB) {  // one stage = up to RB row slices
-          const int rs = min(RB, rows - r);
-          if (issued >= NS) mbar_wait_bounded(&empty[s], ph ^ 1, a.error);
-          mbar_arrive_expect_tx(&full[s], slice_bytes * (uint32_t)rs);
-          for (int i = 0; i < rs; ++i)
-            bulk_g2s(ring + ((size_t)s * RB + i) * WM, a.O + (r0 + r + i) * a.ld_u + col0, slice_bytes, &full[s]);
-          ++issued;
-          if (++s == NS) {
-            s = 0;
-            ph ^= 1;
-          }
-        }
-      };
-      stream_block(0);
       for (int b = 0; b < NB; ++b) {
-        if (b + 1 < NB) stream_block(b + 1);
-        stream_block(b);
+        const int s = b % NS;
+        if (b >= NS) mbar_wait(&empty[s], ((b / NS) & 1) ^ 1);
+        const int64_t r0 = (int64_t)b * RS;
+        const int rows = (int)min((int64_t)RS, N - r0);
+        WIDE_STAMP(b, 0);
+        mbar_arrive_expect_tx(&full[s], slice_bytes * (uint32_t)rows);
+        for (int i = 0; i < rows; ++i)
+          bulk_g2s(ring + ((size_t)s * RS + i) * WM, a.O + (r0 + i) * a.ld_u + col0, slice_bytes, &full[s]);
       }
     }
     return;
   }
 
-  // ----------------------------------------------------------- consumers --
-  // v slice -> smem; this slice's shares of Obar . v and (F/2) . v
-  S sp = T::zero();
-  double gp = 0.0;
-  for (int u = tid; u < W; u += WIDE_NT) {
-    const double2 v = load_vec_unit<CPLX>(a.v_re, a.v_im, col0 + u);
-    vs[u] = v;
-    if (a.obar) T::dot_acc(sp, a.obar[col0 + u], v);
-    if (a.hf_re) {
-      const double2 h = load_vec_unit<CPLX>(a.hf_re, a.hf_im, col0 + u);
-      gp = fma(h.x, v.x, gp);
-      gp = fma(h.y, v.y, gp);
+  // ----------------------------------------------------------- publisher --
+  if (warp == W_PUB) {
+    const S s_c = s_c_sh;
+    for (int b = 0; b < NB; ++b) {
+      const int j = b % K;
+      mbar_wait(&dotdone[j], (b / K) & 1);
+      if (lane < RS) {
+        S t = T::zero();
+        for (int q = 0; q < Q; ++q) t = T::add(t, pd[(j * RS + lane) * Q + q]);
+        st_ll_s<CPLX>(a.part + (((size_t)(b % WIDE_NBUF) * RS + lane) * G + c) * SW, T::sub(t, s_c), (uint32_t)b + 1);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        published = b + 1;
+        WIDE_STAMP(b, 2);
+      }
     }
+    return;
   }
-  sp = warp_sum<CPLX>(sp);
-  gp = warp_sum<false>(gp);
-  if (lane == 0) {
-    shs[warp] = sp;
-    shg[warp] = gp;
-  }
-  named_bar_sync(1, WIDE_NT);
-  S s_c = T::zero();
-  double g_c = 0.0;
-  for (int w = 0; w < WIDE_NW; ++w) {
-    s_c = T::add(s_c, shs[w]);
-    g_c += shg[w];
-  }
-  if (tid == 0) a.gpart[c] = g_c;  // published with the first arrive
 
+  // --------------------------------------------------------- aggregators --
+  // row r of the matrix is aggregated by CTA r % G: one row's G partials per
+  // visit, two per aggregator lane
+  if (warp >= W_AGG && warp < W_RED) {
+    constexpr int AL = WIDE_AW * 32;            // aggregator lanes
+    const int al = (warp - W_AGG) * 32 + lane;  // partials al, al + AL
+    for (int64_t r = c; r < N; r += G) {
+      const int b = (int)(r / RS), i = (int)(r - (int64_t)b * RS);
+      // pace: start once this CTA has published block b itself (the others are
+      // close); a row comes up every ~G / RS blocks, so sleep long
+      while (published <= b) __nanosleep(256);
+      const uint32_t tag = (uint32_t)b + 1;
+      const ulonglong2* src = a.part + ((size_t)(b % WIDE_NBUF) * RS + i) * G * SW;
+      S x[WIDE_QPL];
+      uint32_t pending = 0;  // bit j: record al + AL j not seen yet
+#pragma unroll
+      for (int j = 0; j < WIDE_QPL; ++j) {
+        x[j] = T::zero();
+        if (al + AL * j < G) pending |= 1u << j;
+      }
+      while (true) {
+#pragma unroll
+        for (int j = 0; j < WIDE_QPL; ++j)
+          if (pending & (1u << j))
+            if (ld_ll_s<CPLX>(src + (size_t)(al + AL * j) * SW, tag, x[j])) pending &= ~(1u << j);
+        if (__all_sync(0xffffffffu, pending == 0)) break;
+        __nanosleep(a.poll_ns);
+      }
+      // fixed order: per lane j = 0, 1, ..., butterfly, then the aggregator warps in order
+      S t = x[0];
+#pragma unroll
+      for (int j = 1; j < WIDE_QPL; ++j) t = T::add(t, x[j]);
+      t = warp_sum<CPLX>(t);
+      if (lane == 0) shagg[warp - W_AGG] = t;
+      named_bar_sync(3, WIDE_AW * 32);
+      if (warp == W_AGG && lane == 0) {
+        S tt = T::zero();
+        for (int w = 0; w < WIDE_AW; ++w) tt = T::add(tt, shagg[w]);
+        st_ll_s<CPLX>(a.fin + ((size_t)(b % WIDE_NBUF) * RS + i) * SW, tt, tag);
+      }
+      named_bar_sync(3, WIDE_AW * 32);  // shagg reused by the next row
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------ reducers --
+  if (warp >= W_RED) {
+    const int k = warp - W_RED;
+    S ysum = T::zero();
+    for (int b = k; b < NB; b += WIDE_RW) {
+      const int j = b % K;
+      const int64_t r0 = (int64_t)b * RS;
+      const int rows = (int)min((int64_t)RS, N - r0);
+      const uint32_t tag = (uint32_t)b + 1;
+      // the row's coefficient loads while the exchange completes
+      const S cf = (lane < rows) ? coeff[r0 + lane] : T::zero();
+      const S ya = (yadd && lane < rows) ? yadd[r0 + lane] : T::zero();
+      const ulonglong2* src = a.fin + ((size_t)(b % WIDE_NBUF) * RS + lane) * SW;
+      S t = T::zero();
+      bool ok = lane >= rows;
+      while (published <= b) __nanosleep(64);  // no total before this CTA's own share
+      const long long t0 = clock64();
+      while (true) {
+        if (!ok) ok = ld_ll_s<CPLX>(src, tag, t);
+        if (__all_sync(0xffffffffu, ok)) break;
+        if (clock64() - t0 > (1LL << 36)) __trap();  // ~30 s: a lost CTA; fail loudly, never hang
+        __nanosleep(a.poll_ns);
+      }
+      if (lane == 0) WIDE_STAMP(b, 3);
+      S y = T::mul(cf, t);
+      if (yadd) y = T::add(y, ya);
+      if (lane < rows) ys[j * RS + lane] = y;
+      for (int i = 0; i < rows; ++i) ysum = T::add(ysum, T::shfl(y, i));  // row order
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&ydone[j]);
+        WIDE_STAMP(b, 4);
+      }
+    }
+    if (lane == 0) shy[k] = ysum;
+    named_bar_sync(2, (WIDE_CW + WIDE_RW) * 32);  // epilogue: shy complete
+    return;
+  }
+
+  // ----------------------------------------------------------- consumers --
+  // warp w: part pq = w % Q of rows rg RPW .. rg RPW + RPW - 1 (rg = w / Q) of every block
+  const int rg = warp / Q;
+  const int pq = warp % Q;
+  const int u0p = pq * PU;
+  const int u1p = min(W, u0p + PU);
+  // this warp's TMEM: lane quarter warp % 4, column half warp / 4, K slots of TMW words
+  const uint32_t tm = tmem_base_sh + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * WIDE_TM_COLS_PER_WARP);
   double2 acc[UPL];
 #pragma unroll
   for (int k = 0; k < UPL; ++k) acc[k] = make_double2(0.0, 0.0);
-  int s = 0, ph = 0;
-  auto advance = [&]() {
-    if (++s == NS) {
-      s = 0;
-      ph ^= 1;
-    }
-  };
-  const S* coeff = reinterpret_cast<const S*>(a.coeff);
-  S ysum = T::zero();  // lane 0 of each warp: sum of the y it formed
-
-  auto phase_d = [&](int b) {
-    const int64_t r0 = (int64_t)b * R;
-    const int rows = (int)min((int64_t)R, N - r0);
-    S* tp = tpart + ((size_t)(b & 3) * R) * G;
-    for (int r = 0; r < rows; r += RB) {
-      mbar_wait_bounded(&full[s], ph, a.error);
-      // this warp's rows of the stage: warp, warp + NW (rpw <= 2); two partial
-      // accumulators per row keep the FMA chains short
-      S t[2][2];
+  int nd = 0, na = 0;
+  int elig = -1;  // debug trace only
+  // ring positions kept incrementally (no integer division in the polling loop):
+  // nd -> stage sd / parity pdp and slot jd; na -> slot ja / parity pap
+  int sd = 0, pdp = 0, jd = 0, ja = 0, pap = 0;
+  // every lane probes (non-blocking test_wait: a suspending try_wait on a
+  // barrier that is not ready would delay the other one); a barrier counts as
+  // passed only when all lanes saw it complete, each lane then holding its
+  // own acquire of the mbarrier phase
+  auto ready = [&](uint64_t* bar, int ph) { return __all_sync(0xffffffffu, mbar_test_wait(smem_addr(bar), ph)); };
+  while (na < NB) {
+    if (na < nd) {  // accumulate the oldest parked block once its y is there
+      const int j = ja;
+      if (ready(&ydone[j], pap)) {
+        const int64_t r0 = (int64_t)na * RS + rg * RPW;
+        if (r0 < N) {
+          tm_wait_st();  // the park of this slot has landed
 #pragma unroll
-      for (int i = 0; i < 2; ++i) t[i][0] = t[i][1] = T::zero();
+          for (int r = 0; r < RPW; ++r) {
+            if (r0 + r < N) {
+              double2 x[UPL];
+              tm_fetch<UPL>(tm + (uint32_t)(j * TMW + r * wide_tm_words(UPL)), x);
+              const S y = ys[j * RS + rg * RPW + r];
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int rr = warp + i * WIDE_NW;
-        if (i < rpw && r + rr < rows) {
-          const double2* row = ring + ((size_t)s * RB + rr) * WM;
-#pragma unroll
-          for (int k = 0; k < UPL; ++k) {
-            const int u = lane + 32 * k;
-            if (u < W) T::dot_acc(t[i][k & 1], row[u], vs[u]);
+              for (int k = 0; k < UPL; ++k) T::axpy(acc[k], x[k], y);  // x = 0 past the part
+            }
           }
         }
-      }
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int rr = warp + i * WIDE_NW;
-        if (i < rpw && r + rr < rows) {
-          const S tt = warp_sum<CPLX>(T::add(t[i][0], t[i][1]));
-          if (lane == 0) tp[(size_t)(r + rr) * G + c] = T::sub(tt, s_c);
+        if (lane == 0 && warp == 0) WIDE_STAMP(na, 5);
+        ++na;
+        if (++ja == K) {
+          ja = 0;
+          pap ^= 1;
         }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-      advance();
-    }
-    named_bar_sync(1, WIDE_NT);  // every warp's partials written
-    if (tid == 0) red_release_add(a.counter + b, 1u);
-  };
-
-  auto phase_a = [&](int b) {
-    const int64_t r0 = (int64_t)b * R;
-    const int rows = (int)min((int64_t)R, N - r0);
-    if (tid == 0) {  // wait until every CTA has published block b
-      // one counter per block: a single running total could reach G (b + 1)
-      // with a fast CTA's later arrivals standing in for a slow CTA's missing
-      // one, and block b's partials would be read before they were all written
-      const unsigned int target = (unsigned int)G;
-      const long long t0 = clock64();
-      while (ld_acquire_u32(a.counter + b) < target) {
-        if (clock64() - t0 > (1LL << 36)) {  // ~30 s: never expected; no hang
-          atomicExch(a.error, 1);
-          break;
-        }
+        continue;
       }
     }
-    named_bar_sync(1, WIDE_NT);
-    const S* tp = tpart + ((size_t)(b & 3) * R) * G;
-    // 4 rows per warp at a time: their partial loads are independent (in flight together)
-    for (int r = warp * 4; r < rows; r += WIDE_NW * 4) {
-      S t[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) t[i] = T::zero();
-      for (int q = lane; q < G; q += 32) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          if (r + i < rows) t[i] = T::add(t[i], __ldcg(tp + (size_t)(r + i) * G + q));
+    if (nd < NB && nd - na < K) {  // dot of the next block once it has landed, then park it
+      const int s = sd;
+      if (a.trace && warp == 0 && lane == 0 && elig != nd) {  // debug: when block nd became eligible
+        elig = nd;
+        WIDE_STAMP(nd, 6);
       }
+      if (ready(&full[s], pdp)) {
+        const int j = jd;
+        const int64_t r0 = (int64_t)nd * RS + rg * RPW;
+        S t[RPW];
+        // row by row: shared memory -> registers -> dot -> TMEM (the TMEM
+        // stores are asynchronous, so the next row's loads overlap them)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        if (r + i >= rows) break;
-        const S tt = warp_sum<CPLX>(t[i]);
-        S y = T::mul(coeff[r0 + r + i], tt);
-        if (a.yadd) y = T::add(y, reinterpret_cast<const S*>(a.yadd)[r0 + r + i]);
+        for (int r = 0; r < RPW; ++r) {
+          const double2* row = ring + ((size_t)s * RS + rg * RPW + r) * WM;
+          const bool live = r0 + r < N;
+          double2 x[UPL];
+#pragma unroll
+          for (int k = 0; k < UPL; ++k) {
+            const int u = u0p + lane + 32 * k;
+            x[k] = (live && u < u1p) ? row[u] : make_double2(0.0, 0.0);
+          }
+          S t0 = T::zero(), t1 = T::zero();
+#pragma unroll
+          for (int k = 0; k < UPL; ++k) T::dot_acc((k & 1) ? t1 : t0, x[k], vsl[min(u0p + lane + 32 * k, WM)]);
+          t[r] = T::add(t0, t1);
+          if (live) tm_park<UPL>(tm + (uint32_t)(j * TMW + r * wide_tm_words(UPL)), x);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);  // the stage is in registers / TMEM: refill it
+#pragma unroll
+        for (int m = 16; m >= 1; m >>= 1)  // the RPW butterflies interleaved
+#pragma unroll
+          for (int r = 0; r < RPW; ++r) t[r] = T::add(t[r], T::shfl_xor(t[r], m));
         if (lane == 0) {
-          ys[r + i] = y;
-          ysum = T::add(ysum, y);
+#pragma unroll
+          for (int r = 0; r < RPW; ++r) pd[(j * RS + rg * RPW + r) * Q + pq] = t[r];
+          mbar_arrive(&dotdone[j]);
+          if (warp == 0) WIDE_STAMP(nd, 1);
         }
+        ++nd;
+        if (++sd == NS) {
+          sd = 0;
+          pdp ^= 1;
+        }
+        if (++jd == K) jd = 0;
+        continue;
       }
     }
-    named_bar_sync(1, WIDE_NT);
-    for (int r = 0; r < rows; r += RB) {
-      mbar_wait_bounded(&full[s], ph, a.error);
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int rr = warp + i * WIDE_NW;
-        if (i < rpw && r + rr < rows) {
-          const double2* row = ring + ((size_t)s * RB + rr) * WM;
-          const S y = ys[r + rr];
-#pragma unroll
-          for (int k = 0; k < UPL; ++k) {
-            const int u = lane + 32 * k;
-            if (u < W) T::axpy(acc[k], row[u], y);
-          }
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-      advance();
-    }
-    named_bar_sync(1, WIDE_NT);  // ys reused by the next block
-  };
-
-  phase_d(0);
-  for (int b = 0; b < NB; ++b) {
-    if (b + 1 < NB) phase_d(b + 1);
-    phase_a(b);
+    if (a.spin_ns) __nanosleep(a.spin_ns);  // nothing ready: back off
   }
 
-  // the warps' accumulators meet in shared memory (ring is free: every stage consumed)
-  double2* red = ring;  // [NW][WM]
-#pragma unroll
-  for (int k = 0; k < UPL; ++k) {
-    const int u = lane + 32 * k;
-    if (u < W) red[(size_t)warp * WM + u] = acc[k];
+  // TMEM is no longer needed: warp 0 frees it once every consumer warp is done
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  named_bar_sync(1, NTC);
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base_sh), "n"(WIDE_TMEM_COLS)
+                 : "memory");
   }
-  if (lane == 0) shs[warp] = ysum;
-  named_bar_sync(1, WIDE_NT);
+
+  // the part accumulators of the RS warps sharing a part meet in shared memory
+  // (the ring is free: every stage consumed), in row order
+  named_bar_sync(2, (WIDE_CW + WIDE_RW) * 32);
+  double2* red = ring;  // [CW][32 * UPL] (ring_bytes covers it)
+  const int pitch = 32 * UPL;
+#pragma unroll
+  for (int k = 0; k < UPL; ++k) red[(size_t)warp * pitch + lane + 32 * k] = acc[k];
   S Y = T::zero();  // sum over all rows of y, the same fixed order in every CTA
-  for (int w = 0; w < WIDE_NW; ++w) Y = T::add(Y, shs[w]);
+  for (int k = 0; k < WIDE_RW; ++k) Y = T::add(Y, shy[k]);
+  named_bar_sync(1, NTC);
   const double uu = (a.hf_re && a.u0) ? *a.u0 : 0.0;
-  for (int u = tid; u < W; u += WIDE_NT) {
-    double2 o = red[u];
-    for (int w = 1; w < WIDE_NW; ++w) {
-      o.x += red[(size_t)w * WM + u].x;
-      o.y += red[(size_t)w * WM + u].y;
+  for (int u = tid; u < W; u += NTC) {
+    const int q = u / PU, j = u - q * PU;
+    double2 o = red[(size_t)q * pitch + j];
+    for (int i = 1; i < WIDE_CW / Q; ++i) {  // the row groups sharing part q, in order
+      const double2 x = red[(size_t)(i * Q + q) * pitch + j];
+      o.x += x.x;
+      o.y += x.y;
     }
     const int64_t gu = col0 + u;
     if (a.obar) {
@@ -337,11 +579,17 @@ __global__ void __launch_bounds__(WIDE_NT + 32, 1) k_wide(const WideArgs a) {
       if (a.out_im) a.out_im[gu] = o.y;
     }
   }
-  if (a.out0 && c == 0 && tid == 0) {  // every CTA arrived for the last block: gpart complete
+  if (a.out0 && c == 0 && warp == 0) {  // (F/2) . u over the slices, fixed order
     double g = 0.0;
-    if (a.hf_re)
-      for (int q = 0; q < G; ++q) g += __ldcg(a.gpart + q);
-    *a.out0 = g;
+    if (a.hf_re) {
+      for (int q0 = 0; q0 < G; q0 += 32) {
+        double x = 0.0;
+        if (q0 + lane < G)
+          while (!ld_ll(a.gpart + q0 + lane, WIDE_GPART_TAG, x)) __nanosleep(32);
+        g += warp_sum<false>(x);
+      }
+    }
+    if (lane == 0) *a.out0 = g;
   }
 }
 

@@ -316,7 +316,7 @@ def test_workspace_and_output_canaries(E, kind):
         en = E.estimate_energy(b)
     nbytes = b.mvp_workspace().numel()
     big = torch.full((nbytes + guard,), 0xA5, dtype=torch.uint8, device="cuda")
-    b._ws = big[:nbytes]
+    b._ws[b._stream()] = big[:nbytes]  # this stream's workspace, exactly sized
     ld, p = b.ld, b.param_count
     herm = b.kind == E.KIND_HERMITIAN
     rows_v = 2 if herm else 1
@@ -389,7 +389,7 @@ def test_connected_workspace_canary(E, mode):
     nbytes = cache.workspace(batch).numel()
     guard = 1 << 20
     big = torch.full((nbytes + guard,), 0x5A, dtype=torch.uint8, device="cuda")
-    cache._ws = big[:nbytes]
+    cache._ws[batch._stream()] = big[:nbytes]  # this stream's workspace, exactly sized
     got = np.asarray(E.connected_heff_matvec(batch, en, cache, v))
     torch.cuda.synchronize()
     assert bool((big[nbytes:] == 0x5A).all()), "connected workspace overrun"
@@ -397,10 +397,11 @@ def test_connected_workspace_canary(E, mode):
 
 
 def test_wide_path_many_blocks_bitwise_stable(E):
-    """The single-read wide path (IRL_MVP_WIDE) synchronises its persistent
-    grid once per row block through per-block counters and a 4-deep partials
-    buffer; with many blocks, repeated products must be bit-identical and match
-    the oracle (a missed arrival shows up as a small, varying error)."""
+    """The single-read wide path (IRL_MVP_WIDE) exchanges every row block's
+    dots across its persistent grid through tagged records in a 64-slot ring
+    (csrc/wide.cuh); with many blocks (ring wrap-around), repeated products must
+    be bit-identical and match the two-pass product (a record read before its
+    writer finished shows up as a small, varying error)."""
     import torch
 
     from paper_2601_01437_b200 import ansatz as A, synthetic as S
@@ -414,7 +415,7 @@ def test_wide_path_many_blocks_bitwise_stable(E):
     first = E.heff_matvec(b, en, v, mode=4)
     two = E.heff_matvec(b, en, v, mode=2)
     assert rel(first.cpu().numpy(), two.cpu().numpy()) < 1e-12
-    for _ in range(12):
+    for _ in range(24):
         assert torch.equal(E.heff_matvec(b, en, v, mode=4), first)
 
 
