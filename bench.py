@@ -2,12 +2,18 @@
 """Benchmark of the IRL-SR hot path on B200 (contract: see DESIGN.md §Measurement).
 
 Metric (BASELINE.json): S*v + H_eff*v MVPs/sec (+ % of HBM roofline, + IRL
-solve wall time) on one B200.  Workload: config 2 (RBM f64, N_s = 65536,
-P = 6600, O = 3.46 GB resident in HBM, larger than the 126 MB L2 so no flush
-is needed).  One step = one H_eff*v product + one S*v product on fresh
-random vectors (2 MVPs).
+solve wall time) on one B200.  Headline workload: config 5, the largest
+single-GPU configuration (shallow MLP, N_s = 65536, P = 208897, O = 109.5 GB
+stored in HBM, far larger than the 126 MB L2).  One step = one H_eff*v product
++ one S*v product on fresh random vectors (2 MVPs).  Beside the headline the
+line carries, for every BASELINE config (cfg1..cfg5): the stored-O product
+(AUTO path) with its one-read and two-pass roofline fractions, the on-the-fly
+product (O regenerated on FP64 tensor cores), the IRL solve wall time and
+matvec count in both modes, and the CPU reference path (the oracle port of
+est.heff_matvec, timed on this box's host cores: full N_s for cfg1-3, N_s/16
+extrapolated x16 for cfg4/5 as BASELINE.md §3 prescribes).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--impl ours|reference]
 
 --impl reference times the reference's algorithm on the host CPU: the
 reference package cannot travel to the GPU box, so the oracle port
@@ -18,6 +24,7 @@ including its per-call centring copy) is timed on a row sample.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -37,9 +44,9 @@ UNIT = "MVP/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
-    ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--mode", type=int, default=0, help="0 auto, 1 fused single pass, 2 two-pass")
     ap.add_argument("--no-irl", action="store_true")
@@ -48,6 +55,9 @@ def parse():
     ap.add_argument("--no-connected", action="store_true")
     ap.add_argument("--partners", type=int, default=4, help="synthetic connected partners per row")
     ap.add_argument("--no-eloc", action="store_true")
+    ap.add_argument("--configs", default="1,2,3,4,5", help="per-config sub-records (empty: none)")
+    ap.add_argument("--ref-budget", type=float, default=180.0,
+                    help="--impl reference: seconds of CPU work the timed + warm-up steps may take")
     return ap.parse_args()
 
 
@@ -170,13 +180,24 @@ def measured_peak_gbs():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(cfg_index: int):
-    """Per-launch dram bytes of the dominant kernel from the committed ncu summary, if any."""
-    path = os.path.join(ROOT, "profiles", "traffic.json")
+def measured_fp64_tensor_tflops():
+    """DMMA (mma.sync f64) peak measured on this pool by tools/fp64_peak.cu
+    (profiles/r02_fp64_peak.json); the on-the-fly GEMMs and the MLP forward
+    are bound by it."""
     try:
-        with open(path) as fh:
-            data = json.load(fh)
-        return data.get(f"cfg{cfg_index}")
+        with open(os.path.join(ROOT, "profiles", "r02_fp64_peak.json")) as fh:
+            d = json.load(fh)
+        return float(d["dmma_tflops"]), "measured (profiles/r02_fp64_peak.json)"
+    except Exception:
+        return 37.0, "fallback (round-1 tools/fp64_peak.cu run)"
+
+
+def ncu_traffic(workload: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
+    kernel, from the committed ncu --set full capture (profiles/traffic.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            return json.load(fh).get(workload)
     except Exception:
         return None
 
@@ -205,35 +226,66 @@ class CpuReference:
         self.oest = oest
 
     def step(self) -> float:
-        """One H_eff*v + one S*v; returns seconds."""
+        """One H_eff*v + one S*v (each with the reference's per-call centring
+        copy, est:166-168); returns seconds."""
         t0 = time.perf_counter()
         self.oest.heff(self.w, self.e, self.o, self.mean, self.v)
         self.oest.qgt(self.w, self.o, self.v)
         return time.perf_counter() - t0
 
 
-def cpu_reference_sample(cfg, n_sub: int, reps: int = 3):
-    """Median seconds per MVP of the oracle port at n_sub rows."""
+def cpu_rows(cfg) -> int:
+    """Rows the CPU reference is timed on: all of them for cfg1-3; N_s/16 for
+    cfg4/5, whose centring copies do not fit host RAM at full N_s."""
+    return cfg.n_rows if cfg.index <= 3 else cfg.n_rows // 16
+
+
+def cpu_leg(cfg, n_sub: int | None = None, reps: int = 1) -> dict:
+    """The oracle port on n_sub rows: one untimed step, then `reps` timed steps."""
+    n_sub = n_sub or cpu_rows(cfg)
     ref = CpuReference(cfg, n_sub)
     ref.step()
-    return statistics.median(ref.step() / 2.0 for _ in range(reps))
+    per = [ref.step() for _ in range(reps)]
+    del ref
+    gc.collect()
+    ms_mvp = statistics.median(per) / 2 * 1e3
+    x = cfg.n_rows / n_sub
+    return {"value": 1e3 / (ms_mvp * x), "unit": UNIT, "cores": cpu_cores(), "kind": "port",
+            "rows_timed": n_sub, "extrapolated_x": x, "ms_per_mvp_timed": ms_mvp,
+            "sample": (f"oracle port of est.heff_matvec (S*v via e_loc = 1), {reps} timed step(s) of H + S on "
+                       f"{n_sub} of {cfg.n_rows} rows, full P = {cfg.param_count}"
+                       + (f", extrapolated x{x:g} in N_s" if x != 1 else ", full N_s")
+                       + f"; numpy/BLAS threads = all {cpu_cores()} cores")}
 
 
 def run_reference(args):
+    """The reference's algorithm (oracle port) on the host cores, on our arm's
+    workload, metric and unit.  Each step is H + S on a row sample; the sample
+    is N_s/16 for cfg4/5, all rows for cfg1-3, shrunk further
+    only if (steps + warmup) steps would exceed --ref-budget seconds."""
     world, rank, _ = dist_env()
     if rank != 0:
         return 0
     from paper_2601_01437_b200 import synthetic as S
 
     cfg = S.CONFIGS[args.config]
-    n_sub = min(cfg.n_rows, 2048)
-    scale = cfg.n_rows / n_sub
+    n_sub = cpu_rows(cfg)
+    # calibrate the per-row cost on a small sample, then bound the whole run
+    n_cal = min(n_sub, 1024)
+    cal = CpuReference(cfg, n_cal)
+    cal.step()
+    per_row = cal.step() / n_cal
+    del cal
+    budget_rows = int(args.ref_budget / max(args.steps + args.warmup, 1) / per_row)
+    if budget_rows < n_sub:
+        n_sub = max(n_cal, 1 << int(np.log2(max(budget_rows, 1))))
     ref = CpuReference(cfg, n_sub)
     for _ in range(args.warmup):
         ref.step()
     per_step = [ref.step() for _ in range(args.steps)]
-    t_step_full = statistics.fmean(per_step) * scale
-    value = 2.0 / t_step_full
+    t_step = statistics.fmean(per_step)
+    scale = cfg.n_rows / n_sub
+    value = 2.0 / (t_step * scale)
     cores = cpu_cores()
     line = {
         "impl": "reference",
@@ -243,21 +295,27 @@ def run_reference(args):
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": t_step_full * 1e3,
+        "ms_per_step": t_step * 1e3,
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "c128" if cfg.complex_params else "f64",
         "data": "synthetic (seeded, BASELINE.json shapes)",
-        "config": {"workload": cfg.name, "n_rows": cfg.n_rows, "param_count": cfg.param_count},
+        "config": {"workload": cfg.name, "n_rows": cfg.n_rows, "param_count": cfg.param_count,
+                   "rows_timed": n_sub, "extrapolated_x": scale,
+                   "ms_per_step_note": "ms_per_step is the measured time of one timed step on rows_timed rows; "
+                                       "value scales it x extrapolated_x to the full N_s (linear in N_s)"},
         "cpu_baseline": {
             "value": value,
             "unit": UNIT,
             "cores": cores,
             "kind": "port",
-            "sample": (f"oracle port of est.heff_matvec (S*v via e_loc=1) on the first {n_sub} of {cfg.n_rows} "
-                       f"rows, full P={cfg.param_count}; per-step time x{scale:g} (linear in N_s); numpy/BLAS "
-                       f"threads = all {cores} cores"),
+            "rows_timed": n_sub,
+            "extrapolated_x": scale,
+            "sample": (f"oracle port of est.heff_matvec (S*v via e_loc=1, per-call centring copy) on the first "
+                       f"{n_sub} of {cfg.n_rows} rows, full P={cfg.param_count}"
+                       + (f"; per-step time x{scale:g} (linear in N_s)" if scale != 1 else "; full N_s")
+                       + f"; numpy/BLAS threads = all {cores} cores"),
         },
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -266,6 +324,188 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------- ours -------
+LAUNCHES_PER_MVP = {"wide": 1, "fused": 2, "rows": 2, "two_pass": 3}
+
+
+def _arch(A, cfg):
+    if cfg.model == "rbm":
+        return A.RBMArchitecture(cfg.n_inputs, cfg.hidden, cfg.complex_params)
+    return A.MLPArchitecture(cfg.n_inputs, cfg.hidden)
+
+
+def _vectors(torch, batch, dev, n, seed):
+    """n random product inputs (zero padding) and 2 outputs, in the kernels' layout."""
+    from paper_2601_01437_b200 import estimators as E
+
+    P, ld = batch.param_count, batch.ld
+    herm = batch.kind == E.KIND_HERMITIAN
+    gen = torch.Generator(device=dev).manual_seed(seed)
+    if herm:
+        vin = torch.randn((n, 2, ld), dtype=torch.float64, device=dev, generator=gen)
+        vin[:, :, P:] = 0
+        vout = torch.empty((2, 2, ld), dtype=torch.float64, device=dev)
+    else:
+        vin = torch.randn((n, ld), dtype=torch.float64, device=dev, generator=gen)
+        vin[:, P:] = 0
+        vout = torch.empty((2, ld), dtype=torch.float64, device=dev)
+
+    def apply(i, coeff, slot, mode=0, **kw):
+        if herm:
+            E._apply(batch, coeff, (vin[i, 0], vin[i, 1]), (vout[slot, 0], vout[slot, 1]), mode=mode, **kw)
+        else:
+            E._apply(batch, coeff, vin[i], vout[slot], mode=mode, **kw)
+
+    return apply
+
+
+def graph_timed(torch, fn, l2buf, k=3, reps=5):
+    """Device time of one fn() after a write flush of L2, free of host launch
+    overhead: CUDA graphs of k x (flush, fn) and k x flush, replayed under
+    events; the difference over k.  (Event-timing one eager call after a
+    flush measures the Python/ctypes launch path when the product is short.)"""
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        fn()
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+
+    def build(with_fn):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(k):
+                l2buf.add_(1.0)
+                if with_fn:
+                    fn()
+        return g
+
+    def run(g):
+        out = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            g.replay()
+            b.record()
+            torch.cuda.synchronize()
+            out.append(a.elapsed_time(b))
+        return statistics.median(out)
+
+    g_both, g_flush = build(True), build(False)
+    t = (run(g_both) - run(g_flush)) / k
+    del g_both, g_flush
+    return t
+
+
+def irl_solve(torch, OPT, batch, cfg, energy):
+    conf = OPT.OptimizerConfig(m=cfg.m, max_restarts=cfg.max_restarts)
+    OPT.solve_step(batch, conf, seed=cfg.lanczos_seed, energy=energy)  # warm (captures the sweep graphs)
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    i0 = time.perf_counter()
+    ev0.record()
+    res = OPT.solve_step(batch, conf, seed=cfg.lanczos_seed, energy=energy)
+    ev1.record()
+    torch.cuda.synchronize()
+    return {"wall_ms": (time.perf_counter() - i0) * 1e3, "device_ms": ev0.elapsed_time(ev1),
+            "n_matvec": res.n_matvec, "lambda_min": res.lambda_min, "converged": res.converged,
+            "m": cfg.m, "max_restarts": cfg.max_restarts}
+
+
+def config_record(torch, cfg, dev, peak, dmma_peak, l2buf, with_irl=True, extra=None):
+    """Per-config sub-record: stored-O AUTO product (device time after an L2
+    write flush), its roofline fractions, the on-the-fly product, the IRL solve
+    in both modes.  Everything is freed before returning."""
+    from paper_2601_01437_b200 import _lib, ansatz as A, estimators as E, optimizer as OPT, synthetic as S
+
+    inp = S.make_inputs(cfg)
+    arch = _arch(A, cfg)
+    params = A.AnsatzParameters(arch, inp.theta)
+    rec = {"workload": cfg.name, "n_rows": cfg.n_rows, "param_count": cfg.param_count,
+           "dtype": "c128" if cfg.complex_params else "f64"}
+    b_el = 16 if cfg.complex_params else 8
+    o_bytes = cfg.n_rows * cfg.param_count * b_el
+    # ---- stored O
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    batch = A.build_batch(params, inp.x, inp.e_loc, device=dev, mode="stored")
+    torch.cuda.synchronize()
+    rec["obuild_wall_ms"] = (time.perf_counter() - t0) * 1e3
+    en = E.estimate_energy(batch)
+    coeff = batch.coefficients(en.mean)
+    batch.obar()
+    apply = _vectors(torch, batch, dev, 2, 77 + cfg.index)
+    plan = _lib.mvp_plan(batch.n_rows, batch.ld, batch.is_complex, 0)
+    ms = graph_timed(torch, lambda: apply(0, coeff, 0), l2buf, k=10 if o_bytes < 1e9 else 3)
+    one = o_bytes / (ms / 1e3) / 1e9
+    rec["stored"] = {"path": plan["path"], "ms_per_product": ms, "mvp_s": 1e3 / ms, "gbs_one_read": one,
+                     "frac_one_read": one / peak, "frac_two_pass": 2 * one / peak,
+                     "frac_two_pass_spec_8tbs": 2 * one / 8000.0, "l2": "256 MB write flush before each product",
+                     "plan": plan}
+    if plan["path"] == "wide":  # the two-pass path beside it, for the record
+        ms2 = graph_timed(torch, lambda: apply(0, coeff, 0, mode=_lib.MVP_TWO_PASS), l2buf,
+                          k=10 if o_bytes < 1e9 else 3)
+        rec["stored"]["two_pass_ms_per_product"] = ms2
+    if with_irl:
+        rec["irl_stored"] = irl_solve(torch, OPT, batch, cfg, en)
+    if extra is not None:
+        extra(batch, params, inp, apply, coeff, rec)
+    del batch, apply, coeff
+    gc.collect()
+    torch.cuda.empty_cache()
+    # ---- on the fly (O never stored)
+    if A.otf_supported(arch):
+        ob = A.build_batch(params, inp.x, inp.e_loc, device=dev, mode="otf")
+        eo = E.estimate_energy(ob)
+        co = ob.coefficients(eo.mean)
+        ob.obar()
+        applo = _vectors(torch, ob, dev, 2, 99 + cfg.index)
+        mso = graph_timed(torch, lambda: applo(0, co, 0), l2buf, k=10)
+        cols = cfg.hidden * (2 if cfg.complex_params else 1)
+        flops = 2.0 * cfg.n_rows * cols * (2 * cfg.n_inputs + 1)  # useful DMMA flops (dot + acc GEMMs)
+        tf = flops / (mso / 1e3) / 1e12
+        rec["otf"] = {"ms_per_product": mso, "mvp_s": 1e3 / mso, "tflops": tf, "frac_fp64_tensor": tf / dmma_peak,
+                      "flops_per_product": flops, "l2": "256 MB write flush before each product"}
+        if with_irl:
+            rec["irl_otf"] = irl_solve(torch, OPT, ob, cfg, eo)
+        del ob, applo, co
+        gc.collect()
+        torch.cuda.empty_cache()
+    return rec
+
+
+def connected_leg(torch, args, dev, cfg, batch, params, inp, apply, coeff, rec):
+    """Connected completion: heff_matvec + heff_offdiag_matvec
+    in one product over a seeded synthetic partner cache."""
+    from paper_2601_01437_b200 import ansatz as A, synthetic as S
+
+    partners, elements, indptr, dist = S.connected_partners(inp.x, args.partners, seed=500 + cfg.index)
+    torch.cuda.synchronize()
+    c0 = time.perf_counter()
+    cache = A.build_connected_cache(params, batch, inp.x, partners, elements, indptr, dist_index=dist)
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - c0
+    for k in range(3):
+        apply(k % 2, coeff, 0, cache=cache)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    ce = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(10)]
+    for k, (a, b) in enumerate(ce):
+        a.record(stream)
+        apply(k % 2, coeff, 0, cache=cache)
+        b.record(stream)
+    torch.cuda.synchronize()
+    c_ms = statistics.median([a.elapsed_time(b) for a, b in ce])
+    b_el = 16 if cfg.complex_params else 8
+    c_bytes = (cache.n_partner + batch.n_rows) * batch.param_count * b_el
+    rec["connected"] = {"ms_per_product": c_ms, "mvp_s": 1e3 / c_ms, "partners_per_row": args.partners,
+                        "n_partner_rows": cache.n_partner, "nnz": int(indptr[-1]), "cache_build_ms": build_s * 1e3,
+                        "alg_bytes": c_bytes, "achieved_gbs": c_bytes / (c_ms / 1e3) / 1e9,
+                        "note": ("connected H_eff v (opt:144-147): partner dot pass over the partner O rows + "
+                                 "per-row CSR kernel + the streaming product with an additive row term; "
+                                 "seeded synthetic single-excitation partners, not a Hamiltonian")}
+    del cache
+
+
 def run_ours(args):
     import torch
 
@@ -276,84 +516,62 @@ def run_ours(args):
 
     from paper_2601_01437_b200 import _lib, ansatz as A, estimators as E, optimizer as OPT, synthetic as S
 
+    peak, peak_src = measured_peak_gbs()
+    dmma_peak, dmma_src = measured_fp64_tensor_tflops()
     cfg = S.CONFIGS[args.config]
     inp = S.make_inputs(cfg)
-    if cfg.model == "rbm":
-        arch = A.RBMArchitecture(cfg.n_inputs, cfg.hidden, cfg.complex_params)
-    else:
-        arch = A.MLPArchitecture(cfg.n_inputs, cfg.hidden)
+    arch = _arch(A, cfg)
     params = A.AnsatzParameters(arch, inp.theta)
     batch = A.build_batch(params, inp.x, inp.e_loc, device=dev)
-    # O-build (K1/K2 + fused stats) timed warm, into the same buffers
+    # O-build (K1/K2 + statistics) timed warm, into the same buffers
     xt = A._x_device(inp.x, arch.n_inputs, dev)
     mean0 = batch._stats_e
     ob_bar, ob_g = batch.colstats(mean0)
     ob_c = batch.gradient_coefficients(mean0)
     torch.cuda.synchronize()
-    ob0 = torch.cuda.Event(enable_timing=True)
-    ob1 = torch.cuda.Event(enable_timing=True)
+    ob0, ob1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ob0.record()
     A.fill_o_rows(params, xt, batch.o_padded, batch.weights, ob_c, ob_bar, ob_g)
     ob1.record()
     torch.cuda.synchronize()
     obuild_ms = ob0.elapsed_time(ob1)
+    del xt, ob_bar, ob_g, ob_c
     energy = E.estimate_energy(batch)
     P, ld, N = batch.param_count, batch.ld, batch.n_rows
     herm = batch.kind == E.KIND_HERMITIAN
+    b_el = 16 if batch.is_complex else 8
     plan = _lib.mvp_plan(N, ld, batch.is_complex, args.mode)
-    launches_per_mvp = 2 if plan["path"] == "fused" else 3
     coef_h = batch.coefficients(energy.mean)
     coef_s = batch.weights if not batch.is_complex else batch.weights.to(torch.complex128)
     batch.obar()
-
-    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
     nvec = 8
-    if herm:
-        vin = torch.randn((nvec, 2, ld), dtype=torch.float64, device=dev, generator=gen)
-        vin[:, :, P:] = 0
-        vout = torch.empty((2, 2, ld), dtype=torch.float64, device=dev)
-    else:
-        vin = torch.randn((nvec, ld), dtype=torch.float64, device=dev, generator=gen)
-        vin[:, P:] = 0
-        vout = torch.empty((2, ld), dtype=torch.float64, device=dev)
-
-    def one(i, coeff, slot):
-        if herm:
-            E._apply(batch, coeff, (vin[i, 0], vin[i, 1]), (vout[slot, 0], vout[slot, 1]), mode=args.mode)
-        else:
-            E._apply(batch, coeff, vin[i], vout[slot], mode=args.mode)
-
-    def step(k):
-        one(k % nvec, coef_h, 0)
-        one((k + 1) % nvec, coef_s, 1)
-
-    barrier = reps.barrier
+    apply = _vectors(torch, batch, dev, nvec, 1234 + rank)
 
     for k in range(args.warmup):
-        step(k)
+        apply(k % nvec, coef_h, 0, mode=args.mode)
+        apply((k + 1) % nvec, coef_s, 1, mode=args.mode)
     torch.cuda.synchronize()
 
-    # ---- device-timed steps (max over ranks)
+    # ---- device-timed steps (max over ranks); O (> L2) is streamed from HBM every product
     stream = torch.cuda.current_stream()
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     per = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(2 * args.steps)]
-    barrier()
+    reps.barrier()
     torch.cuda.synchronize()
     with ClockSampler(torch.cuda.current_device()) as clocks:
         t0.record(stream)
         for k in range(args.steps):
             a, b = per[2 * k]
             a.record(stream)
-            one(k % nvec, coef_h, 0)
+            apply(k % nvec, coef_h, 0, mode=args.mode)
             b.record(stream)
             a, b = per[2 * k + 1]
             a.record(stream)
-            one((k + 1) % nvec, coef_s, 1)
+            apply((k + 1) % nvec, coef_s, 1, mode=args.mode)
             b.record(stream)
         t1.record(stream)
         torch.cuda.synchronize()
-    barrier()
+    reps.barrier()
     elapsed = reps.max(t0.elapsed_time(t1) / 1e3)
     mvp_ms = [a.elapsed_time(b) for a, b in per]
     mvps = 2 * args.steps
@@ -362,177 +580,115 @@ def run_ours(args):
     # ---- end to end through the public API with pinned host vectors
     vh = torch.randn(P, dtype=torch.complex128 if herm else torch.float64, generator=torch.Generator().manual_seed(7))
     vh = vh.pin_memory()
-    e2e_steps = max(args.steps // 2, 5)
+    e2e_steps = max(args.steps // 2, 3)
     for _ in range(max(args.warmup, 3)):  # untimed: also builds each call's captured graph
         E.heff_matvec(batch, energy, vh)
         E.qgt_matvec(batch, vh)
-    barrier()
+    reps.barrier()
     torch.cuda.synchronize()
     h0 = time.perf_counter()
     for _ in range(e2e_steps):
         E.heff_matvec(batch, energy, vh)
         E.qgt_matvec(batch, vh)
     torch.cuda.synchronize()
-    e2e_time = time.perf_counter() - h0
-    barrier()
-    e2e_time = reps.max(e2e_time)
+    e2e_time = reps.max(time.perf_counter() - h0)
+    reps.barrier()
     vbytes = P * (16 if herm else 8)
     e2e = {"value": world * 2 * e2e_steps / e2e_time, "unit": UNIT, "h2d_bytes_per_step": 2 * vbytes,
            "d2h_bytes_per_step": 2 * vbytes,
            "api": "estimators.heff_matvec + qgt_matvec on pinned host tensors (H2D, product, D2H, sync)"}
 
-    # ---- IRL solve wall time (one outer step's eigen-solve + direction)
-    irl = None
-    if not args.no_irl:
-        conf = OPT.OptimizerConfig(m=cfg.m, max_restarts=cfg.max_restarts)
-        OPT.solve_step(batch, conf, seed=cfg.lanczos_seed, energy=energy)  # warm
-        torch.cuda.synchronize()
-        i0 = time.perf_counter()
-        ev0 = torch.cuda.Event(enable_timing=True)
-        ev1 = torch.cuda.Event(enable_timing=True)
-        ev0.record()
-        res = OPT.solve_step(batch, conf, seed=cfg.lanczos_seed, energy=energy)
-        ev1.record()
-        torch.cuda.synchronize()
-        irl = {"wall_ms": (time.perf_counter() - i0) * 1e3, "device_ms": ev0.elapsed_time(ev1),
-               "n_matvec": res.n_matvec, "lambda_min": res.lambda_min, "converged": res.converged,
-               "m": cfg.m, "max_restarts": cfg.max_restarts}
+    irl = None if args.no_irl else irl_solve(torch, OPT, batch, cfg, energy)
 
-    # ---- on-the-fly mode (K6: O never stored) on the same workload, for reference;
-    # the headline above is the stored-O path BASELINE.json names
-    otf = None
-    if not cfg.complex_params and not args.no_otf:
-        ob = A.build_batch(params, inp.x, inp.e_loc, device=dev, mode="otf")
-        eo = E.estimate_energy(ob)
-        co_h, co_s = ob.coefficients(eo.mean), ob.weights
-        ob.obar()
-        vo = torch.randn((2, ld), dtype=torch.float64, device=dev, generator=gen)
-        vo[:, P:] = 0
-        oo = torch.empty((2, ld), dtype=torch.float64, device=dev)
-        for _ in range(3):
-            E._apply(ob, co_h, vo[0], oo[0])
-        # the activations (cfg2: T = 84 MB) would stay L2-resident between steps:
-        # write a 256 MB buffer before every step and time only the two products
-        l2buf = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
-        torch.cuda.synchronize()
-        oe = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-        for k in range(args.steps):
-            l2buf.fill_(float(k))
-            oe[k][0].record(stream)
-            E._apply(ob, co_h, vo[k % 2], oo[0])
-            E._apply(ob, co_s, vo[(k + 1) % 2], oo[1])
-            oe[k][1].record(stream)
-        torch.cuda.synchronize()
-        otf_s = sum(a.elapsed_time(b) for a, b in oe) / 1e3
-        del l2buf
-        conf = OPT.OptimizerConfig(m=cfg.m, max_restarts=cfg.max_restarts)
-        OPT.solve_step(ob, conf, seed=cfg.lanczos_seed, energy=eo)
-        torch.cuda.synchronize()
-        i0 = time.perf_counter()
-        ro = OPT.solve_step(ob, conf, seed=cfg.lanczos_seed, energy=eo)
-        torch.cuda.synchronize()
-        otf = {"value": 2 * args.steps / otf_s, "unit": UNIT, "irl_wall_ms": (time.perf_counter() - i0) * 1e3,
-               "n_matvec": ro.n_matvec, "lambda_min": ro.lambda_min,
-               "l2": "256 MB write before every step (the hidden activations fit in L2)",
-               "note": "O regenerated inside every product from packed inputs + hidden activations (DMMA GEMMs); "
-                       "not the headline: BASELINE cfg2 stores O in HBM"}
-        del ob
-
-    # ---- connected completion: heff_matvec + heff_offdiag_matvec in one
-    # product over a seeded synthetic partner cache (single excitations, per-row CSR)
-    conn = None
-    if not args.no_connected and args.partners > 0:
-        partners, elements, indptr, dist = S.connected_partners(inp.x, args.partners, seed=500 + cfg.index)
-        torch.cuda.synchronize()
-        c0 = time.perf_counter()
-        cache = A.build_connected_cache(params, batch, inp.x, partners, elements, indptr, dist_index=dist)
-        torch.cuda.synchronize()
-        build_s = time.perf_counter() - c0
-        m_part = cache.n_partner
-        def one_conn(i):
-            if herm:
-                E._apply(batch, coef_h, (vin[i, 0], vin[i, 1]), (vout[0, 0], vout[0, 1]), mode=args.mode,
-                         cache=cache)
-            else:
-                E._apply(batch, coef_h, vin[i], vout[0], mode=args.mode, cache=cache)
-
-        for k in range(3):
-            one_conn(k % nvec)
-        torch.cuda.synchronize()
-        c_steps = max(4, min(args.steps, 20))
-        ce = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(c_steps)]
-        for k in range(c_steps):
-            ce[k][0].record(stream)
-            one_conn(k % nvec)
-            ce[k][1].record(stream)
-        torch.cuda.synchronize()
-        c_ms = statistics.median([a.elapsed_time(b) for a, b in ce])
-        b_el_c = 16 if batch.is_complex else 8
-        c_bytes = (m_part + N) * P * b_el_c
-        # the same completion on an on-the-fly batch (O regenerated; partner rows stored)
-        otf_c_ms = None
-        if not cfg.complex_params and A.otf_supported(arch):
-            ob2 = A.build_batch(params, inp.x, inp.e_loc, device=dev, mode="otf")
-            cache2 = A.build_connected_cache(params, ob2, inp.x, partners, elements, indptr, dist_index=dist)
-            eo2 = E.estimate_energy(ob2)
-            c2 = ob2.coefficients(eo2.mean)
-            vo2 = torch.randn((2, ld), dtype=torch.float64, device=dev, generator=gen)
-            vo2[:, P:] = 0
-            oo2 = torch.empty(ld, dtype=torch.float64, device=dev)
-            for k in range(3):
-                E._apply(ob2, c2, vo2[k % 2], oo2, cache=cache2)
-            torch.cuda.synchronize()
-            ce2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(c_steps)]
-            for k in range(c_steps):
-                ce2[k][0].record(stream)
-                E._apply(ob2, c2, vo2[k % 2], oo2, cache=cache2)
-                ce2[k][1].record(stream)
-            torch.cuda.synchronize()
-            otf_c_ms = statistics.median([a.elapsed_time(b) for a, b in ce2])
-            del ob2, cache2
-        conn = {"value": 1e3 / c_ms, "unit": "MVP/s", "ms_per_product": c_ms, "partners_per_row": args.partners,
-                "otf_batch_ms_per_product": otf_c_ms,
-                "n_partner_rows": m_part, "nnz": int(indptr[-1]), "cache_build_ms": build_s * 1e3,
-                "alg_bytes": c_bytes, "achieved_gbs": c_bytes / (c_ms / 1e3) / 1e9,
-                "note": ("connected H_eff v (opt:144-147): partner dot pass over the partner O rows + per-row CSR "
-                         "kernel + the streaming product with an additive row term; alg bytes = (M + N) P b; "
-                         "seeded synthetic single-excitation partners, not a Hamiltonian")}
-        del cache
-
-    # ---- local energies (SURVEY 8(f) 2): cfg2-shaped RBM on a seeded synthetic molecule
-    eloc = None
-    if not args.no_eloc:
-        sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "tools"))
-        import eloc_bench
-
-        eloc = eloc_bench.run(n_samples=cfg.n_rows if cfg.model == "rbm" else 65536, cpu_samples=1,
-                              with_cpu=(rank == 0 and not args.no_cpu))
+    # ---- roofline of the dominant kernel (the streaming MVP launch)
+    passes = 2 if plan["path"] == "two_pass" else 1
+    alg_bytes = passes * N * P * b_el
+    mvp_avg_s = statistics.mean(mvp_ms) / 1e3
+    achieved = alg_bytes / mvp_avg_s / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": ncu_traffic(cfg.name), "peak_source": peak_src, "bytes_per_launch": alg_bytes,
+                "kernel": {"wide": "k_wide", "fused": "k_stream<FUSED>", "rows": "k_rows_mvp",
+                           "two_pass": "k_stream<DOT>+<ACC>"}[plan["path"]],
+                "accounting": (f"{passes} read(s) of O (N*P*b = {N * P * b_el} bytes) per MVP; SURVEY 8(d)'s "
+                               "two-pass figure is 2*N*P*b, i.e. frac_two_pass_accounting"),
+                "frac_two_pass_accounting": 2 * N * P * b_el / mvp_avg_s / 1e9 / peak,
+                "kernel_ms_mean": mvp_avg_s * 1e3, "kernel_ms_median": statistics.median(mvp_ms)}
+    del batch, apply, coef_h, coef_s
+    gc.collect()
+    torch.cuda.empty_cache()
 
     if rank != 0:
         reps.close()
         return 0
 
-    # ---- roofline of the dominant kernel (the streaming MVP launch)
-    b_el = 16 if batch.is_complex else 8
-    alg_bytes = (1 if plan["path"] == "fused" else 2) * N * P * b_el
-    mvp_avg_s = statistics.mean(mvp_ms) / 1e3
-    achieved = alg_bytes / mvp_avg_s / 1e9
-    peak, peak_src = measured_peak_gbs()
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": ncu_traffic(args.config), "peak_source": peak_src,
-                "bytes_per_launch": alg_bytes,
-                "accounting": ("one read of O (N*P*b) per MVP: the fused kernel streams O once; "
-                               "SURVEY 8(d)'s 2-pass figure would be 2*N*P*b"),
-                "kernel_ms_mean": mvp_avg_s * 1e3, "kernel_ms_median": statistics.median(mvp_ms)}
+    # ---- the headline workload on the fly (O never stored): FP64 tensor-core bound
+    l2buf = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    otf = None
+    if not args.no_otf and A.otf_supported(arch):
+        ob = A.build_batch(params, inp.x, inp.e_loc, device=dev, mode="otf")
+        eo = E.estimate_energy(ob)
+        co_h, co_s = ob.coefficients(eo.mean), ob.weights if not cfg.complex_params else ob.weights.to(torch.complex128)
+        ob.obar()
+        applo = _vectors(torch, ob, dev, 2, 4321)
+        for k in range(3):
+            applo(k % 2, co_h, 0)
+        torch.cuda.synchronize()
+        oe = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        for k in range(args.steps):
+            l2buf.fill_(float(k))  # the activations must come from HBM each step
+            oe[k][0].record(stream)
+            applo(k % 2, co_h, 0)
+            applo((k + 1) % 2, co_s, 1)
+            oe[k][1].record(stream)
+        torch.cuda.synchronize()
+        otf_s = sum(a.elapsed_time(b) for a, b in oe) / 1e3
+        cols = cfg.hidden * (2 if cfg.complex_params else 1)
+        flops = 2.0 * N * cols * (2 * cfg.n_inputs + 1)
+        tf = 2 * args.steps * flops / otf_s / 1e12
+        otf = {"value": 2 * args.steps / otf_s, "unit": UNIT,
+               "roofline": {"bound": "fp64_tensor", "achieved": tf, "peak": dmma_peak, "unit": "TFLOP/s",
+                            "frac": tf / dmma_peak, "peak_source": dmma_src, "flops_per_product": flops},
+               "irl_solve": None if args.no_irl else irl_solve(torch, OPT, ob, cfg, eo),
+               "l2": "256 MB write before every step",
+               "note": "O regenerated inside every product from packed inputs + hidden activations (DMMA GEMMs)"}
+        del ob, applo, co_h, co_s
+        gc.collect()
+        torch.cuda.empty_cache()
 
+    # ---- every BASELINE config: stored and on-the-fly products, IRL solves
+    configs = {}
+    want = [int(c) for c in args.configs.split(",") if c.strip()] if args.configs else []
+    for idx in want:
+        c = S.CONFIGS[idx]
+        extra = None
+        if idx == 2 and not args.no_connected and args.partners > 0:
+            def extra(b_, p_, i_, ap_, co_, rec_):
+                connected_leg(torch, args, dev, c, b_, p_, i_, ap_, co_, rec_)
+        configs[f"cfg{idx}"] = config_record(torch, c, dev, peak, dmma_peak, l2buf, with_irl=not args.no_irl,
+                                             extra=extra)
+    del l2buf
+    torch.cuda.empty_cache()
+
+    # ---- local energies (SURVEY 8(f) 2): cfg2-shaped RBM on a seeded synthetic molecule
+    eloc = None
+    if not args.no_eloc:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import eloc_bench
+
+        eloc = eloc_bench.run(n_samples=65536, cpu_samples=64, with_cpu=not args.no_cpu)
+
+    # ---- the CPU reference path, timed on this box's host cores (rank 0, N = 1 only)
     cpu = None
     if not args.no_cpu and world == 1:
-        n_sub = min(cfg.n_rows, 8192)
-        sec = cpu_reference_sample(cfg, n_sub)
-        full = sec * cfg.n_rows / n_sub
-        cpu = {"value": 1.0 / full, "unit": UNIT, "cores": cpu_cores(), "kind": "port",
-               "sample": (f"oracle port of est.heff_matvec / S-trick, median of 3 on the first {n_sub} of "
-                          f"{cfg.n_rows} rows (full P), x{cfg.n_rows / n_sub:g} to full N_s")}
+        cpu = cpu_leg(cfg)
+        for idx in want:
+            rec = configs[f"cfg{idx}"]
+            c = S.CONFIGS[idx]
+            cl = cpu if idx == cfg.index else cpu_leg(c, reps=3 if c.n_rows * c.param_count < 1e8 else 1)
+            rec["cpu_baseline"] = cl
+            rec["speedup_stored_vs_cpu"] = rec["stored"]["mvp_s"] / cl["value"]
+            if "otf" in rec:
+                rec["speedup_otf_vs_cpu"] = rec["otf"]["mvp_s"] / cl["value"]
 
     line = {
         "metric": BASELINE_METRIC,
@@ -545,20 +701,20 @@ def run_ours(args):
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "c128" if batch.is_complex else "f64",
+        "dtype": "c128" if cfg.complex_params else "f64",
         "data": "synthetic (seeded, BASELINE.json shapes)",
-        "config": {"workload": cfg.name, "n_rows": N, "param_count": P, "ld": ld,
+        "config": {"workload": cfg.name, "n_rows": N, "param_count": P, "ld": ld, "mode": "stored O",
                    "o_bytes": N * ld * b_el, "step": "1 H_eff*v + 1 S*v (2 MVPs)",
                    "l2": "O (%.2f GB) > 126 MB L2: no flush needed" % (N * ld * b_el / 1e9),
                    "parallelism": f"replicas x{world}", "mvp_path": plan["path"], "plan": plan},
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": mvps * launches_per_mvp,
+        "gpu_launches": mvps * LAUNCHES_PER_MVP[plan["path"]],
         "clocks": clocks.summary(),
         "irl_solve": irl,
         "otf_mode": otf,
-        "connected_mode": conn,
+        "configs": configs,
         "local_energy_mode": eloc,
         "obuild_ms": obuild_ms,
         "obuild_write_gbs": N * P * b_el / (obuild_ms / 1e3) / 1e9,

@@ -42,6 +42,7 @@ from .estimators import (
     EnergyEstimate,
     SampleBatch,
     _apply,
+    _qgt_coeff,
     energy_gradient,
     estimate_energy,
 )
@@ -54,7 +55,7 @@ DEFAULT_LINE_SEARCH_GRID = tuple(2.0**k for k in range(-6, 2))  # opt:29
 class OptimizerConfig:
     """``opt:41-57`` minus Adam (defaults identical)."""
 
-    method: str = "irl"  # irl | sl
+    method: str = "irl"  # irl | sl | gevp
     m: int = 20
     tol: float = 1e-12
     max_restarts: int = 300
@@ -64,9 +65,11 @@ class OptimizerConfig:
     convergence_eps: float = 1e-10
     line_search: tuple = DEFAULT_LINE_SEARCH_GRID
     n_samples: int = 0  # 0 = exact enumeration
+    gevp_tol: float = 1e-12  # method "gevp": relative residual of A c = lambda B c
+    gevp_max_iter: int = 2000
 
     def __post_init__(self):
-        if self.method not in ("irl", "sl"):
+        if self.method not in ("irl", "sl", "gevp"):
             raise ValueError(f"unknown method {self.method!r}")
 
 
@@ -152,6 +155,18 @@ class BorderedOperator:
             self._sweepers[key] = sw
         return sw
 
+    def metric(self, u: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """The bordered metric S~ [u0; u] = [u0; S u] of the GEVP form:
+        the normalised state is orthogonal to the centred derivatives, so S~ = diag(1, S)."""
+        if out is None:
+            out = torch.zeros(self.layout.length, dtype=torch.float64, device=u.device)
+        u0, uin = self.layout.parts(u)
+        out0, uout = self.layout.parts(out)
+        _apply(self.batch, _qgt_coeff(self.batch), uin, uout, mode=self.mode)
+        out0.copy_(u0)
+        self.count += 1
+        return out
+
     def __call__(self, u: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         if out is None:
             out = torch.zeros(self.layout.length, dtype=torch.float64, device=u.device)
@@ -212,6 +227,11 @@ def solve_step(batch: SampleBatch, config: OptimizerConfig = OptimizerConfig(), 
     if config.method == "irl":
         pair = krylov.irl_smallest(op, lay.dim, m=config.m, tol=config.tol, max_restarts=config.max_restarts,
                                    seed=s, device=batch.device, layout=lay)
+    elif config.method == "gevp":
+        if connected is not None:
+            raise ValueError("the GEVP form takes the batch operator without the connected completion")
+        pair = krylov.lobpcg_smallest(op, op.metric, lay.dim, tol=config.gevp_tol, max_iter=config.gevp_max_iter,
+                                      seed=s, device=batch.device, layout=lay)
     else:
         pair = krylov.sl_smallest(op, lay.dim, budget=config.sl_budget, seed=s, device=batch.device, layout=lay)
     d = direction_from_vector(pair.vector, gradient, batch.param_count, lay.hermitian)

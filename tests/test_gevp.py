@@ -1,0 +1,87 @@
+"""GEVP form of the update, H~ c = lambda S~ c (Eq. 11; the
+reference validates it only through its dense oracles at small p, SPEC.md:408,
+est:319-344): the device LOBPCG solver (krylov.lobpcg_smallest) on the
+bordered pencil against scipy.linalg.eigh of the dense oracle matrices."""
+
+import numpy as np
+import pytest
+import scipy.linalg
+
+from oracle import estimators as oest
+
+
+def _pencil(rng, p, cond=1e3):
+    a = rng.standard_normal((p, p))
+    a = (a + a.T) / 2
+    q, _ = np.linalg.qr(rng.standard_normal((p, p)))
+    b = (q * np.geomspace(1.0, 1.0 / cond, p)) @ q.T
+    return a, (b + b.T) / 2
+
+
+@pytest.mark.parametrize("p,cond", [(1, 1.0), (7, 10.0), (60, 1e3), (200, 1e4)])
+def test_lobpcg_matches_dense_eigh(p, cond):
+    import torch
+    from paper_2601_01437_b200 import krylov
+
+    rng = np.random.default_rng(p)
+    a, b = _pencil(rng, p, cond)
+    ta, tb = torch.as_tensor(a), torch.as_tensor(b)
+    pair = krylov.lobpcg_smallest(lambda v: ta @ v, lambda v: tb @ v, p, tol=1e-11, max_iter=20000, seed=3)
+    lam, vec = scipy.linalg.eigh(a, b)
+    assert pair.converged
+    assert abs(pair.value - lam[0]) <= 1e-10 * max(1.0, abs(lam[0]))
+    x = pair.vector.numpy()
+    x = x * np.sign(x @ b @ vec[:, 0])
+    assert np.linalg.norm(x - vec[:, 0]) <= 1e-6 * np.linalg.norm(vec[:, 0])
+
+
+def test_lobpcg_rejects_bad_input():
+    import torch
+    from paper_2601_01437_b200 import krylov
+
+    with pytest.raises(ValueError):
+        krylov.lobpcg_smallest(lambda v: v, lambda v: v, 0)
+    with pytest.raises(ValueError):
+        krylov.lobpcg_smallest(lambda v: v * float("nan"), lambda v: v, 3)
+    with pytest.raises(ValueError):  # indefinite metric
+        krylov.lobpcg_smallest(lambda v: v, lambda v: -v, 3)
+
+
+def _bordered_dense(w, e, o, mean):
+    """[[0, (F/2)^T], [F/2, H_eff]] and diag(1, S) from the dense oracles."""
+    h = oest.dense_heff(w, e, o, mean)
+    s = oest.dense_qgt(w, o)
+    g = 0.5 * oest.gradient(w, e, o, mean)
+    p = len(g)
+    a = np.zeros((p + 1, p + 1))
+    a[0, 1:] = g
+    a[1:, 0] = g
+    a[1:, 1:] = h
+    b = np.zeros((p + 1, p + 1))
+    b[0, 0] = 1.0
+    b[1:, 1:] = s
+    return a, b
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,p", [(400, 17), (3000, 150), (2311, 200)])
+def test_gevp_solve_step_vs_dense_oracle(cuda, n, p):
+    """optimizer.solve_step(method="gevp") on a device batch: lambda within
+    1e-10 and the direction c[1:]/c0 within 1e-8 of scipy's dense eigh."""
+    from paper_2601_01437_b200 import estimators as E, optimizer as OPT
+
+    rng = np.random.default_rng(n + p)
+    o = rng.standard_normal((n, p)) * 0.1
+    e = -1.0 + 0.05 * rng.standard_normal(n) + 0.02 * (o @ rng.standard_normal(p))
+    w = np.full(n, 1.0 / n)
+    batch = E.SampleBatch([None] * n, w, e, o, n)
+    res = OPT.solve_step(batch, OPT.OptimizerConfig(method="gevp"), seed=5)
+    mean, _, _ = oest.energy(w, e, n)
+    a, b = _bordered_dense(w, e, o, mean)
+    lam, vec = scipy.linalg.eigh(a, b)
+    c = vec[:, 0]
+    d_ref = c[1:] / c[0]
+    assert res.converged
+    assert abs(res.lambda_min - lam[0]) <= 1e-10 * abs(lam[0])
+    d = res.direction.cpu().numpy()
+    assert np.linalg.norm(d - d_ref) <= 1e-8 * np.linalg.norm(d_ref)
