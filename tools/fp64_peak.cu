@@ -1,6 +1,7 @@
 // FP64 throughput microbenchmark on the GPU box: DFMA (CUDA cores) vs DMMA
 // (mma.sync m8n8k4 f64 tensor path).  Development tool.
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 __global__ void k_dfma(double* out, int iters) {
@@ -28,7 +29,8 @@ __global__ void k_dmma(double* out, int iters) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
-int main() {
+int main(int argc, char** argv) {
+  const int mult = argc > 1 ? atoi(argv[1]) : 1;  // x iterations: long enough to sample clocks under load
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   double* out;
@@ -37,7 +39,7 @@ int main() {
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   for (int threads : {256, 512, 1024}) {
-    const int iters = 20000;
+    const int iters = 20000 * mult;
     k_dfma<<<sms * 2, threads>>>(out, 100);
     cudaEventRecord(e0);
     k_dfma<<<sms * 2, threads>>>(out, iters);
