@@ -478,10 +478,11 @@ int make_wide_plan(int64_t n, int64_t ld_u, bool cplx, WidePlan& p) {
   p.WM = (int)cdiv(ld_u, p.G);
   // fewest parts per row slice (most rows per block, the biggest TMA stages)
   // whose per-lane share fits a kernel instance
+  // (at most 6 units per lane: the 8-unit instances spill with two rows per step)
   p.Q = 0;
   for (int q = 1; q <= WIDE_CW; q *= 2) {
     const int upl = wide_upl((int)cdiv(cdiv(p.WM, q), 32));
-    if (upl) {
+    if (upl && upl <= 6) {
       p.Q = q;
       p.upl = upl;
       break;
