@@ -6,6 +6,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <vector>
 #include <set>
 #include <string>
 #include <unordered_map>
@@ -1312,6 +1313,78 @@ int pack_bits(const uint8_t* x, int64_t n, int n_vis, uint64_t* xbits, cudaStrea
   return cuda_check(cudaGetLastError(), "pack bits launch");
 }
 
+// A second stream per device for work that overlaps the caller's stream (the
+// O-build's hidden layer and FP64-tensor statistics beside its HBM-write-bound
+// row writer).  Fork / join by events recorded per call, so the caller's
+// stream order (and graph capture of it) is kept.
+int side_stream(cudaStream_t& out) {
+  static std::mutex mu;
+  static cudaStream_t streams[64] = {};
+  int dev = 0;
+  IRL_TRY(cuda_check(cudaGetDevice(&dev), "cudaGetDevice"));
+  if (dev < 0 || dev >= 64) return fail(IRL_ERR_DEVICE, "device index %d", dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (!streams[dev]) IRL_TRY(cuda_check(cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking), "side stream"));
+  out = streams[dev];
+  return IRL_OK;
+}
+
+struct Fork {
+  cudaStream_t main = nullptr, side = nullptr;
+  cudaEvent_t ev = nullptr;
+  int begin(cudaStream_t st) {  // side waits for everything issued on st so far
+    main = st;
+    IRL_TRY(side_stream(side));
+    IRL_TRY(cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "fork event"));
+    IRL_TRY(cuda_check(cudaEventRecord(ev, st), "fork record"));
+    return cuda_check(cudaStreamWaitEvent(side, ev, 0), "fork wait");
+  }
+  int join() {  // st waits for everything issued on side since begin()
+    IRL_TRY(cuda_check(cudaEventRecord(ev, side), "join record"));
+    IRL_TRY(cuda_check(cudaStreamWaitEvent(main, ev, 0), "join wait"));
+    return cuda_check(cudaEventDestroy(ev), "join event");
+  }
+};
+
+// column statistics Obar = sum w conj(O), F/2 = sum c conj(O) from the hidden
+// activations and the packed inputs (no O read): the DMMA GEMMs of the
+// on-the-fly product with y = w and y = c
+int obuild_stats(bool cplx, int model, const uint64_t* xbits, const void* T, const double* G, int64_t n, int n_vis,
+                 int hidden, int64_t ld, const double* w, const double* coeff, double* obar, double* g, char* scratch,
+                 cudaStream_t st) {
+  if (cplx) {
+    // complex theta: obar = conj(sum w conj(O)), grad = sum c conj(O) from the
+    // real N x 2h view of T (as irl_otf_colstats_rbm_c128)
+    OtfCPlan op;
+    IRL_TRY(make_otfc_plan(n, n_vis, hidden, op));
+    OtfCWs wl = otfc_ws_layout(op, n, n_vis, hidden, scratch);
+    OtfCArgs oa{};
+    oa.xbits = xbits;
+    oa.T = reinterpret_cast<const double*>(T);
+    oa.n_rows = n;
+    oa.n_in = n_vis;
+    oa.hidden = hidden;
+    IRL_TRY(otfc_colsum(op, oa, wl, ld, nullptr, w, reinterpret_cast<double2*>(obar), 1, st));
+    return otfc_colsum(op, oa, wl, ld, reinterpret_cast<const double2*>(coeff), nullptr,
+                       reinterpret_cast<double2*>(g), 0, st);
+  }
+  OtfPlan op;
+  IRL_TRY(make_otf_plan(n, n_vis, hidden, op));
+  OtfWs wl = otf_ws_layout(op, n, hidden, scratch);
+  double* xpart = reinterpret_cast<double*>(scratch + align256(wl.bytes));
+  OtfArgs oa{};
+  oa.xbits = xbits;
+  oa.T = reinterpret_cast<const double*>(T);
+  oa.G = model == MODEL_MLP ? G : reinterpret_cast<const double*>(T);
+  oa.n_rows = n;
+  oa.n_in = n_vis;
+  oa.hidden = hidden;
+  DevInfo d;
+  IRL_TRY(dev_info(d));
+  const int nbx = std::min<int>(4 * d.sms, (int)std::max<int64_t>(1, n / 64));
+  return otf_stats(op, oa, wl, model, n, n_vis, hidden, ld, w, coeff, obar, g, xpart, nbx, st);
+}
+
 int obuild_impl(bool cplx, int model, const uint8_t* x, int64_t n, int n_vis, int hidden, const double* theta,
                 double* O, int64_t ld, const double* w, const double* coeff, double* obar, double* g, void* ws,
                 size_t ws_bytes, cudaStream_t st) {
@@ -1349,7 +1422,8 @@ int obuild_impl(bool cplx, int model, const uint8_t* x, int64_t n, int n_vis, in
   const int xrow = cplx ? n_vis : (n_vis + 1) & ~1;
   void* xd = base + off;
   off += align256((size_t)n * xrow * sS);
-  {
+  const bool sweep = gstats && sweep_ok(cplx, model, n_vis, hidden);
+  if (!sweep) {  // table entries of the inputs: the column-tile writer only
     const int64_t total = n * xrow;
     const unsigned grid = (unsigned)std::min<int64_t>(cdiv(total, 256), 4 * 148 * 8);
     if (cplx)
@@ -1358,19 +1432,60 @@ int obuild_impl(bool cplx, int model, const uint8_t* x, int64_t n, int n_vis, in
       k_x_expand<false><<<grid, 256, 0, st>>>(x, n, n_vis, xrow, reinterpret_cast<double*>(xd));
     IRL_TRY(cuda_check(cudaGetLastError(), "x expand launch"));
   }
-  if (model == MODEL_RBM) {
-    const double* bvec = theta + (size_t)n_vis * (cplx ? 2 : 1);
-    const double* Wm = theta + (size_t)(n_vis + hidden) * (cplx ? 2 : 1);
-    if (cplx)
-      IRL_TRY((launch_hidden<true, MODEL_RBM>(x, xbits, n, n_vis, hidden, Wm, bvec, nullptr, T, nullptr, st)));
-    else
-      IRL_TRY((launch_hidden<false, MODEL_RBM>(x, xbits, n, n_vis, hidden, Wm, bvec, nullptr, T, nullptr, st)));
-  } else {
+  // hidden layer of rows [r0, r0 + rows) (row offsets into x, xbits, T, G)
+  auto hidden_rows = [&](int64_t r0, int64_t rows, cudaStream_t hs) -> int {
+    const uint8_t* xr = x + r0 * n_vis;
+    const uint64_t* xb = xbits ? xbits + r0 * OTF_XW : nullptr;
+    if (model == MODEL_RBM) {
+      const double* bvec = theta + (size_t)n_vis * (cplx ? 2 : 1);
+      const double* Wm = theta + (size_t)(n_vis + hidden) * (cplx ? 2 : 1);
+      void* Tr = static_cast<char*>(T) + (size_t)r0 * hidden * sS;
+      if (cplx) return launch_hidden<true, MODEL_RBM>(xr, xb, rows, n_vis, hidden, Wm, bvec, nullptr, Tr, nullptr, hs);
+      return launch_hidden<false, MODEL_RBM>(xr, xb, rows, n_vis, hidden, Wm, bvec, nullptr, Tr, nullptr, hs);
+    }
     const double* Wm = theta;
     const double* bvec = theta + (size_t)hidden * n_vis;
     const double* uvec = bvec + hidden;
-    IRL_TRY((launch_hidden<false, MODEL_MLP>(x, xbits, n, n_vis, hidden, Wm, bvec, uvec, T, G, st)));
+    return launch_hidden<false, MODEL_MLP>(xr, xb, rows, n_vis, hidden, Wm, bvec, uvec,
+                                           static_cast<char*>(T) + (size_t)r0 * hidden * sS, G + (size_t)r0 * hidden, hs);
+  };
+  if (sweep) {
+    // row-chunk pipeline: the side stream computes the hidden layer chunk by
+    // chunk (FP64 tensor cores) and then the column statistics, while the
+    // caller's stream writes O (HBM-write bound) for each chunk once its
+    // activations exist; only the first chunk's hidden layer is exposed
+    DevInfo d;
+    IRL_TRY(dev_info(d));
+    auto fn = cplx ? k_orows_sweep<true, MODEL_RBM>
+                   : (model == MODEL_MLP ? k_orows_sweep<false, MODEL_MLP> : k_orows_sweep<false, MODEL_RBM>);
+    const size_t sm = (size_t)hidden * (cplx ? 16 : 8);
+    IRL_TRY(ensure_fn_attrs((const void*)fn, d.smem_optin));
+    const int64_t want = getenv("IRL_OBUILD_CHUNKS") ? atoi(getenv("IRL_OBUILD_CHUNKS")) : 4;
+    const int nc = (int)std::max<int64_t>(1, std::min<int64_t>(want, n / 4096));
+    Fork fork;
+    IRL_TRY(fork.begin(st));
+    std::vector<cudaEvent_t> evs((size_t)nc, nullptr);
+    for (int c = 0; c < nc; ++c) {
+      const int64_t r0 = n * c / nc, r1 = n * (c + 1) / nc;
+      IRL_TRY(hidden_rows(r0, r1 - r0, fork.side));
+      IRL_TRY(cuda_check(cudaEventCreateWithFlags(&evs[c], cudaEventDisableTiming), "chunk event"));
+      IRL_TRY(cuda_check(cudaEventRecord(evs[c], fork.side), "chunk record"));
+    }
+    for (int c = 0; c < nc; ++c) {
+      const int64_t r0 = n * c / nc, r1 = n * (c + 1) / nc;
+      IRL_TRY(cuda_check(cudaStreamWaitEvent(st, evs[c], 0), "chunk wait"));
+      IRL_TRY(cuda_check(cudaEventDestroy(evs[c]), "chunk event"));
+      const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(r1 - r0, 2 * (int64_t)d.sms));
+      fn<<<grid, SWEEP_NT, sm, st>>>(x + r0 * n_vis, r1 - r0, n_vis, hidden,
+                                     static_cast<char*>(T) + (size_t)r0 * hidden * sS,
+                                     G ? G + (size_t)r0 * hidden : nullptr, reinterpret_cast<double2*>(O) + r0 * ld_u,
+                                     ld_u);
+      IRL_TRY(cuda_check(cudaGetLastError(), "orows sweep launch"));
+    }
+    IRL_TRY(obuild_stats(cplx, model, xbits, T, G, n, n_vis, hidden, ld, w, coeff, obar, g, base + off, fork.side));
+    return fork.join();
   }
+  IRL_TRY(hidden_rows(0, n, st));
   ORowArgs a{};
   a.x = x;
   a.xd = xd;
@@ -1402,54 +1517,13 @@ int obuild_impl(bool cplx, int model, const uint8_t* x, int64_t n, int n_vis, in
     if (smem > (size_t)d.smem_optin) return fail(IRL_ERR_ARG, "hidden layer too wide for the row table");
     IRL_TRY(ensure_fn_attrs((const void*)p.fn, d.smem_optin));
   }
-  if (gstats && sweep_ok(cplx, model, n_vis, hidden)) {
-    DevInfo d;
-    IRL_TRY(dev_info(d));
-    auto fn = cplx ? k_orows_sweep<true, MODEL_RBM>
-                   : (model == MODEL_MLP ? k_orows_sweep<false, MODEL_MLP> : k_orows_sweep<false, MODEL_RBM>);
-    const size_t sm = (size_t)hidden * (cplx ? 16 : 8);
-    IRL_TRY(ensure_fn_attrs((const void*)fn, d.smem_optin));
-    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(n, 2 * (int64_t)d.sms));
-    fn<<<grid, SWEEP_NT, sm, st>>>(x, n, n_vis, hidden, T, G, reinterpret_cast<double2*>(O), ld_u);
-  } else {
-    p.fn<<<(unsigned)(p.nb * p.C), p.NT, smem, st>>>(a, (int)buf_bytes);
-  }
+  p.fn<<<(unsigned)(p.nb * p.C), p.NT, smem, st>>>(a, (int)buf_bytes);
   IRL_TRY(cuda_check(cudaGetLastError(), "orows launch"));
-  if (gstats && cplx) {
-    // complex theta: obar = conj(sum w conj(O)), grad = sum c conj(O) from the
-    // real N x 2h view of T (as irl_otf_colstats_rbm_c128)
-    OtfCPlan op;
-    IRL_TRY(make_otfc_plan(n, n_vis, hidden, op));
-    OtfCWs wl = otfc_ws_layout(op, n, n_vis, hidden, base + off);
-    OtfCArgs oa{};
-    oa.xbits = xbits;
-    oa.T = reinterpret_cast<const double*>(T);
-    oa.n_rows = n;
-    oa.n_in = n_vis;
-    oa.hidden = hidden;
-    IRL_TRY(otfc_colsum(op, oa, wl, ld, nullptr, w, reinterpret_cast<double2*>(obar), 1, st));
-    return otfc_colsum(op, oa, wl, ld, reinterpret_cast<const double2*>(coeff), nullptr,
-                       reinterpret_cast<double2*>(g), 0, st);
-  }
-  if (gstats) {
-    // column statistics from the hidden activations and the packed inputs
-    OtfPlan op;
-    IRL_TRY(make_otf_plan(n, n_vis, hidden, op));
-    OtfWs wl = otf_ws_layout(op, n, hidden, base + off);
-    off += align256(wl.bytes);
-    double* xpart = reinterpret_cast<double*>(base + off);
-    OtfArgs oa{};
-    oa.xbits = xbits;
-    oa.T = reinterpret_cast<const double*>(T);
-    oa.G = model == MODEL_MLP ? G : reinterpret_cast<const double*>(T);
-    oa.n_rows = n;
-    oa.n_in = n_vis;
-    oa.hidden = hidden;
-    DevInfo d;
-    IRL_TRY(dev_info(d));
-    const int nbx = std::min<int>(4 * d.sms, (int)std::max<int64_t>(1, n / 64));
-    IRL_TRY(otf_stats(op, oa, wl, model, n, n_vis, hidden, ld, w, coeff, obar, g, xpart, nbx, st));
-    return IRL_OK;
+  if (gstats) {  // statistics on FP64 tensor cores beside the writer (they read T, G, not O)
+    Fork fork;
+    IRL_TRY(fork.begin(st));
+    IRL_TRY(obuild_stats(cplx, model, xbits, T, G, n, n_vis, hidden, ld, w, coeff, obar, g, base + off, fork.side));
+    return fork.join();
   }
   const unsigned blocks = (unsigned)cdiv(ld_u, 32);
   if (cplx)

@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_gpu_edge.py tests/test_gpu_estimators.py -x -q -k "wide or canaries or matvec or Heff or heff" > gpurun_out/wide_tests.log 2>&1; echo "rc $?" >> gpurun_out/wide_tests.log
-timeout 900 python tools/wide_time.py 4,5 - IRL_WIDE_RPW=4 IRL_WIDE_NS=3 > gpurun_out/wide_time.txt 2>&1
+timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_edge.py -x -q -k "orows or obuild or rows_vs or golden or canar or config_products" > gpurun_out/ob_tests.log 2>&1; echo "rc $?" >> gpurun_out/ob_tests.log
+for c in 1 2 4 8; do echo "chunks $c" >> gpurun_out/obuild_time.txt; IRL_OBUILD_CHUNKS=$c timeout 600 python tools/obuild_time.py 3,4,5 >> gpurun_out/obuild_time.txt 2>&1; done
