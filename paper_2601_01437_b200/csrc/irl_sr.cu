@@ -225,6 +225,8 @@ struct PlanKeyHash {
   }
 };
 
+constexpr int kMaxFusedCluster = 2;
+
 int make_plan_uncached(int64_t n, int64_t ld_u, bool cplx, int mode, Plan& out) {
   DevInfo d;
   IRL_TRY(dev_info(d));
@@ -236,7 +238,11 @@ int make_plan_uncached(int64_t n, int64_t ld_u, bool cplx, int mode, Plan& out) 
     int best_active = 0;
     const char* force = getenv("IRL_FUSED_CLUSTER");  // tuning override
     const int c_force = force ? atoi(force) : 0;
-    for (int C = 1; C <= 16; ++C) {
+    // clusters of at most kMaxFusedCluster CTAs: beyond two, the per-row DSMEM
+    // exchange and GPC packing cost more than a second HBM pass (cfg4 C = 6:
+    // 26.6 ms against 17.4 two-pass), and rows that wide take the single-read
+    // wide product instead
+    for (int C = 1; C <= kMaxFusedCluster; ++C) {
       if (c_force > 0 && C != c_force) continue;
       Plan p;
       if (!choose_geom(ld_u, C, cplx, mode, budget, p)) continue;
@@ -373,7 +379,6 @@ int launch_finish_mvp(const double2* part, int nb, int64_t ld_u, const void* ysu
                     "finish kernel launch");
 }
 
-constexpr int kAutoMaxCluster = 2;
 
 // MVP workspace layout for one plan
 struct MvpWs {
@@ -634,9 +639,7 @@ int mvp_impl(bool cplx, const double* O, int64_t n, int64_t p, int64_t ld, const
     return launch_wide(wp, cplx, wa, ws, st);
   } else if (mode == IRL_MVP_AUTO || mode == IRL_MVP_FUSED) {
     int rc = make_plan(n, ld_u, cplx, MODE_FUSED, pl);
-    // AUTO: the per-row DSMEM exchange of wide clusters costs more than the
-    // second HBM pass (measured: C <= 2 wins, C >= 6 loses; tools/tune_cluster.py)
-    if (rc == IRL_OK && (mode == IRL_MVP_FUSED || pl.C <= kAutoMaxCluster)) {
+    if (rc == IRL_OK) {
       path = IRL_MVP_FUSED;
     } else if (mode == IRL_MVP_FUSED) {
       return rc;
@@ -2116,8 +2119,7 @@ int irl_mvp_plan(int64_t n, int64_t ld, int is_complex, int mode, int* out_path,
     memcpy(out_geom7, g, sizeof(g));
     return IRL_OK;
   } else if (mode == IRL_MVP_AUTO || mode == IRL_MVP_FUSED) {
-    if (make_plan(n, ld_u, is_complex != 0, MODE_FUSED, p) == IRL_OK &&
-        (mode == IRL_MVP_FUSED || p.C <= kAutoMaxCluster)) {
+    if (make_plan(n, ld_u, is_complex != 0, MODE_FUSED, p) == IRL_OK) {
       path = IRL_MVP_FUSED;
     } else if (mode == IRL_MVP_FUSED) {
       return IRL_ERR_DEVICE;
