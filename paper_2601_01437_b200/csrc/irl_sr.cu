@@ -849,7 +849,9 @@ int make_otf_plan_uncached(int64_t n, int n_in, int hidden, OtfPlan& p) {
   p.kc = 8 * p.nkt;
   p.nb = 1;
   IRL_TRY(ensure_fn_attrs((const void*)k_otf_dot<true>, d.smem_optin));
+  IRL_TRY(ensure_fn_attrs((const void*)k_otf_dot<true, true>, d.smem_optin));
   IRL_TRY(ensure_fn_attrs((const void*)k_otf_dot<false>, d.smem_optin));
+  IRL_TRY(ensure_fn_attrs((const void*)k_otf_dot<false, true>, d.smem_optin));
   for (int nyv = 1; nyv <= 2; ++nyv)
     for (int ht = 0; ht < 3; ++ht) {
       p.nb_v[nyv - 1][ht] = 0;
@@ -986,19 +988,25 @@ int launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStre
   return cuda_check(cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...), what);
 }
 
+constexpr int kOtfLowRegMaxNin = 40;
+
 int otf_dot_launch(OtfArgs& a, bool has_t, cudaStream_t st) {
-  const void* fn = has_t ? (const void*)k_otf_dot<true> : (const void*)k_otf_dot<false>;
+  const bool low = a.n_in <= kOtfLowRegMaxNin && !getenv("IRL_OTF_NO_LOWREG");
+  const void* fn = has_t ? (low ? (const void*)k_otf_dot<true, true> : (const void*)k_otf_dot<true>)
+                         : (low ? (const void*)k_otf_dot<false, true> : (const void*)k_otf_dot<false>);
   const bool gu = has_t && a.u != nullptr;
   const size_t smem = otf_dot_smem(a.n_in, has_t, false, gu);
   int grid = 0;
-  IRL_TRY(otf_dot_grid(fn, smem, (a.n_in << 3) | (gu ? 4 : 0) | (has_t ? 1 : 0), grid));
+  IRL_TRY(otf_dot_grid(fn, smem, (a.n_in << 4) | (low ? 8 : 0) | (gu ? 4 : 0) | (has_t ? 1 : 0), grid));
   CUtensorMap mg, mt;
   IRL_TRY(tile_map(mg, a.G, a.hidden, a.n_rows));
   if (has_t)
     IRL_TRY(tile_map(mt, a.T, a.hidden, a.n_rows));
   else
     mt = mg;
+  if (has_t && low) return launch_pdl(k_otf_dot<true, true>, dim3(grid), dim3(288), smem, st, "otf dot launch", a, mg, mt);
   if (has_t) return launch_pdl(k_otf_dot<true>, dim3(grid), dim3(288), smem, st, "otf dot launch", a, mg, mt);
+  if (low) return launch_pdl(k_otf_dot<false, true>, dim3(grid), dim3(288), smem, st, "otf dot launch", a, mg, mt);
   return launch_pdl(k_otf_dot<false>, dim3(grid), dim3(288), smem, st, "otf dot launch", a, mg, mt);
 }
 

@@ -180,8 +180,11 @@ __device__ __forceinline__ void otf_cta_range(int64_t total, int64_t& t0, int64_
 // The producer streams the G/T tiles (2-D swizzled TMA boxes) and the packed
 // bits through a 2-stage mbarrier ring; the per-row cross-warp sums use a
 // double-buffered exchange and one named barrier of the consumers per tile.
-template <bool HAS_T>
-__global__ void __maxnreg__(HAS_T ? 168 : 96)
+// LOWREG (short input rows, n_in <= 40): 80 registers, so two 288-thread CTAs
+// share an SM (a short K loop leaves the tile epilogue latency-bound; twice
+// the warps hide it); long rows keep the register budget for the K loop.
+template <bool HAS_T, bool LOWREG = false>
+__global__ void __maxnreg__(LOWREG ? 80 : (HAS_T ? 168 : 96))
     k_otf_dot(const OtfArgs a, const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmT) {
   extern __shared__ __align__(16) unsigned char smem_o[];
   constexpr int ST = OTF_DOT_STAGES;
@@ -505,7 +508,6 @@ __global__ void __maxnreg__((NKT <= 8 && NY == 1 && !HAS_T) ? 96 : 168)
     }
   } else {  // ---------------------------------------------------- consumers
     const int sh_base = lane >> 2;  // B column offset within an n-tile
-    const double one_b = (lane >> 2) == 0 ? 1.0 : 0.0;
     // the ones column (k = n_in) is bit n_in of every packed row
     const uint64_t one0 = nin < 64 ? (1ull << nin) : 0ull, one1 = nin >= 64 ? (1ull << (nin - 64)) : 0ull;
     for (int it = 0; it < ntiles; ++it) {
@@ -546,16 +548,27 @@ __global__ void __maxnreg__((NKT <= 8 && NY == 1 && !HAS_T) ? 96 : 168)
             dmma(c[q][0][nt][0], c[q][0][nt][1], g0, bv);
             dmma(c[q][1][nt][0], c[q][1][nt][1], g1, bv);
           }
-          if (HAS_T) {
-            const double yb = one_b != 0.0 ? yq : 0.0;
-            dmma(cu[q][0][0], cu[q][0][1], t0, yb);
-            dmma(cu[q][1][0], cu[q][1][1], t1, yb);
+          if (HAS_T) {  // u block sum_n T_nj y_n: two FMAs per lane (a DMMA here would be 7/8 zeros)
+            cu[q][0][0] = fma(t0, yq, cu[q][0][0]);
+            cu[q][1][0] = fma(t1, yq, cu[q][1][0]);
           }
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
     }
+  }
+  if (HAS_T) {  // the u-block partials: lanes of a quad hold rows kk*4 + (lane & 3): sum the quad
+#pragma unroll
+    for (int q = 0; q < NY; ++q)
+#pragma unroll
+      for (int f = 0; f < 2; ++f) {
+        double v = cu[q][f][0];
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        v += __shfl_xor_sync(0xffffffffu, v, 2);
+        cu[q][f][0] = v;
+        cu[q][f][1] = 0.0;
+      }
   }
   __syncthreads();  // every stage consumed and every copy landed: the tiles are free
   // row halves: warps 4..7 hand their fragments to warps 0..3
