@@ -67,6 +67,10 @@ class OptimizerConfig:
     n_samples: int = 0  # 0 = exact enumeration
     gevp_tol: float = 1e-12  # method "gevp": relative residual of A c = lambda B c
     gevp_max_iter: int = 2000
+    # method "gevp": S -> S + eps I with eps = gevp_shift * mean(diag S) (the SR diagonal
+    # shift): the BASELINE batches have an exactly singular S (fixed particle number
+    # makes the visible columns, and x_i t_j against t_j, linearly dependent)
+    gevp_shift: float = 1e-3
 
     def __post_init__(self):
         if self.method not in ("irl", "sl", "gevp"):
@@ -155,16 +159,48 @@ class BorderedOperator:
             self._sweepers[key] = sw
         return sw
 
+    shift = 0.0  # absolute diagonal shift of S in the metric (set by solve_step's GEVP form)
+
     def metric(self, u: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
-        """The bordered metric S~ [u0; u] = [u0; S u] of the GEVP form:
+        """The bordered metric S~ [u0; u] = [u0; (S + shift) u] of the GEVP form:
         the normalised state is orthogonal to the centred derivatives, so S~ = diag(1, S)."""
         if out is None:
             out = torch.zeros(self.layout.length, dtype=torch.float64, device=u.device)
         u0, uin = self.layout.parts(u)
         out0, uout = self.layout.parts(out)
         _apply(self.batch, _qgt_coeff(self.batch), uin, uout, mode=self.mode)
+        if self.shift:
+            if self.layout.hermitian:
+                uout[0].add_(uin[0], alpha=self.shift)
+                uout[1].add_(uin[1], alpha=self.shift)
+            else:
+                uout.add_(uin, alpha=self.shift)
         out0.copy_(u0)
         self.count += 1
+        return out
+
+    def metric_diagonal(self) -> torch.Tensor | None:
+        """diag(S~) = [1, S_ii] in the physical layout: S_ii = sum_n w_n |O_ni - Obar_i|^2
+        (est:335-344's diagonal), from the stored O in row chunks; None for an
+        on-the-fly batch (no stored rows to square)."""
+        b = self.batch
+        if b.otf is not None:
+            return None
+        lay = self.layout
+        obar = b.obar()
+        diag = torch.zeros(b.ld, dtype=torch.float64, device=b.device)
+        w = b.weights
+        step = max(1, (256 << 20) // (b.ld * b.o_padded.element_size()))
+        for r0 in range(0, b.n_rows, step):
+            oc = b.o_padded[r0 : r0 + step] - obar
+            diag += (w[r0 : r0 + step, None] * (oc.real ** 2 + oc.imag ** 2 if oc.is_complex() else oc * oc)).sum(0)
+        out = torch.ones(lay.length, dtype=torch.float64, device=b.device)
+        _, parts = lay.parts(out)
+        if lay.hermitian:
+            parts[0].copy_(diag)
+            parts[1].copy_(diag)
+        else:
+            parts.copy_(diag)
         return out
 
     def __call__(self, u: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
@@ -230,8 +266,23 @@ def solve_step(batch: SampleBatch, config: OptimizerConfig = OptimizerConfig(), 
     elif config.method == "gevp":
         if connected is not None:
             raise ValueError("the GEVP form takes the batch operator without the connected completion")
+        d = op.__dict__.get("_metric_diag")
+        if d is None:
+            d = op.metric_diagonal()
+            op._metric_diag = d
+        if d is not None:
+            p_idx = lay.index[1:]  # the logical P-part (padding slots excluded)
+            op.shift = float(config.gevp_shift) * float(d[p_idx].mean())
+            dd = d.clone()
+            dd[p_idx] += op.shift
+            # Jacobi preconditioner: the inverse diagonal of S~ (padding slots stay 0)
+            inv = torch.where(dd > 0, 1.0 / dd.clamp_min(1e-300), torch.zeros_like(dd))
+            precond = lambda r: r * inv  # noqa: E731
+        else:  # on-the-fly batch: no stored rows for diag(S); relative shift against tr(S)/P from the products
+            op.shift = 0.0
+            precond = None
         pair = krylov.lobpcg_smallest(op, op.metric, lay.dim, tol=config.gevp_tol, max_iter=config.gevp_max_iter,
-                                      seed=s, device=batch.device, layout=lay)
+                                      seed=s, device=batch.device, layout=lay, precond=precond)
     else:
         pair = krylov.sl_smallest(op, lay.dim, budget=config.sl_budget, seed=s, device=batch.device, layout=lay)
     d = direction_from_vector(pair.vector, gradient, batch.param_count, lay.hermitian)

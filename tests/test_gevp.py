@@ -75,7 +75,7 @@ def test_gevp_solve_step_vs_dense_oracle(cuda, n, p):
     e = -1.0 + 0.05 * rng.standard_normal(n) + 0.02 * (o @ rng.standard_normal(p))
     w = np.full(n, 1.0 / n)
     batch = E.SampleBatch([None] * n, w, e, o, n)
-    res = OPT.solve_step(batch, OPT.OptimizerConfig(method="gevp"), seed=5)
+    res = OPT.solve_step(batch, OPT.OptimizerConfig(method="gevp", gevp_shift=0.0), seed=5)
     mean, _, _ = oest.energy(w, e, n)
     a, b = _bordered_dense(w, e, o, mean)
     lam, vec = scipy.linalg.eigh(a, b)
@@ -85,3 +85,32 @@ def test_gevp_solve_step_vs_dense_oracle(cuda, n, p):
     assert abs(res.lambda_min - lam[0]) <= 1e-10 * abs(lam[0])
     d = res.direction.cpu().numpy()
     assert np.linalg.norm(d - d_ref) <= 1e-8 * np.linalg.norm(d_ref)
+
+
+@pytest.mark.gpu
+def test_gevp_with_diagonal_shift_vs_dense_oracle(cuda):
+    """With the SR diagonal shift (S + eps I, eps = shift * mean diag S) on a
+    batch whose S is exactly singular (fixed particle number, like the BASELINE
+    batches): the solve matches scipy's eigh(H~, diag(1, S + eps I))."""
+    from oracle import nqs
+    from paper_2601_01437_b200 import ansatz as A, estimators as E, optimizer as OPT, synthetic as S
+
+    cfg = S.CONFIGS[1].with_rows(2048)
+    inp = S.make_inputs(cfg)
+    arch = A.RBMArchitecture(cfg.n_inputs, cfg.hidden)
+    batch = A.build_batch(A.AnsatzParameters(arch, inp.theta), inp.x, inp.e_loc)
+    conf = OPT.OptimizerConfig(method="gevp", gevp_shift=1e-3, gevp_tol=1e-11, gevp_max_iter=5000)
+    res = OPT.solve_step(batch, conf, seed=cfg.lanczos_seed)
+    o = nqs.rbm_rows(inp.theta, inp.x, cfg.n_inputs, cfg.hidden)
+    n = len(o)
+    w = np.full(n, 1.0 / n)
+    mean, _, _ = oest.energy(w, inp.e_loc, n)
+    a, b = _bordered_dense(w, inp.e_loc, o, mean)
+    eps = 1e-3 * float(np.mean(np.diag(b)[1:]))
+    b[1:, 1:] += eps * np.eye(len(b) - 1)
+    lam, vec = scipy.linalg.eigh(a, b)
+    assert np.linalg.matrix_rank(oest.dense_qgt(w, o)) < o.shape[1]  # S itself is singular
+    assert res.converged
+    assert abs(res.lambda_min - lam[0]) <= 1e-8 * abs(lam[0])
+    d_ref = vec[1:, 0] / vec[0, 0]
+    assert np.linalg.norm(res.direction.cpu().numpy() - d_ref) <= 1e-6 * np.linalg.norm(d_ref)
