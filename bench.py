@@ -440,7 +440,8 @@ def config_record(torch, cfg, dev, peak, dmma_peak, l2buf, with_irl=True, extra=
     rec["stored"] = {"path": plan["path"], "ms_per_product": ms, "mvp_s": 1e3 / ms, "gbs_one_read": one,
                      "frac_one_read": one / peak, "frac_two_pass": 2 * one / peak,
                      "frac_two_pass_spec_8tbs": 2 * one / 8000.0, "l2": "256 MB write flush before each product",
-                     "plan": plan}
+                     "plan": plan, "alg_bytes_per_launch": o_bytes,
+                     "ncu_traffic_per_launch": ncu_traffic(cfg.name)}
     if plan["path"] == "wide":  # the two-pass path beside it, for the record
         ms2 = graph_timed(torch, lambda: apply(0, coeff, 0, mode=_lib.MVP_TWO_PASS), l2buf,
                           k=10 if o_bytes < 1e9 else 3)

@@ -31,6 +31,10 @@ else:
     vi = torch.randn(ld, dtype=torch.float64, device="cuda")
     vi[P:] = 0
     vo = torch.empty_like(vi)
+E._apply(b, c, vi, vo, mode=args.mode)  # plans, attributes, first-touch
+torch.cuda.synchronize()
+torch.cuda.cudart().cudaProfilerStart()
 for _ in range(args.reps):
     E._apply(b, c, vi, vo, mode=args.mode)
 torch.cuda.synchronize()
+torch.cuda.cudart().cudaProfilerStop()
