@@ -473,9 +473,13 @@ __global__ void __maxnreg__((NKT <= 8 && NY == 1 && !HAS_T) ? 96 : 168)
       for (int nt = 0; nt < NKT; ++nt) c[q][f][nt][0] = c[q][f][nt][1] = 0.0;
     }
   const int wj = warp & 3, wk = (warp >> 2) & 1;
-  const int jl = wj * 16 + (lane >> 2);  // A rows jl, jl + 8 (hidden units) of this lane
+  // A rows of this lane: hidden units jl (m-tile 0) and jl + 1 (m-tile 1), jl even, so one
+  // 16-byte load gives both; a quarter-warp then reads 8 distinct 16-byte chunks of one
+  // swizzled tile row (conflict-free, where consecutive units jl, jl + 8 hit 8 of the
+  // 16 bank pairs from 4 rows at once)
+  const int jl = wj * 16 + 2 * (lane >> 2);
   const double u_lo = (gu && j0 + jl < h) ? a.u[j0 + jl] : 0.0;
-  const double u_hi = (gu && j0 + jl + 8 < h) ? a.u[j0 + jl + 8] : 0.0;
+  const double u_hi = (gu && j0 + jl + 1 < h) ? a.u[j0 + jl + 1] : 0.0;
 
   if (warp == 8) {  // ---------------------------------------------- producer
     const double* yv_src[2] = {a.y, a.y2};
@@ -522,18 +526,20 @@ __global__ void __maxnreg__((NKT <= 8 && NY == 1 && !HAS_T) ? 96 : 168)
 #pragma unroll 2
       for (int kk = wk; kk < kk_end; kk += 2) {
         const int rl = kk * 4 + (lane & 3);
-        const int o0 = swz64(rl, jl), o1 = swz64(rl, jl + 8);
+        const int o0 = swz64(rl, jl);  // jl even: (jl, jl + 1) is one 16-byte chunk
         double g0, g1, t0 = 0.0, t1 = 0.0;
         if (HAS_T) {
-          t0 = Tt[o0];
-          t1 = Tt[o1];
+          const double2 tt = *reinterpret_cast<const double2*>(Tt + o0);
+          t0 = tt.x;
+          t1 = tt.y;
         }
         if (HAS_T && gu) {
           g0 = u_lo * (1.0 - t0 * t0);
           g1 = u_hi * (1.0 - t1 * t1);
         } else {
-          g0 = G[o0];
-          g1 = G[o1];
+          const double2 gg = *reinterpret_cast<const double2*>(G + o0);
+          g0 = gg.x;
+          g1 = gg.y;
         }
         const uint64_t w0 = (X[rl * OTF_XW] | one0) >> sh_base, w1 = (X[rl * OTF_XW + 1] | one1) >> sh_base;
         // the row weight rides on the B operand: B = x ? y : 0 (integer selects, no FP64
@@ -616,7 +622,7 @@ __global__ void __maxnreg__((NKT <= 8 && NY == 1 && !HAS_T) ? 96 : 168)
   // partials: C[j][kc] fragment -> part[q][blk][j][kc]
 #pragma unroll
   for (int f = 0; f < 2; ++f) {
-    const int jrow = j0 + jl + 8 * f;
+    const int jrow = j0 + jl + f;
     if (jrow >= h) continue;
 #pragma unroll
     for (int q = 0; q < NY; ++q) {
