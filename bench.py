@@ -449,7 +449,7 @@ def config_record(torch, cfg, dev, peak, dmma_peak, l2buf, with_irl=True, extra=
     if with_irl:
         rec["irl_stored"] = irl_solve(torch, OPT, batch, cfg, en)
     if with_irl and cfg.index == 2:  # the GEVP form on the same batch
-        conf = OPT.OptimizerConfig(method="gevp", gevp_tol=1e-8, gevp_max_iter=3000)
+        conf = OPT.OptimizerConfig(method="gevp", gevp_tol=1e-10, gevp_max_iter=4000)
         torch.cuda.synchronize()
         g0 = time.perf_counter()
         res = OPT.solve_step(batch, conf, seed=cfg.lanczos_seed, energy=en)
@@ -457,8 +457,8 @@ def config_record(torch, cfg, dev, peak, dmma_peak, l2buf, with_irl=True, extra=
         rec["gevp_stored"] = {"wall_ms": (time.perf_counter() - g0) * 1e3, "n_products": res.n_matvec,
                               "lambda_min": res.lambda_min, "converged": res.converged,
                               "residual": res.pair.residual, "tol": conf.gevp_tol, "shift": conf.gevp_shift,
-                              "solver": ("Jacobi-preconditioned LOBPCG on (H~, diag(1, S + eps I)), "
-                                         "eps = shift * mean diag S; one H and one S product per iteration")}
+                              "solver": ("LOBPCG on (H~, diag(1, S + eps I)), eps = shift * mean diag S; "
+                                         "one H and one S product per iteration")}
     if extra is not None:
         extra(batch, params, inp, apply, coeff, rec)
     del batch, apply, coeff

@@ -71,6 +71,7 @@ class OptimizerConfig:
     # shift): the BASELINE batches have an exactly singular S (fixed particle number
     # makes the visible columns, and x_i t_j against t_j, linearly dependent)
     gevp_shift: float = 1e-3
+    gevp_precond: bool = False  # Jacobi (inverse diag S~) preconditioning of the LOBPCG residuals
 
     def __post_init__(self):
         if self.method not in ("irl", "sl", "gevp"):
@@ -275,8 +276,11 @@ def solve_step(batch: SampleBatch, config: OptimizerConfig = OptimizerConfig(), 
             op.shift = float(config.gevp_shift) * float(d[p_idx].mean())
             dd = d.clone()
             dd[p_idx] += op.shift
-            # Jacobi preconditioner: the inverse diagonal of S~ (padding slots stay 0)
+            # Jacobi preconditioner: the inverse diagonal of S~ (padding slots stay 0); without
+            # it, a 0/1 mask keeps the search space out of S~'s exact null coordinates
             inv = torch.where(dd > 0, 1.0 / dd.clamp_min(1e-300), torch.zeros_like(dd))
+            if not config.gevp_precond:
+                inv = (inv > 0).to(inv.dtype)
             precond = lambda r: r * inv  # noqa: E731
         else:  # on-the-fly batch: no stored rows for diag(S); relative shift against tr(S)/P from the products
             op.shift = 0.0
