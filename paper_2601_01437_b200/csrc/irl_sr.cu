@@ -1222,8 +1222,8 @@ bool sweep_ok(bool cplx, int model, int n_vis, int hidden) {
   if (mode == 0) return false;
   if (cplx)  // complex-theta RBM (cfg4: 470 KB rows): statistics from the complex DMMA colsums
     return model == MODEL_RBM && n_vis <= OTF_MAX_NIN && n_vis <= 32 * SWEEP_UQ;
-  if ((n_vis & 1) || n_vis > 2 * 32 * SWEEP_UQ) return false;
-  return model == MODEL_MLP || (mode == 2 && (hidden & 1) == 0);
+  if ((n_vis & 1) || (hidden & 1) || n_vis > 2 * 32 * SWEEP_UQ) return false;  // 16-byte factor rows
+  return model == MODEL_MLP || mode == 2;
 }
 
 bool gemm_stats(bool cplx, int model, int n_vis, int hidden) {
@@ -1469,7 +1469,9 @@ int obuild_impl(bool cplx, int model, const uint8_t* x, int64_t n, int n_vis, in
     IRL_TRY(dev_info(d));
     auto fn = cplx ? k_orows_sweep<true, MODEL_RBM>
                    : (model == MODEL_MLP ? k_orows_sweep<false, MODEL_MLP> : k_orows_sweep<false, MODEL_RBM>);
-    const size_t sm = (size_t)hidden * (cplx ? 16 : 8);
+    // short rows (cfg3: 90 KB) double-buffer the factor row, long rows load it in place
+    const int dbuf = ld_u * 16 < (256 << 10) ? 1 : 0;
+    const size_t sm = (size_t)(1 + dbuf) * hidden * (cplx ? 16 : 8);
     IRL_TRY(ensure_fn_attrs((const void*)fn, d.smem_optin));
     const int64_t want = getenv("IRL_OBUILD_CHUNKS") ? atoi(getenv("IRL_OBUILD_CHUNKS")) : 4;
     const int nc = (int)std::max<int64_t>(1, std::min<int64_t>(want, n / 4096));
@@ -1490,7 +1492,7 @@ int obuild_impl(bool cplx, int model, const uint8_t* x, int64_t n, int n_vis, in
       fn<<<grid, SWEEP_NT, sm, st>>>(x + r0 * n_vis, r1 - r0, n_vis, hidden,
                                      static_cast<char*>(T) + (size_t)r0 * hidden * sS,
                                      G ? G + (size_t)r0 * hidden : nullptr, reinterpret_cast<double2*>(O) + r0 * ld_u,
-                                     ld_u);
+                                     ld_u, dbuf);
       IRL_TRY(cuda_check(cudaGetLastError(), "orows sweep launch"));
     }
     IRL_TRY(obuild_stats(cplx, model, xbits, T, G, n, n_vis, hidden, ld, w, coeff, obar, g, base + off, fork.side));

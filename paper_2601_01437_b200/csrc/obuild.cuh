@@ -485,10 +485,10 @@ template <bool CPLX, int MODEL>
 __global__ void __launch_bounds__(SWEEP_NT, 2) k_orows_sweep(const uint8_t* __restrict__ x, int64_t n_rows, int n,
                                                             int h, const void* __restrict__ Tv,
                                                             const double* __restrict__ G, double2* __restrict__ O,
-                                                            int64_t ld_u) {
+                                                            int64_t ld_u, int dbuf) {
   using S = typename Traits<CPLX>::S;
   extern __shared__ __align__(16) unsigned char smem_sw[];
-  S* fs = reinterpret_cast<S*>(smem_sw);  // [h] factor row (t or g)
+  S* fs = reinterpret_cast<S*>(smem_sw);  // [2][h] factor rows (t or g), double-buffered
   const S* T = reinterpret_cast<const S*>(Tv);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, NW = SWEEP_NT / 32;
   const int upj = CPLX ? n : n / 2;  // units per j segment
@@ -500,12 +500,35 @@ __global__ void __launch_bounds__(SWEEP_NT, 2) k_orows_sweep(const uint8_t* __re
   const int64_t P = MODEL == MODEL_RBM ? (int64_t)n + h + hn : hn + 2 * (int64_t)h + 1;
   const int64_t wb = MODEL == MODEL_MLP ? 0 : (CPLX ? (int64_t)n + h : ((int64_t)n + h) / 2);  // W block, units
   const int64_t we = wb + (int64_t)h * upj;
-  for (int64_t r = blockIdx.x; r < n_rows; r += gridDim.x) {
-    const uint8_t* xr = x + r * n;
-    __syncthreads();  // previous row's factors consumed
-    for (int j = tid; j < h; j += SWEEP_NT) {
-      if constexpr (MODEL == MODEL_MLP) fs[j] = G[r * h + j]; else fs[j] = T[r * h + j];
+  // the factor row (t or g) of the next row is copied into the other half of a
+  // double buffer with cp.async while this row is written (h * sizeof(S) is a
+  // multiple of 16 bytes: h even for real rows)
+  const S* F = MODEL == MODEL_MLP ? reinterpret_cast<const S*>(G) : T;
+  const int fchunks = (int)((size_t)h * sizeof(S) / 16);
+  auto prefetch = [&](int64_t row, S* dst) {
+    if (row < n_rows) {
+      const char* src = reinterpret_cast<const char*>(F + row * h);
+      for (int q = tid; q < fchunks; q += SWEEP_NT)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(reinterpret_cast<char*>(dst) + 16 * q)),
+                     "l"(src + 16 * q)
+                     : "memory");
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  // dbuf = 0 (long rows, whose writes dwarf the factor load): one buffer, loaded
+  // in place at the top of every row
+  int cur = 0;
+  if (dbuf) prefetch(blockIdx.x, fs);
+  for (int64_t r = blockIdx.x; r < n_rows; r += gridDim.x, cur ^= dbuf) {
+    const uint8_t* xr = x + r * n;
+    if (!dbuf) {
+      __syncthreads();  // previous row's factors consumed
+      prefetch(r, fs);
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();  // this row's factors landed; the other buffer's previous row is consumed
+    if (dbuf) prefetch(r + gridDim.x, fs + (cur ^ 1) * h);
+    const S* fr = fs + cur * h;
     // this lane's x values (its units of every segment)
     double xa[SWEEP_UQ], xb[SWEEP_UQ];
 #pragma unroll
@@ -521,11 +544,10 @@ __global__ void __launch_bounds__(SWEEP_NT, 2) k_orows_sweep(const uint8_t* __re
         }
       }
     }
-    __syncthreads();
     double2* orow = O + r * ld_u;
     if (active) {
       for (int j = warp * JW + jo; j < h; j += NW * JW) {
-        const S f = fs[j];
+        const S f = fr[j];
         double2* seg = orow + wb + (int64_t)j * upj;
 #pragma unroll
         for (int q = 0; q < SWEEP_UQ; ++q) {
@@ -545,7 +567,7 @@ __global__ void __launch_bounds__(SWEEP_NT, 2) k_orows_sweep(const uint8_t* __re
         if (e < n) {
           if constexpr (CPLX) v.x = xr[e] ? 1.0 : 0.0; else v = xr[e] ? 1.0 : 0.0;
         } else if (e < (int64_t)n + h) {
-          v = fs[e - n];
+          v = fr[e - n];
         }
       } else {
         if (e >= hn && e < hn + h) {
