@@ -380,6 +380,7 @@ __global__ void __launch_bounds__(256) k_otf_y(const double* __restrict__ tpart,
   const int64_t lo = blockIdx.x * per, hi = min(n, lo + per);
   for (int64_t r = lo + threadIdx.x; r < hi; r += blockDim.x) {
     double t = 0.0;
+#pragma unroll 4
     for (int q = 0; q < jc_count; ++q) t += tpart[(int64_t)q * n + r];
     if (offa >= 0) {
       double xa = 0.0;
