@@ -458,7 +458,7 @@ constexpr int64_t kWideMinUnits = 16384;
 
 struct WidePlan {
   int G, WM, RS, Q, PU, NS, K, upl, rpw;
-  size_t smem, ws, part_bytes, fin_bytes, ring_bytes, vsl_off;
+  size_t smem, ws, part_bytes, fin_bytes, fin_copy_bytes, ring_bytes, vsl_off;
 };
 
 using WideFn = void (*)(WideArgs);
@@ -536,7 +536,8 @@ int make_wide_plan(int64_t n, int64_t ld_u, bool cplx, WidePlan& p) {
   if (p.smem > budget) return fail(IRL_ERR_DEVICE, "wide path: shared memory");
   const size_t rec = cplx ? 32 : 16;  // LL record bytes per scalar
   p.part_bytes = align256((size_t)WIDE_NBUF * p.RS * p.G * rec);
-  p.fin_bytes = align256((size_t)WIDE_NBUF * p.RS * rec);
+  p.fin_copy_bytes = align256((size_t)WIDE_NBUF * p.RS * rec) + 256;  // + 256: replicas start on different L2 slices
+  p.fin_bytes = (size_t)WIDE_FIN_COPIES * p.fin_copy_bytes;
   p.ws = p.part_bytes + p.fin_bytes + align256((size_t)p.G * 16);
   (void)n;
   return IRL_OK;
@@ -568,6 +569,9 @@ int launch_wide(const WidePlan& p, bool cplx, WideArgs a, void* ws, cudaStream_t
   a.part = reinterpret_cast<ulonglong2*>(base);
   a.fin = reinterpret_cast<ulonglong2*>(base + p.part_bytes);
   a.gpart = reinterpret_cast<ulonglong2*>(base + p.part_bytes + p.fin_bytes);
+  a.fin_copies = WIDE_FIN_COPIES;
+  if (getenv("IRL_WIDE_FINC")) a.fin_copies = std::min(WIDE_FIN_COPIES, std::max(1, atoi(getenv("IRL_WIDE_FINC"))));
+  a.fin_stride = p.fin_copy_bytes / sizeof(ulonglong2);
   a.RS = p.RS;
   a.Q = p.Q;
   a.PU = p.PU;
@@ -581,6 +585,8 @@ int launch_wide(const WidePlan& p, bool cplx, WideArgs a, void* ws, cudaStream_t
   a.poll_ns = getenv("IRL_WIDE_POLL_NS") ? atoi(getenv("IRL_WIDE_POLL_NS")) : 160;
   a.rot = getenv("IRL_WIDE_ROT") ? atoi(getenv("IRL_WIDE_ROT")) % p.G : 0;
   a.spin_ns = getenv("IRL_WIDE_SPIN_NS") ? atoi(getenv("IRL_WIDE_SPIN_NS")) : 32;
+  a.red_delay_ns = getenv("IRL_WIDE_RDELAY") ? atoi(getenv("IRL_WIDE_RDELAY")) : 0;
+  a.agg_delay_ns = getenv("IRL_WIDE_ADELAY") ? atoi(getenv("IRL_WIDE_ADELAY")) : 0;
   // tags are block numbers: zeroed records can never match a stale one
   IRL_TRY(cuda_check(cudaMemsetAsync(base, 0, p.ws, st), "wide record reset"));
   int occ = 0;

@@ -75,6 +75,7 @@ static_assert(WIDE_NBUF >= 2 * WIDE_MAX_K + 2, "exchange ring too short for the 
 constexpr int WIDE_QPL = 2;  // partials per aggregator lane: 2 * 32 * WIDE_AW >= G
 static_assert(WIDE_QPL * 32 * WIDE_AW >= 160, "aggregator lanes must cover every SM");
 constexpr int WIDE_MAX_RS = 32;  // rows per block: one reducer lane each
+constexpr int WIDE_FIN_COPIES = 16;  // replicas of the row totals (every CTA polls them: one copy is an L2 hot spot)
 constexpr int WIDE_TMEM_COLS = 512;  // whole TMEM: one CTA per SM
 // TMEM words (32-bit columns) one consumer lane parks per block: UPL 16-byte units
 __host__ __device__ constexpr int wide_tm_words(int upl) { return 4 * upl; }
@@ -96,7 +97,9 @@ struct WideArgs {
   double* out_im;
   double* out0;
   ulonglong2* part;  // LL records [NBUF][RS][G][S doubles]   (zeroed per launch)
-  ulonglong2* fin;   // LL records [NBUF][RS][S doubles]      (zeroed per launch)
+  ulonglong2* fin;   // LL records [copies][NBUF][RS][S doubles]   (zeroed per launch)
+  int fin_copies;    // replicas of fin written by the aggregator; CTA c polls copy c % fin_copies
+  size_t fin_stride;  // records between replicas
   ulonglong2* gpart;  // LL records [G]: each slice's (F/2) . v share   (zeroed per launch)
   int RS;            // rows per block (= per stage), WIDE_CW / Q
   int Q;             // parts per row slice
@@ -111,6 +114,8 @@ struct WideArgs {
   int poll_ns;                // reducer / aggregator poll back-off (ns)
   int rot;                    // debug: CTA c takes column slice (c + rot) % G
   int spin_ns;                // consumer back-off when no stage is ready (0 = spin)
+  int red_delay_ns;           // reducers: pause between this CTA's own publish and the first poll of the totals
+  int agg_delay_ns;           // aggregators: the same before the first poll of a row's partials
 };
 
 constexpr int WIDE_TRACE_B = 512;  // traced blocks per CTA
@@ -165,53 +170,58 @@ __device__ __forceinline__ bool ld_ll_s(const ulonglong2* p, uint32_t tag, typen
 // ------------------------------------------------------------------ TMEM --
 // 32x32b shapes: thread t of the warp moves 32-bit words to / from TMEM lane
 // (lane quarter base + t), consecutive columns.
-#define TM_R8(p) "r"(p[0]), "r"(p[1]), "r"(p[2]), "r"(p[3]), "r"(p[4]), "r"(p[5]), "r"(p[6]), "r"(p[7])
-#define TM_W8(p) "=r"(p[0]), "=r"(p[1]), "=r"(p[2]), "=r"(p[3]), "=r"(p[4]), "=r"(p[5]), "=r"(p[6]), "=r"(p[7])
-__device__ __forceinline__ void tm_st8(uint32_t ta, const uint32_t* r) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(ta), TM_R8(r)
-               : "memory");
-}
-__device__ __forceinline__ void tm_ld8(uint32_t ta, uint32_t* r) {
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-               : TM_W8(r)
-               : "r"(ta)
-               : "memory");
-}
-#undef TM_R8
-#undef TM_W8
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
-// park / fetch UPL units (4 UPL words, a multiple of 8) of one lane
-template <int UPL>
-__device__ __forceinline__ void tm_park(uint32_t ta, const double2 (&x)[UPL]) {
-  static_assert((4 * UPL) % 8 == 0, "TMEM chunks of 8 words");
-#pragma unroll
-  for (int c8 = 0; c8 < UPL / 2; ++c8) {
-    uint32_t r[8];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const double2 v = x[2 * c8 + h];
-      r[4 * h + 0] = (uint32_t)__double2loint(v.x);
-      r[4 * h + 1] = (uint32_t)__double2hiint(v.x);
-      r[4 * h + 2] = (uint32_t)__double2loint(v.y);
-      r[4 * h + 3] = (uint32_t)__double2hiint(v.y);
-    }
-    tm_st8(ta + 8 * c8, r);
-  }
+// One 16-byte unit per TMEM access: the four words are the registers an
+// LDS.128 delivered (wider accesses cost register shuffles and measured slower).
+__device__ __forceinline__ void tm_st4(uint32_t ta, int4 v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(ta), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
 }
+__device__ __forceinline__ void tm_ld4(uint32_t ta, int4& v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(ta)
+               : "memory");
+}
+__device__ __forceinline__ double2 unit_of(int4 w) {
+  return make_double2(__hiloint2double(w.y, w.x), __hiloint2double(w.w, w.z));
+}
+// park UPL units (4 UPL words) of one lane
 template <int UPL>
-__device__ __forceinline__ void tm_fetch(uint32_t ta, double2 (&x)[UPL]) {
-  uint32_t r[UPL / 2][8];
+__device__ __forceinline__ void tm_park(uint32_t ta, const int4 (&x)[UPL]) {
 #pragma unroll
-  for (int c8 = 0; c8 < UPL / 2; ++c8) tm_ld8(ta + 8 * c8, r[c8]);
-  tm_wait_ld();
+  for (int k = 0; k < UPL; ++k) tm_st4(ta + 4 * k, x[k]);
+}
+
+// Sum NV values per lane over the warp with the fewest shuffles: while more
+// than one value is left, the lanes of a butterfly pair split them (one keeps
+// the lower half, its partner the upper half, each adds what the other sent),
+// then plain butterflies.  Lane l ends with the warp total of value
+// l / (32 / NV) in v[0]; the order of the additions is fixed.
+template <int NV>
+__device__ __forceinline__ void warp_sum_split(double (&v)[NV], int lane) {
+  static_assert(NV == 1 || NV == 2 || NV == 4 || NV == 8 || NV == 16, "power of two");
+  int n = NV;
 #pragma unroll
-  for (int c8 = 0; c8 < UPL / 2; ++c8)
+  for (int m = 16; m >= 1; m >>= 1) {
+    if (n > 1) {
+      n >>= 1;
+      const bool up = (lane & m) != 0;
 #pragma unroll
-    for (int h = 0; h < 2; ++h)
-      x[2 * c8 + h] = make_double2(__hiloint2double((int)r[c8][4 * h + 1], (int)r[c8][4 * h + 0]),
-                                   __hiloint2double((int)r[c8][4 * h + 3], (int)r[c8][4 * h + 2]));
+      for (int i = 0; i < NV / 2; ++i) {
+        if (i < n) {
+          const double send = up ? v[i] : v[i + n];
+          const double keep = up ? v[i + n] : v[i];
+          v[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+        }
+      }
+    } else {
+      v[0] += __shfl_xor_sync(0xffffffffu, v[0], m);
+    }
+  }
 }
 
 template <bool CPLX, int UPL, int RPW>
@@ -220,6 +230,9 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1) k_wide(const WideArgs a) {
   using S = typename T::S;
   constexpr int SW = CPLX ? 2 : 1;  // LL records per scalar
   constexpr int TMW = RPW * wide_tm_words(UPL);  // TMEM words a lane parks per block
+  constexpr int SC = CPLX ? 2 : 1;               // doubles per scalar
+  constexpr int NV = RPW * SC;                   // doubles a lane reduces per warp-step
+  constexpr int RB = UPL >= 8 ? 1 : (RPW * UPL <= 16 ? RPW : (RPW >= 2 && (RPW / 2) * UPL <= 16 ? RPW / 2 : 1));  // rows per TMEM fetch
   extern __shared__ __align__(16) unsigned char smem_w[];
   const int NS = a.NS, K = a.K, WM = a.WM, RS = a.RS, Q = a.Q, PU = a.PU;
   double2* ring = reinterpret_cast<double2*>(smem_w);                    // [NS][RS][WM]
@@ -360,6 +373,7 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1) k_wide(const WideArgs a) {
       // pace: start once this CTA has published block b itself (the others are
       // close); a row comes up every ~G / RS blocks, so sleep long
       while (published <= b) __nanosleep(256);
+      if (a.agg_delay_ns) __nanosleep(a.agg_delay_ns);
       const uint32_t tag = (uint32_t)b + 1;
       const ulonglong2* src = a.part + ((size_t)(b % WIDE_NBUF) * RS + i) * G * SW;
       S x[WIDE_QPL];
@@ -384,10 +398,10 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1) k_wide(const WideArgs a) {
       t = warp_sum<CPLX>(t);
       if (lane == 0) shagg[warp - W_AGG] = t;
       named_bar_sync(3, WIDE_AW * 32);
-      if (warp == W_AGG && lane == 0) {
+      if (warp == W_AGG && lane < a.fin_copies) {  // one replica per lane, the same total in each
         S tt = T::zero();
         for (int w = 0; w < WIDE_AW; ++w) tt = T::add(tt, shagg[w]);
-        st_ll_s<CPLX>(a.fin + ((size_t)(b % WIDE_NBUF) * RS + i) * SW, tt, tag);
+        st_ll_s<CPLX>(a.fin + (size_t)lane * a.fin_stride + ((size_t)(b % WIDE_NBUF) * RS + i) * SW, tt, tag);
       }
       named_bar_sync(3, WIDE_AW * 32);  // shagg reused by the next row
     }
@@ -406,10 +420,11 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1) k_wide(const WideArgs a) {
       // the row's coefficient loads while the exchange completes
       const S cf = (lane < rows) ? coeff[r0 + lane] : T::zero();
       const S ya = (yadd && lane < rows) ? yadd[r0 + lane] : T::zero();
-      const ulonglong2* src = a.fin + ((size_t)(b % WIDE_NBUF) * RS + lane) * SW;
+      const ulonglong2* src = a.fin + (size_t)(c % a.fin_copies) * a.fin_stride + ((size_t)(b % WIDE_NBUF) * RS + lane) * SW;
       S t = T::zero();
       bool ok = lane >= rows;
       while (published <= b) __nanosleep(64);  // no total before this CTA's own share
+      if (a.red_delay_ns) __nanosleep(a.red_delay_ns);
       const long long t0 = clock64();
       while (true) {
         if (!ok) ok = ld_ll_s<CPLX>(src, tag, t);
@@ -421,12 +436,12 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1) k_wide(const WideArgs a) {
       S y = T::mul(cf, t);
       if (yadd) y = T::add(y, ya);
       if (lane < rows) ys[j * RS + lane] = y;
-      for (int i = 0; i < rows; ++i) ysum = T::add(ysum, T::shfl(y, i));  // row order
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(&ydone[j]);
         WIDE_STAMP(b, 4);
       }
+      for (int i = 0; i < rows; ++i) ysum = T::add(ysum, T::shfl(y, i));  // row order (off the critical path)
     }
     if (lane == 0) shy[k] = ysum;
     named_bar_sync(2, (WIDE_CW + WIDE_RW) * 32);  // epilogue: shy complete
@@ -442,8 +457,14 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1) k_wide(const WideArgs a) {
   // this warp's TMEM: lane quarter warp % 4, column half warp / 4, K slots of TMW words
   const uint32_t tm = tmem_base_sh + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * WIDE_TM_COLS_PER_WARP);
   double2 acc[UPL];
+  double2 vreg[UPL];  // this lane's units of the v slice (0 past the part)
+  bool inpart[UPL];
 #pragma unroll
-  for (int k = 0; k < UPL; ++k) acc[k] = make_double2(0.0, 0.0);
+  for (int k = 0; k < UPL; ++k) {
+    acc[k] = make_double2(0.0, 0.0);
+    inpart[k] = u0p + lane + 32 * k < u1p;
+    vreg[k] = inpart[k] ? vsl[u0p + lane + 32 * k] : make_double2(0.0, 0.0);
+  }
   int nd = 0, na = 0;
   int elig = -1;  // debug trace only
   // ring positions kept incrementally (no integer division in the polling loop):
@@ -459,16 +480,26 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1) k_wide(const WideArgs a) {
       const int j = ja;
       if (ready(&ydone[j], pap)) {
         const int64_t r0 = (int64_t)na * RS + rg * RPW;
-        if (r0 < N) {
+        const int nlive = (int)min((int64_t)RPW, N - r0);  // rows of this warp that exist (<= 0: none)
+        if (nlive > 0) {
           tm_wait_st();  // the park of this slot has landed
+          // RB rows per TMEM round trip: all their loads in flight, one wait
 #pragma unroll
-          for (int r = 0; r < RPW; ++r) {
-            if (r0 + r < N) {
-              double2 x[UPL];
-              tm_fetch<UPL>(tm + (uint32_t)(j * TMW + r * wide_tm_words(UPL)), x);
-              const S y = ys[j * RS + rg * RPW + r];
+          for (int rb = 0; rb < RPW; rb += RB) {
+            int4 w[RB][UPL];
 #pragma unroll
-              for (int k = 0; k < UPL; ++k) T::axpy(acc[k], x[k], y);  // x = 0 past the part
+            for (int r = 0; r < RB; ++r)
+#pragma unroll
+              for (int k = 0; k < UPL; ++k)
+                tm_ld4(tm + (uint32_t)(j * TMW + (rb + r) * wide_tm_words(UPL) + 4 * k), w[r][k]);
+            tm_wait_ld();
+#pragma unroll
+            for (int r = 0; r < RB; ++r) {
+              if (rb + r < nlive) {
+                const S y = ys[j * RS + rg * RPW + rb + r];
+#pragma unroll
+                for (int k = 0; k < UPL; ++k) T::axpy(acc[k], unit_of(w[r][k]), y);  // x = 0 past the part
+              }
             }
           }
         }
@@ -490,34 +521,37 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1) k_wide(const WideArgs a) {
       if (ready(&full[s], pdp)) {
         const int j = jd;
         const int64_t r0 = (int64_t)nd * RS + rg * RPW;
-        S t[RPW];
+        const int nlive = (int)min((int64_t)RPW, N - r0);
+        double t[NV];
         // row by row: shared memory -> registers -> dot -> TMEM (the TMEM
         // stores are asynchronous, so the next row's loads overlap them)
 #pragma unroll
         for (int r = 0; r < RPW; ++r) {
-          const double2* row = ring + ((size_t)s * RS + rg * RPW + r) * WM;
-          const bool live = r0 + r < N;
-          double2 x[UPL];
+          const int4* row = reinterpret_cast<const int4*>(ring + ((size_t)s * RS + rg * RPW + r) * WM + u0p + lane);
+          const bool live = r < nlive;
+          int4 x[UPL];  // the unit's four words as loaded: parked as they are
 #pragma unroll
-          for (int k = 0; k < UPL; ++k) {
-            const int u = u0p + lane + 32 * k;
-            x[k] = (live && u < u1p) ? row[u] : make_double2(0.0, 0.0);
-          }
+          for (int k = 0; k < UPL; ++k) x[k] = (live && inpart[k]) ? row[32 * k] : make_int4(0, 0, 0, 0);
           S t0 = T::zero(), t1 = T::zero();
 #pragma unroll
-          for (int k = 0; k < UPL; ++k) T::dot_acc((k & 1) ? t1 : t0, x[k], vsl[min(u0p + lane + 32 * k, WM)]);
-          t[r] = T::add(t0, t1);
+          for (int k = 0; k < UPL; ++k) T::dot_acc((k & 1) ? t1 : t0, unit_of(x[k]), vreg[k]);
+          const S tr = T::add(t0, t1);
+          if constexpr (CPLX) {
+            t[2 * r] = tr.x;
+            t[2 * r + 1] = tr.y;
+          } else {
+            t[r] = tr;
+          }
           if (live) tm_park<UPL>(tm + (uint32_t)(j * TMW + r * wide_tm_words(UPL)), x);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);  // the stage is in registers / TMEM: refill it
-#pragma unroll
-        for (int m = 16; m >= 1; m >>= 1)  // the RPW butterflies interleaved
-#pragma unroll
-          for (int r = 0; r < RPW; ++r) t[r] = T::add(t[r], T::shfl_xor(t[r], m));
+        warp_sum_split<NV>(t, lane);            // lane l: the total of value l / (32 / NV)
+        if ((lane & (32 / NV - 1)) == 0)
+          reinterpret_cast<double*>(pd)[((j * RS + rg * RPW) * Q) * SC + ((lane / (32 / NV)) / SC * Q + pq) * SC +
+                                        (lane / (32 / NV)) % SC] = t[0];
+        __syncwarp();
         if (lane == 0) {
-#pragma unroll
-          for (int r = 0; r < RPW; ++r) pd[(j * RS + rg * RPW + r) * Q + pq] = t[r];
           mbar_arrive(&dotdone[j]);
           if (warp == 0) WIDE_STAMP(nd, 1);
         }

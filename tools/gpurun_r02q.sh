@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+timeout 600 python -m pytest tests -m gpu -x -q -k "wide or repeat_bitwise or config_products or guard" > gpurun_out/q_tests.txt 2>&1
+timeout 900 python tools/wide_time.py 4,5 - IRL_WIDE_STREAM=3 IRL_WIDE_STREAM=4 IRL_WIDE_STREAM=2,IRL_WIDE_ADELAY=500 IRL_WIDE_STREAM=4,IRL_WIDE_K=3 > gpurun_out/q_time.txt 2>&1
+timeout 600 python tools/wide_trace.py 4 32768 > gpurun_out/q_trace4.txt 2>&1
