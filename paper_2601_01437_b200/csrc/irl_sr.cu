@@ -480,6 +480,7 @@ int make_wide_plan(int64_t n, int64_t ld_u, bool cplx, WidePlan& p) {
   DevInfo d;
   IRL_TRY(dev_info(d));
   p.G = d.sms;
+  if (getenv("IRL_WIDE_G")) p.G = std::max(2, std::min(d.sms, atoi(getenv("IRL_WIDE_G"))));  // tuning: fewer, wider slices
   if (p.G > WIDE_QPL * 32 * WIDE_AW) return fail(IRL_ERR_DEVICE, "wide path: %d SMs exceed the aggregator lanes", p.G);
   p.WM = (int)cdiv(ld_u, p.G);
   // fewest parts per row slice (most rows per block, the biggest TMA stages)
