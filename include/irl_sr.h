@@ -124,6 +124,21 @@ int irl_mvp_c128(const double* O, int64_t n, int64_t p, int64_t ld, const double
                  const double* v_re, const double* v_im, double* out_re, double* out_im, const double* hf_re,
                  const double* hf_im, const double* u0, double* out0, int mode, void* ws, size_t ws_bytes,
                  void* stream);
+/* Two centred products for the same v over one read of O (the GEVP form
+ * H_eff v = lambda S v, PAPER Eq. 11, applies dense_heff's and dense_qgt's
+ * operators, estimators.py:319-344, to every iterate):
+ *   out_a = O_c^H (coeff_a * (O_c v)) (+ u0 * half_f), out0 = half_f . v
+ *   out_b = O_c^H (coeff_b * (O_c v))
+ * Rows on the single-CTA fused path stream O once for both; narrow (ROWS),
+ * clustered and very wide (WIDE) rows run the two products one after the other. */
+size_t irl_mvp2_workspace_bytes(int64_t n, int64_t ld, int is_complex);
+int irl_mvp2_f64(const double* O, int64_t n, int64_t p, int64_t ld, const double* obar, const double* coeff_a,
+                 const double* coeff_b, const double* v, double* out_a, double* out_b, const double* half_f,
+                 const double* u0, double* out0, void* ws, size_t ws_bytes, void* stream);
+int irl_mvp2_c128(const double* O, int64_t n, int64_t p, int64_t ld, const double* obar, const double* coeff_a,
+                  const double* coeff_b, const double* v_re, const double* v_im, double* outa_re, double* outa_im,
+                  double* outb_re, double* outb_im, const double* hf_re, const double* hf_im, const double* u0,
+                  double* out0, void* ws, size_t ws_bytes, void* stream);
 /* Which path (IRL_MVP_FUSED / IRL_MVP_TWO_PASS / IRL_MVP_ROWS / IRL_MVP_WIDE) AUTO takes, and its launch
  * geometry (cluster size, units per slice, threads, rows per stage, stages,
  * row blocks); for benches and tests.  Returns IRL_OK or an error. */

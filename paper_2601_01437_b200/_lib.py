@@ -58,6 +58,9 @@ SIGNATURES = {
     "irl_mvp_workspace_bytes": (_SZ, [_I64, _I64, _I]),
     "irl_mvp_f64": (_I, [_P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _I, _P, _SZ, _P]),
     "irl_mvp_c128": (_I, [_P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P, _SZ, _P]),
+    "irl_mvp2_workspace_bytes": (_SZ, [_I64, _I64, _I]),
+    "irl_mvp2_f64": (_I, [_P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "irl_mvp2_c128": (_I, [_P, _I64, _I64, _I64] + [_P] * 14 + [_SZ, _P]),
     "irl_mvp_plan": (_I, [_I64, _I64, _I, _I, _P, _P]),
     "irl_lanczos_step_small": (_I, [_P, _I64, _P, _I64, _I, _I, _P, _P]),
     "irl_lanczos_step_cluster": (_I, [_P, _I64, _P, _I64, _I, _I, _P, _P]),

@@ -111,10 +111,10 @@ bool aligned16(const void* p) { return p == nullptr || (reinterpret_cast<uintptr
 // ----------------------------------------------------------- kernels ----
 using StreamFn = void (*)(StreamArgs);
 
-template <bool CPLX, int MODE, bool ADD = false>
+template <bool CPLX, int MODE, bool ADD = false, bool DUAL = false>
 StreamFn pick_stream(int ppt, int R) {
 #define IRL_CASE(P, RR) \
-  if (ppt == P && R == RR) return k_stream<CPLX, P, RR, MODE, ADD>;
+  if (ppt == P && R == RR) return k_stream<CPLX, P, RR, MODE, ADD, DUAL>;
   IRL_CASE(2, 1) IRL_CASE(2, 2) IRL_CASE(2, 4) IRL_CASE(4, 1) IRL_CASE(4, 2) IRL_CASE(4, 4)
   IRL_CASE(8, 1) IRL_CASE(8, 2) IRL_CASE(8, 4) IRL_CASE(16, 1) IRL_CASE(16, 2) IRL_CASE(16, 4)
 #undef IRL_CASE
@@ -136,6 +136,7 @@ struct Plan {
   size_t smem = 0;
   StreamFn fn = nullptr;
   StreamFn fn_add = nullptr;  // MODE_FUSED with the additive row term (connected product)
+  StreamFn fn_dual = nullptr;  // MODE_FUSED with two coefficient vectors (H_eff v and S v over one read)
 };
 
 size_t stream_extra_smem(bool cplx, int R, int C, int NS) {
@@ -180,8 +181,11 @@ bool choose_geom(int64_t ld_u, int C, bool cplx, int mode, int budget, Plan& p, 
   p.NS = NS;
   p.smem = (size_t)NS * R * slice + stream_extra_smem(cplx, R, C, NS);
   p.fn = pick_stream_any(cplx, mode, best_ppt, R);
-  if (mode == MODE_FUSED)
+  if (mode == MODE_FUSED) {
     p.fn_add = cplx ? pick_stream<true, MODE_FUSED, true>(best_ppt, R) : pick_stream<false, MODE_FUSED, true>(best_ppt, R);
+    p.fn_dual = cplx ? pick_stream<true, MODE_FUSED, false, true>(best_ppt, R)
+                     : pick_stream<false, MODE_FUSED, false, true>(best_ppt, R);
+  }
   return p.fn != nullptr;
 }
 
@@ -248,6 +252,7 @@ int make_plan_uncached(int64_t n, int64_t ld_u, bool cplx, int mode, Plan& out) 
       if (!choose_geom(ld_u, C, cplx, mode, budget, p)) continue;
       IRL_TRY(ensure_fn_attrs((const void*)p.fn, budget));
       if (p.fn_add) IRL_TRY(ensure_fn_attrs((const void*)p.fn_add, budget));
+      if (p.fn_dual) IRL_TRY(ensure_fn_attrs((const void*)p.fn_dual, budget));
       int active = 0;
       if (C == 1) {
         int occ = 0;
@@ -351,7 +356,9 @@ int launch_stream(const Plan& p, const StreamArgs& a, cudaStream_t st) {
   args.stages = p.NS;
   args.dbg = 0;
   void* kargs[] = {&args};
-  const StreamFn fn = (args.yadd && p.mode == MODE_FUSED) ? p.fn_add : p.fn;
+  const StreamFn fn = (p.mode == MODE_FUSED && args.coeff1) ? p.fn_dual
+                      : (args.yadd && p.mode == MODE_FUSED) ? p.fn_add
+                                                             : p.fn;
   if (!fn) return fail(IRL_ERR_DEVICE, "no stream kernel instance");
   return cuda_check(cudaLaunchKernelExC(&cfg, (const void*)fn, kargs), "stream kernel launch");
 }
@@ -724,6 +731,86 @@ size_t mvp_ws_bytes(int64_t n, int64_t ld, bool cplx) {
   }
   g_err.clear();
   return best;
+}
+
+// ------------------------------------------------------ dual product ---
+// H_eff v and S v for the same v (the GEVP form applies both to every
+// iterate): rows on the fused single-pass path read O once for both
+// (k_stream DUAL); other shapes (rows, wide) run two products.
+bool mvp2_fused(int64_t n, int64_t ld_u, bool cplx, Plan& pl) {
+  if (ld_u <= kRowsMaxUnits) return false;
+  WidePlan wp{};
+  if (ld_u >= kWideMinUnits && make_wide_plan(n, ld_u, cplx, wp) == IRL_OK) return false;
+  // single-CTA rows only: the 2-CTA cluster plans (cfg3) run their 4-unit instances at 80 registers, where the
+  // second accumulator spills and the pair measured slower than two products (4.38 against 4.23 ms)
+  const bool ok = make_plan(n, ld_u, cplx, MODE_FUSED, pl) == IRL_OK && pl.C == 1 && pl.fn_dual;
+  g_err.clear();
+  return ok;
+}
+
+size_t mvp2_ws_bytes(int64_t n, int64_t ld, bool cplx) {
+  const int64_t ld_u = cplx ? ld : ld / 2;
+  size_t best = mvp_ws_bytes(n, ld, cplx);
+  Plan pl;
+  if (mvp2_fused(n, ld_u, cplx, pl))
+    best = std::max(best, mvp_ws_layout(pl, n, ld_u, cplx, nullptr).bytes + align256((size_t)pl.nb * ld_u * 16) +
+                              align256((size_t)pl.nb * (cplx ? 16 : 8)));
+  return best;
+}
+
+int mvp2_impl(bool cplx, const double* O, int64_t n, int64_t p, int64_t ld, const double* obar, const double* coeff_a,
+              const double* coeff_b, const double* v_re, const double* v_im, double* outa_re, double* outa_im,
+              double* outb_re, double* outb_im, const double* hf_re, const double* hf_im, const double* u0,
+              double* out0, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (!O || !coeff_a || !coeff_b || !v_re || !outa_re || !outb_re) return fail(IRL_ERR_ARG, "null required pointer");
+  if (n < 1 || p < 1 || ld < p) return fail(IRL_ERR_ARG, "bad shape n=%lld p=%lld ld=%lld", (long long)n,
+                                            (long long)p, (long long)ld);
+  if (ld != irl_padded_ld(p, cplx)) return fail(IRL_ERR_ALIGN, "ld must equal irl_padded_ld(p)");
+  if (!aligned16(O) || !aligned16(obar) || !aligned16(ws) ||
+      (!cplx && (!aligned16(v_re) || !aligned16(outa_re) || !aligned16(outb_re) || !aligned16(hf_re))))
+    return fail(IRL_ERR_ALIGN, "pointers must be 16-byte aligned");
+  const int64_t ld_u = cplx ? ld : ld / 2;
+  Plan pl;
+  if (!mvp2_fused(n, ld_u, cplx, pl)) {  // two products (each picks its own path)
+    IRL_TRY(mvp_impl(cplx, O, n, p, ld, obar, coeff_a, nullptr, v_re, v_im, outa_re, outa_im, hf_re, hf_im, u0, out0,
+                     IRL_MVP_AUTO, ws, ws_bytes, st));
+    return mvp_impl(cplx, O, n, p, ld, obar, coeff_b, nullptr, v_re, v_im, outb_re, outb_im, nullptr, nullptr, nullptr,
+                    nullptr, IRL_MVP_AUTO, ws, ws_bytes, st);
+  }
+  const size_t sS = cplx ? 16 : 8;
+  MvpWs w = mvp_ws_layout(pl, n, ld_u, cplx, ws);
+  const size_t part_b = align256((size_t)pl.nb * ld_u * 16), ysum_b = align256((size_t)pl.nb * sS);
+  if (ws_bytes < w.bytes + part_b + ysum_b) return fail(IRL_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes,
+                                                        w.bytes + part_b + ysum_b);
+  char* extra = static_cast<char*>(ws) + w.bytes;
+  StreamArgs a{};
+  a.O = reinterpret_cast<const double2*>(O);
+  a.n_rows = n;
+  a.ld_u = ld_u;
+  a.v_re = v_re;
+  a.v_im = v_im;
+  a.hf_re = hf_re;
+  a.hf_im = hf_im;
+  a.obar = reinterpret_cast<const double2*>(obar);
+  a.coeff0 = coeff_a;
+  a.coeff1 = coeff_b;
+  a.part0 = w.part;
+  a.part1 = reinterpret_cast<double2*>(extra);
+  a.ysum = w.ysum;
+  a.ysum1 = extra + part_b;
+  a.spart = w.spart;
+  a.gpart = w.gpart;
+  IRL_TRY(launch_stream(pl, a, st));
+  if (cplx) {
+    IRL_TRY(launch_finish_mvp<true>(a.part0, pl.nb, ld_u, a.ysum, a.obar, hf_re, hf_im, u0, outa_re, outa_im, w.gpart, 1,
+                                    out0, st));
+    return launch_finish_mvp<true>(a.part1, pl.nb, ld_u, a.ysum1, a.obar, nullptr, nullptr, nullptr, outb_re, outb_im,
+                                   w.gpart, 1, nullptr, st);
+  }
+  IRL_TRY(launch_finish_mvp<false>(a.part0, pl.nb, ld_u, a.ysum, a.obar, hf_re, hf_im, u0, outa_re, outa_im, w.gpart, 1,
+                                   out0, st));
+  return launch_finish_mvp<false>(a.part1, pl.nb, ld_u, a.ysum1, a.obar, nullptr, nullptr, nullptr, outb_re, outb_im,
+                                  w.gpart, 1, nullptr, st);
 }
 
 // --------------------------------------------------------- colstats ----
@@ -2117,6 +2204,23 @@ int irl_mvp_c128(const double* O, int64_t n, int64_t p, int64_t ld, const double
                  void* stream) {
   return mvp_impl(true, O, n, p, ld, obar, coeff, nullptr, v_re, v_im, out_re, out_im, hf_re, hf_im, u0, out0, mode, ws,
                   ws_bytes, (cudaStream_t)stream);
+}
+
+size_t irl_mvp2_workspace_bytes(int64_t n, int64_t ld, int is_complex) { return mvp2_ws_bytes(n, ld, is_complex != 0); }
+
+int irl_mvp2_f64(const double* O, int64_t n, int64_t p, int64_t ld, const double* obar, const double* coeff_a,
+                 const double* coeff_b, const double* v, double* out_a, double* out_b, const double* half_f,
+                 const double* u0, double* out0, void* ws, size_t ws_bytes, void* stream) {
+  return mvp2_impl(false, O, n, p, ld, obar, coeff_a, coeff_b, v, nullptr, out_a, nullptr, out_b, nullptr, half_f,
+                   nullptr, u0, out0, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int irl_mvp2_c128(const double* O, int64_t n, int64_t p, int64_t ld, const double* obar, const double* coeff_a,
+                  const double* coeff_b, const double* v_re, const double* v_im, double* outa_re, double* outa_im,
+                  double* outb_re, double* outb_im, const double* hf_re, const double* hf_im, const double* u0,
+                  double* out0, void* ws, size_t ws_bytes, void* stream) {
+  return mvp2_impl(true, O, n, p, ld, obar, coeff_a, coeff_b, v_re, v_im, outa_re, outa_im, outb_re, outb_im, hf_re,
+                   hf_im, u0, out0, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 int irl_mvp_plan(int64_t n, int64_t ld, int is_complex, int mode, int* out_path, int* out_geom7) {

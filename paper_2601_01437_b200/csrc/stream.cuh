@@ -56,6 +56,7 @@ struct StreamArgs {
   double2* part0;  // [nb][ld_u]
   double2* part1;  // [nb][ld_u]   (STATS)
   void* ysum;      // S[nb]
+  void* ysum1;     // S[nb]         (FUSED DUAL: the second product's sum of y)
   void* tpart;     // S[C][n_rows]  (DOT -> ACC)
   void* spart;     // S[C]          (DOT -> ACC; FUSED writes [0])
   double* gpart;   // double[C]     (DOT; FUSED writes [0])
@@ -82,8 +83,13 @@ __host__ __device__ constexpr int stream_max_nt(int ppt) {
 // connected product, so the plain fused product keeps its exact schedule
 // (a runtime test cost the clustered cfg3 product 2.15 -> 2.72 ms).  MODE_ACC
 // tests yadd at run time (no measurable cost there).
-template <bool CPLX, int PPT, int R, int MODE, bool ADD = false>
+//
+// DUAL (MODE_FUSED only): two products over the same read of O for the same
+// v -- y0 = coeff0 (t - s), y1 = coeff1 (t - s), acc0 / acc1 -> part0 / part1
+// (the GEVP form needs H_eff v and S v together, PAPER Eq. 11).
+template <bool CPLX, int PPT, int R, int MODE, bool ADD = false, bool DUAL = false>
 __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const StreamArgs a) {
+  static_assert(!DUAL || (MODE == MODE_FUSED && !ADD), "DUAL is a plain fused product with two coefficient vectors");
   constexpr bool kAdd = (MODE == MODE_FUSED && ADD) || MODE == MODE_ACC;
   using T = Traits<CPLX>;
   using S = typename T::S;
@@ -302,10 +308,12 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
 
   // finish group g: cluster-summed t -> y -> accumulate -> release the stage
   S ys = T::zero();
+  S ys1 = T::zero();
   auto acc_group = [&](int g, Pos p, S tin, S cf0, S cf1) {
     const int rows = rows_of(g);
     const double2* st = ring + (size_t)p.s * R * WM;
     S yv = T::zero();
+    S yv1 = T::zero();  // DUAL: the second product's y
     if constexpr (MODE == MODE_FUSED || MODE == MODE_ACC) {
       S t = tin;
       if constexpr (MODE == MODE_FUSED) {
@@ -322,6 +330,7 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
       if (lane < rows) {
         yv = T::mul(cf0, T::sub(t, s_val));
         if constexpr (kAdd) yv = T::add(yv, cf1);  // cf1 = yadd_n (0 without)
+        if constexpr (DUAL) yv1 = T::mul(cf1, T::sub(t, s_val));
       }
     } else {
       yv = cf0;
@@ -333,13 +342,15 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
         const S y = T::shfl(yv, r);
         S y1 = T::zero();
         if constexpr (MODE == MODE_STATS) y1 = T::shfl(cf1, r);
+        if constexpr (DUAL) y1 = T::shfl(yv1, r);
         if (MODE != MODE_STATS && tid == 0) ys = T::add(ys, y);
+        if (DUAL && tid == 0) ys1 = T::add(ys1, y1);
 #pragma unroll
         for (int k = 0; k < PPT; ++k) {
           if (k < kval) {
             const double2 u = st[(size_t)r * WM + tid + k * NT];
             T::axpy(acc0[k], u, y);
-            if constexpr (MODE == MODE_STATS) T::axpy(acc1[k], u, y1);
+            if constexpr (MODE == MODE_STATS || DUAL) T::axpy(acc1[k], u, y1);
           }
         }
       }
@@ -365,6 +376,7 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
         if constexpr (kAdd) {
           if (a.yadd) cf1 = reinterpret_cast<const S*>(a.yadd)[r0 + lane];
         }
+        if constexpr (DUAL) cf1 = reinterpret_cast<const S*>(a.coeff1)[r0 + lane];
       }
       if constexpr (MODE == MODE_ACC) {
         for (int c = 0; c < C; ++c)
@@ -399,7 +411,7 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
         acc_group(g, pa, T::zero(), cf0, cf1);
         advance(pa);
         cf0 = cn0;
-        if constexpr (kAdd) cf1 = cn1;
+        if constexpr (kAdd || DUAL) cf1 = cn1;
       }
     }
   } else {
@@ -413,15 +425,16 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
 
   if constexpr (MODE != MODE_DOT) {
     double2* p0 = a.part0 + (int64_t)blk * a.ld_u + col0;
-    double2* p1 = (MODE == MODE_STATS) ? a.part1 + (int64_t)blk * a.ld_u + col0 : nullptr;
+    double2* p1 = (MODE == MODE_STATS || DUAL) ? a.part1 + (int64_t)blk * a.ld_u + col0 : nullptr;
 #pragma unroll
     for (int k = 0; k < PPT; ++k) {
       if (k < kval) {
         p0[tid + k * NT] = acc0[k];
-        if constexpr (MODE == MODE_STATS) p1[tid + k * NT] = acc1[k];
+        if constexpr (MODE == MODE_STATS || DUAL) p1[tid + k * NT] = acc1[k];
       }
     }
     if (MODE != MODE_STATS && rank == 0 && tid == 0) reinterpret_cast<S*>(a.ysum)[blk] = ys;
+    if (DUAL && rank == 0 && tid == 0) reinterpret_cast<S*>(a.ysum1)[blk] = ys1;
   }
   if (clustered) cluster_sync();
 }

@@ -203,6 +203,16 @@ class SampleBatch:
             self._ws[key] = ws
         return ws
 
+    def mvp2_workspace(self) -> torch.Tensor:
+        """Workspace of the two-output product (``irl_mvp2_*``) on the current stream."""
+        key = ("mvp2", self._stream())
+        ws = self._ws.get(key)
+        if ws is None:
+            nbytes = int(_lib.lib().irl_mvp2_workspace_bytes(self.n_rows, self.ld, int(self.is_complex)))
+            ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
+            self._ws[key] = ws
+        return ws
+
     def coefficients(self, mean: float) -> torch.Tensor:
         """Product coefficient c_n = w_n (e_n - E): est:166-168, est:186
         (Hermitian batches: w_n Re(e_n - E))."""
@@ -410,6 +420,39 @@ def _apply(batch: SampleBatch, coeff: torch.Tensor | None, v: torch.Tensor, out:
               _lib.ptr(h_im), _lib.ptr(u0), _lib.ptr(out0), int(mode), _lib.ptr(ws), ws.numel(), stream)
 
 
+def _apply2(batch: SampleBatch, coeff_a: torch.Tensor, coeff_b: torch.Tensor, v, out_a, out_b, *, half_f=None,
+            u0=None, out0=None) -> None:
+    """Two raw device products for the same padded ``v`` (``irl_mvp2_*``):
+    ``out_a`` with ``coeff_a`` and the optional bordered terms, ``out_b`` with
+    ``coeff_b``.  Stored batches whose rows take the fused single-pass path
+    stream O once for both; every other batch runs two ``_apply`` calls."""
+    if batch.otf is not None:
+        _apply(batch, coeff_a, v, out_a, half_f=half_f, u0=u0, out0=out0)
+        _apply(batch, coeff_b, v, out_b)
+        return
+    obar = batch.obar()
+    stream = batch._stream()
+    ws = batch.mvp2_workspace()
+    n = batch.n_rows
+    if not batch.is_complex:
+        _lib.call("irl_mvp2_f64", _lib.ptr(batch.o_padded), n, batch.param_count, batch.ld, _lib.ptr(obar),
+                  _lib.ptr(coeff_a), _lib.ptr(coeff_b), _lib.ptr(v), _lib.ptr(out_a), _lib.ptr(out_b),
+                  _lib.ptr(half_f), _lib.ptr(u0), _lib.ptr(out0), _lib.ptr(ws), ws.numel(), stream)
+        return
+    if batch.kind == KIND_HERMITIAN:
+        v_re, v_im = v
+        a_re, a_im = out_a
+        b_re, b_im = out_b
+        h_re, h_im = half_f if half_f is not None else (None, None)
+    else:
+        v_re, v_im, a_re, a_im, b_re, b_im = v, None, out_a, None, out_b, None
+        h_re, h_im = half_f, None
+    _lib.call("irl_mvp2_c128", _lib.ptr(batch.o_padded), n, batch.param_count, batch.ld, _lib.ptr(obar),
+              _lib.ptr(coeff_a), _lib.ptr(coeff_b), _lib.ptr(v_re), _lib.ptr(v_im), _lib.ptr(a_re), _lib.ptr(a_im),
+              _lib.ptr(b_re), _lib.ptr(b_im), _lib.ptr(h_re), _lib.ptr(h_im), _lib.ptr(u0), _lib.ptr(out0),
+              _lib.ptr(ws), ws.numel(), stream)
+
+
 def _apply_connected(batch, cache, coeff, obar, v, out, mode, half_f, u0, out0, stream) -> None:
     cache._check_batch(batch)
     ws = cache.workspace(batch)
@@ -594,6 +637,47 @@ def _qgt_coeff(batch: SampleBatch) -> torch.Tensor:
 def qgt_matvec(batch: SampleBatch, v, *, mode: int = _lib.MVP_AUTO):
     """S v = O_c^H (w (O_c v)) — matrix-free ``dense_qgt`` (est:335-344)."""
     return _product(batch, _qgt_coeff(batch), v, mode)
+
+
+def heff_qgt_matvec(batch: SampleBatch, energy: EnergyEstimate, v):
+    """(H_eff v, S v) for one v -- est:171-186 with both coefficient vectors
+    (w e_c and w) over a single read of the stored O where the rows take the
+    fused single-pass path (``irl_mvp2_*``); the GEVP form H_eff c = lambda S c
+    (PAPER Eq. 11; dense oracles est:319-344) applies both to every iterate.
+
+    numpy in -> numpy pair out; torch (device) in -> torch pair out.
+    """
+    p = batch.param_count
+    as_numpy = not isinstance(v, torch.Tensor)
+    shape = np.asarray(v).shape if as_numpy else tuple(v.shape)
+    if shape != (p,):  # est:178-181
+        raise ValueError(f"vector length {shape} does not match p={p}")
+    dev, ld = batch.device, batch.ld
+    ch, cs = batch.coefficients(energy.mean), _qgt_coeff(batch)
+    if batch.kind == KIND_HERMITIAN:
+        vt = _as_tensor(v, torch.complex128, dev)
+        if not bool(torch.isfinite(torch.view_as_real(vt)).all()):  # est:182-183
+            raise ValueError("non-finite input vector")
+        vin = _staging(batch, (2, ld))
+        vin[0, :p] = vt.real
+        vin[1, :p] = vt.imag
+        out = torch.empty((4, ld), dtype=torch.float64, device=dev)
+        _apply2(batch, ch, cs, (vin[0], vin[1]), (out[0], out[1]), (out[2], out[3]))
+        hv, sv = torch.complex(out[0, :p], out[1, :p]), torch.complex(out[2, :p], out[3, :p])
+    else:
+        if (not as_numpy) and torch.is_complex(v):
+            raise ValueError("complex vector needs a hermitian batch")
+        vt = _as_tensor(v, torch.float64, dev)
+        if not bool(torch.isfinite(vt).all()):
+            raise ValueError("non-finite input vector")
+        vin = _staging(batch, (ld,))
+        vin[:p] = vt
+        out = torch.empty((2, ld), dtype=torch.float64, device=dev)
+        _apply2(batch, ch, cs, vin, out[0], out[1])
+        hv, sv = out[0, :p], out[1, :p]
+    if as_numpy:
+        return hv.cpu().numpy(), sv.cpu().numpy()
+    return hv, sv
 
 
 class ConnectedCache:

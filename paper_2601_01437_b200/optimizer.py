@@ -42,6 +42,7 @@ from .estimators import (
     EnergyEstimate,
     SampleBatch,
     _apply,
+    _apply2,
     _qgt_coeff,
     energy_gradient,
     estimate_energy,
@@ -180,6 +181,29 @@ class BorderedOperator:
         self.count += 1
         return out
 
+    def both(self, u: torch.Tensor):
+        """(H~ u, S~ u) of the GEVP form in one launch sequence: where the rows
+        take the fused single-pass path, O is read once for both products
+        (``irl_mvp2_*``); counts as two products."""
+        if self.connected is not None or self.mode != _lib.MVP_AUTO:
+            return self(u), self.metric(u)
+        lay = self.layout
+        ha = torch.zeros(lay.length, dtype=torch.float64, device=u.device)
+        sb = torch.zeros(lay.length, dtype=torch.float64, device=u.device)
+        u0, uin = lay.parts(u)
+        a0, aout = lay.parts(ha)
+        b0, bout = lay.parts(sb)
+        _apply2(self.batch, self.coeff, _qgt_coeff(self.batch), uin, aout, bout, half_f=self.half_f, u0=u0, out0=a0)
+        if self.shift:
+            if lay.hermitian:
+                bout[0].add_(uin[0], alpha=self.shift)
+                bout[1].add_(uin[1], alpha=self.shift)
+            else:
+                bout.add_(uin, alpha=self.shift)
+        b0.copy_(u0)
+        self.count += 2
+        return ha, sb
+
     def metric_diagonal(self) -> torch.Tensor | None:
         """diag(S~) = [1, S_ii] in the physical layout: S_ii = sum_n w_n |O_ni - Obar_i|^2
         (est:335-344's diagonal), from the stored O in row chunks; None for an
@@ -286,7 +310,7 @@ def solve_step(batch: SampleBatch, config: OptimizerConfig = OptimizerConfig(), 
             op.shift = 0.0
             precond = None
         pair = krylov.lobpcg_smallest(op, op.metric, lay.dim, tol=config.gevp_tol, max_iter=config.gevp_max_iter,
-                                      seed=s, device=batch.device, layout=lay, precond=precond)
+                                      seed=s, device=batch.device, layout=lay, precond=precond, apply_ab=op.both)
     else:
         pair = krylov.sl_smallest(op, lay.dim, budget=config.sl_budget, seed=s, device=batch.device, layout=lay)
     d = direction_from_vector(pair.vector, gradient, batch.param_count, lay.hermitian)

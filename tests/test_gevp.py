@@ -114,3 +114,93 @@ def test_gevp_with_diagonal_shift_vs_dense_oracle(cuda):
     assert abs(res.lambda_min - lam[0]) <= 1e-8 * abs(lam[0])
     d_ref = vec[1:, 0] / vec[0, 0]
     assert np.linalg.norm(res.direction.cpu().numpy() - d_ref) <= 1e-6 * np.linalg.norm(d_ref)
+
+
+def test_lobpcg_apply_ab_equals_separate_products():
+    """lobpcg_smallest(apply_ab=...) takes (A v, B v) from one call (the device
+    operator streams O once for the pair): same iterates, same answer and the
+    same product count as two separate calls."""
+    import torch
+    from paper_2601_01437_b200 import krylov
+
+    rng = np.random.default_rng(11)
+    a, b = _pencil(rng, 40, 100.0)
+    ta, tb = torch.as_tensor(a), torch.as_tensor(b)
+    calls = [0]
+
+    def both(v):
+        calls[0] += 1
+        return ta @ v, tb @ v
+
+    one = krylov.lobpcg_smallest(lambda v: ta @ v, lambda v: tb @ v, 40, tol=1e-11, max_iter=5000, seed=2)
+    two = krylov.lobpcg_smallest(lambda v: ta @ v, lambda v: tb @ v, 40, tol=1e-11, max_iter=5000, seed=2,
+                                 apply_ab=both)
+    assert two.converged and one.converged
+    assert two.value == one.value and two.n_matvec == one.n_matvec == 2 * calls[0]
+    assert torch.equal(two.vector, one.vector)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,p,kind", [
+    (3000, 1500, "real"),        # fused single-pass rows: one read of O for both products
+    (2048, 11265, "real"),       # cfg3 width (2-CTA cluster plan): two products
+    (1501, 430, "real"),         # narrow rows: two products (warp-per-row path)
+    (2500, 700, "hermitian"),    # complex fused rows
+    (1200, 300, "complex_raw"),
+])
+def test_heff_qgt_matvec_one_read(cuda, n, p, kind):
+    """estimators.heff_qgt_matvec (irl_mvp2_*): H_eff v and S v for one v equal
+    the separate heff_matvec / qgt_matvec products bit for bit (the same
+    operations in the same order, one pass over O) and the oracle's est:171-186
+    restatement within 1e-10."""
+    import torch
+    from paper_2601_01437_b200 import estimators as E
+
+    rng = np.random.default_rng(n + p)
+    o = rng.standard_normal((n, p)) * 0.1
+    v = rng.standard_normal(p)
+    e = -1.0 + 0.05 * rng.standard_normal(n)
+    if kind != "real":
+        o = o + 0.1j * rng.standard_normal((n, p))
+        e = e + 0.01j * rng.standard_normal(n)
+    if kind == "hermitian":
+        v = v + 1j * rng.standard_normal(p)
+    w = rng.random(n)
+    w /= w.sum()
+    batch = E.SampleBatch([None] * n, w, e, o, n, kind=kind)
+    en = E.estimate_energy(batch)
+    vt = torch.as_tensor(v, device="cuda")
+    hv, sv = E.heff_qgt_matvec(batch, en, vt)
+    assert torch.equal(hv, E.heff_matvec(batch, en, vt))
+    assert torch.equal(sv, E.qgt_matvec(batch, vt))
+    hn, sn = E.heff_qgt_matvec(batch, en, v)  # numpy in -> numpy out
+    assert np.array_equal(hn, hv.cpu().numpy()) and np.array_equal(sn, sv.cpu().numpy())
+    if kind == "real":
+        mean, _, _ = oest.energy(w, e, n)
+        ref_h = oest.heff(w, e, o, mean, v)
+        ref_s = oest.qgt(w, o, v)
+        assert np.linalg.norm(hn - ref_h) <= 1e-10 * np.linalg.norm(ref_h)
+        assert np.linalg.norm(sn - ref_s) <= 1e-10 * np.linalg.norm(ref_s)
+    with pytest.raises(ValueError):
+        E.heff_qgt_matvec(batch, en, np.zeros(p + 1))
+
+
+@pytest.mark.gpu
+def test_gevp_fused_pair_solve(cuda):
+    """solve_step(method="gevp") on rows wide enough for the one-read pair
+    (p = 1200): lambda within 1e-9 of scipy's dense eigh of the oracle pencil."""
+    from paper_2601_01437_b200 import estimators as E, optimizer as OPT
+
+    n, p = 4000, 1200
+    rng = np.random.default_rng(77)
+    o = rng.standard_normal((n, p)) * 0.1
+    e = -1.0 + 0.05 * rng.standard_normal(n) + 0.02 * (o @ rng.standard_normal(p))
+    w = np.full(n, 1.0 / n)
+    batch = E.SampleBatch([None] * n, w, e, o, n)
+    res = OPT.solve_step(batch, OPT.OptimizerConfig(method="gevp", gevp_shift=0.0, gevp_tol=1e-11,
+                                                    gevp_max_iter=6000), seed=5)
+    mean, _, _ = oest.energy(w, e, n)
+    a, b = _bordered_dense(w, e, o, mean)
+    lam = scipy.linalg.eigh(a, b, eigvals_only=True, subset_by_index=[0, 0])
+    assert res.converged
+    assert abs(res.lambda_min - lam[0]) <= 1e-9 * abs(lam[0])
