@@ -31,9 +31,11 @@
 //              Obar.v) to part[b % NBUF][row][c];
 //   aggregate  CTA r % G polls the G partials of row r, sums them in a
 //              fixed order (the same order whichever CTA aggregates) and
-//              writes t_r to fin[b % NBUF][row];
-//   reduce     every CTA polls fin, forms y_row = c_row t_row (+ yadd) --
-//              bit-identical in every CTA -- and accumulates with it.
+//              writes t_r to fin[copy][b % NBUF][row], WIDE_FIN_COPIES replicas
+//              (every CTA polls the totals: one copy is an L2 hot spot);
+//   reduce     every CTA polls its replica (c % copies), forms
+//              y_row = c_row t_row (+ yadd) -- bit-identical in every CTA --
+//              and accumulates with it.
 //
 // Warp roles (one CTA, WIDE_THREADS threads):
 //   consumers (WIDE_CW warps)  warp w owns rows (w / Q) RPW ... + RPW - 1 of a
