@@ -446,6 +446,24 @@ def config_record(torch, cfg, dev, peak, dmma_peak, l2buf, with_irl=True, extra=
         ms2 = graph_timed(torch, lambda: apply(0, coeff, 0, mode=_lib.MVP_TWO_PASS), l2buf,
                           k=10 if o_bytes < 1e9 else 3)
         rec["stored"]["two_pass_ms_per_product"] = ms2
+    if plan["path"] == "fused" and plan["cluster"] == 1 and not batch.is_complex:
+        # H_eff v and S v for one v over one read of O (irl_mvp2_f64), against the two products
+        ld = batch.ld
+        pv = torch.zeros(ld, dtype=torch.float64, device=dev)
+        pv[: batch.param_count] = torch.randn(batch.param_count, dtype=torch.float64, device=dev)
+        pa, pb = torch.empty_like(pv), torch.empty_like(pv)
+        cs = E._qgt_coeff(batch)
+
+        def two():
+            E._apply(batch, coeff, pv, pa)
+            E._apply(batch, cs, pv, pb)
+
+        t2 = graph_timed(torch, two, l2buf, k=5)
+        tp = graph_timed(torch, lambda: E._apply2(batch, coeff, cs, pv, pa, pb), l2buf, k=5)
+        rec["pair_stored"] = {"ms_pair_one_read": tp, "ms_two_products": t2,
+                              "gbs_pair": o_bytes / (tp / 1e3) / 1e9, "frac_one_read": o_bytes / (tp / 1e3) / 1e9 / peak,
+                              "api": "estimators.heff_qgt_matvec / irl_mvp2_f64 (k_stream DUAL)"}
+        del pv, pa, pb
     if with_irl:
         rec["irl_stored"] = irl_solve(torch, OPT, batch, cfg, en)
     if with_irl and cfg.index == 2:  # the GEVP form on the same batch
@@ -458,7 +476,8 @@ def config_record(torch, cfg, dev, peak, dmma_peak, l2buf, with_irl=True, extra=
                               "lambda_min": res.lambda_min, "converged": res.converged,
                               "residual": res.pair.residual, "tol": conf.gevp_tol, "shift": conf.gevp_shift,
                               "solver": ("LOBPCG on (H~, diag(1, S + eps I)), eps = shift * mean diag S; "
-                                         "one H and one S product per iteration")}
+                                         "one H and one S product per iteration, taken as a one-read pair "
+                                         "(irl_mvp2_f64)")}
     if extra is not None:
         extra(batch, params, inp, apply, coeff, rec)
     del batch, apply, coeff
