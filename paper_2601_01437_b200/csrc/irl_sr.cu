@@ -530,7 +530,7 @@ int make_wide_plan(int64_t n, int64_t ld_u, bool cplx, WidePlan& p) {
   p.K = std::min(WIDE_MAX_K, WIDE_TM_COLS_PER_WARP / (p.rpw * wide_tm_words(p.upl)));
   if (getenv("IRL_WIDE_K")) p.K = std::min(p.K, std::max(2, atoi(getenv("IRL_WIDE_K"))));
   const size_t stage = (size_t)p.RS * p.WM * 16;
-  const size_t per_slot = 2 * 8 + (size_t)p.RS * p.Q * sS + (size_t)p.RS * sS;  // dotdone, ydone, pd, ys
+  const size_t per_slot = 4 * 8 + (size_t)p.RS * p.Q * sS + (size_t)p.RS * sS;  // dotdone, ydone, parked, slotfree, pd, ys
   const size_t budget = (size_t)d.smem_optin - 2048;  // static smem of the kernel
   const size_t fixed = (size_t)p.K * per_slot;
   const size_t vbytes = (size_t)(p.WM + 1) * 16 + 16;

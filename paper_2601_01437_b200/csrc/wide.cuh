@@ -66,10 +66,23 @@
 
 namespace irl {
 
-constexpr int WIDE_CW = 8;  // consumer warps
+constexpr int WIDE_CW = 8;  // dot warps, and as many accumulate warps (warp w + WIDE_CW takes what warp w parked)
 constexpr int WIDE_AW = 3;  // aggregator warps
 constexpr int WIDE_RW = 3;  // reducer warps
-constexpr int WIDE_THREADS = (WIDE_CW + 2 + WIDE_AW + WIDE_RW) * 32;
+constexpr int WIDE_THREADS = (2 * WIDE_CW + 2 + WIDE_AW + WIDE_RW) * 32;
+// Registers: the CTA launches at WIDE_REGS_LAUNCH per thread; then the dot and
+// accumulate warpgroups grow and the other roles shrink (setmaxnreg, issued
+// inside each role's branch so that ptxas allocates per role).  The pool is
+// the launch allocation: asking for more than the others gave back never returns.
+constexpr int WIDE_REGS_LAUNCH = (65536 / WIDE_THREADS) / 8 * 8;
+constexpr int WIDE_REGS_DOT = 88;
+constexpr int WIDE_REGS_ACC = 104;
+constexpr int WIDE_REGS_AUX = 48;
+static_assert(WIDE_CW % 4 == 0 && (WIDE_THREADS / 32) % 4 == 0, "setmaxnreg works on whole warpgroups");
+static_assert(WIDE_CW * 32 * (WIDE_REGS_DOT + WIDE_REGS_ACC) + (WIDE_THREADS - 2 * WIDE_CW * 32) * WIDE_REGS_AUX <=
+                  WIDE_THREADS * WIDE_REGS_LAUNCH,
+              "setmaxnreg.inc can only take what the CTA's own warps gave back");
+#define WIDE_SET_REGS(op, n) asm volatile("setmaxnreg." op ".sync.aligned.u32 %0;" ::"n"(n))
 constexpr int WIDE_MAX_NS = 24;  // shared-memory stages
 constexpr int WIDE_MAX_K = 24;   // blocks parked in TMEM per consumer warp (pending exchange)
 constexpr int WIDE_NBUF = 64;    // exchange record ring (>= 2 K + 2)
@@ -242,7 +255,9 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1) k_wide(const WideArgs a) {
   uint64_t* empty = full + NS;                                           // [NS]
   uint64_t* dotdone = empty + NS;                                        // [K]
   uint64_t* ydone = dotdone + K;                                         // [K]
-  S* pd = reinterpret_cast<S*>(ydone + K);                               // [K][RS][Q] part dots
+  uint64_t* parked = ydone + K;                                          // [K] block b is in TMEM (dot warps -> accumulate warps)
+  uint64_t* slotfree = parked + K;                                       // [K] block b left TMEM (accumulate warps -> dot warps)
+  S* pd = reinterpret_cast<S*>(slotfree + K);                            // [K][RS][Q] part dots
   S* ys = pd + (size_t)K * RS * Q;                                       // [K][RS] y of the rows
   double2* vsl = reinterpret_cast<double2*>(a.vsl_off + smem_w);         // [WM + 1] v slice (+ a zero unit)
   __shared__ S shs[WIDE_CW];
@@ -262,7 +277,7 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1) k_wide(const WideArgs a) {
   const int NB = (int)((N + RS - 1) / RS);
   const S* coeff = reinterpret_cast<const S*>(a.coeff);
   const S* yadd = reinterpret_cast<const S*>(a.yadd);
-  constexpr int W_PROD = WIDE_CW, W_PUB = WIDE_CW + 1, W_AGG = WIDE_CW + 2, W_RED = WIDE_CW + 2 + WIDE_AW;
+  constexpr int W_ACC = WIDE_CW, W_PROD = 2 * WIDE_CW, W_PUB = W_PROD + 1, W_AGG = W_PROD + 2, W_RED = W_AGG + WIDE_AW;
   constexpr int NTC = WIDE_CW * 32;
 
   if (tid == 0) {
@@ -278,6 +293,8 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1) k_wide(const WideArgs a) {
     for (int j = 0; j < K; ++j) {
       mbar_init(&dotdone[j], WIDE_CW);
       mbar_init(&ydone[j], 1);
+      mbar_init(&parked[j], WIDE_CW);
+      mbar_init(&slotfree[j], WIDE_CW);
     }
     published = 0;
     fence_mbar_init();
@@ -328,6 +345,7 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1) k_wide(const WideArgs a) {
 
   // ------------------------------------------------------------ producer --
   if (warp == W_PROD) {
+    WIDE_SET_REGS("dec", WIDE_REGS_AUX);
     if (lane == 0) {
       const uint32_t slice_bytes = (uint32_t)W * 16u;
       for (int b = 0; b < NB; ++b) {
@@ -346,6 +364,7 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1) k_wide(const WideArgs a) {
 
   // ----------------------------------------------------------- publisher --
   if (warp == W_PUB) {
+    WIDE_SET_REGS("dec", WIDE_REGS_AUX);
     const S s_c = s_c_sh;
     for (int b = 0; b < NB; ++b) {
       const int j = b % K;
@@ -368,6 +387,7 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1) k_wide(const WideArgs a) {
   // row r of the matrix is aggregated by CTA r % G: one row's G partials per
   // visit, two per aggregator lane
   if (warp >= W_AGG && warp < W_RED) {
+    WIDE_SET_REGS("dec", WIDE_REGS_AUX);
     constexpr int AL = WIDE_AW * 32;            // aggregator lanes
     const int al = (warp - W_AGG) * 32 + lane;  // partials al, al + AL
     for (int64_t r = c; r < N; r += G) {
@@ -412,6 +432,7 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1) k_wide(const WideArgs a) {
 
   // ------------------------------------------------------------ reducers --
   if (warp >= W_RED) {
+    WIDE_SET_REGS("dec", WIDE_REGS_AUX);
     const int k = warp - W_RED;
     S ysum = T::zero();
     for (int b = k; b < NB; b += WIDE_RW) {
@@ -446,150 +467,164 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1) k_wide(const WideArgs a) {
       for (int i = 0; i < rows; ++i) ysum = T::add(ysum, T::shfl(y, i));  // row order (off the critical path)
     }
     if (lane == 0) shy[k] = ysum;
-    named_bar_sync(2, (WIDE_CW + WIDE_RW) * 32);  // epilogue: shy complete
+    named_bar_sync(2, (WIDE_CW + WIDE_RW) * 32);  // epilogue (accumulate warps): shy complete
     return;
   }
 
-  // ----------------------------------------------------------- consumers --
-  // warp w: part pq = w % Q of rows rg RPW .. rg RPW + RPW - 1 (rg = w / Q) of every block
-  const int rg = warp / Q;
-  const int pq = warp % Q;
+  // ------------------------------------------------- dot / accumulate warps --
+  // Dot warp w and accumulate warp w + WIDE_CW own the same place: part
+  // pq = w % Q of rows rg RPW .. rg RPW + RPW - 1 (rg = w / Q) of every block,
+  // and the same TMEM columns (warp % 4 is the TMEM lane quarter of both).
+  // A warp that did both steps of a block one after the other was the bound of
+  // the CTA (~0.65 + 0.45 us of dependent latencies per block whatever the
+  // rows per step); split, the block rate is that of the slower step.
+  const int wi = warp % WIDE_CW;
+  const int rg = wi / Q;
+  const int pq = wi % Q;
   const int u0p = pq * PU;
   const int u1p = min(W, u0p + PU);
-  // this warp's TMEM: lane quarter warp % 4, column half warp / 4, K slots of TMW words
-  const uint32_t tm = tmem_base_sh + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * WIDE_TM_COLS_PER_WARP);
-  double2 acc[UPL];
-  double2 vreg[UPL];  // this lane's units of the v slice (0 past the part)
+  static_assert(WIDE_CW % 4 == 0, "a warp's TMEM lane quarter is warp % 4");
+  // this place's TMEM: lane quarter wi % 4, column half wi / 4, K slots of TMW words
+  const uint32_t tm = tmem_base_sh + ((uint32_t)(32 * (wi & 3)) << 16) + (uint32_t)((wi >> 2) * WIDE_TM_COLS_PER_WARP);
   bool inpart[UPL];
 #pragma unroll
-  for (int k = 0; k < UPL; ++k) {
-    acc[k] = make_double2(0.0, 0.0);
-    inpart[k] = u0p + lane + 32 * k < u1p;
-    vreg[k] = inpart[k] ? vsl[u0p + lane + 32 * k] : make_double2(0.0, 0.0);
+  for (int k = 0; k < UPL; ++k) inpart[k] = u0p + lane + 32 * k < u1p;
+
+  if (warp < W_ACC) {
+    // ---- dot warps: stage -> registers -> partial dots (published at once) -> TMEM
+    WIDE_SET_REGS("inc", WIDE_REGS_DOT);
+    int sd = 0, pdp = 0, jd = 0, pk = 0;  // stage / parity, slot, parity of nd / K
+    for (int nd = 0; nd < NB; ++nd) {
+      const int s = sd, j = jd;
+      if (nd >= K) mbar_wait(&slotfree[j], pk ^ 1);  // block nd - K left this slot (window of K pending blocks)
+      if (wi == 0 && lane == 0) WIDE_STAMP(nd, 6);
+      mbar_wait(&full[s], pdp);
+      const int64_t r0 = (int64_t)nd * RS + rg * RPW;
+      const int nlive = (int)min((int64_t)RPW, N - r0);
+      double t[NV];
+      // row by row: shared memory -> registers -> dot -> TMEM (the TMEM
+      // stores are asynchronous, so the next row's loads overlap them)
+#pragma unroll
+      for (int r = 0; r < RPW; ++r) {
+        const int4* row = reinterpret_cast<const int4*>(ring + ((size_t)s * RS + rg * RPW + r) * WM + u0p + lane);
+        const bool live = r < nlive;
+        int4 x[UPL];  // the unit's four words as loaded: parked as they are
+#pragma unroll
+        for (int k = 0; k < UPL; ++k) x[k] = (live && inpart[k]) ? row[32 * k] : make_int4(0, 0, 0, 0);
+        S t0 = T::zero(), t1 = T::zero();
+#pragma unroll
+        for (int k = 0; k < UPL; ++k)  // x = 0 past the part, so any finite v will do there
+          T::dot_acc((k & 1) ? t1 : t0, unit_of(x[k]), vsl[min(u0p + lane + 32 * k, WM)]);
+        const S tr = T::add(t0, t1);
+        if constexpr (CPLX) {
+          t[2 * r] = tr.x;
+          t[2 * r + 1] = tr.y;
+        } else {
+          t[r] = tr;
+        }
+        if (live) tm_park<UPL>(tm + (uint32_t)(j * TMW + r * wide_tm_words(UPL)), x);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);  // the stage is in registers / TMEM: refill it
+      warp_sum_split<NV>(t, lane);            // lane l: the total of value l / (32 / NV)
+      if ((lane & (32 / NV - 1)) == 0)
+        reinterpret_cast<double*>(pd)[((j * RS + rg * RPW) * Q) * SC + ((lane / (32 / NV)) / SC * Q + pq) * SC +
+                                      (lane / (32 / NV)) % SC] = t[0];
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&dotdone[j]);
+        if (wi == 0) WIDE_STAMP(nd, 1);
+      }
+      // the park has landed: hand the slot to the accumulate warps
+      tm_wait_st();
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&parked[j]);
+      if (++sd == NS) {
+        sd = 0;
+        pdp ^= 1;
+      }
+      if (++jd == K) {
+        jd = 0;
+        pk ^= 1;
+      }
+    }
+    // TMEM is no longer needed once the accumulate warps are done: warp 0 frees it
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    named_bar_sync(4, 2 * NTC);
+    if (warp == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base_sh), "n"(WIDE_TMEM_COLS)
+                   : "memory");
+    }
+    return;
   }
-  int nd = 0, na = 0;
-  int elig = -1;  // debug trace only
-  // ring positions kept incrementally (no integer division in the polling loop):
-  // nd -> stage sd / parity pdp and slot jd; na -> slot ja / parity pap
-  int sd = 0, pdp = 0, jd = 0, ja = 0, pap = 0;
-  // every lane probes (non-blocking test_wait: a suspending try_wait on a
-  // barrier that is not ready would delay the other one); a barrier counts as
-  // passed only when all lanes saw it complete, each lane then holding its
-  // own acquire of the mbarrier phase
-  auto ready = [&](uint64_t* bar, int ph) { return __all_sync(0xffffffffu, mbar_test_wait(smem_addr(bar), ph)); };
-  while (na < NB) {
-    if (na < nd) {  // accumulate the oldest parked block once its y is there
+
+  // ---- accumulate warps: y and the parked block -> registers -> acc += conj(O) y
+  WIDE_SET_REGS("inc", WIDE_REGS_ACC);
+  double2 acc[UPL];
+#pragma unroll
+  for (int k = 0; k < UPL; ++k) acc[k] = make_double2(0.0, 0.0);
+  {
+    int ja = 0, pap = 0;
+    for (int na = 0; na < NB; ++na) {
       const int j = ja;
-      if (ready(&ydone[j], pap)) {
-        const int64_t r0 = (int64_t)na * RS + rg * RPW;
-        const int nlive = (int)min((int64_t)RPW, N - r0);  // rows of this warp that exist (<= 0: none)
-        if (nlive > 0) {
-          tm_wait_st();  // the park of this slot has landed
-          // RB rows per TMEM round trip: all their loads in flight, one wait
+      mbar_wait(&ydone[j], pap);
+      mbar_wait(&parked[j], pap);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int64_t r0 = (int64_t)na * RS + rg * RPW;
+      const int nlive = (int)min((int64_t)RPW, N - r0);  // rows of this warp that exist (<= 0: none)
+      // RB rows per TMEM round trip: all their loads in flight, one wait
 #pragma unroll
-          for (int rb = 0; rb < RPW; rb += RB) {
-            int4 w[RB][UPL];
+      for (int rb = 0; rb < RPW; rb += RB) {
+        int4 w[RB][UPL];
+        if (rb < nlive) {
 #pragma unroll
-            for (int r = 0; r < RB; ++r)
+          for (int r = 0; r < RB; ++r)
 #pragma unroll
-              for (int k = 0; k < UPL; ++k)
-                tm_ld4(tm + (uint32_t)(j * TMW + (rb + r) * wide_tm_words(UPL) + 4 * k), w[r][k]);
-            tm_wait_ld();
+            for (int k = 0; k < UPL; ++k)
+              tm_ld4(tm + (uint32_t)(j * TMW + (rb + r) * wide_tm_words(UPL) + 4 * k), w[r][k]);
+          tm_wait_ld();
+        }
+        if (rb + RB >= RPW) {  // the slot's last rows are in registers: the dot warps may park block na + K
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&slotfree[j]);
+        }
+        if (rb < nlive) {
 #pragma unroll
-            for (int r = 0; r < RB; ++r) {
-              if (rb + r < nlive) {
-                const S y = ys[j * RS + rg * RPW + rb + r];
+          for (int r = 0; r < RB; ++r) {
+            if (rb + r < nlive) {
+              const S y = ys[j * RS + rg * RPW + rb + r];
 #pragma unroll
-                for (int k = 0; k < UPL; ++k) T::axpy(acc[k], unit_of(w[r][k]), y);  // x = 0 past the part
-              }
+              for (int k = 0; k < UPL; ++k) T::axpy(acc[k], unit_of(w[r][k]), y);  // x = 0 past the part
             }
           }
         }
-        if (lane == 0 && warp == 0) WIDE_STAMP(na, 5);
-        ++na;
-        if (++ja == K) {
-          ja = 0;
-          pap ^= 1;
-        }
-        continue;
+      }
+      if (lane == 0 && wi == 0) WIDE_STAMP(na, 5);
+      if (++ja == K) {
+        ja = 0;
+        pap ^= 1;
       }
     }
-    if (nd < NB && nd - na < K) {  // dot of the next block once it has landed, then park it
-      const int s = sd;
-      if (a.trace && warp == 0 && lane == 0 && elig != nd) {  // debug: when block nd became eligible
-        elig = nd;
-        WIDE_STAMP(nd, 6);
-      }
-      if (ready(&full[s], pdp)) {
-        const int j = jd;
-        const int64_t r0 = (int64_t)nd * RS + rg * RPW;
-        const int nlive = (int)min((int64_t)RPW, N - r0);
-        double t[NV];
-        // row by row: shared memory -> registers -> dot -> TMEM (the TMEM
-        // stores are asynchronous, so the next row's loads overlap them)
-#pragma unroll
-        for (int r = 0; r < RPW; ++r) {
-          const int4* row = reinterpret_cast<const int4*>(ring + ((size_t)s * RS + rg * RPW + r) * WM + u0p + lane);
-          const bool live = r < nlive;
-          int4 x[UPL];  // the unit's four words as loaded: parked as they are
-#pragma unroll
-          for (int k = 0; k < UPL; ++k) x[k] = (live && inpart[k]) ? row[32 * k] : make_int4(0, 0, 0, 0);
-          S t0 = T::zero(), t1 = T::zero();
-#pragma unroll
-          for (int k = 0; k < UPL; ++k) T::dot_acc((k & 1) ? t1 : t0, unit_of(x[k]), vreg[k]);
-          const S tr = T::add(t0, t1);
-          if constexpr (CPLX) {
-            t[2 * r] = tr.x;
-            t[2 * r + 1] = tr.y;
-          } else {
-            t[r] = tr;
-          }
-          if (live) tm_park<UPL>(tm + (uint32_t)(j * TMW + r * wide_tm_words(UPL)), x);
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);  // the stage is in registers / TMEM: refill it
-        warp_sum_split<NV>(t, lane);            // lane l: the total of value l / (32 / NV)
-        if ((lane & (32 / NV - 1)) == 0)
-          reinterpret_cast<double*>(pd)[((j * RS + rg * RPW) * Q) * SC + ((lane / (32 / NV)) / SC * Q + pq) * SC +
-                                        (lane / (32 / NV)) % SC] = t[0];
-        __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&dotdone[j]);
-          if (warp == 0) WIDE_STAMP(nd, 1);
-        }
-        ++nd;
-        if (++sd == NS) {
-          sd = 0;
-          pdp ^= 1;
-        }
-        if (++jd == K) jd = 0;
-        continue;
-      }
-    }
-    if (a.spin_ns) __nanosleep(a.spin_ns);  // nothing ready: back off
   }
-
-  // TMEM is no longer needed: warp 0 frees it once every consumer warp is done
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  named_bar_sync(1, NTC);
-  if (warp == 0) {
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base_sh), "n"(WIDE_TMEM_COLS)
-                 : "memory");
-  }
+  named_bar_sync(4, 2 * NTC);  // with the dot warps: TMEM may go
 
   // the part accumulators of the RS warps sharing a part meet in shared memory
   // (the ring is free: every stage consumed), in row order
   named_bar_sync(2, (WIDE_CW + WIDE_RW) * 32);
   double2* red = ring;  // [CW][32 * UPL] (ring_bytes covers it)
   const int pitch = 32 * UPL;
+  const int ta = tid - W_ACC * 32;  // thread index among the accumulate warps
 #pragma unroll
-  for (int k = 0; k < UPL; ++k) red[(size_t)warp * pitch + lane + 32 * k] = acc[k];
+  for (int k = 0; k < UPL; ++k) red[(size_t)wi * pitch + lane + 32 * k] = acc[k];
   S Y = T::zero();  // sum over all rows of y, the same fixed order in every CTA
   for (int k = 0; k < WIDE_RW; ++k) Y = T::add(Y, shy[k]);
-  named_bar_sync(1, NTC);
+  named_bar_sync(5, NTC);
   const double uu = (a.hf_re && a.u0) ? *a.u0 : 0.0;
-  for (int u = tid; u < W; u += NTC) {
+  for (int u = ta; u < W; u += NTC) {
     const int q = u / PU, j = u - q * PU;
     double2 o = red[(size_t)q * pitch + j];
     for (int i = 1; i < WIDE_CW / Q; ++i) {  // the row groups sharing part q, in order
@@ -615,7 +650,7 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1) k_wide(const WideArgs a) {
       if (a.out_im) a.out_im[gu] = o.y;
     }
   }
-  if (a.out0 && c == 0 && warp == 0) {  // (F/2) . u over the slices, fixed order
+  if (a.out0 && c == 0 && wi == 0) {  // (F/2) . u over the slices, fixed order
     double g = 0.0;
     if (a.hf_re) {
       for (int q0 = 0; q0 < G; q0 += 32) {
