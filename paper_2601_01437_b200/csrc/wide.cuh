@@ -38,27 +38,30 @@
 //              and accumulates with it.
 //
 // Warp roles (one CTA, WIDE_THREADS threads):
-//   consumers (WIDE_CW warps)  warp w owns rows (w / Q) RPW ... + RPW - 1 of a
+//   dot warps (WIDE_CW)        warp w owns rows (w / Q) RPW ... + RPW - 1 of a
 //       stage, part w % Q of the slice (RS = RPW WIDE_CW / Q rows per block;
-//       several rows per warp-step hide the step's latencies).  D(b): part -> registers,
-//       arrive empty (the stage refills at once), partial dot -> smem, arrive
-//       dotdone, park the part in TMEM slot b % K.  A(b): part back from TMEM,
-//       y from smem, acc += conj(O) y.  Each warp runs A(b) as soon as block
-//       b's y is there and D(b') as soon as block b' landed and a slot is free
-//       (non-blocking mbarrier probes), so the lag between the two adapts to
-//       the grid's exchange latency.
+//       several rows per warp-step hide the step's latencies).  D(b): wait for
+//       slot b % K to be free and for the stage; part -> registers -> partial
+//       dots -> smem, arrive dotdone (published at once); part -> TMEM slot,
+//       arrive empty (the stage refills); wait::st, arrive parked.
+//   accumulate warps (WIDE_CW) warp w + WIDE_CW shares warp w's place and TMEM
+//       columns (same warp % 4 = TMEM lane quarter).  A(b): wait ydone and
+//       parked, part back from TMEM, arrive slotfree, acc += conj(O) y.
+//       A single warp doing D(b) and A(b - K) in turn was the bound of the CTA
+//       (their dependent latencies add up per block); split, every wait is a
+//       blocking mbarrier wait on the one thing the warp needs next.
 //   producer (1 warp)          lane 0 streams block after block into the ring.
 //   publisher (1 warp)         sums the Q part dots of each row, writes part.
 //   aggregators (WIDE_AW warps) the rows this CTA aggregates.
 //   reducers (WIDE_RW warps)   block b (b = k mod RW): fin -> y -> smem,
 //       arrive ydone; several warps keep several blocks' polls in flight.
 //
-// Slot reuse: a consumer warp parks at most K blocks, so CTA X publishes block
-// b only after its consumers ran A(b - K), i.e. after fin of b - K existed,
-// i.e. after every CTA published b - K; a CTA publishes b - K only after its
-// consumers ran A(b - 2 K), i.e. after its reducers finished every block
-// <= b - 2 K.  With NBUF >= 2 K + 2 no record is overwritten while some CTA
-// may still read it; tags are unique within a launch.
+// Slot reuse: a slot holds one pending block, so CTA X publishes block b only
+// after its accumulate warps fetched b - K, i.e. after fin of b - K existed,
+// i.e. after every CTA published b - K; a CTA publishes b - K only after it
+// fetched b - 2 K, i.e. after its reducers finished every block <= b - 2 K.
+// With NBUF >= 2 K + 2 no record is overwritten while some CTA may still read
+// it; tags are unique within a launch.
 //
 // Replaces est:184-186 (centring copy + the two GEMVs) for stored O.
 #pragma once
