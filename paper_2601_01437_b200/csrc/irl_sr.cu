@@ -464,22 +464,29 @@ int launch_rows(const Plan& p, bool cplx, const StreamArgs& a, cudaStream_t st) 
 constexpr int64_t kWideMinUnits = 16384;
 
 struct WidePlan {
-  int G, WM, RS, Q, PU, NS, K, upl, rpw;
-  size_t smem, ws, part_bytes, fin_bytes, fin_copy_bytes, ring_bytes, vsl_off;
+  int G, WM, RS, Q, PU, NS, K, upl, rpw, ut, pr;
+  size_t smem, ws, part_bytes, fin_bytes, fin_copy_bytes, ring_bytes, vsl_off, side_off;
 };
 
 using WideFn = void (*)(WideArgs);
 // instances: units per lane x rows per warp-step <= 16 (register budget)
 constexpr bool wide_inst(int upl, int rpw) { return upl * rpw <= 16; }
 template <bool CPLX>
-WideFn pick_wide_c(int upl, int rpw) {
-#define WIDE_CASE(U, R) if (upl == U && rpw == R) return k_wide<CPLX, U, R>;
+WideFn pick_wide_c(int upl, int rpw, bool side) {
+#define WIDE_CASE(U, R) if (upl == U && rpw == R && !side) return k_wide<CPLX, U, R>;
   WIDE_CASE(2, 1) WIDE_CASE(2, 2) WIDE_CASE(2, 4) WIDE_CASE(4, 1) WIDE_CASE(4, 2) WIDE_CASE(4, 4)
   WIDE_CASE(6, 1) WIDE_CASE(6, 2) WIDE_CASE(8, 1) WIDE_CASE(8, 2)
 #undef WIDE_CASE
+#define WIDE_CASE(U, R) if (upl == U && rpw == R && side) return k_wide<CPLX, U, R, true>;
+  WIDE_CASE(4, 1) WIDE_CASE(4, 2) WIDE_CASE(4, 4) WIDE_CASE(6, 1) WIDE_CASE(6, 2)
+#undef WIDE_CASE
   return nullptr;
 }
-WideFn pick_wide(bool cplx, int upl, int rpw) { return cplx ? pick_wide_c<true>(upl, rpw) : pick_wide_c<false>(upl, rpw); }
+// side-buffer instances exist for 4 and 6 units per lane
+constexpr bool wide_side_inst(int upl) { return upl == 4 || upl == 6; }
+WideFn pick_wide(bool cplx, int upl, int rpw, bool side) {
+  return cplx ? pick_wide_c<true>(upl, rpw, side) : pick_wide_c<false>(upl, rpw, side);
+}
 
 int wide_upl(int need) { return need <= 2 ? 2 : need <= 4 ? 4 : need <= 6 ? 6 : need <= 8 ? 8 : 0; }
 
@@ -513,34 +520,51 @@ int make_wide_plan(int64_t n, int64_t ld_u, bool cplx, WidePlan& p) {
   // rows per warp-step: each consumer step has fixed latencies (barrier probes,
   // butterfly, TMEM round trip), so a step should move ~5 KB or more
   const int part_bytes_row = (int)cdiv(p.WM, p.Q) * 16;
+  p.PU = (int)cdiv(p.WM, p.Q);
+  // TMEM takes a lane's full lane-rows of a part (units lane + 32 k, k < ut);
+  // a partly filled last lane-row (pr units) waits in a shared-memory side
+  // buffer instead, so no TMEM columns are spent on empty lanes: the TMEM slots
+  // set the number of pending blocks, which bounds the product (cfg4: 100 units
+  // a part = 3 lane-rows + 4 units, 5 slots instead of 4; cfg5: 5 + 17 units, 6
+  // instead of 5)
+  p.ut = p.upl;
+  p.pr = 0;
+  {
+    const int ut = p.PU / 32, pr = p.PU - 32 * ut;
+    if (!getenv("IRL_WIDE_NOSIDE") && ut == p.upl - 1 && wide_side_inst(p.upl) && pr > 0 && pr <= 24) {
+      p.ut = ut;
+      p.pr = pr;
+    }
+  }
   p.rpw = 1;
   while (p.rpw < 4 && part_bytes_row * p.rpw < 4096 && wide_inst(p.upl, 2 * p.rpw) &&
-         2 * p.rpw * WIDE_CW / p.Q <= WIDE_MAX_RS && 2 * p.rpw * wide_tm_words(p.upl) * 2 <= WIDE_TM_COLS_PER_WARP)
+         2 * p.rpw * WIDE_CW / p.Q <= WIDE_MAX_RS && 2 * p.rpw * 4 * p.ut * 2 <= WIDE_TM_COLS_PER_WARP)
     p.rpw *= 2;
   if (getenv("IRL_WIDE_RPW")) {
     const int r = atoi(getenv("IRL_WIDE_RPW"));
     if ((r == 1 || r == 2 || r == 4) && wide_inst(p.upl, r) && r * WIDE_CW / p.Q <= WIDE_MAX_RS &&
-        r * wide_tm_words(p.upl) * 2 <= WIDE_TM_COLS_PER_WARP)
+        r * 4 * p.ut * 2 <= WIDE_TM_COLS_PER_WARP)
       p.rpw = r;
   }
   p.RS = p.rpw * WIDE_CW / p.Q;
-  p.PU = (int)cdiv(p.WM, p.Q);
   const size_t sS = cplx ? 16 : 8;
-  // TMEM slots per consumer warp: its half of the 512 columns over 4 UPL words a block
-  p.K = std::min(WIDE_MAX_K, WIDE_TM_COLS_PER_WARP / (p.rpw * wide_tm_words(p.upl)));
+  // TMEM slots per dot / accumulate warp pair: its half of the 512 columns over 4 ut words a row
+  p.K = std::min(WIDE_MAX_K, WIDE_TM_COLS_PER_WARP / (p.rpw * 4 * p.ut));
   if (getenv("IRL_WIDE_K")) p.K = std::min(p.K, std::max(2, atoi(getenv("IRL_WIDE_K"))));
   const size_t stage = (size_t)p.RS * p.WM * 16;
   const size_t per_slot = 4 * 8 + (size_t)p.RS * p.Q * sS + (size_t)p.RS * sS;  // dotdone, ydone, parked, slotfree, pd, ys
   const size_t budget = (size_t)d.smem_optin - 2048;  // static smem of the kernel
+  const size_t side_bytes = (size_t)p.K * p.RS * p.Q * p.pr * 16;
   const size_t fixed = (size_t)p.K * per_slot;
-  const size_t vbytes = (size_t)(p.WM + 1) * 16 + 16;
+  const size_t vbytes = (size_t)(p.WM + 1) * 16 + 32 + side_bytes;
   p.NS = (int)std::min<size_t>(WIDE_MAX_NS, (budget - fixed - vbytes) / (stage + 16));
   if (getenv("IRL_WIDE_NS")) p.NS = std::min(p.NS, std::max(2, atoi(getenv("IRL_WIDE_NS"))));
   if (p.NS < 2) return fail(IRL_ERR_DEVICE, "wide path: row slices too wide for the ring");
   p.ring_bytes = std::max((size_t)p.NS * stage, (size_t)WIDE_CW * 32 * p.upl * 16);  // ring / epilogue scratch
   p.vsl_off = p.ring_bytes + (size_t)p.NS * 16 + fixed;
   p.vsl_off = (p.vsl_off + 15) / 16 * 16;
-  p.smem = p.vsl_off + (size_t)(p.WM + 1) * 16;
+  p.side_off = (p.vsl_off + (size_t)(p.WM + 1) * 16 + 15) / 16 * 16;
+  p.smem = p.side_off + side_bytes;
   if (p.smem > budget) return fail(IRL_ERR_DEVICE, "wide path: shared memory");
   const size_t rec = cplx ? 32 : 16;  // LL record bytes per scalar
   p.part_bytes = align256((size_t)WIDE_NBUF * p.RS * p.G * rec);
@@ -568,7 +592,7 @@ unsigned long long* wide_trace_buffer(int G) {
 }
 
 int launch_wide(const WidePlan& p, bool cplx, WideArgs a, void* ws, cudaStream_t st) {
-  WideFn fn = pick_wide(cplx, p.upl, p.rpw);
+  WideFn fn = pick_wide(cplx, p.upl, p.rpw, p.pr > 0);
   if (!fn) return fail(IRL_ERR_DEVICE, "no wide instance for %d units per lane, %d rows per warp", p.upl, p.rpw);
   DevInfo d;
   IRL_TRY(dev_info(d));
@@ -588,6 +612,9 @@ int launch_wide(const WidePlan& p, bool cplx, WideArgs a, void* ws, cudaStream_t
   a.WM = p.WM;
   a.ring_bytes = p.ring_bytes;
   a.vsl_off = p.vsl_off;
+  a.UT = p.ut;
+  a.PR = p.pr;
+  a.side_off = p.side_off;
   a.trace = wide_trace_buffer(p.G);
   a.trace_stride = getenv("IRL_WIDE_TRACE") ? std::max(1, atoi(getenv("IRL_WIDE_TRACE"))) : 1;
   a.poll_ns = getenv("IRL_WIDE_POLL_NS") ? atoi(getenv("IRL_WIDE_POLL_NS")) : 160;

@@ -123,7 +123,11 @@ struct WideArgs {
   int Q;             // parts per row slice
   int PU;            // units per part (ceil(WM / Q))
   int NS;            // ring stages
-  int K;             // TMEM slots per consumer warp (blocks in flight between dot and accumulate)
+  int K;             // TMEM slots per dot / accumulate warp pair (blocks in flight between dot and accumulate)
+  int UT;            // a lane's first UT units of a row part go to TMEM ...
+  int PR;            // ... and the PR units of the partly filled last lane-row (units 32 UT ..) to a side buffer in
+  size_t side_off;   // shared memory [K][RS][Q][PR]: TMEM columns are not spent on empty lanes (cfg4: 100 units a
+                     // part = 3 full lane-rows + 4 units; K = 5 instead of 4)
   int WM;            // max slice width (units): ring row pitch
   size_t ring_bytes;  // ring + epilogue scratch (>= both)
   size_t vsl_off;     // shared-memory offset of the v slice
@@ -242,12 +246,16 @@ __device__ __forceinline__ void warp_sum_split(double (&v)[NV], int lane) {
   }
 }
 
-template <bool CPLX, int UPL, int RPW>
+// SIDE: the last lane-row of a part (k = UPL - 1) is only partly filled and
+// waits in the shared-memory side buffer; TMEM takes the UT = UPL - 1 full ones.
+template <bool CPLX, int UPL, int RPW, bool SIDE = false>
 __global__ void __launch_bounds__(WIDE_THREADS, 1) k_wide(const WideArgs a) {
   using T = Traits<CPLX>;
   using S = typename T::S;
   constexpr int SW = CPLX ? 2 : 1;  // LL records per scalar
-  constexpr int TMW = RPW * wide_tm_words(UPL);  // TMEM words a lane parks per block
+  constexpr int UT = SIDE ? UPL - 1 : UPL;
+  const int PR = a.PR;
+  constexpr int TMW = RPW * 4 * UT;  // TMEM words a lane parks per block
   constexpr int SC = CPLX ? 2 : 1;               // doubles per scalar
   constexpr int NV = RPW * SC;                   // doubles a lane reduces per warp-step
   constexpr int RB = UPL >= 8 ? 1 : (RPW * UPL <= 16 ? RPW : (RPW >= 2 && (RPW / 2) * UPL <= 16 ? RPW / 2 : 1));  // rows per TMEM fetch
@@ -263,6 +271,7 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1) k_wide(const WideArgs a) {
   S* pd = reinterpret_cast<S*>(slotfree + K);                            // [K][RS][Q] part dots
   S* ys = pd + (size_t)K * RS * Q;                                       // [K][RS] y of the rows
   double2* vsl = reinterpret_cast<double2*>(a.vsl_off + smem_w);         // [WM + 1] v slice (+ a zero unit)
+  double2* side = reinterpret_cast<double2*>(a.side_off + smem_w);       // [K][RS][Q][PR] last lane-rows of pending blocks
   __shared__ S shs[WIDE_CW];
   __shared__ double shg[WIDE_CW];
   __shared__ S shy[WIDE_RW];
@@ -525,7 +534,17 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1) k_wide(const WideArgs a) {
         } else {
           t[r] = tr;
         }
-        if (live) tm_park<UPL>(tm + (uint32_t)(j * TMW + r * wide_tm_words(UPL)), x);
+        if (live) {
+          const uint32_t tr0 = tm + (uint32_t)(j * TMW + r * 4 * UT);
+#pragma unroll
+          for (int k = 0; k < UPL; ++k) {
+            if (k < UT) {
+              tm_st4(tr0 + 4 * k, x[k]);
+            } else if (SIDE && k == UT && lane < PR) {
+              reinterpret_cast<int4*>(side)[((size_t)(j * RS + rg * RPW + r) * Q + pq) * PR + lane] = x[k];
+            }
+          }
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);  // the stage is in registers / TMEM: refill it
@@ -585,8 +604,16 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1) k_wide(const WideArgs a) {
 #pragma unroll
           for (int r = 0; r < RB; ++r)
 #pragma unroll
-            for (int k = 0; k < UPL; ++k)
-              tm_ld4(tm + (uint32_t)(j * TMW + (rb + r) * wide_tm_words(UPL) + 4 * k), w[r][k]);
+            for (int k = 0; k < UPL; ++k) {
+              if (k < UT) {
+                tm_ld4(tm + (uint32_t)(j * TMW + (rb + r) * 4 * UT + 4 * k), w[r][k]);
+              } else {
+                w[r][k] = (SIDE && k == UT && lane < PR)
+                              ? reinterpret_cast<const int4*>(
+                                    side)[((size_t)(j * RS + rg * RPW + rb + r) * Q + pq) * PR + lane]
+                              : make_int4(0, 0, 0, 0);
+              }
+            }
           tm_wait_ld();
         }
         if (rb + RB >= RPW) {  // the slot's last rows are in registers: the dot warps may park block na + K
