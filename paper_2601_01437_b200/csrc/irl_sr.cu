@@ -622,7 +622,6 @@ int launch_wide(const WidePlan& p, bool cplx, WideArgs a, void* ws, cudaStream_t
   // within about that time, and the earlier polls only added L2 traffic (cfg4 12.6 -> 12.25 ms, cfg5 18.6 -> 18.2)
   a.agg_delay_ns = getenv("IRL_WIDE_ADELAY") ? atoi(getenv("IRL_WIDE_ADELAY")) : 500;
   a.rot = getenv("IRL_WIDE_ROT") ? atoi(getenv("IRL_WIDE_ROT")) % p.G : 0;
-  a.spin_ns = getenv("IRL_WIDE_SPIN_NS") ? atoi(getenv("IRL_WIDE_SPIN_NS")) : 32;
   a.red_delay_ns = getenv("IRL_WIDE_RDELAY") ? atoi(getenv("IRL_WIDE_RDELAY")) : 0;
   // tags are block numbers: zeroed records can never match a stale one
   IRL_TRY(cuda_check(cudaMemsetAsync(base, 0, p.ws, st), "wide record reset"));

@@ -135,7 +135,6 @@ struct WideArgs {
   int trace_stride;           // every trace_stride-th block is stamped
   int poll_ns;                // reducer / aggregator poll back-off (ns)
   int rot;                    // debug: CTA c takes column slice (c + rot) % G
-  int spin_ns;                // consumer back-off when no stage is ready (0 = spin)
   int red_delay_ns;           // reducers: pause between this CTA's own publish and the first poll of the totals
   int agg_delay_ns;           // aggregators: the same before the first poll of a row's partials
 };
