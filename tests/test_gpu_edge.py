@@ -521,3 +521,37 @@ def test_rows_path_o_at_end_of_allocation(E, p):
     finally:
         torch.cuda.synchronize()
         rt.cudaFree(base)
+
+
+@pytest.mark.parametrize("units,n,cplx", [
+    (148 * 97, 211, False),    # 97 units per SM slice: 3 full lane-rows + 1 unit in the side buffer
+    (148 * 120, 130, False),   # + 24 units: the widest side buffer
+    (148 * 125, 130, False),   # + 29 units: all four lane-rows in TMEM (no side buffer)
+    (148 * 97 + 5, 77, True),  # complex rows, uneven slices
+    (148 * 177 - 3, 70, False),  # 6 lane-rows per lane (cfg5's instance), rows not a multiple of the block
+])
+def test_wide_path_lane_row_split(E, units, n, cplx):
+    """The wide product parks a part's full lane-rows (32 units) in tensor
+    memory and its partly filled last lane-row in a shared-memory side buffer
+    (csrc/wide.cuh, SIDE instances): products over slice widths on both sides
+    of the split match the oracle's est:171-186 restatement and the two-pass
+    path, and repeat bit for bit."""
+    import torch
+
+    from paper_2601_01437_b200 import _lib
+
+    rng = np.random.default_rng(units + n)
+    p = units if cplx else 2 * units - 1
+    o, e, w = random_batch(rng, n, p, cplx=cplx, exact=True)
+    b = E.SampleBatch(None, w, e, o, 0, kind="hermitian" if cplx else None)
+    en = E.estimate_energy(b)
+    mean, _, _ = oest.energy(w, e, 0)
+    assert _lib.mvp_plan(b.n_rows, b.ld, b.is_complex, 4)["path"] == "wide"
+    v = rng.standard_normal(p) + (1j * rng.standard_normal(p) if cplx else 0)
+    ref = oest.heff_hermitian(w, e, o, mean, v) if cplx else oest.heff(w, e, o, mean, v)
+    vt = torch.as_tensor(v, device="cuda")
+    first = E.heff_matvec(b, en, vt, mode=4)
+    assert rel(first.cpu().numpy(), ref) < 1e-10
+    assert rel(first.cpu().numpy(), E.heff_matvec(b, en, vt, mode=2).cpu().numpy()) < 1e-12
+    for _ in range(5):
+        assert torch.equal(E.heff_matvec(b, en, vt, mode=4), first)
