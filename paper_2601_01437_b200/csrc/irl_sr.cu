@@ -771,7 +771,8 @@ bool mvp2_fused(int64_t n, int64_t ld_u, bool cplx, Plan& pl) {
   if (ld_u >= kWideMinUnits && make_wide_plan(n, ld_u, cplx, wp) == IRL_OK) return false;
   // single-CTA rows only: the 2-CTA cluster plans (cfg3) run their 4-unit instances at 80 registers, where the
   // second accumulator spills and the pair measured slower than two products (4.38 against 4.23 ms)
-  const bool ok = make_plan(n, ld_u, cplx, MODE_FUSED, pl) == IRL_OK && pl.C == 1 && pl.fn_dual;
+  // (one ring stage is given to the v slice, so the plan needs four)
+  const bool ok = make_plan(n, ld_u, cplx, MODE_FUSED, pl) == IRL_OK && pl.C == 1 && pl.fn_dual && pl.NS >= 4;
   g_err.clear();
   return ok;
 }
@@ -828,7 +829,12 @@ int mvp2_impl(bool cplx, const double* O, int64_t n, int64_t p, int64_t ld, cons
   a.ysum1 = extra + part_b;
   a.spart = w.spart;
   a.gpart = w.gpart;
-  IRL_TRY(launch_stream(pl, a, st));
+  // the second accumulator takes the registers of the v slice: v goes to the
+  // shared memory of the last ring stage, the ring runs on one stage less
+  Plan pd = pl;
+  pd.NS = pl.NS - 1;
+  a.vs_off = (pl.smem - (size_t)pl.R * pl.W * 16) & ~size_t(15);
+  IRL_TRY(launch_stream(pd, a, st));
   if (cplx) {
     IRL_TRY(launch_finish_mvp<true>(a.part0, pl.nb, ld_u, a.ysum, a.obar, hf_re, hf_im, u0, outa_re, outa_im, w.gpart, 1,
                                     out0, st));

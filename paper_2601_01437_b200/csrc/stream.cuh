@@ -57,6 +57,7 @@ struct StreamArgs {
   double2* part1;  // [nb][ld_u]   (STATS)
   void* ysum;      // S[nb]
   void* ysum1;     // S[nb]         (FUSED DUAL: the second product's sum of y)
+  size_t vs_off;   // FUSED DUAL: shared-memory offset of the v slice (the second accumulator takes v's registers)
   void* tpart;     // S[C][n_rows]  (DOT -> ACC)
   void* spart;     // S[C]          (DOT -> ACC; FUSED writes [0])
   double* gpart;   // double[C]     (DOT; FUSED writes [0])
@@ -203,6 +204,12 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
         }
       }
     }
+    if constexpr (DUAL) {  // each thread reads back only what it wrote: no barrier needed
+      double2* vsm = reinterpret_cast<double2*>(smem + a.vs_off);
+#pragma unroll
+      for (int k = 0; k < PPT; ++k)
+        if (k < kval) vsm[tid + k * NT] = vreg[k];
+    }
     sp = warp_sum<CPLX>(sp);
     gp = warp_sum<false>(gp);
     S* scr = red;  // red[0][0][*] is free before the main loop
@@ -270,9 +277,11 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
     for (int k = 0; k < PPT; ++k) {
       if (k < kval) {
         const int idx = tid + k * NT;
+        double2 vk;
+        if constexpr (DUAL) vk = reinterpret_cast<const double2*>(smem + a.vs_off)[idx]; else vk = vreg[k];
 #pragma unroll
         for (int r = 0; r < R; ++r)
-          if (r < rows) T::dot_acc(dp[r], st[(size_t)r * WM + idx], vreg[k]);
+          if (r < rows) T::dot_acc(dp[r], st[(size_t)r * WM + idx], vk);
       }
     }
 #pragma unroll
@@ -345,12 +354,27 @@ __global__ void __launch_bounds__(stream_max_nt(PPT) + 32, 1) k_stream(const Str
         if constexpr (DUAL) y1 = T::shfl(yv1, r);
         if (MODE != MODE_STATS && tid == 0) ys = T::add(ys, y);
         if (DUAL && tid == 0) ys1 = T::add(ys1, y1);
+        if constexpr (DUAL) {
+          // all the row's units in flight before the two axpys (the per-unit
+          // branches of the loop below serialise the shared-memory loads here);
+          // units past the slice add 0 to accumulators that are never stored
+          double2 u[PPT];
 #pragma unroll
-        for (int k = 0; k < PPT; ++k) {
-          if (k < kval) {
-            const double2 u = st[(size_t)r * WM + tid + k * NT];
-            T::axpy(acc0[k], u, y);
-            if constexpr (MODE == MODE_STATS || DUAL) T::axpy(acc1[k], u, y1);
+          for (int k = 0; k < PPT; ++k)
+            u[k] = (k < kval) ? st[(size_t)r * WM + tid + k * NT] : make_double2(0.0, 0.0);
+#pragma unroll
+          for (int k = 0; k < PPT; ++k) {
+            T::axpy(acc0[k], u[k], y);
+            T::axpy(acc1[k], u[k], y1);
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < PPT; ++k) {
+            if (k < kval) {
+              const double2 u = st[(size_t)r * WM + tid + k * NT];
+              T::axpy(acc0[k], u, y);
+              if constexpr (MODE == MODE_STATS) T::axpy(acc1[k], u, y1);
+            }
           }
         }
       }
