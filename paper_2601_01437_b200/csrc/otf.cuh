@@ -475,10 +475,13 @@ __global__ void __maxnreg__((NKT <= 8 && NY == 1 && !HAS_T) ? 96 : 168)
     }
   const int wj = warp & 3, wk = (warp >> 2) & 1;
   // A rows of this lane: hidden units jl (m-tile 0) and jl + 1 (m-tile 1), jl even, so one
-  // 16-byte load gives both; a quarter-warp then reads 8 distinct 16-byte chunks of one
-  // swizzled tile row (conflict-free, where consecutive units jl, jl + 8 hit 8 of the
-  // 16 bank pairs from 4 rows at once)
-  const int jl = wj * 16 + 2 * (lane >> 2);
+  // 16-byte load gives both.  A quarter-warp (8 lanes) reads 4 tile rows (lane & 3) x 2
+  // chunks; row r's chunk q sits at bank group q ^ (r & 7), so the two chunks must differ
+  // in bit 2 for the 8 accesses to hit 8 distinct groups (chunks q, q + 1 collided
+  // pairwise: ncu counted 2 wavefronts per ideal one on this load).  MMA row g = lane >> 2
+  // therefore takes unit pair ((g & 1) << 2) | (g >> 1); the accumulator rows follow the
+  // same lane, so the epilogue's jl is all that changes.
+  const int jl = wj * 16 + 2 * ((((lane >> 2) & 1) << 2) | (lane >> 3));
   const double u_lo = (gu && j0 + jl < h) ? a.u[j0 + jl] : 0.0;
   const double u_hi = (gu && j0 + jl + 1 < h) ? a.u[j0 + jl + 1] : 0.0;
 
