@@ -555,7 +555,7 @@ int make_wide_plan(int64_t n, int64_t ld_u, bool cplx, WidePlan& p) {
   const size_t per_slot = 4 * 8 + (size_t)p.RS * p.Q * sS + (size_t)p.RS * sS;  // dotdone, ydone, parked, slotfree, pd, ys
   const size_t budget = (size_t)d.smem_optin - 2048;  // static smem of the kernel
   const size_t side_bytes = (size_t)p.K * p.RS * p.Q * p.pr * 16;
-  const size_t fixed = (size_t)p.K * per_slot;
+  const size_t fixed = (size_t)p.K * per_slot + 16 + (size_t)p.RS * sS;  // + the y ring's extra slot (ydone + pad, ys)
   const size_t vbytes = (size_t)(p.WM + 1) * 16 + 32 + side_bytes;
   p.NS = (int)std::min<size_t>(WIDE_MAX_NS, (budget - fixed - vbytes) / (stage + 16));
   if (getenv("IRL_WIDE_NS")) p.NS = std::min(p.NS, std::max(2, atoi(getenv("IRL_WIDE_NS"))));

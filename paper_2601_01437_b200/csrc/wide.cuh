@@ -89,7 +89,7 @@ static_assert(WIDE_CW * 32 * (WIDE_REGS_DOT + WIDE_REGS_ACC) + (WIDE_THREADS - 2
 constexpr int WIDE_MAX_NS = 24;  // shared-memory stages
 constexpr int WIDE_MAX_K = 24;   // blocks parked in TMEM per consumer warp (pending exchange)
 constexpr int WIDE_NBUF = 64;    // exchange record ring (>= 2 K + 2)
-static_assert(WIDE_NBUF >= 2 * WIDE_MAX_K + 2, "exchange ring too short for the deepest pending ring");
+static_assert(WIDE_NBUF >= 2 * (WIDE_MAX_K + 1) + 2, "exchange ring too short for the deepest pending window");
 constexpr int WIDE_QPL = 2;  // partials per aggregator lane: 2 * 32 * WIDE_AW >= G
 static_assert(WIDE_QPL * 32 * WIDE_AW >= 160, "aggregator lanes must cover every SM");
 constexpr int WIDE_MAX_RS = 32;  // rows per block: one reducer lane each
@@ -264,11 +264,14 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1) k_wide(const WideArgs a) {
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_w + a.ring_bytes);  // [NS]
   uint64_t* empty = full + NS;                                           // [NS]
   uint64_t* dotdone = empty + NS;                                        // [K]
-  uint64_t* ydone = dotdone + K;                                         // [K]
-  uint64_t* parked = ydone + K;                                          // [K] block b is in TMEM (dot warps -> accumulate warps)
+  // y of the rows has one slot more than the pending ring: an accumulate warp fetches block b into registers as
+  // soon as it is parked and frees its slot, so block b + K may get its y while block b still waits for its own
+  const int KY = K + 1;
+  uint64_t* ydone = dotdone + K;                                         // [KY]
+  uint64_t* parked = ydone + KY + 1;                                     // [K] (+ 1: pd stays 16-byte aligned) block b is in TMEM
   uint64_t* slotfree = parked + K;                                       // [K] block b left TMEM (accumulate warps -> dot warps)
   S* pd = reinterpret_cast<S*>(slotfree + K);                            // [K][RS][Q] part dots
-  S* ys = pd + (size_t)K * RS * Q;                                       // [K][RS] y of the rows
+  S* ys = pd + (size_t)K * RS * Q;                                       // [KY][RS] y of the rows
   double2* vsl = reinterpret_cast<double2*>(a.vsl_off + smem_w);         // [WM + 1] v slice (+ a zero unit)
   double2* side = reinterpret_cast<double2*>(a.side_off + smem_w);       // [K][RS][Q][PR] last lane-rows of pending blocks
   __shared__ S shs[WIDE_CW];
@@ -303,10 +306,10 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1) k_wide(const WideArgs a) {
     }
     for (int j = 0; j < K; ++j) {
       mbar_init(&dotdone[j], WIDE_CW);
-      mbar_init(&ydone[j], 1);
       mbar_init(&parked[j], WIDE_CW);
       mbar_init(&slotfree[j], WIDE_CW);
     }
+    for (int j = 0; j <= K; ++j) mbar_init(&ydone[j], 1);
     published = 0;
     fence_mbar_init();
   }
@@ -447,7 +450,7 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1) k_wide(const WideArgs a) {
     const int k = warp - W_RED;
     S ysum = T::zero();
     for (int b = k; b < NB; b += WIDE_RW) {
-      const int j = b % K;
+      const int j = b % KY;  // slot of the y ring
       const int64_t r0 = (int64_t)b * RS;
       const int rows = (int)min((int64_t)RS, N - r0);
       const uint32_t tag = (uint32_t)b + 1;
@@ -587,10 +590,13 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1) k_wide(const WideArgs a) {
 #pragma unroll
   for (int k = 0; k < UPL; ++k) acc[k] = make_double2(0.0, 0.0);
   {
-    int ja = 0, pap = 0;
+    // EARLY (all the rows of a step fit one TMEM round trip): the block is fetched into registers as soon as it
+    // is parked and its slot freed before its y arrives, so the window is K blocks in TMEM plus this one
+    constexpr bool EARLY = RB == RPW;
+    int ja = 0, pap = 0, jy = 0, py = 0;
     for (int na = 0; na < NB; ++na) {
       const int j = ja;
-      mbar_wait(&ydone[j], pap);
+      if (!EARLY) mbar_wait(&ydone[jy], py);
       mbar_wait(&parked[j], pap);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int64_t r0 = (int64_t)na * RS + rg * RPW;
@@ -619,12 +625,13 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1) k_wide(const WideArgs a) {
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
           __syncwarp();
           if (lane == 0) mbar_arrive(&slotfree[j]);
+          if (EARLY) mbar_wait(&ydone[jy], py);
         }
         if (rb < nlive) {
 #pragma unroll
           for (int r = 0; r < RB; ++r) {
             if (rb + r < nlive) {
-              const S y = ys[j * RS + rg * RPW + rb + r];
+              const S y = ys[jy * RS + rg * RPW + rb + r];
 #pragma unroll
               for (int k = 0; k < UPL; ++k) T::axpy(acc[k], unit_of(w[r][k]), y);  // x = 0 past the part
             }
@@ -635,6 +642,10 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1) k_wide(const WideArgs a) {
       if (++ja == K) {
         ja = 0;
         pap ^= 1;
+      }
+      if (++jy == KY) {
+        jy = 0;
+        py ^= 1;
       }
     }
   }
