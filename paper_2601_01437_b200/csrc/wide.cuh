@@ -45,8 +45,10 @@
 //       dots -> smem, arrive dotdone (published at once); part -> TMEM slot,
 //       arrive empty (the stage refills); wait::st, arrive parked.
 //   accumulate warps (WIDE_CW) warp w + WIDE_CW shares warp w's place and TMEM
-//       columns (same warp % 4 = TMEM lane quarter).  A(b): wait ydone and
-//       parked, part back from TMEM, arrive slotfree, acc += conj(O) y.
+//       columns (same warp % 4 = TMEM lane quarter).  A(b): wait parked,
+//       part back from TMEM into registers, arrive slotfree (the slot is free
+//       before y arrives: the window is K blocks in TMEM plus this one), wait
+//       ydone, acc += conj(O) y.
 //       A single warp doing D(b) and A(b - K) in turn was the bound of the CTA
 //       (their dependent latencies add up per block); split, every wait is a
 //       blocking mbarrier wait on the one thing the warp needs next.
