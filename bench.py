@@ -644,6 +644,9 @@ def run_ours(args):
                                "two-pass figure is 2*N*P*b, i.e. frac_two_pass_accounting"),
                 "frac_two_pass_accounting": 2 * N * P * b_el / mvp_avg_s / 1e9 / peak,
                 "kernel_ms_mean": mvp_avg_s * 1e3, "kernel_ms_median": statistics.median(mvp_ms)}
+    roofline["peak_note"] = ("peak is the measured COPY bandwidth (read + write); a read-only stream such as this "
+                             "product can run a few percent above it (6.7 TB/s, profiles/r01g_read_bw.json), so frac "
+                             "may slightly exceed 1")
     del batch, apply, coef_h, coef_s
     gc.collect()
     torch.cuda.empty_cache()
